@@ -1,0 +1,552 @@
+"""Pins of the CPU oracle (oracle/) against what the paper and FE theory fix.
+
+CPU only (-m "not gpu").  Each test names the pin of DESIGN.md "Oracle pins":
+P1-P3 closed forms (exact rationals computed here with fractions, independently
+of the oracle), P4-P10 invariants, P11 the second einsum oracle on the paper's
+own strings (tests/einsum_oracle.py), plus the paper's printed shapes
+(tests/golden/paper_einsum_examples.txt).
+"""
+from __future__ import annotations
+
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import einsum_oracle as eo
+import fe_inputs as fi
+import oracle
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ---------------------------------------------------------------- exact 1D
+def _poly_mul(a, b):
+    out = [Fraction(0)] * (len(a) + len(b) - 1)
+    for i, x in enumerate(a):
+        for j, y in enumerate(b):
+            out[i + j] += x * y
+    return out
+
+
+def _poly_deriv(a):
+    return [a[i] * i for i in range(1, len(a))] or [Fraction(0)]
+
+
+def _poly_int01(a):
+    return sum(c / (i + 1) for i, c in enumerate(a))
+
+
+def _lagrange_exact(p):
+    nodes = [Fraction(i, p) for i in range(p + 1)]
+    polys = []
+    for i in range(p + 1):
+        P = [Fraction(1)]
+        for j in range(p + 1):
+            if j != i:
+                P = _poly_mul(P, [-nodes[j] / (nodes[i] - nodes[j]), 1 / (nodes[i] - nodes[j])])
+        polys.append(P)
+    return polys
+
+
+def exact_1d(p):
+    """M1 = int phi_i phi_j, S1 = int phi_i' phi_j', C1 = int phi_i' phi_j on [0,1]."""
+    L = _lagrange_exact(p)
+    dL = [_poly_deriv(P) for P in L]
+    n = p + 1
+    M = [[_poly_int01(_poly_mul(L[i], L[j])) for j in range(n)] for i in range(n)]
+    S = [[_poly_int01(_poly_mul(dL[i], dL[j])) for j in range(n)] for i in range(n)]
+    C = [[_poly_int01(_poly_mul(dL[i], L[j])) for j in range(n)] for i in range(n)]
+    return M, S, C
+
+
+def _kron3(Az, Ay, Ax):
+    """Exact Kronecker product with x fastest: index k = i + n(j + n l)."""
+    nz, ny, nx = len(Az), len(Ay), len(Ax)
+    N = nx * ny * nz
+    out = [[None] * N for _ in range(N)]
+    for l in range(nz):
+        for j in range(ny):
+            for i in range(nx):
+                r = i + nx * (j + ny * l)
+                for l2 in range(nz):
+                    for j2 in range(ny):
+                        for i2 in range(nx):
+                            c = i2 + nx * (j2 + ny * l2)
+                            out[r][c] = Az[l][l2] * Ay[j][j2] * Ax[i][i2]
+    return out
+
+
+def _to_np(A):
+    return np.array([[float(x) for x in row] for row in A])
+
+
+def exact_box_matrices(p, hx, hy, hz):
+    """Exact Q_p stiffness and mass on an axis-aligned box (pin P2)."""
+    M, S, _ = exact_1d(p)
+    vol = Fraction(hx) * Fraction(hy) * Fraction(hz)
+    Mx = [[m for m in row] for row in M]
+    Kx = _kron3(M, M, S)
+    Ky = _kron3(M, S, M)
+    Kz = _kron3(S, M, M)
+    Mm = _kron3(M, M, M)
+    n = len(Mm)
+    hx, hy, hz = Fraction(hx), Fraction(hy), Fraction(hz)
+    K = [[vol * (Kx[r][c] / hx ** 2 + Ky[r][c] / hy ** 2 + Kz[r][c] / hz ** 2) for c in range(n)]
+         for r in range(n)]
+    Mass = [[vol * Mm[r][c] for c in range(n)] for r in range(n)]
+    del Mx
+    return K, Mass
+
+
+def exact_elasticity_unit(p, lam, mu):
+    """Exact isotropic elasticity on the unit cube (pin P3):
+    K_(a,k),(b,l) = lam int d_a phi_k d_b phi_l + mu (delta_ab int grad phi_k . grad phi_l
+                    + int d_b phi_k d_a phi_l)."""
+    M, S, C = exact_1d(p)
+    CT = [list(r) for r in zip(*C)]
+
+    def factor(a, b, d):
+        # 1D factor along axis d of int (d==a ? phi' : phi)_k (d==b ? phi' : phi)_l
+        if d == a and d == b:
+            return S
+        if d == a:
+            return C       # int phi_k' phi_l
+        if d == b:
+            return CT      # int phi_k phi_l'
+        return M
+
+    def Dab(a, b):
+        return _kron3(factor(a, b, 2), factor(a, b, 1), factor(a, b, 0))
+
+    nb = (p + 1) ** 3
+    G = {(a, b): Dab(a, b) for a in range(3) for b in range(3)}
+    K = np.zeros((3 * nb, 3 * nb))
+    lam, mu = Fraction(lam), Fraction(mu)
+    for a in range(3):
+        for b in range(3):
+            for k in range(nb):
+                for l in range(nb):
+                    v = lam * G[(a, b)][k][l] + mu * G[(b, a)][k][l]
+                    if a == b:
+                        v += mu * sum(G[(d, d)][k][l] for d in range(3))
+                    K[a * nb + k, b * nb + l] = float(v)
+    return K
+
+
+def _golden_kv(fname):
+    out = {}
+    for line in open(os.path.join(GOLDEN, fname)):
+        line = line.split("#")[0].strip()
+        if "=" in line:
+            k, v = line.split("=", 1)
+            out[k.strip()] = [Fraction(x) for x in v.split()]
+    return out
+
+
+def unit_cube():
+    return fi.grid_vertices(1, 1, 1), fi.hex_connectivity(1, 1, 1)
+
+
+def box(hx, hy, hz, origin=(0.0, 0.0, 0.0)):
+    c = fi.grid_vertices(1, 1, 1) * np.array([hx, hy, hz]) + np.array(origin)
+    return c, fi.hex_connectivity(1, 1, 1)
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+# ---------------------------------------------------------------- tables
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 8, 12])
+def test_gauss_legendre_matches_library(n):
+    """Oracle Gauss rule == numpy leggauss mapped to [0,1] (textbook rule)."""
+    x, w = oracle.gauss_legendre(n)
+    t, wt = np.polynomial.legendre.leggauss(n)
+    np.testing.assert_allclose(x, (t + 1) / 2, rtol=0, atol=1e-15)
+    np.testing.assert_allclose(w, wt / 2, rtol=0, atol=1e-15)
+    assert abs(w.sum() - 1.0) < 1e-15
+    # exactness: int_0^1 x^k = 1/(k+1) for k <= 2n-1
+    for k in range(2 * n):
+        assert abs((w * x ** k).sum() - 1.0 / (k + 1)) < 1e-14
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
+def test_lagrange_1d_properties(p):
+    """Kronecker-delta at nodes, partition of unity, derivatives sum to 0,
+    derivative matches the exact polynomial."""
+    L = _lagrange_exact(p)
+    for i in range(p + 1):
+        phi, _ = oracle.lagrange_1d(p, i / p)
+        np.testing.assert_allclose(phi, np.eye(p + 1)[i], atol=1e-14)
+    for t in np.linspace(-0.2, 1.3, 11):
+        phi, dphi = oracle.lagrange_1d(p, t)
+        assert abs(phi.sum() - 1) < 1e-13 and abs(dphi.sum()) < 1e-12
+        exact_d = [float(sum(c * Fraction(t) ** (k - 1) * k for k, c in enumerate(P) if k > 0))
+                   for P in L]
+        np.testing.assert_allclose(dphi, exact_d, rtol=1e-12, atol=1e-12)
+
+
+def test_tables_match_independent_construction():
+    """Tensorised Phi / grad Phi equal the numpy-polynomial construction."""
+    for p, q in [(1, 2), (2, 3), (4, 5), (2, 2)]:
+        xi, w, Phi, dPhi = oracle.tables(p, q)
+        X, W, bf, bfg = eo.tables(p, q)
+        np.testing.assert_allclose(xi, X, atol=1e-15)
+        np.testing.assert_allclose(w, W, atol=1e-16)
+        np.testing.assert_allclose(Phi, bf, atol=1e-13)
+        np.testing.assert_allclose(dPhi, bfg, atol=1e-12)
+
+
+# ---------------------------------------------------------------- P1 / P2 / P3
+def test_P1_q1_unit_cube_golden():
+    g = _golden_kv("q1_unit_cube.txt")
+    c, conn = unit_cube()
+    K = oracle.eval_matrix(fi.DIFFUSION, 1, 2, c, conn, None, 0, np.ones((1, 8)))[0]
+    M = oracle.eval_matrix(fi.MASS, 1, 2, c, conn, None, 0, np.ones((1, 8)))[0]
+    np.testing.assert_allclose(M[0], [float(x) for x in g["mass_row0"]], rtol=1e-14, atol=1e-17)
+    np.testing.assert_allclose(K[0], [float(x) for x in g["stiffness_row0"]], rtol=1e-14,
+                               atol=1e-15)
+    assert abs(M.sum() - float(g["mass_sum"][0])) < 1e-14
+    # the golden rationals agree with the exact 1D-factor construction
+    Ke, Me = exact_box_matrices(1, 1, 1, 1)
+    assert [Fraction(x) for x in Me[0]] == g["mass_row0"]
+    assert [Fraction(x) for x in Ke[0]] == g["stiffness_row0"]
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+@pytest.mark.parametrize("dims", [(1, 1, 1), (Fraction(1, 2), Fraction(1, 3), Fraction(2, 5))])
+def test_P2_box_closed_form(p, dims):
+    Ke, Me = exact_box_matrices(p, *dims)
+    c, conn = box(*[float(d) for d in dims], origin=(0.3, -0.2, 1.1))
+    nb = (p + 1) ** 3
+    dc, _ = fi.lattice_dof_conn(1, 1, 1, p)
+    K = oracle.eval_matrix(fi.DIFFUSION, p, p + 1, c, conn, dc, 0, np.ones((1, (p + 1) ** 3)))[0]
+    M = oracle.eval_matrix(fi.MASS, p, p + 1, c, conn, dc, 0, np.ones((1, (p + 1) ** 3)))[0]
+    assert K.shape == (nb, nb)
+    assert rel(K, _to_np(Ke)) < 1e-14
+    assert rel(M, _to_np(Me)) < 1e-14
+
+
+def test_P2_golden_diagonals():
+    g = _golden_kv("q1_unit_cube.txt")
+    for p, kk, mk in [(2, "q2_K00", "q2_M00"), (4, "q4_K00", "q4_M00")]:
+        Ke, Me = exact_box_matrices(p, 1, 1, 1)
+        assert Ke[0][0] == g[kk][0] and Me[0][0] == g[mk][0]
+        c, conn = unit_cube()
+        dc, _ = fi.lattice_dof_conn(1, 1, 1, p)
+        nq = (p + 1) ** 3
+        K = oracle.eval_matrix(fi.DIFFUSION, p, p + 1, c, conn, dc, 0, np.ones((1, nq)))[0]
+        M = oracle.eval_matrix(fi.MASS, p, p + 1, c, conn, dc, 0, np.ones((1, nq)))[0]
+        assert abs(K[0, 0] / float(g[kk][0]) - 1) < 1e-14
+        assert abs(M[0, 0] / float(g[mk][0]) - 1) < 1e-14
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_P3_elasticity_closed_form(p):
+    c, conn = unit_cube()
+    dc, _ = fi.lattice_dof_conn(1, 1, 1, p)
+    lam, mu = 1.25, 0.75
+    K = oracle.eval_matrix(fi.ELASTICITY, p, p + 1, c, conn, dc, fi.MAT_PER_ELEM,
+                           np.array([lam]), np.array([mu]))[0]
+    Kx = exact_elasticity_unit(p, Fraction(5, 4), Fraction(3, 4))
+    assert rel(K, Kx) < 1e-14
+    if p == 1:
+        g = _golden_kv("q1_unit_cube.txt")
+        K1 = oracle.eval_matrix(fi.ELASTICITY, 1, 2, c, conn, None, fi.MAT_PER_ELEM,
+                                np.array([1.0]), np.array([1.0]))[0]
+        assert abs(K1[0, 0] - float(g["el_K_x0x0"][0])) < 1e-15
+        assert abs(K1[0, 8] - float(g["el_K_x0y0"][0])) < 1e-15
+
+
+def test_P3_full_D_equals_isotropic():
+    pr = fi.make_problem(fi.ELASTICITY, 2, (2, 1, 1), 3)
+    Dfull = np.broadcast_to(np.stack([np.stack([oracle.isotropic_D(a, b)] * pr.nq)
+                                      for a, b in zip(pr.mat_a, pr.mat_b)]), (2, pr.nq, 6, 6))
+    K1 = oracle.problem_matrix(pr)
+    K2 = oracle.eval_matrix(fi.ELASTICITY, 2, 3, pr.coords, pr.conn, pr.dof_conn, fi.MAT_FULL_D,
+                            np.ascontiguousarray(Dfull))
+    assert rel(K2, K1) < 1e-15
+
+
+# ---------------------------------------------------------------- P4 .. P10
+def node_coords(prob):
+    """Physical coordinates of the order-p lattice nodes: trilinear image of
+    the reference nodes (i/p, j/p, k/p) of each element (reading 4)."""
+    p = prob.p
+    X = np.zeros((prob.n_nodes, 3))
+    t = np.arange(p + 1) / p
+    for l in range(p + 1):
+        for j in range(p + 1):
+            for i in range(p + 1):
+                k = i + (p + 1) * (j + (p + 1) * l)
+                xi = (t[i], t[j], t[l])
+                w = np.array([(xi[0] if a else 1 - xi[0]) * (xi[1] if b else 1 - xi[1]) *
+                              (xi[2] if cc else 1 - xi[2])
+                              for cc in (0, 1) for b in (0, 1) for a in (0, 1)])
+                X[prob.dof_conn[:, k]] = np.einsum("v,evi->ei", w, prob.coords[prob.conn])
+    return X
+
+
+@pytest.mark.parametrize("p", [1, 2, 4])
+def test_P4_volume(p):
+    pr = fi.make_problem(fi.MASS, p, (3, 3, 2), 11)
+    M = oracle.eval_matrix(fi.MASS, p, p + 1, pr.coords, pr.conn, pr.dof_conn, 0,
+                           np.ones((pr.n_elems, pr.nq)))
+    assert abs(M.sum() - 1.0) < 1e-13
+    detw, _ = oracle.geometry(p + 1, pr.coords, pr.conn)
+    np.testing.assert_allclose(M.sum(axis=(1, 2)), detw.sum(axis=1), rtol=1e-13)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_P5_patch_test(p):
+    pr = fi.make_problem(fi.DIFFUSION, p, (3, 3, 3), 5)
+    X = node_coords(pr)
+    u = X @ np.array([0.3, -1.1, 0.7]) + 0.25
+    kappa = np.full((pr.n_elems, pr.nq), 1.7)
+    r = oracle.eval_residual(fi.DIFFUSION, p, p + 1, pr.coords, pr.conn, pr.dof_conn, u[:, None],
+                             0, kappa)
+    R = oracle.assemble(r, pr.dof_conn, pr.n_nodes, 1)
+    M = p * 3 + 1
+    idx = np.arange(pr.n_nodes)
+    ix, iy, iz = idx % M, (idx // M) % M, idx // (M * M)
+    interior = (ix > 0) & (ix < M - 1) & (iy > 0) & (iy < M - 1) & (iz > 0) & (iz < M - 1)
+    assert np.abs(R[interior]).max() <= 1e-13 * np.abs(R).max()
+    assert np.abs(R[~interior]).max() > 1e-3
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_P6_rigid_modes(p):
+    pr = fi.make_problem(fi.ELASTICITY, p, (2, 2, 1), 9)
+    X = node_coords(pr)
+    K = oracle.problem_matrix(pr)
+    nb = pr.nb
+    for e in range(pr.n_elems):
+        xe = X[pr.dof_conn[e]]
+        modes = []
+        for a in range(3):
+            m = np.zeros((3, nb))
+            m[a] = 1.0
+            modes.append(m)
+        for w in np.eye(3):
+            modes.append(np.cross(w, xe).T)
+        for m in modes:
+            v = m.reshape(-1)
+            assert np.linalg.norm(K[e] @ v) <= 1e-13 * np.linalg.norm(K[e]) * np.linalg.norm(v)
+    # a one-sided Psg (6 ones) would not annihilate rotations: K must be rank 3*nb-6
+    s = np.linalg.svd(K[0], compute_uv=False)
+    assert (s < 1e-12 * s[0]).sum() == 6
+
+
+@pytest.mark.parametrize("form,p", [(fi.DIFFUSION, 1), (fi.DIFFUSION, 2), (fi.MASS, 2),
+                                    (fi.ELASTICITY, 2), (fi.VECTOR_MASS, 1),
+                                    (fi.MASS_DIFFUSION, 2)])
+def test_P7_symmetry_rowsums(form, p):
+    pr = fi.make_problem(form, p, (2, 2, 2), 13)
+    K = oracle.problem_matrix(pr)
+    assert rel(K, K.transpose(0, 2, 1)) < 1e-14
+    if form == fi.DIFFUSION:
+        assert np.abs(K.sum(axis=2)).max() < 1e-13 * np.abs(K).max()
+
+
+def test_P7_vector_mass_blocks():
+    """Vector mass = D copies of the scalar mass block."""
+    pr = fi.make_problem(fi.VECTOR_MASS, 2, (2, 1, 2), 21)
+    Kv = oracle.problem_matrix(pr)
+    Ms = oracle.eval_matrix(fi.MASS, 2, 3, pr.coords, pr.conn, pr.dof_conn, 0, pr.mat_a)
+    nb = pr.nb
+    for r in range(3):
+        for s in range(3):
+            blk = Kv[:, r * nb:(r + 1) * nb, s * nb:(s + 1) * nb]
+            if r == s:
+                assert rel(blk, Ms) < 1e-15
+            else:
+                assert np.abs(blk).max() == 0.0
+
+
+def test_P7_mass_diffusion_constant():
+    pr = fi.make_problem(fi.MASS_DIFFUSION, 2, (2, 2, 2), 4)
+    rho = np.ones_like(pr.mat_a)
+    r = oracle.eval_residual(fi.MASS_DIFFUSION, 2, 3, pr.coords, pr.conn, pr.dof_conn,
+                             np.ones((pr.n_nodes, 1)), 0, rho, pr.mat_b)
+    assert abs(r.sum() - 1.0) < 1e-13
+
+
+@pytest.mark.parametrize("form,p", [(fi.DIFFUSION, 1), (fi.DIFFUSION, 2), (fi.MASS, 2),
+                                    (fi.VECTOR_MASS, 2), (fi.MASS_DIFFUSION, 2),
+                                    (fi.ELASTICITY, 1), (fi.ELASTICITY, 2)])
+def test_P8_linear_consistency(form, p):
+    """r_e = K_e u_e for the linear forms (Alg. 1 vs Alg. 2)."""
+    pr = fi.make_problem(form, p, (3, 2, 2), 17)
+    K = oracle.problem_matrix(pr)
+    r = oracle.problem_residual(pr)
+    ue = pr.u[pr.dof_conn].transpose(0, 2, 1).reshape(pr.n_elems, -1)
+    Ku = np.einsum("eij,ej->ei", K, ue)
+    assert rel(r, Ku) < 1e-13
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_P8_convective_identities(p):
+    """Quadratic residual: K(u) u = 2 r(u); (r(u+d) - r(u-d))/2 = K(u) d exactly."""
+    pr = fi.make_problem(fi.CONVECTIVE, p, (2, 2, 2), 23)
+    K = oracle.problem_matrix(pr)
+    r = oracle.problem_residual(pr)
+    ue = pr.u[pr.dof_conn].transpose(0, 2, 1).reshape(pr.n_elems, -1)
+    assert rel(np.einsum("eij,ej->ei", K, ue), 2 * r) < 1e-13
+    rng = np.random.default_rng(1)
+    d = rng.uniform(-0.3, 0.3, size=pr.u.shape)
+    args = (fi.CONVECTIVE, p, p + 1, pr.coords, pr.conn, pr.dof_conn)
+    rp = oracle.eval_residual(*args, pr.u + d)
+    rm = oracle.eval_residual(*args, pr.u - d)
+    de = d[pr.dof_conn].transpose(0, 2, 1).reshape(pr.n_elems, -1)
+    assert rel((rp - rm) / 2, np.einsum("eij,ej->ei", K, de)) < 1e-13
+
+
+def test_P9_scaling_rotation():
+    pr = fi.make_problem(fi.DIFFUSION, 2, (1, 1, 1), 2, perturb=0.0)
+    rng = np.random.default_rng(5)
+    c = pr.coords + rng.uniform(-0.1, 0.1, size=pr.coords.shape)
+    one = np.ones((1, 27))
+    args = (2, 3)
+    K = oracle.eval_matrix(fi.DIFFUSION, *args, c, pr.conn, pr.dof_conn, 0, one)
+    M = oracle.eval_matrix(fi.MASS, *args, c, pr.conn, pr.dof_conn, 0, one)
+    s = 2.5
+    Ks = oracle.eval_matrix(fi.DIFFUSION, *args, c * s, pr.conn, pr.dof_conn, 0, one)
+    Ms = oracle.eval_matrix(fi.MASS, *args, c * s, pr.conn, pr.dof_conn, 0, one)
+    assert rel(Ks, s * K) < 1e-14 and rel(Ms, s ** 3 * M) < 1e-14
+    th = 0.7
+    R = np.array([[np.cos(th), -np.sin(th), 0], [np.sin(th), np.cos(th), 0], [0, 0, 1.0]])
+    R = R @ np.array([[1, 0, 0], [0, np.cos(0.3), -np.sin(0.3)], [0, np.sin(0.3), np.cos(0.3)]])
+    Kr = oracle.eval_matrix(fi.DIFFUSION, *args, c @ R.T, pr.conn, pr.dof_conn, 0, one)
+    assert rel(Kr, K) < 1e-14
+
+
+def test_P10_zero_and_constant():
+    for form in (fi.DIFFUSION, fi.ELASTICITY, fi.CONVECTIVE, fi.MASS_DIFFUSION):
+        pr = fi.make_problem(form, 2, (2, 1, 1), 8)
+        r = oracle.eval_residual(form, 2, 3, pr.coords, pr.conn, pr.dof_conn,
+                                 np.zeros_like(pr.u), pr.mat_kind, pr.mat_a, pr.mat_b)
+        assert np.abs(r).max() == 0.0
+    pr = fi.make_problem(fi.DIFFUSION, 2, (2, 2, 1), 8)
+    r = oracle.eval_residual(fi.DIFFUSION, 2, 3, pr.coords, pr.conn, pr.dof_conn,
+                             np.full_like(pr.u, 3.0), 0, pr.mat_a)
+    assert np.abs(r).max() < 1e-14
+    # constant velocity: the reaction block (term 2 of Eq. fe4) vanishes
+    pr = fi.make_problem(fi.CONVECTIVE, 2, (2, 1, 1), 8)
+    u = np.tile([0.3, -0.2, 0.5], (pr.n_nodes, 1))
+    K = oracle.eval_matrix(fi.CONVECTIVE, 2, 3, pr.coords, pr.conn, pr.dof_conn, 0, None, None, u)
+    nb = pr.nb
+    for a in range(3):
+        for b in range(3):
+            if a != b:
+                assert np.abs(K[:, a * nb:(a + 1) * nb, b * nb:(b + 1) * nb]).max() < 1e-15
+
+
+def test_degenerate_element_reported():
+    pr = fi.make_problem(fi.DIFFUSION, 1, (3, 1, 1), 1)
+    c = pr.coords.copy()
+    conn = pr.conn.copy()
+    conn[1] = conn[1][[1, 0, 3, 2, 5, 4, 7, 6]]     # mirror element 1 -> det J < 0
+    with pytest.raises(oracle.OracleError) as ei:
+        oracle.eval_matrix(fi.DIFFUSION, 1, 2, c, conn, None, 0, pr.mat_a)
+    assert ei.value.status == oracle.ERR_DEGENERATE and ei.value.element == 1
+    with pytest.raises(oracle.OracleError) as ei:
+        oracle.geometry(2, c, conn)
+    assert ei.value.element == 1
+
+
+# ---------------------------------------------------------------- P11
+@pytest.mark.parametrize("form,p,kind", [(0, 1, 0), (0, 2, 0), (0, 4, 0), (1, 2, 0), (2, 1, 0),
+                                         (2, 2, 0), (3, 2, 0), (3, 4, 0), (4, 1, 1), (4, 2, 1),
+                                         (4, 2, 0), (4, 2, 2), (5, 1, 0), (5, 2, 0)])
+def test_P11_second_oracle(form, p, kind):
+    pr = fi.make_problem(form, p, (3, 2, 2), 100 + form, mat_kind=kind if form == 4 else None)
+    K = oracle.problem_matrix(pr)
+    K2 = eo.matrix(form, pr.coords, pr.conn, p, pr.q1d, pr.dof_conn, pr.mat_a, pr.mat_b,
+                   pr.mat_kind, pr.u)
+    assert rel(K, K2) < 1e-13
+    r = oracle.problem_residual(pr)
+    r2 = eo.residual(form, pr.coords, pr.conn, p, pr.q1d, pr.dof_conn, pr.u, pr.mat_a, pr.mat_b,
+                     pr.mat_kind)
+    assert rel(r, r2) < 1e-13
+
+
+def test_P11_C1_in_full():
+    pr = fi.make_config("C1")
+    K = oracle.problem_matrix(pr)
+    K2 = eo.matrix(0, pr.coords, pr.conn, 1, 2, None, pr.mat_a)
+    assert K.shape == (64, 8, 8)
+    assert rel(K, K2) < 1e-13
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+def test_P11_config_subsets(name):
+    """Seeded <= 64-element subsets of the BASELINE configs (small N, same recipe)."""
+    pr = fi.make_config(name, N=4)
+    rng = np.random.default_rng(0)
+    sel = np.sort(rng.choice(pr.n_elems, size=16, replace=False))
+    sub = fi.Problem(name, pr.form, pr.p, pr.q1d, pr.shape, pr.coords, pr.conn[sel],
+                     pr.dof_conn[sel], pr.n_nodes, pr.mat_kind,
+                     None if pr.mat_a is None else pr.mat_a[sel],
+                     None if pr.mat_b is None else pr.mat_b[sel], pr.u)
+    r = oracle.problem_residual(sub)
+    r2 = eo.residual(sub.form, sub.coords, sub.conn, sub.p, sub.q1d, sub.dof_conn, sub.u,
+                     sub.mat_a, sub.mat_b, sub.mat_kind)
+    assert rel(r, r2) < 1e-13
+    if name != "C4":
+        K = oracle.problem_matrix(sub)
+        K2 = eo.matrix(sub.form, sub.coords, sub.conn, sub.p, sub.q1d, sub.dof_conn, sub.mat_a,
+                       sub.mat_b, sub.mat_kind, sub.u)
+        assert rel(K, K2) < 1e-13
+
+
+def _parse_examples():
+    rows = []
+    for line in open(os.path.join(GOLDEN, "paper_einsum_examples.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        name, cite, expr, p, nc, out, ops = [x.strip() for x in line.split("|")]
+        shapes = {kv.split("=")[0]: tuple(int(x) for x in kv.split("=")[1].split(","))
+                  for kv in ops.split()}
+        rows.append((name, cite, expr, int(p), int(nc), tuple(int(x) for x in out.split(",")),
+                     shapes))
+    return rows
+
+
+@pytest.mark.parametrize("row", _parse_examples(), ids=lambda r: r[0])
+def test_paper_worked_examples(row):
+    """The paper's printed einsum strings and sizes (Sec. 5.3) on a 1D bar of 1024
+    hexahedra: operand shapes are the printed ones and the result equals
+    the oracle."""
+    name, cite, expr, p, nc, out_shape, shapes = row
+    c = fi.grid_vertices(1, 1, nc)
+    conn = fi.hex_connectivity(1, 1, nc)
+    dc, n_nodes = fi.lattice_dof_conn(1, 1, nc, p)
+    q1d = p + 1
+    det, bf, bfg = eo.operands(c, conn, p, q1d)
+    rng = np.random.default_rng(2)
+    ops = {"cq": det, "qd": bf, "qe": bf, "ir": np.eye(3), "is": np.eye(3),
+           "cqjd": bfg, "cqje": bfg, "cqlf": bfg, "rjI": eo.psg(), "slK": eo.psg()}
+    if "cqIK" in shapes:
+        lam = rng.uniform(0.5, 2, nc)
+        mu = rng.uniform(0.5, 2, nc)
+        ops["cqIK"] = np.ascontiguousarray(
+            np.broadcast_to(eo.iso_D(lam, mu)[:, None], (nc, q1d ** 3, 6, 6)))
+    u = rng.uniform(-1, 1, size=(n_nodes, 3))
+    ops["cie"] = u[dc].transpose(0, 2, 1)
+    names = expr.split("->")[0].split(",")
+    for nm in names:
+        assert ops[nm].shape == shapes[nm], (nm, ops[nm].shape, shapes[nm])
+    res = np.einsum(expr, *[ops[nm] for nm in names], optimize=True)
+    assert res.shape == out_shape
+    if name == "laplace_matrix":
+        K = oracle.eval_matrix(fi.DIFFUSION, p, q1d, c, conn, dc, 0, np.ones((nc, q1d ** 3)))
+    elif name == "dot_matrix":
+        K = oracle.eval_matrix(fi.VECTOR_MASS, p, q1d, c, conn, dc, 0, np.ones((nc, q1d ** 3)))
+    elif name == "dot_residual":
+        K = oracle.eval_residual(fi.VECTOR_MASS, p, q1d, c, conn, dc, u, 0,
+                                 np.ones((nc, q1d ** 3)))
+    else:
+        K = oracle.eval_matrix(fi.ELASTICITY, p, q1d, c, conn, dc, fi.MAT_PER_ELEM, lam, mu)
+    assert rel(K.reshape(res.shape), res) < 1e-13
