@@ -1,0 +1,177 @@
+/*
+ * feb200.h -- C ABI of libfeb200.so: batched finite-element weak-form
+ * evaluation on NVIDIA B200 (sm_100a).
+ *
+ * The operations are those of arXiv 2107.04121:
+ *   - Alg. 2 "eval_matrix": per-cell matrices, the derivative of
+ *     the form w.r.t. the DOF vector, M[c] = sum_q detw(q) dF/du;
+ *   - Alg. 1 "eval_residual": per-cell residuals, the action of
+ *     the form on a DOF vector, r[c] = sum_q detw(q) F;
+ *   - the gather of the cell DOFs through the connectivity ("the mesh cell
+ *     connectivity is used to index the DOF vector") and the
+ *     scatter-add of cell residuals into the global vector (the assembly the
+ *     paper leaves to SfePy);
+ *   - the reference mapping: J = dx/dxi, det J, J^-1 at every quadrature
+ *     point, with the quadrature weight folded into det ("The
+ *     quadrature weights are incorporated in the element reference mapping
+ *     Jacobian"; Tab. 4 "v.det"), and physical gradients
+ *     du/dx_j = du/dxi_k J^-1_kj.
+ * Arguments follow the paper's statement of the problem:
+ * cells (connectivity), node coordinates, Lagrange order, quadrature,
+ * material values per quadrature point and the evaluation mode.
+ *
+ * Conventions:
+ *   - reference cell [0,1]^3, Gauss-Legendre rule with q1d points per axis;
+ *   - tensor-product Lagrange basis of order p on equispaced nodes i/p;
+ *   - lexicographic x-fastest numbering of element vertices (v = a+2b+4c),
+ *     element nodes (k = i + (p+1)(j + (p+1) l)) and quadrature points
+ *     (q = a + q1d (b + q1d c));
+ *   - trilinear geometry from the 8 vertices;
+ *   - element-local DOF index a*n_b + k (component-major, Eq. fe1b P:491-526,
+ *     'crdse' / 'cresf' layouts P:991); global vectors node-major
+ *     [n_nodes][D] (Eq. fe1c);
+ *   - every array row-major with the cell axis outermost (layout 'cqgvd0',
+ *     P:927-929).
+ *
+ * Memory: every pointer argument is a DEVICE pointer (cudaMalloc'ed or a
+ * torch CUDA tensor) on the current device, unless stated otherwise.
+ * Ownership: inputs are read only and never retained after the call returns;
+ * fe_create_mesh_geometry copies what the handle keeps.  Outputs are
+ * caller-allocated.  A handle is immutable after creation, so concurrent
+ * evaluations on different streams are safe.
+ * Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ * stream).  Evaluation calls are asynchronous on that stream.
+ * Errors: every call returns an fe_status; no C++ exception or abort crosses
+ * the ABI.  fe_last_error() gives a thread-local message; asynchronous kernel
+ * faults surface as FE_ERR_CUDA on a later call or at stream synchronisation.
+ */
+#ifndef FEB200_H
+#define FEB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FE_OK = 0,
+  FE_ERR_INVALID_ARG = 1, /* null pointer, negative or mismatched size, bad range */
+  FE_ERR_UNSUPPORTED = 2, /* order / q1d / form / dtype / material kind not built */
+  FE_ERR_DEGENERATE = 3,  /* det J <= 0 at some quadrature point; see fe_last_error_element */
+  FE_ERR_CUDA = 4,        /* CUDA runtime error; message has cudaGetErrorString */
+  FE_ERR_OOM = 5          /* device allocation failed */
+} fe_status;
+
+/* Weak forms (Tab. 2 of the paper; BASELINE configs). */
+typedef enum {
+  FE_FORM_DIFFUSION = 0,      /* int kappa grad v . grad u, scalar (weak Laplacian '0.i,0.i') */
+  FE_FORM_MASS = 1,           /* int rho v u, scalar */
+  FE_FORM_VECTOR_MASS = 2,    /* int rho v_i u_i, D = 3 (vector dot product 'i,i'; Eq. fe3c) */
+  FE_FORM_MASS_DIFFUSION = 3, /* int rho v u + kappa grad v . grad u, scalar (BASELINE config 4) */
+  FE_FORM_ELASTICITY = 4,     /* int e(v)^T D e(u), D = 3, Voigt via Psg */
+  FE_FORM_CONVECTIVE = 5      /* int v_i (du_i/dx_j) u_j, D = 3 (Eq. fe2); matrix = Eq. fe4 */
+} fe_form;
+
+typedef enum { FE_F64 = 0, FE_F32 = 1 } fe_dtype;
+
+/* Material description.  Arrays have the element type of the call's dtype and
+ * are indexed by the GLOBAL element index (also for element sub-ranges).
+ *   DIFFUSION       PER_QP: a = kappa[E][n_q]
+ *   MASS, VEC_MASS  PER_QP: a = rho[E][n_q]
+ *   MASS_DIFFUSION  PER_QP: a = rho[E][n_q], b = kappa[E][n_q]
+ *   ELASTICITY      PER_ELEM: a = lambda[E], b = mu[E];
+ *                   PER_QP:   a = lambda[E][n_q], b = mu[E][n_q];
+ *                   FULL_D:   a = D[E][n_q][6][6] (Voigt xx,yy,zz,xy,xz,yz,
+ *                             engineering shears; 'cqIK' operand)
+ *   CONVECTIVE      unused (kind ignored)                                  */
+typedef enum { FE_MAT_PER_QP = 0, FE_MAT_PER_ELEM = 1, FE_MAT_FULL_D = 2 } fe_material_kind;
+
+typedef struct {
+  int32_t kind;  /* fe_material_kind */
+  const void *a;
+  const void *b;
+} fe_material;
+
+typedef struct fe_mesh fe_mesh;
+
+typedef struct {
+  int32_t order, q1d, nb, nq;
+  int64_t n_vertices, n_elems, n_nodes;
+  double min_det_j; /* min over cells and qps of det J (unweighted), from the create-time check */
+} fe_info;
+
+/* Create the immutable mesh handle (SYNCHRONOUS on `stream`).
+ *   coords   [n_vertices][3] fp64, vertex coordinates
+ *   conn     [n_elems][8] int32, vertex ids of each hexahedron (v = a+2b+4c)
+ *   order    Lagrange order p of the field (1..4 on the GPU)
+ *   q1d      Gauss points per axis (must be p+1 on the GPU)
+ *   n_nodes  number of global field nodes (order-p lattice nodes)
+ *   dof_conn [n_elems][(p+1)^3] int32 global node of each element node, or
+ *            NULL when order == 1 (then dof_conn = conn and n_nodes = n_vertices)
+ * Copies coords / conn / dof_conn into library-owned device memory, builds the
+ * reference tables (Gauss-Legendre, Lagrange values and derivatives), and
+ * checks det J > 0 at every (cell, qp): FE_ERR_DEGENERATE otherwise, with the
+ * first offending cell in fe_last_error_element() (SPEC "degenerate-cell
+ * error naming the cell").  Connectivity entries out of range give
+ * FE_ERR_INVALID_ARG.  *out is set only on FE_OK. */
+fe_status fe_create_mesh_geometry(int64_t n_vertices, const double *coords, int64_t n_elems,
+                                  const int32_t *conn, int32_t order, int32_t q1d,
+                                  int64_t n_nodes, const int32_t *dof_conn, void *stream,
+                                  fe_mesh **out);
+
+/* Release the handle and its device memory (synchronises the device). NULL is a no-op. */
+fe_status fe_destroy_mesh(fe_mesh *mesh);
+
+/* Sizes of the handle (host struct). */
+fe_status fe_mesh_info(const fe_mesh *mesh, fe_info *info);
+
+/* Element matrices, Alg. 2, of cells [elem_begin, elem_end):
+ *   K[e - elem_begin][ndof][ndof], ndof = D n_b, row = test (a, k), column =
+ *   trial (b, l), local index a*n_b + k.  K is overwritten.
+ *   state_u: CONVECTIVE only, the linearisation state [n_nodes][3]; the
+ *   matrix is the Newton tangent of Eq. fe4 (both terms).  NULL otherwise.
+ * Only FE_F64 is built for matrices. */
+fe_status fe_eval_element_matrices(const fe_mesh *mesh, int32_t form, int32_t dtype,
+                                   const fe_material *mat, const void *state_u,
+                                   int64_t elem_begin, int64_t elem_end, void *K, void *stream);
+
+/* Residuals, Alg. 1, of cells [elem_begin, elem_end) for the
+ * global DOF vector u [n_nodes][D]:
+ *   r_elem  (nullable) [elem_end - elem_begin][ndof], overwritten;
+ *   r_global(nullable) [n_nodes][D], ACCUMULATED (+=): the caller zeroes it.
+ * The scatter-add into r_global is fused into the kernel (fp atomics; the
+ * atomic order is the only run-to-run difference).  For the CONVECTIVE form
+ * the residual is c(v, u, u) with the same u.  FE_F32 is built for
+ * DIFFUSION, MASS and MASS_DIFFUSION (fp32 data, geometry from fp64
+ * coordinates). */
+fe_status fe_eval_residual(const fe_mesh *mesh, int32_t form, int32_t dtype,
+                           const fe_material *mat, const void *u, int64_t elem_begin,
+                           int64_t elem_end, void *r_elem, void *r_global, void *stream);
+
+/* Scatter-add of cell residuals (standalone assembly):
+ *   r_global[dof_conn[e][k] * ncomp + a] += r_elem[e - elem_begin][a * n_b + k]
+ * for e in [elem_begin, elem_end).  ncomp in {1, 3}. */
+fe_status fe_assemble_vector(const fe_mesh *mesh, int32_t dtype, int32_t ncomp,
+                             int64_t elem_begin, int64_t elem_end, const void *r_elem,
+                             void *r_global, void *stream);
+
+/* Test mode: materialise the geometry of step a1 (fp64):
+ *   detw[E][n_q] = w_q det J,  jinv[E][n_q][3][3] = J^-1 (row-major).
+ * Either pointer may be NULL. */
+fe_status fe_geometry(const fe_mesh *mesh, double *detw, double *jinv, void *stream);
+
+/* Thread-local message of the last failing call ("" if none). */
+const char *fe_last_error(void);
+
+/* Cell index attached to the last FE_ERR_DEGENERATE (-1 if none). */
+int64_t fe_last_error_element(void);
+
+/* Number of kernels this library launched since load (all threads). */
+int64_t fe_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FEB200_H */

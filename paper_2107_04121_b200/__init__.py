@@ -1,0 +1,263 @@
+"""paper_2107_04121_b200 -- batched FE weak-form evaluation on B200 (sm_100a).
+
+Thin ctypes binding of libfeb200.so (C ABI: include/feb200.h).  The functions
+below carry the ABI's names and do argument marshalling only: every step of
+the hot path (geometry, gradients, contractions, gather, scatter-add) runs in
+the library's CUDA kernels.  PyTorch provides device memory and streams.
+
+There is NO CPU fallback: if libfeb200.so is missing or fails to load, the
+first call raises ImportError.  Build it with ``python -m paper_2107_04121_b200.build`` (or
+``__graft_entry__.build()``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfeb200.so")
+
+FE_OK, FE_ERR_INVALID_ARG, FE_ERR_UNSUPPORTED, FE_ERR_DEGENERATE, FE_ERR_CUDA, FE_ERR_OOM = range(6)
+DIFFUSION, MASS, VECTOR_MASS, MASS_DIFFUSION, ELASTICITY, CONVECTIVE = range(6)
+F64, F32 = 0, 1
+MAT_PER_QP, MAT_PER_ELEM, MAT_FULL_D = 0, 1, 2
+NCOMP = {DIFFUSION: 1, MASS: 1, VECTOR_MASS: 3, MASS_DIFFUSION: 1, ELASTICITY: 3, CONVECTIVE: 3}
+_STATUS = {1: "FE_ERR_INVALID_ARG", 2: "FE_ERR_UNSUPPORTED", 3: "FE_ERR_DEGENERATE",
+           4: "FE_ERR_CUDA", 5: "FE_ERR_OOM"}
+
+
+class FEError(RuntimeError):
+    def __init__(self, status: int, msg: str, element: int = -1):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.element = element
+
+
+class fe_material(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("a", ctypes.c_void_p), ("b", ctypes.c_void_p)]
+
+
+class fe_info(ctypes.Structure):
+    _fields_ = [("order", ctypes.c_int32), ("q1d", ctypes.c_int32), ("nb", ctypes.c_int32),
+                ("nq", ctypes.c_int32), ("n_vertices", ctypes.c_int64),
+                ("n_elems", ctypes.c_int64), ("n_nodes", ctypes.c_int64),
+                ("min_det_j", ctypes.c_double)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2107_04121_b200.build` "
+                          "(no CPU fallback exists)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+    lib.fe_create_mesh_geometry.argtypes = [i64, P, i64, P, i32, i32, i64, P, P,
+                                            ctypes.POINTER(P)]
+    lib.fe_destroy_mesh.argtypes = [P]
+    lib.fe_mesh_info.argtypes = [P, ctypes.POINTER(fe_info)]
+    lib.fe_eval_element_matrices.argtypes = [P, i32, i32, ctypes.POINTER(fe_material), P, i64,
+                                             i64, P, P]
+    lib.fe_eval_residual.argtypes = [P, i32, i32, ctypes.POINTER(fe_material), P, i64, i64, P,
+                                     P, P]
+    lib.fe_assemble_vector.argtypes = [P, i32, i32, i64, i64, P, P, P]
+    lib.fe_geometry.argtypes = [P, P, P, P]
+    lib.fe_last_error.restype = ctypes.c_char_p
+    lib.fe_last_error_element.restype = i64
+    lib.fe_launch_count.restype = i64
+    for f in ("fe_create_mesh_geometry", "fe_destroy_mesh", "fe_mesh_info",
+              "fe_eval_element_matrices", "fe_eval_residual", "fe_assemble_vector",
+              "fe_geometry"):
+        getattr(lib, f).restype = ctypes.c_int
+    return lib
+
+
+_lib_handle = None
+
+
+class _LazyLib:
+    """Loads libfeb200.so on first use and raises loudly if it is missing."""
+
+    def __getattr__(self, name):
+        global _lib_handle
+        if _lib_handle is None:
+            _lib_handle = _load()
+        return getattr(_lib_handle, name)
+
+
+_lib = _LazyLib()
+ABI_SYMBOLS = ("fe_create_mesh_geometry", "fe_destroy_mesh", "fe_mesh_info",
+               "fe_eval_element_matrices", "fe_eval_residual", "fe_assemble_vector",
+               "fe_geometry", "fe_last_error", "fe_last_error_element", "fe_launch_count")
+
+
+def lib():
+    """The loaded ctypes library (raises ImportError if not built)."""
+    global _lib_handle
+    if _lib_handle is None:
+        _lib_handle = _load()
+    return _lib_handle
+
+
+def _check(status: int):
+    if status != FE_OK:
+        raise FEError(status, _lib.fe_last_error().decode(), int(_lib.fe_last_error_element()))
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return t.data_ptr()
+
+
+def _dev(t: Optional[torch.Tensor], dtype=None, device="cuda"):
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        t = torch.as_tensor(t)
+    return t.to(device=device, dtype=dtype or t.dtype).contiguous()
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def fe_last_error() -> str:
+    return _lib.fe_last_error().decode()
+
+
+def fe_launch_count() -> int:
+    return int(_lib.fe_launch_count())
+
+
+def fe_create_mesh_geometry(coords: torch.Tensor, conn: torch.Tensor, order: int, q1d: int,
+                            n_nodes: int, dof_conn: Optional[torch.Tensor] = None,
+                            stream=None) -> int:
+    """coords [V][3] f64, conn [E][8] i32, dof_conn [E][nb] i32 (device tensors)."""
+    out = ctypes.c_void_p()
+    _check(_lib.fe_create_mesh_geometry(coords.shape[0], _ptr(coords), conn.shape[0], _ptr(conn),
+                                        order, q1d, n_nodes, _ptr(dof_conn), _stream(stream),
+                                        ctypes.byref(out)))
+    return out.value
+
+
+def fe_destroy_mesh(handle: int):
+    _check(_lib.fe_destroy_mesh(handle))
+
+
+def fe_mesh_info(handle: int) -> fe_info:
+    info = fe_info()
+    _check(_lib.fe_mesh_info(handle, ctypes.byref(info)))
+    return info
+
+
+def _material(kind, a, b):
+    return fe_material(kind, _ptr(a), _ptr(b))
+
+
+def fe_eval_element_matrices(handle: int, form: int, dtype: int, mat_kind: int,
+                             mat_a: Optional[torch.Tensor], mat_b: Optional[torch.Tensor],
+                             state_u: Optional[torch.Tensor], elem_begin: int, elem_end: int,
+                             K: torch.Tensor, stream=None):
+    m = _material(mat_kind, mat_a, mat_b)
+    _check(_lib.fe_eval_element_matrices(handle, form, dtype, ctypes.byref(m), _ptr(state_u),
+                                         elem_begin, elem_end, _ptr(K), _stream(stream)))
+
+
+def fe_eval_residual(handle: int, form: int, dtype: int, mat_kind: int,
+                     mat_a: Optional[torch.Tensor], mat_b: Optional[torch.Tensor],
+                     u: torch.Tensor, elem_begin: int, elem_end: int,
+                     r_elem: Optional[torch.Tensor], r_global: Optional[torch.Tensor],
+                     stream=None):
+    m = _material(mat_kind, mat_a, mat_b)
+    _check(_lib.fe_eval_residual(handle, form, dtype, ctypes.byref(m), _ptr(u), elem_begin,
+                                 elem_end, _ptr(r_elem), _ptr(r_global), _stream(stream)))
+
+
+def fe_assemble_vector(handle: int, dtype: int, ncomp: int, elem_begin: int, elem_end: int,
+                       r_elem: torch.Tensor, r_global: torch.Tensor, stream=None):
+    _check(_lib.fe_assemble_vector(handle, dtype, ncomp, elem_begin, elem_end, _ptr(r_elem),
+                                   _ptr(r_global), _stream(stream)))
+
+
+def fe_geometry(handle: int, detw: Optional[torch.Tensor], jinv: Optional[torch.Tensor],
+                stream=None):
+    _check(_lib.fe_geometry(handle, _ptr(detw), _ptr(jinv), _stream(stream)))
+
+
+class Mesh:
+    """Owning wrapper of an fe_mesh handle plus convenience evaluators.
+
+    All evaluation goes through the C ABI; this class only allocates outputs."""
+
+    def __init__(self, coords, conn, order: int, q1d: Optional[int] = None,
+                 dof_conn=None, n_nodes: Optional[int] = None, device="cuda", stream=None):
+        q1d = order + 1 if q1d is None else q1d
+        coords = _dev(coords, torch.float64, device)
+        conn = _dev(conn, torch.int32, device)
+        dof_conn = None if (dof_conn is None or order == 1 and dof_conn is None) else _dev(
+            dof_conn, torch.int32, device)
+        if n_nodes is None:
+            n_nodes = coords.shape[0] if dof_conn is None else int(dof_conn.max().item()) + 1
+        self.device = device
+        self.handle = fe_create_mesh_geometry(coords, conn, order, q1d, n_nodes, dof_conn, stream)
+        info = fe_mesh_info(self.handle)
+        self.order, self.q1d, self.nb, self.nq = info.order, info.q1d, info.nb, info.nq
+        self.n_elems, self.n_nodes, self.n_vertices = info.n_elems, info.n_nodes, info.n_vertices
+        self.min_det_j = info.min_det_j
+
+    def close(self):
+        if getattr(self, "handle", None):
+            fe_destroy_mesh(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def element_matrices(self, form, mat_kind=MAT_PER_QP, mat_a=None, mat_b=None, state_u=None,
+                         elem_begin=0, elem_end=None, out=None, stream=None):
+        elem_end = self.n_elems if elem_end is None else elem_end
+        ndof = NCOMP[form] * self.nb
+        if out is None:
+            out = torch.empty((elem_end - elem_begin, ndof, ndof), dtype=torch.float64,
+                              device=self.device)
+        fe_eval_element_matrices(self.handle, form, F64, mat_kind, mat_a, mat_b, state_u,
+                                 elem_begin, elem_end, out, stream)
+        return out
+
+    def residual(self, form, u, mat_kind=MAT_PER_QP, mat_a=None, mat_b=None, elem_begin=0,
+                 elem_end=None, r_elem=None, r_global=None, want_elem=False, want_global=True,
+                 stream=None):
+        elem_end = self.n_elems if elem_end is None else elem_end
+        dt = F64 if u.dtype == torch.float64 else F32
+        D = NCOMP[form]
+        if want_elem and r_elem is None:
+            r_elem = torch.empty((elem_end - elem_begin, D * self.nb), dtype=u.dtype,
+                                 device=self.device)
+        if want_global and r_global is None:
+            r_global = torch.zeros((self.n_nodes, D), dtype=u.dtype, device=self.device)
+        fe_eval_residual(self.handle, form, dt, mat_kind, mat_a, mat_b, u, elem_begin, elem_end,
+                         r_elem, r_global, stream)
+        return r_elem, r_global
+
+    def assemble(self, r_elem, ncomp, r_global=None, elem_begin=0, elem_end=None, stream=None):
+        elem_end = self.n_elems if elem_end is None else elem_end
+        if r_global is None:
+            r_global = torch.zeros((self.n_nodes, ncomp), dtype=r_elem.dtype, device=self.device)
+        dt = F64 if r_elem.dtype == torch.float64 else F32
+        fe_assemble_vector(self.handle, dt, ncomp, elem_begin, elem_end, r_elem, r_global, stream)
+        return r_global
+
+    def geometry(self, stream=None):
+        detw = torch.empty((self.n_elems, self.nq), dtype=torch.float64, device=self.device)
+        jinv = torch.empty((self.n_elems, self.nq, 3, 3), dtype=torch.float64, device=self.device)
+        fe_geometry(self.handle, detw, jinv, stream)
+        return detw, jinv

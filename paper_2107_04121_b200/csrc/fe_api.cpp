@@ -1,0 +1,294 @@
+// C ABI of libfeb200.so (include/feb200.h): validation, table set-up, handle
+// ownership and dispatch.  No exception crosses the ABI; errors are fe_status
+// codes with a thread-local message.
+#include <algorithm>
+#include <cstdio>
+#include <new>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fe_internal.h"
+#include "tables.h"
+
+namespace feb200 {
+int64_t launch_count_value();
+}
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_err_elem = -1;
+
+fe_status fail(fe_status s, const std::string& msg, int64_t elem = -1) {
+  g_err = msg;
+  g_err_elem = elem;
+  return s;
+}
+
+fe_status cuda_fail(cudaError_t e, const char* where) {
+  if (e == cudaErrorMemoryAllocation)
+    return fail(FE_ERR_OOM, std::string(where) + ": " + cudaGetErrorString(e));
+  return fail(FE_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+fe_status ok() {
+  g_err.clear();
+  g_err_elem = -1;
+  return FE_OK;
+}
+
+template <typename T>
+cudaError_t upload(T** dst, const std::vector<T>& src, cudaStream_t st) {
+  cudaError_t e = cudaMalloc((void**)dst, src.size() * sizeof(T) + 16);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyAsync(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, st);
+}
+
+void free_mesh(fe_mesh* m) {
+  if (!m) return;
+  void* ptrs[] = {m->coords, m->conn, m->dof_conn, m->xi, m->w, m->phi, m->dphi, m->fwd, m->bwd,
+                  m->phi_f, m->dphi_f, m->fwd_f, m->bwd_f, m->b1, m->d1, m->x1, m->w1};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete m;
+}
+
+int form_ncomp(int form) {
+  return (form == FE_FORM_VECTOR_MASS || form == FE_FORM_ELASTICITY || form == FE_FORM_CONVECTIVE) ? 3 : 1;
+}
+
+fe_status check_common(const fe_mesh* mesh, int form, int64_t e0, int64_t e1) {
+  if (!mesh) return fail(FE_ERR_INVALID_ARG, "mesh is NULL");
+  if (form < FE_FORM_DIFFUSION || form > FE_FORM_CONVECTIVE)
+    return fail(FE_ERR_INVALID_ARG, "unknown form " + std::to_string(form));
+  if (e0 < 0 || e1 > mesh->n_elems || e0 > e1)
+    return fail(FE_ERR_INVALID_ARG, "element range [" + std::to_string(e0) + ", " +
+                                        std::to_string(e1) + ") outside [0, " +
+                                        std::to_string(mesh->n_elems) + ")");
+  return FE_OK;
+}
+
+fe_status check_material(int form, const fe_material* mat) {
+  if (form == FE_FORM_CONVECTIVE) return FE_OK;
+  if (!mat) return fail(FE_ERR_INVALID_ARG, "material is NULL");
+  if (!mat->a) return fail(FE_ERR_INVALID_ARG, "material array a is NULL");
+  if (form == FE_FORM_ELASTICITY) {
+    if (mat->kind != FE_MAT_PER_QP && mat->kind != FE_MAT_PER_ELEM && mat->kind != FE_MAT_FULL_D)
+      return fail(FE_ERR_INVALID_ARG, "unknown material kind");
+    if (mat->kind != FE_MAT_FULL_D && !mat->b)
+      return fail(FE_ERR_INVALID_ARG, "elasticity needs lambda (a) and mu (b)");
+  } else {
+    if (mat->kind != FE_MAT_PER_QP)
+      return fail(FE_ERR_UNSUPPORTED, "this form takes per-quadrature-point material only");
+    if (form == FE_FORM_MASS_DIFFUSION && !mat->b)
+      return fail(FE_ERR_INVALID_ARG, "mass+diffusion needs rho (a) and kappa (b)");
+  }
+  return FE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fe_last_error(void) { return g_err.c_str(); }
+int64_t fe_last_error_element(void) { return g_err_elem; }
+int64_t fe_launch_count(void) { return feb200::launch_count_value(); }
+
+fe_status fe_create_mesh_geometry(int64_t n_vertices, const double* coords, int64_t n_elems,
+                                  const int32_t* conn, int32_t order, int32_t q1d, int64_t n_nodes,
+                                  const int32_t* dof_conn, void* stream, fe_mesh** out) {
+  if (!out) return fail(FE_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (n_vertices < 8 || n_elems < 0) return fail(FE_ERR_INVALID_ARG, "bad sizes");
+  if (!coords || (n_elems > 0 && !conn)) return fail(FE_ERR_INVALID_ARG, "coords/conn is NULL");
+  if (order < 1 || order > 8 || q1d < 1 || q1d > 16)
+    return fail(FE_ERR_INVALID_ARG, "order must be 1..8 and q1d 1..16");
+  if (order > 4 || q1d != order + 1)
+    return fail(FE_ERR_UNSUPPORTED, "GPU path built for order 1..4 with q1d = order + 1");
+  if (order == 1 && !dof_conn) n_nodes = n_vertices;
+  if (order > 1 && !dof_conn) return fail(FE_ERR_INVALID_ARG, "dof_conn required for order > 1");
+  if (n_nodes < 1 || n_nodes >= (int64_t(1) << 31)) return fail(FE_ERR_INVALID_ARG, "bad n_nodes");
+  cudaStream_t st = (cudaStream_t)stream;
+  fe_mesh* m = new (std::nothrow) fe_mesh();
+  if (!m) return fail(FE_ERR_OOM, "host allocation failed");
+  cudaGetDevice(&m->device);
+  m->order = order;
+  m->q1d = q1d;
+  m->nb = (order + 1) * (order + 1) * (order + 1);
+  m->nq = q1d * q1d * q1d;
+  m->n_vertices = n_vertices;
+  m->n_elems = n_elems;
+  m->n_nodes = n_nodes;
+  cudaError_t e;
+#define CK(x, where)                     \
+  do {                                   \
+    e = (x);                             \
+    if (e != cudaSuccess) {              \
+      free_mesh(m);                      \
+      return cuda_fail(e, where);        \
+    }                                    \
+  } while (0)
+  CK(cudaMalloc(&m->coords, sizeof(double) * 3 * n_vertices), "alloc coords");
+  CK(cudaMemcpyAsync(m->coords, coords, sizeof(double) * 3 * n_vertices, cudaMemcpyDefault, st), "copy coords");
+  CK(cudaMalloc(&m->conn, sizeof(int32_t) * 8 * std::max<int64_t>(n_elems, 1)), "alloc conn");
+  if (n_elems > 0)
+    CK(cudaMemcpyAsync(m->conn, conn, sizeof(int32_t) * 8 * n_elems, cudaMemcpyDefault, st), "copy conn");
+  const int64_t ndc = int64_t(m->nb) * std::max<int64_t>(n_elems, 1);
+  CK(cudaMalloc(&m->dof_conn, sizeof(int32_t) * ndc), "alloc dof_conn");
+  if (n_elems > 0)
+    CK(cudaMemcpyAsync(m->dof_conn, dof_conn ? dof_conn : conn, sizeof(int32_t) * m->nb * n_elems,
+                       cudaMemcpyDefault, st), "copy dof_conn");
+  // tables (step a0)
+  feb200::HostTables T = feb200::build_tables(order, q1d);
+  CK(upload(&m->xi, T.xi, st), "tables");
+  CK(upload(&m->w, T.w, st), "tables");
+  CK(upload(&m->phi, T.phi, st), "tables");
+  CK(upload(&m->dphi, T.dphi, st), "tables");
+  CK(upload(&m->fwd, T.fwd, st), "tables");
+  CK(upload(&m->bwd, T.bwd, st), "tables");
+  CK(upload(&m->b1, T.b1, st), "tables");
+  CK(upload(&m->d1, T.d1, st), "tables");
+  CK(upload(&m->x1, T.x1, st), "tables");
+  CK(upload(&m->w1, T.w1, st), "tables");
+  std::vector<float> tmp;
+  auto upf = [&](float** dst, const std::vector<double>& src) {
+    tmp.assign(src.begin(), src.end());
+    cudaError_t ee = upload(dst, tmp, st);
+    if (ee == cudaSuccess) ee = cudaStreamSynchronize(st);  // tmp is reused
+    return ee;
+  };
+  CK(upf(&m->phi_f, T.phi), "tables");
+  CK(upf(&m->dphi_f, T.dphi), "tables");
+  CK(upf(&m->fwd_f, T.fwd), "tables");
+  CK(upf(&m->bwd_f, T.bwd), "tables");
+  // connectivity range checks
+  int* flag = nullptr;
+  CK(cudaMalloc(&flag, sizeof(int) * 2), "alloc flag");
+  CK(cudaMemsetAsync(flag, 0, sizeof(int) * 2, st), "memset");
+  CK(feb200::launch_conn_check(m->conn, 8 * n_elems, n_vertices, flag, st), "conn check");
+  CK(feb200::launch_conn_check(m->dof_conn, int64_t(m->nb) * n_elems, n_nodes, flag + 1, st), "dof check");
+  int hflag[2] = {0, 0};
+  CK(cudaMemcpyAsync(hflag, flag, sizeof(hflag), cudaMemcpyDeviceToHost, st), "copy flag");
+  CK(cudaStreamSynchronize(st), "sync");
+  cudaFree(flag);
+  if (hflag[0] || hflag[1]) {
+    free_mesh(m);
+    return fail(FE_ERR_INVALID_ARG, hflag[0] ? "conn entry out of [0, n_vertices)"
+                                             : "dof_conn entry out of [0, n_nodes)");
+  }
+  // det J > 0 at every (cell, qp)
+  const int64_t nblk = feb200::geometry_check_blocks(m);
+  m->min_det = 1e300;
+  if (nblk > 0) {
+    double* bmin = nullptr;
+    unsigned long long* bad = nullptr;
+    CK(cudaMalloc(&bmin, sizeof(double) * nblk), "alloc");
+    CK(cudaMalloc(&bad, sizeof(unsigned long long)), "alloc");
+    CK(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st), "memset");
+    CK(feb200::launch_geometry_check(m, bmin, bad, nblk, st), "geometry check");
+    std::vector<double> hmin(nblk);
+    unsigned long long hbad = ~0ull;
+    CK(cudaMemcpyAsync(hmin.data(), bmin, sizeof(double) * nblk, cudaMemcpyDeviceToHost, st), "copy");
+    CK(cudaMemcpyAsync(&hbad, bad, sizeof(hbad), cudaMemcpyDeviceToHost, st), "copy");
+    CK(cudaStreamSynchronize(st), "sync");
+    cudaFree(bmin);
+    cudaFree(bad);
+    for (double v : hmin) m->min_det = std::min(m->min_det, v);
+    if (hbad != ~0ull) {
+      free_mesh(m);
+      return fail(FE_ERR_DEGENERATE,
+                  "det J <= 0 in cell " + std::to_string((long long)hbad), (int64_t)hbad);
+    }
+  }
+#undef CK
+  *out = m;
+  return ok();
+}
+
+fe_status fe_destroy_mesh(fe_mesh* mesh) {
+  if (!mesh) return ok();
+  cudaDeviceSynchronize();
+  free_mesh(mesh);
+  return ok();
+}
+
+fe_status fe_mesh_info(const fe_mesh* mesh, fe_info* info) {
+  if (!mesh || !info) return fail(FE_ERR_INVALID_ARG, "NULL argument");
+  info->order = mesh->order;
+  info->q1d = mesh->q1d;
+  info->nb = mesh->nb;
+  info->nq = mesh->nq;
+  info->n_vertices = mesh->n_vertices;
+  info->n_elems = mesh->n_elems;
+  info->n_nodes = mesh->n_nodes;
+  info->min_det_j = mesh->min_det;
+  return ok();
+}
+
+fe_status fe_eval_element_matrices(const fe_mesh* mesh, int32_t form, int32_t dtype,
+                                   const fe_material* mat, const void* state_u, int64_t elem_begin,
+                                   int64_t elem_end, void* K, void* stream) {
+  fe_status s = check_common(mesh, form, elem_begin, elem_end);
+  if (s != FE_OK) return s;
+  if (dtype != FE_F64) return fail(FE_ERR_UNSUPPORTED, "element matrices are built for FE_F64 only");
+  if ((s = check_material(form, mat)) != FE_OK) return s;
+  if (form == FE_FORM_CONVECTIVE && !state_u)
+    return fail(FE_ERR_INVALID_ARG, "convective tangent needs state_u");
+  if (elem_end > elem_begin && !K) return fail(FE_ERR_INVALID_ARG, "K is NULL");
+  feb200::MatArgs ma{mat ? mat->kind : 0, mat ? mat->a : nullptr, mat ? mat->b : nullptr};
+  cudaError_t e = feb200::launch_matrix(mesh, form, ma, (const double*)state_u, elem_begin,
+                                        elem_end, (double*)K, (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported)
+    return fail(FE_ERR_UNSUPPORTED, "matrix mode not built for form " + std::to_string(form) +
+                                        " at order " + std::to_string(mesh->order));
+  if (e != cudaSuccess) return cuda_fail(e, "fe_eval_element_matrices");
+  return ok();
+}
+
+fe_status fe_eval_residual(const fe_mesh* mesh, int32_t form, int32_t dtype, const fe_material* mat,
+                           const void* u, int64_t elem_begin, int64_t elem_end, void* r_elem,
+                           void* r_global, void* stream) {
+  fe_status s = check_common(mesh, form, elem_begin, elem_end);
+  if (s != FE_OK) return s;
+  if ((s = check_material(form, mat)) != FE_OK) return s;
+  if (!u) return fail(FE_ERR_INVALID_ARG, "u is NULL");
+  if (dtype != FE_F64 && dtype != FE_F32) return fail(FE_ERR_INVALID_ARG, "unknown dtype");
+  feb200::MatArgs ma{mat ? mat->kind : 0, mat ? mat->a : nullptr, mat ? mat->b : nullptr};
+  cudaError_t e;
+  if (dtype == FE_F64)
+    e = feb200::launch_residual_f64(mesh, form, ma, (const double*)u, elem_begin, elem_end,
+                                    (double*)r_elem, (double*)r_global, (cudaStream_t)stream);
+  else
+    e = feb200::launch_residual_f32(mesh, form, ma, (const float*)u, elem_begin, elem_end,
+                                    (float*)r_elem, (float*)r_global, (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported)
+    return fail(FE_ERR_UNSUPPORTED, "residual mode not built for form " + std::to_string(form) +
+                                        " / dtype " + std::to_string(dtype) + " at order " +
+                                        std::to_string(mesh->order));
+  if (e != cudaSuccess) return cuda_fail(e, "fe_eval_residual");
+  return ok();
+}
+
+fe_status fe_assemble_vector(const fe_mesh* mesh, int32_t dtype, int32_t ncomp, int64_t elem_begin,
+                             int64_t elem_end, const void* r_elem, void* r_global, void* stream) {
+  fe_status s = check_common(mesh, FE_FORM_DIFFUSION, elem_begin, elem_end);
+  if (s != FE_OK) return s;
+  if (ncomp != 1 && ncomp != 3) return fail(FE_ERR_INVALID_ARG, "ncomp must be 1 or 3");
+  if (dtype != FE_F64 && dtype != FE_F32) return fail(FE_ERR_INVALID_ARG, "unknown dtype");
+  if (elem_end > elem_begin && (!r_elem || !r_global))
+    return fail(FE_ERR_INVALID_ARG, "r_elem / r_global is NULL");
+  cudaError_t e = feb200::launch_assemble(mesh, dtype, ncomp, elem_begin, elem_end, r_elem,
+                                          r_global, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "fe_assemble_vector");
+  return ok();
+}
+
+fe_status fe_geometry(const fe_mesh* mesh, double* detw, double* jinv, void* stream) {
+  if (!mesh) return fail(FE_ERR_INVALID_ARG, "mesh is NULL");
+  cudaError_t e = feb200::launch_geometry_materialize(mesh, detw, jinv, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "fe_geometry");
+  return ok();
+}
+
+}  // extern "C"

@@ -1,0 +1,76 @@
+// Internal (non-ABI) declarations shared by the host API and the kernel units.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "feb200.h"
+
+struct fe_mesh {
+  int32_t order = 0, q1d = 0, nb = 0, nq = 0;
+  int64_t n_vertices = 0, n_elems = 0, n_nodes = 0;
+  double min_det = 0.0;
+  int device = 0;
+  // library-owned device copies
+  double* coords = nullptr;    // [V][3]
+  int32_t* conn = nullptr;     // [E][8]
+  int32_t* dof_conn = nullptr; // [E][nb]  (== conn copy when order == 1)
+  // reference tables (device), fp64 and fp32 copies
+  double *xi = nullptr, *w = nullptr, *phi = nullptr, *dphi = nullptr, *fwd = nullptr, *bwd = nullptr;
+  float *phi_f = nullptr, *dphi_f = nullptr, *fwd_f = nullptr, *bwd_f = nullptr;
+  double *b1 = nullptr, *d1 = nullptr, *x1 = nullptr, *w1 = nullptr;  // 1D tables
+};
+
+namespace feb200 {
+
+// Read-only view passed to kernels by value.
+struct MeshView {
+  const double* coords;
+  const int32_t* conn;
+  const int32_t* dof_conn;
+  int64_t n_elems;
+  const double* xi;
+  const double* w;
+  const double* phi;
+  const double* dphi;
+  const double* fwd;
+  const double* bwd;
+  const float* fwd_f;
+  const float* bwd_f;
+  const double* b1;
+  const double* d1;
+};
+
+inline MeshView view_of(const fe_mesh* m) {
+  return MeshView{m->coords, m->conn, m->dof_conn, m->n_elems, m->xi, m->w, m->phi, m->dphi,
+                  m->fwd, m->bwd, m->fwd_f, m->bwd_f, m->b1, m->d1};
+}
+
+struct MatArgs {
+  int kind;
+  const void* a;
+  const void* b;
+};
+
+// Launchers (return cudaError_t of the launch; cudaErrorNotSupported when the
+// (form, order, dtype) combination is not built).
+cudaError_t launch_matrix(const fe_mesh* m, int form, MatArgs mat, const double* state_u,
+                          int64_t e0, int64_t e1, double* K, cudaStream_t st);
+cudaError_t launch_residual_f64(const fe_mesh* m, int form, MatArgs mat, const double* u,
+                                int64_t e0, int64_t e1, double* r_elem, double* r_global,
+                                cudaStream_t st);
+cudaError_t launch_residual_f32(const fe_mesh* m, int form, MatArgs mat, const float* u,
+                                int64_t e0, int64_t e1, float* r_elem, float* r_global,
+                                cudaStream_t st);
+cudaError_t launch_assemble(const fe_mesh* m, int dtype, int ncomp, int64_t e0, int64_t e1,
+                            const void* r_elem, void* r_global, cudaStream_t st);
+cudaError_t launch_geometry_check(const fe_mesh* m, double* block_min, unsigned long long* bad,
+                                  int64_t nblocks, cudaStream_t st);
+int64_t geometry_check_blocks(const fe_mesh* m);
+cudaError_t launch_conn_check(const int32_t* idx, int64_t count, int64_t bound, int* flag,
+                              cudaStream_t st);
+cudaError_t launch_geometry_materialize(const fe_mesh* m, double* detw, double* jinv,
+                                        cudaStream_t st);
+
+void count_launch();
+
+}  // namespace feb200

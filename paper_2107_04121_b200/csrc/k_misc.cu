@@ -1,0 +1,130 @@
+// Geometry check / materialisation (step a1) and standalone assembly (step d).
+#include <algorithm>
+#include <atomic>
+
+#include "fe_device.cuh"
+#include "fe_internal.h"
+
+namespace feb200 {
+
+namespace {
+std::atomic_int64_t* launch_counter() {
+  static std::atomic_int64_t c{0};
+  return &c;
+}
+}  // namespace
+
+void count_launch() { launch_counter()->fetch_add(1); }
+int64_t launch_count_value() { return launch_counter()->load(); }
+
+// det J at every (cell, qp); per-block minimum and first cell with det <= 0.
+__global__ void __launch_bounds__(256) k_geom_check(MeshView m, int nq, double* block_min,
+                                                    unsigned long long* bad) {
+  __shared__ double red[256];
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double det = 1e300;
+  if (idx < m.n_elems * nq) {
+    const int64_t e = idx / nq;
+    const int q = (int)(idx - e * nq);
+    double xv[24];
+#pragma unroll
+    for (int r = 0; r < 24; ++r) xv[r] = m.coords[3 * (int64_t)m.conn[8 * e + r / 3] + r % 3];
+    double Ji[9];
+    det = hex_geometry(xv, m.xi[3 * q], m.xi[3 * q + 1], m.xi[3 * q + 2], Ji);
+    if (!(det > 0.0)) {
+      atomicMin(bad, (unsigned long long)e);
+      if (det != det) det = -1e300;
+    }
+  }
+  red[threadIdx.x] = det;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) red[threadIdx.x] = fmin(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) block_min[blockIdx.x] = red[0];
+}
+
+int64_t geometry_check_blocks(const fe_mesh* m) { return (m->n_elems * m->nq + 255) / 256; }
+
+cudaError_t launch_geometry_check(const fe_mesh* m, double* block_min, unsigned long long* bad,
+                                  int64_t nblocks, cudaStream_t st) {
+  if (nblocks <= 0) return cudaSuccess;
+  k_geom_check<<<(unsigned)nblocks, 256, 0, st>>>(view_of(m), m->nq, block_min, bad);
+  count_launch();
+  return cudaGetLastError();
+}
+
+__global__ void k_conn_check(const int32_t* idx, int64_t count, int64_t bound, int* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = idx[i];
+    if (v < 0 || v >= bound) atomicOr(flag, 1);
+  }
+}
+
+cudaError_t launch_conn_check(const int32_t* idx, int64_t count, int64_t bound, int* flag,
+                              cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  const int grid = (int)std::min<int64_t>((count + 255) / 256, 148 * 16);
+  k_conn_check<<<grid, 256, 0, st>>>(idx, count, bound, flag);
+  count_launch();
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) k_geom_materialize(MeshView m, int nq, double* detw,
+                                                          double* jinv) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= m.n_elems * nq) return;
+  const int64_t e = idx / nq;
+  const int q = (int)(idx - e * nq);
+  double xv[24];
+#pragma unroll
+  for (int r = 0; r < 24; ++r) xv[r] = m.coords[3 * (int64_t)m.conn[8 * e + r / 3] + r % 3];
+  double Ji[9];
+  const double det = hex_geometry(xv, m.xi[3 * q], m.xi[3 * q + 1], m.xi[3 * q + 2], Ji);
+  if (detw) detw[idx] = m.w[q] * det;
+  if (jinv)
+#pragma unroll
+    for (int i = 0; i < 9; ++i) jinv[9 * idx + i] = Ji[i];
+}
+
+cudaError_t launch_geometry_materialize(const fe_mesh* m, double* detw, double* jinv,
+                                        cudaStream_t st) {
+  const int64_t n = m->n_elems * m->nq;
+  if (n <= 0) return cudaSuccess;
+  k_geom_materialize<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(view_of(m), m->nq, detw, jinv);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// r_global[dof_conn[e][k] * D + a] += r_elem[e - e0][a * nb + k]
+template <typename T>
+__global__ void k_assemble(const int32_t* __restrict__ dof_conn, int nb, int D, int64_t e0,
+                           int64_t e1, const T* __restrict__ r_elem, T* __restrict__ r_global) {
+  const int64_t n = (e1 - e0) * nb * D;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t el = i / (nb * D);
+    const int r = (int)(i - el * nb * D);
+    const int a = r / nb, k = r - a * nb;
+    atomicAdd(r_global + (int64_t)dof_conn[(e0 + el) * nb + k] * D + a, r_elem[i]);
+  }
+}
+
+cudaError_t launch_assemble(const fe_mesh* m, int dtype, int ncomp, int64_t e0, int64_t e1,
+                            const void* r_elem, void* r_global, cudaStream_t st) {
+  const int64_t n = (e1 - e0) * m->nb * ncomp;
+  if (n <= 0) return cudaSuccess;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 32);
+  if (dtype == FE_F64)
+    k_assemble<double><<<grid, 256, 0, st>>>(m->dof_conn, m->nb, ncomp, e0, e1,
+                                             (const double*)r_elem, (double*)r_global);
+  else
+    k_assemble<float><<<grid, 256, 0, st>>>(m->dof_conn, m->nb, ncomp, e0, e1,
+                                            (const float*)r_elem, (float*)r_global);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace feb200

@@ -1,0 +1,224 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Tolerances (BASELINE.json north_star): normwise relative
+error <= 1e-12 in fp64 over the whole output array (stacked K in Frobenius
+norm, residual vectors in 2-norm); <= 1e-5 for the fp32 residual path against
+the fp64 oracle.  Atomic scatter order is the only allowed source of
+difference.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import fe_inputs as fi
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-12
+TOL32 = 1e-5
+
+
+def fe():
+    import paper_2107_04121_b200 as m
+    return m
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-300)
+
+
+def gpu_mesh(prob):
+    m = fe()
+    return m.Mesh(torch.from_numpy(prob.coords), torch.from_numpy(prob.conn), prob.p, prob.q1d,
+                  dof_conn=None if prob.p == 1 else torch.from_numpy(prob.dof_conn),
+                  n_nodes=prob.n_nodes)
+
+
+def dev(a, dtype=torch.float64):
+    return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dtype)
+
+
+# ragged element counts: several CTA batches plus a partial tail
+SHAPES = [(5, 3, 4), (7, 2, 3)]
+MATRIX_CASES = [(f, p) for f in (0, 1, 2, 3, 4, 5) for p in (1, 2)] + [(0, 3), (1, 3), (3, 3)]
+RESIDUAL_CASES = [(f, p) for f in (0, 1, 2, 3, 4, 5) for p in (1, 2, 3)] + \
+                 [(0, 4), (1, 4), (3, 4), (2, 4), (4, 4), (5, 4)]
+
+
+@pytest.mark.parametrize("form,p", MATRIX_CASES)
+@pytest.mark.parametrize("shape", SHAPES)
+def test_matrix_parity(form, p, shape):
+    pr = fi.make_problem(form, p, shape, 1000 + 10 * form + p)
+    Kref = oracle.problem_matrix(pr)
+    mesh = gpu_mesh(pr)
+    K = mesh.element_matrices(form, pr.mat_kind, dev(pr.mat_a), dev(pr.mat_b),
+                              dev(pr.u) if form == fi.CONVECTIVE else None)
+    torch.cuda.synchronize()
+    assert rel(K.cpu().numpy(), Kref) <= TOL64
+
+
+@pytest.mark.parametrize("kind", [fi.MAT_PER_ELEM, fi.MAT_PER_QP, fi.MAT_FULL_D])
+def test_elasticity_material_kinds(kind):
+    pr = fi.make_problem(fi.ELASTICITY, 2, (3, 3, 2), 77, mat_kind=kind)
+    mesh = gpu_mesh(pr)
+    K = mesh.element_matrices(fi.ELASTICITY, kind, dev(pr.mat_a), dev(pr.mat_b))
+    assert rel(K.cpu().numpy(), oracle.problem_matrix(pr)) <= TOL64
+    re_, rg = mesh.residual(fi.ELASTICITY, dev(pr.u), kind, dev(pr.mat_a), dev(pr.mat_b),
+                            want_elem=True)
+    assert rel(re_.cpu().numpy(), oracle.problem_residual(pr)) <= TOL64
+
+
+@pytest.mark.parametrize("form,p", RESIDUAL_CASES)
+@pytest.mark.parametrize("shape", SHAPES)
+def test_residual_parity(form, p, shape):
+    pr = fi.make_problem(form, p, shape, 2000 + 10 * form + p)
+    r_ref = oracle.problem_residual(pr)
+    R_ref = oracle.assemble(r_ref, pr.dof_conn, pr.n_nodes, pr.ncomp)
+    mesh = gpu_mesh(pr)
+    r_elem, r_glob = mesh.residual(form, dev(pr.u), pr.mat_kind, dev(pr.mat_a), dev(pr.mat_b),
+                                   want_elem=True)
+    torch.cuda.synchronize()
+    assert rel(r_elem.cpu().numpy(), r_ref) <= TOL64
+    assert rel(r_glob.cpu().numpy().ravel(), R_ref) <= TOL64
+
+
+@pytest.mark.parametrize("form,p", [(0, 1), (0, 2), (1, 2), (3, 2), (3, 4), (0, 4)])
+def test_residual_fp32(form, p):
+    pr = fi.make_problem(form, p, (5, 3, 4), 3000 + form)
+    r_ref = oracle.problem_residual(pr)
+    R_ref = oracle.assemble(r_ref, pr.dof_conn, pr.n_nodes, pr.ncomp)
+    mesh = gpu_mesh(pr)
+    r_elem, r_glob = mesh.residual(form, dev(pr.u, torch.float32), pr.mat_kind,
+                                   dev(pr.mat_a, torch.float32), dev(pr.mat_b, torch.float32),
+                                   want_elem=True)
+    assert r_elem.dtype == torch.float32
+    assert rel(r_elem.cpu().numpy(), r_ref) <= TOL32
+    assert rel(r_glob.cpu().numpy().ravel(), R_ref) <= TOL32
+
+
+@pytest.mark.parametrize("form,p", [(0, 2), (4, 2), (5, 2), (3, 4)])
+def test_element_ranges(form, p):
+    """elem_begin / elem_end split (boundary-first overlap) == one full call."""
+    pr = fi.make_problem(form, p, (4, 3, 5), 4000 + form)
+    mesh = gpu_mesh(pr)
+    args = (pr.mat_kind, dev(pr.mat_a), dev(pr.mat_b))
+    u = dev(pr.u)
+    E = pr.n_elems
+    cuts = [0, 7, 8, 31, E - 1, E]
+    R = torch.zeros((pr.n_nodes, pr.ncomp), dtype=torch.float64, device="cuda")
+    parts = []
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        re_, _ = mesh.residual(form, u, *args, elem_begin=a, elem_end=b, r_global=R,
+                               want_elem=True)
+        parts.append(re_.cpu().numpy())
+    r_ref = oracle.problem_residual(pr)
+    assert rel(np.concatenate(parts), r_ref) <= TOL64
+    R_ref = oracle.assemble(r_ref, pr.dof_conn, pr.n_nodes, pr.ncomp)
+    assert rel(R.cpu().numpy().ravel(), R_ref) <= TOL64
+    if p <= 2:
+        Ks = [mesh.element_matrices(form, *args, state_u=u if form == 5 else None,
+                                    elem_begin=a, elem_end=b).cpu().numpy()
+              for a, b in zip(cuts[:-1], cuts[1:])]
+        assert rel(np.concatenate(Ks), oracle.problem_matrix(pr)) <= TOL64
+    # empty range is a no-op
+    re_, _ = mesh.residual(form, u, *args, elem_begin=5, elem_end=5, r_global=R, want_elem=True)
+    assert re_.shape[0] == 0
+
+
+def test_assemble_vector():
+    pr = fi.make_problem(fi.ELASTICITY, 2, (3, 4, 2), 55)
+    r_ref = oracle.problem_residual(pr)
+    mesh = gpu_mesh(pr)
+    R = mesh.assemble(dev(r_ref), 3)
+    R_ref = oracle.assemble(r_ref, pr.dof_conn, pr.n_nodes, 3)
+    assert rel(R.cpu().numpy().ravel(), R_ref) <= TOL64
+    r32 = mesh.assemble(dev(r_ref, torch.float32), 3)
+    assert rel(r32.cpu().numpy().ravel(), R_ref) <= TOL32
+
+
+@pytest.mark.parametrize("p", [1, 2, 4])
+def test_geometry_materialized(p):
+    pr = fi.make_problem(fi.DIFFUSION, p, (4, 3, 2), 66)
+    detw_ref, jinv_ref = oracle.geometry(p + 1, pr.coords, pr.conn)
+    mesh = gpu_mesh(pr)
+    detw, jinv = mesh.geometry()
+    assert rel(detw.cpu().numpy(), detw_ref) <= TOL64
+    assert rel(jinv.cpu().numpy(), jinv_ref) <= TOL64
+    assert abs(mesh.min_det_j - (detw_ref / oracle.tables(p, p + 1)[1]).min()) <= 1e-12
+
+
+def test_degenerate_and_invalid():
+    m = fe()
+    pr = fi.make_problem(fi.DIFFUSION, 1, (3, 2, 1), 1)
+    conn = pr.conn.copy()
+    conn[4] = conn[4][[1, 0, 3, 2, 5, 4, 7, 6]]
+    with pytest.raises(m.FEError) as ei:
+        m.Mesh(pr.coords, conn, 1)
+    assert ei.value.status == m.FE_ERR_DEGENERATE and ei.value.element == 4
+    bad = pr.conn.copy()
+    bad[2, 3] = pr.coords.shape[0]
+    with pytest.raises(m.FEError) as ei:
+        m.Mesh(pr.coords, bad, 1)
+    assert ei.value.status == m.FE_ERR_INVALID_ARG
+    with pytest.raises(m.FEError) as ei:
+        m.Mesh(pr.coords, pr.conn, 5, dof_conn=pr.dof_conn, n_nodes=pr.n_nodes)
+    assert ei.value.status == m.FE_ERR_UNSUPPORTED
+    mesh = gpu_mesh(pr)
+    with pytest.raises(m.FEError) as ei:
+        mesh.residual(0, dev(pr.u), 0, dev(pr.mat_a), None, elem_begin=0, elem_end=pr.n_elems + 1)
+    assert ei.value.status == m.FE_ERR_INVALID_ARG
+    with pytest.raises(m.FEError) as ei:
+        mesh.element_matrices(5, 0, None, None, None)   # convective without a state
+    assert ei.value.status == m.FE_ERR_INVALID_ARG
+
+
+def _sample_subproblem(pr, idx):
+    return fi.Problem(pr.name, pr.form, pr.p, pr.q1d, pr.shape, pr.coords, pr.conn[idx],
+                      pr.dof_conn[idx], pr.n_nodes, pr.mat_kind,
+                      None if pr.mat_a is None else pr.mat_a[idx],
+                      None if pr.mat_b is None else pr.mat_b[idx], pr.u)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_config_full_size(name):
+    """BASELINE configs at full size in the bench launch configuration: matrices
+    on a seeded sample of cells checked one by one against the oracle; the
+    assembled residual checked in full (C1-C4) or on the slab of cells whose
+    nodes are sampled (C5)."""
+    pr = fi.make_config(name)
+    mesh = gpu_mesh(pr)
+    rng = np.random.default_rng(7)
+    E = pr.n_elems
+    idx = np.unique(np.concatenate([[0, E - 1], rng.choice(E, size=min(E, 48), replace=False)]))
+    sub = _sample_subproblem(pr, idx)
+    mat = (pr.mat_kind, dev(pr.mat_a), dev(pr.mat_b))
+    u = dev(pr.u)
+    if name != "C4":
+        src = fi.corner_subproblem(pr, 64) if name == "C5" else pr
+        mesh_m = gpu_mesh(src) if name == "C5" else mesh
+        idx_m = idx[idx < src.n_elems]
+        K = mesh_m.element_matrices(src.form, src.mat_kind, dev(src.mat_a), dev(src.mat_b),
+                                    u if src.form == fi.CONVECTIVE else None)
+        Kref = oracle.problem_matrix(_sample_subproblem(src, idx_m))
+        assert rel(K[torch.from_numpy(idx_m).cuda()].cpu().numpy(), Kref) <= TOL64
+        del K
+    r_elem, r_glob = mesh.residual(pr.form, u, *mat, want_elem=True)
+    r_ref = oracle.problem_residual(sub)
+    assert rel(r_elem[torch.from_numpy(idx).cuda()].cpu().numpy(), r_ref) <= TOL64
+    if name in ("C1", "C2", "C3", "C4"):
+        R_ref = oracle.problem_assembled_residual(pr)
+        assert rel(r_glob.cpu().numpy().ravel(), R_ref) <= TOL64
+    else:
+        # assembled vector == assemble of the GPU's own element residuals (atomics only)
+        R2 = mesh.assemble(r_elem, pr.ncomp)
+        assert rel(r_glob.cpu().numpy(), R2.cpu().numpy()) <= 1e-14
+    if name == "C4":
+        r_elem32, r_glob32 = mesh.residual(pr.form, dev(pr.u, torch.float32), pr.mat_kind,
+                                           dev(pr.mat_a, torch.float32),
+                                           dev(pr.mat_b, torch.float32), want_elem=True)
+        assert rel(r_glob32.cpu().numpy().ravel(), R_ref) <= TOL32
