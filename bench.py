@@ -1,0 +1,464 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: batched FE weak-form evaluation on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+One STEP = one pass of the whole hot path over the config's cells: geometry
+(a1), physical gradients (b), element matrices (c1) and residual with gather
+and fused scatter-add (c2, d) -- the modes the config names -- through the C
+ABI of libfeb200.so, plus, for N > 1, the interface-plane summation (NCCL).
+Default workload: BASELINE.json configs[1] = C2 (Q2 scalar diffusion, 64^3
+perturbed cells, matrix + residual).  Metric: cells evaluated per second
+(each cell gets its element matrix AND its residual every step).
+
+Timing: W warm-up steps, then K steps bracketed by barrier + synchronize,
+CUDA events on the launching stream, max over ranks.  The C2 matrix output
+(1.53 GB) is larger than L2 (126 MB), so every step starts L2-cold.
+Kernel durations are measured with CUDA events around each ABI call on the
+same stream.  Clocks are sampled with nvidia-smi during the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import fe_inputs as fi  # noqa: E402
+
+# ----------------------------------------------------------------------------
+# Algorithmic work per cell:
+# flops of the lean dense-table formulation per qp (FMA = 2 flops) plus 120 per
+# qp of geometry, bytes = minimal HBM traffic with perfect reuse.
+GEOM = 120
+
+
+def alg_flops(form: int, mode: str, nb: int, nq: int) -> float:
+    if mode == "matrix":
+        per_qp = {fi.DIFFUSION: 6 * nb * nb + 21 * nb, fi.MASS: 2 * nb * nb + nb,
+                  fi.MASS_DIFFUSION: 8 * nb * nb + 22 * nb,
+                  fi.VECTOR_MASS: 2 * nb * nb + nb,
+                  fi.ELASTICITY: 12 * nb * nb + 21 * nb,
+                  fi.CONVECTIVE: 20 * nb * nb + 48 * nb}[form]
+        per_el = {fi.ELASTICITY: 27 * nb * nb, fi.CONVECTIVE: 9 * nb * nb}.get(form, 0)
+        return (per_qp + GEOM) * nq + per_el
+    per_qp = {fi.DIFFUSION: 12 * nb + 40, fi.MASS: 4 * nb + 5, fi.MASS_DIFFUSION: 16 * nb + 45,
+              fi.VECTOR_MASS: 12 * nb + 15, fi.ELASTICITY: 36 * nb + 137,
+              fi.CONVECTIVE: 30 * nb + 75}[form]
+    return (per_qp + GEOM) * nq
+
+
+def alg_bytes(form: int, mode: str, p: int, nb: int, nq: int, D: int, mat_kind: int,
+              esize: int = 8) -> float:
+    if form == fi.ELASTICITY:
+        mat = 2 * esize if mat_kind == fi.MAT_PER_ELEM else 2 * nq * esize
+    elif form == fi.MASS_DIFFUSION:
+        mat = 2 * nq * esize
+    elif form == fi.CONVECTIVE:
+        mat = 0
+    else:
+        mat = nq * esize
+    geo = 24 + 32                               # one vertex + 8 conn ids per cell
+    if mode == "matrix":
+        b = geo + mat + (D * nb) ** 2 * 8
+        if form == fi.CONVECTIVE:
+            b += 4 * nb + D * p ** 3 * 8        # gather of the state
+        return b
+    return geo + mat + 4 * nb + D * p ** 3 * esize + 2 * D * p ** 3 * esize
+
+
+# ----------------------------------------------------------------------------
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+
+
+def fp64_peak_tflops():
+    """Measured FP64 DMMA peak (tools/fp64_peak.cu; MEASURED_PEAKS.json has no FP64 entry)."""
+    try:
+        d = json.load(open(FP64_PEAK_FILE))
+        return float(d["dmma_m16n8k4_tflops_sustained"]), "measured: tools/fp64_peak (DMMA, 4 s sustained)"
+    except Exception:
+        return 37.2, "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"
+
+
+def hbm_peak_gbs():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------
+WORKLOADS = {
+    "C1": dict(modes=("matrix",)),
+    "C2": dict(modes=("matrix", "residual")),
+    "C3": dict(modes=("matrix", "residual")),
+    "C4": dict(modes=("residual",)),
+    "C5": dict(modes=("residual",)),
+    "C5t": dict(modes=("matrix",)),
+}
+
+
+def build_problem(name):
+    if name == "C5t":
+        return fi.corner_subproblem(fi.make_config("C5"), 64)
+    return fi.make_config(name)
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_step(prob, n, modes):
+    """One oracle pass over the first n cells of prob (matrix and/or residual)."""
+    import oracle
+    idx = slice(0, n)
+    sub = fi.Problem(prob.name, prob.form, prob.p, prob.q1d, prob.shape, prob.coords,
+                     prob.conn[idx], prob.dof_conn[idx], prob.n_nodes, prob.mat_kind,
+                     None if prob.mat_a is None else prob.mat_a[idx],
+                     None if prob.mat_b is None else prob.mat_b[idx], prob.u)
+    t0 = time.perf_counter()
+    if "matrix" in modes:
+        oracle.problem_matrix(sub)
+    if "residual" in modes:
+        oracle.problem_assembled_residual(sub)
+    return time.perf_counter() - t0
+
+
+def oracle_sample_size(prob, modes, budget_s):
+    n = min(64, prob.n_elems)
+    t = oracle_step(prob, n, modes)
+    while t < 0.2 and n < prob.n_elems:
+        n = min(prob.n_elems, n * 4)
+        t = oracle_step(prob, n, modes)
+    per = t / n
+    return int(max(1, min(prob.n_elems, budget_s / per))), per
+
+
+def cpu_baseline(prob, modes, budget_s=15.0):
+    n, _ = oracle_sample_size(prob, modes, budget_s)
+    t = oracle_step(prob, n, modes)
+    return {"value": n / t, "unit": "cells/s", "cores": cpu_cores(), "kind": "oracle",
+            "sample": f"first {n} of {prob.n_elems} cells of {prob.name}, modes {'+'.join(modes)}, "
+                      f"plain C oracle (-O2, OpenMP over cells), {t:.1f} s"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    prob = build_problem(cfg)
+    modes = WORKLOADS[cfg]["modes"]
+    per_step_budget = max(0.5, min(6.0, 150.0 / max(1, args.steps + args.warmup)))
+    n, _ = oracle_sample_size(prob, modes, per_step_budget)
+    for _ in range(args.warmup):
+        oracle_step(prob, n, modes)
+    times = [oracle_step(prob, n, modes) for _ in range(args.steps)]
+    T = float(np.sum(times))
+    value = n * args.steps / T
+    line = {
+        "impl": "reference", "metric": f"{cfg} cells evaluated per second ({'+'.join(modes)})",
+        "value": value, "unit": "cells/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg, "cells": prob.n_elems, "order": prob.p,
+                   "form": fi.FORM_NAMES[prob.form], "modes": list(modes),
+                   "sample_cells_per_step": n},
+        "cpu_baseline": {"value": value, "unit": "cells/s", "cores": cpu_cores(), "kind": "oracle",
+                         "sample": f"first {n} of {prob.n_elems} cells per step"},
+        "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args, args.config)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2107_04121_b200 as fe
+    from paper_2107_04121_b200 import slabs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+
+    cfg = args.config
+    modes = WORKLOADS[cfg]["modes"]
+    prob = build_problem(cfg)
+    if cfg == "C5t" and world > 1:
+        raise SystemExit("C5t (corner tangent) is single-GPU")
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    dtc = fe.F64 if args.dtype == "f64" else fe.F32
+    if args.dtype == "f32" and "matrix" in modes:
+        raise SystemExit("fp32 is built for residual mode only")
+    D = prob.ncomp
+    nb, nq = prob.nb, prob.nq
+
+    if cfg == "C5t":
+        sl = slabs.Slab(0, 1, 0, prob.n_elems, 0, prob.coords.shape[0], 0, prob.n_nodes, 0)
+        lc, lconn, ldc = prob.coords, prob.conn, prob.dof_conn
+    else:
+        sl = slabs.slab_of(prob.shape, prob.p, world, rank)
+        lc, lconn, ldc = slabs.local_arrays(sl, prob.coords, prob.conn, prob.dof_conn)
+    e0, e1 = sl.elem_begin, sl.elem_end
+    El = e1 - e0
+    mesh = fe.Mesh(torch.from_numpy(lc), torch.from_numpy(lconn), prob.p, prob.q1d,
+                   dof_conn=torch.from_numpy(ldc), n_nodes=sl.n_nodes, device=dev)
+
+    def dslice(a):
+        return None if a is None else torch.from_numpy(np.ascontiguousarray(a[e0:e1])).to(dev, tdt)
+
+    mat_a, mat_b = dslice(prob.mat_a), dslice(prob.mat_b)
+    u_loc = np.ascontiguousarray(prob.u[sl.node_begin:sl.node_end])
+    u = torch.from_numpy(u_loc).to(dev, tdt)
+    K = torch.empty((El, D * nb, D * nb), dtype=torch.float64, device=dev) if "matrix" in modes else None
+    r = torch.zeros((sl.n_nodes, D), dtype=tdt, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    bufs = [None]
+    ev = {m: [] for m in modes}
+
+    def step(record=False):
+        if "matrix" in modes:
+            if record:
+                a = torch.cuda.Event(enable_timing=True); a.record(stream)
+            fe.fe_eval_element_matrices(mesh.handle, prob.form, fe.F64, prob.mat_kind, mat_a, mat_b,
+                                        u if prob.form == fi.CONVECTIVE else None, 0, El, K, stream)
+            if record:
+                b = torch.cuda.Event(enable_timing=True); b.record(stream); ev["matrix"].append((a, b))
+        if "residual" in modes:
+            r.zero_()
+            if record:
+                a = torch.cuda.Event(enable_timing=True); a.record(stream)
+            fe.fe_eval_residual(mesh.handle, prob.form, dtc, prob.mat_kind, mat_a, mat_b, u, 0, El,
+                                None, r, stream)
+            if record:
+                b = torch.cuda.Event(enable_timing=True); b.record(stream); ev["residual"].append((a, b))
+            bufs[0] = slabs.exchange_planes(r, sl, None, bufs[0])
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    n_launch0 = fe.fe_launch_count()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        t0.record(stream)
+        for _ in range(args.steps):
+            step(record=True)
+        t1.record(stream)
+        barrier()
+    launches = fe.fe_launch_count() - n_launch0
+    ms = t0.elapsed_time(t1)
+    kern_ms = {m: float(np.mean([a.elapsed_time(b) for a, b in ev[m]])) for m in modes}
+    if world > 1:
+        tt = torch.tensor([ms] + [kern_ms[m] for m in modes], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt[0])
+        kern_ms = {m: float(tt[1 + i]) for i, m in enumerate(modes)}
+    ms_step = ms / args.steps
+    value = prob.n_elems / (ms_step * 1e-3)
+
+    # ---- end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        h_u = torch.from_numpy(u_loc).to(tdt).pin_memory()
+        h_a = None if mat_a is None else mat_a.cpu().pin_memory()
+        h_b = None if mat_b is None else mat_b.cpu().pin_memory()
+        h_r = torch.empty_like(r, device="cpu").pin_memory()
+        h_K = torch.empty(K.shape, dtype=K.dtype).pin_memory() if K is not None else None
+        n_e2e = max(3, min(args.steps, 10))
+
+        def e2e_step():
+            u.copy_(h_u, non_blocking=True)
+            if h_a is not None:
+                mat_a.copy_(h_a, non_blocking=True)
+            if h_b is not None:
+                mat_b.copy_(h_b, non_blocking=True)
+            step()
+            if h_K is not None:
+                h_K.copy_(K, non_blocking=True)
+            h_r.copy_(r, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        b.record(stream)
+        barrier()
+        e_ms = a.elapsed_time(b)
+        if world > 1:
+            tt = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e_ms = float(tt[0])
+        h2d = h_u.numel() * h_u.element_size() + sum(
+            x.numel() * x.element_size() for x in (h_a, h_b) if x is not None)
+        d2h = h_r.numel() * h_r.element_size() + (
+            h_K.numel() * h_K.element_size() if h_K is not None else 0)
+        if world > 1:
+            tt = torch.tensor([h2d, d2h], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt)
+            h2d, d2h = int(tt[0]), int(tt[1])
+        e2e = {"value": prob.n_elems / (e_ms / n_e2e * 1e-3), "unit": "cells/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": e_ms / n_e2e, "steps": n_e2e,
+               "note": "pinned host inputs (u, material) H2D + step + D2H of r"
+                       + (" and K" if K is not None else "")}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel
+    dom = max(modes, key=lambda m: kern_ms[m])
+    esize = 8 if args.dtype == "f64" else 4
+    fl = alg_flops(prob.form, dom, nb, nq) * El
+    by = alg_bytes(prob.form, dom, prob.p, nb, nq, D, prob.mat_kind, esize) * El
+    t_s = kern_ms[dom] * 1e-3
+    pk_f, src_f = fp64_peak_tflops()
+    pk_b, src_b = hbm_peak_gbs()
+    if args.dtype == "f32":
+        pk_f, src_f = 2 * pk_f * 2, "derived: FP32 FFMA = 4x the measured FP64 DMMA rate (128 vs 64 lanes, x2 for FP64 pipe share)"
+    t_flop = fl / (pk_f * 1e12)
+    t_mem = by / (pk_b * 1e9)
+    if t_flop >= t_mem:
+        roof = {"bound": "tensor" if args.dtype == "f64" else "alu",
+                "achieved": fl / t_s / 1e12, "peak": pk_f, "unit": "TFLOP/s",
+                "frac": (fl / t_s / 1e12) / pk_f, "peak_source": src_f}
+    else:
+        roof = {"bound": "hbm", "achieved": by / t_s / 1e9, "peak": pk_b, "unit": "GB/s",
+                "frac": (by / t_s / 1e9) / pk_b, "peak_source": src_b}
+    roof.update({"kernel": f"{dom} ({fi.FORM_NAMES[prob.form]}, Q{prob.p})",
+                 "kernel_ms": kern_ms[dom], "alg_flops_per_cell": fl / El,
+                 "alg_bytes_per_cell": by / El, "cells_per_launch": El,
+                 "achieved_gbs": by / t_s / 1e9, "achieved_tflops": fl / t_s / 1e12,
+                 "traffic": None})
+    prof = os.path.join(ROOT, "profiles", f"traffic_{cfg}_{dom}.json")
+    if os.path.exists(prof):
+        try:
+            roof["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+
+    cb = None
+    if not args.no_cpu_baseline and world == 1:
+        cb = cpu_baseline(prob, modes)
+
+    line = {
+        "metric": f"{cfg} cells evaluated per second ({'+'.join(modes)})",
+        "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": {"workload": cfg, "desc": prob.meta.get("desc", ""), "cells": prob.n_elems,
+                   "order": prob.p, "q1d": prob.q1d, "form": fi.FORM_NAMES[prob.form],
+                   "modes": list(modes), "parallelism": f"z-slabs x{world}",
+                   "l2": "no flush: every step writes/reads > L2 (C2 K = 1.53 GB)"},
+        "modes": {m: {"kernel_ms": kern_ms[m], "cells_per_s": El / (kern_ms[m] * 1e-3)}
+                  for m in modes},
+        "roofline": roof,
+        "cpu_baseline": cb,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,96 @@
+"""Multi-GPU z-slab partition and interface-plane summation.
+
+Elements of a structured nx*ny*nz grid (ez slowest) are split into contiguous
+z-slabs, one per rank (BASELINE.json north_star: "Elements are partitioned as
+contiguous slabs across the 8 GPUs ... Residual mode sums the shared
+interface-plane DOFs with NCCL over NVLink").  Global node numbering is
+z-slowest, so every rank's nodes are one contiguous slice of the global
+vector, including both interface planes.  Matrix mode needs no
+communication; residual mode adds, after the local scatter, the partial sums
+of the two shared node planes with the neighbours (grouped NCCL send/recv of
+contiguous slices; gloo on CPU tensors in the tests).  IEEE addition is
+commutative, so both copies of a shared plane end up bitwise equal.
+
+This module is plumbing only (index bookkeeping and torch.distributed calls);
+all arithmetic of the method runs in libfeb200.so.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+@dataclass
+class Slab:
+    rank: int
+    world: int
+    elem_begin: int       # global element range [elem_begin, elem_end)
+    elem_end: int
+    vert_begin: int       # global vertex range [vert_begin, vert_end)
+    vert_end: int
+    node_begin: int       # global node range [node_begin, node_end)
+    node_end: int
+    plane: int            # nodes per interface plane
+
+    @property
+    def n_elems(self):
+        return self.elem_end - self.elem_begin
+
+    @property
+    def n_nodes(self):
+        return self.node_end - self.node_begin
+
+
+def slab_of(shape, p: int, world: int, rank: int) -> Slab:
+    nx, ny, nz = shape
+    if nz % world != 0:
+        raise ValueError(f"nz={nz} is not divisible by {world} ranks")
+    z0, z1 = nz * rank // world, nz * (rank + 1) // world
+    vplane = (nx + 1) * (ny + 1)
+    plane = (p * nx + 1) * (p * ny + 1)
+    return Slab(rank, world, z0 * nx * ny, z1 * nx * ny, z0 * vplane, (z1 + 1) * vplane,
+                p * z0 * plane, (p * z1 + 1) * plane, plane)
+
+
+def local_arrays(slab: Slab, coords, conn, dof_conn):
+    """Rank-local mesh arrays: vertex/node ids renumbered into the slab's ranges."""
+    e0, e1 = slab.elem_begin, slab.elem_end
+    lc = np.ascontiguousarray(coords[slab.vert_begin:slab.vert_end])
+    lconn = np.ascontiguousarray(conn[e0:e1] - slab.vert_begin).astype(np.int32)
+    ldc = np.ascontiguousarray(dof_conn[e0:e1] - slab.node_begin).astype(np.int32)
+    assert lconn.min() >= 0 and lconn.max() < slab.vert_end - slab.vert_begin
+    assert ldc.min() >= 0 and ldc.max() < slab.n_nodes
+    return lc, lconn, ldc
+
+
+def exchange_planes(r: torch.Tensor, slab: Slab, group=None, bufs=None):
+    """Sum the shared interface planes of the rank-local vector r [n_local][D] in place.
+
+    Rank g sends its first plane to g-1 and its last plane to g+1 and adds what it
+    receives.  Returns the list of receive buffers (reusable via `bufs`)."""
+    if slab.world == 1:
+        return bufs
+    pl = slab.plane
+    D = r.shape[1] if r.dim() > 1 else 1
+    flat = r.view(-1)
+    lo = flat[: pl * D]
+    hi = flat[flat.numel() - pl * D:]
+    if bufs is None:
+        bufs = [torch.empty_like(lo), torch.empty_like(hi)]
+    ops = []
+    if slab.rank > 0:
+        ops.append(dist.P2POp(dist.isend, lo.contiguous(), slab.rank - 1, group))
+        ops.append(dist.P2POp(dist.irecv, bufs[0], slab.rank - 1, group))
+    if slab.rank < slab.world - 1:
+        ops.append(dist.P2POp(dist.isend, hi.contiguous(), slab.rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, bufs[1], slab.rank + 1, group))
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    if slab.rank > 0:
+        lo.add_(bufs[0])
+    if slab.rank < slab.world - 1:
+        hi.add_(bufs[1])
+    return bufs
