@@ -55,6 +55,8 @@ struct MatArgs {
 // (form, order, dtype) combination is not built).
 cudaError_t launch_matrix(const fe_mesh* m, int form, MatArgs mat, const double* state_u,
                           int64_t e0, int64_t e1, double* K, cudaStream_t st);
+cudaError_t launch_matrix_sf(const fe_mesh* m, int form, MatArgs mat, int64_t e0, int64_t e1,
+                             double* K, cudaStream_t st);
 cudaError_t launch_residual_f64(const fe_mesh* m, int form, MatArgs mat, const double* u,
                                 int64_t e0, int64_t e1, double* r_elem, double* r_global,
                                 cudaStream_t st);

@@ -14,6 +14,10 @@
 //                      'cq,cqje,rjI,cqIK,cqlf,slK->cresf' P:1033)
 //         convective   K_ab = sum_q phi^T detw (delta_ab (u.G) + d_b u_a phi)  (Eq. fe4)
 // Output K[e - e0][a*nb + k][b*nb + l] written straight from the MMA fragments.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
 #include "fe_device.cuh"
 #include "fe_internal.h"
 
@@ -256,6 +260,12 @@ static cudaError_t dispatch_form(const fe_mesh* mh, int form, MatArgs mat, const
 cudaError_t launch_matrix(const fe_mesh* mh, int form, MatArgs mat, const double* state_u,
                           int64_t e0, int64_t e1, double* K, cudaStream_t st) {
   if (mh->q1d != mh->order + 1) return cudaErrorNotSupported;
+  // sum-factorised kernels first; FEB200_MATRIX_IMPL=dense selects the dense DMMA kernels
+  const char* impl = std::getenv("FEB200_MATRIX_IMPL");
+  if (!(impl && std::strcmp(impl, "dense") == 0)) {
+    cudaError_t e = launch_matrix_sf(mh, form, mat, e0, e1, K, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
   switch (mh->order) {
     case 1: return dispatch_form<1>(mh, form, mat, state_u, e0, e1, K, st);
     case 2: return dispatch_form<2>(mh, form, mat, state_u, e0, e1, K, st);

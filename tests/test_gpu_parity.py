@@ -50,9 +50,19 @@ RESIDUAL_CASES = [(f, p) for f in (0, 1, 2, 3, 4, 5) for p in (1, 2, 3)] + \
                  [(0, 4), (1, 4), (3, 4), (2, 4), (4, 4), (5, 4)]
 
 
+@pytest.fixture(params=["default", "dense"])
+def matrix_impl(request, monkeypatch):
+    """default = sum-factorised kernels where built; dense = the DMMA dense kernels."""
+    if request.param == "dense":
+        monkeypatch.setenv("FEB200_MATRIX_IMPL", "dense")
+    else:
+        monkeypatch.delenv("FEB200_MATRIX_IMPL", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("form,p", MATRIX_CASES)
 @pytest.mark.parametrize("shape", SHAPES)
-def test_matrix_parity(form, p, shape):
+def test_matrix_parity(form, p, shape, matrix_impl):
     pr = fi.make_problem(form, p, shape, 1000 + 10 * form + p)
     Kref = oracle.problem_matrix(pr)
     mesh = gpu_mesh(pr)
@@ -60,6 +70,9 @@ def test_matrix_parity(form, p, shape):
                               dev(pr.u) if form == fi.CONVECTIVE else None)
     torch.cuda.synchronize()
     assert rel(K.cpu().numpy(), Kref) <= TOL64
+    if form in (fi.DIFFUSION, fi.MASS, fi.MASS_DIFFUSION):
+        Kn = K.cpu().numpy()
+        assert np.abs(Kn - Kn.transpose(0, 2, 1)).max() <= 1e-14 * np.abs(Kn).max()
 
 
 @pytest.mark.parametrize("kind", [fi.MAT_PER_ELEM, fi.MAT_PER_QP, fi.MAT_FULL_D])
