@@ -74,5 +74,7 @@ cudaError_t launch_geometry_materialize(const fe_mesh* m, double* detw, double* 
                                         cudaStream_t st);
 
 void count_launch();
+cudaError_t upload_const_tables(int order, const double* b1, const double* d1, const double* x1,
+                                const double* w1, cudaStream_t st);
 
 }  // namespace feb200

@@ -19,6 +19,9 @@
 // Q2: ~12k FMA per cell instead of ~66k for the dense form; the 5.8 KB K_e
 // write then dominates, so K is staged in shared memory and written with TMA
 // bulk stores (cp.async.bulk) that overlap the next batch.
+#ifndef FEB200_SF_E2
+#define FEB200_SF_E2 2
+#endif
 #include "fe_device.cuh"
 #include "fe_internal.h"
 
@@ -29,23 +32,57 @@ struct SFM {
   static constexpr int N1 = P + 1, Q1 = P + 1, NB = N1 * N1 * N1, NQ = Q1 * Q1 * Q1;
   static constexpr int NUP = (DIFF ? 6 : 0) + (MASS ? 1 : 0);   // unique (m <= n) pairs
   static constexpr int NOP = (DIFF ? 9 : 0) + (MASS ? 1 : 0);   // ordered pairs
-  static constexpr int ZP = N1 * (N1 + 1) / 2, YP = N1 * N1;
-  static constexpr int TPE = ZP * YP;                          // stage-y/x threads per cell
-  static constexpr int E = P == 1 ? 16 : (P == 2 ? 4 : 1);      // cells per CTA iteration
-  static constexpr int T_GEO = E * NQ, T_Z = E * NUP * Q1 * Q1, T_YX = E * TPE;
-  static constexpr int TMAX = T_GEO > T_Z ? (T_GEO > T_YX ? T_GEO : T_YX) : (T_Z > T_YX ? T_Z : T_YX);
-  static constexpr int THREADS = (TMAX + 31) / 32 * 32;
+  static constexpr int YP = N1 * N1, YPS = N1 * (N1 + 1) / 2;
+  // stage-y/x threads per cell: z-pairs iz < jz with every y-pair, and iz == jz
+  // with y-pairs iy <= jy (the rest of K follows by symmetry)
+  static constexpr int TOFF = YP * (N1 * (N1 - 1) / 2);
+  static constexpr int TPE = TOFF + N1 * YPS;
+  static constexpr int E = P == 1 ? 8 : (P == 2 ? FEB200_SF_E2 : 1);  // cells per CTA iteration
+  static constexpr int T_GEO = E * NQ, T_Z = E * NUP * Q1 * Q1, T_YX = E * TPE, T_EDGE = E * 36;
+  static constexpr int M1 = T_GEO > T_Z ? T_GEO : T_Z, M2 = T_YX > T_EDGE ? T_YX : T_EDGE;
+  static constexpr int THREADS = ((M1 > M2 ? M1 : M2) + 31) / 32 * 32;
   // shared memory (doubles)
   static constexpr int KST = E * NB * NB;                       // one staging buffer
+  static constexpr int QQP = (Q1 * Q1 + 1) / 2 * 2;             // (qx,qy) padded for LDS.128
   static constexpr int OFF_K = 0;                               // 2 x KST (16-B aligned)
-  static constexpr int OFF_XV = OFF_K + 2 * KST;
-  static constexpr int OFF_COEF = OFF_XV + E * 24;              // [E][2][NQ] kappa, rho
+  static constexpr int OFF_EDGE = OFF_K + 2 * KST;              // [E][3 dirs][4][3]
+  static constexpr int OFF_COEF = OFF_EDGE + E * 36;            // [E][2][NQ] kappa, rho
   static constexpr int OFF_W = OFF_COEF + E * 2 * NQ;           // [E][NUP][NQ]
-  static constexpr int OFF_T1 = OFF_W + E * NUP * NQ;           // [E][NUP][Q1*Q1][N1*N1]
-  static constexpr int OFF_B = OFF_T1 + E * NUP * Q1 * Q1 * N1 * N1;  // [2][Q1][N1]
-  static constexpr int TOTAL = OFF_B + 2 * Q1 * N1;
+  static constexpr int OFF_T1 = (OFF_W + E * NUP * NQ + 1) / 2 * 2;  // [E][NUP][N1*N1][QQP]
+  static constexpr int OFF_XW = OFF_T1 + E * NUP * N1 * N1 * QQP;  // [2][Q1] 1D points, weights
+  static constexpr int TOTAL = OFF_XW + 2 * Q1;
   static constexpr size_t BYTES = size_t(TOTAL) * 8;
 };
+
+// 1D tables B^a[q][i] per order (a = 0 values, 1 derivatives), uploaded at mesh
+// creation; the values depend only on (p, q1d = p + 1).  Warp-uniform reads
+// become constant-bank operands of the DFMAs.
+__constant__ double c_tab1d[5][2][5][5];
+__constant__ double c_x1d[5][5];   // 1D Gauss points on [0,1]
+__constant__ double c_w1d[5][5];   // 1D Gauss weights
+
+cudaError_t upload_const_tables(int order, const double* b1, const double* d1, const double* x1,
+                                const double* w1, cudaStream_t st) {
+  if (order < 1 || order > 4) return cudaSuccess;
+  double h[2][5][5] = {}, hx[5] = {}, hw[5] = {};
+  const int n1 = order + 1, q1 = order + 1;
+  for (int q = 0; q < q1; ++q) {
+    hx[q] = x1[q];
+    hw[q] = w1[q];
+    for (int i = 0; i < n1; ++i) {
+      h[0][q][i] = b1[q * n1 + i];
+      h[1][q][i] = d1[q * n1 + i];
+    }
+  }
+  cudaError_t e = cudaMemcpyToSymbolAsync(c_tab1d, h, sizeof(h), sizeof(h) * order,
+                                          cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyToSymbolAsync(c_x1d, hx, sizeof(hx), sizeof(hx) * order, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyToSymbolAsync(c_w1d, hw, sizeof(hw), sizeof(hw) * order, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return e;
+}
 
 // unique pair u -> (m, n), m <= n; index 6 is the value-value pair (3,3)
 __device__ __forceinline__ void upair(int u, int& m, int& n) {
@@ -58,6 +95,19 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// edge e (0..11) of a hex: direction d = e / 4, the other two bits k = e % 4;
+// returns the two vertex ids (v = a + 2b + 4c) of the edge.
+__device__ __forceinline__ void hex_edge(int e, int& v0, int& v1) {
+  const int d = e >> 2, k = e & 3;
+  const int lo = k & 1, hi = k >> 1;
+  int a0, b0, c0;
+  if (d == 0) { a0 = 0; b0 = lo; c0 = hi; }
+  else if (d == 1) { a0 = lo; b0 = 0; c0 = hi; }
+  else { a0 = lo; b0 = hi; c0 = 0; }
+  v0 = a0 + 2 * b0 + 4 * c0;
+  v1 = v0 + (1 << d);
+}
+
 template <int P, int FORM>
 __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_DIFFUSION>::THREADS)
     k_matrix_sf(MeshView mv, const double* __restrict__ ma, const double* __restrict__ mb,
@@ -65,115 +115,188 @@ __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_D
   constexpr bool DIFF = FORM != FE_FORM_MASS, MASS = FORM != FE_FORM_DIFFUSION;
   using L = SFM<P, DIFF, MASS>;
   constexpr int N1 = L::N1, Q1 = L::Q1, NB = L::NB, NQ = L::NQ, NUP = L::NUP, E = L::E;
+  constexpr int QQP = L::QQP;
   constexpr int UBASE = DIFF ? 0 : 6;  // first unique-pair id
   extern __shared__ __align__(128) double sm[];
-  double* xv = sm + L::OFF_XV;
+  double* edge = sm + L::OFF_EDGE;
   double* coef = sm + L::OFF_COEF;
   double* W = sm + L::OFF_W;
   double* T1 = sm + L::OFF_T1;
-  double* Bt = sm + L::OFF_B;
   const int tid = threadIdx.x;
 
-  for (int i = tid; i < 2 * Q1 * N1; i += blockDim.x) Bt[i] = (i < Q1 * N1) ? mv.b1[i] : mv.d1[i - Q1 * N1];
-  __syncthreads();
+  // 1D tables B^a[q][i] (a = 0 values, 1 derivatives) from constant memory
+#define Bt(a, q, i) c_tab1d[P][a][q][i]
 
-  // thread-constant stage-y/x data
-  const int yx_el = tid / L::TPE, yx_r = tid - yx_el * L::TPE;
-  const int zp = yx_r / L::YP, yp = yx_r - zp * L::YP;
-  int iz = 0, jz = 0;
+  // ---- thread-constant stage-z task (one per thread)
+  const int z_el = tid / (NUP * Q1 * Q1), z_r = tid - z_el * (NUP * Q1 * Q1);
+  const int z_ul = z_r / (Q1 * Q1), z_qxy = z_r - z_ul * (Q1 * Q1);
+  const int z_qx = z_qxy / Q1, z_qy = z_qxy - z_qx * Q1;
+  double Bza[Q1][N1], Bzb[Q1][N1];
   {
-    int c = zp;
+    int m, n;
+    upair(UBASE + (z_ul < NUP ? z_ul : 0), m, n);
+#pragma unroll
+    for (int q = 0; q < Q1; ++q)
+#pragma unroll
+      for (int i = 0; i < N1; ++i) {
+        Bza[q][i] = m == 2 ? Bt(1, q, i) : Bt(0, q, i);
+        Bzb[q][i] = n == 2 ? Bt(1, q, i) : Bt(0, q, i);
+      }
+  }
+
+  // ---- thread-constant stage-y/x task
+  const int yx_el = tid / L::TPE, yx_r = tid - yx_el * L::TPE;
+  int iz, jz, iy, jy;
+  if (yx_r < L::TOFF) {  // off-diagonal z pair, any y pair
+    int c = yx_r / L::YP;
+    const int yp = yx_r - c * L::YP;
+    iy = yp / N1;
+    jy = yp - iy * N1;
+    iz = 0;
+    jz = 1;
     for (int a = 0; a < N1; ++a) {
-      if (c < N1 - a) { iz = a; jz = a + c; break; }
+      if (c < N1 - 1 - a) { iz = a; jz = a + 1 + c; break; }
+      c -= N1 - 1 - a;
+    }
+  } else {               // diagonal z pair, y pairs iy <= jy
+    const int r = yx_r - L::TOFF;
+    iz = jz = r / L::YPS;
+    int c = r - iz * L::YPS;
+    iy = 0;
+    jy = 0;
+    for (int a = 0; a < N1; ++a) {
+      if (c < N1 - a) { iy = a; jy = a + c; break; }
       c -= N1 - a;
     }
   }
-  const int iy = yp / N1, jy = yp - iy * N1;
+  const bool mirror = (iz < jz) || (iy < jy);
   double Byp[4][Q1];  // Byp[ay*2+by][qy] = B^ay[qy][iy] B^by[qy][jy]
-  double Bx[2][Q1][N1];
 #pragma unroll
-  for (int q = 0; q < Q1; ++q) {
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) Byp[a * 2 + b][q] = Bt[(a * Q1 + q) * N1 + iy] * Bt[(b * Q1 + q) * N1 + jy];
+  for (int q = 0; q < Q1; ++q)
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int i = 0; i < N1; ++i) Bx[a][q][i] = Bt[(a * Q1 + q) * N1 + i];
-  }
+      for (int b = 0; b < 2; ++b) Byp[a * 2 + b][q] = Bt(a, q, iy) * Bt(b, q, jy);
 
+  // ---- software pipeline of the global reads: conn two batches ahead,
+  // edge vectors and coefficients one batch ahead, held in registers.
   const int64_t nloc = e1 - e0;
   const int64_t nbatch = (nloc + E - 1) / E;
+  static_assert(E * 36 <= L::THREADS && E * NQ <= L::THREADS, "one prefetch slot per thread");
+  const int pe_el = tid / 36, pe_r = tid - pe_el * 36;       // edge slot: edge pe_r/3, comp pe_r%3
+  int pe_v0, pe_v1;
+  hex_edge(pe_r / 3, pe_v0, pe_v1);
+  const int pe_c = pe_r % 3;
+  const int pk_el = tid / NQ, pk_q = tid - pk_el * NQ;       // coefficient slot
+  const bool pe_on = tid < E * 36, pk_on = tid < E * NQ;
+  auto ld_conn2 = [&](int64_t b, int& c0, int& c1) {
+    const int64_t le = b * E + pe_el;
+    if (pe_on && b < nbatch && le < nloc) {
+      const int32_t* cn = mv.conn + 8 * (e0 + le);
+      c0 = cn[pe_v0];
+      c1 = cn[pe_v1];
+    } else {
+      c0 = c1 = -1;
+    }
+  };
+  auto ld_edge = [&](int c0, int c1) -> double {
+    return c0 >= 0 ? mv.coords[3 * (int64_t)c1 + pe_c] - mv.coords[3 * (int64_t)c0 + pe_c] : 0.0;
+  };
+  auto ld_k = [&](int64_t b, double& kap, double& rho) {
+    kap = rho = 0.0;
+    const int64_t le = b * E + pk_el;
+    if (pk_on && b < nbatch && le < nloc) {
+      const int64_t g = (e0 + le) * NQ + pk_q;
+      if constexpr (FORM == FE_FORM_DIFFUSION) kap = ma[g];
+      if constexpr (FORM == FE_FORM_MASS) rho = ma[g];
+      if constexpr (FORM == FE_FORM_MASS_DIFFUSION) { rho = ma[g]; kap = mb[g]; }
+    }
+  };
+  int cn0, cn1;
+  ld_conn2(blockIdx.x, cn0, cn1);
+  double edge_cur = ld_edge(cn0, cn1), k_cur, r_cur;
+  ld_k(blockIdx.x, k_cur, r_cur);
+  ld_conn2(blockIdx.x + gridDim.x, cn0, cn1);
+
   int it = 0;
   for (int64_t bidx = blockIdx.x; bidx < nbatch; bidx += gridDim.x, ++it) {
     const int64_t lb = bidx * E;                 // local index of the first cell
     const int ne = (int)((nloc - lb) < E ? (nloc - lb) : E);
     double* Kst = sm + L::OFF_K + (it & 1) * L::KST;
-    // A. cell data: vertices and per-qp coefficients
-    for (int i = tid; i < E * 24; i += blockDim.x) {
-      const int el = i / 24, r = i - el * 24;
-      xv[i] = el < ne ? mv.coords[3 * (int64_t)mv.conn[8 * (e0 + lb + el) + r / 3] + r % 3] : 0.0;
+    // A. this batch's data from the prefetch registers; issue the next reads
+    if (pe_on) edge[tid] = edge_cur;
+    if (pk_on) {
+      coef[(pk_el * 2) * NQ + pk_q] = k_cur;
+      coef[(pk_el * 2 + 1) * NQ + pk_q] = r_cur;
     }
-    for (int i = tid; i < E * NQ; i += blockDim.x) {
-      const int el = i / NQ, q = i - el * NQ;
-      const int64_t g = (e0 + lb + el) * NQ + q;
-      double kap = 0.0, rho = 0.0;
-      if (el < ne) {
-        if constexpr (FORM == FE_FORM_DIFFUSION) kap = ma[g];
-        if constexpr (FORM == FE_FORM_MASS) rho = ma[g];
-        if constexpr (FORM == FE_FORM_MASS_DIFFUSION) { rho = ma[g]; kap = mb[g]; }
-      }
-      coef[(el * 2) * NQ + q] = kap;
-      coef[(el * 2 + 1) * NQ + q] = rho;
-    }
+    edge_cur = ld_edge(cn0, cn1);
+    ld_k(bidx + gridDim.x, k_cur, r_cur);
+    ld_conn2(bidx + 2 * (int64_t)gridDim.x, cn0, cn1);
     // the TMA store issued two batches ago read this staging buffer: wait for it
     if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
     __syncthreads();
-    // B. geometry -> W^{mn}[q]
-    for (int i = tid; i < E * NQ; i += blockDim.x) {
-      const int el = i / NQ, q = i - el * NQ;
-      double Ji[9];
-      const double det = hex_geometry(xv + 24 * el, mv.xi[3 * q], mv.xi[3 * q + 1], mv.xi[3 * q + 2], Ji);
-      const double dw = det * mv.w[q];
+    // B. geometry from the 12 edge vectors -> W^{mn}[q]
+    if (tid < E * NQ) {
+      const int el = tid / NQ, q = tid - el * NQ;
+      const double t0 = mv.xi[3 * q], t1 = mv.xi[3 * q + 1], t2 = mv.xi[3 * q + 2];
+      const double* ed = edge + el * 36;
+      // J[:,d] = sum_k w_k e_d[k], bilinear weights of the two other coordinates
+      double J[3][3];
+      const double wA[4] = {(1 - t1) * (1 - t2), t1 * (1 - t2), (1 - t1) * t2, t1 * t2};
+      const double wB[4] = {(1 - t0) * (1 - t2), t0 * (1 - t2), (1 - t0) * t2, t0 * t2};
+      const double wC[4] = {(1 - t0) * (1 - t1), t0 * (1 - t1), (1 - t0) * t1, t0 * t1};
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        J[i][0] = wA[0] * ed[0 * 3 + i] + wA[1] * ed[1 * 3 + i] + wA[2] * ed[2 * 3 + i] + wA[3] * ed[3 * 3 + i];
+        J[i][1] = wB[0] * ed[4 * 3 + i] + wB[1] * ed[5 * 3 + i] + wB[2] * ed[6 * 3 + i] + wB[3] * ed[7 * 3 + i];
+        J[i][2] = wC[0] * ed[8 * 3 + i] + wC[1] * ed[9 * 3 + i] + wC[2] * ed[10 * 3 + i] + wC[3] * ed[11 * 3 + i];
+      }
+      // cofactors; J^-1[m][k] = cof[k][m] / det
+      const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+      const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+      const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+      const double c10 = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+      const double c11 = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+      const double c12 = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+      const double c20 = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+      const double c21 = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+      const double c22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+      const double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+      const double wq = mv.w[q];
       double* Wel = W + el * NUP * NQ;
       if constexpr (DIFF) {
-        const double s = dw * coef[(el * 2) * NQ + q];
+        // W^{mn} = detw kappa sum_k Jinv[m][k] Jinv[n][k] = w kappa / det * sum_k cof[k][m] cof[k][n]
+        const double s = wq * coef[(el * 2) * NQ + q] / det;
+        const double C[3][3] = {{c00, c01, c02}, {c10, c11, c12}, {c20, c21, c22}};
 #pragma unroll
         for (int u = 0; u < 6; ++u) {
           int m, n;
           upair(u, m, n);
-          Wel[u * NQ + q] = s * (Ji[3 * m] * Ji[3 * n] + Ji[3 * m + 1] * Ji[3 * n + 1] + Ji[3 * m + 2] * Ji[3 * n + 2]);
+          Wel[u * NQ + q] = s * (C[0][m] * C[0][n] + C[1][m] * C[1][n] + C[2][m] * C[2][n]);
         }
       }
-      if constexpr (MASS) Wel[(NUP - 1) * NQ + q] = dw * coef[(el * 2 + 1) * NQ + q];
+      if constexpr (MASS) Wel[(NUP - 1) * NQ + q] = wq * det * coef[(el * 2 + 1) * NQ + q];
     }
     __syncthreads();
-    // C. stage z
-    for (int i = tid; i < L::T_Z; i += blockDim.x) {
-      const int el = i / (NUP * Q1 * Q1), r = i - el * NUP * Q1 * Q1;
-      const int ul = r / (Q1 * Q1), qxy = r - ul * Q1 * Q1;  // qxy = qx * Q1 + qy
-      const int qx = qxy / Q1, qy = qxy - qx * Q1;
-      int m, n;
-      upair(UBASE + ul, m, n);
-      const int az = m == 2, bz = n == 2;
-      const double* w = W + (el * NUP + ul) * NQ + qx + Q1 * qy;
+    // C. stage z: T1^{u}[iz,jz][qx,qy] = sum_qz B^{mz}[qz][iz] B^{nz}[qz][jz] W^u[qx,qy,qz]
+    if (tid < L::T_Z) {
+      const double* w = W + (z_el * NUP + z_ul) * NQ + z_qx + Q1 * z_qy;
       double t[Q1][N1];
 #pragma unroll
       for (int qz = 0; qz < Q1; ++qz) {
         const double c = w[Q1 * Q1 * qz];
 #pragma unroll
-        for (int a = 0; a < N1; ++a) t[qz][a] = c * Bt[(az * Q1 + qz) * N1 + a];
+        for (int a = 0; a < N1; ++a) t[qz][a] = c * Bza[qz][a];
       }
-      double* out = T1 + ((el * NUP + ul) * Q1 * Q1 + qxy) * N1 * N1;
+      double* out = T1 + (z_el * NUP + z_ul) * N1 * N1 * QQP + z_qxy;
 #pragma unroll
       for (int a = 0; a < N1; ++a)
 #pragma unroll
         for (int b = 0; b < N1; ++b) {
           double s = 0.0;
 #pragma unroll
-          for (int qz = 0; qz < Q1; ++qz) s = fma(t[qz][a], Bt[(bz * Q1 + qz) * N1 + b], s);
-          out[a * N1 + b] = s;
+          for (int qz = 0; qz < Q1; ++qz) s = fma(t[qz][a], Bzb[qz][b], s);
+          out[(a * N1 + b) * QQP] = s;
         }
     }
     __syncthreads();
@@ -184,7 +307,7 @@ __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_D
       for (int c = 0; c < 4; ++c)
 #pragma unroll
         for (int q = 0; q < Q1; ++q) S[c][q] = 0.0;
-      const double* T1e = T1 + yx_el * NUP * Q1 * Q1 * N1 * N1;
+      const double* T1e = T1 + yx_el * NUP * N1 * N1 * QQP;
 #pragma unroll
       for (int op = 0; op < L::NOP; ++op) {
         int m, n;
@@ -193,12 +316,19 @@ __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_D
         const int ul = (mm == 3) ? NUP - 1 : (mm == 0 ? nn : (mm == 1 ? 2 + nn : 5));
         const int zidx = (m > n) ? (jz * N1 + iz) : (iz * N1 + jz);
         const int ay = m == 1, by = n == 1, cls = (m == 0) * 2 + (n == 0);
-        const double* src = T1e + ul * Q1 * Q1 * N1 * N1 + zidx;
+        const double2* src = reinterpret_cast<const double2*>(T1e + (ul * N1 * N1 + zidx) * QQP);
+        double tv[QQP];
+#pragma unroll
+        for (int h = 0; h < QQP / 2; ++h) {
+          const double2 v = src[h];
+          tv[2 * h] = v.x;
+          tv[2 * h + 1] = v.y;
+        }
 #pragma unroll
         for (int qx = 0; qx < Q1; ++qx)
 #pragma unroll
           for (int qy = 0; qy < Q1; ++qy)
-            S[cls][qx] = fma(Byp[ay * 2 + by][qy], src[(qx * Q1 + qy) * N1 * N1], S[cls][qx]);
+            S[cls][qx] = fma(Byp[ay * 2 + by][qy], tv[qx * Q1 + qy], S[cls][qx]);
       }
       double acc[N1][N1];
 #pragma unroll
@@ -211,11 +341,11 @@ __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_D
         for (int ax = 0; ax < 2; ++ax) {
           double u[N1];
 #pragma unroll
-          for (int b = 0; b < N1; ++b) u[b] = Bx[0][qx][b] * S[ax * 2 + 0][qx] + Bx[1][qx][b] * S[ax * 2 + 1][qx];
+          for (int b = 0; b < N1; ++b) u[b] = Bt(0, qx, b) * S[ax * 2 + 0][qx] + Bt(1, qx, b) * S[ax * 2 + 1][qx];
 #pragma unroll
           for (int a = 0; a < N1; ++a)
 #pragma unroll
-            for (int b = 0; b < N1; ++b) acc[a][b] = fma(Bx[ax][qx][a], u[b], acc[a][b]);
+            for (int b = 0; b < N1; ++b) acc[a][b] = fma(Bt(ax, qx, a), u[b], acc[a][b]);
         }
       double* Ke = Kst + yx_el * NB * NB;
       const int ib = N1 * (iy + N1 * iz), jb = N1 * (jy + N1 * jz);
@@ -224,7 +354,7 @@ __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_D
 #pragma unroll
         for (int b = 0; b < N1; ++b) {
           Ke[(ib + a) * NB + jb + b] = acc[a][b];
-          if (iz < jz) Ke[(jb + b) * NB + ib + a] = acc[a][b];
+          if (mirror) Ke[(jb + b) * NB + ib + a] = acc[a][b];
         }
     }
     // E. write the batch: one TMA bulk store of ne * NB^2 doubles (contiguous in K)
@@ -244,6 +374,7 @@ __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_D
     }
   }
   if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#undef Bt
 }
 
 template <int P, int FORM>
