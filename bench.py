@@ -56,6 +56,25 @@ def alg_flops(form: int, mode: str, nb: int, nq: int) -> float:
     return (per_qp + GEOM) * nq
 
 
+def sf_matrix_flops(form: int, p: int) -> float:
+    """Flops per cell of the sum-factorised matrix kernel (k_matrix_sf.cu), FMA = 2."""
+    n1 = q1 = p + 1
+    nq = q1 ** 3
+    nup = (6 if form != fi.MASS else 0) + (1 if form != fi.DIFFUSION else 0)
+    nop = (9 if form != fi.MASS else 0) + (1 if form != fi.DIFFUSION else 0)
+    tpe = n1 * n1 * (n1 * (n1 - 1) // 2) + n1 * (n1 * (n1 + 1) // 2)
+    geo = (GEOM + 32) * nq
+    z = nup * q1 * q1 * (q1 * n1 + 2 * n1 * n1 * q1)
+    y = 2 * tpe * nop * q1 * q1
+    x = tpe * q1 * 2 * (3 * n1 + 2 * n1 * n1)
+    return geo + z + y + x
+
+
+def uses_sf_matrix(form: int, p: int) -> bool:
+    return (form in (fi.DIFFUSION, fi.MASS, fi.MASS_DIFFUSION) and p <= 3
+            and os.environ.get("FEB200_MATRIX_IMPL", "") != "dense")
+
+
 def alg_bytes(form: int, mode: str, p: int, nb: int, nq: int, D: int, mat_kind: int,
               esize: int = 8) -> float:
     if form == fi.ELASTICITY:
@@ -79,11 +98,12 @@ def alg_bytes(form: int, mode: str, p: int, nb: int, nq: int, D: int, mat_kind: 
 FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
 
 
-def fp64_peak_tflops():
-    """Measured FP64 DMMA peak (tools/fp64_peak.cu; MEASURED_PEAKS.json has no FP64 entry)."""
+def fp64_peak_tflops(key="dmma_m16n8k4_tflops_sustained"):
+    """Measured FP64 peak (tools/fp64_peak.cu, profiles/fp64_peak_r01.json): DMMA for the
+    tensor-core kernels, DFMA for the CUDA-core kernels.  MEASURED_PEAKS.json has no FP64 entry."""
     try:
         d = json.load(open(FP64_PEAK_FILE))
-        return float(d["dmma_m16n8k4_tflops_sustained"]), "measured: tools/fp64_peak (DMMA, 4 s sustained)"
+        return float(d[key]), f"measured: tools/fp64_peak {key} (4 s sustained, 1965 MHz)"
     except Exception:
         return 37.2, "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"
 
@@ -406,23 +426,31 @@ def main():
     # ---- roofline of the dominant kernel
     dom = max(modes, key=lambda m: kern_ms[m])
     esize = 8 if args.dtype == "f64" else 4
-    fl = alg_flops(prob.form, dom, nb, nq) * El
+    fl_lean = alg_flops(prob.form, dom, nb, nq) * El
+    impl = "sum-factorised" if (dom == "matrix" and uses_sf_matrix(prob.form, prob.p)) else "dense-table"
+    fl = sf_matrix_flops(prob.form, prob.p) * El if impl == "sum-factorised" else fl_lean
     by = alg_bytes(prob.form, dom, prob.p, nb, nq, D, prob.mat_kind, esize) * El
     t_s = kern_ms[dom] * 1e-3
-    pk_f, src_f = fp64_peak_tflops()
     pk_b, src_b = hbm_peak_gbs()
     if args.dtype == "f32":
-        pk_f, src_f = 2 * pk_f * 2, "derived: FP32 FFMA = 4x the measured FP64 DMMA rate (128 vs 64 lanes, x2 for FP64 pipe share)"
+        pk_f, src_f, fbound = 74.4, "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz", "alu"
+    elif impl == "sum-factorised":
+        pk_f, src_f = fp64_peak_tflops("dfma_tflops_sustained")
+        fbound = "alu"
+    else:
+        pk_f, src_f = fp64_peak_tflops("dmma_m16n8k4_tflops_sustained")
+        fbound = "tensor"
     t_flop = fl / (pk_f * 1e12)
     t_mem = by / (pk_b * 1e9)
     if t_flop >= t_mem:
-        roof = {"bound": "tensor" if args.dtype == "f64" else "alu",
-                "achieved": fl / t_s / 1e12, "peak": pk_f, "unit": "TFLOP/s",
+        roof = {"bound": fbound, "achieved": fl / t_s / 1e12, "peak": pk_f, "unit": "TFLOP/s",
                 "frac": (fl / t_s / 1e12) / pk_f, "peak_source": src_f}
     else:
         roof = {"bound": "hbm", "achieved": by / t_s / 1e9, "peak": pk_b, "unit": "GB/s",
                 "frac": (by / t_s / 1e9) / pk_b, "peak_source": src_b}
-    roof.update({"kernel": f"{dom} ({fi.FORM_NAMES[prob.form]}, Q{prob.p})",
+    roof.update({"kernel": f"{dom} ({fi.FORM_NAMES[prob.form]}, Q{prob.p}, {impl})",
+                 "lean_dense_flops_per_cell": fl_lean / El,
+                 "effective_lean_tflops": fl_lean / t_s / 1e12,
                  "kernel_ms": kern_ms[dom], "alg_flops_per_cell": fl / El,
                  "alg_bytes_per_cell": by / El, "cells_per_launch": El,
                  "achieved_gbs": by / t_s / 1e9, "achieved_tflops": fl / t_s / 1e12,

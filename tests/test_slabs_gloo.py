@@ -1,0 +1,93 @@
+"""Multi-rank z-slab path on CPU (gloo, world_size 2 and 4): partition bookkeeping and the
+interface-plane summation of paper_2107_04121_b200.slabs.
+
+The per-rank element residuals come from the oracle here (CPU test infrastructure stands in
+for the kernel); what is tested is the product's plumbing: local renumbering, the contiguous
+node slices and the NCCL/gloo exchange of the shared planes.  After the exchange every rank's
+slice must equal the single-process assembled vector restricted to its node range.
+"""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import fe_inputs as fi
+import oracle
+from paper_2107_04121_b200 import slabs
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+CASES = {"diff_q2": (fi.DIFFUSION, 2, (3, 2, 4)), "elas_q2": (fi.ELASTICITY, 2, (2, 3, 4)),
+         "conv_q1": (fi.CONVECTIVE, 1, (3, 3, 4)), "md_q4": (fi.MASS_DIFFUSION, 4, (2, 2, 4))}
+
+
+def _worker(rank, world, port, case, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    form, p, shape = CASES[case]
+    pr = fi.make_problem(form, p, shape, 4242)
+    sl = slabs.slab_of(shape, p, world, rank)
+    lc, lconn, ldc = slabs.local_arrays(sl, pr.coords, pr.conn, pr.dof_conn)
+    e0, e1 = sl.elem_begin, sl.elem_end
+    ma = None if pr.mat_a is None else pr.mat_a[e0:e1]
+    mb = None if pr.mat_b is None else pr.mat_b[e0:e1]
+    u_loc = pr.u[sl.node_begin:sl.node_end]
+    r_el = oracle.eval_residual(form, p, p + 1, lc, lconn, ldc, u_loc, pr.mat_kind, ma, mb)
+    R = oracle.assemble(r_el, ldc, sl.n_nodes, pr.ncomp).reshape(sl.n_nodes, pr.ncomp)
+    Rt = torch.from_numpy(R.copy())
+    slabs.exchange_planes(Rt, sl)
+    out[rank] = (sl.node_begin, sl.node_end, Rt.numpy().copy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_slab_exchange_matches_global(world, case):
+    form, p, shape = CASES[case]
+    pr = fi.make_problem(form, p, shape, 4242)
+    Rg = oracle.problem_assembled_residual(pr).reshape(pr.n_nodes, pr.ncomp)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), case, out), nprocs=world, join=True)
+    covered = np.zeros(pr.n_nodes, dtype=bool)
+    for rank in range(world):
+        a, b, R = out[rank]
+        np.testing.assert_allclose(R, Rg[a:b], rtol=1e-13, atol=1e-15 * np.abs(Rg).max())
+        covered[a:b] = True
+    assert covered.all()
+    # shared planes are bitwise equal on both neighbours
+    for rank in range(world - 1):
+        a0, b0, R0 = out[rank]
+        a1, b1, R1 = out[rank + 1]
+        assert b0 - a1 == slabs.slab_of(shape, p, world, rank).plane
+        assert np.array_equal(R0[a1 - a0:], R1[: b0 - a1])
+
+
+def test_slab_bookkeeping():
+    shape, p = (4, 3, 8), 2
+    pr = fi.make_problem(fi.DIFFUSION, p, shape, 1)
+    for world in (1, 2, 4, 8):
+        elems = []
+        for r in range(world):
+            sl = slabs.slab_of(shape, p, world, r)
+            lc, lconn, ldc = slabs.local_arrays(sl, pr.coords, pr.conn, pr.dof_conn)
+            np.testing.assert_array_equal(lc[lconn], pr.coords[pr.conn[sl.elem_begin:sl.elem_end]])
+            np.testing.assert_array_equal(ldc + sl.node_begin, pr.dof_conn[sl.elem_begin:sl.elem_end])
+            elems.append((sl.elem_begin, sl.elem_end))
+        assert elems[0][0] == 0 and elems[-1][1] == pr.n_elems
+        assert all(a[1] == b[0] for a, b in zip(elems[:-1], elems[1:]))
+    with pytest.raises(ValueError):
+        slabs.slab_of((4, 4, 6), 2, 4, 0)
