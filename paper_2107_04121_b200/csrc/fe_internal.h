@@ -57,6 +57,9 @@ cudaError_t launch_matrix(const fe_mesh* m, int form, MatArgs mat, const double*
                           int64_t e0, int64_t e1, double* K, cudaStream_t st);
 cudaError_t launch_matrix_sf(const fe_mesh* m, int form, MatArgs mat, int64_t e0, int64_t e1,
                              double* K, cudaStream_t st);
+template <typename T>
+cudaError_t launch_residual_sf(const fe_mesh* m, int form, MatArgs mat, const T* u, int64_t e0,
+                               int64_t e1, T* r_elem, T* r_global, cudaStream_t st);
 cudaError_t launch_residual_f64(const fe_mesh* m, int form, MatArgs mat, const double* u,
                                 int64_t e0, int64_t e1, double* r_elem, double* r_global,
                                 cudaStream_t st);
@@ -74,7 +77,9 @@ cudaError_t launch_geometry_materialize(const fe_mesh* m, double* detw, double* 
                                         cudaStream_t st);
 
 void count_launch();
-cudaError_t upload_const_tables(int order, const double* b1, const double* d1, const double* x1,
-                                const double* w1, cudaStream_t st);
+cudaError_t upload_const_tables_matrix(int order, const double* b1, const double* d1,
+                                      const double* x1, const double* w1, cudaStream_t st);
+cudaError_t upload_const_tables_residual(int order, const double* b1, const double* d1,
+                                        const double* x1, const double* w1, cudaStream_t st);
 
 }  // namespace feb200

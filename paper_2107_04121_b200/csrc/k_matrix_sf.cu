@@ -22,6 +22,7 @@
 #ifndef FEB200_SF_E2
 #define FEB200_SF_E2 2
 #endif
+#include "fe_const.cuh"
 #include "fe_device.cuh"
 #include "fe_internal.h"
 
@@ -54,34 +55,9 @@ struct SFM {
   static constexpr size_t BYTES = size_t(TOTAL) * 8;
 };
 
-// 1D tables B^a[q][i] per order (a = 0 values, 1 derivatives), uploaded at mesh
-// creation; the values depend only on (p, q1d = p + 1).  Warp-uniform reads
-// become constant-bank operands of the DFMAs.
-__constant__ double c_tab1d[5][2][5][5];
-__constant__ double c_x1d[5][5];   // 1D Gauss points on [0,1]
-__constant__ double c_w1d[5][5];   // 1D Gauss weights
-
-cudaError_t upload_const_tables(int order, const double* b1, const double* d1, const double* x1,
-                                const double* w1, cudaStream_t st) {
-  if (order < 1 || order > 4) return cudaSuccess;
-  double h[2][5][5] = {}, hx[5] = {}, hw[5] = {};
-  const int n1 = order + 1, q1 = order + 1;
-  for (int q = 0; q < q1; ++q) {
-    hx[q] = x1[q];
-    hw[q] = w1[q];
-    for (int i = 0; i < n1; ++i) {
-      h[0][q][i] = b1[q * n1 + i];
-      h[1][q][i] = d1[q * n1 + i];
-    }
-  }
-  cudaError_t e = cudaMemcpyToSymbolAsync(c_tab1d, h, sizeof(h), sizeof(h) * order,
-                                          cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess)
-    e = cudaMemcpyToSymbolAsync(c_x1d, hx, sizeof(hx), sizeof(hx) * order, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess)
-    e = cudaMemcpyToSymbolAsync(c_w1d, hw, sizeof(hw), sizeof(hw) * order, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  return e;
+cudaError_t upload_const_tables_matrix(int order, const double* b1, const double* d1,
+                                      const double* x1, const double* w1, cudaStream_t st) {
+  return upload_tables_this_tu(order, b1, d1, x1, w1, st);
 }
 
 // unique pair u -> (m, n), m <= n; index 6 is the value-value pair (3,3)

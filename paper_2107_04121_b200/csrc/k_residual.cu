@@ -16,8 +16,11 @@
 // fp64 GEMMs run on the FP64 tensor cores (DMMA); the fp32 variant uses FFMA
 // with geometry still computed from the fp64 coordinates.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "fe_device.cuh"
+#include "fe_flux.cuh"
 #include "fe_internal.h"
 
 namespace feb200 {
@@ -113,57 +116,7 @@ __global__ void __launch_bounds__(256) k_residual(MeshView m, int mat_kind, cons
 #pragma unroll
         for (int j = 0; j < 3; ++j) gu[a][j] = gr[a][0] * Ji[j] + gr[a][1] * Ji[3 + j] + gr[a][2] * Ji[6 + j];
       double f0[D], f1[D][3];
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        f0[a] = 0.0;
-        f1[a][0] = f1[a][1] = f1[a][2] = 0.0;
-      }
-      if constexpr (FORM == FE_FORM_DIFFUSION) {
-        const double kap = (double)ma[e * NQ + q];
-        f1[0][0] = kap * gu[0][0]; f1[0][1] = kap * gu[0][1]; f1[0][2] = kap * gu[0][2];
-      } else if constexpr (FORM == FE_FORM_MASS || FORM == FE_FORM_VECTOR_MASS) {
-        const double rho = (double)ma[e * NQ + q];
-#pragma unroll
-        for (int a = 0; a < D; ++a) f0[a] = rho * uq[a];
-      } else if constexpr (FORM == FE_FORM_MASS_DIFFUSION) {
-        const double rho = (double)ma[e * NQ + q], kap = (double)mb[e * NQ + q];
-        f0[0] = rho * uq[0];
-        f1[0][0] = kap * gu[0][0]; f1[0][1] = kap * gu[0][1]; f1[0][2] = kap * gu[0][2];
-      } else if constexpr (FORM == FE_FORM_ELASTICITY) {
-        // engineering strain (xx, yy, zz, xy, xz, yz)
-        const double eps[6] = {gu[0][0], gu[1 % D][1], gu[2 % D][2], gu[0][1] + gu[1 % D][0],
-                               gu[0][2] + gu[2 % D][0], gu[1 % D][2] + gu[2 % D][1]};
-        double sig[6];
-        if (mat_kind == FE_MAT_FULL_D) {
-          const T* Dm = ma + (e * NQ + q) * 36;
-#pragma unroll
-          for (int I = 0; I < 6; ++I) {
-            double s = 0.0;
-#pragma unroll
-            for (int K = 0; K < 6; ++K) s += (double)Dm[6 * I + K] * eps[K];
-            sig[I] = s;
-          }
-        } else {
-          const double lam = mat_kind == FE_MAT_PER_ELEM ? (double)ma[e] : (double)ma[e * NQ + q];
-          const double mu = mat_kind == FE_MAT_PER_ELEM ? (double)mb[e] : (double)mb[e * NQ + q];
-          const double tr = eps[0] + eps[1] + eps[2];
-          sig[0] = lam * tr + 2.0 * mu * eps[0];
-          sig[1] = lam * tr + 2.0 * mu * eps[1];
-          sig[2] = lam * tr + 2.0 * mu * eps[2];
-          sig[3] = mu * eps[3];
-          sig[4] = mu * eps[4];
-          sig[5] = mu * eps[5];
-        }
-        // f1[a][j] = sum_I Psg[a][j][I] sig_I  (symmetric stress tensor)
-        const double st[3][3] = {{sig[0], sig[3], sig[4]}, {sig[3], sig[1], sig[5]}, {sig[4], sig[5], sig[2]}};
-#pragma unroll
-        for (int a = 0; a < D; ++a)
-#pragma unroll
-          for (int j = 0; j < 3; ++j) f1[a][j] = st[a][j];
-      } else {  // CONVECTIVE
-#pragma unroll
-        for (int a = 0; a < D; ++a) f0[a] = gu[a][0] * uq[0] + gu[a][1] * uq[1 % D] + gu[a][2] * uq[2 % D];
-      }
+      qp_flux<FORM, T>(uq, gu, e, q, NQ, mat_kind, ma, mb, f0, f1);
 #pragma unroll
       for (int a = 0; a < D; ++a) {
         V[(4 * q) * NCOL + el * D + a] = (T)(dw * f0[a]);
@@ -252,15 +205,29 @@ static cudaError_t res_dispatch(const fe_mesh* mh, int form, MatArgs mat, const 
   return cudaErrorNotSupported;
 }
 
+// sum-factorised kernels first; FEB200_RESIDUAL_IMPL=dense selects the dense DMMA kernels
+static bool want_dense_residual() {
+  const char* impl = std::getenv("FEB200_RESIDUAL_IMPL");
+  return impl && std::strcmp(impl, "dense") == 0;
+}
+
 cudaError_t launch_residual_f64(const fe_mesh* m, int form, MatArgs mat, const double* u,
                                 int64_t e0, int64_t e1, double* r_elem, double* r_global,
                                 cudaStream_t st) {
+  if (!want_dense_residual()) {
+    cudaError_t e = launch_residual_sf<double>(m, form, mat, u, e0, e1, r_elem, r_global, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
   return res_dispatch<double>(m, form, mat, u, e0, e1, r_elem, r_global, st);
 }
 
 cudaError_t launch_residual_f32(const fe_mesh* m, int form, MatArgs mat, const float* u,
                                 int64_t e0, int64_t e1, float* r_elem, float* r_global,
                                 cudaStream_t st) {
+  if (!want_dense_residual()) {
+    cudaError_t e = launch_residual_sf<float>(m, form, mat, u, e0, e1, r_elem, r_global, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
   return res_dispatch<float>(m, form, mat, u, e0, e1, r_elem, r_global, st);
 }
 

@@ -1,0 +1,390 @@
+// Sum-factorised residual mode (Alg. 1) with
+// the gather of the cell DOFs and the fused scatter-add.
+//
+// Same integral as k_residual.cu, with the dense stacked table T = [Phi; grad Phi]
+// replaced by its tensor-product factors (Eq. fe1):
+//   Phi_k(q) = B0[qx][kx] B0[qy][ky] B0[qz][kz],  d Phi_k/d xi_x = B1[qx][kx] B0 B0, ...
+// so interpolation and testing are sequences of 1D contractions of length p+1.
+// One thread per (x, y) column of a cell holds its z-column in registers:
+//   gather  -> stage x (smem exchange) -> stage y (smem exchange) -> stage z (registers)
+//   -> per-qp geometry (edge vectors) + flux (fe_flux.cuh), pulled back to reference
+//   -> z^T (registers) -> y^T (smem) -> x^T (smem) -> fused atomic scatter.
+// Q2: ~1.5k FMA per cell and component for the contractions instead of ~4.4k
+// (dense); Q4: ~11k instead of ~125k.
+#include "fe_const.cuh"
+#include "fe_device.cuh"
+#include "fe_flux.cuh"
+#include "fe_internal.h"
+
+namespace feb200 {
+
+cudaError_t upload_const_tables_residual(int order, const double* b1, const double* d1,
+                                        const double* x1, const double* w1, cudaStream_t st) {
+  return upload_tables_this_tu(order, b1, d1, x1, w1, st);
+}
+
+template <int P, int FORM, typename T>
+struct RSF {
+  static constexpr int N1 = P + 1, Q1 = P + 1, NB = N1 * N1 * N1, NQ = Q1 * Q1 * Q1;
+  static constexpr int D = FormD<FORM>::D;
+  static constexpr int TPE = Q1 * Q1;  // threads per cell
+  static constexpr int EB0 = P == 1 ? 32 : (P == 2 ? 28 : (P == 3 ? 16 : 10));
+  static constexpr int EB = (D == 3 && P >= 3) ? EB0 / 2 : EB0;  // cells per CTA iteration
+  static constexpr int THREADS = (EB * TPE + 31) / 32 * 32;
+  static constexpr int XS = 3 * D * NQ;  // exchange buffer per cell (elements of T)
+  static constexpr size_t BYTES = size_t(EB) * 36 * 8 + 2 * Q1 * N1 * 8 + size_t(EB) * XS * sizeof(T);
+  static constexpr bool VAL = FORM == FE_FORM_MASS || FORM == FE_FORM_VECTOR_MASS ||
+                              FORM == FE_FORM_MASS_DIFFUSION || FORM == FE_FORM_CONVECTIVE;
+  static constexpr bool GRAD = FORM != FE_FORM_MASS && FORM != FE_FORM_VECTOR_MASS;
+};
+
+template <int P, int FORM, typename T>
+__global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
+    k_residual_sf(MeshView mv, int mat_kind, const T* __restrict__ ma, const T* __restrict__ mb,
+                  const T* __restrict__ u, int64_t e0, int64_t e1, T* __restrict__ r_elem,
+                  T* __restrict__ r_global) {
+  using L = RSF<P, FORM, T>;
+  constexpr int N1 = L::N1, Q1 = L::Q1, NB = L::NB, NQ = L::NQ, D = L::D, EB = L::EB;
+  constexpr int Q2 = Q1 * Q1;
+  constexpr bool VAL = L::VAL, GRAD = L::GRAD;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* edge = reinterpret_cast<double*>(smem_raw);        // [EB][12][3]
+  double* Bs = reinterpret_cast<double*>(smem_raw + size_t(EB) * 36 * 8);  // [2][Q1][N1]
+  T* X = reinterpret_cast<T*>(smem_raw + size_t(EB) * 36 * 8 + 2 * Q1 * N1 * 8);  // [EB][D][3][Q1^3]
+  const int tid = threadIdx.x;
+  const int el = tid / L::TPE, tt = tid - el * L::TPE;
+  const int tx = tt % Q1, ty = tt / Q1;
+  const bool active = tid < EB * L::TPE;
+#define B(a, q, i) c_tab1d[P][a][q][i]
+  // 1D tables in smem for the thread-dependent rows / columns (stages x, y, y^T, x^T);
+  // stage z and z^T use the warp-uniform constant copy.
+  for (int i = tid; i < 2 * Q1 * N1; i += blockDim.x) Bs[i] = (&c_tab1d[P][0][0][0])[(i / (Q1 * N1)) * 25 + ((i / N1) % Q1) * 5 + i % N1];
+#define Rx(a, i) Bs[((a) * Q1 + tx) * N1 + (i)]
+#define Ry(a, i) Bs[((a) * Q1 + ty) * N1 + (i)]
+#define Cx(a, q) Bs[((a) * Q1 + (q)) * N1 + tx]
+#define Cy(a, q) Bs[((a) * Q1 + (q)) * N1 + ty]
+  __syncthreads();
+
+  const int64_t nloc = e1 - e0;
+  const int64_t nbatch = (nloc + EB - 1) / EB;
+  for (int64_t bidx = blockIdx.x; bidx < nbatch; bidx += gridDim.x) {
+    const int64_t eb = e0 + bidx * EB;
+    const int ne = (int)((e1 - eb) < EB ? (e1 - eb) : EB);
+    const bool valid = active && el < ne;
+    const int64_t e = eb + el;
+    // edge vectors of the batch's cells
+    for (int i = tid; i < EB * 36; i += blockDim.x) {
+      const int c = i / 36, r = i - c * 36;
+      double v = 0.0;
+      if (c < ne) {
+        const int ed = r / 3, comp = r - ed * 3;
+        const int d = ed >> 2, k = ed & 3, lo = k & 1, hi = k >> 1;
+        const int v0 = d == 0 ? (2 * lo + 4 * hi) : (d == 1 ? (lo + 4 * hi) : (lo + 2 * hi));
+        const int32_t* cn = mv.conn + 8 * (eb + c);
+        v = mv.coords[3 * (int64_t)cn[v0 + (1 << d)] + comp] - mv.coords[3 * (int64_t)cn[v0] + comp];
+      }
+      edge[i] = v;
+    }
+    // gather this thread's z-column
+    int dcol[N1];
+    double uc[D][N1];
+#pragma unroll
+    for (int kz = 0; kz < N1; ++kz) {
+      dcol[kz] = valid ? mv.dof_conn[e * NB + tx + N1 * ty + N1 * N1 * kz] : 0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) uc[a][kz] = valid ? (double)u[(int64_t)dcol[kz] * D + a] : 0.0;
+    }
+    MatQ<T> mq[Q1];  // material of this column's qps, loaded early
+#pragma unroll
+    for (int qz = 0; qz < Q1; ++qz)
+      mq[qz] = valid ? load_matq<FORM, T>(e, tx + Q1 * ty + Q1 * Q1 * qz, NQ, mat_kind, ma, mb)
+                     : MatQ<T>{0.0, 0.0, nullptr};
+    T* Xe = X + el * L::XS;
+    // ---- stage x: contract kx -> qx
+    if (active) {
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int kz = 0; kz < N1; ++kz) Xe[(a * 3) * NQ + kz * Q2 + ty * Q1 + tx] = (T)uc[a][kz];
+    }
+    __syncthreads();
+    double a0[D][N1], a1[D][N1];  // [kz] at (qx = tx, ky = ty)
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int kz = 0; kz < N1; ++kz) {
+        double s0 = 0.0, s1 = 0.0;
+        const T* src = Xe + (a * 3) * NQ + kz * Q2 + ty * Q1;
+#pragma unroll
+        for (int kx = 0; kx < N1; ++kx) {
+          const double v = active ? (double)src[kx] : 0.0;
+          s0 = fma(Rx(0, kx), v, s0);
+          if (GRAD) s1 = fma(Rx(1, kx), v, s1);
+        }
+        a0[a][kz] = s0;
+        a1[a][kz] = s1;
+      }
+    __syncthreads();
+    // ---- stage y: contract ky -> qy
+    if (active) {
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int kz = 0; kz < N1; ++kz) {
+          Xe[(a * 3 + 0) * NQ + kz * Q2 + ty * Q1 + tx] = (T)a0[a][kz];
+          if (GRAD) Xe[(a * 3 + 1) * NQ + kz * Q2 + ty * Q1 + tx] = (T)a1[a][kz];
+        }
+    }
+    __syncthreads();
+    double c00[D][N1], c01[D][N1], c10[D][N1];  // [kz] at (qx = tx, qy = ty)
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int kz = 0; kz < N1; ++kz) {
+        double s00 = 0.0, s01 = 0.0, s10 = 0.0;
+#pragma unroll
+        for (int ky = 0; ky < N1; ++ky) {
+          const double v0 = active ? (double)Xe[(a * 3 + 0) * NQ + kz * Q2 + ky * Q1 + tx] : 0.0;
+          s00 = fma(Ry(0, ky), v0, s00);
+          if (GRAD) {
+            const double v1 = active ? (double)Xe[(a * 3 + 1) * NQ + kz * Q2 + ky * Q1 + tx] : 0.0;
+            s01 = fma(Ry(1, ky), v0, s01);
+            s10 = fma(Ry(0, ky), v1, s10);
+          }
+        }
+        c00[a][kz] = s00;
+        c01[a][kz] = s01;
+        c10[a][kz] = s10;
+      }
+    // ---- geometry constants of this column (edge vectors are in smem since the first sync)
+    const double* ed = edge + el * 36;
+    const double tX = mv.xi[3 * tx], tY = mv.xi[3 * Q1 * ty + 1];
+    double col2[3], e0y[2][3], e1x[2][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      // J[:,2] = sum_{a,b} L_a(x) L_b(y) e2[a][b]
+      col2[i] = (1 - tX) * (1 - tY) * ed[(8 + 0) * 3 + i] + tX * (1 - tY) * ed[(8 + 1) * 3 + i] +
+                (1 - tX) * tY * ed[(8 + 2) * 3 + i] + tX * tY * ed[(8 + 3) * 3 + i];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        // e0 interpolated in y: sum_b L_b(y) e0[b][c];  e1 interpolated in x: sum_a L_a(x) e1[a][c]
+        e0y[c][i] = (1 - tY) * ed[(0 + 2 * c) * 3 + i] + tY * ed[(1 + 2 * c) * 3 + i];
+        e1x[c][i] = (1 - tX) * ed[(4 + 2 * c) * 3 + i] + tX * ed[(5 + 2 * c) * 3 + i];
+      }
+    }
+    // ---- stage z (registers) + pointwise flux + z^T (registers)
+    double Hv[D][N1], Hx[D][N1], Hy[D][N1];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int kz = 0; kz < N1; ++kz) Hv[a][kz] = Hx[a][kz] = Hy[a][kz] = 0.0;
+#pragma unroll
+    for (int qz = 0; qz < Q1; ++qz) {
+      double uq[D], gr[D][3];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        double su = 0.0, sx = 0.0, sy = 0.0, sz = 0.0;
+#pragma unroll
+        for (int kz = 0; kz < N1; ++kz) {
+          su = fma(B(0, qz, kz), c00[a][kz], su);
+          if (GRAD) {
+            sz = fma(B(1, qz, kz), c00[a][kz], sz);
+            sy = fma(B(0, qz, kz), c01[a][kz], sy);
+            sx = fma(B(0, qz, kz), c10[a][kz], sx);
+          }
+        }
+        uq[a] = su;
+        gr[a][0] = sx;
+        gr[a][1] = sy;
+        gr[a][2] = sz;
+      }
+      // geometry at (tx, ty, qz)
+      const double tZ = mv.xi[3 * Q2 * qz + 2];
+      double J[3][3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        J[i][0] = (1 - tZ) * e0y[0][i] + tZ * e0y[1][i];
+        J[i][1] = (1 - tZ) * e1x[0][i] + tZ * e1x[1][i];
+        J[i][2] = col2[i];
+      }
+      const double c00g = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+      const double c01g = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+      const double c02g = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+      const double c10g = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+      const double c11g = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+      const double c12g = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+      const double c20g = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+      const double c21g = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+      const double c22g = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+      const double det = J[0][0] * c00g + J[0][1] * c01g + J[0][2] * c02g;
+      const double id = 1.0 / det;
+      // Jinv[m][j] = cof[j][m] / det
+      const double Ji[9] = {c00g * id, c10g * id, c20g * id, c01g * id, c11g * id,
+                            c21g * id, c02g * id, c12g * id, c22g * id};
+      const int q = tx + Q1 * ty + Q2 * qz;
+      const double dw = mv.w[q] * det;
+      double gu[D][3];
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) gu[a][j] = gr[a][0] * Ji[j] + gr[a][1] * Ji[3 + j] + gr[a][2] * Ji[6 + j];
+      double f0[D], f1[D][3];
+      if (valid) {
+        qp_flux_m<FORM, T>(uq, gu, mq[qz], mat_kind, f0, f1);
+      } else {
+#pragma unroll
+        for (int a = 0; a < D; ++a) f0[a] = f1[a][0] = f1[a][1] = f1[a][2] = 0.0;
+      }
+      // pull back and test along z
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const double F0 = dw * f0[a];
+        const double Fx = dw * (Ji[0] * f1[a][0] + Ji[1] * f1[a][1] + Ji[2] * f1[a][2]);
+        const double Fy = dw * (Ji[3] * f1[a][0] + Ji[4] * f1[a][1] + Ji[5] * f1[a][2]);
+        const double Fz = dw * (Ji[6] * f1[a][0] + Ji[7] * f1[a][1] + Ji[8] * f1[a][2]);
+#pragma unroll
+        for (int kz = 0; kz < N1; ++kz) {
+          double hv = 0.0;
+          if (VAL) hv = B(0, qz, kz) * F0;
+          if (GRAD) {
+            hv = fma(B(1, qz, kz), Fz, hv);
+            Hx[a][kz] = fma(B(0, qz, kz), Fx, Hx[a][kz]);
+            Hy[a][kz] = fma(B(0, qz, kz), Fy, Hy[a][kz]);
+          }
+          Hv[a][kz] += hv;
+        }
+      }
+    }
+    __syncthreads();  // everyone is done reading Xe (stage y)
+    // ---- y^T: contract qy -> ky
+    if (active) {
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int kz = 0; kz < N1; ++kz) {
+          Xe[(a * 3 + 0) * NQ + kz * Q2 + ty * Q1 + tx] = (T)Hv[a][kz];
+          if (GRAD) {
+            Xe[(a * 3 + 1) * NQ + kz * Q2 + ty * Q1 + tx] = (T)Hx[a][kz];
+            Xe[(a * 3 + 2) * NQ + kz * Q2 + ty * Q1 + tx] = (T)Hy[a][kz];
+          }
+        }
+    }
+    __syncthreads();
+    double Iv[D][N1], Ix[D][N1];  // [kz] at (qx = tx, ky = ty)
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int kz = 0; kz < N1; ++kz) {
+        double sv = 0.0, sx = 0.0;
+#pragma unroll
+        for (int qy = 0; qy < Q1; ++qy) {
+          const int o = kz * Q2 + qy * Q1 + tx;
+          const double hv = active ? (double)Xe[(a * 3 + 0) * NQ + o] : 0.0;
+          sv = fma(Cy(0, qy), hv, sv);
+          if (GRAD) {
+            sv = fma(Cy(1, qy), active ? (double)Xe[(a * 3 + 2) * NQ + o] : 0.0, sv);
+            sx = fma(Cy(0, qy), active ? (double)Xe[(a * 3 + 1) * NQ + o] : 0.0, sx);
+          }
+        }
+        Iv[a][kz] = sv;
+        Ix[a][kz] = sx;
+      }
+    __syncthreads();
+    // ---- x^T: contract qx -> kx
+    if (active) {
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int kz = 0; kz < N1; ++kz) {
+          Xe[(a * 3 + 0) * NQ + kz * Q2 + ty * Q1 + tx] = (T)Iv[a][kz];
+          if (GRAD) Xe[(a * 3 + 1) * NQ + kz * Q2 + ty * Q1 + tx] = (T)Ix[a][kz];
+        }
+    }
+    __syncthreads();
+    if (valid) {
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int kz = 0; kz < N1; ++kz) {
+          double s = 0.0;
+#pragma unroll
+          for (int qx = 0; qx < Q1; ++qx) {
+            const int o = kz * Q2 + ty * Q1 + qx;
+            s = fma(Cx(0, qx), (double)Xe[(a * 3 + 0) * NQ + o], s);
+            if (GRAD) s = fma(Cx(1, qx), (double)Xe[(a * 3 + 1) * NQ + o], s);
+          }
+          const T v = (T)s;
+          const int k = tx + N1 * ty + N1 * N1 * kz;
+          if (r_elem) r_elem[(e - e0) * (int64_t)(D * NB) + a * NB + k] = v;
+          if (r_global) atomicAdd(r_global + (int64_t)dcol[kz] * D + a, v);
+        }
+    }
+    __syncthreads();
+  }
+#undef B
+#undef Rx
+#undef Ry
+#undef Cx
+#undef Cy
+}
+
+template <int P, int FORM, typename T>
+static cudaError_t launch_rsf_t(const fe_mesh* mh, MatArgs mat, const T* u, int64_t e0, int64_t e1,
+                                T* r_elem, T* r_global, cudaStream_t st) {
+  using L = RSF<P, FORM, T>;
+  auto kern = k_residual_sf<P, FORM, T>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
+  if (err != cudaSuccess) return err;
+  int nsm = 148, per_sm = 1, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::THREADS, L::BYTES);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t nbatch = (e1 - e0 + L::EB - 1) / L::EB;
+  const int grid = (int)((nbatch < (int64_t)nsm * per_sm) ? nbatch : (int64_t)nsm * per_sm);
+  if (grid <= 0) return cudaSuccess;
+  kern<<<grid, L::THREADS, L::BYTES, st>>>(view_of(mh), mat.kind, (const T*)mat.a, (const T*)mat.b,
+                                           u, e0, e1, r_elem, r_global);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int P, typename T>
+static cudaError_t rsf_form(const fe_mesh* mh, int form, MatArgs mat, const T* u, int64_t e0,
+                            int64_t e1, T* re, T* rg, cudaStream_t st) {
+  switch (form) {
+    case FE_FORM_DIFFUSION: return launch_rsf_t<P, FE_FORM_DIFFUSION, T>(mh, mat, u, e0, e1, re, rg, st);
+    case FE_FORM_MASS: return launch_rsf_t<P, FE_FORM_MASS, T>(mh, mat, u, e0, e1, re, rg, st);
+    case FE_FORM_MASS_DIFFUSION: return launch_rsf_t<P, FE_FORM_MASS_DIFFUSION, T>(mh, mat, u, e0, e1, re, rg, st);
+    default: break;
+  }
+  if constexpr (sizeof(T) == 8) {
+    switch (form) {
+      case FE_FORM_VECTOR_MASS: return launch_rsf_t<P, FE_FORM_VECTOR_MASS, T>(mh, mat, u, e0, e1, re, rg, st);
+      case FE_FORM_ELASTICITY: return launch_rsf_t<P, FE_FORM_ELASTICITY, T>(mh, mat, u, e0, e1, re, rg, st);
+      case FE_FORM_CONVECTIVE: return launch_rsf_t<P, FE_FORM_CONVECTIVE, T>(mh, mat, u, e0, e1, re, rg, st);
+      default: break;
+    }
+  }
+  return cudaErrorNotSupported;
+}
+
+template <typename T>
+cudaError_t launch_residual_sf(const fe_mesh* mh, int form, MatArgs mat, const T* u, int64_t e0,
+                               int64_t e1, T* re, T* rg, cudaStream_t st) {
+  if (mh->q1d != mh->order + 1) return cudaErrorNotSupported;
+  switch (mh->order) {
+    case 1: return rsf_form<1, T>(mh, form, mat, u, e0, e1, re, rg, st);
+    case 2: return rsf_form<2, T>(mh, form, mat, u, e0, e1, re, rg, st);
+    case 3: return rsf_form<3, T>(mh, form, mat, u, e0, e1, re, rg, st);
+    case 4: return rsf_form<4, T>(mh, form, mat, u, e0, e1, re, rg, st);
+  }
+  return cudaErrorNotSupported;
+}
+
+template cudaError_t launch_residual_sf<double>(const fe_mesh*, int, MatArgs, const double*, int64_t,
+                                                int64_t, double*, double*, cudaStream_t);
+template cudaError_t launch_residual_sf<float>(const fe_mesh*, int, MatArgs, const float*, int64_t,
+                                               int64_t, float*, float*, cudaStream_t);
+
+}  // namespace feb200
