@@ -18,7 +18,8 @@ from typing import Optional
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfeb200.so")
+# FEB200_LIB_PATH selects another in-tree build of the same library (A/B kernel experiments)
+LIB_PATH = os.environ.get("FEB200_LIB_PATH", os.path.join(_HERE, "libfeb200.so"))
 
 FE_OK, FE_ERR_INVALID_ARG, FE_ERR_UNSUPPORTED, FE_ERR_DEGENERATE, FE_ERR_CUDA, FE_ERR_OOM = range(6)
 DIFFUSION, MASS, VECTOR_MASS, MASS_DIFFUSION, ELASTICITY, CONVECTIVE = range(6)

@@ -175,8 +175,11 @@ __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_D
       c0 = c1 = -1;
     }
   };
-  auto ld_edge = [&](int c0, int c1) -> double {
-    return c0 >= 0 ? mv.coords[3 * (int64_t)c1 + pe_c] - mv.coords[3 * (int64_t)c0 + pe_c] : 0.0;
+  // the two end-point coordinates stay in registers until the next batch: subtracting
+  // them right away would wait for the loads here instead of overlapping them
+  auto ld_edge = [&](int c0, int c1, double& xa, double& xb) {
+    xa = c0 >= 0 ? mv.coords[3 * (int64_t)c0 + pe_c] : 0.0;
+    xb = c0 >= 0 ? mv.coords[3 * (int64_t)c1 + pe_c] : 0.0;
   };
   auto ld_k = [&](int64_t b, double& kap, double& rho) {
     kap = rho = 0.0;
@@ -190,7 +193,8 @@ __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_D
   };
   int cn0, cn1;
   ld_conn2(blockIdx.x, cn0, cn1);
-  double edge_cur = ld_edge(cn0, cn1), k_cur, r_cur;
+  double xa_cur, xb_cur, k_cur, r_cur;
+  ld_edge(cn0, cn1, xa_cur, xb_cur);
   ld_k(blockIdx.x, k_cur, r_cur);
   ld_conn2(blockIdx.x + gridDim.x, cn0, cn1);
 
@@ -200,12 +204,12 @@ __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_D
     const int ne = (int)((nloc - lb) < E ? (nloc - lb) : E);
     double* Kst = sm + L::OFF_K + (it & 1) * L::KST;
     // A. this batch's data from the prefetch registers; issue the next reads
-    if (pe_on) edge[tid] = edge_cur;
+    if (pe_on) edge[tid] = xb_cur - xa_cur;
     if (pk_on) {
       coef[(pk_el * 2) * NQ + pk_q] = k_cur;
       coef[(pk_el * 2 + 1) * NQ + pk_q] = r_cur;
     }
-    edge_cur = ld_edge(cn0, cn1);
+    ld_edge(cn0, cn1, xa_cur, xb_cur);
     ld_k(bidx + gridDim.x, k_cur, r_cur);
     ld_conn2(bidx + 2 * (int64_t)gridDim.x, cn0, cn1);
     // the TMA store issued two batches ago read this staging buffer: wait for it
