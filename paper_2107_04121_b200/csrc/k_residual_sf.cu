@@ -23,16 +23,53 @@ cudaError_t upload_const_tables_residual(int order, const double* b1, const doub
   return upload_tables_this_tu(order, b1, d1, x1, w1, st);
 }
 
+__device__ __forceinline__ uint32_t saddr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(saddr(bar)), "r"(parity) : "memory");
+}
+// TMA bulk copy global -> shared, completion counted on an mbarrier (16-B aligned, size % 16 == 0)
+__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(saddr(dst)), "l"(src), "r"(bytes), "r"(saddr(bar)) : "memory");
+}
+
 template <int P, int FORM, typename T>
 struct RSF {
   static constexpr int N1 = P + 1, Q1 = P + 1, NB = N1 * N1 * N1, NQ = Q1 * Q1 * Q1;
   static constexpr int D = FormD<FORM>::D;
   static constexpr int TPE = Q1 * Q1;  // threads per cell
-  static constexpr int EB0 = P == 1 ? 32 : (P == 2 ? 28 : (P == 3 ? 16 : 10));
+  static constexpr int EB0 = P == 1 ? 32 : (P == 2 ? 28 : (P == 3 ? 16 : 8));  // multiples of 4 (TMA alignment)
   static constexpr int EB = (D == 3 && P >= 3) ? EB0 / 2 : EB0;  // cells per CTA iteration
   static constexpr int THREADS = (EB * TPE + 31) / 32 * 32;
+  static constexpr int THREADS_ = THREADS;
   static constexpr int XS = 3 * D * NQ;  // exchange buffer per cell (elements of T)
-  static constexpr size_t BYTES = size_t(EB) * 36 * 8 + 2 * Q1 * N1 * 8 + size_t(EB) * XS * sizeof(T);
+  // prefetch slots (x2): conn [EB][8], dof_conn [EB][NB] (int32), material a, b [EB][NQ] (T),
+  // vertex coordinates [EB][24]; plus two mbarriers
+  static constexpr size_t SL_CONN = 0;
+  static constexpr size_t SL_DOF = SL_CONN + size_t(EB) * 8 * 4;
+  static constexpr size_t SL_MA = (SL_DOF + size_t(EB) * NB * 4 + 15) / 16 * 16;
+  static constexpr size_t SL_MB = (SL_MA + size_t(EB) * NQ * sizeof(T) + 15) / 16 * 16;
+  static constexpr size_t SL_SIZE = (SL_MB + size_t(EB) * NQ * sizeof(T) + 15) / 16 * 16;
+  static constexpr size_t OFF_X = size_t(EB) * 36 * 8 + 2 * Q1 * N1 * 8;
+  static constexpr size_t OFF_XV = (OFF_X + size_t(EB) * XS * sizeof(T) + 15) / 16 * 16;
+  static constexpr size_t OFF_SLOT = OFF_XV + size_t(EB) * 24 * 8;
+  static constexpr size_t OFF_BAR = OFF_SLOT + 2 * SL_SIZE;
+  static constexpr size_t BYTES = OFF_BAR + 16;
+  static constexpr int PX = (EB * 24 + THREADS_ - 1) / THREADS_;  // vertex coordinates per thread
   static constexpr bool VAL = FORM == FE_FORM_MASS || FORM == FE_FORM_VECTOR_MASS ||
                               FORM == FE_FORM_MASS_DIFFUSION || FORM == FE_FORM_CONVECTIVE;
   static constexpr bool GRAD = FORM != FE_FORM_MASS && FORM != FE_FORM_VECTOR_MASS;
@@ -50,7 +87,10 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* edge = reinterpret_cast<double*>(smem_raw);        // [EB][12][3]
   double* Bs = reinterpret_cast<double*>(smem_raw + size_t(EB) * 36 * 8);  // [2][Q1][N1]
-  T* X = reinterpret_cast<T*>(smem_raw + size_t(EB) * 36 * 8 + 2 * Q1 * N1 * 8);  // [EB][D][3][Q1^3]
+  T* X = reinterpret_cast<T*>(smem_raw + L::OFF_X);  // [EB][D][3][Q1^3]
+  double* xvs = reinterpret_cast<double*>(smem_raw + L::OFF_XV);  // [EB][24] vertex coordinates
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + L::OFF_BAR);
+  auto slot_base = [&](int s_) { return smem_raw + L::OFF_SLOT + s_ * L::SL_SIZE; };
   const int tid = threadIdx.x;
   const int el = tid / L::TPE, tt = tid - el * L::TPE;
   const int tx = tt % Q1, ty = tt / Q1;
@@ -67,38 +107,130 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
 
   const int64_t nloc = e1 - e0;
   const int64_t nbatch = (nloc + EB - 1) / EB;
-  for (int64_t bidx = blockIdx.x; bidx < nbatch; bidx += gridDim.x) {
+  const int64_t G = gridDim.x;
+  // material blocks fetched with the indices: per-qp arrays of the scalar forms / elasticity
+  constexpr bool MAT_QP = FORM == FE_FORM_DIFFUSION || FORM == FE_FORM_MASS ||
+                          FORM == FE_FORM_VECTOR_MASS || FORM == FE_FORM_MASS_DIFFUSION;
+  const int nma = MAT_QP ? NQ : ((FORM == FE_FORM_ELASTICITY && mat_kind == FE_MAT_PER_QP) ? NQ
+                                 : (FORM == FE_FORM_ELASTICITY && mat_kind == FE_MAT_PER_ELEM) ? 1 : 0);
+  const bool has_mb = FORM == FE_FORM_MASS_DIFFUSION || (FORM == FE_FORM_ELASTICITY && nma > 0);
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // TMA bulk loads of the contiguous per-batch blocks (conn, dof_conn, material) into slot j % 2
+  auto fetch_idx = [&](int64_t j) {
+    const int64_t b = blockIdx.x + j * G;
+    if (b >= nbatch) return;
+    const int sl = (int)(j & 1);
+    unsigned char* base = slot_base(sl);
+    const int64_t eb = e0 + b * EB;
+    const int ne = (int)((e1 - eb) < EB ? (e1 - eb) : EB);
+    const uint32_t bc = ne * 32u, bd = ne * NB * 4u, bm = ne * nma * (uint32_t)sizeof(T);
+    const void* gc = mv.conn + 8 * eb;
+    const void* gd = mv.dof_conn + eb * NB;
+    const void* ga = ma + eb * nma;
+    const void* gb = has_mb ? (const void*)(mb + eb * nma) : nullptr;
+    auto al = [](const void* p, uint32_t n) { return ((reinterpret_cast<uintptr_t>(p) | n) & 15u) == 0; };
+    const bool ok = al(gc, bc) && al(gd, bd) && (nma == 0 || (al(ga, bm) && (!has_mb || al(gb, bm))));
+    if (ok) {
+      if (tid == 0) {
+        mbar_expect_tx(&bars[sl], bc + bd + (nma ? bm * (has_mb ? 2 : 1) : 0));
+        tma_load(base + L::SL_CONN, gc, bc, &bars[sl]);
+        tma_load(base + L::SL_DOF, gd, bd, &bars[sl]);
+        if (nma) {
+          tma_load(base + L::SL_MA, ga, bm, &bars[sl]);
+          if (has_mb) tma_load(base + L::SL_MB, gb, bm, &bars[sl]);
+        }
+      }
+    } else {  // unaligned range: plain copies, then a plain arrival
+      int32_t* cs = reinterpret_cast<int32_t*>(base + L::SL_CONN);
+      int32_t* ds = reinterpret_cast<int32_t*>(base + L::SL_DOF);
+      T* as_ = reinterpret_cast<T*>(base + L::SL_MA);
+      T* bs_ = reinterpret_cast<T*>(base + L::SL_MB);
+      for (int i = tid; i < ne * 8; i += blockDim.x) cs[i] = mv.conn[8 * eb + i];
+      for (int i = tid; i < ne * NB; i += blockDim.x) ds[i] = mv.dof_conn[eb * NB + i];
+      for (int i = tid; i < ne * nma; i += blockDim.x) {
+        as_[i] = ma[eb * nma + i];
+        if (has_mb) bs_[i] = mb[eb * nma + i];
+      }
+      __syncthreads();
+      if (tid == 0) mbar_arrive(&bars[sl]);
+    }
+  };
+  // register prefetch of the dependent gathers (u at the column's nodes, vertex coordinates)
+  double u_next[D][N1];
+  double x_next[L::PX];
+  auto gather_next = [&](int64_t j) {
+    const int64_t b = blockIdx.x + j * G;
+    const int sl = (int)(j & 1);
+    const unsigned char* base = slot_base(sl);
+    const int32_t* cs = reinterpret_cast<const int32_t*>(base + L::SL_CONN);
+    const int32_t* ds = reinterpret_cast<const int32_t*>(base + L::SL_DOF);
+    const int64_t eb = e0 + b * EB;
+    const int ne = b < nbatch ? (int)((e1 - eb) < EB ? (e1 - eb) : EB) : 0;
+    if (ne > 0) mbar_wait(&bars[sl], (uint32_t)((j >> 1) & 1));
+    const bool v = active && el < ne;
+#pragma unroll
+    for (int kz = 0; kz < N1; ++kz) {
+      const int dof = v ? ds[el * NB + tx + N1 * ty + N1 * N1 * kz] : 0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) u_next[a][kz] = v ? (double)u[(int64_t)dof * D + a] : 0.0;
+    }
+#pragma unroll
+    for (int h = 0; h < L::PX; ++h) {
+      const int i = tid + h * blockDim.x;
+      const int c = i / 24, r = i - c * 24;
+      x_next[h] = (i < EB * 24 && c < ne) ? mv.coords[3 * (int64_t)cs[c * 8 + r / 3] + r % 3] : 0.0;
+    }
+  };
+  fetch_idx(0);
+  gather_next(0);
+  int64_t it = 0;
+  for (int64_t bidx = blockIdx.x; bidx < nbatch; bidx += G, ++it) {
     const int64_t eb = e0 + bidx * EB;
     const int ne = (int)((e1 - eb) < EB ? (e1 - eb) : EB);
     const bool valid = active && el < ne;
     const int64_t e = eb + el;
-    // edge vectors of the batch's cells
-    for (int i = tid; i < EB * 36; i += blockDim.x) {
-      const int c = i / 36, r = i - c * 36;
-      double v = 0.0;
-      if (c < ne) {
-        const int ed = r / 3, comp = r - ed * 3;
-        const int d = ed >> 2, k = ed & 3, lo = k & 1, hi = k >> 1;
-        const int v0 = d == 0 ? (2 * lo + 4 * hi) : (d == 1 ? (lo + 4 * hi) : (lo + 2 * hi));
-        const int32_t* cn = mv.conn + 8 * (eb + c);
-        v = mv.coords[3 * (int64_t)cn[v0 + (1 << d)] + comp] - mv.coords[3 * (int64_t)cn[v0] + comp];
-      }
-      edge[i] = v;
+    const int sl = (int)(it & 1);
+    const unsigned char* base = slot_base(sl);
+    fetch_idx(it + 1);  // slot (it+1)%2 was last read by batch it-1 (done)
+    // this batch's vertex coordinates and column values from the prefetch registers
+#pragma unroll
+    for (int h = 0; h < L::PX; ++h) {
+      const int i = tid + h * blockDim.x;
+      if (i < EB * 24) xvs[i] = x_next[h];
     }
-    // gather this thread's z-column
+    const int32_t* ds = reinterpret_cast<const int32_t*>(base + L::SL_DOF) + el * NB;
+    const T* msa = reinterpret_cast<const T*>(base + L::SL_MA) + el * nma;
+    const T* msb = reinterpret_cast<const T*>(base + L::SL_MB) + el * nma;
     int dcol[N1];
     double uc[D][N1];
 #pragma unroll
     for (int kz = 0; kz < N1; ++kz) {
-      dcol[kz] = valid ? mv.dof_conn[e * NB + tx + N1 * ty + N1 * N1 * kz] : 0;
+      dcol[kz] = valid ? ds[tx + N1 * ty + N1 * N1 * kz] : 0;
 #pragma unroll
-      for (int a = 0; a < D; ++a) uc[a][kz] = valid ? (double)u[(int64_t)dcol[kz] * D + a] : 0.0;
+      for (int a = 0; a < D; ++a) uc[a][kz] = u_next[a][kz];
     }
-    MatQ<T> mq[Q1];  // material of this column's qps, loaded early
+    MatQ<T> mq[Q1];
 #pragma unroll
-    for (int qz = 0; qz < Q1; ++qz)
-      mq[qz] = valid ? load_matq<FORM, T>(e, tx + Q1 * ty + Q1 * Q1 * qz, NQ, mat_kind, ma, mb)
-                     : MatQ<T>{0.0, 0.0, nullptr};
+    for (int qz = 0; qz < Q1; ++qz) {
+      const int q = tx + Q1 * ty + Q1 * Q1 * qz;
+      MatQ<T> m{0.0, 0.0, nullptr};
+      if (valid) {
+        if constexpr (FORM == FE_FORM_ELASTICITY) {
+          if (mat_kind == FE_MAT_FULL_D) m.Dm = ma + (e * NQ + q) * 36;
+          else if (mat_kind == FE_MAT_PER_ELEM) { m.a = (double)msa[0]; m.b = (double)msb[0]; }
+          else { m.a = (double)msa[q]; m.b = (double)msb[q]; }
+        } else if constexpr (MAT_QP) {
+          m.a = (double)msa[q];
+          if constexpr (FORM == FE_FORM_MASS_DIFFUSION) m.b = (double)msb[q];
+        }
+      }
+      mq[qz] = m;
+    }
     T* Xe = X + el * L::XS;
     // ---- stage x: contract kx -> qx
     if (active) {
@@ -108,6 +240,14 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
         for (int kz = 0; kz < N1; ++kz) Xe[(a * 3) * NQ + kz * Q2 + ty * Q1 + tx] = (T)uc[a][kz];
     }
     __syncthreads();
+    // edge vectors of the batch's cells from the staged vertex coordinates
+    for (int i = tid; i < EB * 36; i += blockDim.x) {
+      const int c = i / 36, r = i - c * 36;
+      const int ed = r / 3, comp = r - ed * 3;
+      const int d = ed >> 2, k = ed & 3, lo = k & 1, hi = k >> 1;
+      const int v0 = d == 0 ? (2 * lo + 4 * hi) : (d == 1 ? (lo + 4 * hi) : (lo + 2 * hi));
+      edge[i] = xvs[c * 24 + 3 * (v0 + (1 << d)) + comp] - xvs[c * 24 + 3 * v0 + comp];
+    }
     double a0[D][N1], a1[D][N1];  // [kz] at (qx = tx, ky = ty)
 #pragma unroll
     for (int a = 0; a < D; ++a)
@@ -319,6 +459,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
           if (r_global) atomicAdd(r_global + (int64_t)dcol[kz] * D + a, v);
         }
     }
+    gather_next(it + 1);
     __syncthreads();
   }
 #undef B
