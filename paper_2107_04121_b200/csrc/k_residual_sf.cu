@@ -84,9 +84,10 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
   constexpr int N1 = L::N1, Q1 = L::Q1, NB = L::NB, NQ = L::NQ, D = L::D, EB = L::EB;
   constexpr int Q2 = Q1 * Q1;
   constexpr bool VAL = L::VAL, GRAD = L::GRAD;
+  using A = T;  // contraction arithmetic in the call's precision (geometry and flux stay fp64)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* edge = reinterpret_cast<double*>(smem_raw);        // [EB][12][3]
-  double* Bs = reinterpret_cast<double*>(smem_raw + size_t(EB) * 36 * 8);  // [2][Q1][N1]
+  T* Bs = reinterpret_cast<T*>(smem_raw + size_t(EB) * 36 * 8);  // [2][Q1][N1] in the arithmetic type
   T* X = reinterpret_cast<T*>(smem_raw + L::OFF_X);  // [EB][D][3][Q1^3]
   double* xvs = reinterpret_cast<double*>(smem_raw + L::OFF_XV);  // [EB][24] vertex coordinates
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + L::OFF_BAR);
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
   const int el = tid / L::TPE, tt = tid - el * L::TPE;
   const int tx = tt % Q1, ty = tt / Q1;
   const bool active = tid < EB * L::TPE;
-#define B(a, q, i) c_tab1d[P][a][q][i]
+#define B(a, q, i) ((A)c_tab1d[P][a][q][i])
   // 1D tables in smem for the thread-dependent rows / columns (stages x, y, y^T, x^T);
   // stage z and z^T use the warp-uniform constant copy.
   for (int i = tid; i < 2 * Q1 * N1; i += blockDim.x) Bs[i] = (&c_tab1d[P][0][0][0])[(i / (Q1 * N1)) * 25 + ((i / N1) % Q1) * 5 + i % N1];
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
     }
   };
   // register prefetch of the dependent gathers (u at the column's nodes, vertex coordinates)
-  double u_next[D][N1];
+  A u_next[D][N1];
   double x_next[L::PX];
   auto gather_next = [&](int64_t j) {
     const int64_t b = blockIdx.x + j * G;
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
     for (int kz = 0; kz < N1; ++kz) {
       const int dof = v ? ds[el * NB + tx + N1 * ty + N1 * N1 * kz] : 0;
 #pragma unroll
-      for (int a = 0; a < D; ++a) u_next[a][kz] = v ? (double)u[(int64_t)dof * D + a] : 0.0;
+      for (int a = 0; a < D; ++a) u_next[a][kz] = v ? (A)u[(int64_t)dof * D + a] : A(0);
     }
 #pragma unroll
     for (int h = 0; h < L::PX; ++h) {
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
     const T* msa = reinterpret_cast<const T*>(base + L::SL_MA) + el * nma;
     const T* msb = reinterpret_cast<const T*>(base + L::SL_MB) + el * nma;
     int dcol[N1];
-    double uc[D][N1];
+    A uc[D][N1];
 #pragma unroll
     for (int kz = 0; kz < N1; ++kz) {
       dcol[kz] = valid ? ds[tx + N1 * ty + N1 * N1 * kz] : 0;
@@ -248,16 +249,16 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
       const int v0 = d == 0 ? (2 * lo + 4 * hi) : (d == 1 ? (lo + 4 * hi) : (lo + 2 * hi));
       edge[i] = xvs[c * 24 + 3 * (v0 + (1 << d)) + comp] - xvs[c * 24 + 3 * v0 + comp];
     }
-    double a0[D][N1], a1[D][N1];  // [kz] at (qx = tx, ky = ty)
+    A a0[D][N1], a1[D][N1];  // [kz] at (qx = tx, ky = ty)
 #pragma unroll
     for (int a = 0; a < D; ++a)
 #pragma unroll
       for (int kz = 0; kz < N1; ++kz) {
-        double s0 = 0.0, s1 = 0.0;
+        A s0 = A(0), s1 = A(0);
         const T* src = Xe + (a * 3) * NQ + kz * Q2 + ty * Q1;
 #pragma unroll
         for (int kx = 0; kx < N1; ++kx) {
-          const double v = active ? (double)src[kx] : 0.0;
+          const A v = active ? (A)src[kx] : A(0);
           s0 = fma(Rx(0, kx), v, s0);
           if (GRAD) s1 = fma(Rx(1, kx), v, s1);
         }
@@ -276,18 +277,18 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
         }
     }
     __syncthreads();
-    double c00[D][N1], c01[D][N1], c10[D][N1];  // [kz] at (qx = tx, qy = ty)
+    A c00[D][N1], c01[D][N1], c10[D][N1];  // [kz] at (qx = tx, qy = ty)
 #pragma unroll
     for (int a = 0; a < D; ++a)
 #pragma unroll
       for (int kz = 0; kz < N1; ++kz) {
-        double s00 = 0.0, s01 = 0.0, s10 = 0.0;
+        A s00 = A(0), s01 = A(0), s10 = A(0);
 #pragma unroll
         for (int ky = 0; ky < N1; ++ky) {
-          const double v0 = active ? (double)Xe[(a * 3 + 0) * NQ + kz * Q2 + ky * Q1 + tx] : 0.0;
+          const A v0 = active ? (A)Xe[(a * 3 + 0) * NQ + kz * Q2 + ky * Q1 + tx] : A(0);
           s00 = fma(Ry(0, ky), v0, s00);
           if (GRAD) {
-            const double v1 = active ? (double)Xe[(a * 3 + 1) * NQ + kz * Q2 + ky * Q1 + tx] : 0.0;
+            const A v1 = active ? (A)Xe[(a * 3 + 1) * NQ + kz * Q2 + ky * Q1 + tx] : A(0);
             s01 = fma(Ry(1, ky), v0, s01);
             s10 = fma(Ry(0, ky), v1, s10);
           }
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
       }
     }
     // ---- stage z (registers) + pointwise flux + z^T (registers)
-    double Hv[D][N1], Hx[D][N1], Hy[D][N1];
+    A Hv[D][N1], Hx[D][N1], Hy[D][N1];
 #pragma unroll
     for (int a = 0; a < D; ++a)
 #pragma unroll
@@ -323,7 +324,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
       double uq[D], gr[D][3];
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        double su = 0.0, sx = 0.0, sy = 0.0, sz = 0.0;
+        A su = A(0), sx = A(0), sy = A(0), sz = A(0);
 #pragma unroll
         for (int kz = 0; kz < N1; ++kz) {
           su = fma(B(0, qz, kz), c00[a][kz], su);
@@ -378,13 +379,13 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
       // pull back and test along z
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        const double F0 = dw * f0[a];
-        const double Fx = dw * (Ji[0] * f1[a][0] + Ji[1] * f1[a][1] + Ji[2] * f1[a][2]);
-        const double Fy = dw * (Ji[3] * f1[a][0] + Ji[4] * f1[a][1] + Ji[5] * f1[a][2]);
-        const double Fz = dw * (Ji[6] * f1[a][0] + Ji[7] * f1[a][1] + Ji[8] * f1[a][2]);
+        const A F0 = (A)(dw * f0[a]);
+        const A Fx = (A)(dw * (Ji[0] * f1[a][0] + Ji[1] * f1[a][1] + Ji[2] * f1[a][2]));
+        const A Fy = (A)(dw * (Ji[3] * f1[a][0] + Ji[4] * f1[a][1] + Ji[5] * f1[a][2]));
+        const A Fz = (A)(dw * (Ji[6] * f1[a][0] + Ji[7] * f1[a][1] + Ji[8] * f1[a][2]));
 #pragma unroll
         for (int kz = 0; kz < N1; ++kz) {
-          double hv = 0.0;
+          A hv = A(0);
           if (VAL) hv = B(0, qz, kz) * F0;
           if (GRAD) {
             hv = fma(B(1, qz, kz), Fz, hv);
@@ -410,20 +411,20 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
         }
     }
     __syncthreads();
-    double Iv[D][N1], Ix[D][N1];  // [kz] at (qx = tx, ky = ty)
+    A Iv[D][N1], Ix[D][N1];  // [kz] at (qx = tx, ky = ty)
 #pragma unroll
     for (int a = 0; a < D; ++a)
 #pragma unroll
       for (int kz = 0; kz < N1; ++kz) {
-        double sv = 0.0, sx = 0.0;
+        A sv = A(0), sx = A(0);
 #pragma unroll
         for (int qy = 0; qy < Q1; ++qy) {
           const int o = kz * Q2 + qy * Q1 + tx;
-          const double hv = active ? (double)Xe[(a * 3 + 0) * NQ + o] : 0.0;
+          const A hv = active ? (A)Xe[(a * 3 + 0) * NQ + o] : A(0);
           sv = fma(Cy(0, qy), hv, sv);
           if (GRAD) {
-            sv = fma(Cy(1, qy), active ? (double)Xe[(a * 3 + 2) * NQ + o] : 0.0, sv);
-            sx = fma(Cy(0, qy), active ? (double)Xe[(a * 3 + 1) * NQ + o] : 0.0, sx);
+            sv = fma(Cy(1, qy), active ? (A)Xe[(a * 3 + 2) * NQ + o] : A(0), sv);
+            sx = fma(Cy(0, qy), active ? (A)Xe[(a * 3 + 1) * NQ + o] : A(0), sx);
           }
         }
         Iv[a][kz] = sv;
@@ -446,12 +447,12 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
       for (int a = 0; a < D; ++a)
 #pragma unroll
         for (int kz = 0; kz < N1; ++kz) {
-          double s = 0.0;
+          A s = A(0);
 #pragma unroll
           for (int qx = 0; qx < Q1; ++qx) {
             const int o = kz * Q2 + ty * Q1 + qx;
-            s = fma(Cx(0, qx), (double)Xe[(a * 3 + 0) * NQ + o], s);
-            if (GRAD) s = fma(Cx(1, qx), (double)Xe[(a * 3 + 1) * NQ + o], s);
+            s = fma(Cx(0, qx), (A)Xe[(a * 3 + 0) * NQ + o], s);
+            if (GRAD) s = fma(Cx(1, qx), (A)Xe[(a * 3 + 1) * NQ + o], s);
           }
           const T v = (T)s;
           const int k = tx + N1 * ty + N1 * N1 * kz;
