@@ -337,6 +337,7 @@ def main():
     K = torch.empty((El, D * nb, D * nb), dtype=torch.float64, device=dev) if "matrix" in modes else None
     r = torch.zeros((sl.n_nodes, D), dtype=tdt, device=dev)
     stream = torch.cuda.current_stream(dev)
+    comm_stream = torch.cuda.Stream(dev) if world > 1 else None
     bufs = [None]
     ev = {m: [] for m in modes}
 
@@ -352,11 +353,16 @@ def main():
             r.zero_()
             if record:
                 a = torch.cuda.Event(enable_timing=True); a.record(stream)
-            fe.fe_eval_residual(mesh.handle, prob.form, dtc, prob.mat_kind, mat_a, mat_b, u, 0, El,
-                                None, r, stream)
+
+            def evaluate(lo, hi):
+                fe.fe_eval_residual(mesh.handle, prob.form, dtc, prob.mat_kind, mat_a, mat_b, u, lo,
+                                    hi, None, r, stream)
+
+            # boundary-first residual; for N > 1 the interface exchange overlaps the interior
+            bufs[0] = slabs.residual_overlapped(evaluate, r, sl, prob.shape,
+                                                comm_stream if world > 1 else None, bufs[0])
             if record:
                 b = torch.cuda.Event(enable_timing=True); b.record(stream); ev["residual"].append((a, b))
-            bufs[0] = slabs.exchange_planes(r, sl, None, bufs[0])
 
     def barrier():
         if world > 1:

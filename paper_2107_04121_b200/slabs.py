@@ -94,3 +94,49 @@ def exchange_planes(r: torch.Tensor, slab: Slab, group=None, bufs=None):
     if slab.rank < slab.world - 1:
         hi.add_(bufs[1])
     return bufs
+
+
+def layer_cells(shape, world: int) -> int:
+    """Cells in one z-layer of a slab (nx * ny)."""
+    return shape[0] * shape[1]
+
+
+def residual_overlapped(evaluate, r: torch.Tensor, slab: Slab, shape, comm_stream=None, bufs=None):
+    """Boundary-first residual step with the interface exchange overlapped.
+
+    evaluate(a, b) launches the fused residual kernel for local cells [a, b) on the current
+    stream.  The two boundary z-layers are evaluated first; their node planes are then final,
+    so the NCCL exchange of those planes runs on `comm_stream` while the interior layers are
+    evaluated (the interior cells never touch the interface planes).  The current stream
+    waits for the exchange before returning."""
+    n_local = slab.n_elems
+    if slab.world == 1:
+        evaluate(0, n_local)
+        return bufs
+    L = layer_cells(shape, slab.world)
+    if comm_stream is None:  # CPU / gloo: same boundary-first order, no concurrency
+        if n_local <= 2 * L:
+            evaluate(0, n_local)
+            return exchange_planes(r, slab, None, bufs)
+        evaluate(0, L)
+        evaluate(n_local - L, n_local)
+        bufs = exchange_planes(r, slab, None, bufs)
+        evaluate(L, n_local - L)
+        return bufs
+    main = torch.cuda.current_stream(r.device)
+    if n_local <= 2 * L:
+        evaluate(0, n_local)
+        lo_hi_done = [(0, n_local)]
+    else:
+        evaluate(0, L)
+        evaluate(n_local - L, n_local)
+        lo_hi_done = None
+    ev = torch.cuda.Event()
+    ev.record(main)
+    comm_stream.wait_event(ev)
+    with torch.cuda.stream(comm_stream):
+        bufs = exchange_planes(r, slab, None, bufs)
+    if lo_hi_done is None:
+        evaluate(L, n_local - L)
+    main.wait_stream(comm_stream)
+    return bufs

@@ -29,7 +29,49 @@ def _free_port():
 
 
 CASES = {"diff_q2": (fi.DIFFUSION, 2, (3, 2, 4)), "elas_q2": (fi.ELASTICITY, 2, (2, 3, 4)),
-         "conv_q1": (fi.CONVECTIVE, 1, (3, 3, 4)), "md_q4": (fi.MASS_DIFFUSION, 4, (2, 2, 4))}
+         "conv_q1": (fi.CONVECTIVE, 1, (3, 3, 4)), "md_q4": (fi.MASS_DIFFUSION, 4, (2, 2, 4)),
+         "diff_q2_deep": (fi.DIFFUSION, 2, (3, 2, 8))}
+
+
+def _worker_overlap(rank, world, port, case, out):
+    """Boundary layers, exchange, then interior (the order of residual_overlapped): the
+    interior cells must not touch the interface planes, or the sums would be incomplete."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    form, p, shape = CASES[case]
+    pr = fi.make_problem(form, p, shape, 4242)
+    sl = slabs.slab_of(shape, p, world, rank)
+    lc, lconn, ldc = slabs.local_arrays(sl, pr.coords, pr.conn, pr.dof_conn)
+    e0, e1 = sl.elem_begin, sl.elem_end
+    ma = None if pr.mat_a is None else pr.mat_a[e0:e1]
+    mb = None if pr.mat_b is None else pr.mat_b[e0:e1]
+    u_loc = pr.u[sl.node_begin:sl.node_end]
+    R = torch.zeros((sl.n_nodes, pr.ncomp), dtype=torch.float64)
+
+    def evaluate(a, b):
+        r_el = oracle.eval_residual(form, p, p + 1, lc, lconn, ldc, u_loc, pr.mat_kind, ma, mb, a, b)
+        Rn = oracle.assemble(r_el, ldc[a:b], sl.n_nodes, pr.ncomp)
+        R.add_(torch.from_numpy(Rn.reshape(sl.n_nodes, pr.ncomp)))
+
+    slabs.residual_overlapped(evaluate, R, sl, shape)
+    out[rank] = (sl.node_begin, sl.node_end, R.numpy().copy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_boundary_first_order_matches_global():
+    world = 2
+    form, p, shape = CASES["diff_q2_deep"]
+    pr = fi.make_problem(form, p, shape, 4242)
+    Rg = oracle.problem_assembled_residual(pr).reshape(pr.n_nodes, 1)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_overlap, args=(world, _free_port(), "diff_q2_deep", out), nprocs=world,
+             join=True)
+    for rank in range(world):
+        a, b, R = out[rank]
+        np.testing.assert_allclose(R, Rg[a:b], rtol=1e-13, atol=1e-15 * np.abs(Rg).max())
 
 
 def _worker(rank, world, port, case, out):
@@ -54,7 +96,7 @@ def _worker(rank, world, port, case, out):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("case", sorted(CASES))
+@pytest.mark.parametrize("case", ["conv_q1", "diff_q2", "elas_q2", "md_q4"])
 def test_slab_exchange_matches_global(world, case):
     form, p, shape = CASES[case]
     pr = fi.make_problem(form, p, shape, 4242)
