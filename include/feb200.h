@@ -149,6 +149,18 @@ fe_status fe_eval_residual(const fe_mesh *mesh, int32_t form, int32_t dtype,
                            const fe_material *mat, const void *u, int64_t elem_begin,
                            int64_t elem_end, void *r_elem, void *r_global, void *stream);
 
+/* 'eval' mode ("the integral value in case all variables passed to
+ * the evaluation function have associated DOFs"): the form with the test
+ * function replaced by the field u itself, over cells [elem_begin, elem_end):
+ *   value += sum_e int_e F(u, u)  (= sum_e u_e . r_e(u): u^T K u for the
+ *   bilinear forms, c(u, u, u) for the convective form).
+ * `value` is ONE device double, ACCUMULATED (+=; the caller zeroes it); fp
+ * atomics make the summation order (and the last bits) run-dependent.
+ * u has the element type of dtype; the sum is accumulated in fp64. */
+fe_status fe_eval_scalar(const fe_mesh *mesh, int32_t form, int32_t dtype, const fe_material *mat,
+                         const void *u, int64_t elem_begin, int64_t elem_end, double *value,
+                         void *stream);
+
 /* Scatter-add of cell residuals (standalone assembly):
  *   r_global[dof_conn[e][k] * ncomp + a] += r_elem[e - elem_begin][a * n_b + k]
  * for e in [elem_begin, elem_end).  ncomp in {1, 3}. */

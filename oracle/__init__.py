@@ -52,6 +52,8 @@ def lib():
         _lib.oracle_eval_residual.argtypes = [ci, ci, ci, i64, P, P, P, ci, P, P, P, i64, i64, P]
         _lib.oracle_assemble.argtypes = [i64, ci, ci, P, P, P]
         _lib.oracle_isotropic_D.argtypes = [ctypes.c_double, ctypes.c_double, P]
+        _lib.oracle_eval_scalar.argtypes = [ci, ci, ci, i64, P, P, P, ci, P, P, P, i64, i64, P]
+        _lib.oracle_eval_scalar.restype = ci
         _lib.oracle_bad_element.restype = i64
         for f in ("oracle_gauss_legendre", "oracle_lagrange_1d", "oracle_tables", "oracle_geometry",
                   "oracle_eval_matrix", "oracle_eval_residual", "oracle_assemble"):
@@ -153,6 +155,25 @@ def eval_residual(form, p, q1d, coords, conn, dof_conn, u, mat_kind=0, mat_a=Non
                                       mat_kind, _ptr(mat_a), _ptr(mat_b), _ptr(u),
                                       elem_begin, elem_end, _ptr(r)))
     return r
+
+
+def eval_scalar(form, p, q1d, coords, conn, dof_conn, u, mat_kind=0, mat_a=None, mat_b=None,
+                elem_begin=0, elem_end=None):
+    """'eval' mode: the form's integral with the test function replaced by u."""
+    coords, conn, dof_conn = _f64(coords), _i32(conn), _i32(dof_conn)
+    mat_a, mat_b, u = _f64(mat_a), _f64(mat_b), _f64(u)
+    E = conn.shape[0]
+    elem_end = E if elem_end is None else elem_end
+    out = np.zeros(1)
+    _check(lib().oracle_eval_scalar(form, p, q1d, E, _ptr(coords), _ptr(conn), _ptr(dof_conn),
+                                    mat_kind, _ptr(mat_a), _ptr(mat_b), _ptr(u), elem_begin,
+                                    elem_end, _ptr(out)))
+    return float(out[0])
+
+
+def problem_eval_scalar(prob):
+    return eval_scalar(prob.form, prob.p, prob.q1d, prob.coords, prob.conn, prob.dof_conn, prob.u,
+                       prob.mat_kind, prob.mat_a, prob.mat_b)
 
 
 def assemble(r_elem, dof_conn, n_nodes, ncomp, r_global=None):

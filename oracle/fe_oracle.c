@@ -528,3 +528,84 @@ int oracle_assemble(int64_t n_elems, int nb, int D, const int32_t *dof_conn,
         r_global[(int64_t)dof_conn[e * nb + k] * D + a] += r_elem[e * (int64_t)D * nb + a * nb + k];
   return OR_OK;
 }
+
+/* ------------------------------------------------------------------ */
+/* 'eval' mode ("returning the integral value in case all variables
+ * passed to the evaluation function have associated DOFs"): the form with the
+ * test function replaced by the field itself, summed over cells [elem_begin, elem_end):
+ *   diffusion    int kappa grad u . grad u
+ *   mass         int rho u u              vector mass  int rho u_i u_i
+ *   mass+diff    int rho u u + kappa grad u . grad u
+ *   elasticity   int e(u)^T D e(u)
+ *   convective   int u_i (du_i/dx_j) u_j  (c(u, u, u), Eq. fe2)
+ * Plain quadrature sum, Alg. 1's loop with F evaluated at v = u. */
+int oracle_eval_scalar(int form, int p, int q1d, int64_t n_elems, const double *coords,
+                       const int32_t *conn, const int32_t *dof_conn, int mat_kind,
+                       const double *mat_a, const double *mat_b, const double *u,
+                       int64_t elem_begin, int64_t elem_end, double *value) {
+  if (p < 1 || p > 8 || q1d < 1 || q1d > 16 || n_elems < 0) return OR_ERR_ARG;
+  if (form < 0 || form > OR_CONVECTIVE || !u || !value) return OR_ERR_ARG;
+  if (elem_begin < 0 || elem_end > n_elems || elem_begin > elem_end) return OR_ERR_ARG;
+  const int n1 = p + 1, nb = n1 * n1 * n1, nq = q1d * q1d * q1d;
+  const int D = form_ncomp(form);
+  if (!dof_conn) {
+    if (p != 1) return OR_ERR_ARG;
+    dof_conn = conn;
+  }
+  double *xi = malloc(sizeof(double) * 3 * nq), *w = malloc(sizeof(double) * nq);
+  double *Phi = malloc(sizeof(double) * nq * nb), *dPhi = malloc(sizeof(double) * nq * 3 * nb);
+  oracle_tables(p, q1d, xi, w, Phi, dPhi);
+  double Psg[3][3][6];
+  build_psg(Psg);
+  int status = OR_OK;
+  double total = 0.0;
+  for (int64_t e = elem_begin; e < elem_end && status == OR_OK; ++e) {
+    for (int q = 0; q < nq; ++q) {
+      double J[3][3], Ji[3][3];
+      double det = cell_jacobian(coords, conn + 8 * e, xi + 3 * q, J, Ji);
+      if (!(det > 0.0)) { status = OR_ERR_DEGENERATE; g_bad_elem = e; break; }
+      const double detw = w[q] * det;
+      const double *phi = Phi + (int64_t)q * nb;
+      double uq[3] = {0, 0, 0}, gu[3][3] = {{0}};
+      for (int k = 0; k < nb; ++k) {
+        double g[3];
+        for (int j = 0; j < 3; ++j) {
+          g[j] = 0.0;
+          for (int m = 0; m < 3; ++m) g[j] += dPhi[((int64_t)q * 3 + m) * nb + k] * Ji[m][j];
+        }
+        for (int a = 0; a < D; ++a) {
+          const double ua = u[(int64_t)dof_conn[e * nb + k] * D + a];
+          uq[a] += ua * phi[k];
+          for (int j = 0; j < 3; ++j) gu[a][j] += ua * g[j];
+        }
+      }
+      double f = 0.0;
+      if (form == OR_DIFFUSION || form == OR_MASS || form == OR_MASS_DIFFUSION) {
+        double kappa = (form == OR_DIFFUSION) ? qp_value(mat_a, e, q, nq)
+                       : (form == OR_MASS_DIFFUSION) ? qp_value(mat_b, e, q, nq) : 0.0;
+        double rho = (form == OR_MASS || form == OR_MASS_DIFFUSION) ? qp_value(mat_a, e, q, nq) : 0.0;
+        f = kappa * (gu[0][0] * gu[0][0] + gu[0][1] * gu[0][1] + gu[0][2] * gu[0][2]) + rho * uq[0] * uq[0];
+      } else if (form == OR_VECTOR_MASS) {
+        double rho = qp_value(mat_a, e, q, nq);
+        f = rho * (uq[0] * uq[0] + uq[1] * uq[1] + uq[2] * uq[2]);
+      } else if (form == OR_ELASTICITY) {
+        double Dm[36], eps[6];
+        material_D(mat_kind, mat_a, mat_b, e, q, nq, Dm);
+        for (int I = 0; I < 6; ++I) {
+          eps[I] = 0.0;
+          for (int r = 0; r < 3; ++r)
+            for (int l = 0; l < 3; ++l) eps[I] += Psg[r][l][I] * gu[r][l];
+        }
+        for (int I = 0; I < 6; ++I)
+          for (int K = 0; K < 6; ++K) f += eps[I] * Dm[6 * I + K] * eps[K];
+      } else {
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) f += uq[i] * gu[i][j] * uq[j];
+      }
+      total += detw * f;
+    }
+  }
+  free(xi); free(w); free(Phi); free(dPhi);
+  if (status == OR_OK) *value = total;
+  return status;
+}

@@ -63,13 +63,14 @@ def _load():
     lib.fe_eval_residual.argtypes = [P, i32, i32, ctypes.POINTER(fe_material), P, i64, i64, P,
                                      P, P]
     lib.fe_assemble_vector.argtypes = [P, i32, i32, i64, i64, P, P, P]
+    lib.fe_eval_scalar.argtypes = [P, i32, i32, ctypes.POINTER(fe_material), P, i64, i64, P, P]
     lib.fe_geometry.argtypes = [P, P, P, P]
     lib.fe_last_error.restype = ctypes.c_char_p
     lib.fe_last_error_element.restype = i64
     lib.fe_launch_count.restype = i64
     for f in ("fe_create_mesh_geometry", "fe_destroy_mesh", "fe_mesh_info",
               "fe_eval_element_matrices", "fe_eval_residual", "fe_assemble_vector",
-              "fe_geometry"):
+              "fe_geometry", "fe_eval_scalar"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -89,7 +90,7 @@ class _LazyLib:
 
 _lib = _LazyLib()
 ABI_SYMBOLS = ("fe_create_mesh_geometry", "fe_destroy_mesh", "fe_mesh_info",
-               "fe_eval_element_matrices", "fe_eval_residual", "fe_assemble_vector",
+               "fe_eval_element_matrices", "fe_eval_residual", "fe_assemble_vector", "fe_eval_scalar",
                "fe_geometry", "fe_last_error", "fe_last_error_element", "fe_launch_count")
 
 
@@ -186,6 +187,15 @@ def fe_assemble_vector(handle: int, dtype: int, ncomp: int, elem_begin: int, ele
                                    _ptr(r_global), _stream(stream)))
 
 
+def fe_eval_scalar(handle: int, form: int, dtype: int, mat_kind: int,
+                   mat_a: Optional[torch.Tensor], mat_b: Optional[torch.Tensor], u: torch.Tensor,
+                   elem_begin: int, elem_end: int, value: torch.Tensor, stream=None):
+    """value (1-element fp64 device tensor) += the form's integral with v = u (eval mode)."""
+    m = _material(mat_kind, mat_a, mat_b)
+    _check(_lib.fe_eval_scalar(handle, form, dtype, ctypes.byref(m), _ptr(u), elem_begin, elem_end,
+                               _ptr(value), _stream(stream)))
+
+
 def fe_geometry(handle: int, detw: Optional[torch.Tensor], jinv: Optional[torch.Tensor],
                 stream=None):
     _check(_lib.fe_geometry(handle, _ptr(detw), _ptr(jinv), _stream(stream)))
@@ -256,6 +266,15 @@ class Mesh:
         dt = F64 if r_elem.dtype == torch.float64 else F32
         fe_assemble_vector(self.handle, dt, ncomp, elem_begin, elem_end, r_elem, r_global, stream)
         return r_global
+
+    def eval_scalar(self, form, u, mat_kind=MAT_PER_QP, mat_a=None, mat_b=None, elem_begin=0,
+                    elem_end=None, stream=None):
+        elem_end = self.n_elems if elem_end is None else elem_end
+        value = torch.zeros(1, dtype=torch.float64, device=self.device)
+        dt = F64 if u.dtype == torch.float64 else F32
+        fe_eval_scalar(self.handle, form, dt, mat_kind, mat_a, mat_b, u, elem_begin, elem_end,
+                       value, stream)
+        return value
 
     def geometry(self, stream=None):
         detw = torch.empty((self.n_elems, self.nq), dtype=torch.float64, device=self.device)

@@ -276,6 +276,28 @@ fe_status fe_eval_residual(const fe_mesh* mesh, int32_t form, int32_t dtype, con
   return ok();
 }
 
+fe_status fe_eval_scalar(const fe_mesh* mesh, int32_t form, int32_t dtype, const fe_material* mat,
+                         const void* u, int64_t elem_begin, int64_t elem_end, double* value,
+                         void* stream) {
+  fe_status s = check_common(mesh, form, elem_begin, elem_end);
+  if (s != FE_OK) return s;
+  if ((s = check_material(form, mat)) != FE_OK) return s;
+  if (!u || !value) return fail(FE_ERR_INVALID_ARG, "u / value is NULL");
+  if (dtype != FE_F64 && dtype != FE_F32) return fail(FE_ERR_INVALID_ARG, "unknown dtype");
+  feb200::MatArgs ma{mat ? mat->kind : 0, mat ? mat->a : nullptr, mat ? mat->b : nullptr};
+  cudaError_t e;
+  if (dtype == FE_F64)
+    e = feb200::launch_residual_sf<double>(mesh, form, ma, (const double*)u, elem_begin, elem_end,
+                                           nullptr, nullptr, (cudaStream_t)stream, value);
+  else
+    e = feb200::launch_residual_sf<float>(mesh, form, ma, (const float*)u, elem_begin, elem_end,
+                                          nullptr, nullptr, (cudaStream_t)stream, value);
+  if (e == cudaErrorNotSupported)
+    return fail(FE_ERR_UNSUPPORTED, "eval mode not built for this form / order / dtype");
+  if (e != cudaSuccess) return cuda_fail(e, "fe_eval_scalar");
+  return ok();
+}
+
 fe_status fe_assemble_vector(const fe_mesh* mesh, int32_t dtype, int32_t ncomp, int64_t elem_begin,
                              int64_t elem_end, const void* r_elem, void* r_global, void* stream) {
   fe_status s = check_common(mesh, FE_FORM_DIFFUSION, elem_begin, elem_end);

@@ -59,7 +59,8 @@ cudaError_t launch_matrix_sf(const fe_mesh* m, int form, MatArgs mat, int64_t e0
                              double* K, cudaStream_t st);
 template <typename T>
 cudaError_t launch_residual_sf(const fe_mesh* m, int form, MatArgs mat, const T* u, int64_t e0,
-                               int64_t e1, T* r_elem, T* r_global, cudaStream_t st);
+                               int64_t e1, T* r_elem, T* r_global, cudaStream_t st,
+                               double* eval_out = nullptr);
 cudaError_t launch_matrix_sfv(const fe_mesh* m, int form, MatArgs mat, const double* state_u,
                               int64_t e0, int64_t e1, double* K, cudaStream_t st);
 cudaError_t upload_const_tables_matrix_v(int order, const double* b1, const double* d1,

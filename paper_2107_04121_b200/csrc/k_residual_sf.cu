@@ -79,7 +79,7 @@ template <int P, int FORM, typename T>
 __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
     k_residual_sf(MeshView mv, int mat_kind, const T* __restrict__ ma, const T* __restrict__ mb,
                   const T* __restrict__ u, int64_t e0, int64_t e1, T* __restrict__ r_elem,
-                  T* __restrict__ r_global) {
+                  T* __restrict__ r_global, double* __restrict__ eval_out) {
   using L = RSF<P, FORM, T>;
   constexpr int N1 = L::N1, Q1 = L::Q1, NB = L::NB, NQ = L::NQ, D = L::D, EB = L::EB;
   constexpr int Q2 = Q1 * Q1;
@@ -442,6 +442,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
         }
     }
     __syncthreads();
+    double ev = 0.0;  // eval mode: sum_k u_k r_k(u) of this column
     if (valid) {
 #pragma unroll
       for (int a = 0; a < D; ++a)
@@ -458,7 +459,13 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
           const int k = tx + N1 * ty + N1 * N1 * kz;
           if (r_elem) r_elem[(e - e0) * (int64_t)(D * NB) + a * NB + k] = v;
           if (r_global) atomicAdd(r_global + (int64_t)dcol[kz] * D + a, v);
+          if (eval_out) ev = fma((double)s, (double)uc[a][kz], ev);
         }
+    }
+    if (eval_out) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
+      if ((tid & 31) == 0 && ev != 0.0) atomicAdd(eval_out, ev);
     }
     gather_next(it + 1);
     __syncthreads();
@@ -472,7 +479,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
 
 template <int P, int FORM, typename T>
 static cudaError_t launch_rsf_t(const fe_mesh* mh, MatArgs mat, const T* u, int64_t e0, int64_t e1,
-                                T* r_elem, T* r_global, cudaStream_t st) {
+                                T* r_elem, T* r_global, double* eval_out, cudaStream_t st) {
   using L = RSF<P, FORM, T>;
   auto kern = k_residual_sf<P, FORM, T>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
@@ -486,25 +493,25 @@ static cudaError_t launch_rsf_t(const fe_mesh* mh, MatArgs mat, const T* u, int6
   const int grid = (int)((nbatch < (int64_t)nsm * per_sm) ? nbatch : (int64_t)nsm * per_sm);
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, L::THREADS, L::BYTES, st>>>(view_of(mh), mat.kind, (const T*)mat.a, (const T*)mat.b,
-                                           u, e0, e1, r_elem, r_global);
+                                           u, e0, e1, r_elem, r_global, eval_out);
   count_launch();
   return cudaGetLastError();
 }
 
 template <int P, typename T>
 static cudaError_t rsf_form(const fe_mesh* mh, int form, MatArgs mat, const T* u, int64_t e0,
-                            int64_t e1, T* re, T* rg, cudaStream_t st) {
+                            int64_t e1, T* re, T* rg, double* ev, cudaStream_t st) {
   switch (form) {
-    case FE_FORM_DIFFUSION: return launch_rsf_t<P, FE_FORM_DIFFUSION, T>(mh, mat, u, e0, e1, re, rg, st);
-    case FE_FORM_MASS: return launch_rsf_t<P, FE_FORM_MASS, T>(mh, mat, u, e0, e1, re, rg, st);
-    case FE_FORM_MASS_DIFFUSION: return launch_rsf_t<P, FE_FORM_MASS_DIFFUSION, T>(mh, mat, u, e0, e1, re, rg, st);
+    case FE_FORM_DIFFUSION: return launch_rsf_t<P, FE_FORM_DIFFUSION, T>(mh, mat, u, e0, e1, re, rg, ev, st);
+    case FE_FORM_MASS: return launch_rsf_t<P, FE_FORM_MASS, T>(mh, mat, u, e0, e1, re, rg, ev, st);
+    case FE_FORM_MASS_DIFFUSION: return launch_rsf_t<P, FE_FORM_MASS_DIFFUSION, T>(mh, mat, u, e0, e1, re, rg, ev, st);
     default: break;
   }
   if constexpr (sizeof(T) == 8) {
     switch (form) {
-      case FE_FORM_VECTOR_MASS: return launch_rsf_t<P, FE_FORM_VECTOR_MASS, T>(mh, mat, u, e0, e1, re, rg, st);
-      case FE_FORM_ELASTICITY: return launch_rsf_t<P, FE_FORM_ELASTICITY, T>(mh, mat, u, e0, e1, re, rg, st);
-      case FE_FORM_CONVECTIVE: return launch_rsf_t<P, FE_FORM_CONVECTIVE, T>(mh, mat, u, e0, e1, re, rg, st);
+      case FE_FORM_VECTOR_MASS: return launch_rsf_t<P, FE_FORM_VECTOR_MASS, T>(mh, mat, u, e0, e1, re, rg, ev, st);
+      case FE_FORM_ELASTICITY: return launch_rsf_t<P, FE_FORM_ELASTICITY, T>(mh, mat, u, e0, e1, re, rg, ev, st);
+      case FE_FORM_CONVECTIVE: return launch_rsf_t<P, FE_FORM_CONVECTIVE, T>(mh, mat, u, e0, e1, re, rg, ev, st);
       default: break;
     }
   }
@@ -513,20 +520,20 @@ static cudaError_t rsf_form(const fe_mesh* mh, int form, MatArgs mat, const T* u
 
 template <typename T>
 cudaError_t launch_residual_sf(const fe_mesh* mh, int form, MatArgs mat, const T* u, int64_t e0,
-                               int64_t e1, T* re, T* rg, cudaStream_t st) {
+                               int64_t e1, T* re, T* rg, cudaStream_t st, double* ev) {
   if (mh->q1d != mh->order + 1) return cudaErrorNotSupported;
   switch (mh->order) {
-    case 1: return rsf_form<1, T>(mh, form, mat, u, e0, e1, re, rg, st);
-    case 2: return rsf_form<2, T>(mh, form, mat, u, e0, e1, re, rg, st);
-    case 3: return rsf_form<3, T>(mh, form, mat, u, e0, e1, re, rg, st);
-    case 4: return rsf_form<4, T>(mh, form, mat, u, e0, e1, re, rg, st);
+    case 1: return rsf_form<1, T>(mh, form, mat, u, e0, e1, re, rg, ev, st);
+    case 2: return rsf_form<2, T>(mh, form, mat, u, e0, e1, re, rg, ev, st);
+    case 3: return rsf_form<3, T>(mh, form, mat, u, e0, e1, re, rg, ev, st);
+    case 4: return rsf_form<4, T>(mh, form, mat, u, e0, e1, re, rg, ev, st);
   }
   return cudaErrorNotSupported;
 }
 
 template cudaError_t launch_residual_sf<double>(const fe_mesh*, int, MatArgs, const double*, int64_t,
-                                                int64_t, double*, double*, cudaStream_t);
+                                                int64_t, double*, double*, cudaStream_t, double*);
 template cudaError_t launch_residual_sf<float>(const fe_mesh*, int, MatArgs, const float*, int64_t,
-                                               int64_t, float*, float*, cudaStream_t);
+                                               int64_t, float*, float*, cudaStream_t, double*);
 
 }  // namespace feb200

@@ -235,3 +235,17 @@ def test_config_full_size(name):
                                            dev(pr.mat_a, torch.float32),
                                            dev(pr.mat_b, torch.float32), want_elem=True)
         assert rel(r_glob32.cpu().numpy().ravel(), R_ref) <= TOL32
+
+
+@pytest.mark.parametrize("form,p", [(0, 1), (0, 2), (1, 2), (2, 2), (3, 4), (4, 2), (5, 2), (5, 1)])
+def test_eval_mode(form, p):
+    """'eval' mode vs the oracle's plain quadrature sum of F(u, u)."""
+    pr = fi.make_problem(form, p, (5, 3, 4), 5000 + form)
+    ref = oracle.problem_eval_scalar(pr)
+    mesh = gpu_mesh(pr)
+    v = mesh.eval_scalar(form, dev(pr.u), pr.mat_kind, dev(pr.mat_a), dev(pr.mat_b))
+    assert abs(v.item() - ref) <= TOL64 * abs(ref)
+    if form in (0, 3):
+        v32 = mesh.eval_scalar(form, dev(pr.u, torch.float32), pr.mat_kind,
+                               dev(pr.mat_a, torch.float32), dev(pr.mat_b, torch.float32))
+        assert abs(v32.item() - ref) <= TOL32 * abs(ref)

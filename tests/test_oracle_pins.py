@@ -550,3 +550,31 @@ def test_paper_worked_examples(row):
     else:
         K = oracle.eval_matrix(fi.ELASTICITY, p, q1d, c, conn, dc, fi.MAT_PER_ELEM, lam, mu)
     assert rel(K.reshape(res.shape), res) < 1e-13
+
+
+# ---------------------------------------------------------------- eval mode (N3)
+def test_eval_mode_closed_forms():
+    """'eval' mode pinned by closed forms on perturbed meshes:
+    int kappa |grad(a.x + b)|^2 = kappa |a|^2 vol, int rho 1 = rho vol, and the definition
+    u^T K u = sum_e u_e . r_e(u) for the bilinear forms."""
+    pr = fi.make_problem(fi.DIFFUSION, 2, (3, 2, 2), 19)
+    X = node_coords(pr)
+    a = np.array([0.4, -1.3, 0.8])
+    u = (X @ a + 0.7)[:, None]
+    kap = np.full((pr.n_elems, pr.nq), 1.5)
+    v = oracle.eval_scalar(fi.DIFFUSION, 2, 3, pr.coords, pr.conn, pr.dof_conn, u, 0, kap)
+    assert abs(v - 1.5 * a @ a) < 1e-13
+    rho = np.full((pr.n_elems, pr.nq), 2.5)
+    v = oracle.eval_scalar(fi.MASS, 2, 3, pr.coords, pr.conn, pr.dof_conn, np.ones_like(u), 0, rho)
+    assert abs(v - 2.5) < 1e-13
+
+
+@pytest.mark.parametrize("form,p", [(fi.DIFFUSION, 2), (fi.MASS_DIFFUSION, 2), (fi.ELASTICITY, 2),
+                                    (fi.VECTOR_MASS, 1), (fi.CONVECTIVE, 2)])
+def test_eval_mode_equals_u_dot_r(form, p):
+    pr = fi.make_problem(form, p, (2, 3, 2), 29)
+    v = oracle.problem_eval_scalar(pr)
+    r = oracle.problem_residual(pr)
+    ue = pr.u[pr.dof_conn].transpose(0, 2, 1).reshape(pr.n_elems, -1)
+    ref = float(np.sum(r * ue))
+    assert abs(v - ref) <= 1e-13 * max(abs(ref), 1e-300)
