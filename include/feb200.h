@@ -168,6 +168,36 @@ fe_status fe_assemble_vector(const fe_mesh *mesh, int32_t dtype, int32_t ncomp,
                              int64_t elem_begin, int64_t elem_end, const void *r_elem,
                              void *r_global, void *stream);
 
+/* ---- Global sparse matrix (CSR) assembly (the assembly the paper
+ * leaves to SfePy).  A CSR object holds the sparsity pattern of the
+ * global matrix for `ncomp` components per node with the interleaved numbering
+ * dof = node * ncomp + a (Eq. fe1c); rows are sorted by column.  It keeps a
+ * pointer to `mesh`, which must outlive it. */
+typedef struct fe_csr fe_csr;
+
+/* Build the pattern on the GPU (SYNCHRONOUS on `stream`): node pairs of every
+ * cell, sort + unique, row pointers, and a cell-to-position map for assembly.
+ * ncomp in {1, 3}.  Memory: ~12 B per (cell, node, node) pair during setup. */
+fe_status fe_create_csr(const fe_mesh *mesh, int32_t ncomp, void *stream, fe_csr **out);
+
+/* n_rows = n_nodes * ncomp; nnz = number of stored entries. Either pointer may be NULL. */
+fe_status fe_csr_info(const fe_csr *csr, int64_t *n_rows, int64_t *nnz);
+
+/* Device arrays owned by the CSR object: row_ptr[n_rows + 1] (int64), col_idx[nnz] (int32). */
+fe_status fe_csr_arrays(const fe_csr *csr, const int64_t **row_ptr, const int32_t **col_idx);
+
+/* Copy the pattern into caller buffers (device or host) on `stream` (asynchronous). */
+fe_status fe_csr_copy_arrays(const fe_csr *csr, int64_t *row_ptr, int32_t *col_idx, void *stream);
+
+/* values[nnz] (fp64, device) += the element matrices K[e - elem_begin][ndof][ndof] of
+ * cells [elem_begin, elem_end) (the layout fe_eval_element_matrices writes), with
+ * fp atomics: the caller zeroes `values`; summation order is run-dependent. */
+fe_status fe_assemble_matrix(const fe_csr *csr, const double *K, int64_t elem_begin,
+                             int64_t elem_end, double *values, void *stream);
+
+/* Release the CSR object (synchronises the device).  NULL is a no-op. */
+fe_status fe_destroy_csr(fe_csr *csr);
+
 /* Test mode: materialise the geometry of step a1 (fp64):
  *   detw[E][n_q] = w_q det J,  jinv[E][n_q][3][3] = J^-1 (row-major).
  * Either pointer may be NULL. */

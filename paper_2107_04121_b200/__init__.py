@@ -64,13 +64,21 @@ def _load():
                                      P, P]
     lib.fe_assemble_vector.argtypes = [P, i32, i32, i64, i64, P, P, P]
     lib.fe_eval_scalar.argtypes = [P, i32, i32, ctypes.POINTER(fe_material), P, i64, i64, P, P]
+    lib.fe_create_csr.argtypes = [P, i32, P, ctypes.POINTER(P)]
+    lib.fe_csr_info.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    lib.fe_csr_arrays.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P)]
+    lib.fe_csr_copy_arrays.argtypes = [P, P, P, P]
+    lib.fe_assemble_matrix.argtypes = [P, P, i64, i64, P, P]
+    lib.fe_destroy_csr.argtypes = [P]
     lib.fe_geometry.argtypes = [P, P, P, P]
     lib.fe_last_error.restype = ctypes.c_char_p
     lib.fe_last_error_element.restype = i64
     lib.fe_launch_count.restype = i64
     for f in ("fe_create_mesh_geometry", "fe_destroy_mesh", "fe_mesh_info",
               "fe_eval_element_matrices", "fe_eval_residual", "fe_assemble_vector",
-              "fe_geometry", "fe_eval_scalar"):
+              "fe_geometry", "fe_eval_scalar", "fe_create_csr", "fe_csr_info", "fe_csr_arrays",
+              "fe_csr_copy_arrays",
+              "fe_assemble_matrix", "fe_destroy_csr"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -91,7 +99,9 @@ class _LazyLib:
 _lib = _LazyLib()
 ABI_SYMBOLS = ("fe_create_mesh_geometry", "fe_destroy_mesh", "fe_mesh_info",
                "fe_eval_element_matrices", "fe_eval_residual", "fe_assemble_vector", "fe_eval_scalar",
-               "fe_geometry", "fe_last_error", "fe_last_error_element", "fe_launch_count")
+               "fe_geometry", "fe_last_error", "fe_last_error_element", "fe_launch_count",
+               "fe_create_csr", "fe_csr_info", "fe_csr_arrays", "fe_csr_copy_arrays",
+               "fe_assemble_matrix", "fe_destroy_csr")
 
 
 def lib():
@@ -199,6 +209,45 @@ def fe_eval_scalar(handle: int, form: int, dtype: int, mat_kind: int,
 def fe_geometry(handle: int, detw: Optional[torch.Tensor], jinv: Optional[torch.Tensor],
                 stream=None):
     _check(_lib.fe_geometry(handle, _ptr(detw), _ptr(jinv), _stream(stream)))
+
+
+class CSR:
+    """Global sparse matrix pattern (fe_create_csr) and assembly (fe_assemble_matrix)."""
+
+    def __init__(self, mesh: "Mesh", ncomp: int, stream=None):
+        out = ctypes.c_void_p()
+        _check(_lib.fe_create_csr(mesh.handle, ncomp, _stream(stream), ctypes.byref(out)))
+        self.handle, self.mesh, self.ncomp = out.value, mesh, ncomp
+        nr, nz = ctypes.c_int64(), ctypes.c_int64()
+        _check(_lib.fe_csr_info(self.handle, ctypes.byref(nr), ctypes.byref(nz)))
+        self.n_rows, self.nnz = nr.value, nz.value
+
+    def arrays(self):
+        """(row_ptr int64 [n_rows+1], col_idx int32 [nnz]) copied to host numpy arrays."""
+        import numpy as np
+        row_ptr = torch.empty(self.n_rows + 1, dtype=torch.int64, device=self.mesh.device)
+        col = torch.empty(self.nnz, dtype=torch.int32, device=self.mesh.device)
+        _check(_lib.fe_csr_copy_arrays(self.handle, _ptr(row_ptr), _ptr(col), _stream(None)))
+        return row_ptr.cpu().numpy(), col.cpu().numpy().astype(np.int64)
+
+    def assemble(self, K, elem_begin=0, elem_end=None, values=None, stream=None):
+        elem_end = self.mesh.n_elems if elem_end is None else elem_end
+        if values is None:
+            values = torch.zeros(self.nnz, dtype=torch.float64, device=self.mesh.device)
+        _check(_lib.fe_assemble_matrix(self.handle, _ptr(K), elem_begin, elem_end, _ptr(values),
+                                       _stream(stream)))
+        return values
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _check(_lib.fe_destroy_csr(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Mesh:

@@ -89,6 +89,14 @@ fe_status check_material(int form, const fe_material* mat) {
 
 }  // namespace
 
+namespace feb200 {
+// error setter shared with the other ABI units (k_csr.cu)
+fe_status set_error(fe_status s, const char* msg) {
+  if (s == FE_OK) return ok();
+  return fail(s, msg);
+}
+}  // namespace feb200
+
 extern "C" {
 
 const char* fe_last_error(void) { return g_err.c_str(); }

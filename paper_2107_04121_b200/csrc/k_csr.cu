@@ -1,0 +1,245 @@
+// Global sparse (CSR) matrix assembly from element matrices -- SURVEY 8(f) N2,
+// "the step after matrix mode" (the paper leaves it to SfePy and times it only
+// in the FEniCS comparison).
+//
+// Pattern (setup, once per mesh and component count): every (cell, k, l) node
+// pair becomes a key row * n_nodes + col; sort + unique on the GPU gives the
+// scalar node-to-node pattern, row pointers come from a vectorised lower_bound,
+// and a per-(cell, k, l) map stores the column's index inside its row.  Vector
+// fields (D = 3) use the interleaved global numbering of Eq. fe1c (dof = node D +
+// a), so every node pair expands to a D x D block laid out row by row:
+//   row (r, a) starts at D^2 rowptr_node[r] + a D n_r,  column (c, b) is at
+//   idx_in_row(r, c) D + b.
+// Assembly: values[pos(e, a k, b l)] += K_e[a k][b l] with fp64 atomics
+// (atomic order is the only run-to-run difference, as for the residual).
+#include <exception>
+#include <new>
+#include <string>
+
+#include <thrust/binary_search.h>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
+#include <thrust/device_ptr.h>
+#include <thrust/execution_policy.h>
+#include <thrust/sort.h>
+#include <thrust/unique.h>
+
+#include "fe_internal.h"
+
+struct fe_csr {
+  const fe_mesh* mesh = nullptr;
+  int32_t ncomp = 1;
+  int64_t n_nodes = 0, nnz_node = 0;
+  int64_t* rowptr_node = nullptr;   // [n_nodes + 1] scalar node pattern
+  int32_t* col_node = nullptr;      // [nnz_node]
+  int32_t* pos_in_row = nullptr;    // [E][nb][nb] index of column node l inside row node k
+  int64_t* rowptr = nullptr;        // [n_nodes D + 1] expanded pattern
+  int32_t* col = nullptr;           // [nnz_node D^2]
+};
+
+namespace feb200 {
+
+struct RowKey {
+  int64_t n;
+  __host__ __device__ int64_t operator()(int64_t r) const { return r * n; }
+};
+
+__global__ void k_pair_keys(const int32_t* __restrict__ dc, int nb, int64_t E, int64_t n_nodes,
+                            int64_t* __restrict__ keys) {
+  const int64_t n = E * nb * nb;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i / (nb * nb);
+    const int r = (int)(i - e * nb * nb), k = r / nb, l = r - k * nb;
+    keys[i] = (int64_t)dc[e * nb + k] * n_nodes + dc[e * nb + l];
+  }
+}
+
+__global__ void k_cols(const int64_t* __restrict__ keys, int64_t nnz, int64_t n_nodes, int32_t* __restrict__ col) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x)
+    col[i] = (int32_t)(keys[i] % n_nodes);
+}
+
+__global__ void k_pos_map(const int32_t* __restrict__ dc, int nb, int64_t E, const int64_t* __restrict__ rowptr,
+                          const int32_t* __restrict__ col, int32_t* __restrict__ pos) {
+  const int64_t n = E * nb * nb;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i / (nb * nb);
+    const int r = (int)(i - e * nb * nb), k = r / nb, l = r - k * nb;
+    const int32_t row = dc[e * nb + k], c = dc[e * nb + l];
+    int64_t lo = rowptr[row], hi = rowptr[row + 1];
+    const int64_t base = lo;
+    while (lo < hi) {  // binary search of c in the sorted row
+      const int64_t mid = (lo + hi) >> 1;
+      if (col[mid] < c) lo = mid + 1; else hi = mid;
+    }
+    pos[i] = (int32_t)(lo - base);
+  }
+}
+
+// expanded (vector) pattern: rowptr[r D + a] = D^2 rowptr_node[r] + a D n_r
+__global__ void k_expand(const int64_t* __restrict__ rpn, const int32_t* __restrict__ cn, int64_t n_nodes, int D,
+                         int64_t* __restrict__ rowptr, int32_t* __restrict__ col) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_nodes; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b0 = rpn[r], nr = rpn[r + 1] - b0;
+    for (int a = 0; a < D; ++a) {
+      const int64_t rs = (int64_t)D * D * b0 + (int64_t)a * D * nr;
+      rowptr[r * D + a] = rs;
+      for (int64_t j = 0; j < nr; ++j)
+        for (int b = 0; b < D; ++b) col[rs + j * D + b] = cn[b0 + j] * D + b;
+    }
+    if (r == n_nodes - 1) rowptr[n_nodes * D] = (int64_t)D * D * rpn[n_nodes];
+  }
+}
+
+// values[pos] += K[e - e0][a nb + k][b nb + l]
+__global__ void __launch_bounds__(256) k_assemble_matrix(const int32_t* __restrict__ dc, int nb, int D,
+                                                         int64_t e0, int64_t e1,
+                                                         const int64_t* __restrict__ rpn,
+                                                         const int32_t* __restrict__ pos,
+                                                         const double* __restrict__ K,
+                                                         double* __restrict__ values) {
+  const int nd = D * nb;
+  const int64_t n = (e1 - e0) * nd * nd;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t el = i / (nd * nd);
+    const int rr = (int)(i - el * nd * nd), row = rr / nd, cl = rr - row * nd;
+    const int a = row / nb, k = row - a * nb, b = cl / nb, l = cl - b * nb;
+    const int64_t e = e0 + el;
+    const int32_t rn = dc[e * nb + k];
+    const int64_t b0 = rpn[rn], nr = rpn[rn + 1] - b0;
+    const int64_t p = (int64_t)D * D * b0 + (int64_t)a * D * nr +
+                      (int64_t)pos[(e * nb + k) * nb + l] * D + b;
+    atomicAdd(values + p, K[i]);
+  }
+}
+
+}  // namespace feb200
+
+namespace feb200 {
+fe_status set_error(fe_status s, const char* msg);
+}
+
+extern "C" {
+
+static void free_csr(fe_csr* c) {
+  if (!c) return;
+  void* p[] = {c->rowptr_node, c->col_node, c->pos_in_row, c->rowptr, c->col};
+  for (void* q : p)
+    if (q) cudaFree(q);
+  delete c;
+}
+
+static fe_status create_csr_impl(const fe_mesh* mesh, int32_t ncomp, void* stream, fe_csr** out);
+
+fe_status fe_create_csr(const fe_mesh* mesh, int32_t ncomp, void* stream, fe_csr** out) {
+  try {  // thrust reports failures with exceptions; none may cross the ABI
+    return create_csr_impl(mesh, ncomp, stream, out);
+  } catch (const std::bad_alloc&) {
+    return feb200::set_error(FE_ERR_OOM, "fe_create_csr: out of memory in sort");
+  } catch (const std::exception& ex) {
+    return feb200::set_error(FE_ERR_CUDA, ex.what());
+  } catch (...) {
+    return feb200::set_error(FE_ERR_CUDA, "fe_create_csr: unknown failure");
+  }
+}
+
+static fe_status create_csr_impl(const fe_mesh* mesh, int32_t ncomp, void* stream, fe_csr** out) {
+  if (!mesh || !out || (ncomp != 1 && ncomp != 3))
+    return feb200::set_error(FE_ERR_INVALID_ARG, "fe_create_csr: NULL argument or ncomp not in {1, 3}");
+  *out = nullptr;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nb = mesh->nb;
+  const int64_t E = mesh->n_elems, N = mesh->n_nodes, npairs = E * nb * nb;
+  if (N * ncomp >= (int64_t(1) << 31) || npairs <= 0)
+    return feb200::set_error(FE_ERR_UNSUPPORTED, "fe_create_csr: empty mesh or > 2^31 rows");
+  fe_csr* c = new fe_csr();
+  c->mesh = mesh;
+  c->ncomp = ncomp;
+  c->n_nodes = N;
+  int64_t* keys = nullptr;
+  cudaError_t e = cudaMalloc(&keys, sizeof(int64_t) * npairs);
+  if (e != cudaSuccess) { free_csr(c); return feb200::set_error(FE_ERR_OOM, "fe_create_csr: keys"); }
+  const int grid = 148 * 16;
+  feb200::k_pair_keys<<<grid, 256, 0, st>>>(mesh->dof_conn, nb, E, N, keys);
+  feb200::count_launch();
+  auto pol = thrust::cuda::par.on(st);
+  thrust::device_ptr<int64_t> kp(keys);
+  thrust::sort(pol, kp, kp + npairs);
+  const int64_t nnz = thrust::unique(pol, kp, kp + npairs) - kp;
+  c->nnz_node = nnz;
+  e = cudaMalloc(&c->rowptr_node, sizeof(int64_t) * (N + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&c->col_node, sizeof(int32_t) * nnz);
+  if (e == cudaSuccess) e = cudaMalloc(&c->pos_in_row, sizeof(int32_t) * npairs);
+  if (e != cudaSuccess) { cudaFree(keys); free_csr(c); return feb200::set_error(FE_ERR_OOM, "fe_create_csr: pattern"); }
+  // rowptr_node[r] = first key >= r * N
+  thrust::device_ptr<int64_t> rp(c->rowptr_node);
+  auto row_keys = thrust::make_transform_iterator(thrust::make_counting_iterator<int64_t>(0),
+                                                  feb200::RowKey{N});
+  thrust::lower_bound(pol, kp, kp + nnz, row_keys, row_keys + N + 1, rp);
+  feb200::k_cols<<<grid, 256, 0, st>>>(keys, nnz, N, c->col_node);
+  feb200::k_pos_map<<<grid, 256, 0, st>>>(mesh->dof_conn, nb, E, c->rowptr_node, c->col_node, c->pos_in_row);
+  feb200::count_launch();
+  feb200::count_launch();
+  e = cudaMalloc(&c->rowptr, sizeof(int64_t) * (N * ncomp + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&c->col, sizeof(int32_t) * nnz * ncomp * ncomp);
+  if (e != cudaSuccess) { cudaFree(keys); free_csr(c); return feb200::set_error(FE_ERR_OOM, "fe_create_csr: expanded pattern"); }
+  feb200::k_expand<<<grid, 256, 0, st>>>(c->rowptr_node, c->col_node, N, ncomp, c->rowptr, c->col);
+  feb200::count_launch();
+  e = cudaStreamSynchronize(st);
+  cudaFree(keys);
+  if (e != cudaSuccess) { free_csr(c); return feb200::set_error(FE_ERR_CUDA, cudaGetErrorString(e)); }
+  *out = c;
+  return feb200::set_error(FE_OK, "");
+}
+
+fe_status fe_csr_info(const fe_csr* csr, int64_t* n_rows, int64_t* nnz) {
+  if (!csr) return feb200::set_error(FE_ERR_INVALID_ARG, "csr is NULL");
+  if (n_rows) *n_rows = csr->n_nodes * csr->ncomp;
+  if (nnz) *nnz = csr->nnz_node * csr->ncomp * csr->ncomp;
+  return FE_OK;
+}
+
+fe_status fe_csr_arrays(const fe_csr* csr, const int64_t** row_ptr, const int32_t** col_idx) {
+  if (!csr) return feb200::set_error(FE_ERR_INVALID_ARG, "csr is NULL");
+  if (row_ptr) *row_ptr = csr->rowptr;
+  if (col_idx) *col_idx = csr->col;
+  return FE_OK;
+}
+
+fe_status fe_csr_copy_arrays(const fe_csr* csr, int64_t* row_ptr, int32_t* col_idx, void* stream) {
+  if (!csr) return feb200::set_error(FE_ERR_INVALID_ARG, "csr is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  const int64_t nr = csr->n_nodes * csr->ncomp, nz = csr->nnz_node * csr->ncomp * csr->ncomp;
+  if (row_ptr) e = cudaMemcpyAsync(row_ptr, csr->rowptr, sizeof(int64_t) * (nr + 1), cudaMemcpyDefault, st);
+  if (e == cudaSuccess && col_idx) e = cudaMemcpyAsync(col_idx, csr->col, sizeof(int32_t) * nz, cudaMemcpyDefault, st);
+  return e == cudaSuccess ? feb200::set_error(FE_OK, "") : feb200::set_error(FE_ERR_CUDA, cudaGetErrorString(e));
+}
+
+fe_status fe_assemble_matrix(const fe_csr* csr, const double* K, int64_t elem_begin, int64_t elem_end,
+                             double* values, void* stream) {
+  if (!csr || (!K && elem_end > elem_begin) || !values)
+    return feb200::set_error(FE_ERR_INVALID_ARG, "fe_assemble_matrix: NULL argument");
+  if (elem_begin < 0 || elem_end > csr->mesh->n_elems || elem_begin > elem_end)
+    return feb200::set_error(FE_ERR_INVALID_ARG, "fe_assemble_matrix: bad element range");
+  const int nd = csr->ncomp * csr->mesh->nb;
+  const int64_t n = (elem_end - elem_begin) * nd * nd;
+  if (n == 0) return FE_OK;
+  const int grid = (int)((n + 255) / 256 < 148 * 32 ? (n + 255) / 256 : 148 * 32);
+  feb200::k_assemble_matrix<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      csr->mesh->dof_conn, csr->mesh->nb, csr->ncomp, elem_begin, elem_end, csr->rowptr_node,
+      csr->pos_in_row, K, values);
+  feb200::count_launch();
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? feb200::set_error(FE_OK, "") : feb200::set_error(FE_ERR_CUDA, cudaGetErrorString(e));
+}
+
+fe_status fe_destroy_csr(fe_csr* csr) {
+  if (csr) {
+    cudaDeviceSynchronize();
+    free_csr(csr);
+  }
+  return FE_OK;
+}
+
+}  // extern "C"

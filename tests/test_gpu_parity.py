@@ -249,3 +249,61 @@ def test_eval_mode(form, p):
         v32 = mesh.eval_scalar(form, dev(pr.u, torch.float32), pr.mat_kind,
                                dev(pr.mat_a, torch.float32), dev(pr.mat_b, torch.float32))
         assert abs(v32.item() - ref) <= TOL32 * abs(ref)
+
+
+def _dense_global(pr, K):
+    """Reference global matrix: plain scatter of element matrices (test infrastructure)."""
+    D, nb = pr.ncomp, pr.nb
+    n = pr.n_nodes * D
+    A = np.zeros((n, n))
+    dofs = (pr.dof_conn[:, None, :] * D + np.arange(D)[None, :, None]).reshape(pr.n_elems, D * nb)
+    for e in range(pr.n_elems):
+        A[np.ix_(dofs[e], dofs[e])] += K[e]
+    return A
+
+
+@pytest.mark.parametrize("form,p", [(0, 1), (0, 2), (3, 2), (4, 1), (4, 2), (5, 2)])
+def test_csr_assembly(form, p):
+    """N2: CSR pattern + assembly of the GPU element matrices == dense scatter of the
+    oracle's element matrices (pattern = every node pair sharing a cell)."""
+    import scipy.sparse as sp
+    m = fe()
+    pr = fi.make_problem(form, p, (3, 2, 3), 6000 + form)
+    mesh = gpu_mesh(pr)
+    K = mesh.element_matrices(form, pr.mat_kind, dev(pr.mat_a), dev(pr.mat_b),
+                              dev(pr.u) if form == fi.CONVECTIVE else None)
+    csr = m.CSR(mesh, pr.ncomp)
+    vals = csr.assemble(K)
+    rp, ci = csr.arrays()
+    assert rp[0] == 0 and rp[-1] == csr.nnz and np.all(np.diff(rp) > 0)
+    for r in range(csr.n_rows):  # sorted, unique columns per row
+        c = ci[rp[r]:rp[r + 1]]
+        assert np.all(np.diff(c) > 0)
+    A = sp.csr_matrix((vals.cpu().numpy(), ci, rp), shape=(csr.n_rows, csr.n_rows)).toarray()
+    Aref = _dense_global(pr, oracle.problem_matrix(pr))
+    assert rel(A, Aref) <= TOL64
+    # structural: the pattern is exactly the set of node pairs sharing a cell
+    S = _dense_global(pr, np.ones_like(K.cpu().numpy())) != 0
+    pattern = sp.csr_matrix((np.ones(csr.nnz), ci, rp), shape=A.shape).toarray() != 0
+    assert np.array_equal(pattern, S)
+
+
+def test_csr_full_size_c2():
+    """C2 at full size: nnz of the Q2 lattice pattern and row sums of the assembled
+    diffusion matrix (= 0 by partition of unity, P7)."""
+    m = fe()
+    pr = fi.make_config("C2")
+    mesh = gpu_mesh(pr)
+    K = mesh.element_matrices(fi.DIFFUSION, pr.mat_kind, dev(pr.mat_a))
+    csr = m.CSR(mesh, 1)
+    vals = csr.assemble(K)
+    rp, ci = csr.arrays()
+    # exact count: a node couples to the lattice nodes of all cells containing it
+    M = 2 * 64 + 1
+    idx = np.arange(M)
+    span = np.where(idx % 2 == 0, np.minimum(idx + 2, M - 1) - np.maximum(idx - 2, 0) + 1, 3)
+    assert csr.nnz == int(span.sum()) ** 3
+    import scipy.sparse as sp
+    A = sp.csr_matrix((vals.cpu().numpy(), ci, rp), shape=(csr.n_rows, csr.n_rows))
+    rs = np.abs(A @ np.ones(csr.n_rows))
+    assert rs.max() <= 1e-12 * np.abs(vals.cpu().numpy()).max()
