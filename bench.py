@@ -42,6 +42,8 @@ GEOM = 120
 
 
 def alg_flops(form: int, mode: str, nb: int, nq: int) -> float:
+    if mode == "csr":
+        return (fi.FORM_NCOMP[form] * nb) ** 2  # one add per element-matrix entry
     if mode == "matrix":
         per_qp = {fi.DIFFUSION: 6 * nb * nb + 21 * nb, fi.MASS: 2 * nb * nb + nb,
                   fi.MASS_DIFFUSION: 8 * nb * nb + 22 * nb,
@@ -91,6 +93,10 @@ def uses_sf_matrix(form: int, p: int) -> bool:
 
 def alg_bytes(form: int, mode: str, p: int, nb: int, nq: int, D: int, mat_kind: int,
               esize: int = 8) -> float:
+    if mode == "csr":
+        # read K_e and the position map, one fp64 read-modify-write per K entry (atomics in L2;
+        # the unique global entries are counted by the caller's traffic measurement)
+        return (D * nb) ** 2 * 8 + nb * nb * 4 + 4 * nb
     if form == fi.ELASTICITY:
         mat = 2 * esize if mat_kind == fi.MAT_PER_ELEM else 2 * nq * esize
     elif form == fi.MASS_DIFFUSION:
@@ -137,12 +143,16 @@ WORKLOADS = {
     "C4": dict(modes=("residual",)),
     "C5": dict(modes=("residual",)),
     "C5t": dict(modes=("matrix",)),
+    "C2csr": dict(modes=("matrix", "csr")),   # N2: element matrices + global CSR assembly
+    "C3csr": dict(modes=("matrix", "csr")),
 }
 
 
 def build_problem(name):
     if name == "C5t":
         return fi.corner_subproblem(fi.make_config("C5"), 64)
+    if name.endswith("csr"):
+        return fi.make_config(name[:-3])
     return fi.make_config(name)
 
 
@@ -336,6 +346,8 @@ def main():
     u = torch.from_numpy(u_loc).to(dev, tdt)
     K = torch.empty((El, D * nb, D * nb), dtype=torch.float64, device=dev) if "matrix" in modes else None
     r = torch.zeros((sl.n_nodes, D), dtype=tdt, device=dev)
+    csr = fe.CSR(mesh, D) if "csr" in modes else None
+    csr_vals = torch.zeros(csr.nnz, dtype=torch.float64, device=dev) if csr is not None else None
     stream = torch.cuda.current_stream(dev)
     comm_stream = torch.cuda.Stream(dev) if world > 1 else None
     bufs = [None]
@@ -349,6 +361,13 @@ def main():
                                         u if prob.form == fi.CONVECTIVE else None, 0, El, K, stream)
             if record:
                 b = torch.cuda.Event(enable_timing=True); b.record(stream); ev["matrix"].append((a, b))
+        if "csr" in modes:
+            csr_vals.zero_()
+            if record:
+                a = torch.cuda.Event(enable_timing=True); a.record(stream)
+            csr.assemble(K, values=csr_vals, stream=stream)
+            if record:
+                b = torch.cuda.Event(enable_timing=True); b.record(stream); ev["csr"].append((a, b))
         if "residual" in modes:
             r.zero_()
             if record:
@@ -447,58 +466,65 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel
-    dom = max(modes, key=lambda m: kern_ms[m])
+    # ---- roofline of every kernel of the step; the dominant one is the headline
     esize = 8 if args.dtype == "f64" else 4
-    fl_lean = alg_flops(prob.form, dom, nb, nq) * El
-    if dom == "matrix":
-        sf = uses_sf_matrix(prob.form, prob.p) or (
-            prob.form in (fi.ELASTICITY, fi.CONVECTIVE, fi.VECTOR_MASS) and prob.p <= 2
-            and os.environ.get("FEB200_MATRIX_IMPL", "") != "dense")
-    else:
-        sf = uses_sf_residual(prob.p)
-    impl = "sum-factorised" if sf else "dense-table"
-    if not sf:
-        fl = fl_lean
-    elif dom == "matrix" and uses_sf_matrix(prob.form, prob.p):
-        fl = sf_matrix_flops(prob.form, prob.p) * El
-    elif dom == "matrix":
-        fl = fl_lean  # vector SF matrix kernels: flop count not modelled, lean dense count reported
-    else:
-        fl = sf_residual_flops(prob.form, prob.p) * El
-    by = alg_bytes(prob.form, dom, prob.p, nb, nq, D, prob.mat_kind, esize) * El
-    t_s = kern_ms[dom] * 1e-3
     pk_b, src_b = hbm_peak_gbs()
-    if args.dtype == "f32":
-        pk_f, src_f, fbound = 74.4, "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz", "alu"
-    elif impl == "sum-factorised":
-        pk_f, src_f = fp64_peak_tflops("dfma_tflops_sustained")
-        fbound = "alu"
-    else:
-        pk_f, src_f = fp64_peak_tflops("dmma_m16n8k4_tflops_sustained")
-        fbound = "tensor"
-    t_flop = fl / (pk_f * 1e12)
-    t_mem = by / (pk_b * 1e9)
-    if t_flop >= t_mem:
-        roof = {"bound": fbound, "achieved": fl / t_s / 1e12, "peak": pk_f, "unit": "TFLOP/s",
-                "frac": (fl / t_s / 1e12) / pk_f, "peak_source": src_f}
-    else:
-        roof = {"bound": "hbm", "achieved": by / t_s / 1e9, "peak": pk_b, "unit": "GB/s",
-                "frac": (by / t_s / 1e9) / pk_b, "peak_source": src_b}
-    roof.update({"kernel": f"{dom} ({fi.FORM_NAMES[prob.form]}, Q{prob.p}, {impl})",
-                 "lean_dense_flops_per_cell": fl_lean / El,
-                 "effective_lean_tflops": fl_lean / t_s / 1e12,
-                 "kernel_ms": kern_ms[dom], "alg_flops_per_cell": fl / El,
-                 "alg_bytes_per_cell": by / El, "cells_per_launch": El,
-                 "achieved_gbs": by / t_s / 1e9, "achieved_tflops": fl / t_s / 1e12,
-                 "traffic": None})
-    prof = os.path.join(ROOT, "profiles", f"traffic_{cfg}_{dom}.json")
-    if os.path.exists(prof):
-        try:
-            roof["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
-        except Exception:
-            pass
 
+    def roofline_for(mode):
+        fl_lean = alg_flops(prob.form, mode, nb, nq) * El
+        if mode == "matrix":
+            sf = uses_sf_matrix(prob.form, prob.p) or (
+                prob.form in (fi.ELASTICITY, fi.CONVECTIVE, fi.VECTOR_MASS) and prob.p <= 2
+                and os.environ.get("FEB200_MATRIX_IMPL", "") != "dense")
+        elif mode == "residual":
+            sf = uses_sf_residual(prob.p)
+        else:
+            sf = False
+        impl = "atomic-scatter" if mode == "csr" else ("sum-factorised" if sf else "dense-table")
+        if not sf:
+            fl = fl_lean
+        elif mode == "matrix" and uses_sf_matrix(prob.form, prob.p):
+            fl = sf_matrix_flops(prob.form, prob.p) * El
+        elif mode == "matrix":
+            fl = fl_lean  # vector SF matrix kernels: flop count not modelled, lean dense count reported
+        else:
+            fl = sf_residual_flops(prob.form, prob.p) * El
+        by = alg_bytes(prob.form, mode, prob.p, nb, nq, D, prob.mat_kind, esize) * El
+        t_s = kern_ms[mode] * 1e-3
+        if args.dtype == "f32":
+            pk_f, src_f, fbound = 74.4, "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz", "alu"
+        elif impl == "sum-factorised" or mode == "csr":
+            pk_f, src_f = fp64_peak_tflops("dfma_tflops_sustained")
+            fbound = "alu"
+        else:
+            pk_f, src_f = fp64_peak_tflops("dmma_m16n8k4_tflops_sustained")
+            fbound = "tensor"
+        t_flop = fl / (pk_f * 1e12)
+        t_mem = by / (pk_b * 1e9)
+        if t_flop >= t_mem:
+            rf = {"bound": fbound, "achieved": fl / t_s / 1e12, "peak": pk_f, "unit": "TFLOP/s",
+                  "frac": (fl / t_s / 1e12) / pk_f, "peak_source": src_f}
+        else:
+            rf = {"bound": "hbm", "achieved": by / t_s / 1e9, "peak": pk_b, "unit": "GB/s",
+                  "frac": (by / t_s / 1e9) / pk_b, "peak_source": src_b}
+        rf.update({"kernel": f"{mode} ({fi.FORM_NAMES[prob.form]}, Q{prob.p}, {impl})",
+                   "lean_dense_flops_per_cell": fl_lean / El,
+                   "effective_lean_tflops": fl_lean / t_s / 1e12,
+                   "kernel_ms": kern_ms[mode], "alg_flops_per_cell": fl / El,
+                   "alg_bytes_per_cell": by / El, "cells_per_launch": El,
+                   "achieved_gbs": by / t_s / 1e9, "achieved_tflops": fl / t_s / 1e12,
+                   "traffic": None})
+        prof_ = os.path.join(ROOT, "profiles", f"traffic_{cfg}_{mode}.json")
+        if os.path.exists(prof_):
+            try:
+                rf["traffic"] = json.load(open(prof_)).get("dram_bytes_per_launch")
+            except Exception:
+                pass
+        return rf
+
+    dom = max(modes, key=lambda m: kern_ms[m])
+    rooflines = {m: roofline_for(m) for m in modes}
+    roof = rooflines[dom]
     cb = None
     if not args.no_cpu_baseline and world == 1:
         cb = cpu_baseline(prob, modes)
@@ -512,7 +538,8 @@ def main():
                    "order": prob.p, "q1d": prob.q1d, "form": fi.FORM_NAMES[prob.form],
                    "modes": list(modes), "parallelism": f"z-slabs x{world}",
                    "l2": "no flush: every step writes/reads > L2 (C2 K = 1.53 GB)"},
-        "modes": {m: {"kernel_ms": kern_ms[m], "cells_per_s": El / (kern_ms[m] * 1e-3)}
+        "modes": {m: {"kernel_ms": kern_ms[m], "cells_per_s": El / (kern_ms[m] * 1e-3),
+                      "roofline": {k: rooflines[m][k] for k in ("bound", "achieved", "unit", "frac")}}
                   for m in modes},
         "roofline": roof,
         "cpu_baseline": cb,
