@@ -22,9 +22,20 @@
 #ifndef FEB200_SF_E2
 #define FEB200_SF_E2 2
 #endif
+#ifndef FEB200_SFP_E2
+#define FEB200_SFP_E2 8
+#endif
+#ifndef FEB200_SFP
+#define FEB200_SFP 1
+#endif
+#ifndef FEB200_SF_MINB
+#define FEB200_SF_MINB 1
+#endif
 #include "fe_const.cuh"
 #include "fe_device.cuh"
 #include "fe_internal.h"
+#include <cstdlib>
+#include <cstring>
 
 namespace feb200 {
 
@@ -85,7 +96,7 @@ __device__ __forceinline__ void hex_edge(int e, int& v0, int& v1) {
 }
 
 template <int P, int FORM>
-__global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_DIFFUSION>::THREADS)
+__global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_DIFFUSION>::THREADS, FEB200_SF_MINB)
     k_matrix_sf(MeshView mv, const double* __restrict__ ma, const double* __restrict__ mb,
                 int64_t e0, int64_t e1, double* __restrict__ K) {
   constexpr bool DIFF = FORM != FE_FORM_MASS, MASS = FORM != FE_FORM_DIFFUSION;
@@ -357,6 +368,401 @@ __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_D
 #undef Bt
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised pipelined variant (P = 1, 2): the same three contraction
+// stages, but run by three groups of warps on different cell batches at once,
+// handing data over through shared-memory rings guarded by mbarriers instead
+// of CTA-wide barriers (one persistent CTA per SM):
+//   L (1 warp)   : gathers the batch's vertex coordinates and coefficients
+//                  into ring slot L[it % 2]                     (loads)
+//   G (NG warps) : one thread per (cell, qx, qy) column: geometry at its Q1
+//                  qps (a1) -> W^{mn} in registers -> stage z
+//                  for all unique pairs -> T1 ring slot [it % 2]
+//   X (NX warps) : one thread per (cell, z-pair, y-pair): stages y and x
+//                  (b, c1) -> K staging slot [it % 2] -> one TMA bulk store
+// The geometry + stage-z thread uses compile-time pair indices, so every 1D
+// table operand is a constant-bank operand.
+template <int P>
+struct SFP {
+  static constexpr int N1 = P + 1, Q1 = P + 1, NB = N1 * N1 * N1, NQ = Q1 * Q1 * Q1, Q2 = Q1 * Q1;
+  static constexpr int YP = N1 * N1, YPS = N1 * (N1 + 1) / 2;
+  static constexpr int TOFF = YP * (N1 * (N1 - 1) / 2);
+  static constexpr int TPE = TOFF + N1 * YPS;             // X tasks per cell
+  static constexpr int E = P == 1 ? 16 : FEB200_SFP_E2;   // cells per batch (even: TMA size)
+  static constexpr int NG = (E * Q2 + 31) / 32;           // G warps
+  static constexpr int NX = (E * TPE + 31) / 32;          // X warps
+  static constexpr int THREADS = 32 * (1 + NG + NX);
+  static constexpr int QQP = (Q2 + 1) / 2 * 2;
+  static constexpr int NUPMAX = 7;
+  // shared memory (bytes)
+  static constexpr size_t LSLOT = size_t(E) * (24 + 2 * NQ) * 8;       // coords, coef a, coef b
+  static constexpr size_t T1SLOT = size_t(E) * NUPMAX * N1 * N1 * QQP * 8;
+  static constexpr size_t KSLOT = size_t(E) * NB * NB * 8;
+  static constexpr size_t OFF_K = 0;                                  // [2][KSLOT]
+  static constexpr size_t OFF_T1 = OFF_K + 2 * KSLOT;                 // [2][T1SLOT]
+  static constexpr size_t OFF_L = OFF_T1 + 2 * T1SLOT;                // [2][LSLOT]
+  static constexpr size_t OFF_CONN = OFF_L + 2 * LSLOT;               // [2][E * 8] int32
+  static constexpr size_t OFF_BAR = (OFF_CONN + 2 * E * 8 * 4 + 15) / 16 * 16;  // 8 mbarriers
+  static constexpr size_t BYTES = OFF_BAR + 8 * 8;
+};
+
+__device__ __forceinline__ void sfp_bar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void sfp_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void sfp_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void sfp_named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <int P, int FORM>
+__global__ void __launch_bounds__(SFP<P>::THREADS, 1)
+    k_matrix_sfp(MeshView mv, const double* __restrict__ ma, const double* __restrict__ mb,
+                 int64_t e0, int64_t e1, double* __restrict__ K) {
+  constexpr bool DIFF = FORM != FE_FORM_MASS, MASS = FORM != FE_FORM_DIFFUSION;
+  using L = SFP<P>;
+  constexpr int N1 = L::N1, Q1 = L::Q1, NB = L::NB, NQ = L::NQ, Q2 = L::Q2, E = L::E;
+  constexpr int QQP = L::QQP;
+  constexpr int NUP = (DIFF ? 6 : 0) + (MASS ? 1 : 0);
+  constexpr int NOP = (DIFF ? 9 : 0) + (MASS ? 1 : 0);
+  constexpr int UBASE = DIFF ? 0 : 6;
+  constexpr int NCOEF = MASS && DIFF ? 2 : 1;
+  extern __shared__ __align__(128) unsigned char smp[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smp + L::OFF_BAR);
+  uint64_t* fullL = bars + 0;   // [2] L -> G
+  uint64_t* emptyL = bars + 2;  // [2] G -> L
+  uint64_t* fullT = bars + 4;   // [2] G -> X
+  uint64_t* emptyT = bars + 6;  // [2] X -> G
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t nloc = e1 - e0;
+  const int64_t nbatch = (nloc + E - 1) / E;
+  if (tid == 0) {
+    sfp_bar_init(&fullL[0], 32);
+    sfp_bar_init(&fullL[1], 32);
+    sfp_bar_init(&emptyL[0], 32 * L::NG);
+    sfp_bar_init(&emptyL[1], 32 * L::NG);
+    sfp_bar_init(&fullT[0], 32 * L::NG);
+    sfp_bar_init(&fullT[1], 32 * L::NG);
+    sfp_bar_init(&emptyT[0], 32 * L::NX);
+    sfp_bar_init(&emptyT[1], 32 * L::NX);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+#define Bt(a, q, i) c_tab1d[P][a][q][i]
+
+  if (warp == 0) {
+    // ======================= L: loader warp =======================
+    int32_t* connb = reinterpret_cast<int32_t*>(smp + L::OFF_CONN);
+    auto load_conn = [&](int64_t j) {  // conn of the j-th batch of this CTA -> connb[j & 1]
+      const int64_t b = blockIdx.x + j * (int64_t)gridDim.x;
+      if (b >= nbatch) return;
+      const int64_t lb = b * E;
+      const int ne = (int)((nloc - lb) < E ? (nloc - lb) : E);
+      for (int i = lane; i < E * 8; i += 32)
+        connb[(j & 1) * E * 8 + i] = i < ne * 8 ? mv.conn[8 * (e0 + lb) + i] : 0;
+    };
+    load_conn(0);
+    __syncwarp();
+    for (int64_t it = 0;; ++it) {
+      const int64_t b = blockIdx.x + it * (int64_t)gridDim.x;
+      if (b >= nbatch) break;
+      const int64_t lb = b * E;
+      const int ne = (int)((nloc - lb) < E ? (nloc - lb) : E);
+      const int sl = (int)(it & 1);
+      constexpr int XPL = (E * 24 + 31) / 32, KPL = (E * NQ + 31) / 32;
+      double xr[XPL], ka[KPL], kb[KPL];
+      const int32_t* cb = connb + sl * E * 8;
+#pragma unroll
+      for (int h = 0; h < XPL; ++h) {
+        const int i = lane + 32 * h, c = i / 24, r = i - c * 24;
+        xr[h] = (i < E * 24 && c < ne) ? mv.coords[3 * (int64_t)cb[c * 8 + r / 3] + r % 3] : 0.0;
+      }
+#pragma unroll
+      for (int h = 0; h < KPL; ++h) {
+        const int i = lane + 32 * h;
+        const bool on = i < ne * NQ;
+        const int64_t g = (e0 + lb) * NQ + i;
+        ka[h] = on ? ma[g] : 0.0;
+        kb[h] = (on && NCOEF == 2) ? mb[g] : 0.0;
+      }
+      __syncwarp();
+      load_conn(it + 1);  // other half of connb: last read in iteration it - 1
+      sfp_wait(&emptyL[sl], (uint32_t)(((it >> 1) & 1) ^ 1));
+      double* slot = reinterpret_cast<double*>(smp + L::OFF_L + sl * L::LSLOT);
+#pragma unroll
+      for (int h = 0; h < XPL; ++h) {
+        const int i = lane + 32 * h;
+        if (i < E * 24) slot[i] = xr[h];
+      }
+#pragma unroll
+      for (int h = 0; h < KPL; ++h) {
+        const int i = lane + 32 * h;
+        if (i < E * NQ) {
+          slot[E * 24 + i] = ka[h];
+          if (NCOEF == 2) slot[E * 24 + E * NQ + i] = kb[h];
+        }
+      }
+      __syncwarp();
+      sfp_arrive(&fullL[sl]);
+    }
+  } else if (warp <= L::NG) {
+    // ======================= G: geometry + stage z =======================
+    const int gtid = tid - 32;
+    const int el = gtid / Q2, qxy = gtid - el * Q2;
+    const int tx = qxy / Q1, ty = qxy - tx * Q1;  // T1's inner index is qx * Q1 + qy
+    const bool gact = gtid < E * Q2;
+    const double tX = c_x1d[P][tx], tY = c_x1d[P][ty];
+    const double wxy = c_w1d[P][tx] * c_w1d[P][ty];
+    for (int64_t it = 0;; ++it) {
+      const int64_t b = blockIdx.x + it * (int64_t)gridDim.x;
+      if (b >= nbatch) break;
+      const int64_t lb = b * E;
+      const int ne = (int)((nloc - lb) < E ? (nloc - lb) : E);
+      const int sl = (int)(it & 1);
+      const uint32_t par = (uint32_t)((it >> 1) & 1);
+      sfp_wait(&fullL[sl], par);
+      const double* slot = reinterpret_cast<const double*>(smp + L::OFF_L + sl * L::LSLOT);
+      const bool on = gact && el < ne;
+      // edge-vector combinations of this column: J[:,0] = (1-tZ) e0y[0] + tZ e0y[1],
+      // J[:,1] = (1-tZ) e1x[0] + tZ e1x[1], J[:,2] = col2 (trilinear map, vertex v = a + 2b + 4c)
+      double e0y[2][3], e1x[2][3], col2[3], ca[Q1], cb[Q1];
+      {
+        const double* X = slot + (on ? el : 0) * 24;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            // x-edges at (b, c): X[1+2b+4c] - X[2b+4c];  y-edges at (a, c): X[a+2+4c] - X[a+4c]
+            e0y[c][i] = (1 - tY) * (X[3 * (1 + 4 * c) + i] - X[3 * (4 * c) + i]) +
+                        tY * (X[3 * (3 + 4 * c) + i] - X[3 * (2 + 4 * c) + i]);
+            e1x[c][i] = (1 - tX) * (X[3 * (2 + 4 * c) + i] - X[3 * (4 * c) + i]) +
+                        tX * (X[3 * (3 + 4 * c) + i] - X[3 * (1 + 4 * c) + i]);
+          }
+          // z-edges at (a, b): X[a+2b+4] - X[a+2b]
+          col2[i] = (1 - tX) * (1 - tY) * (X[3 * 4 + i] - X[3 * 0 + i]) +
+                    tX * (1 - tY) * (X[3 * 5 + i] - X[3 * 1 + i]) +
+                    (1 - tX) * tY * (X[3 * 6 + i] - X[3 * 2 + i]) + tX * tY * (X[3 * 7 + i] - X[3 * 3 + i]);
+        }
+#pragma unroll
+        for (int qz = 0; qz < Q1; ++qz) {
+          const int q = tx + Q1 * ty + Q2 * qz;
+          ca[qz] = on ? slot[E * 24 + el * NQ + q] : 0.0;
+          cb[qz] = (on && NCOEF == 2) ? slot[E * 24 + E * NQ + el * NQ + q] : 0.0;
+        }
+      }
+      sfp_arrive(&emptyL[sl]);
+      // W^{u}[qz] for the unique pairs u (m <= n), value-value pair last
+      double Wr[NUP][Q1];
+#pragma unroll
+      for (int qz = 0; qz < Q1; ++qz) {
+        const double tZ = c_x1d[P][qz];
+        double J[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          J[i][0] = (1 - tZ) * e0y[0][i] + tZ * e0y[1][i];
+          J[i][1] = (1 - tZ) * e1x[0][i] + tZ * e1x[1][i];
+          J[i][2] = col2[i];
+        }
+        const double C[3][3] = {{J[1][1] * J[2][2] - J[1][2] * J[2][1], J[1][2] * J[2][0] - J[1][0] * J[2][2],
+                                 J[1][0] * J[2][1] - J[1][1] * J[2][0]},
+                                {J[0][2] * J[2][1] - J[0][1] * J[2][2], J[0][0] * J[2][2] - J[0][2] * J[2][0],
+                                 J[0][1] * J[2][0] - J[0][0] * J[2][1]},
+                                {J[0][1] * J[1][2] - J[0][2] * J[1][1], J[0][2] * J[1][0] - J[0][0] * J[1][2],
+                                 J[0][0] * J[1][1] - J[0][1] * J[1][0]}};
+        const double det = J[0][0] * C[0][0] + J[0][1] * C[0][1] + J[0][2] * C[0][2];
+        const double wq = wxy * c_w1d[P][qz];
+        if constexpr (DIFF) {
+          const double kap = MASS ? cb[qz] : ca[qz];
+          const double sc = on ? wq * kap / det : 0.0;
+#pragma unroll
+          for (int u = 0; u < 6; ++u) {
+            int m, n;
+            upair(u, m, n);
+            Wr[u][qz] = sc * (C[0][m] * C[0][n] + C[1][m] * C[1][n] + C[2][m] * C[2][n]);
+          }
+        }
+        if constexpr (MASS) Wr[NUP - 1][qz] = wq * det * ca[qz];
+      }
+      // stage z into T1 slot it % 2 once X has released it
+      sfp_wait(&emptyT[sl], par ^ 1u);
+      double* T1 = reinterpret_cast<double*>(smp + L::OFF_T1 + sl * L::T1SLOT);
+      if (gact) {
+#pragma unroll
+        for (int ul = 0; ul < NUP; ++ul) {
+          int m, n;
+          upair(UBASE + ul, m, n);
+          const int az = m == 2, bz = n == 2;
+          double t[Q1][N1];
+#pragma unroll
+          for (int qz = 0; qz < Q1; ++qz)
+#pragma unroll
+            for (int a = 0; a < N1; ++a) t[qz][a] = Wr[ul][qz] * Bt(az, qz, a);
+          double* out = T1 + (el * NUP + ul) * N1 * N1 * QQP + qxy;
+#pragma unroll
+          for (int a = 0; a < N1; ++a)
+#pragma unroll
+            for (int bb = 0; bb < N1; ++bb) {
+              double sacc = 0.0;
+#pragma unroll
+              for (int qz = 0; qz < Q1; ++qz) sacc = fma(t[qz][a], Bt(bz, qz, bb), sacc);
+              out[(a * N1 + bb) * QQP] = sacc;
+            }
+        }
+      }
+      sfp_arrive(&fullT[sl]);
+    }
+  } else {
+    // ======================= X: stages y and x, K store =======================
+    const int xtid = tid - 32 * (1 + L::NG);
+    const int yx_el = xtid / L::TPE, yx_r = xtid - yx_el * L::TPE;
+    const bool xact = xtid < E * L::TPE;
+    int iz = 0, jz = 0, iy = 0, jy = 0;
+    if (yx_r < L::TOFF) {
+      int c = yx_r / L::YP;
+      const int yp = yx_r - c * L::YP;
+      iy = yp / N1;
+      jy = yp - iy * N1;
+      for (int a = 0; a < N1; ++a) {
+        if (c < N1 - 1 - a) { iz = a; jz = a + 1 + c; break; }
+        c -= N1 - 1 - a;
+      }
+    } else {
+      const int r = yx_r - L::TOFF;
+      iz = jz = r / L::YPS;
+      int c = r - iz * L::YPS;
+      for (int a = 0; a < N1; ++a) {
+        if (c < N1 - a) { iy = a; jy = a + c; break; }
+        c -= N1 - a;
+      }
+    }
+    const bool mirror = (iz < jz) || (iy < jy);
+    double Byp[4][Q1];
+#pragma unroll
+    for (int q = 0; q < Q1; ++q)
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb) Byp[a * 2 + bb][q] = Bt(a, q, iy) * Bt(bb, q, jy);
+    constexpr int NXT = 32 * L::NX;
+    for (int64_t it = 0;; ++it) {
+      const int64_t b = blockIdx.x + it * (int64_t)gridDim.x;
+      if (b >= nbatch) break;
+      const int64_t lb = b * E;
+      const int ne = (int)((nloc - lb) < E ? (nloc - lb) : E);
+      const int sl = (int)(it & 1);
+      // the elected thread waited (end of iteration it - 1) for the store that last read
+      // K slot it % 2; this barrier publishes that to the group
+      sfp_named_bar(1, NXT);
+      sfp_wait(&fullT[sl], (uint32_t)((it >> 1) & 1));
+      const double* T1e = reinterpret_cast<const double*>(smp + L::OFF_T1 + sl * L::T1SLOT) +
+                          yx_el * NUP * N1 * N1 * QQP;
+      double acc[N1][N1];
+      if (xact) {
+        double S[4][Q1];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int q = 0; q < Q1; ++q) S[c][q] = 0.0;
+#pragma unroll
+        for (int op = 0; op < NOP; ++op) {
+          int m, n;
+          if (DIFF && op < 9) { m = op / 3; n = op % 3; } else { m = 3; n = 3; }
+          const int mm = m < n ? m : n, nn = m < n ? n : m;
+          const int ul = (mm == 3) ? NUP - 1 : (mm == 0 ? nn : (mm == 1 ? 2 + nn : 5));
+          const int zidx = (m > n) ? (jz * N1 + iz) : (iz * N1 + jz);
+          const int ay = m == 1, by = n == 1, cls = (m == 0) * 2 + (n == 0);
+          const double2* src = reinterpret_cast<const double2*>(T1e + (ul * N1 * N1 + zidx) * QQP);
+          double tv[QQP];
+#pragma unroll
+          for (int h = 0; h < QQP / 2; ++h) {
+            const double2 v = src[h];
+            tv[2 * h] = v.x;
+            tv[2 * h + 1] = v.y;
+          }
+#pragma unroll
+          for (int qx = 0; qx < Q1; ++qx)
+#pragma unroll
+            for (int qy = 0; qy < Q1; ++qy)
+              S[cls][qx] = fma(Byp[ay * 2 + by][qy], tv[qx * Q1 + qy], S[cls][qx]);
+        }
+        sfp_arrive(&emptyT[sl]);
+#pragma unroll
+        for (int a = 0; a < N1; ++a)
+#pragma unroll
+          for (int bb = 0; bb < N1; ++bb) acc[a][bb] = 0.0;
+#pragma unroll
+        for (int qx = 0; qx < Q1; ++qx)
+#pragma unroll
+          for (int ax = 0; ax < 2; ++ax) {
+            double u[N1];
+#pragma unroll
+            for (int bb = 0; bb < N1; ++bb) u[bb] = Bt(0, qx, bb) * S[ax * 2 + 0][qx] + Bt(1, qx, bb) * S[ax * 2 + 1][qx];
+#pragma unroll
+            for (int a = 0; a < N1; ++a)
+#pragma unroll
+              for (int bb = 0; bb < N1; ++bb) acc[a][bb] = fma(Bt(ax, qx, a), u[bb], acc[a][bb]);
+          }
+      } else {
+        sfp_arrive(&emptyT[sl]);
+      }
+      double* Kst = reinterpret_cast<double*>(smp + L::OFF_K + sl * L::KSLOT);
+      if (xact && yx_el < ne) {
+        double* Ke = Kst + yx_el * NB * NB;
+        const int ib = N1 * (iy + N1 * iz), jb = N1 * (jy + N1 * jz);
+#pragma unroll
+        for (int a = 0; a < N1; ++a)
+#pragma unroll
+          for (int bb = 0; bb < N1; ++bb) {
+            Ke[(ib + a) * NB + jb + bb] = acc[a][bb];
+            if (mirror) Ke[(jb + bb) * NB + ib + a] = acc[a][bb];
+          }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      sfp_named_bar(2, NXT);
+      const uint32_t bytes = (uint32_t)ne * NB * NB * 8;
+      double* gdst = K + lb * NB * NB;
+      if (((reinterpret_cast<uintptr_t>(gdst) | bytes) & 15u) == 0) {
+        if (xtid == 0) {
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                       :: "l"(gdst), "r"(smem_u32(Kst)), "r"(bytes) : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        }
+      } else {
+        for (int i = xtid; i < ne * NB * NB; i += NXT) gdst[i] = Kst[i];
+      }
+    }
+    if (xtid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+#undef Bt
+}
+
+template <int P, int FORM>
+static cudaError_t launch_sfp_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int64_t e1, double* K,
+                                cudaStream_t st) {
+  using L = SFP<P>;
+  auto kern = k_matrix_sfp<P, FORM>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
+  if (err != cudaSuccess) return err;
+  int nsm = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t nbatch = (e1 - e0 + L::E - 1) / L::E;
+  const int grid = (int)(nbatch < nsm ? nbatch : nsm);
+  if (grid <= 0) return cudaSuccess;
+  kern<<<grid, L::THREADS, L::BYTES, st>>>(view_of(mh), (const double*)mat.a, (const double*)mat.b,
+                                           e0, e1, K);
+  count_launch();
+  return cudaGetLastError();
+}
+
 template <int P, int FORM>
 static cudaError_t launch_sf_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int64_t e1, double* K,
                                cudaStream_t st) {
@@ -383,6 +789,20 @@ static cudaError_t launch_sf_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int64
 cudaError_t launch_matrix_sf(const fe_mesh* mh, int form, MatArgs mat, int64_t e0, int64_t e1,
                              double* K, cudaStream_t st) {
   if (mh->q1d != mh->order + 1) return cudaErrorNotSupported;
+  const char* impl = std::getenv("FEB200_MATRIX_IMPL");
+  const bool pipelined = FEB200_SFP && !(impl && std::strcmp(impl, "sf1") == 0);
+  if (pipelined && (mh->order == 1 || mh->order == 2)) {
+#define SFP_CASE(P)                                                                                \
+  if (mh->order == P) switch (form) {                                                              \
+      case FE_FORM_DIFFUSION: return launch_sfp_t<P, FE_FORM_DIFFUSION>(mh, mat, e0, e1, K, st);   \
+      case FE_FORM_MASS: return launch_sfp_t<P, FE_FORM_MASS>(mh, mat, e0, e1, K, st);             \
+      case FE_FORM_MASS_DIFFUSION: return launch_sfp_t<P, FE_FORM_MASS_DIFFUSION>(mh, mat, e0, e1, K, st); \
+      default: return cudaErrorNotSupported;                                                       \
+    }
+    SFP_CASE(1)
+    SFP_CASE(2)
+#undef SFP_CASE
+  }
 #define SF_CASE(P)                                                                              \
   case P:                                                                                       \
     switch (form) {                                                                             \

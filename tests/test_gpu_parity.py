@@ -50,11 +50,12 @@ RESIDUAL_CASES = [(f, p) for f in (0, 1, 2, 3, 4, 5) for p in (1, 2, 3)] + \
                  [(0, 4), (1, 4), (3, 4), (2, 4), (4, 4), (5, 4)]
 
 
-@pytest.fixture(params=["default", "dense"])
+@pytest.fixture(params=["default", "sf1", "dense"])
 def matrix_impl(request, monkeypatch):
-    """default = sum-factorised kernels where built; dense = the DMMA dense kernels."""
-    if request.param == "dense":
-        monkeypatch.setenv("FEB200_MATRIX_IMPL", "dense")
+    """default = sum-factorised kernels where built (warp-specialised pipeline for the scalar
+    forms at p <= 2); sf1 = the single-stage sum-factorised kernel; dense = the DMMA kernels."""
+    if request.param in ("dense", "sf1"):
+        monkeypatch.setenv("FEB200_MATRIX_IMPL", request.param)
     else:
         monkeypatch.delenv("FEB200_MATRIX_IMPL", raising=False)
     return request.param
