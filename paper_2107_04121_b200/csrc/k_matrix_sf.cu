@@ -28,6 +28,18 @@
 #ifndef FEB200_SFP
 #define FEB200_SFP 1
 #endif
+#ifndef FEB200_SFP_X3
+#define FEB200_SFP_X3 0
+#endif
+#ifndef FEB200_SFP_NOSTORE
+#define FEB200_SFP_NOSTORE 0
+#endif
+#ifndef FEB200_SFP_NOX
+#define FEB200_SFP_NOX 0
+#endif
+#ifndef FEB200_SFP_GH
+#define FEB200_SFP_GH 1
+#endif
 #ifndef FEB200_SF_MINB
 #define FEB200_SF_MINB 1
 #endif
@@ -36,6 +48,7 @@
 #include "fe_internal.h"
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 namespace feb200 {
 
@@ -66,9 +79,25 @@ struct SFM {
   static constexpr size_t BYTES = size_t(TOTAL) * 8;
 };
 
+// stage-z outer products c_zz[p][az][bz][qz][a][b] = B^az[qz][a] B^bz[qz][b] (p <= 3), so the
+// pipelined kernel's stage z is one constant-operand FMA per term
+__constant__ double c_zz[4][2][2][4][4][4];
+
 cudaError_t upload_const_tables_matrix(int order, const double* b1, const double* d1,
                                       const double* x1, const double* w1, cudaStream_t st) {
-  return upload_tables_this_tu(order, b1, d1, x1, w1, st);
+  cudaError_t e = upload_tables_this_tu(order, b1, d1, x1, w1, st);
+  if (e != cudaSuccess || order < 1 || order > 3) return e;
+  static double h[2][2][4][4][4];
+  const int n1 = order + 1, q1 = order + 1;
+  for (int az = 0; az < 2; ++az)
+    for (int bz = 0; bz < 2; ++bz)
+      for (int q = 0; q < q1; ++q)
+        for (int a = 0; a < n1; ++a)
+          for (int b = 0; b < n1; ++b)
+            h[az][bz][q][a][b] = (az ? d1 : b1)[q * n1 + a] * (bz ? d1 : b1)[q * n1 + b];
+  e = cudaMemcpyToSymbolAsync(c_zz, h, sizeof(h), sizeof(h) * order, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return e;
 }
 
 // unique pair u -> (m, n), m <= n; index 6 is the value-value pair (3,3)
@@ -382,28 +411,34 @@ __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_D
 //                  (b, c1) -> K staging slot [it % 2] -> one TMA bulk store
 // The geometry + stage-z thread uses compile-time pair indices, so every 1D
 // table operand is a constant-bank operand.
-template <int P>
+template <int P, int NUPMAX>
 struct SFP {
   static constexpr int N1 = P + 1, Q1 = P + 1, NB = N1 * N1 * N1, NQ = Q1 * Q1 * Q1, Q2 = Q1 * Q1;
   static constexpr int YP = N1 * N1, YPS = N1 * (N1 + 1) / 2;
   static constexpr int TOFF = YP * (N1 * (N1 - 1) / 2);
-  static constexpr int TPE = TOFF + N1 * YPS;             // X tasks per cell
+  static constexpr int TPE = TOFF + N1 * YPS;             // X tasks per cell (one y pair each)
+  // X3: one task per (z pair, iy) doing all jy (diagonal z pairs redundantly: no symmetry
+  // in y) -- each T1 vector loaded from shared memory serves N1 y pairs instead of one
+  static constexpr bool X3 = FEB200_SFP_X3 != 0;
+  static constexpr int TPE3 = N1 * N1 * (N1 + 1) / 2;
   static constexpr int E = P == 1 ? 16 : FEB200_SFP_E2;   // cells per batch (even: TMA size)
-  static constexpr int NG = (E * Q2 + 31) / 32;           // G warps
-  static constexpr int NX = (E * TPE + 31) / 32;          // X warps
+  static constexpr int GH = FEB200_SFP_GH;                // G thread groups per column
+  static constexpr int NGW = (E * Q2 + 31) / 32;          // G warps per group
+  static constexpr int NG = GH * NGW;                     // G warps
+  static constexpr int NXW = (E * (N1 * (N1 + 1) / 2) + 31) / 32;  // X3 warps per iy
+  static constexpr int NX = X3 ? N1 * NXW : (E * TPE + 31) / 32;  // X warps
   static constexpr int THREADS = 32 * (1 + NG + NX);
   static constexpr int QQP = (Q2 + 1) / 2 * 2;
-  static constexpr int NUPMAX = 7;
   // shared memory (bytes)
-  static constexpr size_t LSLOT = size_t(E) * (24 + 2 * NQ) * 8;       // coords, coef a, coef b
+  static constexpr size_t LSLOT = size_t(E) * (24 + (NUPMAX == 7 ? 2 : 1) * NQ) * 8;  // coords, coef a[, b]
   static constexpr size_t T1SLOT = size_t(E) * NUPMAX * N1 * N1 * QQP * 8;
   static constexpr size_t KSLOT = size_t(E) * NB * NB * 8;
   static constexpr size_t OFF_K = 0;                                  // [2][KSLOT]
   static constexpr size_t OFF_T1 = OFF_K + 2 * KSLOT;                 // [2][T1SLOT]
   static constexpr size_t OFF_L = OFF_T1 + 2 * T1SLOT;                // [2][LSLOT]
-  static constexpr size_t OFF_CONN = OFF_L + 2 * LSLOT;               // [2][E * 8] int32
-  static constexpr size_t OFF_BAR = (OFF_CONN + 2 * E * 8 * 4 + 15) / 16 * 16;  // 8 mbarriers
-  static constexpr size_t BYTES = OFF_BAR + 8 * 8;
+  static constexpr size_t OFF_CONN = OFF_L + 2 * LSLOT;               // [3][E * 8] int32
+  static constexpr size_t OFF_BAR = (OFF_CONN + 3 * E * 8 * 4 + 15) / 16 * 16;  // 11 mbarriers
+  static constexpr size_t BYTES = OFF_BAR + 16 * 8;
 };
 
 __device__ __forceinline__ void sfp_bar_init(uint64_t* bar, int count) {
@@ -418,19 +453,42 @@ __device__ __forceinline__ void sfp_wait(uint64_t* bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
+__device__ __forceinline__ void sfp_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void sfp_expect_arrive(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// TMA bulk copy global -> shared (16-B aligned, size % 16 == 0), completion on an mbarrier
+__device__ __forceinline__ void sfp_tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+#ifdef FEB200_SFP_PROF
+// per-role wait-cycle counters (A/B builds only): sum over warps of clock64 deltas
+__device__ unsigned long long g_sfp_prof[16];
+#define SFP_T(k, stmt)                                  \
+  do {                                                  \
+    const long long t0_ = clock64();                    \
+    stmt;                                               \
+    prof_[k] += (unsigned long long)(clock64() - t0_);  \
+  } while (0)
+#else
+#define SFP_T(k, stmt) stmt
+#endif
 __device__ __forceinline__ void sfp_named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 template <int P, int FORM>
-__global__ void __launch_bounds__(SFP<P>::THREADS, 1)
+__global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM != FE_FORM_DIFFUSION ? 1 : 0)>::THREADS, 1)
     k_matrix_sfp(MeshView mv, const double* __restrict__ ma, const double* __restrict__ mb,
                  int64_t e0, int64_t e1, double* __restrict__ K) {
   constexpr bool DIFF = FORM != FE_FORM_MASS, MASS = FORM != FE_FORM_DIFFUSION;
-  using L = SFP<P>;
+  constexpr int NUP = (DIFF ? 6 : 0) + (MASS ? 1 : 0);
+  using L = SFP<P, NUP>;
   constexpr int N1 = L::N1, Q1 = L::Q1, NB = L::NB, NQ = L::NQ, Q2 = L::Q2, E = L::E;
   constexpr int QQP = L::QQP;
-  constexpr int NUP = (DIFF ? 6 : 0) + (MASS ? 1 : 0);
   constexpr int NOP = (DIFF ? 9 : 0) + (MASS ? 1 : 0);
   constexpr int UBASE = DIFF ? 0 : 6;
   constexpr int NCOEF = MASS && DIFF ? 2 : 1;
@@ -443,6 +501,10 @@ __global__ void __launch_bounds__(SFP<P>::THREADS, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t nloc = e1 - e0;
   const int64_t nbatch = (nloc + E - 1) / E;
+#ifdef FEB200_SFP_PROF
+  unsigned long long prof_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long tstart_ = clock64();
+#endif
   if (tid == 0) {
     sfp_bar_init(&fullL[0], 32);
     sfp_bar_init(&fullL[1], 32);
@@ -452,6 +514,9 @@ __global__ void __launch_bounds__(SFP<P>::THREADS, 1)
     sfp_bar_init(&fullT[1], 32 * L::NG);
     sfp_bar_init(&emptyT[0], 32 * L::NX);
     sfp_bar_init(&emptyT[1], 32 * L::NX);
+    sfp_bar_init(&bars[8], 1);
+    sfp_bar_init(&bars[9], 1);
+    sfp_bar_init(&bars[10], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -459,65 +524,95 @@ __global__ void __launch_bounds__(SFP<P>::THREADS, 1)
 
   if (warp == 0) {
     // ======================= L: loader warp =======================
+    // conn blocks arrive by TMA two batches ahead (3-deep ring, own mbarriers); the vertex
+    // coordinates of batch it + 1 are gathered into registers while batch it is handed
+    // over; coefficient blocks go by TMA straight into the slot (tx-counted on fullL).
     int32_t* connb = reinterpret_cast<int32_t*>(smp + L::OFF_CONN);
-    auto load_conn = [&](int64_t j) {  // conn of the j-th batch of this CTA -> connb[j & 1]
+    uint64_t* connbar = bars + 8;  // [3]
+    auto batch_of = [&](int64_t j, int64_t& lb, int& ne) {
       const int64_t b = blockIdx.x + j * (int64_t)gridDim.x;
-      if (b >= nbatch) return;
-      const int64_t lb = b * E;
-      const int ne = (int)((nloc - lb) < E ? (nloc - lb) : E);
-      for (int i = lane; i < E * 8; i += 32)
-        connb[(j & 1) * E * 8 + i] = i < ne * 8 ? mv.conn[8 * (e0 + lb) + i] : 0;
+      lb = b * E;
+      ne = b < nbatch ? (int)((nloc - lb) < E ? (nloc - lb) : E) : 0;
     };
-    load_conn(0);
-    __syncwarp();
-    for (int64_t it = 0;; ++it) {
-      const int64_t b = blockIdx.x + it * (int64_t)gridDim.x;
-      if (b >= nbatch) break;
-      const int64_t lb = b * E;
-      const int ne = (int)((nloc - lb) < E ? (nloc - lb) : E);
-      const int sl = (int)(it & 1);
-      constexpr int XPL = (E * 24 + 31) / 32, KPL = (E * NQ + 31) / 32;
-      double xr[XPL], ka[KPL], kb[KPL];
-      const int32_t* cb = connb + sl * E * 8;
+    auto conn_issue = [&](int64_t j) {  // lane 0
+      int64_t lb;
+      int ne;
+      batch_of(j, lb, ne);
+      if (ne <= 0) return;
+      const int k = (int)(j % 3);
+      sfp_expect_arrive(&connbar[k], (uint32_t)ne * 32u);
+      sfp_tma_load(connb + k * E * 8, mv.conn + 8 * (e0 + lb), (uint32_t)ne * 32u, &connbar[k]);
+    };
+    constexpr int XPL = (E * 24 + 31) / 32, KPL = (E * NQ + 31) / 32;
+    double xr[XPL];
+    auto coords_issue = [&](int64_t j) {
+      int64_t lb;
+      int ne;
+      batch_of(j, lb, ne);
+      if (ne <= 0) return;
+      const int k = (int)(j % 3);
+      SFP_T(0, sfp_wait(&connbar[k], (uint32_t)((j / 3) & 1)));
+      const int32_t* cb = connb + k * E * 8;
 #pragma unroll
       for (int h = 0; h < XPL; ++h) {
         const int i = lane + 32 * h, c = i / 24, r = i - c * 24;
         xr[h] = (i < E * 24 && c < ne) ? mv.coords[3 * (int64_t)cb[c * 8 + r / 3] + r % 3] : 0.0;
       }
-#pragma unroll
-      for (int h = 0; h < KPL; ++h) {
-        const int i = lane + 32 * h;
-        const bool on = i < ne * NQ;
-        const int64_t g = (e0 + lb) * NQ + i;
-        ka[h] = on ? ma[g] : 0.0;
-        kb[h] = (on && NCOEF == 2) ? mb[g] : 0.0;
-      }
+    };
+    if (lane == 0) {
+      conn_issue(0);
+      conn_issue(1);
+    }
+    coords_issue(0);
+    for (int64_t it = 0;; ++it) {
+      int64_t lb;
+      int ne;
+      batch_of(it, lb, ne);
+      if (ne <= 0) break;
+      const int sl = (int)(it & 1);
       __syncwarp();
-      load_conn(it + 1);  // other half of connb: last read in iteration it - 1
-      sfp_wait(&emptyL[sl], (uint32_t)(((it >> 1) & 1) ^ 1));
+      if (lane == 0) conn_issue(it + 2);  // ring slot (it+2)%3 was last read in iteration it-2
+      SFP_T(1, sfp_wait(&emptyL[sl], (uint32_t)(((it >> 1) & 1) ^ 1)));
       double* slot = reinterpret_cast<double*>(smp + L::OFF_L + sl * L::LSLOT);
+      const double* ga = ma + (e0 + lb) * NQ;
+      const double* gb = NCOEF == 2 ? mb + (e0 + lb) * NQ : nullptr;
+      const uint32_t kbytes = (uint32_t)ne * NQ * 8u;
+      const bool tma_ok = (((reinterpret_cast<uintptr_t>(ga) | (NCOEF == 2 ? reinterpret_cast<uintptr_t>(gb) : 0) |
+                             kbytes) & 15u) == 0);
+      if (tma_ok) {
+        if (lane == 0) {
+          sfp_expect_tx(&fullL[sl], kbytes * NCOEF);
+          sfp_tma_load(slot + E * 24, ga, kbytes, &fullL[sl]);
+          if (NCOEF == 2) sfp_tma_load(slot + E * 24 + E * NQ, gb, kbytes, &fullL[sl]);
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < KPL; ++h) {
+          const int i = lane + 32 * h;
+          if (i < ne * NQ) {
+            slot[E * 24 + i] = ga[i];
+            if (NCOEF == 2) slot[E * 24 + E * NQ + i] = gb[i];
+          }
+        }
+      }
 #pragma unroll
       for (int h = 0; h < XPL; ++h) {
         const int i = lane + 32 * h;
         if (i < E * 24) slot[i] = xr[h];
       }
-#pragma unroll
-      for (int h = 0; h < KPL; ++h) {
-        const int i = lane + 32 * h;
-        if (i < E * NQ) {
-          slot[E * 24 + i] = ka[h];
-          if (NCOEF == 2) slot[E * 24 + E * NQ + i] = kb[h];
-        }
-      }
-      __syncwarp();
       sfp_arrive(&fullL[sl]);
+      coords_issue(it + 1);
     }
   } else if (warp <= L::NG) {
     // ======================= G: geometry + stage z =======================
-    const int gtid = tid - 32;
+    // GH warp-uniform groups per column; group h forms the unique pairs [ulo, uhi)
+    const int gtid0 = tid - 32;
+    const int h = gtid0 / (32 * L::NGW), gtid = gtid0 - h * 32 * L::NGW;
+    constexpr int UPH = (NUP + L::GH - 1) / L::GH;
+    const int ulo = h * UPH, uhi = (h + 1) * UPH < NUP ? (h + 1) * UPH : NUP;
     const int el = gtid / Q2, qxy = gtid - el * Q2;
     const int tx = qxy / Q1, ty = qxy - tx * Q1;  // T1's inner index is qx * Q1 + qy
-    const bool gact = gtid < E * Q2;
+    const bool gact = gtid < E * Q2 && ulo < uhi;
     const double tX = c_x1d[P][tx], tY = c_x1d[P][ty];
     const double wxy = c_w1d[P][tx] * c_w1d[P][ty];
     for (int64_t it = 0;; ++it) {
@@ -527,7 +622,7 @@ __global__ void __launch_bounds__(SFP<P>::THREADS, 1)
       const int ne = (int)((nloc - lb) < E ? (nloc - lb) : E);
       const int sl = (int)(it & 1);
       const uint32_t par = (uint32_t)((it >> 1) & 1);
-      sfp_wait(&fullL[sl], par);
+      SFP_T(2, sfp_wait(&fullL[sl], par));
       const double* slot = reinterpret_cast<const double*>(smp + L::OFF_L + sl * L::LSLOT);
       const bool on = gact && el < ne;
       // edge-vector combinations of this column: J[:,0] = (1-tZ) e0y[0] + tZ e0y[1],
@@ -580,9 +675,17 @@ __global__ void __launch_bounds__(SFP<P>::THREADS, 1)
         const double wq = wxy * c_w1d[P][qz];
         if constexpr (DIFF) {
           const double kap = MASS ? cb[qz] : ca[qz];
-          const double sc = on ? wq * kap / det : 0.0;
+          // 1/det: rcp.approx + two Newton steps (relative error ~1 ulp; det > 0 checked at create)
+          double rd;
+          asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(det));
+          double er = fma(-det, rd, 1.0);
+          rd = fma(rd, er, rd);
+          er = fma(-det, rd, 1.0);
+          rd = fma(rd, er, rd);
+          const double sc = on ? wq * kap * rd : 0.0;
 #pragma unroll
           for (int u = 0; u < 6; ++u) {
+            if (L::GH > 1 && (u < ulo || u >= uhi)) continue;
             int m, n;
             upair(u, m, n);
             Wr[u][qz] = sc * (C[0][m] * C[0][n] + C[1][m] * C[1][n] + C[2][m] * C[2][n]);
@@ -591,19 +694,15 @@ __global__ void __launch_bounds__(SFP<P>::THREADS, 1)
         if constexpr (MASS) Wr[NUP - 1][qz] = wq * det * ca[qz];
       }
       // stage z into T1 slot it % 2 once X has released it
-      sfp_wait(&emptyT[sl], par ^ 1u);
+      SFP_T(3, sfp_wait(&emptyT[sl], par ^ 1u));
       double* T1 = reinterpret_cast<double*>(smp + L::OFF_T1 + sl * L::T1SLOT);
       if (gact) {
 #pragma unroll
         for (int ul = 0; ul < NUP; ++ul) {
+          if (L::GH > 1 && (ul < ulo || ul >= uhi)) continue;
           int m, n;
           upair(UBASE + ul, m, n);
           const int az = m == 2, bz = n == 2;
-          double t[Q1][N1];
-#pragma unroll
-          for (int qz = 0; qz < Q1; ++qz)
-#pragma unroll
-            for (int a = 0; a < N1; ++a) t[qz][a] = Wr[ul][qz] * Bt(az, qz, a);
           double* out = T1 + (el * NUP + ul) * N1 * N1 * QQP + qxy;
 #pragma unroll
           for (int a = 0; a < N1; ++a)
@@ -611,13 +710,146 @@ __global__ void __launch_bounds__(SFP<P>::THREADS, 1)
             for (int bb = 0; bb < N1; ++bb) {
               double sacc = 0.0;
 #pragma unroll
-              for (int qz = 0; qz < Q1; ++qz) sacc = fma(t[qz][a], Bt(bz, qz, bb), sacc);
+              for (int qz = 0; qz < Q1; ++qz) sacc = fma(Wr[ul][qz], c_zz[P][az][bz][qz][a][bb], sacc);
               out[(a * N1 + bb) * QQP] = sacc;
             }
         }
       }
       sfp_arrive(&fullT[sl]);
     }
+  } else if constexpr (L::X3) {
+    // ============ X3: one task per (cell, z pair, iy) doing every jy; iy is warp-uniform ============
+    // Each T1 vector read from shared memory serves N1 y pairs (the shared-memory data pipe
+    // is the binding resource of this kernel); with iy and jy compile-time, the stage-y
+    // coefficients B^ay[qy][iy] B^by[qy][jy] are constant-bank operands (c_zz).
+    const int xtid = tid - 32 * (1 + L::NG);
+    const int iyw = xtid / (32 * L::NXW), xr_ = xtid - iyw * 32 * L::NXW;
+    constexpr int NZP = N1 * (N1 + 1) / 2, NOFF = N1 * (N1 - 1) / 2;
+    const int x_el = xr_ / NZP, zp = xr_ - x_el * NZP;
+    const bool xact = xr_ < E * NZP;
+    int iz = 0, jz = 0;
+    if (zp < NOFF) {
+      int c = zp;
+      for (int a = 0; a < N1; ++a) {
+        if (c < N1 - 1 - a) { iz = a; jz = a + 1 + c; break; }
+        c -= N1 - 1 - a;
+      }
+    } else {
+      iz = jz = zp - NOFF;
+    }
+    const bool offz = iz < jz;
+    constexpr int NXT = 32 * L::NX;
+    auto body = [&](auto IYc, const double* T1e, double* Ke) {
+      constexpr int IY = decltype(IYc)::value;
+      double S[N1][4][Q1];
+#pragma unroll
+      for (int j = 0; j < N1; ++j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int q = 0; q < Q1; ++q) S[j][c][q] = 0.0;
+#pragma unroll
+      for (int op = 0; op < NOP; ++op) {
+        int m, n;
+        if (DIFF && op < 9) { m = op / 3; n = op % 3; } else { m = 3; n = 3; }
+        const int mm = m < n ? m : n, nn = m < n ? n : m;
+        const int ul = (mm == 3) ? NUP - 1 : (mm == 0 ? nn : (mm == 1 ? 2 + nn : 5));
+        const int zidx = (m > n) ? (jz * N1 + iz) : (iz * N1 + jz);
+        const int ay = m == 1, by = n == 1, cls = (m == 0) * 2 + (n == 0);
+        const double2* src = reinterpret_cast<const double2*>(T1e + (ul * N1 * N1 + zidx) * QQP);
+        double tv[QQP];
+#pragma unroll
+        for (int h = 0; h < Q2 / 2; ++h) {  // Q2 of the QQP values: the odd one by LDS.64
+          const double2 v = src[h];
+          tv[2 * h] = v.x;
+          tv[2 * h + 1] = v.y;
+        }
+        if (Q2 & 1) tv[Q2 - 1] = reinterpret_cast<const double*>(src)[Q2 - 1];
+#pragma unroll
+        for (int j = 0; j < N1; ++j)
+#pragma unroll
+          for (int qx = 0; qx < Q1; ++qx)
+#pragma unroll
+            for (int qy = 0; qy < Q1; ++qy)
+              S[j][cls][qx] = fma(c_zz[P][ay][by][qy][IY][j], tv[qx * Q1 + qy], S[j][cls][qx]);
+      }
+      return [&, S]() {  // stage x + K writes, run after the T1 slot is released
+#pragma unroll
+        for (int j = 0; j < N1; ++j) {
+          double acc[N1][N1];
+#pragma unroll
+          for (int a = 0; a < N1; ++a)
+#pragma unroll
+            for (int bb = 0; bb < N1; ++bb) acc[a][bb] = 0.0;
+#pragma unroll
+          for (int qx = 0; qx < Q1; ++qx)
+#pragma unroll
+            for (int ax = 0; ax < 2; ++ax) {
+              double u[N1];
+#pragma unroll
+              for (int bb = 0; bb < N1; ++bb)
+                u[bb] = Bt(0, qx, bb) * S[j][ax * 2 + 0][qx] + Bt(1, qx, bb) * S[j][ax * 2 + 1][qx];
+#pragma unroll
+              for (int a = 0; a < N1; ++a)
+#pragma unroll
+                for (int bb = 0; bb < N1; ++bb) acc[a][bb] = fma(Bt(ax, qx, a), u[bb], acc[a][bb]);
+            }
+          const int ib = N1 * (IY + N1 * iz), jb = N1 * (j + N1 * jz);
+#pragma unroll
+          for (int a = 0; a < N1; ++a)
+#pragma unroll
+            for (int bb = 0; bb < N1; ++bb) {
+              Ke[(ib + a) * NB + jb + bb] = acc[a][bb];
+              if (offz) Ke[(jb + bb) * NB + ib + a] = acc[a][bb];
+            }
+        }
+      };
+    };
+    for (int64_t it = 0;; ++it) {
+      const int64_t b = blockIdx.x + it * (int64_t)gridDim.x;
+      if (b >= nbatch) break;
+      const int64_t lb = b * E;
+      const int ne = (int)((nloc - lb) < E ? (nloc - lb) : E);
+      const int sl = (int)(it & 1);
+      SFP_T(5, sfp_named_bar(1, NXT));
+      SFP_T(4, sfp_wait(&fullT[sl], (uint32_t)((it >> 1) & 1)));
+      double* Kst = reinterpret_cast<double*>(smp + L::OFF_K + sl * L::KSLOT);
+      const double* T1e = reinterpret_cast<const double*>(smp + L::OFF_T1 + sl * L::T1SLOT) +
+                          (xact ? x_el : 0) * NUP * N1 * N1 * QQP;
+      double* Ke = Kst + x_el * NB * NB;
+      const bool wr = xact && x_el < ne;
+      auto run = [&](auto IYc) {
+        auto fin = body(IYc, T1e, Ke);
+        sfp_arrive(&emptyT[sl]);
+        if (wr) fin();
+      };
+      if (!xact) {
+        sfp_arrive(&emptyT[sl]);
+      } else if (iyw == 0) {
+        run(std::integral_constant<int, 0>{});
+      } else if (iyw == 1) {
+        run(std::integral_constant<int, 1>{});
+      } else if constexpr (N1 > 2) {
+        if (iyw == 2) run(std::integral_constant<int, 2>{});
+        else if constexpr (N1 > 3) run(std::integral_constant<int, 3>{});
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      SFP_T(6, sfp_named_bar(2, NXT));
+      const uint32_t bytes = (uint32_t)ne * NB * NB * 8;
+      double* gdst = K + lb * NB * NB;
+      if (FEB200_SFP_NOSTORE) {
+      } else if (((reinterpret_cast<uintptr_t>(gdst) | bytes) & 15u) == 0) {
+        if (xtid == 0) {
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                       :: "l"(gdst), "r"(smem_u32(Kst)), "r"(bytes) : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        }
+      } else {
+        for (int i = xtid; i < ne * NB * NB; i += NXT) gdst[i] = Kst[i];
+      }
+    }
+    if (xtid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else {
     // ======================= X: stages y and x, K store =======================
     const int xtid = tid - 32 * (1 + L::NG);
@@ -659,12 +891,18 @@ __global__ void __launch_bounds__(SFP<P>::THREADS, 1)
       const int sl = (int)(it & 1);
       // the elected thread waited (end of iteration it - 1) for the store that last read
       // K slot it % 2; this barrier publishes that to the group
-      sfp_named_bar(1, NXT);
-      sfp_wait(&fullT[sl], (uint32_t)((it >> 1) & 1));
+      SFP_T(5, sfp_named_bar(1, NXT));
+      SFP_T(4, sfp_wait(&fullT[sl], (uint32_t)((it >> 1) & 1)));
       const double* T1e = reinterpret_cast<const double*>(smp + L::OFF_T1 + sl * L::T1SLOT) +
                           yx_el * NUP * N1 * N1 * QQP;
       double acc[N1][N1];
-      if (xact) {
+      if (FEB200_SFP_NOX) {
+#pragma unroll
+        for (int a = 0; a < N1; ++a)
+#pragma unroll
+          for (int bb = 0; bb < N1; ++bb) acc[a][bb] = (double)(a + bb);
+        sfp_arrive(&emptyT[sl]);
+      } else if (xact) {
         double S[4][Q1];
 #pragma unroll
         for (int c = 0; c < 4; ++c)
@@ -681,11 +919,12 @@ __global__ void __launch_bounds__(SFP<P>::THREADS, 1)
           const double2* src = reinterpret_cast<const double2*>(T1e + (ul * N1 * N1 + zidx) * QQP);
           double tv[QQP];
 #pragma unroll
-          for (int h = 0; h < QQP / 2; ++h) {
+          for (int h = 0; h < Q2 / 2; ++h) {  // Q2 of the QQP values: the odd one by LDS.64
             const double2 v = src[h];
             tv[2 * h] = v.x;
             tv[2 * h + 1] = v.y;
           }
+          if (Q2 & 1) tv[Q2 - 1] = reinterpret_cast<const double*>(src)[Q2 - 1];
 #pragma unroll
           for (int qx = 0; qx < Q1; ++qx)
 #pragma unroll
@@ -725,10 +964,11 @@ __global__ void __launch_bounds__(SFP<P>::THREADS, 1)
           }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      sfp_named_bar(2, NXT);
+      SFP_T(6, sfp_named_bar(2, NXT));
       const uint32_t bytes = (uint32_t)ne * NB * NB * 8;
       double* gdst = K + lb * NB * NB;
-      if (((reinterpret_cast<uintptr_t>(gdst) | bytes) & 15u) == 0) {
+      if (FEB200_SFP_NOSTORE) {
+      } else if (((reinterpret_cast<uintptr_t>(gdst) | bytes) & 15u) == 0) {
         if (xtid == 0) {
           asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                        :: "l"(gdst), "r"(smem_u32(Kst)), "r"(bytes) : "memory");
@@ -741,13 +981,21 @@ __global__ void __launch_bounds__(SFP<P>::THREADS, 1)
     }
     if (xtid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
+#ifdef FEB200_SFP_PROF
+  if (lane == 0) {
+    for (int k = 0; k < 7; ++k) if (prof_[k]) atomicAdd(&g_sfp_prof[k], prof_[k]);
+    const int role = warp == 0 ? 0 : (warp <= L::NG ? 1 : 2);
+    atomicAdd(&g_sfp_prof[8 + role], (unsigned long long)(clock64() - tstart_));
+    atomicAdd(&g_sfp_prof[12 + role], 1ull);
+  }
+#endif
 #undef Bt
 }
 
 template <int P, int FORM>
 static cudaError_t launch_sfp_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int64_t e1, double* K,
                                 cudaStream_t st) {
-  using L = SFP<P>;
+  using L = SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM != FE_FORM_DIFFUSION ? 1 : 0)>;
   auto kern = k_matrix_sfp<P, FORM>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
   if (err != cudaSuccess) return err;
@@ -822,3 +1070,15 @@ cudaError_t launch_matrix_sf(const fe_mesh* mh, int form, MatArgs mat, int64_t e
 }
 
 }  // namespace feb200
+
+#ifdef FEB200_SFP_PROF
+extern "C" int fe_debug_sfp_prof(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, feb200::g_sfp_prof, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(feb200::g_sfp_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
