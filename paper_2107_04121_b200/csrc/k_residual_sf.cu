@@ -74,9 +74,10 @@ struct RSF {
   static constexpr size_t SL_MA = (SL_DOF + size_t(EB) * NB * 4 + 15) / 16 * 16;
   static constexpr size_t SL_MB = (SL_MA + size_t(EB) * NQ * sizeof(T) + 15) / 16 * 16;
   static constexpr size_t SL_SIZE = (SL_MB + size_t(EB) * NQ * sizeof(T) + 15) / 16 * 16;
-  static constexpr size_t OFF_X = size_t(EB) * 36 * 8 + 2 * Q1 * N1 * 8;
+  static constexpr size_t OFF_X = (2 * Q1 * N1 * 8 + 15) / 16 * 16;
   static constexpr size_t OFF_XV = (OFF_X + size_t(EB) * XS * sizeof(T) + 15) / 16 * 16;
-  static constexpr size_t OFF_SLOT = OFF_XV + size_t(EB) * 24 * 8;
+  static constexpr int XVS = 28;  // per-cell stride of the staged vertex coordinates (bank spread)
+  static constexpr size_t OFF_SLOT = OFF_XV + size_t(EB) * XVS * 8;
   static constexpr size_t OFF_BAR = OFF_SLOT + 2 * SL_SIZE;
   static constexpr size_t BYTES = OFF_BAR + 16;
   static constexpr int PX = (EB * 24 + THREADS_ - 1) / THREADS_;  // vertex coordinates per thread
@@ -96,8 +97,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
   constexpr bool VAL = L::VAL, GRAD = L::GRAD;
   using A = T;  // contraction arithmetic in the call's precision (geometry and flux stay fp64)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* edge = reinterpret_cast<double*>(smem_raw);        // [EB][12][3]
-  T* Bs = reinterpret_cast<T*>(smem_raw + size_t(EB) * 36 * 8);  // [2][Q1][N1] in the arithmetic type
+  T* Bs = reinterpret_cast<T*>(smem_raw);  // [2][Q1][N1] in the arithmetic type
   T* X = reinterpret_cast<T*>(smem_raw + L::OFF_X);  // [EB][D][3][Q1^3]
   double* xvs = reinterpret_cast<double*>(smem_raw + L::OFF_XV);  // [EB][24] vertex coordinates
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + L::OFF_BAR);
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
 #pragma unroll
     for (int h = 0; h < L::PX; ++h) {
       const int i = tid + h * blockDim.x;
-      if (i < EB * 24) xvs[i] = x_next[h];
+      if (i < EB * 24) xvs[(i / 24) * L::XVS + i % 24] = x_next[h];
     }
     const int32_t* ds = reinterpret_cast<const int32_t*>(base + L::SL_DOF) + el * NB;
     const T* msa = reinterpret_cast<const T*>(base + L::SL_MA) + el * nma;
@@ -251,14 +251,6 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
         for (int kz = 0; kz < N1; ++kz) Xe[(a * 3) * NQ + kz * Q2 + ty * Q1 + tx] = (T)uc[a][kz];
     }
     __syncthreads();
-    // edge vectors of the batch's cells from the staged vertex coordinates
-    for (int i = tid; i < EB * 36; i += blockDim.x) {
-      const int c = i / 36, r = i - c * 36;
-      const int ed = r / 3, comp = r - ed * 3;
-      const int d = ed >> 2, k = ed & 3, lo = k & 1, hi = k >> 1;
-      const int v0 = d == 0 ? (2 * lo + 4 * hi) : (d == 1 ? (lo + 4 * hi) : (lo + 2 * hi));
-      edge[i] = xvs[c * 24 + 3 * (v0 + (1 << d)) + comp] - xvs[c * 24 + 3 * v0 + comp];
-    }
     A a0[D][N1], a1[D][N1];  // [kz] at (qx = tx, ky = ty)
 #pragma unroll
     for (int a = 0; a < D; ++a)
@@ -307,20 +299,22 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
         c01[a][kz] = s01;
         c10[a][kz] = s10;
       }
-    // ---- geometry constants of this column (edge vectors are in smem since the first sync)
-    const double* ed = edge + el * 36;
+    // ---- geometry constants of this column from the cell's vertex coordinates (staged in
+    // smem before the first sync; vertex v = a + 2b + 4c at X[3 v + i]):
+    // J[:,0] = (1-tZ) e0y[0] + tZ e0y[1], J[:,1] = (1-tZ) e1x[0] + tZ e1x[1], J[:,2] = col2
+    const double* X = xvs + el * L::XVS;
     const double tX = mv.xi[3 * tx], tY = mv.xi[3 * Q1 * ty + 1];
     double col2[3], e0y[2][3], e1x[2][3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      // J[:,2] = sum_{a,b} L_a(x) L_b(y) e2[a][b]
-      col2[i] = (1 - tX) * (1 - tY) * ed[(8 + 0) * 3 + i] + tX * (1 - tY) * ed[(8 + 1) * 3 + i] +
-                (1 - tX) * tY * ed[(8 + 2) * 3 + i] + tX * tY * ed[(8 + 3) * 3 + i];
+      col2[i] = (1 - tX) * (1 - tY) * (X[12 + i] - X[i]) + tX * (1 - tY) * (X[15 + i] - X[3 + i]) +
+                (1 - tX) * tY * (X[18 + i] - X[6 + i]) + tX * tY * (X[21 + i] - X[9 + i]);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        // e0 interpolated in y: sum_b L_b(y) e0[b][c];  e1 interpolated in x: sum_a L_a(x) e1[a][c]
-        e0y[c][i] = (1 - tY) * ed[(0 + 2 * c) * 3 + i] + tY * ed[(1 + 2 * c) * 3 + i];
-        e1x[c][i] = (1 - tX) * ed[(4 + 2 * c) * 3 + i] + tX * ed[(5 + 2 * c) * 3 + i];
+        e0y[c][i] = (1 - tY) * (X[3 * (1 + 4 * c) + i] - X[3 * (4 * c) + i]) +
+                    tY * (X[3 * (3 + 4 * c) + i] - X[3 * (2 + 4 * c) + i]);
+        e1x[c][i] = (1 - tX) * (X[3 * (2 + 4 * c) + i] - X[3 * (4 * c) + i]) +
+                    tX * (X[3 * (3 + 4 * c) + i] - X[3 * (1 + 4 * c) + i]);
       }
     }
     // ---- stage z (registers) + pointwise flux + z^T (registers)

@@ -18,6 +18,8 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 rows = list(csv.reader(io.StringIO(out)))
 cur_file, hdr = None, None
 tot = {n: [0, 0] for _, _, n in ranges}
+wfs = {n: 0.0 for _, _, n in ranges}
+allwf = [0.0]
 stalls = {n: {} for _, _, n in ranges}
 allv = [0, 0]
 for r in rows:
@@ -42,19 +44,23 @@ for r in rows:
         except ValueError:
             return 0.0
     inst = num("Instructions Executed")
+    wf = num("L1 Wavefronts Shared")
     samp = num("Warp Stall Sampling (All Samples)")
     if cur_file and cur_file.endswith(fname):
         allv[0] += inst
         allv[1] += samp
+        allwf[0] += wf
         for a, b, n in ranges:
             if a <= ln <= b:
                 tot[n][0] += inst
                 tot[n][1] += samp
+                wfs[n] += wf
                 for ci, c in enumerate(hdr):
                     if c.startswith("stall_") and "Not Issued" not in c:
                         stalls[n][c] = stalls[n].get(c, 0.0) + num(c)
-print(f"all {fname}: inst {allv[0]:.3e} samples {allv[1]:.0f}")
+print(f"all {fname}: inst {allv[0]:.3e} samples {allv[1]:.0f} smem wavefronts {allwf[0]:.3e}")
 for n, (i, s) in tot.items():
-    print(f"{n:12s} inst {i:.3e} ({i / max(allv[0], 1):5.1%})  samples {s:.0f} ({s / max(allv[1], 1):5.1%})")
+    print(f"{n:12s} inst {i:.3e} ({i / max(allv[0], 1):5.1%})  samples {s:.0f} ({s / max(allv[1], 1):5.1%})"
+          f"  smem wf {wfs[n]:.3e} ({wfs[n] / max(allwf[0], 1):5.1%})")
     top = sorted(stalls[n].items(), key=lambda x: -x[1])[:6]
     print("             " + ", ".join(f"{k[6:]} {v / max(s, 1):.0%}" for k, v in top))
