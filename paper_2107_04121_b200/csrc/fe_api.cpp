@@ -163,6 +163,8 @@ fe_status fe_create_mesh_geometry(int64_t n_vertices, const double* coords, int6
      "constant tables");
   CK(feb200::upload_const_tables_matrix_v(order, T.b1.data(), T.d1.data(), T.x1.data(), T.w1.data(), st),
      "constant tables");
+  CK(feb200::upload_const_tables_matrix_vp(order, T.b1.data(), T.d1.data(), T.x1.data(), T.w1.data(), st),
+     "constant tables");
   CK(feb200::upload_const_tables_residual(order, T.b1.data(), T.d1.data(), T.x1.data(), T.w1.data(), st),
      "constant tables");
   std::vector<float> tmp;

@@ -63,6 +63,10 @@ cudaError_t launch_residual_sf(const fe_mesh* m, int form, MatArgs mat, const T*
                                double* eval_out = nullptr);
 cudaError_t launch_matrix_sfv(const fe_mesh* m, int form, MatArgs mat, const double* state_u,
                               int64_t e0, int64_t e1, double* K, cudaStream_t st);
+cudaError_t launch_matrix_vp(const fe_mesh* m, int form, MatArgs mat, const double* state_u,
+                             int64_t e0, int64_t e1, double* K, cudaStream_t st);
+cudaError_t upload_const_tables_matrix_vp(int order, const double* b1, const double* d1,
+                                         const double* x1, const double* w1, cudaStream_t st);
 cudaError_t upload_const_tables_matrix_v(int order, const double* b1, const double* d1,
                                         const double* x1, const double* w1, cudaStream_t st);
 cudaError_t launch_residual_f64(const fe_mesh* m, int form, MatArgs mat, const double* u,

@@ -265,6 +265,8 @@ cudaError_t launch_matrix(const fe_mesh* mh, int form, MatArgs mat, const double
   if (!(impl && std::strcmp(impl, "dense") == 0)) {
     cudaError_t e = launch_matrix_sf(mh, form, mat, e0, e1, K, st);
     if (e != cudaErrorNotSupported) return e;
+    e = launch_matrix_vp(mh, form, mat, state_u, e0, e1, K, st);
+    if (e != cudaErrorNotSupported) return e;
     e = launch_matrix_sfv(mh, form, mat, state_u, e0, e1, K, st);
     if (e != cudaErrorNotSupported) return e;
   }

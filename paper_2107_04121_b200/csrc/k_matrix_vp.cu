@@ -1,0 +1,629 @@
+// Warp-specialised, pipelined, sum-factorised element matrices for the vector forms
+// (isotropic elasticity, convective Newton tangent) -- Alg. 2 with
+// the integrands of 'cq,cqje,rjI,cqIK,cqlf,slK->cresf' and Eq. fe4.
+//
+// The 3 x 3 block structure K_ab[k][l] = sum_q sum_{(m,n)} W^{ab}_{mn}(q) D^m_k(q) D^n_l(q)
+// (D^m_k = prod_d B^{[m == d]}[q_d][k_d], m = 3 the value) is processed one block ("item")
+// at a time through the same three-role pipeline as the scalar kernel (k_matrix_sf.cu):
+//   L (1 warp)    gathers vertex coordinates, material (lambda, mu per cell or per qp)
+//                 or the state u_e of the convective tangent into a 2-deep ring;
+//   G (NG warps)  phase 1 per batch: per-qp geometry J^-1, detw
+//                 and the per-qp data of the form (lambda, mu | u, grad u, J^-1 u);
+//                 phase 2 per item: the block's pair weights W^{ab}_{mn} and stage z
+//                 -> T1 ring slot (3 deep, mbarrier full/empty handshake with X);
+//   X (NX warps)  per item: stages y and x of one (z pair, y pair) per thread -> K_e
+//                 staged in shared memory; one TMA bulk store per batch.
+// Items (blocks) per form:
+//   elasticity  (0,0) (1,1) (2,2): symmetric, 6 unique pairs m <= n,
+//               W^{aa}_{mn} = detw ((lam + mu) Ji[m][a] Ji[n][a] + mu (Ji Ji^T)_{mn});
+//               (0,1) (0,2) (1,2): 9 pairs, W^{ab}_{mn} = detw (lam Ji[m][a] Ji[n][b] +
+//               mu Ji[m][b] Ji[n][a]), mirrored into K_ba = K_ab^T.  (Psg contracted
+//               analytically, reading 7.)
+//   convective  (a,a): pairs (3,n) with detw (Ji u)_n (advection) and (3,3) with detw du_a/dx_a;
+//               (a,b), a != b: pair (3,3) with detw du_a/dx_b (reaction; symmetric block).
+#include "fe_const.cuh"
+#include "fe_device.cuh"
+#include "fe_internal.h"
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
+
+#ifndef FEB200_VP_E
+#define FEB200_VP_E 2
+#endif
+#ifndef FEB200_VP_GH
+#define FEB200_VP_GH 3
+#endif
+
+namespace feb200 {
+
+namespace {
+// c_zzv[p][az][bz][q][a][b] = B^az[q][a] B^bz[q][b]: stage-z (and stage-y) coefficients
+__constant__ double c_zzv[4][2][2][4][4][4];
+
+__device__ __forceinline__ uint32_t vp_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void vp_bar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(vp_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void vp_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(vp_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void vp_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(vp_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void vp_named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+// unique pair u -> (m, n), m <= n; index 6 is the value-value pair (3,3)
+__host__ __device__ constexpr int vp_um(int u) { return (0x3211000 >> (4 * u)) & 0xF; }
+__host__ __device__ constexpr int vp_un(int u) { return (0x3221210 >> (4 * u)) & 0xF; }
+template <int I, int N, class F>
+__device__ __forceinline__ void vp_static_for(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    vp_static_for<I + 1, N>(f);
+  }
+}
+}  // namespace
+
+cudaError_t upload_const_tables_matrix_vp(int order, const double* b1, const double* d1,
+                                         const double* x1, const double* w1, cudaStream_t st) {
+  cudaError_t e = upload_tables_this_tu(order, b1, d1, x1, w1, st);
+  if (e != cudaSuccess || order < 1 || order > 3) return e;
+  static double h[2][2][4][4][4];
+  const int n1 = order + 1, q1 = order + 1;
+  for (int az = 0; az < 2; ++az)
+    for (int bz = 0; bz < 2; ++bz)
+      for (int q = 0; q < q1; ++q)
+        for (int a = 0; a < n1; ++a)
+          for (int b = 0; b < n1; ++b)
+            h[az][bz][q][a][b] = (az ? d1 : b1)[q * n1 + a] * (bz ? d1 : b1)[q * n1 + b];
+  e = cudaMemcpyToSymbolAsync(c_zzv, h, sizeof(h), sizeof(h) * order, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return e;
+}
+
+// ---------------------------------------------------------------------------------------
+// Item (block) tables.  SYM items list unique pairs (m <= n) and are consumed with the
+// transposition trick of the scalar kernel; FULL items list ordered pairs.
+template <int FORM>
+struct VItems;
+
+template <>
+struct VItems<FE_FORM_ELASTICITY> {
+  static constexpr int NITEM = 6, NPMAX = 9, QD = 12;
+  __host__ __device__ static constexpr int a(int i) { return i < 3 ? i : (i == 5 ? 1 : 0); }
+  __host__ __device__ static constexpr int b(int i) { return i < 3 ? i : (i == 3 ? 1 : 2); }
+  __host__ __device__ static constexpr bool sym(int i) { return i < 3; }
+  __host__ __device__ static constexpr bool mirror(int i) { return i >= 3; }
+  __host__ __device__ static constexpr int np(int i) { return i < 3 ? 6 : 9; }
+  __host__ __device__ static constexpr int pm(int i, int p) { return i < 3 ? vp_um(p) : p / 3; }
+  __host__ __device__ static constexpr int pn(int i, int p) { return i < 3 ? vp_un(p) : p % 3; }
+  // SYM items: ordered pairs (m, n) of the block and their unique index
+  static constexpr int NOP = 9;
+};
+
+template <>
+struct VItems<FE_FORM_CONVECTIVE> {
+  static constexpr int NITEM = 9, NPMAX = 4, QD = 22;
+  // items 0..2 diagonal (a,a); 3..8 off-diagonal (0,1) (0,2) (1,0) (1,2) (2,0) (2,1)
+  __host__ __device__ static constexpr int a(int i) { return i < 3 ? i : (i - 3) / 2; }
+  __host__ __device__ static constexpr int b(int i) {
+    return i < 3 ? i : ((i - 3) % 2 == 0 ? ((i - 3) / 2 == 0 ? 1 : 0) : ((i - 3) / 2 == 2 ? 1 : 2));
+  }
+  __host__ __device__ static constexpr bool sym(int i) { return i >= 3; }
+  __host__ __device__ static constexpr bool mirror(int) { return false; }
+  __host__ __device__ static constexpr int np(int i) { return i < 3 ? 4 : 1; }
+  __host__ __device__ static constexpr int pm(int, int) { return 3; }
+  __host__ __device__ static constexpr int pn(int i, int p) { return i < 3 ? p : 3; }
+  static constexpr int NOP = 1;
+};
+
+template <int P, int FORM>
+struct VPL {
+  using IT = VItems<FORM>;
+  static constexpr int N1 = P + 1, Q1 = P + 1, NB = N1 * N1 * N1, NQ = Q1 * Q1 * Q1, Q2 = Q1 * Q1;
+  static constexpr int NDOF = 3 * NB;
+  static constexpr int E = FEB200_VP_E;                  // cells per batch
+  static constexpr int GH = FEB200_VP_GH;                // G threads per column (pair split)
+  static constexpr int QQP = (Q2 + 1) / 2 * 2;
+  static constexpr int QDS = IT::QD | 1;                 // odd per-qp stride (banks)
+  static constexpr int G1T = E * NQ;                     // phase-1 tasks (per qp)
+  static constexpr int G2W = (E * Q2 + 31) / 32;         // warps per pair group (warp-uniform group)
+  static constexpr int NG = ((G1T + 31) / 32 > GH * G2W) ? (G1T + 31) / 32 : GH * G2W;
+  static constexpr int NFULL = N1 * N1 * N1 * N1;        // (z pair, y pair) tasks, ordered
+  static constexpr int NSYM = N1 * N1 * (N1 * (N1 - 1) / 2) + N1 * (N1 * (N1 + 1) / 2);
+  static constexpr int NX = (E * NFULL + 31) / 32;
+  static constexpr int THREADS = 32 * (1 + NG + NX);
+  static constexpr int S = 3;                            // T1 ring depth (items)
+  static constexpr bool CONV = FORM == FE_FORM_CONVECTIVE;
+  // L slot (doubles): coords [E][24], material a/b [E][NQ] | state [E][3][NB]
+  static constexpr int LS_X = 0, LS_A = E * 24, LS_B = LS_A + E * NQ, LS_U = LS_B + E * NQ;
+  static constexpr int LSLOT = CONV ? LS_A + E * 3 * NB : LS_B + E * NQ;
+  static constexpr size_t KBYTES = size_t(E) * NDOF * NDOF * 8;
+  static constexpr size_t T1SLOT = size_t(E) * IT::NPMAX * N1 * N1 * QQP * 8;
+  static constexpr size_t OFF_K = 0;
+  static constexpr size_t OFF_T1 = (OFF_K + KBYTES + 127) / 128 * 128;
+  static constexpr size_t OFF_QD = OFF_T1 + S * T1SLOT;
+  static constexpr size_t OFF_L = OFF_QD + size_t(E) * NQ * QDS * 8;
+  static constexpr size_t OFF_IDX = OFF_L + 2 * size_t(LSLOT) * 8;       // [2][E][8 + NB] int32
+  static constexpr size_t OFF_BAR = (OFF_IDX + 2 * size_t(E) * (8 + NB) * 4 + 15) / 16 * 16;
+  static constexpr size_t BYTES = OFF_BAR + 16 * 8;
+};
+
+template <int P, int FORM>
+__global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
+    k_matrix_vp(MeshView mv, int mat_kind, const double* __restrict__ ma, const double* __restrict__ mb,
+                const double* __restrict__ state_u, int64_t e0, int64_t e1, double* __restrict__ K) {
+  using L = VPL<P, FORM>;
+  using IT = typename L::IT;
+  constexpr int N1 = L::N1, Q1 = L::Q1, NB = L::NB, NQ = L::NQ, Q2 = L::Q2, E = L::E, QQP = L::QQP;
+  constexpr int NDOF = L::NDOF, QDS = L::QDS, NITEM = IT::NITEM, S = L::S, GH = L::GH;
+  extern __shared__ __align__(128) unsigned char smv[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smv + L::OFF_BAR);
+  uint64_t* fullL = bars + 0;   // [2]
+  uint64_t* emptyL = bars + 2;  // [2]
+  uint64_t* fullT = bars + 4;   // [S]
+  uint64_t* emptyT = bars + 8;  // [S]
+  double* Kst = reinterpret_cast<double*>(smv + L::OFF_K);
+  double* QDa = reinterpret_cast<double*>(smv + L::OFF_QD);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t nloc = e1 - e0;
+  const int64_t nbatch = (nloc + E - 1) / E;
+  if (tid == 0) {
+    vp_bar_init(&fullL[0], 32);
+    vp_bar_init(&fullL[1], 32);
+    vp_bar_init(&emptyL[0], 32 * L::NG);
+    vp_bar_init(&emptyL[1], 32 * L::NG);
+    for (int s = 0; s < S; ++s) {
+      vp_bar_init(&fullT[s], 32 * L::NG);
+      vp_bar_init(&emptyT[s], 32 * L::NX);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+#define Bt(a, q, i) c_tab1d[P][a][q][i]
+  auto batch_of = [&](int64_t j, int64_t& lb, int& ne) {
+    const int64_t b = blockIdx.x + j * (int64_t)gridDim.x;
+    lb = b * E;
+    ne = b < nbatch ? (int)((nloc - lb) < E ? (nloc - lb) : E) : 0;
+  };
+
+  if (warp == 0) {
+    // ======================= L: loader warp =======================
+    int32_t* idxb = reinterpret_cast<int32_t*>(smv + L::OFF_IDX);  // [2][E][8 + NB]
+    constexpr int IDXN = E * (8 + (L::CONV ? NB : 0));
+    auto load_idx = [&](int64_t j) {
+      int64_t lb;
+      int ne;
+      batch_of(j, lb, ne);
+      if (ne <= 0) return;
+      int32_t* ib = idxb + (j & 1) * E * (8 + NB);
+      for (int i = lane; i < IDXN; i += 32) {
+        const int c = i < E * 8 ? i / 8 : (i - E * 8) / NB;
+        int v = 0;
+        if (c < ne) v = i < E * 8 ? mv.conn[8 * (e0 + lb) + i] : mv.dof_conn[(e0 + lb) * NB + (i - E * 8)];
+        ib[i] = v;
+      }
+    };
+    constexpr int XPL = (E * 24 + 31) / 32;
+    constexpr int MPL = L::CONV ? 0 : (E * NQ + 31) / 32;
+    constexpr int UPL = L::CONV ? (E * 3 * NB + 31) / 32 : 0;
+    load_idx(0);
+    __syncwarp();
+    for (int64_t it = 0;; ++it) {
+      int64_t lb;
+      int ne;
+      batch_of(it, lb, ne);
+      if (ne <= 0) break;
+      const int sl = (int)(it & 1);
+      const int32_t* ib = idxb + sl * E * (8 + NB);
+      double xr[XPL], mra[MPL > 0 ? MPL : 1], mrb[MPL > 0 ? MPL : 1], ur[UPL > 0 ? UPL : 1];
+#pragma unroll
+      for (int h = 0; h < XPL; ++h) {
+        const int i = lane + 32 * h, c = i / 24, r = i - c * 24;
+        xr[h] = (i < E * 24 && c < ne) ? mv.coords[3 * (int64_t)ib[c * 8 + r / 3] + r % 3] : 0.0;
+      }
+      if constexpr (!L::CONV) {
+#pragma unroll
+        for (int h = 0; h < MPL; ++h) {
+          const int i = lane + 32 * h, c = i / NQ, q = i - c * NQ;
+          double va = 0.0, vb = 0.0;
+          if (i < E * NQ && c < ne) {
+            if (mat_kind == FE_MAT_PER_ELEM) {
+              va = ma[e0 + lb + c];
+              vb = mb[e0 + lb + c];
+            } else {
+              va = ma[(e0 + lb + c) * NQ + q];
+              vb = mb[(e0 + lb + c) * NQ + q];
+            }
+          }
+          mra[h] = va;
+          mrb[h] = vb;
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < UPL; ++h) {
+          const int i = lane + 32 * h, c = i / (3 * NB), r = i - c * 3 * NB;
+          const int a = r / NB, k = r - a * NB;
+          ur[h] = (i < E * 3 * NB && c < ne) ? state_u[3 * (int64_t)ib[E * 8 + c * NB + k] + a] : 0.0;
+        }
+      }
+      __syncwarp();
+      load_idx(it + 1);  // other half of the index ring (read in iteration it - 1)
+      vp_wait(&emptyL[sl], (uint32_t)(((it >> 1) & 1) ^ 1));
+      double* slot = reinterpret_cast<double*>(smv + L::OFF_L) + sl * L::LSLOT;
+#pragma unroll
+      for (int h = 0; h < XPL; ++h) {
+        const int i = lane + 32 * h;
+        if (i < E * 24) slot[L::LS_X + i] = xr[h];
+      }
+      if constexpr (!L::CONV) {
+#pragma unroll
+        for (int h = 0; h < MPL; ++h) {
+          const int i = lane + 32 * h;
+          if (i < E * NQ) {
+            slot[L::LS_A + i] = mra[h];
+            slot[L::LS_B + i] = mrb[h];
+          }
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < UPL; ++h) {
+          const int i = lane + 32 * h;
+          if (i < E * 3 * NB) slot[L::LS_A + i] = ur[h];
+        }
+      }
+      __syncwarp();
+      vp_arrive(&fullL[sl]);
+    }
+  } else if (warp <= L::NG) {
+    // ======================= G: per-qp data, pair weights, stage z =======================
+    const int gtid = tid - 32;
+    constexpr int NGT = 32 * L::NG;
+    // phase-2 mapping: warp-uniform pair group h (pairs p with p % GH == h), column (el, qxy)
+    const int h2 = gtid / (32 * L::G2W), r2 = gtid - h2 * (32 * L::G2W);
+    const int el2 = r2 / Q2, qxy = r2 - el2 * Q2;
+    const int tx = qxy / Q1, ty = qxy - tx * Q1;  // T1's inner index is qx * Q1 + qy
+    const bool act2 = h2 < GH && r2 < E * Q2;
+    int64_t gi = 0;  // global item counter (T1 ring position)
+    for (int64_t it = 0;; ++it) {
+      int64_t lb;
+      int ne;
+      batch_of(it, lb, ne);
+      if (ne <= 0) break;
+      const int sl = (int)(it & 1);
+      vp_wait(&fullL[sl], (uint32_t)((it >> 1) & 1));
+      const double* slot = reinterpret_cast<const double*>(smv + L::OFF_L) + sl * L::LSLOT;
+      // ---- phase 1: per-qp data of the batch (QD is free: phase 2 of it-1 ended at the barrier)
+      vp_named_bar(1, NGT);
+      for (int t = gtid; t < L::G1T; t += NGT) {
+        const int el = t / NQ, q = t - el * NQ;
+        const int qx = q % Q1, qy = (q / Q1) % Q1, qz = q / Q2;
+        const double t0 = c_x1d[P][qx], t1 = c_x1d[P][qy], t2 = c_x1d[P][qz];
+        const double* X = slot + L::LS_X + el * 24;
+        double J[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          // edges: x at (b,c): X[1+2b+4c]-X[2b+4c]; y at (a,c): X[a+2+4c]-X[a+4c]; z at (a,b): X[a+2b+4]-X[a+2b]
+          J[i][0] = (1 - t1) * (1 - t2) * (X[3 * 1 + i] - X[3 * 0 + i]) + t1 * (1 - t2) * (X[3 * 3 + i] - X[3 * 2 + i]) +
+                    (1 - t1) * t2 * (X[3 * 5 + i] - X[3 * 4 + i]) + t1 * t2 * (X[3 * 7 + i] - X[3 * 6 + i]);
+          J[i][1] = (1 - t0) * (1 - t2) * (X[3 * 2 + i] - X[3 * 0 + i]) + t0 * (1 - t2) * (X[3 * 3 + i] - X[3 * 1 + i]) +
+                    (1 - t0) * t2 * (X[3 * 6 + i] - X[3 * 4 + i]) + t0 * t2 * (X[3 * 7 + i] - X[3 * 5 + i]);
+          J[i][2] = (1 - t0) * (1 - t1) * (X[3 * 4 + i] - X[3 * 0 + i]) + t0 * (1 - t1) * (X[3 * 5 + i] - X[3 * 1 + i]) +
+                    (1 - t0) * t1 * (X[3 * 6 + i] - X[3 * 2 + i]) + t0 * t1 * (X[3 * 7 + i] - X[3 * 3 + i]);
+        }
+        const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+        const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+        const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+        const double c10 = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+        const double c11 = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+        const double c12 = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+        const double c20 = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+        const double c21 = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+        const double c22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+        const double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+        const bool on = el < ne;
+        const double id = on ? 1.0 / det : 0.0;
+        // Ji[m][j] = cof[j][m] / det
+        const double Ji[9] = {c00 * id, c10 * id, c20 * id, c01 * id, c11 * id, c21 * id, c02 * id, c12 * id, c22 * id};
+        double* o = QDa + (el * NQ + q) * QDS;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) o[k] = Ji[k];
+        o[9] = on ? c_w1d[P][qx] * c_w1d[P][qy] * c_w1d[P][qz] * det : 0.0;
+        if constexpr (!L::CONV) {
+          o[10] = slot[L::LS_A + el * NQ + q];  // per-cell material is replicated per qp by L
+          o[11] = slot[L::LS_B + el * NQ + q];
+        } else {
+          // state at the qp: u_a and reference gradient du_a/dxi_m, 1D factors of Phi (Eq. fe1)
+          const double* U = slot + L::LS_A + el * 3 * NB;
+          double b0x[N1], b1x[N1], b0y[N1], b1y[N1], b0z[N1], b1z[N1];
+#pragma unroll
+          for (int i = 0; i < N1; ++i) {
+            b0x[i] = Bt(0, qx, i); b1x[i] = Bt(1, qx, i);
+            b0y[i] = Bt(0, qy, i); b1y[i] = Bt(1, qy, i);
+            b0z[i] = Bt(0, qz, i); b1z[i] = Bt(1, qz, i);
+          }
+          double uq[3], du[3][3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            double s0 = 0, sx = 0, sy = 0, sz = 0;
+#pragma unroll
+            for (int kz = 0; kz < N1; ++kz) {
+              double y00 = 0, y01 = 0, y10 = 0;
+#pragma unroll
+              for (int ky = 0; ky < N1; ++ky) {
+                double x0 = 0, x1 = 0;
+#pragma unroll
+                for (int kx = 0; kx < N1; ++kx) {
+                  const double v = U[a * NB + kx + N1 * (ky + N1 * kz)];
+                  x0 = fma(b0x[kx], v, x0);
+                  x1 = fma(b1x[kx], v, x1);
+                }
+                y00 = fma(b0y[ky], x0, y00);
+                y01 = fma(b1y[ky], x0, y01);
+                y10 = fma(b0y[ky], x1, y10);
+              }
+              s0 = fma(b0z[kz], y00, s0);
+              sz = fma(b1z[kz], y00, sz);
+              sy = fma(b0z[kz], y01, sy);
+              sx = fma(b0z[kz], y10, sx);
+            }
+            uq[a] = s0;
+            du[a][0] = sx;
+            du[a][1] = sy;
+            du[a][2] = sz;
+          }
+#pragma unroll
+          for (int n = 0; n < 3; ++n) o[10 + n] = Ji[3 * n] * uq[0] + Ji[3 * n + 1] * uq[1] + Ji[3 * n + 2] * uq[2];
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)  // du_a/dx_j = sum_m du_a/dxi_m Ji[m][j]
+              o[13 + 3 * a + j] = du[a][0] * Ji[j] + du[a][1] * Ji[3 + j] + du[a][2] * Ji[6 + j];
+        }
+      }
+      vp_arrive(&emptyL[sl]);
+      vp_named_bar(1, NGT);
+      // ---- phase 2: items
+      auto item = [&](auto Ic) {
+        constexpr int I = decltype(Ic)::value;
+        constexpr int ia = IT::a(I), ib = IT::b(I), NP = IT::np(I);
+        const int s = (int)(gi % S);
+        vp_wait(&emptyT[s], (uint32_t)(((gi / S) & 1) ^ 1));
+        double* T1 = reinterpret_cast<double*>(smv + L::OFF_T1 + s * L::T1SLOT);
+        if (act2) {
+#pragma unroll
+          for (int p = 0; p < NP; ++p) {
+            if (p % GH != h2) continue;
+            const int m = IT::pm(I, p), n = IT::pn(I, p);
+            double Wq[Q1];
+#pragma unroll
+            for (int qz = 0; qz < Q1; ++qz) {
+              const double* o = QDa + (el2 * NQ + tx + Q1 * ty + Q2 * qz) * QDS;
+              const double dw = o[9];
+              double w;
+              if constexpr (!L::CONV) {
+                const double lam = o[10], mu = o[11];
+                if (ia == ib) {
+                  const double g = o[3 * m] * o[3 * n] + o[3 * m + 1] * o[3 * n + 1] + o[3 * m + 2] * o[3 * n + 2];
+                  w = dw * ((lam + mu) * o[3 * m + ia] * o[3 * n + ia] + mu * g);
+                } else {
+                  w = dw * (lam * o[3 * m + ia] * o[3 * n + ib] + mu * o[3 * m + ib] * o[3 * n + ia]);
+                }
+              } else {
+                if (n < 3) w = dw * o[10 + n];                    // (Ji u)_n, advection
+                else w = dw * o[13 + 3 * ia + ib];                // du_a/dx_b, reaction
+              }
+              Wq[qz] = w;
+            }
+            const int az = m == 2, bz = n == 2;
+            double* out = T1 + (el2 * IT::NPMAX + p) * N1 * N1 * QQP + qxy;
+#pragma unroll
+            for (int a = 0; a < N1; ++a)
+#pragma unroll
+              for (int bb = 0; bb < N1; ++bb) {
+                double sacc = 0.0;
+#pragma unroll
+                for (int qz = 0; qz < Q1; ++qz) sacc = fma(Wq[qz], c_zzv[P][az][bz][qz][a][bb], sacc);
+                out[(a * N1 + bb) * QQP] = sacc;
+              }
+          }
+        }
+        vp_arrive(&fullT[s]);
+        ++gi;
+      };
+      vp_static_for<0, NITEM>(item);
+    }
+  } else {
+    // ======================= X: stages y and x per item, K staging, TMA store =======================
+    const int xtid = tid - 32 * (1 + L::NG);
+    constexpr int NXT = 32 * L::NX;
+    int64_t gi = 0;
+    for (int64_t it = 0;; ++it) {
+      int64_t lb;
+      int ne;
+      batch_of(it, lb, ne);
+      if (ne <= 0) break;
+      auto item = [&](auto Ic) {
+        constexpr int I = decltype(Ic)::value;
+        constexpr int ia = IT::a(I), ib_ = IT::b(I), NP = IT::np(I);
+        constexpr bool SYM = IT::sym(I), MIR = IT::mirror(I);
+        constexpr int TPE = SYM ? L::NSYM : L::NFULL;
+        const int el = xtid / TPE, r = xtid - el * TPE;
+        const bool xact = xtid < E * TPE;
+        int iz = 0, jz = 0, iy = 0, jy = 0;
+        if constexpr (SYM) {
+          constexpr int YP = N1 * N1, YPS = N1 * (N1 + 1) / 2, TOFF = YP * (N1 * (N1 - 1) / 2);
+          if (r < TOFF) {
+            int c = r / YP;
+            const int yp = r - c * YP;
+            iy = yp / N1;
+            jy = yp - iy * N1;
+            for (int a = 0; a < N1; ++a) {
+              if (c < N1 - 1 - a) { iz = a; jz = a + 1 + c; break; }
+              c -= N1 - 1 - a;
+            }
+          } else {
+            const int rr = r - TOFF;
+            iz = jz = rr / YPS;
+            int c = rr - iz * YPS;
+            for (int a = 0; a < N1; ++a) {
+              if (c < N1 - a) { iy = a; jy = a + c; break; }
+              c -= N1 - a;
+            }
+          }
+        } else {
+          const int zp = r / (N1 * N1), yp = r - zp * (N1 * N1);
+          iz = zp / N1; jz = zp - iz * N1;
+          iy = yp / N1; jy = yp - iy * N1;
+        }
+        const int s = (int)(gi % S);
+        vp_wait(&fullT[s], (uint32_t)((gi / S) & 1));
+        const double* T1e = reinterpret_cast<const double*>(smv + L::OFF_T1 + s * L::T1SLOT) +
+                            (xact ? el : 0) * IT::NPMAX * N1 * N1 * QQP;
+        double acc[N1][N1];
+        if (xact) {
+          double Byp[4][Q1];
+#pragma unroll
+          for (int q = 0; q < Q1; ++q)
+#pragma unroll
+            for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+              for (int b2 = 0; b2 < 2; ++b2) Byp[a2 * 2 + b2][q] = Bt(a2, q, iy) * Bt(b2, q, jy);
+          double Sx[4][Q1];
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int q = 0; q < Q1; ++q) Sx[c][q] = 0.0;
+          constexpr int NOPS = SYM ? (NP == 1 ? 1 : 9) : NP;
+#pragma unroll
+          for (int op = 0; op < NOPS; ++op) {
+            int m, n, pidx, zidx;
+            if constexpr (SYM) {
+              if constexpr (NP == 1) {
+                m = IT::pm(I, 0); n = IT::pn(I, 0); pidx = 0; zidx = iz * N1 + jz;
+              } else {
+                m = op / 3; n = op % 3;
+                const int mm = m < n ? m : n, nn = m < n ? n : m;
+                pidx = mm == 0 ? nn : (mm == 1 ? 2 + nn : 5);
+                zidx = (m > n) ? (jz * N1 + iz) : (iz * N1 + jz);
+              }
+            } else {
+              m = IT::pm(I, op); n = IT::pn(I, op); pidx = op; zidx = iz * N1 + jz;
+            }
+            const int ay = m == 1, by = n == 1, cls = (m == 0) * 2 + (n == 0);
+            const double* src = T1e + (pidx * N1 * N1 + zidx) * QQP;
+            double tv[QQP];
+#pragma unroll
+            for (int hh = 0; hh < Q2 / 2; ++hh) {
+              const double2 v = reinterpret_cast<const double2*>(src)[hh];
+              tv[2 * hh] = v.x;
+              tv[2 * hh + 1] = v.y;
+            }
+            if (Q2 & 1) tv[Q2 - 1] = src[Q2 - 1];
+#pragma unroll
+            for (int qx = 0; qx < Q1; ++qx)
+#pragma unroll
+              for (int qy = 0; qy < Q1; ++qy)
+                Sx[cls][qx] = fma(Byp[ay * 2 + by][qy], tv[qx * Q1 + qy], Sx[cls][qx]);
+          }
+#pragma unroll
+          for (int a = 0; a < N1; ++a)
+#pragma unroll
+            for (int bb = 0; bb < N1; ++bb) acc[a][bb] = 0.0;
+#pragma unroll
+          for (int qx = 0; qx < Q1; ++qx)
+#pragma unroll
+            for (int ax = 0; ax < 2; ++ax) {
+              double u[N1];
+#pragma unroll
+              for (int bb = 0; bb < N1; ++bb) u[bb] = Bt(0, qx, bb) * Sx[ax * 2 + 0][qx] + Bt(1, qx, bb) * Sx[ax * 2 + 1][qx];
+#pragma unroll
+              for (int a = 0; a < N1; ++a)
+#pragma unroll
+                for (int bb = 0; bb < N1; ++bb) acc[a][bb] = fma(Bt(ax, qx, a), u[bb], acc[a][bb]);
+            }
+        }
+        vp_arrive(&emptyT[s]);
+        ++gi;
+        if constexpr (I == 0) {
+          // the store of batch it-1 has finished reading K staging (elected thread, before this barrier)
+          vp_named_bar(2, NXT);
+        }
+        if (xact && el < ne) {
+          double* Kc = Kst + el * NDOF * NDOF;
+          const int ib = N1 * (iy + N1 * iz), jb = N1 * (jy + N1 * jz);
+          const bool mir_in = SYM && (iz < jz || iy < jy);
+#pragma unroll
+          for (int a = 0; a < N1; ++a)
+#pragma unroll
+            for (int bb = 0; bb < N1; ++bb) {
+              const double v = acc[a][bb];
+              Kc[(ia * NB + ib + a) * NDOF + ib_ * NB + jb + bb] = v;
+              if (mir_in) Kc[(ia * NB + jb + bb) * NDOF + ib_ * NB + ib + a] = v;
+              if (MIR) Kc[(ib_ * NB + jb + bb) * NDOF + ia * NB + ib + a] = v;
+            }
+        }
+      };
+      vp_static_for<0, NITEM>(item);
+      // ---- store the batch
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      vp_named_bar(3, NXT);
+      const uint32_t bytes = (uint32_t)((size_t)ne * NDOF * NDOF * 8);
+      double* gdst = K + lb * NDOF * NDOF;
+      if (((reinterpret_cast<uintptr_t>(gdst) | bytes) & 15u) == 0) {
+        if (xtid == 0) {
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                       :: "l"(gdst), "r"(vp_u32(Kst)), "r"(bytes) : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+      } else {
+        for (int i = xtid; i < ne * NDOF * NDOF; i += NXT) gdst[i] = Kst[i];
+      }
+    }
+    if (xtid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+#undef Bt
+}
+
+template <int P, int FORM>
+static cudaError_t launch_vp_t(const fe_mesh* mh, MatArgs mat, const double* state_u, int64_t e0,
+                               int64_t e1, double* K, cudaStream_t st) {
+  using L = VPL<P, FORM>;
+  if (L::BYTES > 227 * 1024) return cudaErrorNotSupported;
+  auto kern = k_matrix_vp<P, FORM>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
+  if (err != cudaSuccess) return err;
+  int nsm = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t nbatch = (e1 - e0 + L::E - 1) / L::E;
+  const int grid = (int)(nbatch < nsm ? nbatch : nsm);
+  if (grid <= 0) return cudaSuccess;
+  kern<<<grid, L::THREADS, L::BYTES, st>>>(view_of(mh), mat.kind, (const double*)mat.a,
+                                           (const double*)mat.b, state_u, e0, e1, K);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// Returns cudaErrorNotSupported when the combination has no pipelined vector kernel
+// (FULL_D elasticity, vector mass, p > 2: the single-stage k_matrix_sfv handles those).
+cudaError_t launch_matrix_vp(const fe_mesh* mh, int form, MatArgs mat, const double* state_u,
+                             int64_t e0, int64_t e1, double* K, cudaStream_t st) {
+  if (mh->q1d != mh->order + 1 || mh->order != 2) return cudaErrorNotSupported;
+  const char* impl = std::getenv("FEB200_MATRIX_IMPL");
+  if (impl && std::strcmp(impl, "sf1") == 0) return cudaErrorNotSupported;
+  if (form == FE_FORM_ELASTICITY && mat.kind != FE_MAT_FULL_D)
+    return launch_vp_t<2, FE_FORM_ELASTICITY>(mh, mat, state_u, e0, e1, K, st);
+  if (form == FE_FORM_CONVECTIVE) return launch_vp_t<2, FE_FORM_CONVECTIVE>(mh, mat, state_u, e0, e1, K, st);
+  return cudaErrorNotSupported;
+}
+
+}  // namespace feb200
