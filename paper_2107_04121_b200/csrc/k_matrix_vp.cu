@@ -390,35 +390,71 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
       }
       vp_arrive(&emptyL[sl]);
       vp_named_bar(1, NGT);
-      // ---- phase 2: items
-      auto item = [&](auto Ic) {
-        constexpr int I = decltype(Ic)::value;
-        constexpr int ia = IT::a(I), ib = IT::b(I), NP = IT::np(I);
+      // ---- phase 2: items.  The column's per-qp data go to registers once per batch; the
+      // item loop is a runtime loop over two compiled bodies (symmetric / full pair sets) so
+      // that the code stays within the instruction cache.
+      constexpr int CD = L::CONV ? 13 : 12;  // conv: dw, (Ji u)[3], du/dx[9]; elasticity: Ji[9], dw, lam, mu
+      double cd[Q1][CD];
+#pragma unroll
+      for (int qz = 0; qz < Q1; ++qz) {
+        const double* o = QDa + ((act2 ? el2 : 0) * NQ + tx + Q1 * ty + Q2 * qz) * QDS;
+        if constexpr (L::CONV) {
+          cd[qz][0] = o[9];
+#pragma unroll
+          for (int k = 0; k < 12; ++k) cd[qz][1 + k] = o[10 + k];
+        } else {
+#pragma unroll
+          for (int k = 0; k < 12; ++k) cd[qz][k] = o[k];
+        }
+      }
+      vp_named_bar(1, NGT);  // QD may be overwritten by the next batch's phase 1 from here on
+      auto g_item = [&](auto SYMc, int ia, int ib) {
+        constexpr bool SYMI = decltype(SYMc)::value;
+        constexpr int NP = SYMI ? (L::CONV ? 1 : 6) : (L::CONV ? 4 : 9);
         const int s = (int)(gi % S);
+        // per-item weight ingredients: Ji[:, a], Ji[:, b] | du_a/dx_b
+        double ca[Q1][3], cbv[Q1][3], gab[Q1];
+#pragma unroll
+        for (int qz = 0; qz < Q1; ++qz) {
+          if constexpr (!L::CONV) {
+#pragma unroll
+            for (int m = 0; m < 3; ++m) {
+              ca[qz][m] = ia == 0 ? cd[qz][3 * m] : (ia == 1 ? cd[qz][3 * m + 1] : cd[qz][3 * m + 2]);
+              cbv[qz][m] = ib == 0 ? cd[qz][3 * m] : (ib == 1 ? cd[qz][3 * m + 1] : cd[qz][3 * m + 2]);
+            }
+            gab[qz] = 0.0;
+          } else {
+            const int k = 3 * ia + ib;
+            double g = cd[qz][4];
+#pragma unroll
+            for (int kk = 1; kk < 9; ++kk) g = k == kk ? cd[qz][4 + kk] : g;
+            gab[qz] = g;
+          }
+        }
         vp_wait(&emptyT[s], (uint32_t)(((gi / S) & 1) ^ 1));
         double* T1 = reinterpret_cast<double*>(smv + L::OFF_T1 + s * L::T1SLOT);
         if (act2) {
 #pragma unroll
           for (int p = 0; p < NP; ++p) {
             if (p % GH != h2) continue;
-            const int m = IT::pm(I, p), n = IT::pn(I, p);
+            const int m = L::CONV ? 3 : (SYMI ? vp_um(p) : p / 3);
+            const int n = L::CONV ? (SYMI ? 3 : p) : (SYMI ? vp_un(p) : p % 3);
             double Wq[Q1];
 #pragma unroll
             for (int qz = 0; qz < Q1; ++qz) {
-              const double* o = QDa + (el2 * NQ + tx + Q1 * ty + Q2 * qz) * QDS;
-              const double dw = o[9];
               double w;
               if constexpr (!L::CONV) {
-                const double lam = o[10], mu = o[11];
-                if (ia == ib) {
-                  const double g = o[3 * m] * o[3 * n] + o[3 * m + 1] * o[3 * n + 1] + o[3 * m + 2] * o[3 * n + 2];
-                  w = dw * ((lam + mu) * o[3 * m + ia] * o[3 * n + ia] + mu * g);
+                const double dw = cd[qz][9], lam = cd[qz][10], mu = cd[qz][11];
+                if (SYMI) {  // diagonal block (a,a)
+                  const double g = cd[qz][3 * m] * cd[qz][3 * n] + cd[qz][3 * m + 1] * cd[qz][3 * n + 1] +
+                                   cd[qz][3 * m + 2] * cd[qz][3 * n + 2];
+                  w = dw * ((lam + mu) * ca[qz][m] * ca[qz][n] + mu * g);
                 } else {
-                  w = dw * (lam * o[3 * m + ia] * o[3 * n + ib] + mu * o[3 * m + ib] * o[3 * n + ia]);
+                  w = dw * (lam * ca[qz][m] * cbv[qz][n] + mu * cbv[qz][m] * ca[qz][n]);
                 }
               } else {
-                if (n < 3) w = dw * o[10 + n];                    // (Ji u)_n, advection
-                else w = dw * o[13 + 3 * ia + ib];                // du_a/dx_b, reaction
+                w = n < 3 ? cd[qz][0] * cd[qz][1 + (n < 3 ? n : 0)]  // detw (Ji u)_n, advection
+                          : cd[qz][0] * gab[qz];                     // detw du_a/dx_b, reaction
               }
               Wq[qz] = w;
             }
@@ -438,7 +474,11 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
         vp_arrive(&fullT[s]);
         ++gi;
       };
-      vp_static_for<0, NITEM>(item);
+#pragma unroll 1
+      for (int i = 0; i < NITEM; ++i) {
+        if (IT::sym(i)) g_item(std::true_type{}, IT::a(i), IT::b(i));
+        else g_item(std::false_type{}, IT::a(i), IT::b(i));
+      }
     }
   } else {
     // ======================= X: stages y and x per item, K staging, TMA store =======================
@@ -450,10 +490,10 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
       int ne;
       batch_of(it, lb, ne);
       if (ne <= 0) break;
-      auto item = [&](auto Ic) {
-        constexpr int I = decltype(Ic)::value;
-        constexpr int ia = IT::a(I), ib_ = IT::b(I), NP = IT::np(I);
-        constexpr bool SYM = IT::sym(I), MIR = IT::mirror(I);
+      auto item = [&](auto SYMc, int I, int ia, int ib_) {
+        constexpr bool SYM = decltype(SYMc)::value;
+        constexpr int NP = SYM ? (L::CONV ? 1 : 6) : (L::CONV ? 4 : 9);
+        const bool MIR = IT::mirror(I);
         constexpr int TPE = SYM ? L::NSYM : L::NFULL;
         const int el = xtid / TPE, r = xtid - el * TPE;
         const bool xact = xtid < E * TPE;
@@ -507,7 +547,7 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
             int m, n, pidx, zidx;
             if constexpr (SYM) {
               if constexpr (NP == 1) {
-                m = IT::pm(I, 0); n = IT::pn(I, 0); pidx = 0; zidx = iz * N1 + jz;
+                m = 3; n = 3; pidx = 0; zidx = iz * N1 + jz;
               } else {
                 m = op / 3; n = op % 3;
                 const int mm = m < n ? m : n, nn = m < n ? n : m;
@@ -515,7 +555,10 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
                 zidx = (m > n) ? (jz * N1 + iz) : (iz * N1 + jz);
               }
             } else {
-              m = IT::pm(I, op); n = IT::pn(I, op); pidx = op; zidx = iz * N1 + jz;
+              m = L::CONV ? 3 : op / 3;
+              n = L::CONV ? op : op % 3;
+              pidx = op;
+              zidx = iz * N1 + jz;
             }
             const int ay = m == 1, by = n == 1, cls = (m == 0) * 2 + (n == 0);
             const double* src = T1e + (pidx * N1 * N1 + zidx) * QQP;
@@ -552,7 +595,7 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
         }
         vp_arrive(&emptyT[s]);
         ++gi;
-        if constexpr (I == 0) {
+        if (I == 0) {
           // the store of batch it-1 has finished reading K staging (elected thread, before this barrier)
           vp_named_bar(2, NXT);
         }
@@ -571,7 +614,11 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
             }
         }
       };
-      vp_static_for<0, NITEM>(item);
+#pragma unroll 1
+      for (int i = 0; i < NITEM; ++i) {
+        if (IT::sym(i)) item(std::true_type{}, i, IT::a(i), IT::b(i));
+        else item(std::false_type{}, i, IT::a(i), IT::b(i));
+      }
       // ---- store the batch
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       vp_named_bar(3, NXT);
