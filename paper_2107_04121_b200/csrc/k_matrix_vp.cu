@@ -31,6 +31,12 @@
 #ifndef FEB200_VP_E
 #define FEB200_VP_E 2
 #endif
+#ifndef FEB200_VP_XG
+#define FEB200_VP_XG 2
+#endif
+#ifndef FEB200_VP_S
+#define FEB200_VP_S 4
+#endif
 #ifndef FEB200_VP_GH
 #define FEB200_VP_GH 3
 #endif
@@ -56,6 +62,17 @@ __device__ __forceinline__ void vp_wait(uint64_t* bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(vp_u32(bar)), "r"(parity) : "memory");
 }
+#ifdef FEB200_VP_PROF
+__device__ unsigned long long g_vp_prof[16];
+#define VP_T(k, stmt)                                   \
+  do {                                                  \
+    const long long t0_ = clock64();                    \
+    stmt;                                               \
+    prof_[k] += (unsigned long long)(clock64() - t0_);  \
+  } while (0)
+#else
+#define VP_T(k, stmt) stmt
+#endif
 __device__ __forceinline__ void vp_named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -104,8 +121,8 @@ struct VItems<FE_FORM_ELASTICITY> {
   __host__ __device__ static constexpr int np(int i) { return i < 3 ? 6 : 9; }
   __host__ __device__ static constexpr int pm(int i, int p) { return i < 3 ? vp_um(p) : p / 3; }
   __host__ __device__ static constexpr int pn(int i, int p) { return i < 3 ? vp_un(p) : p % 3; }
-  // SYM items: ordered pairs (m, n) of the block and their unique index
-  static constexpr int NOP = 9;
+  __host__ __device__ static constexpr int pbase(int i) { return i < 3 ? 6 * i : 18 + 9 * (i - 3); }
+  static constexpr int NWP = 45;
 };
 
 template <>
@@ -121,7 +138,8 @@ struct VItems<FE_FORM_CONVECTIVE> {
   __host__ __device__ static constexpr int np(int i) { return i < 3 ? 4 : 1; }
   __host__ __device__ static constexpr int pm(int, int) { return 3; }
   __host__ __device__ static constexpr int pn(int i, int p) { return i < 3 ? p : 3; }
-  static constexpr int NOP = 1;
+  __host__ __device__ static constexpr int pbase(int i) { return i < 3 ? 4 * i : 12 + (i - 3); }
+  static constexpr int NWP = 18;
 };
 
 template <int P, int FORM>
@@ -132,15 +150,17 @@ struct VPL {
   static constexpr int E = FEB200_VP_E;                  // cells per batch
   static constexpr int GH = FEB200_VP_GH;                // G threads per column (pair split)
   static constexpr int QQP = (Q2 + 1) / 2 * 2;
-  static constexpr int QDS = IT::QD | 1;                 // odd per-qp stride (banks)
+  static constexpr int NWP = IT::NWP;                    // pair weights per qp (all items)
   static constexpr int G1T = E * NQ;                     // phase-1 tasks (per qp)
   static constexpr int G2W = (E * Q2 + 31) / 32;         // warps per pair group (warp-uniform group)
   static constexpr int NG = ((G1T + 31) / 32 > GH * G2W) ? (G1T + 31) / 32 : GH * G2W;
   static constexpr int NFULL = N1 * N1 * N1 * N1;        // (z pair, y pair) tasks, ordered
   static constexpr int NSYM = N1 * N1 * (N1 * (N1 - 1) / 2) + N1 * (N1 * (N1 + 1) / 2);
-  static constexpr int NX = (E * NFULL + 31) / 32;
+  static constexpr int XG = FEB200_VP_XG;                // X groups working on alternate items
+  static constexpr int NXW = (E * NFULL + 31) / 32;      // warps per X group
+  static constexpr int NX = XG * NXW;
   static constexpr int THREADS = 32 * (1 + NG + NX);
-  static constexpr int S = 3;                            // T1 ring depth (items)
+  static constexpr int S = FEB200_VP_S;                  // T1 ring depth (items)
   static constexpr bool CONV = FORM == FE_FORM_CONVECTIVE;
   // L slot (doubles): coords [E][24], material a/b [E][NQ] | state [E][3][NB]
   static constexpr int LS_X = 0, LS_A = E * 24, LS_B = LS_A + E * NQ, LS_U = LS_B + E * NQ;
@@ -150,10 +170,10 @@ struct VPL {
   static constexpr size_t OFF_K = 0;
   static constexpr size_t OFF_T1 = (OFF_K + KBYTES + 127) / 128 * 128;
   static constexpr size_t OFF_QD = OFF_T1 + S * T1SLOT;
-  static constexpr size_t OFF_L = OFF_QD + size_t(E) * NQ * QDS * 8;
+  static constexpr size_t OFF_L = OFF_QD + size_t(E) * IT::NWP * NQ * 8;
   static constexpr size_t OFF_IDX = OFF_L + 2 * size_t(LSLOT) * 8;       // [2][E][8 + NB] int32
   static constexpr size_t OFF_BAR = (OFF_IDX + 2 * size_t(E) * (8 + NB) * 4 + 15) / 16 * 16;
-  static constexpr size_t BYTES = OFF_BAR + 16 * 8;
+  static constexpr size_t BYTES = OFF_BAR + (4 + 2 * S) * 8;
 };
 
 template <int P, int FORM>
@@ -163,18 +183,22 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
   using L = VPL<P, FORM>;
   using IT = typename L::IT;
   constexpr int N1 = L::N1, Q1 = L::Q1, NB = L::NB, NQ = L::NQ, Q2 = L::Q2, E = L::E, QQP = L::QQP;
-  constexpr int NDOF = L::NDOF, QDS = L::QDS, NITEM = IT::NITEM, S = L::S, GH = L::GH;
+  constexpr int NDOF = L::NDOF, NITEM = IT::NITEM, S = L::S, GH = L::GH;
   extern __shared__ __align__(128) unsigned char smv[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smv + L::OFF_BAR);
   uint64_t* fullL = bars + 0;   // [2]
   uint64_t* emptyL = bars + 2;  // [2]
-  uint64_t* fullT = bars + 4;   // [S]
-  uint64_t* emptyT = bars + 8;  // [S]
+  uint64_t* fullT = bars + 4;          // [S]
+  uint64_t* emptyT = bars + 4 + L::S;  // [S]
   double* Kst = reinterpret_cast<double*>(smv + L::OFF_K);
-  double* QDa = reinterpret_cast<double*>(smv + L::OFF_QD);
+  double* Wsm = reinterpret_cast<double*>(smv + L::OFF_QD);  // [E][NWP][NQ] pair weights
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t nloc = e1 - e0;
   const int64_t nbatch = (nloc + E - 1) / E;
+#ifdef FEB200_VP_PROF
+  unsigned long long prof_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long tstart_ = clock64();
+#endif
   if (tid == 0) {
     vp_bar_init(&fullL[0], 32);
     vp_bar_init(&fullL[1], 32);
@@ -182,7 +206,7 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
     vp_bar_init(&emptyL[1], 32 * L::NG);
     for (int s = 0; s < S; ++s) {
       vp_bar_init(&fullT[s], 32 * L::NG);
-      vp_bar_init(&emptyT[s], 32 * L::NX);
+      vp_bar_init(&emptyT[s], 32 * L::NXW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -256,7 +280,7 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
       }
       __syncwarp();
       load_idx(it + 1);  // other half of the index ring (read in iteration it - 1)
-      vp_wait(&emptyL[sl], (uint32_t)(((it >> 1) & 1) ^ 1));
+      VP_T(1, vp_wait(&emptyL[sl], (uint32_t)(((it >> 1) & 1) ^ 1)));
       double* slot = reinterpret_cast<double*>(smv + L::OFF_L) + sl * L::LSLOT;
 #pragma unroll
       for (int h = 0; h < XPL; ++h) {
@@ -298,10 +322,10 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
       batch_of(it, lb, ne);
       if (ne <= 0) break;
       const int sl = (int)(it & 1);
-      vp_wait(&fullL[sl], (uint32_t)((it >> 1) & 1));
+      VP_T(2, vp_wait(&fullL[sl], (uint32_t)((it >> 1) & 1)));
       const double* slot = reinterpret_cast<const double*>(smv + L::OFF_L) + sl * L::LSLOT;
-      // ---- phase 1: per-qp data of the batch (QD is free: phase 2 of it-1 ended at the barrier)
-      vp_named_bar(1, NGT);
+      // ---- phase 1: pair weights of the batch (Wsm is free once every G thread left phase 2 of it-1)
+      VP_T(0, vp_named_bar(1, NGT));
       for (int t = gtid; t < L::G1T; t += NGT) {
         const int el = t / NQ, q = t - el * NQ;
         const int qx = q % Q1, qy = (q / Q1) % Q1, qz = q / Q2;
@@ -332,13 +356,31 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
         const double id = on ? 1.0 / det : 0.0;
         // Ji[m][j] = cof[j][m] / det
         const double Ji[9] = {c00 * id, c10 * id, c20 * id, c01 * id, c11 * id, c21 * id, c02 * id, c12 * id, c22 * id};
-        double* o = QDa + (el * NQ + q) * QDS;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) o[k] = Ji[k];
-        o[9] = on ? c_w1d[P][qx] * c_w1d[P][qy] * c_w1d[P][qz] * det : 0.0;
+        const double dw = on ? c_w1d[P][qx] * c_w1d[P][qy] * c_w1d[P][qz] * det : 0.0;
+        // all pair weights W^{ab}_{mn}(q) of the batch, item-major: Wsm[el][PB(i) + p][q]
+        double* Wq = Wsm + el * L::NWP * NQ + q;
         if constexpr (!L::CONV) {
-          o[10] = slot[L::LS_A + el * NQ + q];  // per-cell material is replicated per qp by L
-          o[11] = slot[L::LS_B + el * NQ + q];
+          const double lam = slot[L::LS_A + el * NQ + q];  // per-cell material replicated per qp by L
+          const double mu = slot[L::LS_B + el * NQ + q];
+          // diagonal blocks (a,a), unique pairs m <= n: dw ((lam + mu) Ji[m][a] Ji[n][a] + mu (Ji Ji^T)_mn)
+#pragma unroll
+          for (int u = 0; u < 6; ++u) {
+            const int m = vp_um(u), n = vp_un(u);
+            const double g = mu * (Ji[3 * m] * Ji[3 * n] + Ji[3 * m + 1] * Ji[3 * n + 1] + Ji[3 * m + 2] * Ji[3 * n + 2]);
+#pragma unroll
+            for (int a2 = 0; a2 < 3; ++a2)
+              Wq[(6 * a2 + u) * NQ] = dw * ((lam + mu) * Ji[3 * m + a2] * Ji[3 * n + a2] + g);
+          }
+          // off-diagonal blocks (0,1) (0,2) (1,2): dw (lam Ji[m][a] Ji[n][b] + mu Ji[m][b] Ji[n][a])
+#pragma unroll
+          for (int ob = 0; ob < 3; ++ob) {
+            const int a2 = ob == 2 ? 1 : 0, b2 = ob == 0 ? 1 : 2;
+#pragma unroll
+            for (int pp = 0; pp < 9; ++pp) {
+              const int m = pp / 3, n = pp % 3;
+              Wq[(18 + 9 * ob + pp) * NQ] = dw * (lam * Ji[3 * m + a2] * Ji[3 * n + b2] + mu * Ji[3 * m + b2] * Ji[3 * n + a2]);
+            }
+          }
         } else {
           // state at the qp: u_a and reference gradient du_a/dxi_m, 1D factors of Phi (Eq. fe1)
           const double* U = slot + L::LS_A + el * 3 * NB;
@@ -379,59 +421,35 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
             du[a][1] = sy;
             du[a][2] = sz;
           }
+          // diagonal blocks: (3,n) advection dw (Ji u)_n, (3,3) reaction dw du_a/dx_a
 #pragma unroll
-          for (int n = 0; n < 3; ++n) o[10 + n] = Ji[3 * n] * uq[0] + Ji[3 * n + 1] * uq[1] + Ji[3 * n + 2] * uq[2];
+          for (int n = 0; n < 3; ++n) {
+            const double jun = dw * (Ji[3 * n] * uq[0] + Ji[3 * n + 1] * uq[1] + Ji[3 * n + 2] * uq[2]);
 #pragma unroll
-          for (int a = 0; a < 3; ++a)
+            for (int a2 = 0; a2 < 3; ++a2) Wq[(4 * a2 + n) * NQ] = jun;
+          }
+          // du_a/dx_b = sum_m du_a/dxi_m Ji[m][b]
 #pragma unroll
-            for (int j = 0; j < 3; ++j)  // du_a/dx_j = sum_m du_a/dxi_m Ji[m][j]
-              o[13 + 3 * a + j] = du[a][0] * Ji[j] + du[a][1] * Ji[3 + j] + du[a][2] * Ji[6 + j];
+          for (int a2 = 0; a2 < 3; ++a2)
+#pragma unroll
+            for (int b2 = 0; b2 < 3; ++b2) {
+              const double g = dw * (du[a2][0] * Ji[b2] + du[a2][1] * Ji[3 + b2] + du[a2][2] * Ji[6 + b2]);
+              // item of block (a2, b2): diagonal -> pair 3 of item a2; off-diagonal -> item 3..8
+              const int slotw = a2 == b2 ? 4 * a2 + 3 : 12 + (2 * a2 + (b2 > a2 ? b2 - 1 : b2));
+              Wq[slotw * NQ] = g;
+            }
         }
       }
       vp_arrive(&emptyL[sl]);
-      vp_named_bar(1, NGT);
-      // ---- phase 2: items.  The column's per-qp data go to registers once per batch; the
-      // item loop is a runtime loop over two compiled bodies (symmetric / full pair sets) so
-      // that the code stays within the instruction cache.
-      constexpr int CD = L::CONV ? 13 : 12;  // conv: dw, (Ji u)[3], du/dx[9]; elasticity: Ji[9], dw, lam, mu
-      double cd[Q1][CD];
-#pragma unroll
-      for (int qz = 0; qz < Q1; ++qz) {
-        const double* o = QDa + ((act2 ? el2 : 0) * NQ + tx + Q1 * ty + Q2 * qz) * QDS;
-        if constexpr (L::CONV) {
-          cd[qz][0] = o[9];
-#pragma unroll
-          for (int k = 0; k < 12; ++k) cd[qz][1 + k] = o[10 + k];
-        } else {
-#pragma unroll
-          for (int k = 0; k < 12; ++k) cd[qz][k] = o[k];
-        }
-      }
-      vp_named_bar(1, NGT);  // QD may be overwritten by the next batch's phase 1 from here on
-      auto g_item = [&](auto SYMc, int ia, int ib) {
+      VP_T(0, vp_named_bar(1, NGT));
+      // ---- phase 2: stage z of every item, one compiled body per item kind (symmetric /
+      // full pair set) inside a runtime item loop, so the code stays in the instruction cache
+      auto g_item = [&](auto SYMc, int i) {
         constexpr bool SYMI = decltype(SYMc)::value;
         constexpr int NP = SYMI ? (L::CONV ? 1 : 6) : (L::CONV ? 4 : 9);
         const int s = (int)(gi % S);
-        // per-item weight ingredients: Ji[:, a], Ji[:, b] | du_a/dx_b
-        double ca[Q1][3], cbv[Q1][3], gab[Q1];
-#pragma unroll
-        for (int qz = 0; qz < Q1; ++qz) {
-          if constexpr (!L::CONV) {
-#pragma unroll
-            for (int m = 0; m < 3; ++m) {
-              ca[qz][m] = ia == 0 ? cd[qz][3 * m] : (ia == 1 ? cd[qz][3 * m + 1] : cd[qz][3 * m + 2]);
-              cbv[qz][m] = ib == 0 ? cd[qz][3 * m] : (ib == 1 ? cd[qz][3 * m + 1] : cd[qz][3 * m + 2]);
-            }
-            gab[qz] = 0.0;
-          } else {
-            const int k = 3 * ia + ib;
-            double g = cd[qz][4];
-#pragma unroll
-            for (int kk = 1; kk < 9; ++kk) g = k == kk ? cd[qz][4 + kk] : g;
-            gab[qz] = g;
-          }
-        }
-        vp_wait(&emptyT[s], (uint32_t)(((gi / S) & 1) ^ 1));
+        const double* Wi = Wsm + (act2 ? el2 : 0) * L::NWP * NQ + IT::pbase(i) * NQ + tx + Q1 * ty;
+        VP_T(3, vp_wait(&emptyT[s], (uint32_t)(((gi / S) & 1) ^ 1)));
         double* T1 = reinterpret_cast<double*>(smv + L::OFF_T1 + s * L::T1SLOT);
         if (act2) {
 #pragma unroll
@@ -441,23 +459,7 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
             const int n = L::CONV ? (SYMI ? 3 : p) : (SYMI ? vp_un(p) : p % 3);
             double Wq[Q1];
 #pragma unroll
-            for (int qz = 0; qz < Q1; ++qz) {
-              double w;
-              if constexpr (!L::CONV) {
-                const double dw = cd[qz][9], lam = cd[qz][10], mu = cd[qz][11];
-                if (SYMI) {  // diagonal block (a,a)
-                  const double g = cd[qz][3 * m] * cd[qz][3 * n] + cd[qz][3 * m + 1] * cd[qz][3 * n + 1] +
-                                   cd[qz][3 * m + 2] * cd[qz][3 * n + 2];
-                  w = dw * ((lam + mu) * ca[qz][m] * ca[qz][n] + mu * g);
-                } else {
-                  w = dw * (lam * ca[qz][m] * cbv[qz][n] + mu * cbv[qz][m] * ca[qz][n]);
-                }
-              } else {
-                w = n < 3 ? cd[qz][0] * cd[qz][1 + (n < 3 ? n : 0)]  // detw (Ji u)_n, advection
-                          : cd[qz][0] * gab[qz];                     // detw du_a/dx_b, reaction
-              }
-              Wq[qz] = w;
-            }
+            for (int qz = 0; qz < Q1; ++qz) Wq[qz] = Wi[p * NQ + Q2 * qz];
             const int az = m == 2, bz = n == 2;
             double* out = T1 + (el2 * IT::NPMAX + p) * N1 * N1 * QQP + qxy;
 #pragma unroll
@@ -476,15 +478,15 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
       };
 #pragma unroll 1
       for (int i = 0; i < NITEM; ++i) {
-        if (IT::sym(i)) g_item(std::true_type{}, IT::a(i), IT::b(i));
-        else g_item(std::false_type{}, IT::a(i), IT::b(i));
+        if (IT::sym(i)) g_item(std::true_type{}, i);
+        else g_item(std::false_type{}, i);
       }
     }
   } else {
     // ======================= X: stages y and x per item, K staging, TMA store =======================
-    const int xtid = tid - 32 * (1 + L::NG);
-    constexpr int NXT = 32 * L::NX;
-    int64_t gi = 0;
+    const int xall = tid - 32 * (1 + L::NG);
+    const int xg = xall / (32 * L::NXW), xtid = xall - xg * 32 * L::NXW;  // group, thread in group
+    constexpr int NXA = 32 * L::NX;
     for (int64_t it = 0;; ++it) {
       int64_t lb;
       int ne;
@@ -523,8 +525,9 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
           iz = zp / N1; jz = zp - iz * N1;
           iy = yp / N1; jy = yp - iy * N1;
         }
+        const int64_t gi = it * NITEM + I;
         const int s = (int)(gi % S);
-        vp_wait(&fullT[s], (uint32_t)((gi / S) & 1));
+        VP_T(4, vp_wait(&fullT[s], (uint32_t)((gi / S) & 1)));
         const double* T1e = reinterpret_cast<const double*>(smv + L::OFF_T1 + s * L::T1SLOT) +
                             (xact ? el : 0) * IT::NPMAX * N1 * N1 * QQP;
         double acc[N1][N1];
@@ -594,10 +597,10 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
             }
         }
         vp_arrive(&emptyT[s]);
-        ++gi;
-        if (I == 0) {
-          // the store of batch it-1 has finished reading K staging (elected thread, before this barrier)
-          vp_named_bar(2, NXT);
+        if (I == xg) {
+          // first item of this group in the batch: the store of batch it-1 has finished reading
+          // K staging (elected thread, before this barrier of all X threads)
+          VP_T(5, vp_named_bar(2, NXA));
         }
         if (xact && el < ne) {
           double* Kc = Kst + el * NDOF * NDOF;
@@ -615,28 +618,36 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
         }
       };
 #pragma unroll 1
-      for (int i = 0; i < NITEM; ++i) {
+      for (int i = xg; i < NITEM; i += L::XG) {
         if (IT::sym(i)) item(std::true_type{}, i, IT::a(i), IT::b(i));
         else item(std::false_type{}, i, IT::a(i), IT::b(i));
       }
       // ---- store the batch
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      vp_named_bar(3, NXT);
+      VP_T(6, vp_named_bar(3, NXA));
       const uint32_t bytes = (uint32_t)((size_t)ne * NDOF * NDOF * 8);
       double* gdst = K + lb * NDOF * NDOF;
       if (((reinterpret_cast<uintptr_t>(gdst) | bytes) & 15u) == 0) {
-        if (xtid == 0) {
+        if (xall == 0) {
           asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                        :: "l"(gdst), "r"(vp_u32(Kst)), "r"(bytes) : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
       } else {
-        for (int i = xtid; i < ne * NDOF * NDOF; i += NXT) gdst[i] = Kst[i];
+        for (int i = xall; i < ne * NDOF * NDOF; i += NXA) gdst[i] = Kst[i];
       }
     }
-    if (xtid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (xall == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
+#ifdef FEB200_VP_PROF
+  if (lane == 0) {
+    for (int k = 0; k < 7; ++k) if (prof_[k]) atomicAdd(&g_vp_prof[k], prof_[k]);
+    const int role = warp == 0 ? 0 : (warp <= L::NG ? 1 : 2);
+    atomicAdd(&g_vp_prof[8 + role], (unsigned long long)(clock64() - tstart_));
+    atomicAdd(&g_vp_prof[12 + role], 1ull);
+  }
+#endif
 #undef Bt
 }
 
@@ -674,3 +685,15 @@ cudaError_t launch_matrix_vp(const fe_mesh* mh, int form, MatArgs mat, const dou
 }
 
 }  // namespace feb200
+
+#ifdef FEB200_VP_PROF
+extern "C" int fe_debug_vp_prof(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, feb200::g_vp_prof, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(feb200::g_vp_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

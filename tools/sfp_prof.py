@@ -13,26 +13,30 @@ sys.path.insert(0, ROOT)
 import fe_inputs as fi  # noqa: E402
 import paper_2107_04121_b200 as fe  # noqa: E402
 
-pr = fi.make_config(sys.argv[1] if len(sys.argv) > 1 else "C2")
+cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
+pr = fi.corner_subproblem(fi.make_config("C5"), 64) if cfg == "C5t" else fi.make_config(cfg)
+VP = pr.form in (fi.ELASTICITY, fi.CONVECTIVE)
+state = torch.from_numpy(pr.u).cuda() if pr.form == fi.CONVECTIVE else None
 mesh = fe.Mesh(torch.from_numpy(pr.coords), torch.from_numpy(pr.conn), pr.p, pr.q1d,
                dof_conn=torch.from_numpy(pr.dof_conn), n_nodes=pr.n_nodes)
-a = torch.from_numpy(pr.mat_a).cuda()
+a = None if pr.mat_a is None else torch.from_numpy(pr.mat_a).cuda()
 b = None if pr.mat_b is None else torch.from_numpy(pr.mat_b).cuda()
 lib = fe.lib()
 buf = (ctypes.c_ulonglong * 16)()
 for _ in range(3):
-    mesh.element_matrices(pr.form, pr.mat_kind, a, b)
-lib.fe_debug_sfp_prof(buf, 1)
+    mesh.element_matrices(pr.form, pr.mat_kind, a, b, state)
+(lib.fe_debug_vp_prof if VP else lib.fe_debug_sfp_prof)(buf, 1)
 n = 20
 for _ in range(n):
-    mesh.element_matrices(pr.form, pr.mat_kind, a, b)
-lib.fe_debug_sfp_prof(buf, 1)
+    mesh.element_matrices(pr.form, pr.mat_kind, a, b, state)
+(lib.fe_debug_vp_prof if VP else lib.fe_debug_sfp_prof)(buf, 1)
 v = np.array(list(buf), dtype=np.float64)
-names = ["L wait conn", "L wait emptyL", "G wait fullL", "G wait emptyT", "X wait fullT",
-         "X bar1", "X bar2"]
+names = (["G bar", "L wait emptyL", "G wait fullL", "G wait emptyT", "X wait fullT", "X bar2", "X bar3"]
+         if VP else ["L wait conn", "L wait emptyL", "G wait fullL", "G wait emptyT", "X wait fullT",
+                     "X bar1", "X bar2"])
 warps = {0: v[12], 1: v[13], 2: v[14]}
 tot = {0: v[8], 1: v[9], 2: v[10]}
-role = [0, 0, 1, 1, 2, 2, 2]
+role = [1 if VP else 0, 0, 1, 1, 2, 2, 2]
 for k, nm in enumerate(names):
     r = role[k]
     print(f"{nm:16s} {v[k] / max(tot[r], 1):6.1%} of role time")
