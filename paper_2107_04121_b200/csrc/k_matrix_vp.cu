@@ -24,6 +24,7 @@
 #include "fe_const.cuh"
 #include "fe_device.cuh"
 #include "fe_internal.h"
+#include "vp_tasks.h"
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -36,6 +37,9 @@
 #endif
 #ifndef FEB200_VP_S
 #define FEB200_VP_S 4
+#endif
+#ifndef FEB200_VP_TASKMAP
+#define FEB200_VP_TASKMAP 1
 #endif
 #ifndef FEB200_VP_GH
 #define FEB200_VP_GH 3
@@ -161,6 +165,7 @@ struct VPL {
   static constexpr int NX = XG * NXW;
   static constexpr int THREADS = 32 * (1 + NG + NX);
   static constexpr int S = FEB200_VP_S;                  // T1 ring depth (items)
+  static constexpr bool TASKMAP = FEB200_VP_TASKMAP && P == 2 && E == 2 && NXW == 6;
   static constexpr bool CONV = FORM == FE_FORM_CONVECTIVE;
   // L slot (doubles): coords [E][24], material a/b [E][NQ] | state [E][3][NB]
   static constexpr int LS_X = 0, LS_A = E * 24, LS_B = LS_A + E * NQ, LS_U = LS_B + E * NQ;
@@ -487,6 +492,11 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
     const int xall = tid - 32 * (1 + L::NG);
     const int xg = xall / (32 * L::NXW), xtid = xall - xg * 32 * L::NXW;  // group, thread in group
     constexpr int NXA = 32 * L::NX;
+    int task_full = -1, task_sym = -1;
+    if constexpr (L::TASKMAP) {
+      task_full = vp_tasks_full[xtid];
+      task_sym = vp_tasks_sym[xtid];
+    }
     for (int64_t it = 0;; ++it) {
       int64_t lb;
       int ne;
@@ -497,10 +507,20 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
         constexpr int NP = SYM ? (L::CONV ? 1 : 6) : (L::CONV ? 4 : 9);
         const bool MIR = IT::mirror(I);
         constexpr int TPE = SYM ? L::NSYM : L::NFULL;
-        const int el = xtid / TPE, r = xtid - el * TPE;
-        const bool xact = xtid < E * TPE;
+        int el = xtid / TPE;
+        const int r = xtid - el * TPE;
+        bool xact = xtid < E * TPE;
         int iz = 0, jz = 0, iy = 0, jy = 0;
-        if constexpr (SYM) {
+        if constexpr (L::TASKMAP) {
+          // bank-conflict-optimised lane -> task permutation (tools/gen_vp_tasks.py)
+          const int tk = SYM ? task_sym : task_full;
+          xact = tk >= 0;
+          el = tk & 15;
+          iz = (tk >> 4) & 15;
+          jz = (tk >> 8) & 15;
+          iy = (tk >> 12) & 15;
+          jy = (tk >> 16) & 15;
+        } else if constexpr (SYM) {
           constexpr int YP = N1 * N1, YPS = N1 * (N1 + 1) / 2, TOFF = YP * (N1 * (N1 - 1) / 2);
           if (r < TOFF) {
             int c = r / YP;
