@@ -72,6 +72,27 @@ def sf_matrix_flops(form: int, p: int) -> float:
     return geo + z + y + x
 
 
+def sf_vector_matrix_flops(form: int, p: int) -> float:
+    """Flops per cell of the pipelined vector SF matrix kernel (k_matrix_vp.cu), FMA = 2:
+    phase 1 per qp (geometry + all pair weights W^{ab}_{mn}; convective: state interpolation),
+    phase 2 stage z per pair, X stages y and x per (block, z pair, y pair) task."""
+    n1 = q1 = p + 1
+    nq = q1 ** 3
+    sym_t = n1 * n1 * (n1 * (n1 - 1) // 2) + n1 * (n1 * (n1 + 1) // 2)
+    full_t = n1 ** 4
+
+    def x_task(nops):
+        return 2 * nops * q1 * q1 + 4 * q1 + q1 * 2 * (3 * n1 + 2 * n1 * n1)
+    if form == fi.ELASTICITY:
+        per_qp, nwp = GEOM + 282, 45
+        x = 3 * sym_t * x_task(9) + 3 * full_t * x_task(9)
+    else:  # convective tangent
+        per_qp, nwp = GEOM + 650, 18
+        x = 3 * full_t * x_task(4) + 6 * sym_t * x_task(1)
+    z = nwp * q1 * q1 * (2 * n1 * n1 * q1)
+    return per_qp * nq + z + x
+
+
 def sf_residual_flops(form: int, p: int) -> float:
     """Flops per cell of the sum-factorised residual kernel (k_residual_sf.cu), FMA = 2:
     1D contractions 2 D (5 + V + 12 G) n^4 plus ~(100 + 40 D) per qp of geometry / flux."""
@@ -485,8 +506,12 @@ def main():
             fl = fl_lean
         elif mode == "matrix" and uses_sf_matrix(prob.form, prob.p):
             fl = sf_matrix_flops(prob.form, prob.p) * El
+        elif mode == "matrix" and prob.form in (fi.ELASTICITY, fi.CONVECTIVE) and prob.p == 2 and \
+                prob.mat_kind != fi.MAT_FULL_D:
+            fl = sf_vector_matrix_flops(prob.form, prob.p) * El
+            impl = "sum-factorised, pipelined"
         elif mode == "matrix":
-            fl = fl_lean  # vector SF matrix kernels: flop count not modelled, lean dense count reported
+            fl = fl_lean  # single-stage vector SF kernel: flop count not modelled, lean dense count
         else:
             fl = sf_residual_flops(prob.form, prob.p) * El
         by = alg_bytes(prob.form, mode, prob.p, nb, nq, D, prob.mat_kind, esize) * El
