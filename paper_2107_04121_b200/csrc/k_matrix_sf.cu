@@ -31,12 +31,6 @@
 #ifndef FEB200_SFP_X3
 #define FEB200_SFP_X3 0
 #endif
-#ifndef FEB200_SQ
-#define FEB200_SQ 0
-#endif
-#ifndef FEB200_SQ_E
-#define FEB200_SQ_E 6
-#endif
 #ifndef FEB200_SFP_NOSTORE
 #define FEB200_SFP_NOSTORE 0
 #endif
@@ -1018,488 +1012,6 @@ static cudaError_t launch_sfp_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int6
 }
 
 
-// ---------------------------------------------------------------------------
-// Four-role variant (p <= 2): stage y gets its own warps so that the stage-x threads read
-// 12 values per task instead of 9 T1 vectors (the shared-memory data pipe is the binding
-// resource of the three-role kernel):
-//   L  loads (as k_matrix_sfp)           G  geometry + stage z -> T1 ring
-//   Y  one thread per (cell, z pair, qx): for all y pairs of the z pair and the 4 stage-x
-//      classes c = ([m == 0], [n == 0]), S_c[y pair][qx] = sum_(m,n in c) sum_qy
-//      B^{[m==1]}[qy][iy] B^{[n==1]}[qy][jy] T1^{(m,n)}[z pair][qx][qy] -> T2 ring
-//   X  one thread per (cell, z pair, y pair): stage x from its 12 values -> K staging -> TMA
-template <int P, int NUPMAX>
-struct SQL {
-  static constexpr int N1 = P + 1, Q1 = P + 1, NB = N1 * N1 * N1, NQ = Q1 * Q1 * Q1, Q2 = Q1 * Q1;
-  static constexpr int YP = N1 * N1, YPS = N1 * (N1 + 1) / 2;
-  static constexpr int NOFF = N1 * (N1 - 1) / 2;          // off-diagonal z pairs
-  static constexpr int NZP = NOFF + N1;                   // z pairs iz <= jz
-  static constexpr int TOFF = YP * NOFF;
-  static constexpr int TPE = TOFF + N1 * YPS;             // X tasks per cell
-  static constexpr int E = P == 1 ? 16 : FEB200_SQ_E;     // cells per batch (even: TMA size)
-  static constexpr int GH = 1, NGW = (E * Q2 + 31) / 32, NG = NGW;
-  static constexpr int NYW = (E * NOFF * Q1 + 31) / 32;   // Y warps for off-diagonal z pairs
-  static constexpr int NYD = (E * N1 * Q1 + 31) / 32;     // Y warps for diagonal z pairs
-  static constexpr int NY = NYW + NYD;
-  static constexpr int NX = (E * TPE + 31) / 32;
-  static constexpr int THREADS = 32 * (1 + NG + NY + NX);
-  static constexpr int T2W = 4 * Q1;                      // values per (z pair, y pair): [c][qx]
-  static constexpr size_t LSLOT = size_t(E) * (24 + (NUPMAX == 7 ? 2 : 1) * NQ) * 8;
-  static constexpr size_t T1SLOT = size_t(E) * NUPMAX * N1 * N1 * Q2 * 8;
-  static constexpr size_t T2SLOT = size_t(E) * NZP * YP * T2W * 8;
-  static constexpr size_t KSLOT = size_t(E) * NB * NB * 8;
-  static constexpr size_t OFF_K = 0;
-  static constexpr size_t OFF_T2 = OFF_K + 2 * KSLOT;
-  static constexpr size_t OFF_T1 = OFF_T2 + 2 * T2SLOT;
-  static constexpr size_t OFF_L = OFF_T1 + 2 * T1SLOT;
-  static constexpr size_t OFF_CONN = OFF_L + 2 * LSLOT;
-  static constexpr size_t OFF_BAR = (OFF_CONN + 3 * E * 8 * 4 + 15) / 16 * 16;
-  static constexpr size_t BYTES = OFF_BAR + 16 * 8;
-};
-
-template <int P, int FORM>
-__global__ void __launch_bounds__(SQL<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM != FE_FORM_DIFFUSION ? 1 : 0)>::THREADS, 1)
-    k_matrix_sq(MeshView mv, const double* __restrict__ ma, const double* __restrict__ mb,
-                int64_t e0, int64_t e1, double* __restrict__ K) {
-  constexpr bool DIFF = FORM != FE_FORM_MASS, MASS = FORM != FE_FORM_DIFFUSION;
-  constexpr int NUP = (DIFF ? 6 : 0) + (MASS ? 1 : 0);
-  constexpr int NOP = (DIFF ? 9 : 0) + (MASS ? 1 : 0);
-  constexpr int UBASE = DIFF ? 0 : 6;
-  constexpr int NCOEF = MASS && DIFF ? 2 : 1;
-  using L = SQL<P, NUP>;
-  constexpr int N1 = L::N1, Q1 = L::Q1, NB = L::NB, NQ = L::NQ, Q2 = L::Q2, E = L::E;
-  constexpr int NZP = L::NZP, NOFF = L::NOFF, YP = L::YP, T2W = L::T2W;
-  extern __shared__ __align__(128) unsigned char smp[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smp + L::OFF_BAR);
-  uint64_t* fullL = bars + 0;    // [2] L -> G
-  uint64_t* emptyL = bars + 2;   // [2] G -> L
-  uint64_t* fullT = bars + 4;    // [2] G -> Y (T1)
-  uint64_t* emptyT = bars + 6;   // [2] Y -> G
-  uint64_t* fullU = bars + 11;   // [2] Y -> X (T2)
-  uint64_t* emptyU = bars + 13;  // [2] X -> Y
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t nloc = e1 - e0;
-  const int64_t nbatch = (nloc + E - 1) / E;
-#ifdef FEB200_SFP_PROF
-  unsigned long long prof_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const long long tstart_ = clock64();
-#endif
-  if (tid == 0) {
-    for (int k = 0; k < 2; ++k) {
-      sfp_bar_init(&fullL[k], 32);
-      sfp_bar_init(&emptyL[k], 32 * L::NG);
-      sfp_bar_init(&fullT[k], 32 * L::NG);
-      sfp_bar_init(&emptyT[k], 32 * L::NY);
-      sfp_bar_init(&fullU[k], 32 * L::NY);
-      sfp_bar_init(&emptyU[k], 32 * L::NX);
-    }
-    sfp_bar_init(&bars[8], 1);
-    sfp_bar_init(&bars[9], 1);
-    sfp_bar_init(&bars[10], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-#define Bt(a, q, i) c_tab1d[P][a][q][i]
-
-  if (warp == 0) {
-    // ======================= L: loader warp =======================
-    // conn blocks arrive by TMA two batches ahead (3-deep ring, own mbarriers); the vertex
-    // coordinates of batch it + 1 are gathered into registers while batch it is handed
-    // over; coefficient blocks go by TMA straight into the slot (tx-counted on fullL).
-    int32_t* connb = reinterpret_cast<int32_t*>(smp + L::OFF_CONN);
-    uint64_t* connbar = bars + 8;  // [3]
-    auto batch_of = [&](int64_t j, int64_t& lb, int& ne) {
-      const int64_t b = blockIdx.x + j * (int64_t)gridDim.x;
-      lb = b * E;
-      ne = b < nbatch ? (int)((nloc - lb) < E ? (nloc - lb) : E) : 0;
-    };
-    auto conn_issue = [&](int64_t j) {  // lane 0
-      int64_t lb;
-      int ne;
-      batch_of(j, lb, ne);
-      if (ne <= 0) return;
-      const int k = (int)(j % 3);
-      sfp_expect_arrive(&connbar[k], (uint32_t)ne * 32u);
-      sfp_tma_load(connb + k * E * 8, mv.conn + 8 * (e0 + lb), (uint32_t)ne * 32u, &connbar[k]);
-    };
-    constexpr int XPL = (E * 24 + 31) / 32, KPL = (E * NQ + 31) / 32;
-    double xr[XPL];
-    auto coords_issue = [&](int64_t j) {
-      int64_t lb;
-      int ne;
-      batch_of(j, lb, ne);
-      if (ne <= 0) return;
-      const int k = (int)(j % 3);
-      SFP_T(0, sfp_wait(&connbar[k], (uint32_t)((j / 3) & 1)));
-      const int32_t* cb = connb + k * E * 8;
-#pragma unroll
-      for (int h = 0; h < XPL; ++h) {
-        const int i = lane + 32 * h, c = i / 24, r = i - c * 24;
-        xr[h] = (i < E * 24 && c < ne) ? mv.coords[3 * (int64_t)cb[c * 8 + r / 3] + r % 3] : 0.0;
-      }
-    };
-    if (lane == 0) {
-      conn_issue(0);
-      conn_issue(1);
-    }
-    coords_issue(0);
-    for (int64_t it = 0;; ++it) {
-      int64_t lb;
-      int ne;
-      batch_of(it, lb, ne);
-      if (ne <= 0) break;
-      const int sl = (int)(it & 1);
-      __syncwarp();
-      if (lane == 0) conn_issue(it + 2);  // ring slot (it+2)%3 was last read in iteration it-2
-      SFP_T(1, sfp_wait(&emptyL[sl], (uint32_t)(((it >> 1) & 1) ^ 1)));
-      double* slot = reinterpret_cast<double*>(smp + L::OFF_L + sl * L::LSLOT);
-      const double* ga = ma + (e0 + lb) * NQ;
-      const double* gb = NCOEF == 2 ? mb + (e0 + lb) * NQ : nullptr;
-      const uint32_t kbytes = (uint32_t)ne * NQ * 8u;
-      const bool tma_ok = (((reinterpret_cast<uintptr_t>(ga) | (NCOEF == 2 ? reinterpret_cast<uintptr_t>(gb) : 0) |
-                             kbytes) & 15u) == 0);
-      if (tma_ok) {
-        if (lane == 0) {
-          sfp_expect_tx(&fullL[sl], kbytes * NCOEF);
-          sfp_tma_load(slot + E * 24, ga, kbytes, &fullL[sl]);
-          if (NCOEF == 2) sfp_tma_load(slot + E * 24 + E * NQ, gb, kbytes, &fullL[sl]);
-        }
-      } else {
-#pragma unroll
-        for (int h = 0; h < KPL; ++h) {
-          const int i = lane + 32 * h;
-          if (i < ne * NQ) {
-            slot[E * 24 + i] = ga[i];
-            if (NCOEF == 2) slot[E * 24 + E * NQ + i] = gb[i];
-          }
-        }
-      }
-#pragma unroll
-      for (int h = 0; h < XPL; ++h) {
-        const int i = lane + 32 * h;
-        if (i < E * 24) slot[i] = xr[h];
-      }
-      sfp_arrive(&fullL[sl]);
-      coords_issue(it + 1);
-    }
-  } else if (warp <= L::NG) {
-    // ======================= G: geometry + stage z =======================
-    // GH warp-uniform groups per column; group h forms the unique pairs [ulo, uhi)
-    const int gtid0 = tid - 32;
-    const int h = gtid0 / (32 * L::NGW), gtid = gtid0 - h * 32 * L::NGW;
-    constexpr int UPH = (NUP + L::GH - 1) / L::GH;
-    const int ulo = h * UPH, uhi = (h + 1) * UPH < NUP ? (h + 1) * UPH : NUP;
-    const int el = gtid / Q2, qxy = gtid - el * Q2;
-    const int tx = qxy / Q1, ty = qxy - tx * Q1;  // T1's inner index is qx * Q1 + qy
-    const bool gact = gtid < E * Q2 && ulo < uhi;
-    const double tX = c_x1d[P][tx], tY = c_x1d[P][ty];
-    const double wxy = c_w1d[P][tx] * c_w1d[P][ty];
-    for (int64_t it = 0;; ++it) {
-      const int64_t b = blockIdx.x + it * (int64_t)gridDim.x;
-      if (b >= nbatch) break;
-      const int64_t lb = b * E;
-      const int ne = (int)((nloc - lb) < E ? (nloc - lb) : E);
-      const int sl = (int)(it & 1);
-      const uint32_t par = (uint32_t)((it >> 1) & 1);
-      SFP_T(2, sfp_wait(&fullL[sl], par));
-      const double* slot = reinterpret_cast<const double*>(smp + L::OFF_L + sl * L::LSLOT);
-      const bool on = gact && el < ne;
-      // edge-vector combinations of this column: J[:,0] = (1-tZ) e0y[0] + tZ e0y[1],
-      // J[:,1] = (1-tZ) e1x[0] + tZ e1x[1], J[:,2] = col2 (trilinear map, vertex v = a + 2b + 4c)
-      double e0y[2][3], e1x[2][3], col2[3], ca[Q1], cb[Q1];
-      {
-        const double* X = slot + (on ? el : 0) * 24;
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            // x-edges at (b, c): X[1+2b+4c] - X[2b+4c];  y-edges at (a, c): X[a+2+4c] - X[a+4c]
-            e0y[c][i] = (1 - tY) * (X[3 * (1 + 4 * c) + i] - X[3 * (4 * c) + i]) +
-                        tY * (X[3 * (3 + 4 * c) + i] - X[3 * (2 + 4 * c) + i]);
-            e1x[c][i] = (1 - tX) * (X[3 * (2 + 4 * c) + i] - X[3 * (4 * c) + i]) +
-                        tX * (X[3 * (3 + 4 * c) + i] - X[3 * (1 + 4 * c) + i]);
-          }
-          // z-edges at (a, b): X[a+2b+4] - X[a+2b]
-          col2[i] = (1 - tX) * (1 - tY) * (X[3 * 4 + i] - X[3 * 0 + i]) +
-                    tX * (1 - tY) * (X[3 * 5 + i] - X[3 * 1 + i]) +
-                    (1 - tX) * tY * (X[3 * 6 + i] - X[3 * 2 + i]) + tX * tY * (X[3 * 7 + i] - X[3 * 3 + i]);
-        }
-#pragma unroll
-        for (int qz = 0; qz < Q1; ++qz) {
-          const int q = tx + Q1 * ty + Q2 * qz;
-          ca[qz] = on ? slot[E * 24 + el * NQ + q] : 0.0;
-          cb[qz] = (on && NCOEF == 2) ? slot[E * 24 + E * NQ + el * NQ + q] : 0.0;
-        }
-      }
-      sfp_arrive(&emptyL[sl]);
-      // W^{u}[qz] for the unique pairs u (m <= n), value-value pair last
-      double Wr[NUP][Q1];
-#pragma unroll
-      for (int qz = 0; qz < Q1; ++qz) {
-        const double tZ = c_x1d[P][qz];
-        double J[3][3];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          J[i][0] = (1 - tZ) * e0y[0][i] + tZ * e0y[1][i];
-          J[i][1] = (1 - tZ) * e1x[0][i] + tZ * e1x[1][i];
-          J[i][2] = col2[i];
-        }
-        const double C[3][3] = {{J[1][1] * J[2][2] - J[1][2] * J[2][1], J[1][2] * J[2][0] - J[1][0] * J[2][2],
-                                 J[1][0] * J[2][1] - J[1][1] * J[2][0]},
-                                {J[0][2] * J[2][1] - J[0][1] * J[2][2], J[0][0] * J[2][2] - J[0][2] * J[2][0],
-                                 J[0][1] * J[2][0] - J[0][0] * J[2][1]},
-                                {J[0][1] * J[1][2] - J[0][2] * J[1][1], J[0][2] * J[1][0] - J[0][0] * J[1][2],
-                                 J[0][0] * J[1][1] - J[0][1] * J[1][0]}};
-        const double det = J[0][0] * C[0][0] + J[0][1] * C[0][1] + J[0][2] * C[0][2];
-        const double wq = wxy * c_w1d[P][qz];
-        if constexpr (DIFF) {
-          const double kap = MASS ? cb[qz] : ca[qz];
-          // 1/det: rcp.approx + two Newton steps (relative error ~1 ulp; det > 0 checked at create)
-          double rd;
-          asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(det));
-          double er = fma(-det, rd, 1.0);
-          rd = fma(rd, er, rd);
-          er = fma(-det, rd, 1.0);
-          rd = fma(rd, er, rd);
-          const double sc = on ? wq * kap * rd : 0.0;
-#pragma unroll
-          for (int u = 0; u < 6; ++u) {
-            if (L::GH > 1 && (u < ulo || u >= uhi)) continue;
-            int m, n;
-            upair(u, m, n);
-            Wr[u][qz] = sc * (C[0][m] * C[0][n] + C[1][m] * C[1][n] + C[2][m] * C[2][n]);
-          }
-        }
-        if constexpr (MASS) Wr[NUP - 1][qz] = wq * det * ca[qz];
-      }
-      // stage z into T1 slot it % 2 once X has released it
-      SFP_T(3, sfp_wait(&emptyT[sl], par ^ 1u));
-      double* T1 = reinterpret_cast<double*>(smp + L::OFF_T1 + sl * L::T1SLOT);
-      if (gact) {
-#pragma unroll
-        for (int ul = 0; ul < NUP; ++ul) {
-          if (L::GH > 1 && (ul < ulo || ul >= uhi)) continue;
-          int m, n;
-          upair(UBASE + ul, m, n);
-          const int az = m == 2, bz = n == 2;
-          double* out = T1 + (el * NUP + ul) * N1 * N1 * Q2 + qxy;
-#pragma unroll
-          for (int a = 0; a < N1; ++a)
-#pragma unroll
-            for (int bb = 0; bb < N1; ++bb) {
-              double sacc = 0.0;
-#pragma unroll
-              for (int qz = 0; qz < Q1; ++qz) sacc = fma(Wr[ul][qz], c_zz[P][az][bz][qz][a][bb], sacc);
-              out[(a * N1 + bb) * Q2] = sacc;
-            }
-        }
-      }
-      sfp_arrive(&fullT[sl]);
-    }
-  } else if (warp <= L::NG + L::NY) {
-    // ======================= Y: stage y, all y pairs of one (cell, z pair, qx) =======================
-    const int ytid0 = tid - 32 * (1 + L::NG);
-    const bool diagw = ytid0 >= 32 * L::NYW;  // warp-uniform: diagonal z pairs in the last NYD warps
-    const int ytid = diagw ? ytid0 - 32 * L::NYW : ytid0;
-    const int nz = diagw ? N1 : NOFF;
-    const int el = ytid / (nz * Q1), rr = ytid - el * nz * Q1;
-    const int zl = rr / Q1, qx = rr - zl * Q1;
-    const bool yact = el < E;
-    int iz = 0, jz = 0;
-    if (diagw) {
-      iz = jz = zl;
-    } else {
-      int c = zl;
-      for (int a = 0; a < N1; ++a) {
-        if (c < N1 - 1 - a) { iz = a; jz = a + 1 + c; break; }
-        c -= N1 - 1 - a;
-      }
-    }
-    const int zp = diagw ? NOFF + zl : zl;  // T2 z-pair slot
-    constexpr int NYT = 32 * L::NY;
-    (void)NYT;
-    auto body = [&](auto DIAGc, const double* T1e, double* T2e) {
-      constexpr bool DG = decltype(DIAGc)::value;
-      double S[N1][N1][4];
-#pragma unroll
-      for (int a = 0; a < N1; ++a)
-#pragma unroll
-        for (int b = 0; b < N1; ++b)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) S[a][b][c] = 0.0;
-#pragma unroll
-      for (int op = 0; op < NOP; ++op) {
-        int m, n;
-        if (DIFF && op < 9) { m = op / 3; n = op % 3; } else { m = 3; n = 3; }
-        const int mm = m < n ? m : n, nn = m < n ? n : m;
-        const int ul = (mm == 3) ? NUP - 1 : (mm == 0 ? nn : (mm == 1 ? 2 + nn : 5));
-        const int zidx = (m > n) ? (jz * N1 + iz) : (iz * N1 + jz);
-        const int ay = m == 1, by = n == 1, cls = (m == 0) * 2 + (n == 0);
-        const double* src = T1e + (ul * N1 * N1 + zidx) * Q2 + qx * Q1;
-        double tv[Q1];
-#pragma unroll
-        for (int qy = 0; qy < Q1; ++qy) tv[qy] = src[qy];
-#pragma unroll
-        for (int iy = 0; iy < N1; ++iy)
-#pragma unroll
-          for (int jy = (DG ? iy : 0); jy < N1; ++jy)
-#pragma unroll
-            for (int qy = 0; qy < Q1; ++qy)
-              S[iy][jy][cls] = fma(c_zz[P][ay][by][qy][iy][jy], tv[qy], S[iy][jy][cls]);
-      }
-      return [&, S, T2e]() {
-#pragma unroll
-        for (int iy = 0; iy < N1; ++iy)
-#pragma unroll
-          for (int jy = (DG ? iy : 0); jy < N1; ++jy)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) T2e[(iy * N1 + jy) * T2W + c * Q1 + qx] = S[iy][jy][c];
-      };
-    };
-    for (int64_t it = 0;; ++it) {
-      const int64_t b = blockIdx.x + it * (int64_t)gridDim.x;
-      if (b >= nbatch) break;
-      const int sl = (int)(it & 1);
-      const uint32_t par = (uint32_t)((it >> 1) & 1);
-      SFP_T(4, sfp_wait(&fullT[sl], par));
-      const double* T1e = reinterpret_cast<const double*>(smp + L::OFF_T1 + sl * L::T1SLOT) +
-                          (yact ? el : 0) * NUP * N1 * N1 * Q2;
-      double* T2e = reinterpret_cast<double*>(smp + L::OFF_T2 + sl * L::T2SLOT) +
-                    ((yact ? el : 0) * NZP + zp) * YP * T2W;
-      auto run = [&](auto DIAGc) {
-        auto fin = body(DIAGc, T1e, T2e);
-        sfp_arrive(&emptyT[sl]);
-        SFP_T(5, sfp_wait(&emptyU[sl], par ^ 1u));
-        if (yact) fin();
-        sfp_arrive(&fullU[sl]);
-      };
-      if (diagw) run(std::true_type{});
-      else run(std::false_type{});
-    }
-  } else {
-    // ======================= X: stage x from T2, K staging, TMA store =======================
-    const int xtid = tid - 32 * (1 + L::NG + L::NY);
-    const int yx_el = xtid / L::TPE, yx_r = xtid - yx_el * L::TPE;
-    const bool xact = xtid < E * L::TPE;
-    int iz = 0, jz = 0, iy = 0, jy = 0, zp = 0;
-    if (yx_r < L::TOFF) {
-      int c = yx_r / L::YP;
-      zp = c;
-      const int yp = yx_r - c * L::YP;
-      iy = yp / N1;
-      jy = yp - iy * N1;
-      for (int a = 0; a < N1; ++a) {
-        if (c < N1 - 1 - a) { iz = a; jz = a + 1 + c; break; }
-        c -= N1 - 1 - a;
-      }
-    } else {
-      const int r = yx_r - L::TOFF;
-      iz = jz = r / L::YPS;
-      zp = NOFF + iz;
-      int c = r - iz * L::YPS;
-      for (int a = 0; a < N1; ++a) {
-        if (c < N1 - a) { iy = a; jy = a + c; break; }
-        c -= N1 - a;
-      }
-    }
-    const bool mirror = (iz < jz) || (iy < jy);
-    constexpr int NXT = 32 * L::NX;
-    for (int64_t it = 0;; ++it) {
-      const int64_t b = blockIdx.x + it * (int64_t)gridDim.x;
-      if (b >= nbatch) break;
-      const int64_t lb = b * E;
-      const int ne = (int)((nloc - lb) < E ? (nloc - lb) : E);
-      const int sl = (int)(it & 1);
-      SFP_T(6, sfp_named_bar(1, NXT));
-      SFP_T(7, sfp_wait(&fullU[sl], (uint32_t)((it >> 1) & 1)));
-      double Sx[4][Q1];
-      if (xact) {
-        const double* src = reinterpret_cast<const double*>(smp + L::OFF_T2 + sl * L::T2SLOT) +
-                            ((yx_el * NZP + zp) * YP + iy * N1 + jy) * T2W;
-#pragma unroll
-        for (int h = 0; h < T2W / 2; ++h) {
-          const double2 v = reinterpret_cast<const double2*>(src)[h];
-          Sx[(2 * h) / Q1][(2 * h) % Q1] = v.x;
-          Sx[(2 * h + 1) / Q1][(2 * h + 1) % Q1] = v.y;
-        }
-      }
-      sfp_arrive(&emptyU[sl]);
-      double* Kst = reinterpret_cast<double*>(smp + L::OFF_K + sl * L::KSLOT);
-      if (xact && yx_el < ne) {
-        double acc[N1][N1];
-#pragma unroll
-        for (int a = 0; a < N1; ++a)
-#pragma unroll
-          for (int bb = 0; bb < N1; ++bb) acc[a][bb] = 0.0;
-#pragma unroll
-        for (int qx = 0; qx < Q1; ++qx)
-#pragma unroll
-          for (int ax = 0; ax < 2; ++ax) {
-            double u[N1];
-#pragma unroll
-            for (int bb = 0; bb < N1; ++bb) u[bb] = Bt(0, qx, bb) * Sx[ax * 2 + 0][qx] + Bt(1, qx, bb) * Sx[ax * 2 + 1][qx];
-#pragma unroll
-            for (int a = 0; a < N1; ++a)
-#pragma unroll
-              for (int bb = 0; bb < N1; ++bb) acc[a][bb] = fma(Bt(ax, qx, a), u[bb], acc[a][bb]);
-          }
-        double* Ke = Kst + yx_el * NB * NB;
-        const int ib = N1 * (iy + N1 * iz), jb = N1 * (jy + N1 * jz);
-#pragma unroll
-        for (int a = 0; a < N1; ++a)
-#pragma unroll
-          for (int bb = 0; bb < N1; ++bb) {
-            Ke[(ib + a) * NB + jb + bb] = acc[a][bb];
-            if (mirror) Ke[(jb + bb) * NB + ib + a] = acc[a][bb];
-          }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      sfp_named_bar(2, NXT);
-      const uint32_t bytes = (uint32_t)ne * NB * NB * 8;
-      double* gdst = K + lb * NB * NB;
-      if (((reinterpret_cast<uintptr_t>(gdst) | bytes) & 15u) == 0) {
-        if (xtid == 0) {
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                       :: "l"(gdst), "r"(smem_u32(Kst)), "r"(bytes) : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        }
-      } else {
-        for (int i = xtid; i < ne * NB * NB; i += NXT) gdst[i] = Kst[i];
-      }
-    }
-    if (xtid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  }
-#ifdef FEB200_SFP_PROF
-  if (lane == 0) {
-    for (int k = 0; k < 8; ++k) if (prof_[k]) atomicAdd(&g_sfp_prof[k], prof_[k]);
-    const int role = warp == 0 ? 0 : (warp <= L::NG ? 1 : (warp <= L::NG + L::NY ? 3 : 2));
-    atomicAdd(&g_sfp_prof[8 + role], (unsigned long long)(clock64() - tstart_));
-    atomicAdd(&g_sfp_prof[12 + role], 1ull);
-  }
-#endif
-#undef Bt
-}
-
-template <int P, int FORM>
-static cudaError_t launch_sq_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int64_t e1, double* K,
-                               cudaStream_t st) {
-  using L = SQL<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM != FE_FORM_DIFFUSION ? 1 : 0)>;
-  if (L::BYTES > 227 * 1024) return cudaErrorNotSupported;
-  auto kern = k_matrix_sq<P, FORM>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
-  if (err != cudaSuccess) return err;
-  int nsm = 148, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t nbatch = (e1 - e0 + L::E - 1) / L::E;
-  const int grid = (int)(nbatch < nsm ? nbatch : nsm);
-  if (grid <= 0) return cudaSuccess;
-  kern<<<grid, L::THREADS, L::BYTES, st>>>(view_of(mh), (const double*)mat.a, (const double*)mat.b,
-                                           e0, e1, K);
-  count_launch();
-  return cudaGetLastError();
-}
-
 template <int P, int FORM>
 static cudaError_t launch_sf_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int64_t e1, double* K,
                                cudaStream_t st) {
@@ -1528,15 +1040,6 @@ cudaError_t launch_matrix_sf(const fe_mesh* mh, int form, MatArgs mat, int64_t e
   if (mh->q1d != mh->order + 1) return cudaErrorNotSupported;
   const char* impl = std::getenv("FEB200_MATRIX_IMPL");
   const bool pipelined = FEB200_SFP && !(impl && std::strcmp(impl, "sf1") == 0);
-  const bool four = FEB200_SQ ? !(impl && std::strcmp(impl, "sfp") == 0) : (impl && std::strcmp(impl, "sq") == 0);
-  if (pipelined && four && mh->order == 2) {
-    switch (form) {
-      case FE_FORM_DIFFUSION: return launch_sq_t<2, FE_FORM_DIFFUSION>(mh, mat, e0, e1, K, st);
-      case FE_FORM_MASS: return launch_sq_t<2, FE_FORM_MASS>(mh, mat, e0, e1, K, st);
-      case FE_FORM_MASS_DIFFUSION: return launch_sq_t<2, FE_FORM_MASS_DIFFUSION>(mh, mat, e0, e1, K, st);
-      default: break;
-    }
-  }
   if (pipelined && (mh->order == 1 || mh->order == 2)) {
 #define SFP_CASE(P)                                                                                \
   if (mh->order == P) switch (form) {                                                              \
