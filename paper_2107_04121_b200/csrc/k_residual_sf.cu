@@ -50,6 +50,9 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 #ifndef FEB200_RSF_PAD
 #define FEB200_RSF_PAD 1
 #endif
+#ifndef FEB200_RSF_PADB
+#define FEB200_RSF_PADB (sizeof(T) == 8 ? 96 : 32)
+#endif
 #ifndef FEB200_RSF_PADP
 #define FEB200_RSF_PADP 3
 #endif
@@ -62,10 +65,11 @@ struct RSF {
   static constexpr int EB = (D == 3 && P >= 3) ? EB0 / 2 : EB0;  // cells per CTA iteration
   static constexpr int THREADS = (EB * TPE + 31) / 32 * 32;
   static constexpr int THREADS_ = THREADS;
-  // exchange buffer per cell (elements of T), padded so that consecutive cells start 32 B
-  // apart modulo 128 B: the column reads of a warp (3-4 cells) then hit disjoint banks
+  // exchange buffer per cell (elements of T), padded so that consecutive cells start PADB
+  // bytes apart modulo 128 B (fp64: 96 B, chosen with a half-warp bank model of the column
+  // stores and the x- / y-direction reads of the stages; fp32: 32 B)
   static constexpr int XS0 = 3 * D * NQ;
-  static constexpr int XSB = (int)(128 / sizeof(T)), XSQ = (int)(32 / sizeof(T));
+  static constexpr int XSB = (int)(128 / sizeof(T)), XSQ = (int)(FEB200_RSF_PADB / sizeof(T));
   static constexpr int XS = (FEB200_RSF_PAD && (P <= FEB200_RSF_PADP)) ? XS0 + ((XSQ - XS0 % XSB) % XSB + XSB) % XSB : XS0;
   // prefetch slots (x2): conn [EB][8], dof_conn [EB][NB] (int32), material a, b [EB][NQ] (T),
   // vertex coordinates [EB][24]; plus two mbarriers
