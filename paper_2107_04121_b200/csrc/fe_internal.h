@@ -86,6 +86,9 @@ cudaError_t launch_geometry_materialize(const fe_mesh* m, double* detw, double* 
                                         cudaStream_t st);
 
 void count_launch();
+// Test hook: FEB200_MAX_CTAS caps the grid of the persistent kernels so that small meshes
+// still run many batches per CTA (ring-buffer phases wrap several times in the parity tests).
+int grid_cap(int grid);
 cudaError_t upload_const_tables_matrix(int order, const double* b1, const double* d1,
                                       const double* x1, const double* w1, cudaStream_t st);
 cudaError_t upload_const_tables_residual(int order, const double* b1, const double* d1,

@@ -235,7 +235,8 @@ static cudaError_t launch_matrix_t(const fe_mesh* mh, MatArgs mat, const double*
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, L::BYTES);
   if (per_sm < 1) per_sm = 1;
   const int64_t n = e1 - e0;
-  const int grid = (int)std::min<int64_t>(n, (int64_t)nsm * per_sm);
+  int grid = (int)std::min<int64_t>(n, (int64_t)nsm * per_sm);
+  grid = grid_cap(grid);
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, 256, L::BYTES, st>>>(view_of(mh), mat.kind, (const double*)mat.a,
                                     (const double*)mat.b, state_u, e0, e1, K);

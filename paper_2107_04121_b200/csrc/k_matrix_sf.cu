@@ -1003,7 +1003,8 @@ static cudaError_t launch_sfp_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int6
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int64_t nbatch = (e1 - e0 + L::E - 1) / L::E;
-  const int grid = (int)(nbatch < nsm ? nbatch : nsm);
+  int grid = (int)(nbatch < nsm ? nbatch : nsm);
+  grid = grid_cap(grid);
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, L::THREADS, L::BYTES, st>>>(view_of(mh), (const double*)mat.a, (const double*)mat.b,
                                            e0, e1, K);
@@ -1026,7 +1027,8 @@ static cudaError_t launch_sf_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int64
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::THREADS, L::BYTES);
   if (per_sm < 1) per_sm = 1;
   const int64_t nbatch = (e1 - e0 + L::E - 1) / L::E;
-  const int grid = (int)((nbatch < (int64_t)nsm * per_sm) ? nbatch : (int64_t)nsm * per_sm);
+  int grid = (int)((nbatch < (int64_t)nsm * per_sm) ? nbatch : (int64_t)nsm * per_sm);
+  grid = grid_cap(grid);
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, L::THREADS, L::BYTES, st>>>(view_of(mh), (const double*)mat.a, (const double*)mat.b,
                                           e0, e1, K);

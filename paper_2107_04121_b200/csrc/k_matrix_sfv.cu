@@ -401,7 +401,8 @@ static cudaError_t launch_sfv_t(const fe_mesh* mh, MatArgs mat, const double* st
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::THREADS, L::BYTES);
   if (per_sm < 1) per_sm = 1;
   const int64_t n = e1 - e0;
-  const int grid = (int)((n < (int64_t)nsm * per_sm) ? n : (int64_t)nsm * per_sm);
+  int grid = (int)((n < (int64_t)nsm * per_sm) ? n : (int64_t)nsm * per_sm);
+  grid = grid_cap(grid);
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, L::THREADS, L::BYTES, st>>>(view_of(mh), mat.kind, (const double*)mat.a,
                                            (const double*)mat.b, state_u, e0, e1, K);

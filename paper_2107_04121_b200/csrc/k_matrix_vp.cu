@@ -683,7 +683,8 @@ static cudaError_t launch_vp_t(const fe_mesh* mh, MatArgs mat, const double* sta
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int64_t nbatch = (e1 - e0 + L::E - 1) / L::E;
-  const int grid = (int)(nbatch < nsm ? nbatch : nsm);
+  int grid = (int)(nbatch < nsm ? nbatch : nsm);
+  grid = grid_cap(grid);
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, L::THREADS, L::BYTES, st>>>(view_of(mh), mat.kind, (const double*)mat.a,
                                            (const double*)mat.b, state_u, e0, e1, K);

@@ -5,7 +5,15 @@
 #include "fe_device.cuh"
 #include "fe_internal.h"
 
+#include <cstdlib>
+
 namespace feb200 {
+
+int grid_cap(int grid) {
+  const char* v = std::getenv("FEB200_MAX_CTAS");  // read per launch: tests toggle it
+  const int cap = v ? std::atoi(v) : 0;
+  return (cap > 0 && grid > cap) ? cap : grid;
+}
 
 namespace {
 std::atomic_int64_t* launch_counter() {

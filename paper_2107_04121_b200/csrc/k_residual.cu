@@ -164,7 +164,8 @@ static cudaError_t launch_res_t(const fe_mesh* mh, MatArgs mat, const T* u, int6
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, bytes);
   if (per_sm < 1) per_sm = 1;
   const int64_t nbatch = (e1 - e0 + L::NE - 1) / L::NE;
-  const int grid = (int)std::min<int64_t>(nbatch, (int64_t)nsm * per_sm);
+  int grid = (int)std::min<int64_t>(nbatch, (int64_t)nsm * per_sm);
+  grid = grid_cap(grid);
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, 256, bytes, st>>>(view_of(mh), mat.kind, (const T*)mat.a, (const T*)mat.b, u, e0, e1,
                                  r_elem, r_global);

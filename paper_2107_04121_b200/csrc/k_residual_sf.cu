@@ -498,7 +498,8 @@ static cudaError_t launch_rsf_t(const fe_mesh* mh, MatArgs mat, const T* u, int6
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::THREADS, L::BYTES);
   if (per_sm < 1) per_sm = 1;
   const int64_t nbatch = (e1 - e0 + L::EB - 1) / L::EB;
-  const int grid = (int)((nbatch < (int64_t)nsm * per_sm) ? nbatch : (int64_t)nsm * per_sm);
+  int grid = (int)((nbatch < (int64_t)nsm * per_sm) ? nbatch : (int64_t)nsm * per_sm);
+  grid = grid_cap(grid);
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, L::THREADS, L::BYTES, st>>>(view_of(mh), mat.kind, (const T*)mat.a, (const T*)mat.b,
                                            u, e0, e1, r_elem, r_global, eval_out);

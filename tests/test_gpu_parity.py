@@ -308,3 +308,24 @@ def test_csr_full_size_c2():
     A = sp.csr_matrix((vals.cpu().numpy(), ci, rp), shape=(csr.n_rows, csr.n_rows))
     rs = np.abs(A @ np.ones(csr.n_rows))
     assert rs.max() <= 1e-12 * np.abs(vals.cpu().numpy()).max()
+
+
+@pytest.mark.parametrize("form,p,shape", [(0, 2, (6, 5, 4)), (3, 2, (5, 5, 3)), (1, 1, (9, 8, 7)),
+                                          (4, 2, (4, 3, 5)), (5, 2, (4, 4, 3)), (0, 4, (4, 3, 3))])
+@pytest.mark.parametrize("ctas", [1, 3])
+def test_pipelined_many_batches_per_cta(form, p, shape, ctas, monkeypatch):
+    """FEB200_MAX_CTAS caps the persistent grids so that each CTA runs many batches: every
+    ring slot and mbarrier phase of the warp-specialised kernels wraps several times (plus a
+    ragged last batch); matrices and residuals still match the oracle in full."""
+    monkeypatch.setenv("FEB200_MAX_CTAS", str(ctas))
+    pr = fi.make_problem(form, p, shape, 6000 + 10 * form + p)
+    mesh = gpu_mesh(pr)
+    mat = (pr.mat_kind, dev(pr.mat_a), dev(pr.mat_b))
+    if p <= 2:
+        K = mesh.element_matrices(form, *mat, dev(pr.u) if form == fi.CONVECTIVE else None)
+        assert rel(K.cpu().numpy(), oracle.problem_matrix(pr)) <= TOL64
+    r_elem, r_glob = mesh.residual(form, dev(pr.u), *mat, want_elem=True)
+    r_ref = oracle.problem_residual(pr)
+    assert rel(r_elem.cpu().numpy(), r_ref) <= TOL64
+    R_ref = oracle.assemble(r_ref, pr.dof_conn, pr.n_nodes, pr.ncomp)
+    assert rel(r_glob.cpu().numpy().ravel(), R_ref) <= TOL64
