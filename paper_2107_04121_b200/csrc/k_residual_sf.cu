@@ -99,6 +99,9 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
   constexpr int N1 = L::N1, Q1 = L::Q1, NB = L::NB, NQ = L::NQ, D = L::D, EB = L::EB;
   constexpr int Q2 = Q1 * Q1;
   constexpr bool VAL = L::VAL, GRAD = L::GRAD;
+  // the backward pass tests against grad v only where the flux has an f1 part
+  // (the convective residual v . (grad u) u has f0 only, Eq. fe2)
+  constexpr bool BGRAD = GRAD && FORM != FE_FORM_CONVECTIVE;
   using A = T;  // contraction arithmetic in the call's precision (geometry and flux stay fp64)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Bs = reinterpret_cast<T*>(smem_raw);  // [2][Q1][N1] in the arithmetic type
@@ -395,7 +398,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
         for (int kz = 0; kz < N1; ++kz) {
           A hv = A(0);
           if (VAL) hv = B(0, qz, kz) * F0;
-          if (GRAD) {
+          if (BGRAD) {
             hv = fma(B(1, qz, kz), Fz, hv);
             Hx[a][kz] = fma(B(0, qz, kz), Fx, Hx[a][kz]);
             Hy[a][kz] = fma(B(0, qz, kz), Fy, Hy[a][kz]);
@@ -412,7 +415,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
 #pragma unroll
         for (int kz = 0; kz < N1; ++kz) {
           Xe[(a * 3 + 0) * NQ + kz * Q2 + ty * Q1 + tx] = (T)Hv[a][kz];
-          if (GRAD) {
+          if (BGRAD) {
             Xe[(a * 3 + 1) * NQ + kz * Q2 + ty * Q1 + tx] = (T)Hx[a][kz];
             Xe[(a * 3 + 2) * NQ + kz * Q2 + ty * Q1 + tx] = (T)Hy[a][kz];
           }
@@ -430,7 +433,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
           const int o = kz * Q2 + qy * Q1 + tx;
           const A hv = active ? (A)Xe[(a * 3 + 0) * NQ + o] : A(0);
           sv = fma(Cy(0, qy), hv, sv);
-          if (GRAD) {
+          if (BGRAD) {
             sv = fma(Cy(1, qy), active ? (A)Xe[(a * 3 + 2) * NQ + o] : A(0), sv);
             sx = fma(Cy(0, qy), active ? (A)Xe[(a * 3 + 1) * NQ + o] : A(0), sx);
           }
@@ -446,7 +449,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
 #pragma unroll
         for (int kz = 0; kz < N1; ++kz) {
           Xe[(a * 3 + 0) * NQ + kz * Q2 + ty * Q1 + tx] = (T)Iv[a][kz];
-          if (GRAD) Xe[(a * 3 + 1) * NQ + kz * Q2 + ty * Q1 + tx] = (T)Ix[a][kz];
+          if (BGRAD) Xe[(a * 3 + 1) * NQ + kz * Q2 + ty * Q1 + tx] = (T)Ix[a][kz];
         }
     }
     __syncthreads();
@@ -461,7 +464,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
           for (int qx = 0; qx < Q1; ++qx) {
             const int o = kz * Q2 + ty * Q1 + qx;
             s = fma(Cx(0, qx), (A)Xe[(a * 3 + 0) * NQ + o], s);
-            if (GRAD) s = fma(Cx(1, qx), (A)Xe[(a * 3 + 1) * NQ + o], s);
+            if (BGRAD) s = fma(Cx(1, qx), (A)Xe[(a * 3 + 1) * NQ + o], s);
           }
           const T v = (T)s;
           const int k = tx + N1 * ty + N1 * N1 * kz;
