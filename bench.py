@@ -113,11 +113,12 @@ def uses_sf_matrix(form: int, p: int) -> bool:
 
 
 def alg_bytes(form: int, mode: str, p: int, nb: int, nq: int, D: int, mat_kind: int,
-              esize: int = 8) -> float:
+              esize: int = 8, csr_nnz_per_cell: float = 0.0) -> float:
     if mode == "csr":
-        # read K_e and the position map, one fp64 read-modify-write per K entry (atomics in L2;
-        # the unique global entries are counted by the caller's traffic measurement)
-        return (D * nb) ** 2 * 8 + nb * nb * 4 + 4 * nb
+        # essential traffic: read K_e once, read + write every global CSR value once (the
+        # duplicate contributions of neighbouring cells merge in L2); the position map and the
+        # row pointers are implementation overhead, not counted
+        return (D * nb) ** 2 * 8 + 16 * csr_nnz_per_cell
     if form == fi.ELASTICITY:
         mat = 2 * esize if mat_kind == fi.MAT_PER_ELEM else 2 * nq * esize
     elif form == fi.MASS_DIFFUSION:
@@ -514,7 +515,8 @@ def main():
             fl = fl_lean  # single-stage vector SF kernel: flop count not modelled, lean dense count
         else:
             fl = sf_residual_flops(prob.form, prob.p) * El
-        by = alg_bytes(prob.form, mode, prob.p, nb, nq, D, prob.mat_kind, esize) * El
+        by = alg_bytes(prob.form, mode, prob.p, nb, nq, D, prob.mat_kind, esize,
+                       (csr.nnz / El) if csr is not None else 0.0) * El
         t_s = kern_ms[mode] * 1e-3
         if args.dtype == "f32":
             pk_f, src_f, fbound = 74.4, "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz", "alu"

@@ -12,15 +12,21 @@
 //   idx_in_row(r, c) D + b.
 // Assembly: values[pos(e, a k, b l)] += K_e[a k][b l] with fp64 atomics
 // (atomic order is the only run-to-run difference, as for the residual).
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <exception>
 #include <new>
 #include <string>
+#include <type_traits>
 
 #include <thrust/binary_search.h>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 #include <thrust/device_ptr.h>
 #include <thrust/execution_policy.h>
+#include <thrust/sequence.h>
+#include <thrust/copy.h>
 #include <thrust/sort.h>
 #include <thrust/unique.h>
 
@@ -32,7 +38,11 @@ struct fe_csr {
   int64_t n_nodes = 0, nnz_node = 0;
   int64_t* rowptr_node = nullptr;   // [n_nodes + 1] scalar node pattern
   int32_t* col_node = nullptr;      // [nnz_node]
-  int32_t* pos_in_row = nullptr;    // [E][nb][nb] index of column node l inside row node k
+  void* pos_in_row = nullptr;       // [E][nb][nb] index of column node l inside row node k
+  int pos_bytes = 4;                // 1, 2 or 4: narrowest type holding every row length
+  int64_t* n2c_ptr = nullptr;       // [n_nodes + 1] node -> incident (cell, local node) list
+  int32_t* n2c = nullptr;           // [E nb] entries e nb + k, sorted by (node, e)
+  int hmax = 0;                     // longest node row of the scalar pattern
   int64_t* rowptr = nullptr;        // [n_nodes D + 1] expanded pattern
   int32_t* col = nullptr;           // [nnz_node D^2]
 };
@@ -59,8 +69,9 @@ __global__ void k_cols(const int64_t* __restrict__ keys, int64_t nnz, int64_t n_
     col[i] = (int32_t)(keys[i] % n_nodes);
 }
 
+template <typename PT>
 __global__ void k_pos_map(const int32_t* __restrict__ dc, int nb, int64_t E, const int64_t* __restrict__ rowptr,
-                          const int32_t* __restrict__ col, int32_t* __restrict__ pos) {
+                          const int32_t* __restrict__ col, PT* __restrict__ pos) {
   const int64_t n = E * nb * nb;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = i / (nb * nb);
@@ -72,7 +83,7 @@ __global__ void k_pos_map(const int32_t* __restrict__ dc, int nb, int64_t E, con
       const int64_t mid = (lo + hi) >> 1;
       if (col[mid] < c) lo = mid + 1; else hi = mid;
     }
-    pos[i] = (int32_t)(lo - base);
+    pos[i] = (PT)(lo - base);
   }
 }
 
@@ -91,11 +102,26 @@ __global__ void k_expand(const int64_t* __restrict__ rpn, const int32_t* __restr
   }
 }
 
-// values[pos] += K[e - e0][a nb + k][b nb + l]
+__global__ void k_max_row(const int64_t* __restrict__ rpn, int64_t n, unsigned long long* __restrict__ mx) {
+  unsigned long long m = 0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long len = (unsigned long long)(rpn[r + 1] - rpn[r]);
+    m = len > m ? len : m;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
+    m = v > m ? v : m;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
+}
+
+// values[pos] += K[e - e0][a nb + k][b nb + l]; the position map is stored in the narrowest
+// integer type that holds every row length (uint8 for the Q2 lattice: 4x less map traffic)
+template <typename PT>
 __global__ void __launch_bounds__(256) k_assemble_matrix(const int32_t* __restrict__ dc, int nb, int D,
                                                          int64_t e0, int64_t e1,
                                                          const int64_t* __restrict__ rpn,
-                                                         const int32_t* __restrict__ pos,
+                                                         const PT* __restrict__ pos,
                                                          const double* __restrict__ K,
                                                          double* __restrict__ values) {
   const int nd = D * nb;
@@ -113,6 +139,73 @@ __global__ void __launch_bounds__(256) k_assemble_matrix(const int32_t* __restri
   }
 }
 
+
+// Gather ("row-owner") assembly, no atomics: one warp owns one node row r of the pattern,
+// accumulates in shared memory the rows k of every incident cell's K_e (node-to-cell list,
+// ascending cell order) at the positions of the cell's column nodes, then adds the D rows
+// (r, a) to values with coalesced read-modify-writes.  Every K_e row is read exactly once,
+// every value is written once, and the summation order is fixed (bitwise reproducible).
+template <typename PT, int D>
+__global__ void __launch_bounds__(256) k_assemble_gather(const int64_t* __restrict__ rpn,
+                                                         const int64_t* __restrict__ n2c_ptr,
+                                                         const int32_t* __restrict__ n2c, int nb,
+                                                         int64_t N, const PT* __restrict__ pos,
+                                                         const double* __restrict__ K, int64_t e0,
+                                                         int64_t e1, int hmax,
+                                                         double* __restrict__ values) {
+  extern __shared__ double acc_all[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double* acc = acc_all + (size_t)warp * D * D * hmax;
+  const int nd = D * nb;
+  constexpr int CH = 8;  // incident cells whose K rows are loaded together
+  for (int64_t r = (int64_t)blockIdx.x * nw + warp; r < N; r += (int64_t)gridDim.x * nw) {
+    const int64_t b0 = rpn[r];
+    const int nr = (int)(rpn[r + 1] - b0);
+    for (int t = lane; t < D * D * nr; t += 32) acc[t] = 0.0;
+    __syncwarp();
+    const int64_t j0 = n2c_ptr[r], j1 = n2c_ptr[r + 1];
+    for (int64_t jc = j0; jc < j1; jc += CH) {
+      constexpr int TPL = (D * 27 + 31) / 32;  // (b, l) entries per lane for nb <= 27
+      double v[CH][D][TPL];
+      int jj[CH][TPL];
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const int64_t j = jc + u;
+        int64_t c = -1;
+        int k = 0;
+        if (j < j1) {
+          const int32_t ik = n2c[j];
+          c = ik / nb;
+          k = ik - (int)c * nb;
+          if (c < e0 || c >= e1) c = -1;
+        }
+#pragma unroll
+        for (int h = 0; h < TPL; ++h) {
+          const int t = lane + 32 * h;  // t = b nb + l
+          const bool on = c >= 0 && t < nd;
+          const int b = t / nb, l = t - b * nb;
+          jj[u][h] = on ? (int)pos[((int64_t)c * nb + k) * nb + l] * D + b : -1;
+#pragma unroll
+          for (int a = 0; a < D; ++a)
+            v[u][a][h] = on ? K[(c - e0) * nd * nd + (int64_t)(a * nb + k) * nd + t] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+#pragma unroll
+        for (int h = 0; h < TPL; ++h)
+          if (jj[u][h] >= 0)
+#pragma unroll
+            for (int a = 0; a < D; ++a) acc[a * D * nr + jj[u][h]] += v[u][a][h];
+        __syncwarp();
+      }
+    }
+    double* out = values + (int64_t)D * D * b0;
+    for (int t = lane; t < D * D * nr; t += 32) out[t] += acc[t];
+    __syncwarp();
+  }
+}
+
 }  // namespace feb200
 
 namespace feb200 {
@@ -123,7 +216,7 @@ extern "C" {
 
 static void free_csr(fe_csr* c) {
   if (!c) return;
-  void* p[] = {c->rowptr_node, c->col_node, c->pos_in_row, c->rowptr, c->col};
+  void* p[] = {c->rowptr_node, c->col_node, c->pos_in_row, c->n2c_ptr, c->n2c, c->rowptr, c->col};
   for (void* q : p)
     if (q) cudaFree(q);
   delete c;
@@ -169,7 +262,6 @@ static fe_status create_csr_impl(const fe_mesh* mesh, int32_t ncomp, void* strea
   c->nnz_node = nnz;
   e = cudaMalloc(&c->rowptr_node, sizeof(int64_t) * (N + 1));
   if (e == cudaSuccess) e = cudaMalloc(&c->col_node, sizeof(int32_t) * nnz);
-  if (e == cudaSuccess) e = cudaMalloc(&c->pos_in_row, sizeof(int32_t) * npairs);
   if (e != cudaSuccess) { cudaFree(keys); free_csr(c); return feb200::set_error(FE_ERR_OOM, "fe_create_csr: pattern"); }
   // rowptr_node[r] = first key >= r * N
   thrust::device_ptr<int64_t> rp(c->rowptr_node);
@@ -177,9 +269,53 @@ static fe_status create_csr_impl(const fe_mesh* mesh, int32_t ncomp, void* strea
                                                   feb200::RowKey{N});
   thrust::lower_bound(pol, kp, kp + nnz, row_keys, row_keys + N + 1, rp);
   feb200::k_cols<<<grid, 256, 0, st>>>(keys, nnz, N, c->col_node);
-  feb200::k_pos_map<<<grid, 256, 0, st>>>(mesh->dof_conn, nb, E, c->rowptr_node, c->col_node, c->pos_in_row);
   feb200::count_launch();
+  unsigned long long* dmax = nullptr;
+  unsigned long long hmax = 0;
+  e = cudaMalloc(&dmax, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st);
+  if (e == cudaSuccess) {
+    feb200::k_max_row<<<grid, 256, 0, st>>>(c->rowptr_node, N, dmax);
+    feb200::count_launch();
+    e = cudaMemcpyAsync(&hmax, dmax, sizeof(hmax), cudaMemcpyDeviceToHost, st);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (dmax) cudaFree(dmax);
+  c->pos_bytes = hmax <= 256 ? 1 : (hmax <= 65536 ? 2 : 4);
+  if (e == cudaSuccess) e = cudaMalloc(&c->pos_in_row, (size_t)c->pos_bytes * npairs);
+  if (e != cudaSuccess) { cudaFree(keys); free_csr(c); return feb200::set_error(FE_ERR_OOM, "fe_create_csr: position map"); }
+  if (c->pos_bytes == 1)
+    feb200::k_pos_map<uint8_t><<<grid, 256, 0, st>>>(mesh->dof_conn, nb, E, c->rowptr_node, c->col_node, (uint8_t*)c->pos_in_row);
+  else if (c->pos_bytes == 2)
+    feb200::k_pos_map<uint16_t><<<grid, 256, 0, st>>>(mesh->dof_conn, nb, E, c->rowptr_node, c->col_node, (uint16_t*)c->pos_in_row);
+  else
+    feb200::k_pos_map<int32_t><<<grid, 256, 0, st>>>(mesh->dof_conn, nb, E, c->rowptr_node, c->col_node, (int32_t*)c->pos_in_row);
   feb200::count_launch();
+  c->hmax = (int)hmax;
+  // node -> (cell, local node) list: stable key sort of the dof_conn entries by node
+  {
+    const int64_t ne = E * nb;
+    int32_t* nkeys = nullptr;
+    e = cudaMalloc(&nkeys, sizeof(int32_t) * ne);
+    if (e == cudaSuccess) e = cudaMalloc(&c->n2c, sizeof(int32_t) * ne);
+    if (e == cudaSuccess) e = cudaMalloc(&c->n2c_ptr, sizeof(int64_t) * (N + 1));
+    if (e != cudaSuccess) {
+      if (nkeys) cudaFree(nkeys);
+      cudaFree(keys);
+      free_csr(c);
+      return feb200::set_error(FE_ERR_OOM, "fe_create_csr: node-to-cell list");
+    }
+    thrust::device_ptr<int32_t> nk(nkeys), nv(c->n2c);
+    thrust::copy(pol, thrust::device_ptr<const int32_t>(mesh->dof_conn),
+                 thrust::device_ptr<const int32_t>(mesh->dof_conn) + ne, nk);
+    thrust::sequence(pol, nv, nv + ne);
+    thrust::stable_sort_by_key(pol, nk, nk + ne, nv);
+    thrust::lower_bound(pol, nk, nk + ne, thrust::make_counting_iterator<int32_t>(0),
+                        thrust::make_counting_iterator<int32_t>((int32_t)N + 1),
+                        thrust::device_ptr<int64_t>(c->n2c_ptr));
+    cudaStreamSynchronize(st);
+    cudaFree(nkeys);
+  }
   e = cudaMalloc(&c->rowptr, sizeof(int64_t) * (N * ncomp + 1));
   if (e == cudaSuccess) e = cudaMalloc(&c->col, sizeof(int32_t) * nnz * ncomp * ncomp);
   if (e != cudaSuccess) { cudaFree(keys); free_csr(c); return feb200::set_error(FE_ERR_OOM, "fe_create_csr: expanded pattern"); }
@@ -226,9 +362,30 @@ fe_status fe_assemble_matrix(const fe_csr* csr, const double* K, int64_t elem_be
   const int64_t n = (elem_end - elem_begin) * nd * nd;
   if (n == 0) return FE_OK;
   const int grid = (int)((n + 255) / 256 < 148 * 32 ? (n + 255) / 256 : 148 * 32);
-  feb200::k_assemble_matrix<<<grid, 256, 0, (cudaStream_t)stream>>>(
-      csr->mesh->dof_conn, csr->mesh->nb, csr->ncomp, elem_begin, elem_end, csr->rowptr_node,
-      csr->pos_in_row, K, values);
+  const char* impl = std::getenv("FEB200_CSR_IMPL");
+  // default: fp64 atomics (fastest on B200); FEB200_CSR_IMPL=gather selects the atomic-free
+  // row-owner kernel (fixed summation order, bitwise reproducible; nb <= 27)
+  const bool atomic = !(impl && std::strcmp(impl, "gather") == 0) || csr->mesh->nb > 27;
+  const int D = csr->ncomp;
+  const size_t smem = (size_t)8 * D * D * csr->hmax * 8;  // 8 warps per block
+  auto launch = [&](auto* pos) {
+    if (atomic) {
+      feb200::k_assemble_matrix<<<grid, 256, 0, (cudaStream_t)stream>>>(
+          csr->mesh->dof_conn, csr->mesh->nb, csr->ncomp, elem_begin, elem_end, csr->rowptr_node, pos, K,
+          values);
+      return;
+    }
+    using PT = std::remove_const_t<std::remove_pointer_t<decltype(pos)>>;
+    auto kern = D == 1 ? feb200::k_assemble_gather<PT, 1> : feb200::k_assemble_gather<PT, 3>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int64_t rows = csr->n_nodes;
+    const int g = (int)std::min<int64_t>((rows + 7) / 8, 148 * 64);
+    kern<<<g, 256, smem, (cudaStream_t)stream>>>(csr->rowptr_node, csr->n2c_ptr, csr->n2c, csr->mesh->nb,
+                                                 rows, pos, K, elem_begin, elem_end, csr->hmax, values);
+  };
+  if (csr->pos_bytes == 1) launch((const uint8_t*)csr->pos_in_row);
+  else if (csr->pos_bytes == 2) launch((const uint16_t*)csr->pos_in_row);
+  else launch((const int32_t*)csr->pos_in_row);
   feb200::count_launch();
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? feb200::set_error(FE_OK, "") : feb200::set_error(FE_ERR_CUDA, cudaGetErrorString(e));

@@ -329,3 +329,25 @@ def test_pipelined_many_batches_per_cta(form, p, shape, ctas, monkeypatch):
     assert rel(r_elem.cpu().numpy(), r_ref) <= TOL64
     R_ref = oracle.assemble(r_ref, pr.dof_conn, pr.n_nodes, pr.ncomp)
     assert rel(r_glob.cpu().numpy().ravel(), R_ref) <= TOL64
+
+
+@pytest.mark.parametrize("form,p", [(0, 1), (0, 2), (3, 2), (4, 2)])
+def test_csr_gather_deterministic(form, p, monkeypatch):
+    """FEB200_CSR_IMPL=gather: atomic-free row-owner assembly == the atomic one, and two runs
+    are bitwise identical (fixed summation order)."""
+    pr = fi.make_problem(form, p, (4, 3, 5), 8000 + form)
+    mesh = gpu_mesh(pr)
+    K = mesh.element_matrices(form, pr.mat_kind, dev(pr.mat_a), dev(pr.mat_b),
+                              dev(pr.u) if form == fi.CONVECTIVE else None)
+    csr = fe().CSR(mesh, pr.ncomp)
+    ref = csr.assemble(K)
+    monkeypatch.setenv("FEB200_CSR_IMPL", "gather")
+    a = csr.assemble(K)
+    b = csr.assemble(K)
+    assert torch.equal(a, b)
+    assert rel(a.cpu().numpy(), ref.cpu().numpy()) <= 1e-14
+    # element ranges accumulate
+    c = torch.zeros_like(a)
+    csr.assemble(K[:7], elem_begin=0, elem_end=7, values=c)
+    csr.assemble(K[7:], elem_begin=7, elem_end=pr.n_elems, values=c)
+    assert rel(c.cpu().numpy(), ref.cpu().numpy()) <= 1e-14
