@@ -28,9 +28,6 @@
 #ifndef FEB200_SFP
 #define FEB200_SFP 1
 #endif
-#ifndef FEB200_SFP_X3
-#define FEB200_SFP_X3 0
-#endif
 #ifndef FEB200_SFP_NOSTORE
 #define FEB200_SFP_NOSTORE 0
 #endif
@@ -417,16 +414,11 @@ struct SFP {
   static constexpr int YP = N1 * N1, YPS = N1 * (N1 + 1) / 2;
   static constexpr int TOFF = YP * (N1 * (N1 - 1) / 2);
   static constexpr int TPE = TOFF + N1 * YPS;             // X tasks per cell (one y pair each)
-  // X3: one task per (z pair, iy) doing all jy (diagonal z pairs redundantly: no symmetry
-  // in y) -- each T1 vector loaded from shared memory serves N1 y pairs instead of one
-  static constexpr bool X3 = FEB200_SFP_X3 != 0;
-  static constexpr int TPE3 = N1 * N1 * (N1 + 1) / 2;
   static constexpr int E = P == 1 ? 16 : FEB200_SFP_E2;   // cells per batch (even: TMA size)
   static constexpr int GH = FEB200_SFP_GH;                // G thread groups per column
   static constexpr int NGW = (E * Q2 + 31) / 32;          // G warps per group
   static constexpr int NG = GH * NGW;                     // G warps
-  static constexpr int NXW = (E * (N1 * (N1 + 1) / 2) + 31) / 32;  // X3 warps per iy
-  static constexpr int NX = X3 ? N1 * NXW : (E * TPE + 31) / 32;  // X warps
+  static constexpr int NX = (E * TPE + 31) / 32;           // X warps
   static constexpr int THREADS = 32 * (1 + NG + NX);
   static constexpr int QQP = (Q2 + 1) / 2 * 2;
   // shared memory (bytes)
@@ -717,139 +709,6 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
       }
       sfp_arrive(&fullT[sl]);
     }
-  } else if constexpr (L::X3) {
-    // ============ X3: one task per (cell, z pair, iy) doing every jy; iy is warp-uniform ============
-    // Each T1 vector read from shared memory serves N1 y pairs (the shared-memory data pipe
-    // is the binding resource of this kernel); with iy and jy compile-time, the stage-y
-    // coefficients B^ay[qy][iy] B^by[qy][jy] are constant-bank operands (c_zz).
-    const int xtid = tid - 32 * (1 + L::NG);
-    const int iyw = xtid / (32 * L::NXW), xr_ = xtid - iyw * 32 * L::NXW;
-    constexpr int NZP = N1 * (N1 + 1) / 2, NOFF = N1 * (N1 - 1) / 2;
-    const int x_el = xr_ / NZP, zp = xr_ - x_el * NZP;
-    const bool xact = xr_ < E * NZP;
-    int iz = 0, jz = 0;
-    if (zp < NOFF) {
-      int c = zp;
-      for (int a = 0; a < N1; ++a) {
-        if (c < N1 - 1 - a) { iz = a; jz = a + 1 + c; break; }
-        c -= N1 - 1 - a;
-      }
-    } else {
-      iz = jz = zp - NOFF;
-    }
-    const bool offz = iz < jz;
-    constexpr int NXT = 32 * L::NX;
-    auto body = [&](auto IYc, const double* T1e, double* Ke) {
-      constexpr int IY = decltype(IYc)::value;
-      double S[N1][4][Q1];
-#pragma unroll
-      for (int j = 0; j < N1; ++j)
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int q = 0; q < Q1; ++q) S[j][c][q] = 0.0;
-#pragma unroll
-      for (int op = 0; op < NOP; ++op) {
-        int m, n;
-        if (DIFF && op < 9) { m = op / 3; n = op % 3; } else { m = 3; n = 3; }
-        const int mm = m < n ? m : n, nn = m < n ? n : m;
-        const int ul = (mm == 3) ? NUP - 1 : (mm == 0 ? nn : (mm == 1 ? 2 + nn : 5));
-        const int zidx = (m > n) ? (jz * N1 + iz) : (iz * N1 + jz);
-        const int ay = m == 1, by = n == 1, cls = (m == 0) * 2 + (n == 0);
-        const double2* src = reinterpret_cast<const double2*>(T1e + (ul * N1 * N1 + zidx) * QQP);
-        double tv[QQP];
-#pragma unroll
-        for (int h = 0; h < Q2 / 2; ++h) {  // Q2 of the QQP values: the odd one by LDS.64
-          const double2 v = src[h];
-          tv[2 * h] = v.x;
-          tv[2 * h + 1] = v.y;
-        }
-        if (Q2 & 1) tv[Q2 - 1] = reinterpret_cast<const double*>(src)[Q2 - 1];
-#pragma unroll
-        for (int j = 0; j < N1; ++j)
-#pragma unroll
-          for (int qx = 0; qx < Q1; ++qx)
-#pragma unroll
-            for (int qy = 0; qy < Q1; ++qy)
-              S[j][cls][qx] = fma(c_zz[P][ay][by][qy][IY][j], tv[qx * Q1 + qy], S[j][cls][qx]);
-      }
-      return [&, S]() {  // stage x + K writes, run after the T1 slot is released
-#pragma unroll
-        for (int j = 0; j < N1; ++j) {
-          double acc[N1][N1];
-#pragma unroll
-          for (int a = 0; a < N1; ++a)
-#pragma unroll
-            for (int bb = 0; bb < N1; ++bb) acc[a][bb] = 0.0;
-#pragma unroll
-          for (int qx = 0; qx < Q1; ++qx)
-#pragma unroll
-            for (int ax = 0; ax < 2; ++ax) {
-              double u[N1];
-#pragma unroll
-              for (int bb = 0; bb < N1; ++bb)
-                u[bb] = Bt(0, qx, bb) * S[j][ax * 2 + 0][qx] + Bt(1, qx, bb) * S[j][ax * 2 + 1][qx];
-#pragma unroll
-              for (int a = 0; a < N1; ++a)
-#pragma unroll
-                for (int bb = 0; bb < N1; ++bb) acc[a][bb] = fma(Bt(ax, qx, a), u[bb], acc[a][bb]);
-            }
-          const int ib = N1 * (IY + N1 * iz), jb = N1 * (j + N1 * jz);
-#pragma unroll
-          for (int a = 0; a < N1; ++a)
-#pragma unroll
-            for (int bb = 0; bb < N1; ++bb) {
-              Ke[(ib + a) * NB + jb + bb] = acc[a][bb];
-              if (offz) Ke[(jb + bb) * NB + ib + a] = acc[a][bb];
-            }
-        }
-      };
-    };
-    for (int64_t it = 0;; ++it) {
-      const int64_t b = blockIdx.x + it * (int64_t)gridDim.x;
-      if (b >= nbatch) break;
-      const int64_t lb = b * E;
-      const int ne = (int)((nloc - lb) < E ? (nloc - lb) : E);
-      const int sl = (int)(it & 1);
-      SFP_T(5, sfp_named_bar(1, NXT));
-      SFP_T(4, sfp_wait(&fullT[sl], (uint32_t)((it >> 1) & 1)));
-      double* Kst = reinterpret_cast<double*>(smp + L::OFF_K + sl * L::KSLOT);
-      const double* T1e = reinterpret_cast<const double*>(smp + L::OFF_T1 + sl * L::T1SLOT) +
-                          (xact ? x_el : 0) * NUP * N1 * N1 * QQP;
-      double* Ke = Kst + x_el * NB * NB;
-      const bool wr = xact && x_el < ne;
-      auto run = [&](auto IYc) {
-        auto fin = body(IYc, T1e, Ke);
-        sfp_arrive(&emptyT[sl]);
-        if (wr) fin();
-      };
-      if (!xact) {
-        sfp_arrive(&emptyT[sl]);
-      } else if (iyw == 0) {
-        run(std::integral_constant<int, 0>{});
-      } else if (iyw == 1) {
-        run(std::integral_constant<int, 1>{});
-      } else if constexpr (N1 > 2) {
-        if (iyw == 2) run(std::integral_constant<int, 2>{});
-        else if constexpr (N1 > 3) run(std::integral_constant<int, 3>{});
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      SFP_T(6, sfp_named_bar(2, NXT));
-      const uint32_t bytes = (uint32_t)ne * NB * NB * 8;
-      double* gdst = K + lb * NB * NB;
-      if (FEB200_SFP_NOSTORE) {
-      } else if (((reinterpret_cast<uintptr_t>(gdst) | bytes) & 15u) == 0) {
-        if (xtid == 0) {
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                       :: "l"(gdst), "r"(smem_u32(Kst)), "r"(bytes) : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        }
-      } else {
-        for (int i = xtid; i < ne * NB * NB; i += NXT) gdst[i] = Kst[i];
-      }
-    }
-    if (xtid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else {
     // ======================= X: stages y and x, K store =======================
     const int xtid = tid - 32 * (1 + L::NG);
