@@ -318,6 +318,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--fused", action="store_true",
+                    help="C2-type steps: fe_eval_matrix_residual (K_e and r_e = K_e u_e from one "
+                         "pass) instead of the separate matrix and residual kernels")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -340,6 +343,10 @@ def main():
     cfg = args.config
     modes = WORKLOADS[cfg]["modes"]
     prob = build_problem(cfg)
+    # linear scalar forms at p <= 2: matrix + residual in one kernel (r_e = K_e u_e, pin P8)
+    fused = (args.fused and tuple(modes) == ("matrix", "residual") and args.dtype == "f64"
+             and prob.form in (fi.DIFFUSION, fi.MASS, fi.MASS_DIFFUSION) and prob.p <= 2)
+    kmodes = ("matrix+residual",) if fused else tuple(modes)
     if cfg == "C5t" and world > 1:
         raise SystemExit("C5t (corner tangent) is single-GPU")
     tdt = torch.float64 if args.dtype == "f64" else torch.float32
@@ -373,9 +380,24 @@ def main():
     stream = torch.cuda.current_stream(dev)
     comm_stream = torch.cuda.Stream(dev) if world > 1 else None
     bufs = [None]
-    ev = {m: [] for m in modes}
+    ev = {m: [] for m in kmodes}
 
     def step(record=False):
+        if fused:
+            r.zero_()
+            if record:
+                a = torch.cuda.Event(enable_timing=True); a.record(stream)
+
+            def evaluate_f(lo, hi):
+                fe.fe_eval_matrix_residual(mesh.handle, prob.form, fe.F64, prob.mat_kind, mat_a,
+                                           mat_b, u, lo, hi, K[lo:hi], None, r, stream)
+
+            bufs[0] = slabs.residual_overlapped(evaluate_f, r, sl, prob.shape,
+                                                comm_stream if world > 1 else None, bufs[0])
+            if record:
+                b = torch.cuda.Event(enable_timing=True); b.record(stream)
+                ev["matrix+residual"].append((a, b))
+            return
         if "matrix" in modes:
             if record:
                 a = torch.cuda.Event(enable_timing=True); a.record(stream)
@@ -425,12 +447,32 @@ def main():
         barrier()
     launches = fe.fe_launch_count() - n_launch0
     ms = t0.elapsed_time(t1)
-    kern_ms = {m: float(np.mean([a.elapsed_time(b) for a, b in ev[m]])) for m in modes}
+    kern_ms = {m: float(np.mean([a.elapsed_time(b) for a, b in ev[m]])) for m in kmodes}
     if world > 1:
-        tt = torch.tensor([ms] + [kern_ms[m] for m in modes], device=dev, dtype=torch.float64)
+        tt = torch.tensor([ms] + [kern_ms[m] for m in kmodes], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt[0])
-        kern_ms = {m: float(tt[1 + i]) for i, m in enumerate(modes)}
+        kern_ms = {m: float(tt[1 + i]) for i, m in enumerate(kmodes)}
+    # the same step with separate matrix and residual kernels (transparency for the fused path)
+    unfused = None
+    if fused and world == 1:
+        n_u = 20
+        ea = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        tm, tr = 0.0, 0.0
+        for _ in range(n_u):
+            ea[0].record(stream)
+            fe.fe_eval_element_matrices(mesh.handle, prob.form, fe.F64, prob.mat_kind, mat_a, mat_b,
+                                        None, 0, El, K, stream)
+            ea[1].record(stream)
+            r.zero_()
+            fe.fe_eval_residual(mesh.handle, prob.form, dtc, prob.mat_kind, mat_a, mat_b, u, 0, El,
+                                None, r, stream)
+            ea[2].record(stream)
+            torch.cuda.synchronize(dev)
+            tm += ea[0].elapsed_time(ea[1])
+            tr += ea[1].elapsed_time(ea[2])
+        unfused = {"matrix_ms": tm / n_u, "residual_ms": tr / n_u, "step_ms": (tm + tr) / n_u,
+                   "note": "separate fe_eval_element_matrices + fe_eval_residual, not the timed step"}
     ms_step = ms / args.steps
     value = prob.n_elems / (ms_step * 1e-3)
 
@@ -493,6 +535,36 @@ def main():
     pk_b, src_b = hbm_peak_gbs()
 
     def roofline_for(mode):
+        if mode == "matrix+residual":
+            kern_ms["matrix"] = kern_ms[mode]       # per-cell work of the matrix part only
+            rf = roofline_for("matrix")
+            del kern_ms["matrix"]
+            extra_b = (4 * nb + 3 * D * prob.p ** 3 * 8) * El      # dof ids, u gather, r RMW
+            extra_f = 2 * nb * nb * El                             # r_e = K_e u_e
+            t_s = kern_ms[mode] * 1e-3
+            by = rf["alg_bytes_per_cell"] * El + extra_b
+            fl = rf["alg_flops_per_cell"] * El + extra_f
+            hb, hsrc = hbm_peak_gbs()
+            fpk, fsrc = fp64_peak_tflops("dfma_tflops_sustained")
+            if fl / (fpk * 1e12) >= by / (hb * 1e9):
+                base = {"bound": "alu", "achieved": fl / t_s / 1e12, "peak": fpk, "unit": "TFLOP/s",
+                        "frac": fl / t_s / 1e12 / fpk, "peak_source": fsrc}
+            else:
+                base = {"bound": "hbm", "achieved": by / t_s / 1e9, "peak": hb, "unit": "GB/s",
+                        "frac": by / t_s / 1e9 / hb, "peak_source": hsrc}
+            rf.update(base)
+            rf.update({"kernel": f"matrix+residual fused ({fi.FORM_NAMES[prob.form]}, Q{prob.p}, "
+                                 "sum-factorised, r_e = K_e u_e)",
+                       "kernel_ms": kern_ms[mode], "alg_flops_per_cell": fl / El,
+                       "alg_bytes_per_cell": by / El, "achieved_gbs": by / t_s / 1e9,
+                       "achieved_tflops": fl / t_s / 1e12, "traffic": None})
+            prof_ = os.path.join(ROOT, "profiles", f"traffic_{cfg}_{mode}.json")
+            if os.path.exists(prof_):
+                try:
+                    rf["traffic"] = json.load(open(prof_)).get("dram_bytes_per_launch")
+                except Exception:
+                    pass
+            return rf
         fl_lean = alg_flops(prob.form, mode, nb, nq) * El
         if mode == "matrix":
             sf = uses_sf_matrix(prob.form, prob.p) or (
@@ -549,8 +621,8 @@ def main():
                 pass
         return rf
 
-    dom = max(modes, key=lambda m: kern_ms[m])
-    rooflines = {m: roofline_for(m) for m in modes}
+    dom = max(kmodes, key=lambda m: kern_ms[m])
+    rooflines = {m: roofline_for(m) for m in kmodes}
     roof = rooflines[dom]
     cb = None
     if not args.no_cpu_baseline and world == 1:
@@ -567,8 +639,9 @@ def main():
                    "l2": "no flush: every step writes/reads > L2 (C2 K = 1.53 GB)"},
         "modes": {m: {"kernel_ms": kern_ms[m], "cells_per_s": El / (kern_ms[m] * 1e-3),
                       "roofline": {k: rooflines[m][k] for k in ("bound", "achieved", "unit", "frac")}}
-                  for m in modes},
+                  for m in kmodes},
         "roofline": roof,
+        "unfused": unfused,
         "cpu_baseline": cb,
         "e2e": e2e,
         "gpu_launches": int(launches),

@@ -149,6 +149,19 @@ fe_status fe_eval_residual(const fe_mesh *mesh, int32_t form, int32_t dtype,
                            const fe_material *mat, const void *u, int64_t elem_begin,
                            int64_t elem_end, void *r_elem, void *r_global, void *stream);
 
+/* Matrix mode and residual mode of a LINEAR scalar form (DIFFUSION, MASS,
+ * MASS_DIFFUSION; order 1 or 2) in ONE pass: the element matrices K as in
+ * fe_eval_element_matrices, and from the same K_e the residual r_e = K_e u_e
+ * (Alg. 1 for a bilinear form, which is exactly K_e u_e up to rounding; oracle
+ * pin P8) with the fused scatter-add of fe_eval_residual (r_elem nullable and
+ * overwritten, r_global nullable and ACCUMULATED).  For a Newton-type step that
+ * needs both, this avoids the second geometry / contraction pass.  FE_F64 only;
+ * FE_ERR_UNSUPPORTED for other forms / orders. */
+fe_status fe_eval_matrix_residual(const fe_mesh *mesh, int32_t form, int32_t dtype,
+                                  const fe_material *mat, const void *u, int64_t elem_begin,
+                                  int64_t elem_end, void *K, void *r_elem, void *r_global,
+                                  void *stream);
+
 /* 'eval' mode ("the integral value in case all variables passed to
  * the evaluation function have associated DOFs"): the form with the test
  * function replaced by the field u itself, over cells [elem_begin, elem_end):

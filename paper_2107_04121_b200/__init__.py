@@ -64,6 +64,8 @@ def _load():
                                      P, P]
     lib.fe_assemble_vector.argtypes = [P, i32, i32, i64, i64, P, P, P]
     lib.fe_eval_scalar.argtypes = [P, i32, i32, ctypes.POINTER(fe_material), P, i64, i64, P, P]
+    lib.fe_eval_matrix_residual.argtypes = [P, i32, i32, ctypes.POINTER(fe_material), P, i64,
+                                            i64, P, P, P, P]
     lib.fe_create_csr.argtypes = [P, i32, P, ctypes.POINTER(P)]
     lib.fe_csr_info.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     lib.fe_csr_arrays.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P)]
@@ -76,7 +78,7 @@ def _load():
     lib.fe_launch_count.restype = i64
     for f in ("fe_create_mesh_geometry", "fe_destroy_mesh", "fe_mesh_info",
               "fe_eval_element_matrices", "fe_eval_residual", "fe_assemble_vector",
-              "fe_geometry", "fe_eval_scalar", "fe_create_csr", "fe_csr_info", "fe_csr_arrays",
+              "fe_geometry", "fe_eval_scalar", "fe_eval_matrix_residual", "fe_create_csr", "fe_csr_info", "fe_csr_arrays",
               "fe_csr_copy_arrays",
               "fe_assemble_matrix", "fe_destroy_csr"):
         getattr(lib, f).restype = ctypes.c_int
@@ -99,6 +101,7 @@ class _LazyLib:
 _lib = _LazyLib()
 ABI_SYMBOLS = ("fe_create_mesh_geometry", "fe_destroy_mesh", "fe_mesh_info",
                "fe_eval_element_matrices", "fe_eval_residual", "fe_assemble_vector", "fe_eval_scalar",
+               "fe_eval_matrix_residual",
                "fe_geometry", "fe_last_error", "fe_last_error_element", "fe_launch_count",
                "fe_create_csr", "fe_csr_info", "fe_csr_arrays", "fe_csr_copy_arrays",
                "fe_assemble_matrix", "fe_destroy_csr")
@@ -189,6 +192,15 @@ def fe_eval_residual(handle: int, form: int, dtype: int, mat_kind: int,
     m = _material(mat_kind, mat_a, mat_b)
     _check(_lib.fe_eval_residual(handle, form, dtype, ctypes.byref(m), _ptr(u), elem_begin,
                                  elem_end, _ptr(r_elem), _ptr(r_global), _stream(stream)))
+
+
+def fe_eval_matrix_residual(handle: int, form: int, dtype: int, mat_kind: int, mat_a, mat_b, u,
+                            elem_begin: int, elem_end: int, K, r_elem, r_global, stream=None):
+    """C-ABI fe_eval_matrix_residual: element matrices and r_e = K_e u_e in one kernel."""
+    m = _material(mat_kind, mat_a, mat_b)
+    _check(_lib.fe_eval_matrix_residual(handle, form, dtype, ctypes.byref(m), _ptr(u), elem_begin,
+                                        elem_end, _ptr(K), _ptr(r_elem), _ptr(r_global),
+                                        _stream(stream)))
 
 
 def fe_assemble_vector(handle: int, dtype: int, ncomp: int, elem_begin: int, elem_end: int,
@@ -307,6 +319,22 @@ class Mesh:
         fe_eval_residual(self.handle, form, dt, mat_kind, mat_a, mat_b, u, elem_begin, elem_end,
                          r_elem, r_global, stream)
         return r_elem, r_global
+
+    def matrix_residual(self, form, u, mat_kind=MAT_PER_QP, mat_a=None, mat_b=None, elem_begin=0,
+                        elem_end=None, K=None, r_elem=None, r_global=None, want_elem=False,
+                        stream=None):
+        """Element matrices and the residual r_e = K_e u_e of a linear scalar form, one pass."""
+        elem_end = self.n_elems if elem_end is None else elem_end
+        n = elem_end - elem_begin
+        if K is None:
+            K = torch.empty((n, self.nb, self.nb), dtype=torch.float64, device=self.device)
+        if want_elem and r_elem is None:
+            r_elem = torch.empty((n, self.nb), dtype=torch.float64, device=self.device)
+        if r_global is None:
+            r_global = torch.zeros((self.n_nodes, 1), dtype=torch.float64, device=self.device)
+        fe_eval_matrix_residual(self.handle, form, F64, mat_kind, mat_a, mat_b, u, elem_begin,
+                                elem_end, K, r_elem, r_global, stream)
+        return K, r_elem, r_global
 
     def assemble(self, r_elem, ncomp, r_global=None, elem_begin=0, elem_end=None, stream=None):
         elem_end = self.n_elems if elem_end is None else elem_end

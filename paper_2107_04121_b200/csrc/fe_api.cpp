@@ -286,6 +286,28 @@ fe_status fe_eval_residual(const fe_mesh* mesh, int32_t form, int32_t dtype, con
   return ok();
 }
 
+fe_status fe_eval_matrix_residual(const fe_mesh* mesh, int32_t form, int32_t dtype,
+                                  const fe_material* mat, const void* u, int64_t elem_begin,
+                                  int64_t elem_end, void* K, void* r_elem, void* r_global,
+                                  void* stream) {
+  fe_status s = check_common(mesh, form, elem_begin, elem_end);
+  if (s != FE_OK) return s;
+  if (dtype != FE_F64) return fail(FE_ERR_UNSUPPORTED, "fe_eval_matrix_residual is built for FE_F64 only");
+  if ((s = check_material(form, mat)) != FE_OK) return s;
+  if (form != FE_FORM_DIFFUSION && form != FE_FORM_MASS && form != FE_FORM_MASS_DIFFUSION)
+    return fail(FE_ERR_UNSUPPORTED, "fe_eval_matrix_residual: linear scalar forms only");
+  if (elem_end > elem_begin && (!K || !u)) return fail(FE_ERR_INVALID_ARG, "K / u is NULL");
+  feb200::MatArgs ma{mat ? mat->kind : 0, mat ? mat->a : nullptr, mat ? mat->b : nullptr};
+  cudaError_t e = feb200::launch_matrix_residual_sf(mesh, form, ma, (const double*)u, elem_begin,
+                                                    elem_end, (double*)K, (double*)r_elem,
+                                                    (double*)r_global, (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported)
+    return fail(FE_ERR_UNSUPPORTED, "fe_eval_matrix_residual: order " + std::to_string(mesh->order) +
+                                        " not built (orders 1, 2)");
+  if (e != cudaSuccess) return cuda_fail(e, "fe_eval_matrix_residual");
+  return ok();
+}
+
 fe_status fe_eval_scalar(const fe_mesh* mesh, int32_t form, int32_t dtype, const fe_material* mat,
                          const void* u, int64_t elem_begin, int64_t elem_end, double* value,
                          void* stream) {

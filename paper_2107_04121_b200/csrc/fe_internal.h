@@ -57,6 +57,9 @@ cudaError_t launch_matrix(const fe_mesh* m, int form, MatArgs mat, const double*
                           int64_t e0, int64_t e1, double* K, cudaStream_t st);
 cudaError_t launch_matrix_sf(const fe_mesh* m, int form, MatArgs mat, int64_t e0, int64_t e1,
                              double* K, cudaStream_t st);
+cudaError_t launch_matrix_residual_sf(const fe_mesh* m, int form, MatArgs mat, const double* u,
+                                      int64_t e0, int64_t e1, double* K, double* r_elem,
+                                      double* r_global, cudaStream_t st);
 template <typename T>
 cudaError_t launch_residual_sf(const fe_mesh* m, int form, MatArgs mat, const T* u, int64_t e0,
                                int64_t e1, T* r_elem, T* r_global, cudaStream_t st,

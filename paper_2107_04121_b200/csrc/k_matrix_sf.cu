@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_D
 //                  (b, c1) -> K staging slot [it % 2] -> one TMA bulk store
 // The geometry + stage-z thread uses compile-time pair indices, so every 1D
 // table operand is a constant-bank operand.
-template <int P, int NUPMAX>
+template <int P, int NUPMAX, bool RES = false>
 struct SFP {
   static constexpr int N1 = P + 1, Q1 = P + 1, NB = N1 * N1 * N1, NQ = Q1 * Q1 * Q1, Q2 = Q1 * Q1;
   static constexpr int YP = N1 * N1, YPS = N1 * (N1 + 1) / 2;
@@ -429,8 +429,15 @@ struct SFP {
   static constexpr size_t OFF_T1 = OFF_K + 2 * KSLOT;                 // [2][T1SLOT]
   static constexpr size_t OFF_L = OFF_T1 + 2 * T1SLOT;                // [2][LSLOT]
   static constexpr size_t OFF_CONN = OFF_L + 2 * LSLOT;               // [3][E * 8] int32
-  static constexpr size_t OFF_BAR = (OFF_CONN + 3 * E * 8 * 4 + 15) / 16 * 16;  // 11 mbarriers
-  static constexpr size_t BYTES = OFF_BAR + 16 * 8;
+  // fused residual (RES): u_e [SU][E][NB] and dof ids [SU][E][NB] in a ring the L warp fills
+  // SU - 1 batches ahead; row-group partial sums [E][NB][N1^2] (written and scattered by X
+  // within one batch)
+  static constexpr int SU = 4;
+  static constexpr size_t OFF_U = (OFF_CONN + 3 * E * 8 * 4 + 15) / 16 * 16;
+  static constexpr size_t OFF_R = OFF_U + (RES ? SU * size_t(E) * NB * 8 : 0);
+  static constexpr size_t OFF_DC = OFF_R + (RES ? size_t(E) * NB * N1 * N1 * 8 : 0);
+  static constexpr size_t OFF_BAR = (OFF_DC + (RES ? SU * size_t(E) * NB * 4 : 0) + 15) / 16 * 16;
+  static constexpr size_t BYTES = OFF_BAR + 24 * 8;  // 11 + 2 SU mbarriers
 };
 
 __device__ __forceinline__ void sfp_bar_init(uint64_t* bar, int count) {
@@ -472,13 +479,14 @@ __device__ __forceinline__ void sfp_named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <int P, int FORM>
+template <int P, int FORM, bool RES>
 __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM != FE_FORM_DIFFUSION ? 1 : 0)>::THREADS, 1)
     k_matrix_sfp(MeshView mv, const double* __restrict__ ma, const double* __restrict__ mb,
-                 int64_t e0, int64_t e1, double* __restrict__ K) {
+                 int64_t e0, int64_t e1, double* __restrict__ K, const double* __restrict__ u,
+                 double* __restrict__ r_elem, double* __restrict__ r_global) {
   constexpr bool DIFF = FORM != FE_FORM_MASS, MASS = FORM != FE_FORM_DIFFUSION;
   constexpr int NUP = (DIFF ? 6 : 0) + (MASS ? 1 : 0);
-  using L = SFP<P, NUP>;
+  using L = SFP<P, NUP, RES>;
   constexpr int N1 = L::N1, Q1 = L::Q1, NB = L::NB, NQ = L::NQ, Q2 = L::Q2, E = L::E;
   constexpr int QQP = L::QQP;
   constexpr int NOP = (DIFF ? 9 : 0) + (MASS ? 1 : 0);
@@ -509,9 +517,21 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
     sfp_bar_init(&bars[8], 1);
     sfp_bar_init(&bars[9], 1);
     sfp_bar_init(&bars[10], 1);
+    if (RES) {
+      for (int k = 0; k < L::SU; ++k) {
+        sfp_bar_init(&bars[11 + k], 32);                 // fullU[SU]: L -> X (u_e, dof ids)
+        sfp_bar_init(&bars[11 + L::SU + k], 32 * L::NX);  // doneR[SU]: X -> L (slot free)
+      }
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  uint64_t* fullU = bars + 11;
+  uint64_t* doneR = bars + 11 + L::SU;
+  double* Ub = reinterpret_cast<double*>(smp + L::OFF_U);    // [2][E][NB] gathered u_e
+  double* Rb = reinterpret_cast<double*>(smp + L::OFF_R);    // [2][E][NB] r_e accumulators
+  int32_t* DCb = reinterpret_cast<int32_t*>(smp + L::OFF_DC); // [2][E][NB] dof ids
+  (void)fullU; (void)doneR; (void)Ub; (void)Rb; (void)DCb;
 #define Bt(a, q, i) c_tab1d[P][a][q][i]
 
   if (warp == 0) {
@@ -556,6 +576,60 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
       conn_issue(1);
     }
     coords_issue(0);
+    constexpr int UPL = RES ? (E * NB + 31) / 32 : 1;
+    int32_t dnext[UPL];
+    auto load_dof = [&](int64_t j) {  // dof ids of the j-th batch (fused residual)
+      int64_t lbj;
+      int nej;
+      batch_of(j, lbj, nej);
+#pragma unroll
+      for (int h = 0; h < UPL; ++h) {
+        const int i = lane + 32 * h;
+        dnext[h] = (RES && i < nej * NB) ? mv.dof_conn[(e0 + lbj) * NB + i] : 0;
+      }
+    };
+    // fused residual: u_e of batch j into slot j % 2 (dof ids loaded one call ahead)
+    // fused residual, software-pipelined gathers: uvn / dcn hold u_e and the dof ids of the
+    // next batch to publish (their loads were issued one call earlier), dnext the dof ids
+    // of the batch after it
+    double uvn[UPL];
+    int32_t dcn[UPL];
+    auto issue_u = [&](int64_t j) {  // dcn = dof(j) (from dnext), uvn = u[dcn], dnext = dof(j+1)
+      int64_t lbj;
+      int nej;
+      batch_of(j, lbj, nej);
+#pragma unroll
+      for (int h = 0; h < UPL; ++h) {
+        const int i = lane + 32 * h;
+        dcn[h] = dnext[h];
+        uvn[h] = i < nej * NB ? u[dcn[h]] : 0.0;
+      }
+      load_dof(j + 1);
+    };
+    auto publish_u = [&](int64_t j) {  // u_e / dof ids of batch j (in uvn / dcn) -> slot j % SU
+      int64_t lbj;
+      int nej;
+      batch_of(j, lbj, nej);
+      if (nej <= 0) return;
+      const int sj = (int)(j % L::SU);
+      if (j >= L::SU)  // X released this slot (batch j - SU)
+        SFP_T(0, sfp_wait(&doneR[sj], (uint32_t)(((j - L::SU) / L::SU) & 1)));
+#pragma unroll
+      for (int h = 0; h < UPL; ++h) {
+        const int i = lane + 32 * h;
+        if (i < E * NB) {
+          DCb[sj * E * NB + i] = dcn[h];
+          Ub[sj * E * NB + i] = uvn[h];
+        }
+      }
+      sfp_arrive(&fullU[sj]);
+    };
+    if constexpr (RES) {
+      load_dof(0);
+      issue_u(0);
+      publish_u(0);
+      issue_u(1);
+    }
     for (int64_t it = 0;; ++it) {
       int64_t lb;
       int ne;
@@ -594,6 +668,12 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
       }
       sfp_arrive(&fullL[sl]);
       coords_issue(it + 1);
+      if constexpr (RES) {
+        // fused residual: scatter batch it-1 once X is done with it, then refill its u slot
+        // with batch it+1 (u_e of batch 0 was filled before the loop)
+        publish_u(it + 1);
+        issue_u(it + 2);
+      }
     }
   } else if (warp <= L::NG) {
     // ======================= G: geometry + stage z =======================
@@ -811,6 +891,8 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
         sfp_arrive(&emptyT[sl]);
       }
       double* Kst = reinterpret_cast<double*>(smp + L::OFF_K + sl * L::KSLOT);
+      const int su = (int)(it % L::SU);
+      if constexpr (RES) SFP_T(7, sfp_wait(&fullU[su], (uint32_t)((it / L::SU) & 1)));
       if (xact && yx_el < ne) {
         double* Ke = Kst + yx_el * NB * NB;
         const int ib = N1 * (iy + N1 * iz), jb = N1 * (jy + N1 * jz);
@@ -821,9 +903,46 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
             Ke[(ib + a) * NB + jb + bb] = acc[a][bb];
             if (mirror) Ke[(jb + bb) * NB + ib + a] = acc[a][bb];
           }
+        if constexpr (RES) {
+          // r_e = K_e u_e (Alg. 1 for a linear form, pin P8).  Row (ix, iy, iz) of K_e is
+          // split into N1^2 column groups (jy, jz) of N1 entries; exactly one task (direct
+          // or mirrored) owns each (row, group), so the partial sums go to fixed slots
+          // R[row][group] without atomics and are summed in a fixed order below.
+          const double* ue = Ub + (su * E + yx_el) * NB;
+          double* re = Rb + yx_el * NB * N1 * N1;
+          const int gj = jy + N1 * jz, gi = iy + N1 * iz;
+#pragma unroll
+          for (int a = 0; a < N1; ++a) {
+            double t = 0.0;
+#pragma unroll
+            for (int bb = 0; bb < N1; ++bb) t = fma(acc[a][bb], ue[jb + bb], t);
+            re[(ib + a) * N1 * N1 + gj] = t;
+          }
+          if (mirror) {
+#pragma unroll
+            for (int bb = 0; bb < N1; ++bb) {
+              double t = 0.0;
+#pragma unroll
+              for (int a = 0; a < N1; ++a) t = fma(acc[a][bb], ue[ib + a], t);
+              re[(jb + bb) * N1 * N1 + gi] = t;
+            }
+          }
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       SFP_T(6, sfp_named_bar(2, NXT));
+      if constexpr (RES) {
+        // sum the row groups, scatter r_e (fused assembly)
+        for (int i = xtid; i < ne * NB; i += NXT) {
+          const double* rg = Rb + (size_t)i * N1 * N1;
+          double v = 0.0;
+#pragma unroll
+          for (int g = 0; g < N1 * N1; ++g) v += rg[g];
+          if (r_elem) r_elem[lb * NB + i] = v;
+          if (r_global) atomicAdd(r_global + DCb[su * E * NB + i], v);
+        }
+        sfp_arrive(&doneR[su]);
+      }
       const uint32_t bytes = (uint32_t)ne * NB * NB * 8;
       double* gdst = K + lb * NB * NB;
       if (FEB200_SFP_NOSTORE) {
@@ -842,7 +961,7 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
   }
 #ifdef FEB200_SFP_PROF
   if (lane == 0) {
-    for (int k = 0; k < 7; ++k) if (prof_[k]) atomicAdd(&g_sfp_prof[k], prof_[k]);
+    for (int k = 0; k < 8; ++k) if (prof_[k]) atomicAdd(&g_sfp_prof[k], prof_[k]);
     const int role = warp == 0 ? 0 : (warp <= L::NG ? 1 : 2);
     atomicAdd(&g_sfp_prof[8 + role], (unsigned long long)(clock64() - tstart_));
     atomicAdd(&g_sfp_prof[12 + role], 1ull);
@@ -851,11 +970,12 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
 #undef Bt
 }
 
-template <int P, int FORM>
+template <int P, int FORM, bool RES = false>
 static cudaError_t launch_sfp_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int64_t e1, double* K,
-                                cudaStream_t st) {
-  using L = SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM != FE_FORM_DIFFUSION ? 1 : 0)>;
-  auto kern = k_matrix_sfp<P, FORM>;
+                                cudaStream_t st, const double* u = nullptr, double* r_elem = nullptr,
+                                double* r_global = nullptr) {
+  using L = SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM != FE_FORM_DIFFUSION ? 1 : 0), RES>;
+  auto kern = k_matrix_sfp<P, FORM, RES>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
   if (err != cudaSuccess) return err;
   int nsm = 148, dev = 0;
@@ -866,11 +986,32 @@ static cudaError_t launch_sfp_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int6
   grid = grid_cap(grid);
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, L::THREADS, L::BYTES, st>>>(view_of(mh), (const double*)mat.a, (const double*)mat.b,
-                                           e0, e1, K);
+                                           e0, e1, K, u, r_elem, r_global);
   count_launch();
   return cudaGetLastError();
 }
 
+// Matrix mode plus the residual of the same linear scalar form from the element matrices
+// (r_e = K_e u_e, scatter-added) in one pass of the pipelined kernel (p = 1, 2).
+cudaError_t launch_matrix_residual_sf(const fe_mesh* mh, int form, MatArgs mat, const double* u,
+                                      int64_t e0, int64_t e1, double* K, double* r_elem,
+                                      double* r_global, cudaStream_t st) {
+  if (mh->q1d != mh->order + 1 || (mh->order != 1 && mh->order != 2)) return cudaErrorNotSupported;
+#define SFPR_CASE(P)                                                                                     \
+  if (mh->order == P) switch (form) {                                                                    \
+      case FE_FORM_DIFFUSION:                                                                            \
+        return launch_sfp_t<P, FE_FORM_DIFFUSION, true>(mh, mat, e0, e1, K, st, u, r_elem, r_global);    \
+      case FE_FORM_MASS:                                                                                 \
+        return launch_sfp_t<P, FE_FORM_MASS, true>(mh, mat, e0, e1, K, st, u, r_elem, r_global);         \
+      case FE_FORM_MASS_DIFFUSION:                                                                       \
+        return launch_sfp_t<P, FE_FORM_MASS_DIFFUSION, true>(mh, mat, e0, e1, K, st, u, r_elem, r_global); \
+      default: return cudaErrorNotSupported;                                                             \
+    }
+  SFPR_CASE(1)
+  SFPR_CASE(2)
+#undef SFPR_CASE
+  return cudaErrorNotSupported;
+}
 
 template <int P, int FORM>
 static cudaError_t launch_sf_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int64_t e1, double* K,

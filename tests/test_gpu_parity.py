@@ -351,3 +351,36 @@ def test_csr_gather_deterministic(form, p, monkeypatch):
     csr.assemble(K[:7], elem_begin=0, elem_end=7, values=c)
     csr.assemble(K[7:], elem_begin=7, elem_end=pr.n_elems, values=c)
     assert rel(c.cpu().numpy(), ref.cpu().numpy()) <= 1e-14
+
+
+@pytest.mark.parametrize("form,p", [(0, 1), (0, 2), (1, 2), (3, 2), (3, 1)])
+@pytest.mark.parametrize("ctas", [0, 2])
+def test_matrix_residual_fused(form, p, ctas, monkeypatch):
+    """fe_eval_matrix_residual: K as fe_eval_element_matrices and r_e = K_e u_e (Alg. 1 for a
+    bilinear form, pin P8) with the fused scatter, against the oracle's direct residual."""
+    if ctas:
+        monkeypatch.setenv("FEB200_MAX_CTAS", str(ctas))
+    pr = fi.make_problem(form, p, (6, 4, 5), 9000 + 10 * form + p)
+    mesh = gpu_mesh(pr)
+    K, r_elem, r_glob = mesh.matrix_residual(form, dev(pr.u), pr.mat_kind, dev(pr.mat_a),
+                                             dev(pr.mat_b), want_elem=True)
+    assert rel(K.cpu().numpy(), oracle.problem_matrix(pr)) <= TOL64
+    r_ref = oracle.problem_residual(pr)
+    assert rel(r_elem.cpu().numpy(), r_ref) <= TOL64
+    R_ref = oracle.assemble(r_ref, pr.dof_conn, pr.n_nodes, pr.ncomp)
+    assert rel(r_glob.cpu().numpy().ravel(), R_ref) <= TOL64
+    # element ranges (ragged) accumulate into one global vector
+    R = torch.zeros_like(r_glob)
+    for a, b in [(0, 9), (9, 10), (10, pr.n_elems)]:
+        mesh.matrix_residual(form, dev(pr.u), pr.mat_kind, dev(pr.mat_a), dev(pr.mat_b),
+                             elem_begin=a, elem_end=b, r_global=R)
+    assert rel(R.cpu().numpy().ravel(), R_ref) <= TOL64
+
+
+def test_matrix_residual_unsupported():
+    m = fe()
+    pr = fi.make_problem(fi.ELASTICITY, 2, (2, 2, 2), 1)
+    mesh = gpu_mesh(pr)
+    with pytest.raises(m.FEError) as ei:
+        mesh.matrix_residual(fi.ELASTICITY, dev(pr.u), pr.mat_kind, dev(pr.mat_a), dev(pr.mat_b))
+    assert ei.value.status == m.FE_ERR_UNSUPPORTED

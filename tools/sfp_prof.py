@@ -23,20 +23,31 @@ a = None if pr.mat_a is None else torch.from_numpy(pr.mat_a).cuda()
 b = None if pr.mat_b is None else torch.from_numpy(pr.mat_b).cuda()
 lib = fe.lib()
 buf = (ctypes.c_ulonglong * 16)()
+FUSED = os.environ.get("SFP_PROF_FUSED") == "1"
+uu = torch.from_numpy(pr.u).cuda()
+
+
+def run():
+    if FUSED:
+        mesh.matrix_residual(pr.form, uu, pr.mat_kind, a, b)
+    else:
+        mesh.element_matrices(pr.form, pr.mat_kind, a, b, state)
+
+
 for _ in range(3):
-    mesh.element_matrices(pr.form, pr.mat_kind, a, b, state)
+    run()
 (lib.fe_debug_vp_prof if VP else lib.fe_debug_sfp_prof)(buf, 1)
 n = 20
 for _ in range(n):
-    mesh.element_matrices(pr.form, pr.mat_kind, a, b, state)
+    run()
 (lib.fe_debug_vp_prof if VP else lib.fe_debug_sfp_prof)(buf, 1)
 v = np.array(list(buf), dtype=np.float64)
 names = (["G bar", "L wait emptyL", "G wait fullL", "G wait emptyT", "X wait fullT", "X bar2", "X bar3"]
          if VP else ["L wait conn", "L wait emptyL", "G wait fullL", "G wait emptyT", "X wait fullT",
-                     "X bar1", "X bar2"])
+                     "X bar1", "X bar2", "X wait fullU"])
 warps = {0: v[12], 1: v[13], 2: v[14]}
 tot = {0: v[8], 1: v[9], 2: v[10]}
-role = [1 if VP else 0, 0, 1, 1, 2, 2, 2]
+role = [1 if VP else 0, 0, 1, 1, 2, 2, 2, 2]
 for k, nm in enumerate(names):
     r = role[k]
     print(f"{nm:16s} {v[k] / max(tot[r], 1):6.1%} of role time")
