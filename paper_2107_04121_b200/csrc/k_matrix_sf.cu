@@ -792,7 +792,18 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
   } else {
     // ======================= X: stages y and x, K store =======================
     const int xtid = tid - 32 * (1 + L::NG);
-    const int yx_el = xtid / L::TPE, yx_r = xtid - yx_el * L::TPE;
+    // task order: all off-diagonal z-pair tasks of the batch, then all diagonal ones, so that
+    // most warps are uniform and the diagonal warps can share T1 vectors between the two
+    // orders (m, n), (n, m) of a pair (same vector when iz == jz)
+    int yx_el, yx_r;
+    if (xtid < E * L::TOFF) {
+      yx_el = xtid / L::TOFF;
+      yx_r = xtid - yx_el * L::TOFF;
+    } else {
+      const int t = xtid - E * L::TOFF;
+      yx_el = t / (L::TPE - L::TOFF);
+      yx_r = L::TOFF + (t - yx_el * (L::TPE - L::TOFF));
+    }
     const bool xact = xtid < E * L::TPE;
     int iz = 0, jz = 0, iy = 0, jy = 0;
     if (yx_r < L::TOFF) {
@@ -814,6 +825,7 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
       }
     }
     const bool mirror = (iz < jz) || (iy < jy);
+    const bool diag_warp = __all_sync(0xffffffffu, !xact || iz == jz);  // all lanes vote
     double Byp[4][Q1];
 #pragma unroll
     for (int q = 0; q < Q1; ++q)
@@ -847,16 +859,8 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
         for (int c = 0; c < 4; ++c)
 #pragma unroll
           for (int q = 0; q < Q1; ++q) S[c][q] = 0.0;
-#pragma unroll
-        for (int op = 0; op < NOP; ++op) {
-          int m, n;
-          if (DIFF && op < 9) { m = op / 3; n = op % 3; } else { m = 3; n = 3; }
-          const int mm = m < n ? m : n, nn = m < n ? n : m;
-          const int ul = (mm == 3) ? NUP - 1 : (mm == 0 ? nn : (mm == 1 ? 2 + nn : 5));
-          const int zidx = (m > n) ? (jz * N1 + iz) : (iz * N1 + jz);
-          const int ay = m == 1, by = n == 1, cls = (m == 0) * 2 + (n == 0);
+        auto load_tv = [&](int ul, int zidx, double (&tv)[QQP]) {
           const double2* src = reinterpret_cast<const double2*>(T1e + (ul * N1 * N1 + zidx) * QQP);
-          double tv[QQP];
 #pragma unroll
           for (int h = 0; h < Q2 / 2; ++h) {  // Q2 of the QQP values: the odd one by LDS.64
             const double2 v = src[h];
@@ -864,11 +868,38 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
             tv[2 * h + 1] = v.y;
           }
           if (Q2 & 1) tv[Q2 - 1] = reinterpret_cast<const double*>(src)[Q2 - 1];
+        };
+        auto add_pair = [&](int m, int n, const double (&tv)[QQP]) {
+          const int ay = m == 1, by = n == 1, cls = (m == 0) * 2 + (n == 0);
 #pragma unroll
           for (int qx = 0; qx < Q1; ++qx)
 #pragma unroll
             for (int qy = 0; qy < Q1; ++qy)
               S[cls][qx] = fma(Byp[ay * 2 + by][qy], tv[qx * Q1 + qy], S[cls][qx]);
+        };
+        if (diag_warp) {
+          // diagonal z pair: T1^{u}[iz,iz] serves both orders of the unique pair u
+#pragma unroll
+          for (int ul = 0; ul < NUP; ++ul) {
+            int m, n;
+            upair(UBASE + ul, m, n);
+            double tv[QQP];
+            load_tv(ul, iz * N1 + iz, tv);
+            add_pair(m, n, tv);
+            if (m != n) add_pair(n, m, tv);
+          }
+        } else {
+#pragma unroll
+          for (int op = 0; op < NOP; ++op) {
+            int m, n;
+            if (DIFF && op < 9) { m = op / 3; n = op % 3; } else { m = 3; n = 3; }
+            const int mm = m < n ? m : n, nn = m < n ? n : m;
+            const int ul = (mm == 3) ? NUP - 1 : (mm == 0 ? nn : (mm == 1 ? 2 + nn : 5));
+            const int zidx = (m > n) ? (jz * N1 + iz) : (iz * N1 + jz);
+            double tv[QQP];
+            load_tv(ul, zidx, tv);
+            add_pair(m, n, tv);
+          }
         }
         sfp_arrive(&emptyT[sl]);
 #pragma unroll

@@ -3,6 +3,6 @@
 K="$1"; shift
 for lib in paper_2107_04121_b200/ab/lib_*.so; do
   v=$(basename $lib .so); echo -n "${v#lib_} parity: "
-  FEB200_LIB_PATH=$PWD/$lib timeout 600 python -m pytest tests -m gpu -x -q -k "$K" 2>&1 | tail -1
+  FEB200_LIB_PATH=$PWD/$lib timeout 300 python -m pytest tests -m gpu -x -q -k "$K" 2>&1 | tail -1
 done
 bash tools/gpu_ab.sh "$@"
