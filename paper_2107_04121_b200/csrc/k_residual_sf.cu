@@ -50,6 +50,12 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 #ifndef FEB200_RSF_PAD
 #define FEB200_RSF_PAD 1
 #endif
+#ifndef FEB200_RSF_EB3
+#define FEB200_RSF_EB3 12
+#endif
+#ifndef FEB200_RSF_MINB3
+#define FEB200_RSF_MINB3 2
+#endif
 #ifndef FEB200_RSF_PADB
 #define FEB200_RSF_PADB (sizeof(T) == 8 ? 96 : 32)
 #endif
@@ -62,7 +68,10 @@ struct RSF {
   static constexpr int D = FormD<FORM>::D;
   static constexpr int TPE = Q1 * Q1;  // threads per cell
   static constexpr int EB0 = P == 1 ? 32 : (P == 2 ? 28 : (P == 3 ? 16 : 8));  // multiples of 4 (TMA alignment)
-  static constexpr int EB = (D == 3 && P >= 3) ? EB0 / 2 : EB0;  // cells per CTA iteration
+  // cells per CTA iteration; vector forms at p = 2 use smaller batches so that the three
+  // components' register arrays fit without spilling (fewer, fatter threads per SM)
+  static constexpr int EB = (D == 3 && P >= 3) ? EB0 / 2 : ((D == 3 && P == 2) ? FEB200_RSF_EB3 : EB0);
+  static constexpr int MINB = (D == 3 && P == 2) ? FEB200_RSF_MINB3 : 2;
   static constexpr int THREADS = (EB * TPE + 31) / 32 * 32;
   static constexpr int THREADS_ = THREADS;
   // exchange buffer per cell (elements of T), padded so that consecutive cells start PADB
@@ -91,7 +100,7 @@ struct RSF {
 };
 
 template <int P, int FORM, typename T>
-__global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, 2)
+__global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MINB)
     k_residual_sf(MeshView mv, int mat_kind, const T* __restrict__ ma, const T* __restrict__ mb,
                   const T* __restrict__ u, int64_t e0, int64_t e1, T* __restrict__ r_elem,
                   T* __restrict__ r_global, double* __restrict__ eval_out) {
