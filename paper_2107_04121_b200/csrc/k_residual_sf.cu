@@ -53,6 +53,18 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 #ifndef FEB200_RSF_EB3
 #define FEB200_RSF_EB3 12
 #endif
+#ifndef FEB200_RSF_EB2
+#define FEB200_RSF_EB2 20
+#endif
+#ifndef FEB200_RSF_MINB2
+#define FEB200_RSF_MINB2 2
+#endif
+#ifndef FEB200_RSF_EB4
+#define FEB200_RSF_EB4 4
+#endif
+#ifndef FEB200_RSF_MINB4
+#define FEB200_RSF_MINB4 3
+#endif
 #ifndef FEB200_RSF_MINB3
 #define FEB200_RSF_MINB3 2
 #endif
@@ -70,8 +82,11 @@ struct RSF {
   static constexpr int EB0 = P == 1 ? 32 : (P == 2 ? 28 : (P == 3 ? 16 : 8));  // multiples of 4 (TMA alignment)
   // cells per CTA iteration; vector forms at p = 2 use smaller batches so that the three
   // components' register arrays fit without spilling (fewer, fatter threads per SM)
-  static constexpr int EB = (D == 3 && P >= 3) ? EB0 / 2 : ((D == 3 && P == 2) ? FEB200_RSF_EB3 : EB0);
-  static constexpr int MINB = (D == 3 && P == 2) ? FEB200_RSF_MINB3 : 2;
+  static constexpr int EB = (D == 3 && P >= 3) ? EB0 / 2
+                           : ((D == 3 && P == 2) ? FEB200_RSF_EB3
+                              : (P == 2 ? FEB200_RSF_EB2 : (P == 4 ? FEB200_RSF_EB4 : EB0)));
+  static constexpr int MINB = (D == 3 && P == 2) ? FEB200_RSF_MINB3
+                              : (D == 1 && P == 2 ? FEB200_RSF_MINB2 : (D == 1 && P == 4 ? FEB200_RSF_MINB4 : 2));
   static constexpr int THREADS = (EB * TPE + 31) / 32 * 32;
   static constexpr int THREADS_ = THREADS;
   // exchange buffer per cell (elements of T), padded so that consecutive cells start PADB
