@@ -28,6 +28,9 @@
 #ifndef FEB200_SFP
 #define FEB200_SFP 1
 #endif
+#ifndef FEB200_SFP_T1PAD
+#define FEB200_SFP_T1PAD 13
+#endif
 #ifndef FEB200_SFP_NOSTORE
 #define FEB200_SFP_NOSTORE 0
 #endif
@@ -423,7 +426,11 @@ struct SFP {
   static constexpr int QQP = (Q2 + 1) / 2 * 2;
   // shared memory (bytes)
   static constexpr size_t LSLOT = size_t(E) * (24 + (NUPMAX == 7 ? 2 : 1) * NQ) * 8;  // coords, coef a[, b]
-  static constexpr size_t T1SLOT = size_t(E) * NUPMAX * N1 * N1 * QQP * 8;
+  // per-cell T1 stride padded by T1PAD doubles (an odd pad makes the G threads' column stores
+  // of consecutive cells hit disjoint banks; X then reads the vectors with 8-B loads)
+  static constexpr int T1PAD = FEB200_SFP_T1PAD;
+  static constexpr int T1CELL = NUPMAX * N1 * N1 * QQP + T1PAD;
+  static constexpr size_t T1SLOT = size_t(E) * T1CELL * 8;
   static constexpr size_t KSLOT = size_t(E) * NB * NB * 8;
   static constexpr size_t OFF_K = 0;                                  // [2][KSLOT]
   static constexpr size_t OFF_T1 = OFF_K + 2 * KSLOT;                 // [2][T1SLOT]
@@ -775,7 +782,7 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
           int m, n;
           upair(UBASE + ul, m, n);
           const int az = m == 2, bz = n == 2;
-          double* out = T1 + (el * NUP + ul) * N1 * N1 * QQP + qxy;
+          double* out = T1 + el * L::T1CELL + ul * N1 * N1 * QQP + qxy;
 #pragma unroll
           for (int a = 0; a < N1; ++a)
 #pragma unroll
@@ -845,7 +852,7 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
       SFP_T(5, sfp_named_bar(1, NXT));
       SFP_T(4, sfp_wait(&fullT[sl], (uint32_t)((it >> 1) & 1)));
       const double* T1e = reinterpret_cast<const double*>(smp + L::OFF_T1 + sl * L::T1SLOT) +
-                          yx_el * NUP * N1 * N1 * QQP;
+                          yx_el * L::T1CELL;
       double acc[N1][N1];
       if (FEB200_SFP_NOX) {
 #pragma unroll
@@ -860,14 +867,20 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
 #pragma unroll
           for (int q = 0; q < Q1; ++q) S[c][q] = 0.0;
         auto load_tv = [&](int ul, int zidx, double (&tv)[QQP]) {
-          const double2* src = reinterpret_cast<const double2*>(T1e + (ul * N1 * N1 + zidx) * QQP);
+          const double* src1 = T1e + (ul * N1 * N1 + zidx) * QQP;
+          if constexpr (L::T1PAD % 2 == 1) {  // 8-B aligned vectors: LDS.64 (same wavefronts)
 #pragma unroll
-          for (int h = 0; h < Q2 / 2; ++h) {  // Q2 of the QQP values: the odd one by LDS.64
-            const double2 v = src[h];
-            tv[2 * h] = v.x;
-            tv[2 * h + 1] = v.y;
+            for (int h = 0; h < Q2; ++h) tv[h] = src1[h];
+          } else {
+            const double2* src = reinterpret_cast<const double2*>(src1);
+#pragma unroll
+            for (int h = 0; h < Q2 / 2; ++h) {  // Q2 of the QQP values: the odd one by LDS.64
+              const double2 v = src[h];
+              tv[2 * h] = v.x;
+              tv[2 * h + 1] = v.y;
+            }
+            if (Q2 & 1) tv[Q2 - 1] = src1[Q2 - 1];
           }
-          if (Q2 & 1) tv[Q2 - 1] = reinterpret_cast<const double*>(src)[Q2 - 1];
         };
         auto add_pair = [&](int m, int n, const double (&tv)[QQP]) {
           const int ay = m == 1, by = n == 1, cls = (m == 0) * 2 + (n == 0);
