@@ -106,8 +106,9 @@ struct RSF {
   static constexpr size_t OFF_XV = (OFF_X + size_t(EB) * XS * sizeof(T) + 15) / 16 * 16;
   static constexpr int XVS = 28;  // per-cell stride of the staged vertex coordinates (bank spread)
   static constexpr size_t OFF_SLOT = OFF_XV + size_t(EB) * XVS * 8;
-  static constexpr size_t OFF_BAR = OFF_SLOT + 2 * SL_SIZE;
-  static constexpr size_t BYTES = OFF_BAR + 16;
+  static constexpr int NSLOT = 3;  // index/material ring: TMA two batches ahead
+  static constexpr size_t OFF_BAR = OFF_SLOT + NSLOT * SL_SIZE;
+  static constexpr size_t BYTES = OFF_BAR + 8 * NSLOT;
   static constexpr int PX = (EB * 24 + THREADS_ - 1) / THREADS_;  // vertex coordinates per thread
   static constexpr bool VAL = FORM == FE_FORM_MASS || FORM == FE_FORM_VECTOR_MASS ||
                               FORM == FE_FORM_MASS_DIFFUSION || FORM == FE_FORM_CONVECTIVE;
@@ -157,16 +158,15 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
                                  : (FORM == FE_FORM_ELASTICITY && mat_kind == FE_MAT_PER_ELEM) ? 1 : 0);
   const bool has_mb = FORM == FE_FORM_MASS_DIFFUSION || (FORM == FE_FORM_ELASTICITY && nma > 0);
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int k = 0; k < L::NSLOT; ++k) mbar_init(&bars[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // TMA bulk loads of the contiguous per-batch blocks (conn, dof_conn, material) into slot j % 2
+  // TMA bulk loads of the contiguous per-batch blocks (conn, dof_conn, material) into slot j % NSLOT
   auto fetch_idx = [&](int64_t j) {
     const int64_t b = blockIdx.x + j * G;
     if (b >= nbatch) return;
-    const int sl = (int)(j & 1);
+    const int sl = (int)(j % L::NSLOT);
     unsigned char* base = slot_base(sl);
     const int64_t eb = e0 + b * EB;
     const int ne = (int)((e1 - eb) < EB ? (e1 - eb) : EB);
@@ -207,13 +207,13 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
   double x_next[L::PX];
   auto gather_next = [&](int64_t j) {
     const int64_t b = blockIdx.x + j * G;
-    const int sl = (int)(j & 1);
+    const int sl = (int)(j % L::NSLOT);
     const unsigned char* base = slot_base(sl);
     const int32_t* cs = reinterpret_cast<const int32_t*>(base + L::SL_CONN);
     const int32_t* ds = reinterpret_cast<const int32_t*>(base + L::SL_DOF);
     const int64_t eb = e0 + b * EB;
     const int ne = b < nbatch ? (int)((e1 - eb) < EB ? (e1 - eb) : EB) : 0;
-    if (ne > 0) mbar_wait(&bars[sl], (uint32_t)((j >> 1) & 1));
+    if (ne > 0) mbar_wait(&bars[sl], (uint32_t)((j / L::NSLOT) & 1));
     const bool v = active && el < ne;
 #pragma unroll
     for (int kz = 0; kz < N1; ++kz) {
@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
     }
   };
   fetch_idx(0);
+  fetch_idx(1);
   gather_next(0);
   int64_t it = 0;
   for (int64_t bidx = blockIdx.x; bidx < nbatch; bidx += G, ++it) {
@@ -236,9 +237,9 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
     const int ne = (int)((e1 - eb) < EB ? (e1 - eb) : EB);
     const bool valid = active && el < ne;
     const int64_t e = eb + el;
-    const int sl = (int)(it & 1);
+    const int sl = (int)(it % L::NSLOT);
     const unsigned char* base = slot_base(sl);
-    fetch_idx(it + 1);  // slot (it+1)%2 was last read by batch it-1 (done)
+    fetch_idx(it + 2);  // slot (it+2)%3 was last read by batch it-1 (done)
     // this batch's vertex coordinates and column values from the prefetch registers
 #pragma unroll
     for (int h = 0; h < L::PX; ++h) {
@@ -256,6 +257,8 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
 #pragma unroll
       for (int a = 0; a < D; ++a) uc[a][kz] = u_next[a][kz];
     }
+    // gathers of the next batch now, so that their latency overlaps this whole batch
+    gather_next(it + 1);
     MatQ<T> mq[Q1];
 #pragma unroll
     for (int qz = 0; qz < Q1; ++qz) {
@@ -502,7 +505,6 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
       for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
       if ((tid & 31) == 0 && ev != 0.0) atomicAdd(eval_out, ev);
     }
-    gather_next(it + 1);
     __syncthreads();
   }
 #undef B
