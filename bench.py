@@ -95,12 +95,14 @@ def sf_vector_matrix_flops(form: int, p: int) -> float:
 
 def sf_residual_flops(form: int, p: int) -> float:
     """Flops per cell of the sum-factorised residual kernel (k_residual_sf.cu), FMA = 2:
-    1D contractions 2 D (5 + V + 12 G) n^4 plus ~(100 + 40 D) per qp of geometry / flux."""
+    1D contractions 2 D (5 + V + 12 G) n^4 plus ~(100 + 40 D) per qp of geometry / flux; the
+    convective backward pass tests against v only (no y^T / x^T gradient arrays: 5 fewer)."""
     n = p + 1
     D = fi.FORM_NCOMP[form]
     G = 0 if form in (fi.MASS, fi.VECTOR_MASS) else 1
     V = 1 if form in (fi.MASS, fi.VECTOR_MASS, fi.MASS_DIFFUSION, fi.CONVECTIVE) else 0
-    return 2 * D * (5 + V + 12 * G) * n ** 4 + n ** 3 * (100 + 40 * D)
+    back = -5 if form == fi.CONVECTIVE else 0
+    return 2 * D * (5 + V + 12 * G + back) * n ** 4 + n ** 3 * (100 + 40 * D)
 
 
 def uses_sf_residual(p: int) -> bool:
