@@ -86,9 +86,11 @@ def sf_vector_matrix_flops(form: int, p: int) -> float:
     if form == fi.ELASTICITY:
         per_qp, nwp = GEOM + 282, 45
         x = 3 * sym_t * x_task(9) + 3 * full_t * x_task(9)
-    else:  # convective tangent
-        per_qp, nwp = GEOM + 650, 18
-        x = 3 * full_t * x_task(4) + 6 * sym_t * x_task(1)
+    else:  # convective tangent: one item for the 3 diagonal blocks (shared advection + 3
+        # reactions, stage x once for A and once per reaction), 6 off-diagonal reaction items
+        per_qp, nwp = GEOM + 650, 12
+        adv = 2 * 6 * q1 * q1 + 4 * q1 + q1 * 2 * (3 * n1 + 2 * n1 * n1) + 3 * q1 * 2 * (n1 + n1 * n1)
+        x = full_t * adv + 6 * sym_t * x_task(1)
     z = nwp * q1 * q1 * (2 * n1 * n1 * q1)
     return per_qp * nq + z + x
 

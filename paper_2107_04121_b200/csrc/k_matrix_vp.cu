@@ -131,19 +131,23 @@ struct VItems<FE_FORM_ELASTICITY> {
 
 template <>
 struct VItems<FE_FORM_CONVECTIVE> {
-  static constexpr int NITEM = 9, NPMAX = 4, QD = 22;
-  // items 0..2 diagonal (a,a); 3..8 off-diagonal (0,1) (0,2) (1,0) (1,2) (2,0) (2,1)
-  __host__ __device__ static constexpr int a(int i) { return i < 3 ? i : (i - 3) / 2; }
+  // item 0: the three diagonal blocks together -- the advection part A (pairs (3,n), n < 3,
+  // weight detw (Ji u)_n) is the same for every (a,a) and is contracted once, plus the three
+  // reaction parts R_aa (pair (3,3), weight detw du_a/dx_a); K_aa = A + R_aa.
+  // items 1..6: off-diagonal reaction blocks (0,1) (0,2) (1,0) (1,2) (2,0) (2,1), pair (3,3)
+  // with weight detw du_a/dx_b (symmetric 27 x 27 blocks).
+  static constexpr int NITEM = 7, NPMAX = 6, QD = 22;
+  __host__ __device__ static constexpr int a(int i) { return i < 1 ? 0 : (i - 1) / 2; }
   __host__ __device__ static constexpr int b(int i) {
-    return i < 3 ? i : ((i - 3) % 2 == 0 ? ((i - 3) / 2 == 0 ? 1 : 0) : ((i - 3) / 2 == 2 ? 1 : 2));
+    return i < 1 ? 0 : ((i - 1) % 2 == 0 ? ((i - 1) / 2 == 0 ? 1 : 0) : ((i - 1) / 2 == 2 ? 1 : 2));
   }
-  __host__ __device__ static constexpr bool sym(int i) { return i >= 3; }
+  __host__ __device__ static constexpr bool sym(int i) { return i >= 1; }
   __host__ __device__ static constexpr bool mirror(int) { return false; }
-  __host__ __device__ static constexpr int np(int i) { return i < 3 ? 4 : 1; }
+  __host__ __device__ static constexpr int np(int i) { return i < 1 ? 6 : 1; }
   __host__ __device__ static constexpr int pm(int, int) { return 3; }
-  __host__ __device__ static constexpr int pn(int i, int p) { return i < 3 ? p : 3; }
-  __host__ __device__ static constexpr int pbase(int i) { return i < 3 ? 4 * i : 12 + (i - 3); }
-  static constexpr int NWP = 18;
+  __host__ __device__ static constexpr int pn(int i, int p) { return (i < 1 && p < 3) ? p : 3; }
+  __host__ __device__ static constexpr int pbase(int i) { return i < 1 ? 0 : 6 + (i - 1); }
+  static constexpr int NWP = 12;
 };
 
 template <int P, int FORM>
@@ -426,21 +430,19 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
             du[a][1] = sy;
             du[a][2] = sz;
           }
-          // diagonal blocks: (3,n) advection dw (Ji u)_n, (3,3) reaction dw du_a/dx_a
+          // item 0: (3,n) advection dw (Ji u)_n (shared by the diagonal blocks), then the
+          // reactions dw du_a/dx_a of the diagonal blocks
 #pragma unroll
-          for (int n = 0; n < 3; ++n) {
-            const double jun = dw * (Ji[3 * n] * uq[0] + Ji[3 * n + 1] * uq[1] + Ji[3 * n + 2] * uq[2]);
-#pragma unroll
-            for (int a2 = 0; a2 < 3; ++a2) Wq[(4 * a2 + n) * NQ] = jun;
-          }
+          for (int n = 0; n < 3; ++n)
+            Wq[n * NQ] = dw * (Ji[3 * n] * uq[0] + Ji[3 * n + 1] * uq[1] + Ji[3 * n + 2] * uq[2]);
           // du_a/dx_b = sum_m du_a/dxi_m Ji[m][b]
 #pragma unroll
           for (int a2 = 0; a2 < 3; ++a2)
 #pragma unroll
             for (int b2 = 0; b2 < 3; ++b2) {
               const double g = dw * (du[a2][0] * Ji[b2] + du[a2][1] * Ji[3 + b2] + du[a2][2] * Ji[6 + b2]);
-              // item of block (a2, b2): diagonal -> pair 3 of item a2; off-diagonal -> item 3..8
-              const int slotw = a2 == b2 ? 4 * a2 + 3 : 12 + (2 * a2 + (b2 > a2 ? b2 - 1 : b2));
+              // diagonal -> pair 3 + a of item 0; off-diagonal -> the single pair of item 1..6
+              const int slotw = a2 == b2 ? 3 + a2 : 6 + (2 * a2 + (b2 > a2 ? b2 - 1 : b2));
               Wq[slotw * NQ] = g;
             }
         }
@@ -451,7 +453,7 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
       // full pair set) inside a runtime item loop, so the code stays in the instruction cache
       auto g_item = [&](auto SYMc, int i) {
         constexpr bool SYMI = decltype(SYMc)::value;
-        constexpr int NP = SYMI ? (L::CONV ? 1 : 6) : (L::CONV ? 4 : 9);
+        constexpr int NP = SYMI ? (L::CONV ? 1 : 6) : (L::CONV ? 6 : 9);
         const int s = (int)(gi % S);
         const double* Wi = Wsm + (act2 ? el2 : 0) * L::NWP * NQ + IT::pbase(i) * NQ + tx + Q1 * ty;
         VP_T(3, vp_wait(&emptyT[s], (uint32_t)(((gi / S) & 1) ^ 1)));
@@ -461,7 +463,7 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
           for (int p = 0; p < NP; ++p) {
             if (p % GH != h2) continue;
             const int m = L::CONV ? 3 : (SYMI ? vp_um(p) : p / 3);
-            const int n = L::CONV ? (SYMI ? 3 : p) : (SYMI ? vp_un(p) : p % 3);
+            const int n = L::CONV ? ((SYMI || p >= 3) ? 3 : p) : (SYMI ? vp_un(p) : p % 3);
             double Wq[Q1];
 #pragma unroll
             for (int qz = 0; qz < Q1; ++qz) Wq[qz] = Wi[p * NQ + Q2 * qz];
@@ -504,7 +506,8 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
       if (ne <= 0) break;
       auto item = [&](auto SYMc, int I, int ia, int ib_) {
         constexpr bool SYM = decltype(SYMc)::value;
-        constexpr int NP = SYM ? (L::CONV ? 1 : 6) : (L::CONV ? 4 : 9);
+        constexpr int NP = SYM ? (L::CONV ? 1 : 6) : (L::CONV ? 6 : 9);
+        constexpr bool ADV = L::CONV && !SYM;  // convective item 0: A + R_aa for the 3 diagonal blocks
         const bool MIR = IT::mirror(I);
         constexpr int TPE = SYM ? L::NSYM : L::NFULL;
         int el = xtid / TPE;
@@ -551,6 +554,7 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
         const double* T1e = reinterpret_cast<const double*>(smv + L::OFF_T1 + s * L::T1SLOT) +
                             (xact ? el : 0) * IT::NPMAX * N1 * N1 * QQP;
         double acc[N1][N1];
+        double accr[ADV ? 3 : 1][N1][N1];  // ADV: K_aa = A + R_aa
         if (xact) {
           double Byp[4][Q1];
 #pragma unroll
@@ -564,7 +568,22 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
           for (int c = 0; c < 4; ++c)
 #pragma unroll
             for (int q = 0; q < Q1; ++q) Sx[c][q] = 0.0;
-          constexpr int NOPS = SYM ? (NP == 1 ? 1 : 9) : NP;
+          constexpr int NOPS = SYM ? (NP == 1 ? 1 : 9) : (ADV ? 3 : NP);
+          double Sr[3][Q1];  // ADV: reaction accumulators of the three diagonal blocks (class (3,3))
+#pragma unroll
+          for (int a2 = 0; a2 < 3; ++a2)
+#pragma unroll
+            for (int q = 0; q < Q1; ++q) Sr[a2][q] = 0.0;
+          if constexpr (ADV) {
+#pragma unroll
+            for (int a2 = 0; a2 < 3; ++a2) {
+              const double* src = T1e + ((3 + a2) * N1 * N1 + iz * N1 + jz) * QQP;
+#pragma unroll
+              for (int qx = 0; qx < Q1; ++qx)
+#pragma unroll
+                for (int qy = 0; qy < Q1; ++qy) Sr[a2][qx] = fma(Byp[0][qy], src[qx * Q1 + qy], Sr[a2][qx]);
+            }
+          }
 #pragma unroll
           for (int op = 0; op < NOPS; ++op) {
             int m, n, pidx, zidx;
@@ -579,7 +598,7 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
               }
             } else {
               m = L::CONV ? 3 : op / 3;
-              n = L::CONV ? op : op % 3;
+              n = L::CONV ? op : op % 3;  // ADV: the advection pairs (3, 0..2)
               pidx = op;
               zidx = iz * N1 + jz;
             }
@@ -615,6 +634,25 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
 #pragma unroll
                 for (int bb = 0; bb < N1; ++bb) acc[a][bb] = fma(Bt(ax, qx, a), u[bb], acc[a][bb]);
             }
+          if constexpr (ADV) {  // stage x of the reaction parts (value x value, class 0)
+#pragma unroll
+            for (int a2 = 0; a2 < 3; ++a2) {
+#pragma unroll
+              for (int a = 0; a < N1; ++a)
+#pragma unroll
+                for (int bb = 0; bb < N1; ++bb) accr[a2][a][bb] = acc[a][bb];
+#pragma unroll
+              for (int qx = 0; qx < Q1; ++qx) {
+                double u[N1];
+#pragma unroll
+                for (int bb = 0; bb < N1; ++bb) u[bb] = Bt(0, qx, bb) * Sr[a2][qx];
+#pragma unroll
+                for (int a = 0; a < N1; ++a)
+#pragma unroll
+                  for (int bb = 0; bb < N1; ++bb) accr[a2][a][bb] = fma(Bt(0, qx, a), u[bb], accr[a2][a][bb]);
+              }
+            }
+          }
         }
         vp_arrive(&emptyT[s]);
         if (I == xg) {
@@ -622,7 +660,17 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
           // K staging (elected thread, before this barrier of all X threads)
           VP_T(5, vp_named_bar(2, NXA));
         }
-        if (xact && el < ne) {
+        if (ADV && xact && el < ne) {  // K_aa = A + R_aa for a = 0, 1, 2
+          double* Kc = Kst + el * NDOF * NDOF;
+          const int ib = N1 * (iy + N1 * iz), jb = N1 * (jy + N1 * jz);
+#pragma unroll
+          for (int a2 = 0; a2 < 3; ++a2)
+#pragma unroll
+            for (int a = 0; a < N1; ++a)
+#pragma unroll
+              for (int bb = 0; bb < N1; ++bb)
+                Kc[(a2 * NB + ib + a) * NDOF + a2 * NB + jb + bb] = accr[a2][a][bb];
+        } else if (xact && el < ne) {
           double* Kc = Kst + el * NDOF * NDOF;
           const int ib = N1 * (iy + N1 * iz), jb = N1 * (jy + N1 * jz);
           const bool mir_in = SYM && (iz < jz || iy < jy);
