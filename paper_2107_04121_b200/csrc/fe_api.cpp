@@ -167,6 +167,8 @@ fe_status fe_create_mesh_geometry(int64_t n_vertices, const double* coords, int6
      "constant tables");
   CK(feb200::upload_const_tables_residual(order, T.b1.data(), T.d1.data(), T.x1.data(), T.w1.data(), st),
      "constant tables");
+  CK(feb200::upload_const_tables_residual_t3(order, T.b1.data(), T.d1.data(), T.x1.data(), T.w1.data(), st),
+     "constant tables");
   std::vector<float> tmp;
   auto upf = [&](float** dst, const std::vector<double>& src) {
     tmp.assign(src.begin(), src.end());
@@ -318,7 +320,12 @@ fe_status fe_eval_scalar(const fe_mesh* mesh, int32_t form, int32_t dtype, const
   if (dtype != FE_F64 && dtype != FE_F32) return fail(FE_ERR_INVALID_ARG, "unknown dtype");
   feb200::MatArgs ma{mat ? mat->kind : 0, mat ? mat->a : nullptr, mat ? mat->b : nullptr};
   cudaError_t e;
-  if (dtype == FE_F64)
+  e = cudaErrorNotSupported;
+  if (dtype == FE_F64 && feb200::want_residual_t3())
+    e = feb200::launch_residual_t3(mesh, form, ma, (const double*)u, elem_begin, elem_end, nullptr,
+                                   nullptr, (cudaStream_t)stream, value);
+  if (e != cudaErrorNotSupported) {
+  } else if (dtype == FE_F64)
     e = feb200::launch_residual_sf<double>(mesh, form, ma, (const double*)u, elem_begin, elem_end,
                                            nullptr, nullptr, (cudaStream_t)stream, value);
   else

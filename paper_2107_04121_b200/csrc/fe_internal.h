@@ -64,6 +64,12 @@ template <typename T>
 cudaError_t launch_residual_sf(const fe_mesh* m, int form, MatArgs mat, const T* u, int64_t e0,
                                int64_t e1, T* r_elem, T* r_global, cudaStream_t st,
                                double* eval_out = nullptr);
+cudaError_t launch_residual_t3(const fe_mesh* m, int form, MatArgs mat, const double* u, int64_t e0,
+                               int64_t e1, double* r_elem, double* r_global, cudaStream_t st,
+                               double* eval_out = nullptr);
+cudaError_t upload_const_tables_residual_t3(int order, const double* b1, const double* d1,
+                                           const double* x1, const double* w1, cudaStream_t st);
+bool want_residual_t3();
 cudaError_t launch_matrix_sfv(const fe_mesh* m, int form, MatArgs mat, const double* state_u,
                               int64_t e0, int64_t e1, double* K, cudaStream_t st);
 cudaError_t launch_matrix_vp(const fe_mesh* m, int form, MatArgs mat, const double* state_u,

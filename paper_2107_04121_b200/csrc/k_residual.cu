@@ -212,11 +212,20 @@ static bool want_dense_residual() {
   return impl && std::strcmp(impl, "dense") == 0;
 }
 
+// FEB200_RESIDUAL_IMPL=sf keeps the shared-memory sum-factorised kernel for every form
+bool want_residual_t3() {
+  const char* impl = std::getenv("FEB200_RESIDUAL_IMPL");
+  return !(impl && (std::strcmp(impl, "sf") == 0 || std::strcmp(impl, "dense") == 0));
+}
+
 cudaError_t launch_residual_f64(const fe_mesh* m, int form, MatArgs mat, const double* u,
                                 int64_t e0, int64_t e1, double* r_elem, double* r_global,
                                 cudaStream_t st) {
   if (!want_dense_residual()) {
-    cudaError_t e = launch_residual_sf<double>(m, form, mat, u, e0, e1, r_elem, r_global, st);
+    cudaError_t e = cudaErrorNotSupported;
+    if (want_residual_t3()) e = launch_residual_t3(m, form, mat, u, e0, e1, r_elem, r_global, st);
+    if (e != cudaErrorNotSupported) return e;
+    e = launch_residual_sf<double>(m, form, mat, u, e0, e1, r_elem, r_global, st);
     if (e != cudaErrorNotSupported) return e;
   }
   return res_dispatch<double>(m, form, mat, u, e0, e1, r_elem, r_global, st);

@@ -1,0 +1,307 @@
+// Register-resident residual mode for the scalar forms at p = 2 (Alg. 1, PAPER.md P:392-429,
+// with the gather and fused scatter-add of P:1093-1095): three threads per cell, thread j
+// owning the z-plane j of the cell -- its 3 x 3 nodes (kz = j) on the way in and its 3 x 3
+// quadrature points (qz = j) at the flux.  The x- and y-contractions of the sum
+// factorisation (Eq. fe1) run in registers; the z-contraction is the only
+// exchange and goes through warp shuffles between the three lanes of a cell (forward: the
+// other planes' partial sums; backward: each plane's contribution to the other node planes).
+// Shared memory is not used at all: the shared-memory data pipe that binds the column-per-
+// thread kernel (k_residual_sf.cu, four exchanges through smem) is bypassed.
+//   forward   u(kx,ky,kz=j) -> [x] -> [y] -> c00, c01, c10 at (qx,qy,kz=j)
+//             -> [z, shuffles] -> u, du/dxi at (qx,qy,qz=j)
+//   flux      geometry at the 9 qps (trilinear map), f0 = rho u, f1 = kappa grad u
+//             pulled back: F = detw J^-1 f1
+//   backward  [z^T, shuffles] -> [y^T] -> [x^T] -> r(kx,ky,kz=j) -> atomic scatter
+// 10 cells per warp (lanes 30, 31 idle).
+#include "fe_const.cuh"
+#include "fe_internal.h"
+
+#ifndef FEB200_T3_THREADS
+#define FEB200_T3_THREADS 128
+#endif
+#ifndef FEB200_T3_MINB
+#define FEB200_T3_MINB 2
+#endif
+
+namespace feb200 {
+
+cudaError_t upload_const_tables_residual_t3(int order, const double* b1, const double* d1,
+                                           const double* x1, const double* w1, cudaStream_t st) {
+  return upload_tables_this_tu(order, b1, d1, x1, w1, st);
+}
+
+template <int FORM, bool EVAL>
+__global__ void __launch_bounds__(FEB200_T3_THREADS, FEB200_T3_MINB)
+    k_residual_t3(MeshView mv, const double* __restrict__ ma, const double* __restrict__ mb,
+                  const double* __restrict__ u, int64_t e0, int64_t e1, double* __restrict__ r_elem,
+                  double* __restrict__ r_global, double* __restrict__ eval_out) {
+  constexpr int P = 2, N = 3, NB = 27, NQ = 27;
+  constexpr bool VAL = FORM == FE_FORM_MASS || FORM == FE_FORM_MASS_DIFFUSION;
+  constexpr bool GRAD = FORM != FE_FORM_MASS;
+#define B0(q, k) c_tab1d[P][0][q][k]
+#define B1(q, k) c_tab1d[P][1][q][k]
+  const int lane = threadIdx.x & 31;
+  const int cl = lane / 3, j = lane - 3 * cl;  // cell in the warp, plane
+  const bool lane_ok = lane < 30;
+  const int base = 3 * cl;
+  // per-lane coefficients B^a[qz = j][kz = (j + s) % 3] and the partner lanes
+  double f0[3], f1[3];
+  int srcf[3], srcb[3];
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    const int k = (j + s) % 3;
+    f0[s] = lane_ok ? c_tab1d[P][0][j][k] : 0.0;
+    f1[s] = lane_ok ? c_tab1d[P][1][j][k] : 0.0;
+    srcf[s] = lane_ok ? base + k : lane;                  // forward: plane (j + s) % 3
+    srcb[s] = lane_ok ? base + (j - s + 3) % 3 : lane;    // backward: plane (j - s) % 3
+  }
+  const double tZ = lane_ok ? c_x1d[P][j] : 0.5, wz = lane_ok ? c_w1d[P][j] : 0.0;
+  const int64_t nloc = e1 - e0;
+  const int wpb = blockDim.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5), nw = (int64_t)gridDim.x * wpb;
+  for (int64_t cg = gw * 10; cg < nloc; cg += nw * 10) {
+    const int64_t le = cg + cl;
+    const bool valid = lane_ok && le < nloc;
+    const int64_t e = e0 + (valid ? le : 0);
+    // ---- gather u at the nodes (kx, ky, kz = j)
+    int dof[N][N];
+    double uv[N][N];
+#pragma unroll
+    for (int ky = 0; ky < N; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < N; ++kx) {
+        dof[ky][kx] = valid ? mv.dof_conn[e * NB + kx + N * ky + N * N * j] : 0;
+        uv[ky][kx] = valid ? u[dof[ky][kx]] : 0.0;
+      }
+    // ---- x- and y-contractions in registers
+    double c00[N][N], c01[N][N], c10[N][N];  // [qy][qx] at kz = j
+    {
+      double a0[N][N], a1[N][N];  // [ky][qx]
+#pragma unroll
+      for (int ky = 0; ky < N; ++ky)
+#pragma unroll
+        for (int qx = 0; qx < N; ++qx) {
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int kx = 0; kx < N; ++kx) {
+            s0 = fma(B0(qx, kx), uv[ky][kx], s0);
+            if (GRAD) s1 = fma(B1(qx, kx), uv[ky][kx], s1);
+          }
+          a0[ky][qx] = s0;
+          a1[ky][qx] = s1;
+        }
+#pragma unroll
+      for (int qy = 0; qy < N; ++qy)
+#pragma unroll
+        for (int qx = 0; qx < N; ++qx) {
+          double s00 = 0.0, s01 = 0.0, s10 = 0.0;
+#pragma unroll
+          for (int ky = 0; ky < N; ++ky) {
+            s00 = fma(B0(qy, ky), a0[ky][qx], s00);
+            if (GRAD) {
+              s01 = fma(B1(qy, ky), a0[ky][qx], s01);
+              s10 = fma(B0(qy, ky), a1[ky][qx], s10);
+            }
+          }
+          c00[qy][qx] = s00;
+          c01[qy][qx] = s01;
+          c10[qy][qx] = s10;
+        }
+    }
+    // ---- z-contraction through the cell's three lanes: value / reference gradient at qz = j
+    double Uq[N][N], Gx[N][N], Gy[N][N], Gz[N][N];
+#pragma unroll
+    for (int qy = 0; qy < N; ++qy)
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        double v00 = c00[qy][qx], v01 = c01[qy][qx], v10 = c10[qy][qx];
+        double uq = f0[0] * v00, gz = f1[0] * v00, gy = f0[0] * v01, gx = f0[0] * v10;
+#pragma unroll
+        for (int s = 1; s < 3; ++s) {
+          const double w00 = __shfl_sync(0xffffffffu, v00, srcf[s]);
+          uq = fma(f0[s], w00, uq);
+          if (GRAD) {
+            const double w01 = __shfl_sync(0xffffffffu, v01, srcf[s]);
+            const double w10 = __shfl_sync(0xffffffffu, v10, srcf[s]);
+            gz = fma(f1[s], w00, gz);
+            gy = fma(f0[s], w01, gy);
+            gx = fma(f0[s], w10, gx);
+          }
+        }
+        Uq[qy][qx] = uq;
+        Gx[qy][qx] = gx;
+        Gy[qy][qx] = gy;
+        Gz[qy][qx] = gz;
+      }
+    // ---- geometry and flux at the 9 qps (qx, qy, qz = j); F = detw J^-1 f1 (reference)
+    double X[8][3];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const int32_t cv = valid ? mv.conn[8 * e + v] : 0;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) X[v][i] = valid ? mv.coords[3 * (int64_t)cv + i] : 0.0;
+    }
+    double Fv[N][N], Fx[N][N], Fy[N][N], Fz[N][N];
+#pragma unroll
+    for (int qy = 0; qy < N; ++qy)
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        const double t0 = c_x1d[P][qx], t1 = c_x1d[P][qy], t2 = tZ;
+        double J[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          J[i][0] = (1 - t1) * (1 - t2) * (X[1][i] - X[0][i]) + t1 * (1 - t2) * (X[3][i] - X[2][i]) +
+                    (1 - t1) * t2 * (X[5][i] - X[4][i]) + t1 * t2 * (X[7][i] - X[6][i]);
+          J[i][1] = (1 - t0) * (1 - t2) * (X[2][i] - X[0][i]) + t0 * (1 - t2) * (X[3][i] - X[1][i]) +
+                    (1 - t0) * t2 * (X[6][i] - X[4][i]) + t0 * t2 * (X[7][i] - X[5][i]);
+          J[i][2] = (1 - t0) * (1 - t1) * (X[4][i] - X[0][i]) + t0 * (1 - t1) * (X[5][i] - X[1][i]) +
+                    (1 - t0) * t1 * (X[6][i] - X[2][i]) + t0 * t1 * (X[7][i] - X[3][i]);
+        }
+        // cofactors C[r][c] of J; J^-1[m][r] = C[r][m] / det
+        const double C00 = J[1][1] * J[2][2] - J[1][2] * J[2][1], C01 = J[1][2] * J[2][0] - J[1][0] * J[2][2],
+                     C02 = J[1][0] * J[2][1] - J[1][1] * J[2][0], C10 = J[0][2] * J[2][1] - J[0][1] * J[2][2],
+                     C11 = J[0][0] * J[2][2] - J[0][2] * J[2][0], C12 = J[0][1] * J[2][0] - J[0][0] * J[2][1],
+                     C20 = J[0][1] * J[1][2] - J[0][2] * J[1][1], C21 = J[0][2] * J[1][0] - J[0][0] * J[1][2],
+                     C22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+        const double det = J[0][0] * C00 + J[0][1] * C01 + J[0][2] * C02;
+        const double wq = c_w1d[P][qx] * c_w1d[P][qy] * wz;
+        const int q = qx + N * qy + N * N * j;
+        double fv = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+        if (valid) {
+          if constexpr (VAL) {
+            const double rho = ma[e * NQ + q];
+            fv = wq * det * rho * Uq[qy][qx];
+          }
+          if constexpr (GRAD) {
+            const double kap = FORM == FE_FORM_MASS_DIFFUSION ? mb[e * NQ + q] : ma[e * NQ + q];
+            // grad u = J^-T grad_ref u: t_r = sum_m C[r][m] g_m (= det * (grad u)_r);
+            // F_m = detw kappa sum_r J^-1[m][r] (grad u)_r = (w kappa / det) sum_r C[r][m] t_r
+            const double g0 = Gx[qy][qx], g1 = Gy[qy][qx], g2 = Gz[qy][qx];
+            const double tr0 = C00 * g0 + C01 * g1 + C02 * g2;
+            const double tr1 = C10 * g0 + C11 * g1 + C12 * g2;
+            const double tr2 = C20 * g0 + C21 * g1 + C22 * g2;
+            const double sc = wq * kap / det;
+            fx = sc * (C00 * tr0 + C10 * tr1 + C20 * tr2);
+            fy = sc * (C01 * tr0 + C11 * tr1 + C21 * tr2);
+            fz = sc * (C02 * tr0 + C12 * tr1 + C22 * tr2);
+          }
+        }
+        Fv[qy][qx] = fv;
+        Fx[qy][qx] = fx;
+        Fy[qy][qx] = fy;
+        Fz[qy][qx] = fz;
+      }
+    // ---- z^T through the cell's lanes: node plane j collects the contributions
+    //      B^a[qz][kz = j] F(qz) of the three qp planes
+    double Hv[N][N], Hx[N][N], Hy[N][N];  // [qy][qx] at kz = j
+#pragma unroll
+    for (int qy = 0; qy < N; ++qy)
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        const double fv = Fv[qy][qx], fx = Fx[qy][qx], fy = Fy[qy][qx], fz = Fz[qy][qx];
+        double hv = 0.0, hx = 0.0, hy = 0.0;
+        if (VAL) hv = f0[0] * fv;
+        if (GRAD) {
+          hv = fma(f1[0], fz, hv);
+          hx = f0[0] * fx;
+          hy = f0[0] * fy;
+        }
+#pragma unroll
+        for (int s = 1; s < 3; ++s) {
+          // this lane's contribution to node plane (j + s) % 3; pulled by that plane's lane
+          double cv = 0.0, cx = 0.0, cy = 0.0;
+          if (VAL) cv = f0[s] * fv;
+          if (GRAD) {
+            cv = fma(f1[s], fz, cv);
+            cx = f0[s] * fx;
+            cy = f0[s] * fy;
+          }
+          hv += __shfl_sync(0xffffffffu, cv, srcb[s]);
+          if (GRAD) {
+            hx += __shfl_sync(0xffffffffu, cx, srcb[s]);
+            hy += __shfl_sync(0xffffffffu, cy, srcb[s]);
+          }
+        }
+        Hv[qy][qx] = hv;
+        Hx[qy][qx] = hx;
+        Hy[qy][qx] = hy;
+      }
+    // ---- y^T and x^T in registers, scatter
+    double ev = 0.0;
+#pragma unroll
+    for (int ky = 0; ky < N; ++ky) {
+      double Iv[N], Ix[N];  // [qx]
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        double sv = 0.0, sx = 0.0;
+#pragma unroll
+        for (int qy = 0; qy < N; ++qy) {
+          sv = fma(B0(qy, ky), Hv[qy][qx], sv);
+          if (GRAD) {
+            sv = fma(B1(qy, ky), Hy[qy][qx], sv);
+            sx = fma(B0(qy, ky), Hx[qy][qx], sx);
+          }
+        }
+        Iv[qx] = sv;
+        Ix[qx] = sx;
+      }
+#pragma unroll
+      for (int kx = 0; kx < N; ++kx) {
+        double rr = 0.0;
+#pragma unroll
+        for (int qx = 0; qx < N; ++qx) {
+          rr = fma(B0(qx, kx), Iv[qx], rr);
+          if (GRAD) rr = fma(B1(qx, kx), Ix[qx], rr);
+        }
+        if (valid) {
+          if (r_elem) r_elem[le * NB + kx + N * ky + N * N * j] = rr;
+          if (r_global) atomicAdd(r_global + dof[ky][kx], rr);
+          if (EVAL) ev = fma(rr, u[dof[ky][kx]], ev);
+        }
+      }
+    }
+    if (EVAL) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
+      if (lane == 0 && ev != 0.0) atomicAdd(eval_out, ev);
+    }
+  }
+#undef B0
+#undef B1
+}
+
+template <int FORM>
+static cudaError_t launch_t3_t(const fe_mesh* mh, MatArgs mat, const double* u, int64_t e0, int64_t e1,
+                               double* r_elem, double* r_global, double* eval_out, cudaStream_t st) {
+  auto kern = eval_out ? k_residual_t3<FORM, true> : k_residual_t3<FORM, false>;
+  int nsm = 148, per_sm = 1, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FEB200_T3_THREADS, 0);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t ncg = (e1 - e0 + 9) / 10;                       // 10 cells per warp
+  const int64_t nblk = (ncg + FEB200_T3_THREADS / 32 - 1) / (FEB200_T3_THREADS / 32);
+  int grid = (int)(nblk < (int64_t)nsm * per_sm ? nblk : (int64_t)nsm * per_sm);
+  grid = grid_cap(grid);
+  if (grid <= 0) return cudaSuccess;
+  kern<<<grid, FEB200_T3_THREADS, 0, st>>>(view_of(mh), (const double*)mat.a, (const double*)mat.b, u,
+                                           e0, e1, r_elem, r_global, eval_out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// Scalar forms at p = 2 in fp64; cudaErrorNotSupported otherwise (the smem kernel runs).
+cudaError_t launch_residual_t3(const fe_mesh* mh, int form, MatArgs mat, const double* u, int64_t e0,
+                               int64_t e1, double* r_elem, double* r_global, cudaStream_t st,
+                               double* eval_out) {
+  if (mh->order != 2 || mh->q1d != 3) return cudaErrorNotSupported;
+  switch (form) {
+    case FE_FORM_DIFFUSION: return launch_t3_t<FE_FORM_DIFFUSION>(mh, mat, u, e0, e1, r_elem, r_global, eval_out, st);
+    case FE_FORM_MASS: return launch_t3_t<FE_FORM_MASS>(mh, mat, u, e0, e1, r_elem, r_global, eval_out, st);
+    case FE_FORM_MASS_DIFFUSION:
+      return launch_t3_t<FE_FORM_MASS_DIFFUSION>(mh, mat, u, e0, e1, r_elem, r_global, eval_out, st);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace feb200
