@@ -25,6 +25,20 @@
 
 namespace feb200 {
 
+namespace {
+__device__ __forceinline__ void t3_cp8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src) : "memory");
+}
+__device__ __forceinline__ void t3_cp4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src) : "memory");
+}
+__device__ __forceinline__ void t3_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void t3_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+}  // namespace
+
 cudaError_t upload_const_tables_residual_t3(int order, const double* b1, const double* d1,
                                            const double* x1, const double* w1, cudaStream_t st) {
   return upload_tables_this_tu(order, b1, d1, x1, w1, st);
@@ -59,19 +73,81 @@ __global__ void __launch_bounds__(FEB200_T3_THREADS, FEB200_T3_MINB)
   const int64_t nloc = e1 - e0;
   const int wpb = blockDim.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5), nw = (int64_t)gridDim.x * wpb;
-  for (int64_t cg = gw * 10; cg < nloc; cg += nw * 10) {
-    const int64_t le = cg + cl;
-    const bool valid = lane_ok && le < nloc;
+  constexpr int NCOEF = FORM == FE_FORM_MASS_DIFFUSION ? 2 : 1;
+  // cp.async prefetch rings in shared memory, lane-interleaved ([slot][element][thread]):
+  // S1 (3 slots, two groups ahead): dof ids, conn, material of the lane's cell plane;
+  // S2 (2 slots, one group ahead): u at the dofs, 8 of the cell's 24 vertex coordinates
+  constexpr int TH = FEB200_T3_THREADS;
+  extern __shared__ __align__(16) unsigned char t3s[];
+  double* s1m = reinterpret_cast<double*>(t3s);                 // [3][NCOEF * 9][TH]
+  double* s2u = s1m + 3 * NCOEF * 9 * TH;                       // [2][9][TH]
+  double* s2x = s2u + 2 * 9 * TH;                               // [2][8][TH]
+  int32_t* s1d = reinterpret_cast<int32_t*>(s2x + 2 * 8 * TH);  // [3][9][TH]
+  int32_t* s1c = s1d + 3 * 9 * TH;                              // [3][8][TH]
+  const int tid = threadIdx.x;
+  auto group_cell = [&](int64_t g, int64_t& le, bool& ok) {
+    le = (gw + g * nw) * 10 + cl;
+    ok = lane_ok && le < nloc;
+  };
+  auto issue_s1 = [&](int64_t g) {
+    int64_t le;
+    bool ok;
+    group_cell(g, le, ok);
+    if (ok) {
+      const int sl = (int)(g % 3);
+      const int64_t e = e0 + le;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) t3_cp4(&s1d[(sl * 9 + k) * TH + tid], mv.dof_conn + e * NB + N * N * j + k);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) t3_cp4(&s1c[(sl * 8 + v) * TH + tid], mv.conn + 8 * e + v);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        t3_cp8(&s1m[(sl * NCOEF * 9 + k) * TH + tid], ma + e * NQ + N * N * j + k);
+        if (NCOEF == 2) t3_cp8(&s1m[(sl * NCOEF * 9 + 9 + k) * TH + tid], mb + e * NQ + N * N * j + k);
+      }
+    }
+    t3_commit();
+  };
+  auto issue_s2 = [&](int64_t g) {  // needs S1(g) in shared memory
+    int64_t le;
+    bool ok;
+    group_cell(g, le, ok);
+    if (ok) {
+      const int s1 = (int)(g % 3), s2 = (int)(g & 1);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) t3_cp8(&s2u[(s2 * 9 + k) * TH + tid], u + s1d[(s1 * 9 + k) * TH + tid]);
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {  // coordinate p = 8 j + h of the cell: vertex p / 3, component p % 3
+        const int pidx = 8 * j + h, v = pidx / 3, i = pidx - 3 * v;
+        t3_cp8(&s2x[(s2 * 8 + h) * TH + tid], mv.coords + 3 * (int64_t)s1c[(s1 * 8 + v) * TH + tid] + i);
+      }
+    }
+    t3_commit();
+  };
+  issue_s1(0);
+  issue_s1(1);
+  t3_wait<1>();
+  issue_s2(0);
+  for (int64_t g = 0;; ++g) {
+    int64_t le;
+    bool valid;
+    group_cell(g, le, valid);
+    if ((gw + g * nw) * 10 >= nloc) break;
+    t3_wait<0>();  // S2(g) and S1(g + 1)
+    __syncwarp();
+    issue_s2(g + 1);
+    issue_s1(g + 2);
     const int64_t e = e0 + (valid ? le : 0);
-    // ---- gather u at the nodes (kx, ky, kz = j)
+    const int s1 = (int)(g % 3), s2 = (int)(g & 1);
+    // ---- u at the nodes (kx, ky, kz = j), gathered by cp.async
     int dof[N][N];
     double uv[N][N];
 #pragma unroll
     for (int ky = 0; ky < N; ++ky)
 #pragma unroll
       for (int kx = 0; kx < N; ++kx) {
-        dof[ky][kx] = valid ? mv.dof_conn[e * NB + kx + N * ky + N * N * j] : 0;
-        uv[ky][kx] = valid ? u[dof[ky][kx]] : 0.0;
+        dof[ky][kx] = s1d[(s1 * 9 + kx + N * ky) * TH + tid];
+        uv[ky][kx] = valid ? s2u[(s2 * 9 + kx + N * ky) * TH + tid] : 0.0;
       }
     // ---- x- and y-contractions in registers
     double c00[N][N], c01[N][N], c10[N][N];  // [qy][qx] at kz = j
@@ -134,13 +210,11 @@ __global__ void __launch_bounds__(FEB200_T3_THREADS, FEB200_T3_MINB)
         Gz[qy][qx] = gz;
       }
     // ---- geometry and flux at the 9 qps (qx, qy, qz = j); F = detw J^-1 f1 (reference)
-    double X[8][3];
+    double X[8][3];  // the cell's vertices, fetched by its three lanes (8 values each)
+    const int wb = tid - lane;
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      const int32_t cv = valid ? mv.conn[8 * e + v] : 0;
-#pragma unroll
-      for (int i = 0; i < 3; ++i) X[v][i] = valid ? mv.coords[3 * (int64_t)cv + i] : 0.0;
-    }
+    for (int pidx = 0; pidx < 24; ++pidx)
+      X[pidx / 3][pidx % 3] = valid ? s2x[(s2 * 8 + pidx % 8) * TH + wb + base + pidx / 8] : 0.0;
     double Fv[N][N], Fx[N][N], Fy[N][N], Fz[N][N];
 #pragma unroll
     for (int qy = 0; qy < N; ++qy)
@@ -169,11 +243,11 @@ __global__ void __launch_bounds__(FEB200_T3_THREADS, FEB200_T3_MINB)
         double fv = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
         if (valid) {
           if constexpr (VAL) {
-            const double rho = ma[e * NQ + q];
+            const double rho = s1m[(s1 * NCOEF * 9 + qx + N * qy) * TH + tid];
             fv = wq * det * rho * Uq[qy][qx];
           }
           if constexpr (GRAD) {
-            const double kap = FORM == FE_FORM_MASS_DIFFUSION ? mb[e * NQ + q] : ma[e * NQ + q];
+            const double kap = s1m[(s1 * NCOEF * 9 + (NCOEF - 1) * 9 + qx + N * qy) * TH + tid];
             // grad u = J^-T grad_ref u: t_r = sum_m C[r][m] g_m (= det * (grad u)_r);
             // F_m = detw kappa sum_r J^-1[m][r] (grad u)_r = (w kappa / det) sum_r C[r][m] t_r
             const double g0 = Gx[qy][qx], g1 = Gy[qy][qx], g2 = Gz[qy][qx];
@@ -266,6 +340,7 @@ __global__ void __launch_bounds__(FEB200_T3_THREADS, FEB200_T3_MINB)
       if (lane == 0 && ev != 0.0) atomicAdd(eval_out, ev);
     }
   }
+  t3_wait<0>();
 #undef B0
 #undef B1
 }
@@ -274,18 +349,22 @@ template <int FORM>
 static cudaError_t launch_t3_t(const fe_mesh* mh, MatArgs mat, const double* u, int64_t e0, int64_t e1,
                                double* r_elem, double* r_global, double* eval_out, cudaStream_t st) {
   auto kern = eval_out ? k_residual_t3<FORM, true> : k_residual_t3<FORM, false>;
+  constexpr int NCOEF = FORM == FE_FORM_MASS_DIFFUSION ? 2 : 1;
+  const size_t smem = (size_t)FEB200_T3_THREADS * (8 * (3 * NCOEF * 9 + 2 * 9 + 2 * 8) + 4 * (3 * 9 + 3 * 8));
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
   int nsm = 148, per_sm = 1, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FEB200_T3_THREADS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FEB200_T3_THREADS, smem);
   if (per_sm < 1) per_sm = 1;
   const int64_t ncg = (e1 - e0 + 9) / 10;                       // 10 cells per warp
   const int64_t nblk = (ncg + FEB200_T3_THREADS / 32 - 1) / (FEB200_T3_THREADS / 32);
   int grid = (int)(nblk < (int64_t)nsm * per_sm ? nblk : (int64_t)nsm * per_sm);
   grid = grid_cap(grid);
   if (grid <= 0) return cudaSuccess;
-  kern<<<grid, FEB200_T3_THREADS, 0, st>>>(view_of(mh), (const double*)mat.a, (const double*)mat.b, u,
-                                           e0, e1, r_elem, r_global, eval_out);
+  kern<<<grid, FEB200_T3_THREADS, smem, st>>>(view_of(mh), (const double*)mat.a, (const double*)mat.b, u,
+                                              e0, e1, r_elem, r_global, eval_out);
   count_launch();
   return cudaGetLastError();
 }
