@@ -17,10 +17,10 @@
 #include "fe_internal.h"
 
 #ifndef FEB200_T3_THREADS
-#define FEB200_T3_THREADS 128
+#define FEB200_T3_THREADS 64
 #endif
 #ifndef FEB200_T3_MINB
-#define FEB200_T3_MINB 2
+#define FEB200_T3_MINB 4
 #endif
 
 namespace feb200 {
