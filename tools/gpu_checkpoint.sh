@@ -11,5 +11,5 @@ CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
 $CMD > gpurun_out/plain_ck.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_ck.csv $CMD > gpurun_out/ncu_ck_launch.log 2>&1; echo ncu1=$?
 ncu --set full --clock-control none --import-source on -k regex:k_matrix_sfp -s 1 -c 1 -o gpurun_out/prof_ck_matrix $CMD > gpurun_out/ncu_ck_full.log 2>&1; echo ncu2=$?
-ncu --set full --clock-control none --import-source on -k regex:k_residual_sf -s 1 -c 1 -o gpurun_out/prof_ck_residual $CMD > gpurun_out/ncu_ck_full_r.log 2>&1; echo ncu3=$?
+ncu --set full --clock-control none --import-source on -k regex:k_residual_t3 -s 1 -c 1 -o gpurun_out/prof_ck_residual $CMD > gpurun_out/ncu_ck_full_r.log 2>&1; echo ncu3=$?
 ncu --set full --clock-control none --import-source on -k regex:k_matrix_vp -s 1 -c 1 -o gpurun_out/prof_ck_c3_matrix python bench.py --config C3 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_ck_c3.log 2>&1; echo ncu4=$?
