@@ -384,3 +384,38 @@ def test_matrix_residual_unsupported():
     with pytest.raises(m.FEError) as ei:
         mesh.matrix_residual(fi.ELASTICITY, dev(pr.u), pr.mat_kind, dev(pr.mat_a), dev(pr.mat_b))
     assert ei.value.status == m.FE_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("form,p", [(0, 1), (0, 2), (1, 2), (3, 2), (4, 2), (5, 2), (2, 2), (3, 4)])
+def test_single_cell(form, p):
+    """One cell: every persistent pipeline runs a single, ragged batch (TMA store fallback for
+    the odd byte count) and the residual kernels a single partial group."""
+    pr = fi.make_problem(form, p, (1, 1, 1), 11000 + 10 * form + p)
+    mesh = gpu_mesh(pr)
+    mat = (pr.mat_kind, dev(pr.mat_a), dev(pr.mat_b))
+    if p <= 2:
+        K = mesh.element_matrices(form, *mat, dev(pr.u) if form == fi.CONVECTIVE else None)
+        assert rel(K.cpu().numpy(), oracle.problem_matrix(pr)) <= TOL64
+    r_elem, r_glob = mesh.residual(form, dev(pr.u), *mat, want_elem=True)
+    r_ref = oracle.problem_residual(pr)
+    assert rel(r_elem.cpu().numpy(), r_ref) <= TOL64
+    assert rel(r_glob.cpu().numpy().ravel(), oracle.assemble(r_ref, pr.dof_conn, pr.n_nodes, pr.ncomp)) <= TOL64
+
+
+@pytest.mark.parametrize("form,p", [(0, 2), (3, 2), (4, 2), (5, 2)])
+def test_unaligned_outputs(form, p):
+    """K and r_elem written through views that start one cell in (8-byte, not 16-byte aligned
+    for odd element counts): the bulk-store paths must fall back, results unchanged."""
+    pr = fi.make_problem(form, p, (3, 3, 3), 12000 + form)
+    mesh = gpu_mesh(pr)
+    mat = (pr.mat_kind, dev(pr.mat_a), dev(pr.mat_b))
+    nd = pr.ncomp * pr.nb
+    big = torch.full((pr.n_elems + 1, nd, nd), float("nan"), dtype=torch.float64, device="cuda")
+    Kv = big[1:]
+    mesh.element_matrices(form, *mat, dev(pr.u) if form == fi.CONVECTIVE else None, out=Kv)
+    assert rel(Kv.cpu().numpy(), oracle.problem_matrix(pr)) <= TOL64
+    assert torch.isnan(big[0]).all()          # nothing written before the view
+    rbig = torch.full((pr.n_elems * nd + 1,), float("nan"), dtype=torch.float64, device="cuda")
+    rv = rbig[1:].view(pr.n_elems, nd)
+    mesh.residual(form, dev(pr.u), *mat, r_elem=rv, want_elem=True)
+    assert rel(rv.cpu().numpy(), oracle.problem_residual(pr)) <= TOL64
