@@ -278,9 +278,21 @@ def cpu_baseline(prob, modes, budget_s=12.0):
     while t < budget_s and passes < 50:
         t += oracle_step(prob, n, modes)
         passes += 1
-    return {"value": n * passes / t, "unit": "cells/s", "cores": cpu_cores(), "kind": "oracle",
-            "sample": f"{passes} pass(es) over the first {n} of {prob.name}'s {prob.n_elems} cells, "
-                      f"modes {'+'.join(modes)}, plain C oracle (-O2, OpenMP over cells), {t:.1f} s"}
+    out = {"value": n * passes / t, "unit": "cells/s", "cores": cpu_cores(), "kind": "oracle",
+           "sample": f"{passes} pass(es) over the first {n} of {prob.name}'s {prob.n_elems} cells, "
+                     f"modes {'+'.join(modes)}, plain C oracle (-O2, OpenMP over cells), {t:.1f} s"}
+    # the same oracle on one core, on a smaller prefix
+    import oracle
+    nthr = oracle.set_threads(1)
+    try:
+        n1 = max(1, n // max(1, cpu_cores()))
+        t1 = oracle_step(prob, n1, modes)
+        out["value_1core"] = n1 / t1
+        out["sample_1core"] = f"first {n1} cells, 1 thread, {t1:.1f} s"
+    finally:
+        oracle.set_threads(cpu_cores())
+    del nthr
+    return out
 
 
 def run_reference(args, cfg):

@@ -80,6 +80,13 @@ def _i32(a):
     return None if a is None else np.ascontiguousarray(a, dtype=np.int32)
 
 
+def set_threads(n: int) -> int:
+    """OpenMP threads of the oracle's cell loops (timing only); returns the active count."""
+    f = lib().oracle_set_threads
+    f.restype = ctypes.c_int
+    return int(f(int(n)))
+
+
 def _check(st):
     if st != OK:
         raise OracleError(st, int(lib().oracle_bad_element()))

@@ -44,6 +44,9 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 #define OR_OK 0
 #define OR_ERR_ARG (-1)
@@ -608,4 +611,15 @@ int oracle_eval_scalar(int form, int p, int q1d, int64_t n_elems, const double *
   free(xi); free(w); free(Phi); free(dPhi);
   if (status == OR_OK) *value = total;
   return status;
+}
+
+/* Thread count of the cell-parallel loops (timing only; results do not depend on it). */
+int oracle_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
+#else
+  (void)n;
+  return 1;
+#endif
 }
