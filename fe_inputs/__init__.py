@@ -37,11 +37,14 @@ VECTOR_MASS = 2
 MASS_DIFFUSION = 3
 ELASTICITY = 4
 CONVECTIVE = 5
+WEIGHTED_DOT = 6    # Tab. 2 'ij,i,j': M per qp [E][n_q][3][3]
+DIVERGENCE = 7      # Tab. 2 'i.i': linear form, no material
 FORM_NAMES = {DIFFUSION: "diffusion", MASS: "mass", VECTOR_MASS: "vector_mass",
               MASS_DIFFUSION: "mass_diffusion", ELASTICITY: "elasticity",
-              CONVECTIVE: "convective"}
+              CONVECTIVE: "convective", WEIGHTED_DOT: "weighted_dot",
+              DIVERGENCE: "divergence"}
 FORM_NCOMP = {DIFFUSION: 1, MASS: 1, VECTOR_MASS: 3, MASS_DIFFUSION: 1,
-              ELASTICITY: 3, CONVECTIVE: 3}
+              ELASTICITY: 3, CONVECTIVE: 3, WEIGHTED_DOT: 3, DIVERGENCE: 3}
 
 # material kinds (include/feb200.h fe_material_kind)
 MAT_PER_QP = 0
@@ -170,7 +173,10 @@ def make_problem(form: int, p: int, shape, seed: int, *, q1d: Optional[int] = No
             Araw = rng.uniform(-1.0, 1.0, size=(E, nq, 6, 6))
             mat_a = np.einsum("eqik,eqjk->eqij", Araw, Araw) + 6.0 * np.eye(6)
             mat_b = None
-    else:  # CONVECTIVE: no material
+    elif form == WEIGHTED_DOT:  # a general (non-symmetric) 3 x 3 weight per qp, U[-1, 1] + 2 I
+        mk = MAT_PER_QP
+        mat_a = rng.uniform(-1.0, 1.0, size=(E, nq, 3, 3)) + 2.0 * np.eye(3)
+    else:  # CONVECTIVE, DIVERGENCE: no material
         mk = MAT_PER_QP
         mat_a = None
     # draw 3: DOF / state vector

@@ -54,6 +54,8 @@ def lib():
         _lib.oracle_isotropic_D.argtypes = [ctypes.c_double, ctypes.c_double, P]
         _lib.oracle_eval_scalar.argtypes = [ci, ci, ci, i64, P, P, P, ci, P, P, P, i64, i64, P]
         _lib.oracle_eval_scalar.restype = ci
+        _lib.oracle_eval_stress.argtypes = [ci, ci, i64, P, P, P, ci, P, P, P, i64, i64, P]
+        _lib.oracle_eval_stress.restype = ci
         _lib.oracle_bad_element.restype = i64
         for f in ("oracle_gauss_legendre", "oracle_lagrange_1d", "oracle_tables", "oracle_geometry",
                   "oracle_eval_matrix", "oracle_eval_residual", "oracle_assemble"):
@@ -133,7 +135,7 @@ def geometry(q1d: int, coords, conn):
 
 
 def _ncomp(form):
-    return 3 if form in (2, 4, 5) else 1
+    return 3 if form in (2, 4, 5, 6, 7) else 1
 
 
 def eval_matrix(form, p, q1d, coords, conn, dof_conn=None, mat_kind=0, mat_a=None, mat_b=None,
@@ -176,6 +178,25 @@ def eval_scalar(form, p, q1d, coords, conn, dof_conn, u, mat_kind=0, mat_a=None,
                                     mat_kind, _ptr(mat_a), _ptr(mat_b), _ptr(u), elem_begin,
                                     elem_end, _ptr(out)))
     return float(out[0])
+
+
+def eval_stress(p, q1d, coords, conn, dof_conn, u, mat_kind=1, mat_a=None, mat_b=None,
+                elem_begin=0, elem_end=None):
+    """Cauchy stress sigma = D e(u) (Tab. 2) at every qp: [E'][nq][6] (Voigt)."""
+    coords, conn, dof_conn = _f64(coords), _i32(conn), _i32(dof_conn)
+    mat_a, mat_b, u = _f64(mat_a), _f64(mat_b), _f64(u)
+    E = conn.shape[0]
+    elem_end = E if elem_end is None else elem_end
+    sig = np.zeros((max(elem_end - elem_begin, 0), q1d ** 3, 6))
+    _check(lib().oracle_eval_stress(p, q1d, E, _ptr(coords), _ptr(conn), _ptr(dof_conn), mat_kind,
+                                    _ptr(mat_a), _ptr(mat_b), _ptr(u), elem_begin, elem_end,
+                                    _ptr(sig)))
+    return sig
+
+
+def problem_stress(prob):
+    return eval_stress(prob.p, prob.q1d, prob.coords, prob.conn, prob.dof_conn, prob.u,
+                       prob.mat_kind, prob.mat_a, prob.mat_b)
 
 
 def problem_eval_scalar(prob):

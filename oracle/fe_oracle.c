@@ -58,8 +58,11 @@ enum {
   OR_VECTOR_MASS = 2,
   OR_MASS_DIFFUSION = 3,
   OR_ELASTICITY = 4,
-  OR_CONVECTIVE = 5
+  OR_CONVECTIVE = 5,
+  OR_WEIGHTED_DOT = 6, /* Tab. 2 'ij,i,j': int v_i M_ij u_j, M per qp [E][nq][3][3] */
+  OR_DIVERGENCE = 7    /* Tab. 2 'i.i': int dv_i/dx_i (linear form, no trial) */
 };
+#define OR_LAST_FORM OR_DIVERGENCE
 
 /* material kinds for the elasticity form */
 enum { OR_MAT_PER_QP = 0, OR_MAT_PER_ELEM = 1, OR_MAT_FULL_D = 2 };
@@ -261,7 +264,8 @@ void oracle_isotropic_D(double lam, double mu, double *D) {
 }
 
 static int form_ncomp(int form) {
-  return (form == OR_VECTOR_MASS || form == OR_ELASTICITY || form == OR_CONVECTIVE) ? 3 : 1;
+  return (form == OR_VECTOR_MASS || form == OR_ELASTICITY || form == OR_CONVECTIVE ||
+          form == OR_WEIGHTED_DOT || form == OR_DIVERGENCE) ? 3 : 1;
 }
 
 /* Elastic matrix at (e, q) from the material description. */
@@ -292,8 +296,9 @@ int oracle_eval_matrix(int form, int p, int q1d, int64_t n_elems, const double *
                        const double *mat_a, const double *mat_b, const double *u_state,
                        double *K) {
   if (p < 1 || p > 8 || q1d < 1 || q1d > 16 || n_elems < 0) return OR_ERR_ARG;
-  if (form < 0 || form > OR_CONVECTIVE) return OR_ERR_ARG;
+  if (form < 0 || form > OR_WEIGHTED_DOT) return OR_ERR_ARG; /* divergence: no trial variable */
   if (form == OR_CONVECTIVE && !u_state) return OR_ERR_ARG;
+  if (form == OR_WEIGHTED_DOT && !mat_a) return OR_ERR_ARG;
   const int n1 = p + 1, nb = n1 * n1 * n1, nq = q1d * q1d * q1d;
   const int D = form_ncomp(form), ndof = D * nb;
   if (!dof_conn) {
@@ -374,6 +379,14 @@ int oracle_eval_matrix(int form, int p, int q1d, int64_t n_elems, const double *
               for (int Kk = 0; Kk < 6; ++Kk) f += Bv[I * ndof + a] * Dm[6 * I + Kk] * Bv[Kk * ndof + b];
             Ke[(int64_t)a * ndof + b] += detw * f;
           }
+      } else if (form == OR_WEIGHTED_DOT) {
+        /* 'ij,i,j': K[(a,k),(b,l)] += detw M_ab phi_k phi_l */
+        const double *M = mat_a + (e * nq + q) * 9;
+        for (int a = 0; a < 3; ++a)
+          for (int k = 0; k < nb; ++k)
+            for (int b = 0; b < 3; ++b)
+              for (int l = 0; l < nb; ++l)
+                Ke[(int64_t)(a * nb + k) * ndof + b * nb + l] += detw * M[3 * a + b] * phi[k] * phi[l];
       } else { /* OR_CONVECTIVE, Eq. fe4 */
         /* state at the qp: u_j(q) = sum_m u^m_j phi_m,  du_i/dx_j = sum_l u^l_i G[j][l] */
         double uq[3] = {0, 0, 0}, gu[3][3] = {{0}};
@@ -415,7 +428,8 @@ int oracle_eval_residual(int form, int p, int q1d, int64_t n_elems, const double
                          const double *mat_a, const double *mat_b, const double *u,
                          int64_t elem_begin, int64_t elem_end, double *r_elem) {
   if (p < 1 || p > 8 || q1d < 1 || q1d > 16 || n_elems < 0) return OR_ERR_ARG;
-  if (form < 0 || form > OR_CONVECTIVE || !u) return OR_ERR_ARG;
+  if (form < 0 || form > OR_LAST_FORM || !u) return OR_ERR_ARG;
+  if (form == OR_WEIGHTED_DOT && !mat_a) return OR_ERR_ARG;
   if (elem_begin < 0 || elem_end > n_elems || elem_begin > elem_end) return OR_ERR_ARG;
   const int n1 = p + 1, nb = n1 * n1 * n1, nq = q1d * q1d * q1d;
   const int D = form_ncomp(form), ndof = D * nb;
@@ -503,6 +517,18 @@ int oracle_eval_residual(int form, int p, int q1d, int64_t n_elems, const double
             }
             re[r * nb + k] += detw * f;
           }
+      } else if (form == OR_WEIGHTED_DOT) {
+        /* int v_a M_ab u_b: tested against v = phi_k e_a */
+        const double *M = mat_a + (e * nq + q) * 9;
+        for (int a = 0; a < 3; ++a) {
+          double f0 = 0.0;
+          for (int b = 0; b < 3; ++b) f0 += M[3 * a + b] * uq[b];
+          for (int k = 0; k < nb; ++k) re[a * nb + k] += detw * phi[k] * f0;
+        }
+      } else if (form == OR_DIVERGENCE) {
+        /* int dv_a/dx_a with v = phi_k e_a: r[(a,k)] = int dphi_k/dx_a (u is not used) */
+        for (int a = 0; a < 3; ++a)
+          for (int k = 0; k < nb; ++k) re[a * nb + k] += detw * G[a * nb + k];
       } else { /* OR_CONVECTIVE: c(v,u,u) = int v_i du_i/dx_j u_j (Eq. fe2) */
         for (int a = 0; a < 3; ++a) {
           double f0 = 0.0;
@@ -547,7 +573,8 @@ int oracle_eval_scalar(int form, int p, int q1d, int64_t n_elems, const double *
                        const double *mat_a, const double *mat_b, const double *u,
                        int64_t elem_begin, int64_t elem_end, double *value) {
   if (p < 1 || p > 8 || q1d < 1 || q1d > 16 || n_elems < 0) return OR_ERR_ARG;
-  if (form < 0 || form > OR_CONVECTIVE || !u || !value) return OR_ERR_ARG;
+  if (form < 0 || form > OR_LAST_FORM || !u || !value) return OR_ERR_ARG;
+  if (form == OR_WEIGHTED_DOT && !mat_a) return OR_ERR_ARG;
   if (elem_begin < 0 || elem_end > n_elems || elem_begin > elem_end) return OR_ERR_ARG;
   const int n1 = p + 1, nb = n1 * n1 * n1, nq = q1d * q1d * q1d;
   const int D = form_ncomp(form);
@@ -601,6 +628,12 @@ int oracle_eval_scalar(int form, int p, int q1d, int64_t n_elems, const double *
         }
         for (int I = 0; I < 6; ++I)
           for (int K = 0; K < 6; ++K) f += eps[I] * Dm[6 * I + K] * eps[K];
+      } else if (form == OR_WEIGHTED_DOT) {
+        const double *M = mat_a + (e * nq + q) * 9;
+        for (int a = 0; a < 3; ++a)
+          for (int b = 0; b < 3; ++b) f += uq[a] * M[3 * a + b] * uq[b];
+      } else if (form == OR_DIVERGENCE) {
+        f = gu[0][0] + gu[1][1] + gu[2][2]; /* int div u */
       } else {
         for (int i = 0; i < 3; ++i)
           for (int j = 0; j < 3; ++j) f += uq[i] * gu[i][j] * uq[j];
@@ -622,4 +655,56 @@ int oracle_set_threads(int n) {
   (void)n;
   return 1;
 #endif
+}
+
+/* Cauchy stress (Tab. 2 'IK,s(k:l)->K'): sigma = D e(u) at every quadrature
+ * point of cells [elem_begin, elem_end), Voigt order (xx, yy, zz, xy, xz, yz), engineering
+ * shear strains (reading 7); "evaluated only" (no test variable):
+ *   sigma[e - elem_begin][q][6]. */
+int oracle_eval_stress(int p, int q1d, int64_t n_elems, const double *coords, const int32_t *conn,
+                       const int32_t *dof_conn, int mat_kind, const double *mat_a,
+                       const double *mat_b, const double *u, int64_t elem_begin, int64_t elem_end,
+                       double *sigma) {
+  if (p < 1 || p > 8 || q1d < 1 || q1d > 16 || n_elems < 0 || !u || !sigma) return OR_ERR_ARG;
+  if (elem_begin < 0 || elem_end > n_elems || elem_begin > elem_end) return OR_ERR_ARG;
+  const int n1 = p + 1, nb = n1 * n1 * n1, nq = q1d * q1d * q1d;
+  if (!dof_conn) {
+    if (p != 1) return OR_ERR_ARG;
+    dof_conn = conn;
+  }
+  double *xi = malloc(sizeof(double) * 3 * nq), *w = malloc(sizeof(double) * nq);
+  double *Phi = malloc(sizeof(double) * nq * nb), *dPhi = malloc(sizeof(double) * nq * 3 * nb);
+  oracle_tables(p, q1d, xi, w, Phi, dPhi);
+  double Psg[3][3][6];
+  build_psg(Psg);
+  int status = OR_OK;
+  for (int64_t e = elem_begin; e < elem_end && status == OR_OK; ++e) {
+    for (int q = 0; q < nq; ++q) {
+      double J[3][3], Ji[3][3];
+      double det = cell_jacobian(coords, conn + 8 * e, xi + 3 * q, J, Ji);
+      if (!(det > 0.0)) { status = OR_ERR_DEGENERATE; g_bad_elem = e; break; }
+      double gu[3][3] = {{0}};
+      for (int k = 0; k < nb; ++k)
+        for (int j = 0; j < 3; ++j) {
+          double g = 0.0;
+          for (int m = 0; m < 3; ++m) g += dPhi[((int64_t)q * 3 + m) * nb + k] * Ji[m][j];
+          for (int a = 0; a < 3; ++a) gu[a][j] += u[(int64_t)dof_conn[e * nb + k] * 3 + a] * g;
+        }
+      double Dm[36], eps[6];
+      material_D(mat_kind, mat_a, mat_b, e, q, nq, Dm);
+      for (int I = 0; I < 6; ++I) {
+        eps[I] = 0.0;
+        for (int r = 0; r < 3; ++r)
+          for (int l = 0; l < 3; ++l) eps[I] += Psg[r][l][I] * gu[r][l];
+      }
+      double *out = sigma + ((e - elem_begin) * nq + q) * 6;
+      for (int I = 0; I < 6; ++I) {
+        double sI = 0.0;
+        for (int K = 0; K < 6; ++K) sI += Dm[6 * I + K] * eps[K];
+        out[I] = sI;
+      }
+    }
+  }
+  free(xi); free(w); free(Phi); free(dPhi);
+  return status;
 }

@@ -578,3 +578,92 @@ def test_eval_mode_equals_u_dot_r(form, p):
     ue = pr.u[pr.dof_conn].transpose(0, 2, 1).reshape(pr.n_elems, -1)
     ref = float(np.sum(r * ue))
     assert abs(v - ref) <= 1e-13 * max(abs(ref), 1e-300)
+
+
+# ---------------------------------------------------------------- N3: remaining Tab. 2 forms
+@pytest.mark.parametrize("p", [1, 2])
+def test_N3_weighted_dot_closed_form(p):
+    """'ij,i,j' with a constant M on an axis-aligned box: K_ab = M_ab * (scalar mass
+    matrix), whose entries are the exact rationals rho h^3 M1 x M1 x M1 (P2)."""
+    dims = (Fraction(1, 2), Fraction(1, 3), Fraction(2, 5))
+    _, Me = exact_box_matrices(p, *dims)
+    Ms = _to_np(Me)
+    c, conn = box(*[float(d) for d in dims], origin=(0.1, 0.2, -0.3))
+    dc, _ = fi.lattice_dof_conn(1, 1, 1, p)
+    nq, nb = (p + 1) ** 3, (p + 1) ** 3
+    Mw = np.array([[1.5, -0.25, 0.5], [0.75, 2.0, -1.0], [0.125, 0.5, 1.25]])
+    K = oracle.eval_matrix(fi.WEIGHTED_DOT, p, p + 1, c, conn, dc, 0,
+                           np.broadcast_to(Mw, (1, nq, 3, 3)).copy())[0]
+    for a in range(3):
+        for b in range(3):
+            assert rel(K[a * nb:(a + 1) * nb, b * nb:(b + 1) * nb], Mw[a, b] * Ms) < 1e-14
+
+
+def test_N3_weighted_dot_reduces_to_vector_mass():
+    """M = rho I per qp gives the vector mass form 'i,i' exactly."""
+    pr = fi.make_problem(fi.VECTOR_MASS, 2, (2, 2, 1), 21)
+    Mw = pr.mat_a[:, :, None, None] * np.eye(3)[None, None]
+    K1 = oracle.problem_matrix(pr)
+    K2 = oracle.eval_matrix(fi.WEIGHTED_DOT, 2, 3, pr.coords, pr.conn, pr.dof_conn, 0,
+                            np.ascontiguousarray(Mw))
+    assert rel(K2, K1) < 1e-15
+    r1 = oracle.problem_residual(pr)
+    r2 = oracle.eval_residual(fi.WEIGHTED_DOT, 2, 3, pr.coords, pr.conn, pr.dof_conn, pr.u, 0,
+                              np.ascontiguousarray(Mw))
+    assert rel(r2, r1) < 1e-15
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_N3_weighted_dot_linear_consistency(p):
+    """r_e = K_e u_e (P8) and eval = u . r (eval mode) for a non-symmetric M per qp."""
+    pr = fi.make_problem(fi.WEIGHTED_DOT, p, (2, 3, 2), 23)
+    K = oracle.problem_matrix(pr)
+    r = oracle.problem_residual(pr)
+    ue = np.stack([pr.u[pr.dof_conn][:, :, a] for a in range(3)], axis=1).reshape(pr.n_elems, -1)
+    assert rel(np.einsum("eij,ej->ei", K, ue), r) < 1e-14
+    assert abs(oracle.problem_eval_scalar(pr) - float((ue * r).sum())) < 1e-13 * abs((ue * r).sum())
+    # non-symmetric weight -> K_ab != K_ba^T in general, but K^T is the form with M^T
+    Mt = np.ascontiguousarray(np.swapaxes(pr.mat_a, 2, 3))
+    Kt = oracle.eval_matrix(fi.WEIGHTED_DOT, p, p + 1, pr.coords, pr.conn, pr.dof_conn, 0, Mt)
+    assert rel(Kt, np.swapaxes(K, 1, 2)) < 1e-15
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_N3_divergence(p):
+    """'i.i': r[(a,k)] = int dphi_k/dx_a.  Partition of unity: sum_k r = 0 per cell
+    and component; eval with u = x (node coordinates, exact in Q_p on trilinear cells) gives
+    int div x = 3 * volume = 3 on the unit cube."""
+    pr = fi.make_problem(fi.DIVERGENCE, p, (2, 2, 3), 31)
+    r = oracle.problem_residual(pr).reshape(pr.n_elems, 3, -1)
+    assert np.abs(r.sum(axis=2)).max() < 1e-14
+    X = node_coords(pr)
+    v = oracle.eval_scalar(fi.DIVERGENCE, p, p + 1, pr.coords, pr.conn, pr.dof_conn, X)
+    assert abs(v - 3.0) < 1e-13
+    # residual mode does not depend on u
+    r2 = oracle.eval_residual(fi.DIVERGENCE, p, p + 1, pr.coords, pr.conn, pr.dof_conn,
+                              np.zeros_like(pr.u)).reshape(pr.n_elems, 3, -1)
+    assert np.array_equal(r, r2)
+    with pytest.raises(oracle.OracleError):  # no trial variable: no matrix mode
+        oracle.eval_matrix(fi.DIVERGENCE, p, p + 1, pr.coords, pr.conn, pr.dof_conn)
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_N3_cauchy_stress(p):
+    """'IK,s(k:l)->K', eval only: an affine displacement u = A x + b is exact in
+    Q_p on trilinear cells, so sigma = D eps(A) at every qp; a rigid motion gives sigma = 0."""
+    pr = fi.make_problem(fi.ELASTICITY, p, (2, 2, 2), 41)
+    X = node_coords(pr)
+    A = np.array([[0.3, -0.2, 0.1], [0.05, -0.4, 0.25], [0.2, 0.15, 0.6]])
+    u = X @ A.T + np.array([0.1, -0.3, 0.2])
+    sig = oracle.eval_stress(p, p + 1, pr.coords, pr.conn, pr.dof_conn, u, pr.mat_kind,
+                             pr.mat_a, pr.mat_b)
+    eps = np.array([A[0, 0], A[1, 1], A[2, 2], A[0, 1] + A[1, 0], A[0, 2] + A[2, 0],
+                    A[1, 2] + A[2, 1]])
+    for e in range(pr.n_elems):
+        ref = oracle.isotropic_D(pr.mat_a[e], pr.mat_b[e]) @ eps
+        assert np.abs(sig[e] - ref[None, :]).max() < 1e-13 * np.abs(ref).max()
+    W = np.array([[0.0, -0.3, 0.2], [0.3, 0.0, -0.1], [-0.2, 0.1, 0.0]])  # skew: rotation
+    sig0 = oracle.eval_stress(p, p + 1, pr.coords, pr.conn, pr.dof_conn, X @ W.T + 1.0,
+                              pr.mat_kind, pr.mat_a, pr.mat_b)
+    scale = max(np.abs(oracle.isotropic_D(a, b)).max() for a, b in zip(pr.mat_a, pr.mat_b))
+    assert np.abs(sig0).max() < 1e-13 * scale * np.abs(W).max()  # zero up to rounding
