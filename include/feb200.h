@@ -70,7 +70,12 @@ typedef enum {
   FE_FORM_VECTOR_MASS = 2,    /* int rho v_i u_i, D = 3 (vector dot product 'i,i'; Eq. fe3c) */
   FE_FORM_MASS_DIFFUSION = 3, /* int rho v u + kappa grad v . grad u, scalar (BASELINE config 4) */
   FE_FORM_ELASTICITY = 4,     /* int e(v)^T D e(u), D = 3, Voigt via Psg */
-  FE_FORM_CONVECTIVE = 5      /* int v_i (du_i/dx_j) u_j, D = 3 (Eq. fe2); matrix = Eq. fe4 */
+  FE_FORM_CONVECTIVE = 5,     /* int v_i (du_i/dx_j) u_j, D = 3 (Eq. fe2); matrix = Eq. fe4 */
+  FE_FORM_WEIGHTED_DOT = 6,   /* int v_i M_ij u_j, D = 3 ('ij,i,j'); M per qp: material a =
+                               * M[E][n_q][3][3] row-major, kind FE_MAT_PER_QP; matrix orders 1-2 */
+  FE_FORM_DIVERGENCE = 7      /* int dv_i/dx_i, D = 3 ('i.i'): a linear form -- residual mode
+                               * (u is read but does not enter) and eval mode (int div u);
+                               * no trial variable, so no matrix mode; no material (mat may be NULL) */
 } fe_form;
 
 typedef enum { FE_F64 = 0, FE_F32 = 1 } fe_dtype;
@@ -173,6 +178,18 @@ fe_status fe_eval_matrix_residual(const fe_mesh *mesh, int32_t form, int32_t dty
 fe_status fe_eval_scalar(const fe_mesh *mesh, int32_t form, int32_t dtype, const fe_material *mat,
                          const void *u, int64_t elem_begin, int64_t elem_end, double *value,
                          void *stream);
+
+/* Cauchy stress at the quadrature points (Tab. 2 'IK,s(k:l)->K'), an
+ * "evaluated only" form (no test variable):
+ *   sigma[e - elem_begin][q][I] = sum_K D_IK(e, q) eps_K(u)(q),  I, K in Voigt order
+ *   (xx, yy, zz, xy, xz, yz), eps with engineering shears (du0/dx1 + du1/dx0, ...).
+ * u: device double [n_nodes][3] (interleaved components, as in residual mode);
+ * mat: the elasticity material (FE_MAT_PER_QP / FE_MAT_PER_ELEM lambda, mu, or
+ * FE_MAT_FULL_D); sigma: device double [elem_end - elem_begin][n_q][6], caller
+ * owned, overwritten.  FE_F64 only; orders 1..4 (the mesh's q1d = order + 1).
+ * Deterministic (no atomics). */
+fe_status fe_eval_stress(const fe_mesh *mesh, const fe_material *mat, const double *u,
+                         int64_t elem_begin, int64_t elem_end, double *sigma, void *stream);
 
 /* Scatter-add of cell residuals (standalone assembly):
  *   r_global[dof_conn[e][k] * ncomp + a] += r_elem[e - elem_begin][a * n_b + k]

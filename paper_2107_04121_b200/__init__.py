@@ -22,10 +22,11 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FEB200_LIB_PATH", os.path.join(_HERE, "libfeb200.so"))
 
 FE_OK, FE_ERR_INVALID_ARG, FE_ERR_UNSUPPORTED, FE_ERR_DEGENERATE, FE_ERR_CUDA, FE_ERR_OOM = range(6)
-DIFFUSION, MASS, VECTOR_MASS, MASS_DIFFUSION, ELASTICITY, CONVECTIVE = range(6)
+DIFFUSION, MASS, VECTOR_MASS, MASS_DIFFUSION, ELASTICITY, CONVECTIVE, WEIGHTED_DOT, DIVERGENCE = range(8)
 F64, F32 = 0, 1
 MAT_PER_QP, MAT_PER_ELEM, MAT_FULL_D = 0, 1, 2
-NCOMP = {DIFFUSION: 1, MASS: 1, VECTOR_MASS: 3, MASS_DIFFUSION: 1, ELASTICITY: 3, CONVECTIVE: 3}
+NCOMP = {DIFFUSION: 1, MASS: 1, VECTOR_MASS: 3, MASS_DIFFUSION: 1, ELASTICITY: 3, CONVECTIVE: 3,
+         WEIGHTED_DOT: 3, DIVERGENCE: 3}
 _STATUS = {1: "FE_ERR_INVALID_ARG", 2: "FE_ERR_UNSUPPORTED", 3: "FE_ERR_DEGENERATE",
            4: "FE_ERR_CUDA", 5: "FE_ERR_OOM"}
 
@@ -66,6 +67,7 @@ def _load():
     lib.fe_eval_scalar.argtypes = [P, i32, i32, ctypes.POINTER(fe_material), P, i64, i64, P, P]
     lib.fe_eval_matrix_residual.argtypes = [P, i32, i32, ctypes.POINTER(fe_material), P, i64,
                                             i64, P, P, P, P]
+    lib.fe_eval_stress.argtypes = [P, ctypes.POINTER(fe_material), P, i64, i64, P, P]
     lib.fe_create_csr.argtypes = [P, i32, P, ctypes.POINTER(P)]
     lib.fe_csr_info.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     lib.fe_csr_arrays.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P)]
@@ -78,7 +80,7 @@ def _load():
     lib.fe_launch_count.restype = i64
     for f in ("fe_create_mesh_geometry", "fe_destroy_mesh", "fe_mesh_info",
               "fe_eval_element_matrices", "fe_eval_residual", "fe_assemble_vector",
-              "fe_geometry", "fe_eval_scalar", "fe_eval_matrix_residual", "fe_create_csr", "fe_csr_info", "fe_csr_arrays",
+              "fe_geometry", "fe_eval_scalar", "fe_eval_matrix_residual", "fe_eval_stress", "fe_create_csr", "fe_csr_info", "fe_csr_arrays",
               "fe_csr_copy_arrays",
               "fe_assemble_matrix", "fe_destroy_csr"):
         getattr(lib, f).restype = ctypes.c_int
@@ -101,7 +103,7 @@ class _LazyLib:
 _lib = _LazyLib()
 ABI_SYMBOLS = ("fe_create_mesh_geometry", "fe_destroy_mesh", "fe_mesh_info",
                "fe_eval_element_matrices", "fe_eval_residual", "fe_assemble_vector", "fe_eval_scalar",
-               "fe_eval_matrix_residual",
+               "fe_eval_matrix_residual", "fe_eval_stress",
                "fe_geometry", "fe_last_error", "fe_last_error_element", "fe_launch_count",
                "fe_create_csr", "fe_csr_info", "fe_csr_arrays", "fe_csr_copy_arrays",
                "fe_assemble_matrix", "fe_destroy_csr")
@@ -216,6 +218,15 @@ def fe_eval_scalar(handle: int, form: int, dtype: int, mat_kind: int,
     m = _material(mat_kind, mat_a, mat_b)
     _check(_lib.fe_eval_scalar(handle, form, dtype, ctypes.byref(m), _ptr(u), elem_begin, elem_end,
                                _ptr(value), _stream(stream)))
+
+
+def fe_eval_stress(handle: int, mat_kind: int, mat_a: Optional[torch.Tensor],
+                   mat_b: Optional[torch.Tensor], u: torch.Tensor, elem_begin: int, elem_end: int,
+                   sigma: torch.Tensor, stream=None):
+    """sigma [E'][nq][6] (fp64 device) = D e(u) at the quadrature points (Tab. 2)."""
+    m = _material(mat_kind, mat_a, mat_b)
+    _check(_lib.fe_eval_stress(handle, ctypes.byref(m), _ptr(u), elem_begin, elem_end, _ptr(sigma),
+                               _stream(stream)))
 
 
 def fe_geometry(handle: int, detw: Optional[torch.Tensor], jinv: Optional[torch.Tensor],
@@ -352,6 +363,14 @@ class Mesh:
         fe_eval_scalar(self.handle, form, dt, mat_kind, mat_a, mat_b, u, elem_begin, elem_end,
                        value, stream)
         return value
+
+    def stress(self, u, mat_kind=MAT_PER_QP, mat_a=None, mat_b=None, elem_begin=0, elem_end=None,
+               stream=None):
+        elem_end = self.n_elems if elem_end is None else elem_end
+        sigma = torch.empty((max(elem_end - elem_begin, 0), self.nq, 6), dtype=torch.float64,
+                            device=self.device)
+        fe_eval_stress(self.handle, mat_kind, mat_a, mat_b, u, elem_begin, elem_end, sigma, stream)
+        return sigma
 
     def geometry(self, stream=None):
         detw = torch.empty((self.n_elems, self.nq), dtype=torch.float64, device=self.device)

@@ -55,12 +55,13 @@ void free_mesh(fe_mesh* m) {
 }
 
 int form_ncomp(int form) {
-  return (form == FE_FORM_VECTOR_MASS || form == FE_FORM_ELASTICITY || form == FE_FORM_CONVECTIVE) ? 3 : 1;
+  return (form == FE_FORM_VECTOR_MASS || form == FE_FORM_ELASTICITY || form == FE_FORM_CONVECTIVE ||
+          form == FE_FORM_WEIGHTED_DOT || form == FE_FORM_DIVERGENCE) ? 3 : 1;
 }
 
 fe_status check_common(const fe_mesh* mesh, int form, int64_t e0, int64_t e1) {
   if (!mesh) return fail(FE_ERR_INVALID_ARG, "mesh is NULL");
-  if (form < FE_FORM_DIFFUSION || form > FE_FORM_CONVECTIVE)
+  if (form < FE_FORM_DIFFUSION || form > FE_FORM_DIVERGENCE)
     return fail(FE_ERR_INVALID_ARG, "unknown form " + std::to_string(form));
   if (e0 < 0 || e1 > mesh->n_elems || e0 > e1)
     return fail(FE_ERR_INVALID_ARG, "element range [" + std::to_string(e0) + ", " +
@@ -70,7 +71,7 @@ fe_status check_common(const fe_mesh* mesh, int form, int64_t e0, int64_t e1) {
 }
 
 fe_status check_material(int form, const fe_material* mat) {
-  if (form == FE_FORM_CONVECTIVE) return FE_OK;
+  if (form == FE_FORM_CONVECTIVE || form == FE_FORM_DIVERGENCE) return FE_OK;
   if (!mat) return fail(FE_ERR_INVALID_ARG, "material is NULL");
   if (!mat->a) return fail(FE_ERR_INVALID_ARG, "material array a is NULL");
   if (form == FE_FORM_ELASTICITY) {
@@ -253,6 +254,8 @@ fe_status fe_eval_element_matrices(const fe_mesh* mesh, int32_t form, int32_t dt
   if ((s = check_material(form, mat)) != FE_OK) return s;
   if (form == FE_FORM_CONVECTIVE && !state_u)
     return fail(FE_ERR_INVALID_ARG, "convective tangent needs state_u");
+  if (form == FE_FORM_DIVERGENCE)
+    return fail(FE_ERR_UNSUPPORTED, "the divergence operator has no trial variable: no matrix mode");
   if (elem_end > elem_begin && !K) return fail(FE_ERR_INVALID_ARG, "K is NULL");
   feb200::MatArgs ma{mat ? mat->kind : 0, mat ? mat->a : nullptr, mat ? mat->b : nullptr};
   cudaError_t e = feb200::launch_matrix(mesh, form, ma, (const double*)state_u, elem_begin,
@@ -334,6 +337,21 @@ fe_status fe_eval_scalar(const fe_mesh* mesh, int32_t form, int32_t dtype, const
   if (e == cudaErrorNotSupported)
     return fail(FE_ERR_UNSUPPORTED, "eval mode not built for this form / order / dtype");
   if (e != cudaSuccess) return cuda_fail(e, "fe_eval_scalar");
+  return ok();
+}
+
+fe_status fe_eval_stress(const fe_mesh* mesh, const fe_material* mat, const double* u,
+                         int64_t elem_begin, int64_t elem_end, double* sigma, void* stream) {
+  fe_status s = check_common(mesh, FE_FORM_ELASTICITY, elem_begin, elem_end);
+  if (s != FE_OK) return s;
+  if ((s = check_material(FE_FORM_ELASTICITY, mat)) != FE_OK) return s;
+  if (elem_end > elem_begin && (!u || !sigma)) return fail(FE_ERR_INVALID_ARG, "u / sigma is NULL");
+  feb200::MatArgs ma{mat->kind, mat->a, mat->b};
+  cudaError_t e = feb200::launch_stress(mesh, ma, u, elem_begin, elem_end, sigma, (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported)
+    return fail(FE_ERR_UNSUPPORTED, "fe_eval_stress: q1d " + std::to_string(mesh->q1d) +
+                                        " not built for order " + std::to_string(mesh->order));
+  if (e != cudaSuccess) return cuda_fail(e, "fe_eval_stress");
   return ok();
 }
 

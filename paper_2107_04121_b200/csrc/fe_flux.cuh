@@ -9,6 +9,8 @@
 //   elasticity       f1 = sigma = D e(u), Voigt with engineering shears
 //                    (Psg of P:942, reading 7)   ('IK,s(i:j)->I,s(k:l)->K')
 //   convective       f0_a = (du_a/dx_j) u_j                (Eq. fe2)
+//   weighted dot     f0_a = M_ab u_b, M per qp             ('ij,i,j')
+//   divergence       f1_aj = delta_aj (u does not enter)   ('i.i')
 #pragma once
 #include "feb200.h"
 
@@ -17,7 +19,8 @@ namespace feb200 {
 template <int FORM>
 struct FormD {
   static constexpr int D = (FORM == FE_FORM_VECTOR_MASS || FORM == FE_FORM_ELASTICITY ||
-                            FORM == FE_FORM_CONVECTIVE) ? 3 : 1;
+                            FORM == FE_FORM_CONVECTIVE || FORM == FE_FORM_WEIGHTED_DOT ||
+                            FORM == FE_FORM_DIVERGENCE) ? 3 : 1;
 };
 
 // Material values at one (cell, qp), loaded ahead of use so the global-load
@@ -32,7 +35,11 @@ template <int FORM, typename T>
 __device__ __forceinline__ MatQ<T> load_matq(int64_t e, int q, int nq, int mat_kind,
                                              const T* __restrict__ ma, const T* __restrict__ mb) {
   MatQ<T> m{0.0, 0.0, nullptr};
-  if constexpr (FORM == FE_FORM_CONVECTIVE) return m;
+  if constexpr (FORM == FE_FORM_CONVECTIVE || FORM == FE_FORM_DIVERGENCE) return m;
+  if constexpr (FORM == FE_FORM_WEIGHTED_DOT) {
+    m.Dm = ma + (e * nq + q) * 9;
+    return m;
+  }
   if constexpr (FORM == FE_FORM_ELASTICITY) {
     if (mat_kind == FE_MAT_FULL_D) {
       m.Dm = ma + (e * nq + q) * 36;
@@ -102,6 +109,14 @@ __device__ __forceinline__ void qp_flux_m(const double (&uq)[FormD<FORM>::D],
     for (int a = 0; a < D; ++a)
 #pragma unroll
       for (int j = 0; j < 3; ++j) f1[a][j] = st[a][j];
+  } else if constexpr (FORM == FE_FORM_WEIGHTED_DOT) {  // f0_a = M_ab u_b ('ij,i,j')
+    const T* M = mq.Dm;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+      f0[a] = (double)M[3 * a] * uq[0] + (double)M[3 * a + 1] * uq[1 % D] + (double)M[3 * a + 2] * uq[2 % D];
+  } else if constexpr (FORM == FE_FORM_DIVERGENCE) {  // f1_aj = delta_aj ('i.i')
+#pragma unroll
+    for (int a = 0; a < D; ++a) f1[a][a] = 1.0;
   } else {  // CONVECTIVE
 #pragma unroll
     for (int a = 0; a < D; ++a) f0[a] = gu[a][0] * uq[0] + gu[a][1] * uq[1 % D] + gu[a][2] * uq[2 % D];

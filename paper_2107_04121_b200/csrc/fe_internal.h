@@ -95,6 +95,8 @@ cudaError_t launch_geometry_materialize(const fe_mesh* m, double* detw, double* 
                                         cudaStream_t st);
 
 void count_launch();
+cudaError_t launch_stress(const fe_mesh* m, MatArgs mat, const double* u, int64_t e0, int64_t e1,
+                          double* sigma, cudaStream_t st);
 // Test hook: FEB200_MAX_CTAS caps the grid of the persistent kernels so that small meshes
 // still run many batches per CTA (ring-buffer phases wrap several times in the parity tests).
 int grid_cap(int grid);

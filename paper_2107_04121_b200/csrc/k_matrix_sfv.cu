@@ -9,6 +9,7 @@
 //               isotropic: C = lam d_aj d_bl + mu (d_ab d_jl + d_al d_jb)
 //   convective  W^{ab}_{3n} = d_ab detw (Jinv u)_n,  W^{ab}_{33} = detw du_a/dx_b   (Eq. fe4)
 //   vector mass W^{aa}_{33} = detw rho, off-diagonal blocks zero
+//   weighted dot W^{ab}_{33} = detw M_ab(q)                                       ('ij,i,j')
 // Each block is contracted axis by axis exactly as in k_matrix_sf.cu (stage z in
 // smem, stages y and x in registers, one (z-pair, y-pair) per thread).  Elasticity
 // blocks satisfy K_ba = K_ab^T, so only a <= b is computed; diagonal blocks are
@@ -34,14 +35,19 @@ __device__ __forceinline__ int voigt(int a, int j) {
 //   elasticity, FULL_D:    all 9 blocks, 9 pairs each, no symmetry assumed
 //   convective:            diagonal blocks pairs (3,0) (3,1) (3,2) (3,3); off-diagonal (3,3), symmetric
 //   vector mass:           3 diagonal blocks, pair (3,3), symmetric
+//   weighted dot:          all 9 blocks, pair (3,3); each block symmetric in (k, l), M need not be
 template <int FORM, bool FULLD>
 struct BlockSet {
-  static constexpr int NBLK = FORM == FE_FORM_VECTOR_MASS ? 3 : ((FORM == FE_FORM_CONVECTIVE || FULLD) ? 9 : 6);
-  static constexpr int NPAIR = FORM == FE_FORM_ELASTICITY ? 9 * NBLK : (FORM == FE_FORM_CONVECTIVE ? 3 * 4 + 6 : 3);
+  static constexpr int NBLK = FORM == FE_FORM_VECTOR_MASS ? 3
+                              : ((FORM == FE_FORM_CONVECTIVE || FORM == FE_FORM_WEIGHTED_DOT || FULLD) ? 9 : 6);
+  static constexpr int NPAIR = FORM == FE_FORM_ELASTICITY ? 9 * NBLK
+                               : (FORM == FE_FORM_CONVECTIVE ? 3 * 4 + 6 : (FORM == FE_FORM_WEIGHTED_DOT ? 9 : 3));
   __host__ __device__ static constexpr void info(int blk, int& a, int& b, bool& sym, bool& mirror, int& np,
                                                  int& pbase) {
     if (FORM == FE_FORM_VECTOR_MASS) {
       a = b = blk; sym = true; mirror = false; np = 1; pbase = blk;
+    } else if (FORM == FE_FORM_WEIGHTED_DOT) {
+      a = blk / 3; b = blk % 3; sym = true; mirror = false; np = 1; pbase = blk;
     } else if (FORM == FE_FORM_CONVECTIVE) {
       a = blk / 3; b = blk % 3; sym = a != b; mirror = false; np = a == b ? 4 : 1;
       pbase = 0;
@@ -71,6 +77,7 @@ struct SFV {
   static constexpr int QQP = (Q1 * Q1 + 1) / 2 * 2;
   static constexpr int T_YX = BS::NBLK * N1 * N1 * N1 * N1;  // upper bound of stage-y/x tasks
   static constexpr int THREADS = FORM == FE_FORM_VECTOR_MASS ? 128 : (FORM == FE_FORM_CONVECTIVE ? 512 : 384);
+  // (weighted dot: 9 symmetric blocks, 384 threads)
   // per-qp data: Jinv (9), detw, lam, mu  | convective: Jinv, detw, u (3), grad u (9)
   static constexpr int QD = FORM == FE_FORM_CONVECTIVE ? 23 : 13;  // odd stride: no bank conflicts
   static constexpr int OFF_K = 0;                        // [NDOF][NDOF]
@@ -260,6 +267,8 @@ __global__ void __launch_bounds__(SFV<P, FORM, FULLD>::THREADS)
           const double jj = o[3 * m] * o[3 * n] + o[3 * m + 1] * o[3 * n + 1] + o[3 * m + 2] * o[3 * n + 2];
           wv = dw * (lam * o[3 * m + ba] * o[3 * n + bb] + mu * ((ba == bb ? jj : 0.0) + o[3 * m + bb] * o[3 * n + ba]));
         }
+      } else if constexpr (FORM == FE_FORM_WEIGHTED_DOT) {
+        wv = dw * ma[(e * NQ + q) * 9 + 3 * ba + bb];
       } else if constexpr (FORM == FE_FORM_CONVECTIVE) {
         if (n == 3) wv = dw * o[13 + 3 * ba + bb];  // du_a/dx_b
         else wv = dw * (o[3 * n] * o[10] + o[3 * n + 1] * o[11] + o[3 * n + 2] * o[12]);  // (Jinv u)_n
@@ -419,6 +428,7 @@ cudaError_t launch_matrix_sfv(const fe_mesh* mh, int form, MatArgs mat, const do
       case FE_FORM_ELASTICITY: return launch_sfv_t<P, FE_FORM_ELASTICITY>(mh, mat, state_u, e0, e1, K, st); \
       case FE_FORM_CONVECTIVE: return launch_sfv_t<P, FE_FORM_CONVECTIVE>(mh, mat, state_u, e0, e1, K, st); \
       case FE_FORM_VECTOR_MASS: return launch_sfv_t<P, FE_FORM_VECTOR_MASS>(mh, mat, state_u, e0, e1, K, st); \
+      case FE_FORM_WEIGHTED_DOT: return launch_sfv_t<P, FE_FORM_WEIGHTED_DOT>(mh, mat, state_u, e0, e1, K, st); \
       default: return cudaErrorNotSupported;                                                              \
     }
   switch (mh->order) {

@@ -27,8 +27,7 @@ namespace feb200 {
 
 template <int FORM>
 struct RForm {
-  static constexpr int D = (FORM == FE_FORM_VECTOR_MASS || FORM == FE_FORM_ELASTICITY ||
-                            FORM == FE_FORM_CONVECTIVE) ? 3 : 1;
+  static constexpr int D = FormD<FORM>::D;
 };
 
 template <int P, int FORM>
@@ -187,6 +186,8 @@ static cudaError_t res_form(const fe_mesh* mh, int form, MatArgs mat, const T* u
       case FE_FORM_VECTOR_MASS: return launch_res_t<P, FE_FORM_VECTOR_MASS, T>(mh, mat, u, e0, e1, re, rg, st);
       case FE_FORM_ELASTICITY: return launch_res_t<P, FE_FORM_ELASTICITY, T>(mh, mat, u, e0, e1, re, rg, st);
       case FE_FORM_CONVECTIVE: return launch_res_t<P, FE_FORM_CONVECTIVE, T>(mh, mat, u, e0, e1, re, rg, st);
+      case FE_FORM_WEIGHTED_DOT: return launch_res_t<P, FE_FORM_WEIGHTED_DOT, T>(mh, mat, u, e0, e1, re, rg, st);
+      case FE_FORM_DIVERGENCE: return launch_res_t<P, FE_FORM_DIVERGENCE, T>(mh, mat, u, e0, e1, re, rg, st);
       default: break;
     }
   }

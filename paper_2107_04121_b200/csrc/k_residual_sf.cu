@@ -111,8 +111,14 @@ struct RSF {
   static constexpr size_t BYTES = OFF_BAR + 8 * NSLOT;
   static constexpr int PX = (EB * 24 + THREADS_ - 1) / THREADS_;  // vertex coordinates per thread
   static constexpr bool VAL = FORM == FE_FORM_MASS || FORM == FE_FORM_VECTOR_MASS ||
-                              FORM == FE_FORM_MASS_DIFFUSION || FORM == FE_FORM_CONVECTIVE;
-  static constexpr bool GRAD = FORM != FE_FORM_MASS && FORM != FE_FORM_VECTOR_MASS;
+                              FORM == FE_FORM_MASS_DIFFUSION || FORM == FE_FORM_CONVECTIVE ||
+                              FORM == FE_FORM_WEIGHTED_DOT;
+  // GRAD: the flux reads grad u (forward gradient stages); BGRAD: the flux has an f1 part
+  // (tested against grad v: backward gradient stages)
+  static constexpr bool GRAD = FORM == FE_FORM_DIFFUSION || FORM == FE_FORM_MASS_DIFFUSION ||
+                               FORM == FE_FORM_ELASTICITY || FORM == FE_FORM_CONVECTIVE;
+  static constexpr bool BGRAD = FORM == FE_FORM_DIFFUSION || FORM == FE_FORM_MASS_DIFFUSION ||
+                                FORM == FE_FORM_ELASTICITY || FORM == FE_FORM_DIVERGENCE;
 };
 
 template <int P, int FORM, typename T>
@@ -126,7 +132,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
   constexpr bool VAL = L::VAL, GRAD = L::GRAD;
   // the backward pass tests against grad v only where the flux has an f1 part
   // (the convective residual v . (grad u) u has f0 only, Eq. fe2)
-  constexpr bool BGRAD = GRAD && FORM != FE_FORM_CONVECTIVE;
+  constexpr bool BGRAD = L::BGRAD;
   using A = T;  // contraction arithmetic in the call's precision (geometry and flux stay fp64)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Bs = reinterpret_cast<T*>(smem_raw);  // [2][Q1][N1] in the arithmetic type
@@ -269,6 +275,8 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
           if (mat_kind == FE_MAT_FULL_D) m.Dm = ma + (e * NQ + q) * 36;
           else if (mat_kind == FE_MAT_PER_ELEM) { m.a = (double)msa[0]; m.b = (double)msb[0]; }
           else { m.a = (double)msa[q]; m.b = (double)msb[q]; }
+        } else if constexpr (FORM == FE_FORM_WEIGHTED_DOT) {
+          m.Dm = ma + (e * NQ + q) * 9;  // 3x3 block read through L1 like FULL_D
         } else if constexpr (MAT_QP) {
           m.a = (double)msa[q];
           if constexpr (FORM == FE_FORM_MASS_DIFFUSION) m.b = (double)msb[q];
@@ -550,6 +558,8 @@ static cudaError_t rsf_form(const fe_mesh* mh, int form, MatArgs mat, const T* u
       case FE_FORM_VECTOR_MASS: return launch_rsf_t<P, FE_FORM_VECTOR_MASS, T>(mh, mat, u, e0, e1, re, rg, ev, st);
       case FE_FORM_ELASTICITY: return launch_rsf_t<P, FE_FORM_ELASTICITY, T>(mh, mat, u, e0, e1, re, rg, ev, st);
       case FE_FORM_CONVECTIVE: return launch_rsf_t<P, FE_FORM_CONVECTIVE, T>(mh, mat, u, e0, e1, re, rg, ev, st);
+      case FE_FORM_WEIGHTED_DOT: return launch_rsf_t<P, FE_FORM_WEIGHTED_DOT, T>(mh, mat, u, e0, e1, re, rg, ev, st);
+      case FE_FORM_DIVERGENCE: return launch_rsf_t<P, FE_FORM_DIVERGENCE, T>(mh, mat, u, e0, e1, re, rg, ev, st);
       default: break;
     }
   }

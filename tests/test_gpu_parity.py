@@ -419,3 +419,77 @@ def test_unaligned_outputs(form, p):
     rv = rbig[1:].view(pr.n_elems, nd)
     mesh.residual(form, dev(pr.u), *mat, r_elem=rv, want_elem=True)
     assert rel(rv.cpu().numpy(), oracle.problem_residual(pr)) <= TOL64
+
+
+# ---- N3: the remaining Tab. 2 forms --------------------------------------------
+
+@pytest.mark.parametrize("p", [1, 2])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_weighted_dot_matrix(p, shape):
+    """'ij,i,j' matrix mode: 9 blocks of weight detw M_ab, M non-symmetric."""
+    pr = fi.make_problem(fi.WEIGHTED_DOT, p, shape, 13000 + p)
+    mesh = gpu_mesh(pr)
+    K = mesh.element_matrices(fi.WEIGHTED_DOT, pr.mat_kind, dev(pr.mat_a))
+    Kref = oracle.problem_matrix(pr)
+    assert rel(K.cpu().numpy(), Kref) <= TOL64
+    # K is not symmetric (M is not), but each (a, b) block is symmetric in (k, l)
+    nb = pr.nb
+    Kn = K.cpu().numpy().reshape(pr.n_elems, 3, nb, 3, nb)
+    assert np.abs(Kn - Kn.transpose(0, 1, 4, 3, 2)).max() <= 1e-14 * np.abs(Kn).max()
+
+
+@pytest.mark.parametrize("form", [fi.WEIGHTED_DOT, fi.DIVERGENCE])
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+@pytest.mark.parametrize("impl", ["default", "dense"])
+def test_n3_residual(form, p, impl, monkeypatch):
+    """Residual mode of 'ij,i,j' (f0 = M u) and 'i.i' (r_k = int dphi_k/dx_a), sum-factorised
+    and dense kernels, ragged cell counts."""
+    if impl == "dense":
+        monkeypatch.setenv("FEB200_RESIDUAL_IMPL", "dense")
+    pr = fi.make_problem(form, p, (5, 3, 4) if p <= 2 else (3, 2, 3), 14000 + 10 * form + p)
+    r_ref = oracle.problem_residual(pr)
+    R_ref = oracle.assemble(r_ref, pr.dof_conn, pr.n_nodes, pr.ncomp)
+    mesh = gpu_mesh(pr)
+    r_elem, r_glob = mesh.residual(form, dev(pr.u), pr.mat_kind, dev(pr.mat_a), dev(pr.mat_b),
+                                   want_elem=True)
+    torch.cuda.synchronize()
+    assert rel(r_elem.cpu().numpy(), r_ref) <= TOL64
+    assert rel(r_glob.cpu().numpy().ravel(), R_ref) <= TOL64
+
+
+@pytest.mark.parametrize("form", [fi.WEIGHTED_DOT, fi.DIVERGENCE])
+@pytest.mark.parametrize("p", [1, 2, 4])
+def test_n3_eval(form, p):
+    """'eval' mode: int u.M.u and int div u."""
+    pr = fi.make_problem(form, p, (5, 3, 4), 15000 + 10 * form + p)
+    ref = oracle.problem_eval_scalar(pr)
+    mesh = gpu_mesh(pr)
+    v = mesh.eval_scalar(form, dev(pr.u), pr.mat_kind, dev(pr.mat_a), dev(pr.mat_b))
+    assert abs(v.item() - ref) <= TOL64 * max(abs(ref), 1.0)
+
+
+def test_divergence_has_no_matrix_mode():
+    m = fe()
+    pr = fi.make_problem(fi.DIVERGENCE, 2, (2, 2, 2), 3)
+    mesh = gpu_mesh(pr)
+    with pytest.raises(m.FEError) as ei:
+        mesh.element_matrices(fi.DIVERGENCE)
+    assert ei.value.status == m.FE_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("kind", [fi.MAT_PER_ELEM, fi.MAT_PER_QP, fi.MAT_FULL_D])
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_stress(kind, p):
+    """Cauchy stress 'IK,s(k:l)->K' at every qp, every material kind, plus an
+    element sub-range and an empty one."""
+    pr = fi.make_problem(fi.ELASTICITY, p, (4, 3, 2), 16000 + 10 * p + kind, mat_kind=kind)
+    ref = oracle.problem_stress(pr)
+    mesh = gpu_mesh(pr)
+    mat = (kind, dev(pr.mat_a), dev(pr.mat_b))
+    sig = mesh.stress(dev(pr.u), *mat)
+    assert sig.shape == ref.shape
+    assert rel(sig.cpu().numpy(), ref) <= TOL64
+    sub = mesh.stress(dev(pr.u), *mat, elem_begin=5, elem_end=17)
+    assert rel(sub.cpu().numpy(), ref[5:17]) <= TOL64
+    empty = mesh.stress(dev(pr.u), *mat, elem_begin=3, elem_end=3)
+    assert empty.shape[0] == 0
