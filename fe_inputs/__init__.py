@@ -190,6 +190,31 @@ def make_problem(form: int, p: int, shape, seed: int, *, q1d: Optional[int] = No
                    u=np.ascontiguousarray(u))
 
 
+@dataclass
+class MixedProblem:
+    """Velocity-pressure pair for the Stokes coupling forms (Tab. 2): `vel` is a
+    vector problem of order pv (its u is the velocity DOF vector [n_nodes][3]); the pressure
+    space has order pp on the same cells (lattice numbering), nodal values `pres` [n_p]."""
+    vel: Problem
+    pp: int
+    p_dof_conn: np.ndarray            # [E][(pp+1)^3] int32
+    n_p_nodes: int
+    pres: np.ndarray                  # [n_p] float64
+
+    @property
+    def nbp(self) -> int:
+        return (self.pp + 1) ** 3
+
+
+def make_mixed_problem(pv: int, pp: int, shape, seed: int, *, perturb: float = 0.15) -> MixedProblem:
+    """Q_pv x Q_pp pair on the perturbed grid of make_problem (draws 1 and 3 as there), plus
+    draw 4: pressure values U[-1, 1] from a second generator seeded seed + 1."""
+    vel = make_problem(DIVERGENCE, pv, shape, seed, perturb=perturb, name="mixed")
+    pdc, n_p = lattice_dof_conn(*shape, pp)
+    pres = np.random.default_rng(seed + 1).uniform(-1.0, 1.0, size=n_p)
+    return MixedProblem(vel=vel, pp=pp, p_dof_conn=pdc, n_p_nodes=n_p, pres=pres)
+
+
 # BASELINE.json configs (index k -> seed 210704121 + k)
 CONFIGS = {
     "C1": dict(index=0, form=DIFFUSION, p=1, N=4,

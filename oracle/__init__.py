@@ -56,6 +56,11 @@ def lib():
         _lib.oracle_eval_scalar.restype = ci
         _lib.oracle_eval_stress.argtypes = [ci, ci, i64, P, P, P, ci, P, P, P, i64, i64, P]
         _lib.oracle_eval_stress.restype = ci
+        _lib.oracle_coupling_matrix.argtypes = [ci, ci, ci, ci, i64, P, P, i64, i64, P]
+        _lib.oracle_coupling_residual.argtypes = [ci, ci, ci, ci, i64, P, P, P, P, P, P, i64, i64, P]
+        _lib.oracle_coupling_eval.argtypes = [ci, ci, ci, i64, P, P, P, P, P, P, i64, i64, P]
+        for f in ("oracle_coupling_matrix", "oracle_coupling_residual", "oracle_coupling_eval"):
+            getattr(_lib, f).restype = ci
         _lib.oracle_bad_element.restype = i64
         for f in ("oracle_gauss_legendre", "oracle_lagrange_1d", "oracle_tables", "oracle_geometry",
                   "oracle_eval_matrix", "oracle_eval_residual", "oracle_assemble"):
@@ -192,6 +197,49 @@ def eval_stress(p, q1d, coords, conn, dof_conn, u, mat_kind=1, mat_a=None, mat_b
                                     _ptr(mat_a), _ptr(mat_b), _ptr(u), elem_begin, elem_end,
                                     _ptr(sig)))
     return sig
+
+
+def coupling_matrix(pv, pp, q1d, coords, conn, transposed=False, elem_begin=0, elem_end=None):
+    """Stokes coupling matrices (Tab. 2 'i.i,0'): B [E'][3 nbv][nbp] (test v,
+    trial p) or, transposed, C [E'][nbp][3 nbv] (test q, trial u)."""
+    coords, conn = _f64(coords), _i32(conn)
+    E = conn.shape[0]
+    elem_end = E if elem_end is None else elem_end
+    nbv, nbp = (pv + 1) ** 3, (pp + 1) ** 3
+    shape = (nbp, 3 * nbv) if transposed else (3 * nbv, nbp)
+    out = np.zeros((max(elem_end - elem_begin, 0),) + shape)
+    _check(lib().oracle_coupling_matrix(int(transposed), pv, pp, q1d, E, _ptr(coords), _ptr(conn),
+                                        elem_begin, elem_end, _ptr(out)))
+    return out
+
+
+def coupling_residual(pv, pp, q1d, coords, conn, dof_v, dof_p, u=None, p=None, transposed=False,
+                      elem_begin=0, elem_end=None):
+    """Residual of the Stokes coupling (r_v = int div v p_h, input p) or of the transposed
+    coupling (r_q = int q div u_h, input u)."""
+    coords, conn, dof_v, dof_p = _f64(coords), _i32(conn), _i32(dof_v), _i32(dof_p)
+    u, p = _f64(u), _f64(p)
+    E = conn.shape[0]
+    elem_end = E if elem_end is None else elem_end
+    n = (pp + 1) ** 3 if transposed else 3 * (pv + 1) ** 3
+    out = np.zeros((max(elem_end - elem_begin, 0), n))
+    _check(lib().oracle_coupling_residual(int(transposed), pv, pp, q1d, E, _ptr(coords), _ptr(conn),
+                                          _ptr(dof_v), _ptr(dof_p), _ptr(u), _ptr(p), elem_begin,
+                                          elem_end, _ptr(out)))
+    return out
+
+
+def coupling_eval(pv, pp, q1d, coords, conn, dof_v, dof_p, u, p, elem_begin=0, elem_end=None):
+    """'eval' mode of the coupling: int p_h div u_h."""
+    coords, conn, dof_v, dof_p = _f64(coords), _i32(conn), _i32(dof_v), _i32(dof_p)
+    u, p = _f64(u), _f64(p)
+    E = conn.shape[0]
+    elem_end = E if elem_end is None else elem_end
+    out = np.zeros(1)
+    _check(lib().oracle_coupling_eval(pv, pp, q1d, E, _ptr(coords), _ptr(conn), _ptr(dof_v),
+                                      _ptr(dof_p), _ptr(u), _ptr(p), elem_begin, elem_end,
+                                      _ptr(out)))
+    return float(out[0])
 
 
 def problem_stress(prob):

@@ -708,3 +708,112 @@ int oracle_eval_stress(int p, int q1d, int64_t n_elems, const double *coords, co
   free(xi); free(w); free(Phi); free(dPhi);
   return status;
 }
+
+/* ------------------------------------------------------------------ */
+/* Mixed velocity-pressure forms (Tab. 2): velocity space Q_pv (vector, D = 3,
+ * tables Phi / dPhi), pressure space Q_pp (scalar, tables Psi), one quadrature rule q1d
+ * shared by both (reading 19).
+ *   Stokes coupling            ('i.i,0', v, p): int (dv_i/dx_i) p
+ *       matrix  B[e'][a*nbv + k][l] = int dphi_k/dx_a psi_l      (test v, trial p)
+ *       residual r[e'][a*nbv + k]   = int dphi_k/dx_a p_h        (p_h = sum_l psi_l p_l)
+ *   transposed Stokes coupling ('i.i,0', u, q): int q (du_i/dx_i)
+ *       matrix  C[e'][l][a*nbv + k] = int psi_l dphi_k/dx_a      (test q, trial u)
+ *       residual r[e'][l]           = int psi_l div u_h
+ *   eval (both):  int p_h div u_h
+ * u: [n_v][3] node-major (Eq. fe1c), p: [n_p].  transposed selects the second form. */
+static int coupling_common(int pv, int pp, int q1d, int64_t n_elems, int64_t e0, int64_t e1) {
+  if (pv < 1 || pv > 8 || pp < 1 || pp > 8 || q1d < 1 || q1d > 16 || n_elems < 0) return OR_ERR_ARG;
+  if (e0 < 0 || e1 > n_elems || e0 > e1) return OR_ERR_ARG;
+  return OR_OK;
+}
+
+/* mode 0: matrix (out = B or C); mode 1: residual (in = p or u, out = r); mode 2: eval */
+static int coupling_run(int mode, int transposed, int pv, int pp, int q1d, int64_t n_elems,
+                        const double *coords, const int32_t *conn, const int32_t *dof_v,
+                        const int32_t *dof_p, const double *u, const double *p, int64_t e0,
+                        int64_t e1, double *out, double *value) {
+  int st = coupling_common(pv, pp, q1d, n_elems, e0, e1);
+  if (st != OR_OK) return st;
+  const int nv1 = pv + 1, nbv = nv1 * nv1 * nv1, np1 = pp + 1, nbp = np1 * np1 * np1;
+  const int nq = q1d * q1d * q1d;
+  double *xi = malloc(sizeof(double) * 3 * nq), *w = malloc(sizeof(double) * nq);
+  double *Phi = malloc(sizeof(double) * nq * nbv), *dPhi = malloc(sizeof(double) * nq * 3 * nbv);
+  double *xi2 = malloc(sizeof(double) * 3 * nq), *w2 = malloc(sizeof(double) * nq);
+  double *Psi = malloc(sizeof(double) * nq * nbp), *dPsi = malloc(sizeof(double) * nq * 3 * nbp);
+  oracle_tables(pv, q1d, xi, w, Phi, dPhi);
+  oracle_tables(pp, q1d, xi2, w2, Psi, dPsi); /* same points: the shared rule */
+  const int64_t osz = mode == 0 ? (int64_t)3 * nbv * nbp : (transposed ? nbp : 3 * nbv);
+  int status = OR_OK;
+  double total = 0.0;
+  double *G = malloc(sizeof(double) * 3 * nbv);
+  for (int64_t e = e0; e < e1 && status == OR_OK; ++e) {
+    double *oe = out ? out + (e - e0) * osz : NULL;
+    if (oe)
+      for (int64_t i = 0; i < osz; ++i) oe[i] = 0.0;
+    for (int q = 0; q < nq; ++q) {
+      double J[3][3], Ji[3][3];
+      double det = cell_jacobian(coords, conn + 8 * e, xi + 3 * q, J, Ji);
+      if (!(det > 0.0)) { status = OR_ERR_DEGENERATE; g_bad_elem = e; break; }
+      const double detw = w[q] * det;
+      const double *psi = Psi + (int64_t)q * nbp;
+      /* G[a][k] = dphi_k/dx_a = sum_m dPhi_m,k Jinv[m][a] */
+      for (int a = 0; a < 3; ++a)
+        for (int k = 0; k < nbv; ++k) {
+          double s = 0.0;
+          for (int m = 0; m < 3; ++m) s += dPhi[((int64_t)q * 3 + m) * nbv + k] * Ji[m][a];
+          G[a * nbv + k] = s;
+        }
+      double ph = 0.0, divu = 0.0;
+      if ((mode == 1 && !transposed) || mode == 2)
+        for (int l = 0; l < nbp; ++l) ph += psi[l] * p[dof_p[e * nbp + l]];
+      if ((mode == 1 && transposed) || mode == 2)
+        for (int a = 0; a < 3; ++a)
+          for (int k = 0; k < nbv; ++k) divu += G[a * nbv + k] * u[(int64_t)dof_v[e * nbv + k] * 3 + a];
+      if (mode == 0) {
+        for (int a = 0; a < 3; ++a)
+          for (int k = 0; k < nbv; ++k)
+            for (int l = 0; l < nbp; ++l) {
+              const double v = detw * G[a * nbv + k] * psi[l];
+              if (transposed) oe[(int64_t)l * 3 * nbv + a * nbv + k] += v;
+              else oe[((int64_t)a * nbv + k) * nbp + l] += v;
+            }
+      } else if (mode == 1) {
+        if (transposed)
+          for (int l = 0; l < nbp; ++l) oe[l] += detw * psi[l] * divu;
+        else
+          for (int i = 0; i < 3 * nbv; ++i) oe[i] += detw * G[i] * ph;
+      } else {
+        total += detw * ph * divu;
+      }
+    }
+  }
+  free(G); free(xi); free(w); free(Phi); free(dPhi); free(xi2); free(w2); free(Psi); free(dPsi);
+  if (status == OR_OK && mode == 2) *value = total;
+  return status;
+}
+
+int oracle_coupling_matrix(int transposed, int pv, int pp, int q1d, int64_t n_elems,
+                           const double *coords, const int32_t *conn, int64_t elem_begin,
+                           int64_t elem_end, double *out) {
+  if (!out) return OR_ERR_ARG;
+  return coupling_run(0, transposed, pv, pp, q1d, n_elems, coords, conn, NULL, NULL, NULL, NULL,
+                      elem_begin, elem_end, out, NULL);
+}
+
+int oracle_coupling_residual(int transposed, int pv, int pp, int q1d, int64_t n_elems,
+                             const double *coords, const int32_t *conn, const int32_t *dof_v,
+                             const int32_t *dof_p, const double *u, const double *p,
+                             int64_t elem_begin, int64_t elem_end, double *r_elem) {
+  if (!r_elem || (transposed ? (!u || !dof_v) : (!p || !dof_p))) return OR_ERR_ARG;
+  return coupling_run(1, transposed, pv, pp, q1d, n_elems, coords, conn, dof_v, dof_p, u, p,
+                      elem_begin, elem_end, r_elem, NULL);
+}
+
+int oracle_coupling_eval(int pv, int pp, int q1d, int64_t n_elems, const double *coords,
+                         const int32_t *conn, const int32_t *dof_v, const int32_t *dof_p,
+                         const double *u, const double *p, int64_t elem_begin, int64_t elem_end,
+                         double *value) {
+  if (!value || !u || !p || !dof_v || !dof_p) return OR_ERR_ARG;
+  return coupling_run(2, 0, pv, pp, q1d, n_elems, coords, conn, dof_v, dof_p, u, p, elem_begin,
+                      elem_end, NULL, value);
+}

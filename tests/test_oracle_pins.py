@@ -667,3 +667,100 @@ def test_N3_cauchy_stress(p):
                               pr.mat_kind, pr.mat_a, pr.mat_b)
     scale = max(np.abs(oracle.isotropic_D(a, b)).max() for a, b in zip(pr.mat_a, pr.mat_b))
     assert np.abs(sig0).max() < 1e-13 * scale * np.abs(W).max()  # zero up to rounding
+
+
+# ---------------------------------------------------------------- N3: Stokes coupling pair
+def _exact_1d_mixed(pv, pp):
+    """Mv[i][j] = int phi_i psi_j, Cv[i][j] = int phi_i' psi_j on [0,1]; phi of order pv, psi
+    of order pp (exact rationals)."""
+    Lv, Lp = _lagrange_exact(pv), _lagrange_exact(pp)
+    dLv = [_poly_deriv(P) for P in Lv]
+    Mv = [[_poly_int01(_poly_mul(Lv[i], Lp[j])) for j in range(pp + 1)] for i in range(pv + 1)]
+    Cv = [[_poly_int01(_poly_mul(dLv[i], Lp[j])) for j in range(pp + 1)] for i in range(pv + 1)]
+    return Mv, Cv
+
+
+def _node_coords_order(prob, p, dof_conn, n_nodes):
+    """Physical coordinates of an order-p node lattice (trilinear images, reading 4)."""
+    X = np.zeros((n_nodes, 3))
+    t = np.arange(p + 1) / p
+    for l in range(p + 1):
+        for j in range(p + 1):
+            for i in range(p + 1):
+                k = i + (p + 1) * (j + (p + 1) * l)
+                w = np.array([(t[i] if a else 1 - t[i]) * (t[j] if b else 1 - t[j]) *
+                              (t[l] if cc else 1 - t[l])
+                              for cc in (0, 1) for b in (0, 1) for a in (0, 1)])
+                X[dof_conn[:, k]] = np.einsum("v,evi->ei", w, prob.coords[prob.conn])
+    return X
+
+
+@pytest.mark.parametrize("pv,pp", [(1, 1), (2, 1), (3, 2), (2, 2)])
+def test_N3_stokes_coupling_box_closed_form(pv, pp):
+    """'i.i,0' on an axis-aligned box: B[(a,k), l] = vol * prod_d F_d[k_d][l_d] / h_a
+    with F_d = Cv (int phi' psi) along d == a and Mv (int phi psi) otherwise, exact rationals;
+    the transposed coupling is C[l, (a,k)] with the same entries."""
+    dims = (Fraction(1, 2), Fraction(1, 3), Fraction(2, 5))
+    vol = dims[0] * dims[1] * dims[2]
+    Mv, Cv = _exact_1d_mixed(pv, pp)
+    nv, npp = pv + 1, pp + 1
+    nbv, nbp = nv ** 3, npp ** 3
+    ref = np.zeros((3 * nbv, nbp))
+    for a in range(3):
+        for kz in range(nv):
+            for ky in range(nv):
+                for kx in range(nv):
+                    k = kx + nv * (ky + nv * kz)
+                    for lz in range(npp):
+                        for ly in range(npp):
+                            for lx in range(npp):
+                                l = lx + npp * (ly + npp * lz)
+                                f = [(Cv if a == d else Mv)[kk][ll]
+                                     for d, (kk, ll) in enumerate(((kx, lx), (ky, ly), (kz, lz)))]
+                                ref[a * nbv + k, l] = float(vol * f[0] * f[1] * f[2] / dims[a])
+    c, conn = box(*[float(d) for d in dims], origin=(0.1, 0.2, -0.3))
+    B = oracle.coupling_matrix(pv, pp, pv + 1, c, conn)[0]
+    assert rel(B, ref) < 1e-14
+    C = oracle.coupling_matrix(pv, pp, pv + 1, c, conn, transposed=True)[0]
+    assert rel(C, ref.T) < 1e-14
+
+
+@pytest.mark.parametrize("pv,pp", [(2, 1), (1, 1), (3, 2)])
+def test_N3_stokes_coupling_consistency(pv, pp):
+    """On a perturbed grid: r_v(p) = B p_e and r_q(u) = C u_e (Alg. 1 = Alg. 2 applied, P8);
+    C = B^T; eval = p_e . r_q(u) = u_e . r_v(p); constant pressure p = 1 gives the divergence
+    form 'i.i' residual exactly."""
+    mp = fi.make_mixed_problem(pv, pp, (3, 2, 2), 51)
+    v = mp.vel
+    q1d = pv + 1
+    args = (pv, pp, q1d, v.coords, v.conn)
+    B = oracle.coupling_matrix(*args)
+    C = oracle.coupling_matrix(*args, transposed=True)
+    assert rel(C, np.swapaxes(B, 1, 2)) < 1e-15
+    pe = mp.pres[mp.p_dof_conn]
+    ue = np.stack([v.u[v.dof_conn][:, :, a] for a in range(3)], axis=1).reshape(v.n_elems, -1)
+    rv = oracle.coupling_residual(*args, v.dof_conn, mp.p_dof_conn, p=mp.pres)
+    rq = oracle.coupling_residual(*args, v.dof_conn, mp.p_dof_conn, u=v.u, transposed=True)
+    assert rel(rv, np.einsum("eij,ej->ei", B, pe)) < 1e-14
+    assert rel(rq, np.einsum("eij,ej->ei", C, ue)) < 1e-14
+    ev = oracle.coupling_eval(*args, v.dof_conn, mp.p_dof_conn, v.u, mp.pres)
+    assert abs(ev - float((pe * rq).sum())) < 1e-13 * max(abs(ev), 1.0)
+    assert abs(ev - float((ue * rv).sum())) < 1e-13 * max(abs(ev), 1.0)
+    r1 = oracle.coupling_residual(*args, v.dof_conn, mp.p_dof_conn, p=np.ones(mp.n_p_nodes))
+    rd = oracle.eval_residual(fi.DIVERGENCE, pv, q1d, v.coords, v.conn, v.dof_conn, v.u)
+    assert rel(r1, rd) < 1e-14
+
+
+@pytest.mark.parametrize("pv,pp", [(2, 1), (1, 1), (3, 2)])
+def test_N3_stokes_coupling_linear_fields(pv, pp):
+    """u = x and p = x_0 + 2 x_1 - x_2 are exact in Q_pv / Q_pp on trilinear cells, so
+    eval = int p div x = 3 int (x_0 + 2 x_1 - x_2) = 3 (1/2 + 1 - 1/2) = 3 on the unit cube;
+    with p = 1: int div x = 3."""
+    mp = fi.make_mixed_problem(pv, pp, (2, 3, 2), 57)
+    v = mp.vel
+    X = _node_coords_order(v, pv, v.dof_conn, v.n_nodes)
+    Xp = _node_coords_order(v, pp, mp.p_dof_conn, mp.n_p_nodes)
+    pl = Xp[:, 0] + 2 * Xp[:, 1] - Xp[:, 2]
+    args = (pv, pp, pv + 1, v.coords, v.conn, v.dof_conn, mp.p_dof_conn)
+    assert abs(oracle.coupling_eval(*args, X, pl) - 3.0) < 1e-13
+    assert abs(oracle.coupling_eval(*args, X, np.ones(mp.n_p_nodes)) - 3.0) < 1e-13
