@@ -191,6 +191,50 @@ fe_status fe_eval_scalar(const fe_mesh *mesh, int32_t form, int32_t dtype, const
 fe_status fe_eval_stress(const fe_mesh *mesh, const fe_material *mat, const double *u,
                          int64_t elem_begin, int64_t elem_end, double *sigma, void *stream);
 
+/* ---- Mixed velocity-pressure forms (Tab. 2) ----------------------
+ * The mesh handle is the velocity space Q_pv (vector, D = 3, its dof_conn and
+ * n_nodes); an fe_field is a scalar pressure space Q_pp on the same cells,
+ * 1 <= pp <= pv, evaluated at the mesh's quadrature points (one rule for both,
+ * DESIGN.md reading 19).  Element-local velocity DOFs are component-major
+ * a * n_bv + k (reading 9); pressure DOFs are l = 0..n_bp-1 (lexicographic).
+ *   Stokes coupling            ('i.i,0', v, p): int (dv_i/dx_i) p
+ *   transposed Stokes coupling ('i.i,0', u, q): int q (du_i/dx_i)           */
+typedef struct fe_field fe_field;
+
+/* Create the pressure space: order pp (1..mesh order), n_nodes pressure nodes,
+ * dof_conn [n_elems][(pp+1)^3] int32 (host or device; copied, range-checked
+ * against n_nodes -> FE_ERR_INVALID_ARG).  The field keeps a pointer to `mesh`,
+ * which must outlive it.  Pairs built: (pv, pp) in (1,1) (2,1) (2,2) (3,2)
+ * (3,3) (4,3) (4,4); others FE_ERR_UNSUPPORTED. */
+fe_status fe_create_field(const fe_mesh *mesh, int32_t order, int64_t n_nodes,
+                          const int32_t *dof_conn, void *stream, fe_field **out);
+fe_status fe_destroy_field(fe_field *field);
+
+/* Matrix mode of the coupling over cells [elem_begin, elem_end):
+ *   transposed = 0: B[e'][a*n_bv + k][l] = int dphi_k/dx_a psi_l   (test v, trial p)
+ *   transposed = 1: C[e'][l][a*n_bv + k] = the same entries         (test q, trial u)
+ * out: device double, caller owned, overwritten. */
+fe_status fe_eval_coupling_matrices(const fe_mesh *mesh, const fe_field *pressure,
+                                    int32_t transposed, int64_t elem_begin, int64_t elem_end,
+                                    double *out, void *stream);
+
+/* Residual mode:
+ *   transposed = 0: input x = pressure p [n_p];        r_elem [E'][3 n_bv],
+ *                   r_v = int dphi_k/dx_a p_h, r_global velocity-shaped [n_v][3]
+ *   transposed = 1: input x = velocity u [n_v][3];     r_elem [E'][n_bp],
+ *                   r_q = int psi_l div u_h,  r_global pressure-shaped [n_p]
+ * r_elem nullable (overwritten), r_global nullable (ACCUMULATED, fp atomics). */
+fe_status fe_eval_coupling_residual(const fe_mesh *mesh, const fe_field *pressure,
+                                    int32_t transposed, const double *x, int64_t elem_begin,
+                                    int64_t elem_end, double *r_elem, double *r_global,
+                                    void *stream);
+
+/* 'eval' mode: value += int p_h div u_h over the cells (one device
+ * double, ACCUMULATED; the caller zeroes it). */
+fe_status fe_eval_coupling_scalar(const fe_mesh *mesh, const fe_field *pressure, const double *u,
+                                  const double *p, int64_t elem_begin, int64_t elem_end,
+                                  double *value, void *stream);
+
 /* Scatter-add of cell residuals (standalone assembly):
  *   r_global[dof_conn[e][k] * ncomp + a] += r_elem[e - elem_begin][a * n_b + k]
  * for e in [elem_begin, elem_end).  ncomp in {1, 3}. */

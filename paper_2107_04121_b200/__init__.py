@@ -68,6 +68,11 @@ def _load():
     lib.fe_eval_matrix_residual.argtypes = [P, i32, i32, ctypes.POINTER(fe_material), P, i64,
                                             i64, P, P, P, P]
     lib.fe_eval_stress.argtypes = [P, ctypes.POINTER(fe_material), P, i64, i64, P, P]
+    lib.fe_create_field.argtypes = [P, i32, i64, P, P, ctypes.POINTER(P)]
+    lib.fe_destroy_field.argtypes = [P]
+    lib.fe_eval_coupling_matrices.argtypes = [P, P, i32, i64, i64, P, P]
+    lib.fe_eval_coupling_residual.argtypes = [P, P, i32, P, i64, i64, P, P, P]
+    lib.fe_eval_coupling_scalar.argtypes = [P, P, P, P, i64, i64, P, P]
     lib.fe_create_csr.argtypes = [P, i32, P, ctypes.POINTER(P)]
     lib.fe_csr_info.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     lib.fe_csr_arrays.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P)]
@@ -80,7 +85,9 @@ def _load():
     lib.fe_launch_count.restype = i64
     for f in ("fe_create_mesh_geometry", "fe_destroy_mesh", "fe_mesh_info",
               "fe_eval_element_matrices", "fe_eval_residual", "fe_assemble_vector",
-              "fe_geometry", "fe_eval_scalar", "fe_eval_matrix_residual", "fe_eval_stress", "fe_create_csr", "fe_csr_info", "fe_csr_arrays",
+              "fe_geometry", "fe_eval_scalar", "fe_eval_matrix_residual", "fe_eval_stress", "fe_create_field", "fe_destroy_field",
+              "fe_eval_coupling_matrices", "fe_eval_coupling_residual", "fe_eval_coupling_scalar",
+              "fe_create_csr", "fe_csr_info", "fe_csr_arrays",
               "fe_csr_copy_arrays",
               "fe_assemble_matrix", "fe_destroy_csr"):
         getattr(lib, f).restype = ctypes.c_int
@@ -104,6 +111,8 @@ _lib = _LazyLib()
 ABI_SYMBOLS = ("fe_create_mesh_geometry", "fe_destroy_mesh", "fe_mesh_info",
                "fe_eval_element_matrices", "fe_eval_residual", "fe_assemble_vector", "fe_eval_scalar",
                "fe_eval_matrix_residual", "fe_eval_stress",
+               "fe_create_field", "fe_destroy_field", "fe_eval_coupling_matrices",
+               "fe_eval_coupling_residual", "fe_eval_coupling_scalar",
                "fe_geometry", "fe_last_error", "fe_last_error_element", "fe_launch_count",
                "fe_create_csr", "fe_csr_info", "fe_csr_arrays", "fe_csr_copy_arrays",
                "fe_assemble_matrix", "fe_destroy_csr")
@@ -232,6 +241,73 @@ def fe_eval_stress(handle: int, mat_kind: int, mat_a: Optional[torch.Tensor],
 def fe_geometry(handle: int, detw: Optional[torch.Tensor], jinv: Optional[torch.Tensor],
                 stream=None):
     _check(_lib.fe_geometry(handle, _ptr(detw), _ptr(jinv), _stream(stream)))
+
+
+class PressureField:
+    """Scalar pressure space Q_pp on the cells of a (velocity) Mesh (fe_create_field), and the
+    Stokes coupling forms of Tab. 2 between the two."""
+
+    def __init__(self, mesh: "Mesh", order: int, dof_conn, n_nodes: Optional[int] = None,
+                 stream=None):
+        dof_conn = _dev(dof_conn, torch.int32, mesh.device)
+        n_nodes = int(dof_conn.max().item()) + 1 if n_nodes is None else n_nodes
+        out = ctypes.c_void_p()
+        _check(_lib.fe_create_field(mesh.handle, order, n_nodes, _ptr(dof_conn), _stream(stream),
+                                    ctypes.byref(out)))
+        self.handle, self.mesh, self.order, self.n_nodes = out.value, mesh, order, n_nodes
+        self.nb = (order + 1) ** 3
+
+    def coupling_matrices(self, transposed=False, elem_begin=0, elem_end=None, out=None,
+                          stream=None):
+        """B [E'][3 nbv][nbp] ('i.i,0', v, p) or, transposed, C [E'][nbp][3 nbv] ('i.i,0', u, q)."""
+        m = self.mesh
+        elem_end = m.n_elems if elem_end is None else elem_end
+        shape = (self.nb, 3 * m.nb) if transposed else (3 * m.nb, self.nb)
+        if out is None:
+            out = torch.empty((max(elem_end - elem_begin, 0),) + shape, dtype=torch.float64,
+                              device=m.device)
+        _check(_lib.fe_eval_coupling_matrices(m.handle, self.handle, int(transposed), elem_begin,
+                                              elem_end, _ptr(out), _stream(stream)))
+        return out
+
+    def coupling_residual(self, x, transposed=False, elem_begin=0, elem_end=None,
+                          want_elem=False, want_global=True, r_elem=None, r_global=None,
+                          stream=None):
+        """transposed=False: x = pressure [n_p] -> r_v (velocity-shaped); True: x = velocity
+        [n_v][3] -> r_q (pressure-shaped).  Returns (r_elem or None, r_global or None)."""
+        m = self.mesh
+        elem_end = m.n_elems if elem_end is None else elem_end
+        n = max(elem_end - elem_begin, 0)
+        if want_elem and r_elem is None:
+            r_elem = torch.empty((n, self.nb if transposed else 3 * m.nb), dtype=torch.float64,
+                                 device=m.device)
+        if want_global and r_global is None:
+            shape = (self.n_nodes,) if transposed else (m.n_nodes, 3)
+            r_global = torch.zeros(shape, dtype=torch.float64, device=m.device)
+        _check(_lib.fe_eval_coupling_residual(m.handle, self.handle, int(transposed), _ptr(x),
+                                              elem_begin, elem_end, _ptr(r_elem), _ptr(r_global),
+                                              _stream(stream)))
+        return r_elem, r_global
+
+    def coupling_eval(self, u, p, elem_begin=0, elem_end=None, stream=None):
+        """int p_h div u_h (eval mode), a 1-element fp64 device tensor."""
+        m = self.mesh
+        elem_end = m.n_elems if elem_end is None else elem_end
+        value = torch.zeros(1, dtype=torch.float64, device=m.device)
+        _check(_lib.fe_eval_coupling_scalar(m.handle, self.handle, _ptr(u), _ptr(p), elem_begin,
+                                            elem_end, _ptr(value), _stream(stream)))
+        return value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _check(_lib.fe_destroy_field(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class CSR:

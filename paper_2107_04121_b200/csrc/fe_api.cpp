@@ -355,6 +355,117 @@ fe_status fe_eval_stress(const fe_mesh* mesh, const fe_material* mat, const doub
   return ok();
 }
 
+fe_status fe_create_field(const fe_mesh* mesh, int32_t order, int64_t n_nodes,
+                          const int32_t* dof_conn, void* stream, fe_field** out) {
+  if (!out) return fail(FE_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (!mesh) return fail(FE_ERR_INVALID_ARG, "mesh is NULL");
+  if (order < 1 || order > mesh->order)
+    return fail(FE_ERR_INVALID_ARG, "pressure order must be 1..mesh order");
+  if (n_nodes < 1 || n_nodes >= (int64_t(1) << 31)) return fail(FE_ERR_INVALID_ARG, "bad n_nodes");
+  if (mesh->n_elems > 0 && !dof_conn) return fail(FE_ERR_INVALID_ARG, "dof_conn is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  fe_field* f = new (std::nothrow) fe_field();
+  if (!f) return fail(FE_ERR_OOM, "host allocation failed");
+  f->order = order;
+  f->nb = (order + 1) * (order + 1) * (order + 1);
+  f->n_elems = mesh->n_elems;
+  f->n_nodes = n_nodes;
+  f->mesh = mesh;
+  auto bail = [&](cudaError_t e, const char* where) {
+    if (f->dof_conn) cudaFree(f->dof_conn);
+    if (f->psi) cudaFree(f->psi);
+    delete f;
+    return cuda_fail(e, where);
+  };
+  cudaError_t e;
+  const int64_t n = int64_t(f->nb) * mesh->n_elems;
+  if ((e = cudaMalloc(&f->dof_conn, sizeof(int32_t) * std::max<int64_t>(n, 1))) != cudaSuccess)
+    return bail(e, "alloc dof_conn");
+  if (n > 0 && (e = cudaMemcpyAsync(f->dof_conn, dof_conn, sizeof(int32_t) * n, cudaMemcpyDefault, st)) != cudaSuccess)
+    return bail(e, "copy dof_conn");
+  // pressure basis at the mesh's quadrature points (the same Gauss rule, step a0)
+  feb200::HostTables T = feb200::build_tables(order, mesh->q1d);
+  if ((e = upload(&f->psi, T.phi, st)) != cudaSuccess) return bail(e, "tables");
+  int* flag = nullptr;
+  int hflag = 0;
+  if ((e = cudaMalloc(&flag, sizeof(int))) != cudaSuccess) return bail(e, "alloc flag");
+  e = cudaMemsetAsync(flag, 0, sizeof(int), st);
+  if (e == cudaSuccess) e = feb200::launch_conn_check(f->dof_conn, n, n_nodes, flag, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(flag);
+  if (e != cudaSuccess) return bail(e, "dof check");
+  if (hflag) {
+    cudaFree(f->dof_conn);
+    cudaFree(f->psi);
+    delete f;
+    return fail(FE_ERR_INVALID_ARG, "pressure dof_conn entry out of [0, n_nodes)");
+  }
+  *out = f;
+  return ok();
+}
+
+fe_status fe_destroy_field(fe_field* field) {
+  if (!field) return ok();
+  cudaDeviceSynchronize();
+  if (field->dof_conn) cudaFree(field->dof_conn);
+  if (field->psi) cudaFree(field->psi);
+  delete field;
+  return ok();
+}
+
+static fe_status check_coupling(const fe_mesh* mesh, const fe_field* f, int64_t e0, int64_t e1) {
+  fe_status s = check_common(mesh, FE_FORM_DIVERGENCE, e0, e1);
+  if (s != FE_OK) return s;
+  if (!f) return fail(FE_ERR_INVALID_ARG, "pressure field is NULL");
+  if (f->mesh != mesh) return fail(FE_ERR_INVALID_ARG, "pressure field belongs to another mesh");
+  return FE_OK;
+}
+
+static fe_status coupling_status(cudaError_t e, const fe_mesh* mesh, const fe_field* f, const char* what) {
+  if (e == cudaErrorNotSupported)
+    return fail(FE_ERR_UNSUPPORTED, std::string(what) + ": pair (" + std::to_string(mesh->order) +
+                                        ", " + std::to_string(f->order) + ") not built");
+  if (e != cudaSuccess) return cuda_fail(e, what);
+  return ok();
+}
+
+fe_status fe_eval_coupling_matrices(const fe_mesh* mesh, const fe_field* pressure, int32_t transposed,
+                                    int64_t elem_begin, int64_t elem_end, double* out, void* stream) {
+  fe_status s = check_coupling(mesh, pressure, elem_begin, elem_end);
+  if (s != FE_OK) return s;
+  if (elem_end > elem_begin && !out) return fail(FE_ERR_INVALID_ARG, "out is NULL");
+  return coupling_status(feb200::launch_coupling(mesh, pressure, 0, transposed != 0, nullptr, nullptr,
+                                                 elem_begin, elem_end, out, nullptr, nullptr,
+                                                 (cudaStream_t)stream),
+                         mesh, pressure, "fe_eval_coupling_matrices");
+}
+
+fe_status fe_eval_coupling_residual(const fe_mesh* mesh, const fe_field* pressure, int32_t transposed,
+                                    const double* x, int64_t elem_begin, int64_t elem_end,
+                                    double* r_elem, double* r_global, void* stream) {
+  fe_status s = check_coupling(mesh, pressure, elem_begin, elem_end);
+  if (s != FE_OK) return s;
+  if (!x) return fail(FE_ERR_INVALID_ARG, "input vector is NULL");
+  const bool tr = transposed != 0;
+  return coupling_status(feb200::launch_coupling(mesh, pressure, 1, tr, tr ? x : nullptr, tr ? nullptr : x,
+                                                 elem_begin, elem_end, r_elem, r_global, nullptr,
+                                                 (cudaStream_t)stream),
+                         mesh, pressure, "fe_eval_coupling_residual");
+}
+
+fe_status fe_eval_coupling_scalar(const fe_mesh* mesh, const fe_field* pressure, const double* u,
+                                  const double* p, int64_t elem_begin, int64_t elem_end,
+                                  double* value, void* stream) {
+  fe_status s = check_coupling(mesh, pressure, elem_begin, elem_end);
+  if (s != FE_OK) return s;
+  if (!u || !p || !value) return fail(FE_ERR_INVALID_ARG, "u / p / value is NULL");
+  return coupling_status(feb200::launch_coupling(mesh, pressure, 2, false, u, p, elem_begin, elem_end,
+                                                 nullptr, nullptr, value, (cudaStream_t)stream),
+                         mesh, pressure, "fe_eval_coupling_scalar");
+}
+
 fe_status fe_assemble_vector(const fe_mesh* mesh, int32_t dtype, int32_t ncomp, int64_t elem_begin,
                              int64_t elem_end, const void* r_elem, void* r_global, void* stream) {
   fe_status s = check_common(mesh, FE_FORM_DIFFUSION, elem_begin, elem_end);

@@ -20,6 +20,16 @@ struct fe_mesh {
   double *b1 = nullptr, *d1 = nullptr, *x1 = nullptr, *w1 = nullptr;  // 1D tables
 };
 
+// A second (scalar) Lagrange space on the cells of a mesh (the pressure space of the Stokes
+// coupling forms): its own connectivity and its basis values at the mesh's quadrature points.
+struct fe_field {
+  int32_t order = 0, nb = 0;
+  int64_t n_elems = 0, n_nodes = 0;
+  const fe_mesh* mesh = nullptr;
+  int32_t* dof_conn = nullptr;  // [E][nb] device
+  double* psi = nullptr;        // [nq][nb] device
+};
+
 namespace feb200 {
 
 // Read-only view passed to kernels by value.
@@ -95,6 +105,9 @@ cudaError_t launch_geometry_materialize(const fe_mesh* m, double* detw, double* 
                                         cudaStream_t st);
 
 void count_launch();
+cudaError_t launch_coupling(const fe_mesh* mh, const fe_field* f, int mode, bool trans,
+                            const double* u, const double* p, int64_t e0, int64_t e1, double* out,
+                            double* rg, double* val, cudaStream_t st);
 cudaError_t launch_stress(const fe_mesh* m, MatArgs mat, const double* u, int64_t e0, int64_t e1,
                           double* sigma, cudaStream_t st);
 // Test hook: FEB200_MAX_CTAS caps the grid of the persistent kernels so that small meshes

@@ -493,3 +493,58 @@ def test_stress(kind, p):
     assert rel(sub.cpu().numpy(), ref[5:17]) <= TOL64
     empty = mesh.stress(dev(pr.u), *mat, elem_begin=3, elem_end=3)
     assert empty.shape[0] == 0
+
+
+# ---- N3: Stokes coupling pair -------------------------------------------------
+
+def _mixed(pv, pp, shape, seed):
+    mp = fi.make_mixed_problem(pv, pp, shape, seed)
+    mesh = gpu_mesh(mp.vel)
+    pf = fe().PressureField(mesh, pp, torch.from_numpy(mp.p_dof_conn), n_nodes=mp.n_p_nodes)
+    return mp, mesh, pf
+
+
+@pytest.mark.parametrize("pv,pp", [(1, 1), (2, 1), (2, 2), (3, 2), (4, 3)])
+def test_stokes_coupling(pv, pp):
+    """Matrix, residual (element + fused scatter) and eval modes of the Stokes coupling and
+    its transpose vs the oracle, ragged cell counts and a sub-range."""
+    shape = (5, 3, 4) if pv <= 2 else (3, 2, 3)
+    mp, mesh, pf = _mixed(pv, pp, shape, 17000 + 10 * pv + pp)
+    v = mp.vel
+    args = (pv, pp, pv + 1, v.coords, v.conn)
+    for tr in (False, True):
+        ref = oracle.coupling_matrix(*args, transposed=tr)
+        assert rel(pf.coupling_matrices(transposed=tr).cpu().numpy(), ref) <= TOL64
+        sub = pf.coupling_matrices(transposed=tr, elem_begin=3, elem_end=11)
+        assert rel(sub.cpu().numpy(), ref[3:11]) <= TOL64
+    u, p = dev(v.u), dev(mp.pres)
+    # Stokes coupling residual: input p, velocity-shaped output
+    rv_ref = oracle.coupling_residual(*args, v.dof_conn, mp.p_dof_conn, p=mp.pres)
+    re_, rg = pf.coupling_residual(p, want_elem=True)
+    assert rel(re_.cpu().numpy(), rv_ref) <= TOL64
+    assert rel(rg.cpu().numpy().ravel(), oracle.assemble(rv_ref, v.dof_conn, v.n_nodes, 3)) <= TOL64
+    # transposed: input u, pressure-shaped output
+    rq_ref = oracle.coupling_residual(*args, v.dof_conn, mp.p_dof_conn, u=v.u, transposed=True)
+    re_, rg = pf.coupling_residual(u, transposed=True, want_elem=True)
+    assert rel(re_.cpu().numpy(), rq_ref) <= TOL64
+    assert rel(rg.cpu().numpy(), oracle.assemble(rq_ref, mp.p_dof_conn, mp.n_p_nodes, 1)) <= TOL64
+    ev_ref = oracle.coupling_eval(*args, v.dof_conn, mp.p_dof_conn, v.u, mp.pres)
+    ev = pf.coupling_eval(u, p).item()
+    assert abs(ev - ev_ref) <= TOL64 * max(abs(ev_ref), 1.0)
+
+
+def test_stokes_coupling_errors():
+    m = fe()
+    mp, mesh, pf = _mixed(4, 1, (2, 2, 1), 5)          # (4, 1) pair not built
+    with pytest.raises(m.FEError) as ei:
+        pf.coupling_matrices()
+    assert ei.value.status == m.FE_ERR_UNSUPPORTED
+    with pytest.raises(m.FEError) as ei:                # pressure order above the mesh order
+        m.PressureField(gpu_mesh(fi.make_problem(fi.DIVERGENCE, 1, (2, 2, 1), 1)), 2,
+                        torch.from_numpy(mp.p_dof_conn))
+    assert ei.value.status == m.FE_ERR_INVALID_ARG
+    bad = torch.from_numpy(mp.p_dof_conn).clone()
+    bad[1, 2] = mp.n_p_nodes + 5                        # out of range
+    with pytest.raises(m.FEError) as ei:
+        m.PressureField(mesh, 1, bad, n_nodes=mp.n_p_nodes)
+    assert ei.value.status == m.FE_ERR_INVALID_ARG
