@@ -124,7 +124,8 @@ def alg_bytes(form: int, mode: str, p: int, nb: int, nq: int, D: int, mat_kind: 
         # row pointers are implementation overhead, not counted
         return (D * nb) ** 2 * 8 + 16 * csr_nnz_per_cell
     if form == fi.ELASTICITY:
-        mat = 2 * esize if mat_kind == fi.MAT_PER_ELEM else 2 * nq * esize
+        mat = (2 * esize if mat_kind == fi.MAT_PER_ELEM
+               else 36 * nq * esize if mat_kind == fi.MAT_FULL_D else 2 * nq * esize)
     elif form == fi.MASS_DIFFUSION:
         mat = 2 * nq * esize
     elif form == fi.CONVECTIVE:
@@ -171,12 +172,19 @@ WORKLOADS = {
     "C5t": dict(modes=("matrix",)),
     "C2csr": dict(modes=("matrix", "csr")),   # N2: element matrices + global CSR assembly
     "C3csr": dict(modes=("matrix", "csr")),
+    "C3d": dict(modes=("matrix", "residual")),  # N4: C3 with a general Voigt D[E][n_q][6][6]
 }
 
 
 def build_problem(name):
     if name == "C5t":
         return fi.corner_subproblem(fi.make_config("C5"), 64)
+    if name == "C3d":
+        c = fi.CONFIGS["C3"]
+        prob = fi.make_problem(c["form"], c["p"], (c["N"],) * 3, fi.SEED_BASE + c["index"],
+                               mat_kind=fi.MAT_FULL_D, name="C3d")
+        prob.meta["desc"] = c["desc"].replace("lambda,mu/elem U[0.5,2]", "D[E][27][6][6] SPD per qp")
+        return prob
     if name.endswith("csr"):
         return fi.make_config(name[:-3])
     return fi.make_config(name)
@@ -617,8 +625,7 @@ def main():
             fl = fl_lean
         elif mode == "matrix" and uses_sf_matrix(prob.form, prob.p):
             fl = sf_matrix_flops(prob.form, prob.p) * El
-        elif mode == "matrix" and prob.form in (fi.ELASTICITY, fi.CONVECTIVE) and prob.p == 2 and \
-                prob.mat_kind != fi.MAT_FULL_D:
+        elif mode == "matrix" and prob.form in (fi.ELASTICITY, fi.CONVECTIVE) and prob.p == 2:
             fl = sf_vector_matrix_flops(prob.form, prob.p) * El
             impl = "sum-factorised, pipelined"
         elif mode == "matrix":

@@ -191,6 +191,27 @@ fe_status fe_eval_scalar(const fe_mesh *mesh, int32_t form, int32_t dtype, const
 fe_status fe_eval_stress(const fe_mesh *mesh, const fe_material *mat, const double *u,
                          int64_t elem_begin, int64_t elem_end, double *sigma, void *stream);
 
+/* ---- Element-kind grouping ---------------------------
+ * One evaluation call covers cells of one kind (order); a p-/hp-mixed mesh is
+ * evaluated group by group.  fe_group_cells is a stable GPU sort of the cell
+ * ids by kind: perm (device int64 [n_cells], caller owned) lists the cells of
+ * kind 0 in ascending id order, then kind 1, ...; offsets (HOST int64
+ * [n_kinds + 1]) gives group g = perm[offsets[g] .. offsets[g+1]).  kind:
+ * device int32 [n_cells], values in [0, n_kinds) else FE_ERR_INVALID_ARG.
+ * Synchronises `stream` (offsets are returned on the host). */
+fe_status fe_group_cells(const int32_t *kind, int64_t n_cells, int32_t n_kinds, int64_t *perm,
+                         int64_t *offsets, void *stream);
+
+/* Gather rows in grouped order: out[i][j] = in[row_ptr[perm[i]] + j] for
+ * i < n, j < width (row_ptr NULL: fixed stride, in[perm[i] * width + j]).
+ * All pointers device; out caller owned [n][width].  Used for the per-group
+ * conn / dof_conn / material blocks of a mixed mesh (ragged per-cell arrays
+ * are addressed through row_ptr). */
+fe_status fe_gather_rows_i32(const int32_t *in, const int64_t *row_ptr, int32_t width,
+                             const int64_t *perm, int64_t n, int32_t *out, void *stream);
+fe_status fe_gather_rows_f64(const double *in, const int64_t *row_ptr, int32_t width,
+                             const int64_t *perm, int64_t n, double *out, void *stream);
+
 /* ---- Mixed velocity-pressure forms (Tab. 2) ----------------------
  * The mesh handle is the velocity space Q_pv (vector, D = 3, its dof_conn and
  * n_nodes); an fe_field is a scalar pressure space Q_pp on the same cells,

@@ -73,6 +73,9 @@ def _load():
     lib.fe_eval_coupling_matrices.argtypes = [P, P, i32, i64, i64, P, P]
     lib.fe_eval_coupling_residual.argtypes = [P, P, i32, P, i64, i64, P, P, P]
     lib.fe_eval_coupling_scalar.argtypes = [P, P, P, P, i64, i64, P, P]
+    lib.fe_group_cells.argtypes = [P, i64, i32, P, P, P]
+    lib.fe_gather_rows_i32.argtypes = [P, P, i32, P, i64, P, P]
+    lib.fe_gather_rows_f64.argtypes = [P, P, i32, P, i64, P, P]
     lib.fe_create_csr.argtypes = [P, i32, P, ctypes.POINTER(P)]
     lib.fe_csr_info.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     lib.fe_csr_arrays.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P)]
@@ -87,6 +90,7 @@ def _load():
               "fe_eval_element_matrices", "fe_eval_residual", "fe_assemble_vector",
               "fe_geometry", "fe_eval_scalar", "fe_eval_matrix_residual", "fe_eval_stress", "fe_create_field", "fe_destroy_field",
               "fe_eval_coupling_matrices", "fe_eval_coupling_residual", "fe_eval_coupling_scalar",
+              "fe_group_cells", "fe_gather_rows_i32", "fe_gather_rows_f64",
               "fe_create_csr", "fe_csr_info", "fe_csr_arrays",
               "fe_csr_copy_arrays",
               "fe_assemble_matrix", "fe_destroy_csr"):
@@ -113,6 +117,7 @@ ABI_SYMBOLS = ("fe_create_mesh_geometry", "fe_destroy_mesh", "fe_mesh_info",
                "fe_eval_matrix_residual", "fe_eval_stress",
                "fe_create_field", "fe_destroy_field", "fe_eval_coupling_matrices",
                "fe_eval_coupling_residual", "fe_eval_coupling_scalar",
+               "fe_group_cells", "fe_gather_rows_i32", "fe_gather_rows_f64",
                "fe_geometry", "fe_last_error", "fe_last_error_element", "fe_launch_count",
                "fe_create_csr", "fe_csr_info", "fe_csr_arrays", "fe_csr_copy_arrays",
                "fe_assemble_matrix", "fe_destroy_csr")
@@ -308,6 +313,87 @@ class PressureField:
             self.close()
         except Exception:
             pass
+
+
+def fe_group_cells(kind: torch.Tensor, n_kinds: int, stream=None):
+    """Stable grouping of cells by kind (GPU): (perm int64 device [E], offsets list [n_kinds+1])."""
+    kind = kind.to(dtype=torch.int32).contiguous()
+    perm = torch.empty(kind.numel(), dtype=torch.int64, device=kind.device)
+    offs = (ctypes.c_int64 * (n_kinds + 1))()
+    _check(_lib.fe_group_cells(_ptr(kind), kind.numel(), n_kinds, _ptr(perm), offs,
+                               _stream(stream)))
+    return perm, list(offs)
+
+
+def fe_gather_rows(src: torch.Tensor, width: int, perm: torch.Tensor, row_ptr=None, stream=None):
+    """out[i][j] = src[row_ptr[perm[i]] + j] (or src[perm[i] * width + j]); int32 or fp64."""
+    n = perm.numel()
+    out = torch.empty((n, width), dtype=src.dtype, device=src.device)
+    f = _lib.fe_gather_rows_i32 if src.dtype == torch.int32 else _lib.fe_gather_rows_f64
+    if src.dtype not in (torch.int32, torch.float64):
+        raise TypeError("fe_gather_rows: int32 or float64 only")
+    _check(f(_ptr(src), _ptr(row_ptr), width, _ptr(perm), n, _ptr(out), _stream(stream)))
+    return out
+
+
+class MixedMesh:
+    """A p-mixed hexahedral mesh evaluated group by group.
+
+    orders[E] (1..4) per cell; dof_ptr[E+1] / dof_idx: each cell's (order+1)^3 node ids
+    (CSR rows, lexicographic local order).  Cells are grouped by order with fe_group_cells;
+    each group is a Mesh of one order built from rows gathered by fe_gather_rows, and every
+    evaluation runs the single-kind kernels per group.  No conformity constraints between
+    orders are applied (the paper's setting has none)."""
+
+    def __init__(self, coords, conn, orders, dof_ptr, dof_idx, n_nodes: int, device="cuda",
+                 stream=None):
+        coords = _dev(coords, torch.float64, device)
+        conn = _dev(conn, torch.int32, device)
+        orders = _dev(orders, torch.int32, device)
+        dof_ptr = _dev(dof_ptr, torch.int64, device)
+        dof_idx = _dev(dof_idx, torch.int32, device)
+        self.device, self.n_nodes, self.n_elems = device, n_nodes, conn.shape[0]
+        self.perm, offs = fe_group_cells(orders - 1, 4, stream)
+        self.groups = []   # (order, begin, end, Mesh, perm slice)
+        for g in range(4):
+            b, e = offs[g], offs[g + 1]
+            if e <= b:
+                continue
+            p = g + 1
+            pg = self.perm[b:e]
+            cg = fe_gather_rows(conn, 8, pg, stream=stream)
+            dg = fe_gather_rows(dof_idx, (p + 1) ** 3, pg, row_ptr=dof_ptr, stream=stream)
+            m = Mesh(coords, cg, p, dof_conn=dg, n_nodes=n_nodes, device=device, stream=stream)
+            self.groups.append((p, b, e, m, pg))
+
+    def group_material(self, arr, row_ptr=None, stream=None):
+        """Per-group blocks of a per-cell array in original cell order: `arr` [E][w] fixed
+        width (row_ptr None), or ragged rows (e.g. per-qp values, (p+1)^3 per cell)."""
+        out = []
+        for p, b, e, m, pg in self.groups:
+            w = (p + 1) ** 3 if row_ptr is not None else arr.shape[1] if arr.dim() > 1 else 1
+            out.append(fe_gather_rows(arr.reshape(arr.shape[0], -1) if row_ptr is None else arr,
+                                      w, pg, row_ptr=row_ptr, stream=stream))
+        return out
+
+    def element_matrices(self, form, mat_kind=MAT_PER_QP, mats_a=None, mats_b=None, stream=None):
+        """List of per-group K blocks [E_g][D nb_g][D nb_g]; group g's cells are
+        perm[begin_g:end_g]."""
+        out = []
+        for i, (p, b, e, m, pg) in enumerate(self.groups):
+            out.append(m.element_matrices(form, mat_kind, None if mats_a is None else mats_a[i],
+                                          None if mats_b is None else mats_b[i], stream=stream))
+        return out
+
+    def residual(self, form, u, mat_kind=MAT_PER_QP, mats_a=None, mats_b=None, r_global=None,
+                 stream=None):
+        """Global residual: the per-group kernels scatter-add into one vector."""
+        if r_global is None:
+            r_global = torch.zeros((self.n_nodes, NCOMP[form]), dtype=u.dtype, device=self.device)
+        for i, (p, b, e, m, pg) in enumerate(self.groups):
+            m.residual(form, u, mat_kind, None if mats_a is None else mats_a[i],
+                       None if mats_b is None else mats_b[i], r_global=r_global, stream=stream)
+        return r_global
 
 
 class CSR:

@@ -23,7 +23,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC]
-SOURCES = ["fe_api.cpp", "tables.cpp", "k_misc.cu", "k_matrix.cu", "k_matrix_sf.cu", "k_matrix_sfv.cu", "k_matrix_vp.cu", "k_residual.cu", "k_residual_sf.cu", "k_residual_t3.cu", "k_csr.cu", "k_stress.cu", "k_coupling.cu"]
+SOURCES = ["fe_api.cpp", "tables.cpp", "k_misc.cu", "k_matrix.cu", "k_matrix_sf.cu", "k_matrix_sfv.cu", "k_matrix_vp.cu", "k_residual.cu", "k_residual_sf.cu", "k_residual_t3.cu", "k_csr.cu", "k_stress.cu", "k_coupling.cu", "k_group.cu"]
 
 
 def _sources():

@@ -129,6 +129,12 @@ __device__ __forceinline__ double hex_geometry(const double* __restrict__ xv, do
   return det;
 }
 
+// Bulk prefetch of a contiguous global range into L2 (TMA engine; one instruction, no
+// completion tracking).  p and bytes must be 16-byte multiples; the caller checks.
+__device__ __forceinline__ void l2_prefetch_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 template <typename T>
 __device__ __forceinline__ void atomic_add(T* p, T v) {
   atomicAdd(p, v);

@@ -86,12 +86,28 @@ __device__ __forceinline__ void qp_flux_m(const double (&uq)[FormD<FORM>::D],
     double sig[6];
     if (mat_kind == FE_MAT_FULL_D) {
       const T* Dm = mq.Dm;
+      if (sizeof(T) == 8 && (reinterpret_cast<uintptr_t>(Dm) & 15u) == 0) {
+        // 16-byte loads: a warp's 36 scalar loads of 288-byte-strided blocks would each touch
+        // 32 sectors for 8 useful bytes; pairs halve the sector re-fetches through L1
+        const double2* D2 = reinterpret_cast<const double2*>(Dm);
 #pragma unroll
-      for (int I = 0; I < 6; ++I) {
-        double s = 0.0;
+        for (int I = 0; I < 6; ++I) {
+          double s = 0.0;
 #pragma unroll
-        for (int K = 0; K < 6; ++K) s += (double)Dm[6 * I + K] * eps[K];
-        sig[I] = s;
+          for (int K2 = 0; K2 < 3; ++K2) {
+            const double2 d = __ldg(D2 + 3 * I + K2);
+            s += d.x * eps[2 * K2] + d.y * eps[2 * K2 + 1];
+          }
+          sig[I] = s;
+        }
+      } else {
+#pragma unroll
+        for (int I = 0; I < 6; ++I) {
+          double s = 0.0;
+#pragma unroll
+          for (int K = 0; K < 6; ++K) s += (double)Dm[6 * I + K] * eps[K];
+          sig[I] = s;
+        }
       }
     } else {
       const double lam = mq.a, mu = mq.b;

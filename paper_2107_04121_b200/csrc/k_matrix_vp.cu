@@ -25,6 +25,9 @@
 #include "fe_device.cuh"
 #include "fe_internal.h"
 #include "vp_tasks.h"
+#ifndef FEB200_VP_L2PF
+#define FEB200_VP_L2PF 1
+#endif
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -81,6 +84,9 @@ __device__ __forceinline__ void vp_named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 // unique pair u -> (m, n), m <= n; index 6 is the value-value pair (3,3)
+__host__ __device__ constexpr int vp_voigt(int a, int j) {
+  return a == j ? a : (a + j == 1 ? 3 : (a + j == 2 ? 4 : 5));
+}
 __host__ __device__ constexpr int vp_um(int u) { return (0x3211000 >> (4 * u)) & 0xF; }
 __host__ __device__ constexpr int vp_un(int u) { return (0x3221210 >> (4 * u)) & 0xF; }
 template <int I, int N, class F>
@@ -237,6 +243,11 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
       batch_of(j, lb, ne);
       if (ne <= 0) return;
       int32_t* ib = idxb + (j & 1) * E * (8 + NB);
+      if (FEB200_VP_L2PF && !L::CONV && mat_kind == FE_MAT_FULL_D && lane == 0) {  // D block of batch j -> L2
+        const double* gD = ma + (e0 + lb) * NQ * 36;
+        const uint32_t bD = (uint32_t)ne * NQ * 36u * 8u;
+        if (((reinterpret_cast<uintptr_t>(gD) | bD) & 15u) == 0) l2_prefetch_bulk(gD, bD);
+      }
       for (int i = lane; i < IDXN; i += 32) {
         const int c = i < E * 8 ? i / 8 : (i - E * 8) / NB;
         int v = 0;
@@ -267,7 +278,7 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
         for (int h = 0; h < MPL; ++h) {
           const int i = lane + 32 * h, c = i / NQ, q = i - c * NQ;
           double va = 0.0, vb = 0.0;
-          if (i < E * NQ && c < ne) {
+          if (i < E * NQ && c < ne && mat_kind != FE_MAT_FULL_D) {
             if (mat_kind == FE_MAT_PER_ELEM) {
               va = ma[e0 + lb + c];
               vb = mb[e0 + lb + c];
@@ -368,7 +379,46 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
         const double dw = on ? c_w1d[P][qx] * c_w1d[P][qy] * c_w1d[P][qz] * det : 0.0;
         // all pair weights W^{ab}_{mn}(q) of the batch, item-major: Wsm[el][PB(i) + p][q]
         double* Wq = Wsm + el * L::NWP * NQ + q;
-        if constexpr (!L::CONV) {
+        if (!L::CONV && mat_kind == FE_MAT_FULL_D) {
+          // general Voigt D (symmetric: upper triangle read, reading 23):
+          // W^{ab}_{mn} = dw sum_{j,l} Ji[m][j] D[v(a,j)][v(b,l)] Ji[n][l]
+          double Dm[36];
+          const double* Dg = ma + ((e0 + lb + el) * NQ + q) * 36;
+#pragma unroll
+          for (int i = 0; i < 36; ++i) Dm[i] = on ? __ldg(Dg + i) : 0.0;
+          auto Dv = [&](int a, int j, int b, int l) {
+            const int I = vp_voigt(a, j), Kk = vp_voigt(b, l);
+            return I <= Kk ? Dm[6 * I + Kk] : Dm[6 * Kk + I];
+          };
+          auto wblk = [&](int a, int b, double (&Wb)[3][3]) {
+            double R[3][3];  // R[j][n] = sum_l C_{ajbl} Ji[n][l]
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+              for (int n = 0; n < 3; ++n)
+                R[j][n] = Dv(a, j, b, 0) * Ji[3 * n] + Dv(a, j, b, 1) * Ji[3 * n + 1] + Dv(a, j, b, 2) * Ji[3 * n + 2];
+#pragma unroll
+            for (int m = 0; m < 3; ++m)
+#pragma unroll
+              for (int n = 0; n < 3; ++n)
+                Wb[m][n] = dw * (Ji[3 * m] * R[0][n] + Ji[3 * m + 1] * R[1][n] + Ji[3 * m + 2] * R[2][n]);
+          };
+#pragma unroll
+          for (int a2 = 0; a2 < 3; ++a2) {
+            double Wb[3][3];
+            wblk(a2, a2, Wb);
+#pragma unroll
+            for (int u = 0; u < 6; ++u) Wq[(6 * a2 + u) * NQ] = Wb[vp_um(u)][vp_un(u)];
+          }
+#pragma unroll
+          for (int ob = 0; ob < 3; ++ob) {
+            const int a2 = ob == 2 ? 1 : 0, b2 = ob == 0 ? 1 : 2;
+            double Wb[3][3];
+            wblk(a2, b2, Wb);
+#pragma unroll
+            for (int pp = 0; pp < 9; ++pp) Wq[(18 + 9 * ob + pp) * NQ] = Wb[pp / 3][pp % 3];
+          }
+        } else if constexpr (!L::CONV) {
           const double lam = slot[L::LS_A + el * NQ + q];  // per-cell material replicated per qp by L
           const double mu = slot[L::LS_B + el * NQ + q];
           // diagonal blocks (a,a), unique pairs m <= n: dw ((lam + mu) Ji[m][a] Ji[n][a] + mu (Ji Ji^T)_mn)
@@ -741,13 +791,14 @@ static cudaError_t launch_vp_t(const fe_mesh* mh, MatArgs mat, const double* sta
 }
 
 // Returns cudaErrorNotSupported when the combination has no pipelined vector kernel
-// (FULL_D elasticity, vector mass, p > 2: the single-stage k_matrix_sfv handles those).
+// (vector mass, weighted dot, p != 2: the single-stage k_matrix_sfv handles those; with
+// FEB200_MATRIX_IMPL=sf1 the general non-symmetric FULL_D path of k_matrix_sfv is used).
 cudaError_t launch_matrix_vp(const fe_mesh* mh, int form, MatArgs mat, const double* state_u,
                              int64_t e0, int64_t e1, double* K, cudaStream_t st) {
   if (mh->q1d != mh->order + 1 || mh->order != 2) return cudaErrorNotSupported;
   const char* impl = std::getenv("FEB200_MATRIX_IMPL");
   if (impl && std::strcmp(impl, "sf1") == 0) return cudaErrorNotSupported;
-  if (form == FE_FORM_ELASTICITY && mat.kind != FE_MAT_FULL_D)
+  if (form == FE_FORM_ELASTICITY)
     return launch_vp_t<2, FE_FORM_ELASTICITY>(mh, mat, state_u, e0, e1, K, st);
   if (form == FE_FORM_CONVECTIVE) return launch_vp_t<2, FE_FORM_CONVECTIVE>(mh, mat, state_u, e0, e1, K, st);
   return cudaErrorNotSupported;

@@ -71,6 +71,9 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 #ifndef FEB200_RSF_PADB
 #define FEB200_RSF_PADB (sizeof(T) == 8 ? 96 : 32)
 #endif
+#ifndef FEB200_RSF_L2PF
+#define FEB200_RSF_L2PF 0  // measured: 0.383 ms with, 0.360 ms without (C3d residual)
+#endif
 #ifndef FEB200_RSF_PADP
 #define FEB200_RSF_PADP 3
 #endif
@@ -182,6 +185,15 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
     const void* ga = ma + eb * nma;
     const void* gb = has_mb ? (const void*)(mb + eb * nma) : nullptr;
     auto al = [](const void* p, uint32_t n) { return ((reinterpret_cast<uintptr_t>(p) | n) & 15u) == 0; };
+    if constexpr (FORM == FE_FORM_ELASTICITY) {
+      // general D (7.8 KB per Q2 cell, read per qp through L1 by the flux): pull this batch's
+      // block into L2 two batches ahead
+      if (FEB200_RSF_L2PF && mat_kind == FE_MAT_FULL_D && tid == 0) {
+        const void* gD = ma + eb * NQ * 36;
+        const uint32_t bD = (uint32_t)ne * NQ * 36u * (uint32_t)sizeof(T);
+        if (al(gD, bD)) l2_prefetch_bulk(gD, bD);
+      }
+    }
     const bool ok = al(gc, bc) && al(gd, bd) && (nma == 0 || (al(ga, bm) && (!has_mb || al(gb, bm))));
     if (ok) {
       if (tid == 0) {

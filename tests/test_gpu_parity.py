@@ -548,3 +548,57 @@ def test_stokes_coupling_errors():
     with pytest.raises(m.FEError) as ei:
         m.PressureField(mesh, 1, bad, n_nodes=mp.n_p_nodes)
     assert ei.value.status == m.FE_ERR_INVALID_ARG
+
+
+# ---- N4: element-kind grouping ------------------------------------------------
+
+def test_group_cells():
+    m = fe()
+    rng = np.random.default_rng(5)
+    kind = rng.integers(0, 5, size=1001).astype(np.int32)
+    perm, offs = m.fe_group_cells(torch.from_numpy(kind).cuda(), 5)
+    ref = np.argsort(kind, kind="stable")
+    assert np.array_equal(perm.cpu().numpy(), ref)
+    assert offs == [0] + list(np.cumsum(np.bincount(kind, minlength=5)))
+    with pytest.raises(m.FEError):
+        m.fe_group_cells(torch.tensor([0, 7, 1], dtype=torch.int32).cuda(), 5)
+    p0, o0 = m.fe_group_cells(torch.zeros(0, dtype=torch.int32).cuda(), 3)
+    assert p0.numel() == 0 and o0 == [0, 0, 0, 0]
+
+
+def test_mixed_order_mesh():
+    """A p-mixed mesh (orders 1-3 per cell, each order's nodes on its own lattice): grouped
+    evaluation == the oracle on each group's cells; the global residual == the sum of the
+    groups' oracle scatters."""
+    m = fe()
+    shape = (4, 3, 3)
+    base = fi.make_problem(fi.DIFFUSION, 1, shape, 19000)
+    E = base.n_elems
+    rng = np.random.default_rng(19001)
+    orders = rng.integers(1, 4, size=E).astype(np.int32)
+    lat = {p: fi.lattice_dof_conn(*shape, p) for p in (1, 2, 3)}
+    off = {1: 0, 2: lat[1][1], 3: lat[1][1] + lat[2][1]}
+    n_nodes = off[3] + lat[3][1]
+    rows = [lat[p][0][e] + off[p] for e, p in enumerate(orders)]
+    dof_ptr = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    dof_idx = np.concatenate(rows).astype(np.int32)
+    kap_rows = [rng.uniform(1, 2, size=(p + 1) ** 3) for p in orders]
+    kap = torch.from_numpy(np.concatenate(kap_rows)).cuda()
+    u = rng.uniform(-1, 1, size=(n_nodes, 1))
+    mm = m.MixedMesh(base.coords, base.conn, orders, dof_ptr, dof_idx, n_nodes)
+    mats = mm.group_material(kap, row_ptr=torch.from_numpy(dof_ptr).cuda())
+    Ks = mm.element_matrices(fi.DIFFUSION, fi.MAT_PER_QP, mats)
+    R = mm.residual(fi.DIFFUSION, dev(u), fi.MAT_PER_QP, mats).cpu().numpy().ravel()
+    R_ref = np.zeros(n_nodes)
+    perm = mm.perm.cpu().numpy()
+    assert np.array_equal(perm, np.argsort(orders, kind="stable"))
+    for (p, b, e, _, _), K in zip(mm.groups, Ks):
+        cells = perm[b:e]
+        assert np.all(orders[cells] == p)
+        dc = np.stack([rows[c] for c in cells]).astype(np.int32)
+        ka = np.stack([kap_rows[c] for c in cells])
+        Kref = oracle.eval_matrix(fi.DIFFUSION, p, p + 1, base.coords, base.conn[cells], dc, 0, ka)
+        assert rel(K.cpu().numpy(), Kref) <= TOL64
+        r = oracle.eval_residual(fi.DIFFUSION, p, p + 1, base.coords, base.conn[cells], dc, u, 0, ka)
+        R_ref = oracle.assemble(r, dc, n_nodes, 1, R_ref)
+    assert rel(R, R_ref) <= TOL64
