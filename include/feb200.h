@@ -88,7 +88,10 @@ typedef enum { FE_F64 = 0, FE_F32 = 1 } fe_dtype;
  *   ELASTICITY      PER_ELEM: a = lambda[E], b = mu[E];
  *                   PER_QP:   a = lambda[E][n_q], b = mu[E][n_q];
  *                   FULL_D:   a = D[E][n_q][6][6] (Voigt xx,yy,zz,xy,xz,yz,
- *                             engineering shears; 'cqIK' operand)
+ *                             engineering shears; 'cqIK' operand);
+ *                             symmetric (major symmetry of the elasticity
+ *                             tensor, reading 23): the pipelined Q2
+ *                             matrix kernel reads its upper triangle only
  *   CONVECTIVE      unused (kind ignored)                                  */
 typedef enum { FE_MAT_PER_QP = 0, FE_MAT_PER_ELEM = 1, FE_MAT_FULL_D = 2 } fe_material_kind;
 
