@@ -28,9 +28,6 @@
 #ifndef FEB200_SFP
 #define FEB200_SFP 1
 #endif
-#ifndef FEB200_SFP_TASKMAP
-#define FEB200_SFP_TASKMAP 1
-#endif
 #ifndef FEB200_SFP_T1PAD
 #define FEB200_SFP_T1PAD 13
 #endif
@@ -427,7 +424,6 @@ struct SFP {
   static constexpr int NX = (E * TPE + 31) / 32;           // X warps
   static constexpr int THREADS = 32 * (1 + NG + NX);
   static constexpr int QQP = (Q2 + 1) / 2 * 2;
-  static constexpr bool TASKMAP = FEB200_SFP_TASKMAP && P == 2 && E == 8;
   // shared memory (bytes)
   static constexpr size_t LSLOT = size_t(E) * (24 + (NUPMAX == 7 ? 2 : 1) * NQ) * 8;  // coords, coef a[, b]
   // per-cell T1 stride padded by T1PAD doubles (an odd pad makes the G threads' column stores
@@ -817,12 +813,7 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
     }
     const bool xact = xtid < E * L::TPE;
     int iz = 0, jz = 0, iy = 0, jy = 0;
-    if constexpr (L::TASKMAP) {
-      // bank-conflict-optimised lane -> task permutation (tools/gen_sfp_tasks.py); keeps the
-      // off-diagonal tasks before the diagonal ones, so warps stay uniform
-      const int pk = xact ? sfp_tasks_e8[xtid] : 0;
-      yx_el = pk & 15; iz = (pk >> 4) & 15; jz = (pk >> 8) & 15; iy = (pk >> 12) & 15; jy = (pk >> 16) & 15;
-    } else if (yx_r < L::TOFF) {
+    if (yx_r < L::TOFF) {
       int c = yx_r / L::YP;
       const int yp = yx_r - c * L::YP;
       iy = yp / N1;
