@@ -602,3 +602,45 @@ def test_mixed_order_mesh():
         r = oracle.eval_residual(fi.DIFFUSION, p, p + 1, base.coords, base.conn[cells], dc, u, 0, ka)
         R_ref = oracle.assemble(r, dc, n_nodes, 1, R_ref)
     assert rel(R, R_ref) <= TOL64
+
+
+@pytest.mark.parametrize("ctas", [1, 3])
+def test_n3_n4_many_batches_per_cta(ctas, monkeypatch):
+    """Grid caps force many batches per CTA through the N3 / N4 kernels (weighted-dot matrix,
+    FULL_D pipelined matrix and its D prefetch, divergence residual, stress, Stokes coupling)."""
+    monkeypatch.setenv("FEB200_MAX_CTAS", str(ctas))
+    pr = fi.make_problem(fi.WEIGHTED_DOT, 2, (5, 4, 3), 18000)
+    mesh = gpu_mesh(pr)
+    K = mesh.element_matrices(fi.WEIGHTED_DOT, pr.mat_kind, dev(pr.mat_a))
+    assert rel(K.cpu().numpy(), oracle.problem_matrix(pr)) <= TOL64
+    pe = fi.make_problem(fi.ELASTICITY, 2, (5, 4, 3), 18001, mat_kind=fi.MAT_FULL_D)
+    me = gpu_mesh(pe)
+    K = me.element_matrices(fi.ELASTICITY, fi.MAT_FULL_D, dev(pe.mat_a))
+    assert rel(K.cpu().numpy(), oracle.problem_matrix(pe)) <= TOL64
+    re_, _ = me.residual(fi.ELASTICITY, dev(pe.u), fi.MAT_FULL_D, dev(pe.mat_a), want_elem=True)
+    assert rel(re_.cpu().numpy(), oracle.problem_residual(pe)) <= TOL64
+    sig = me.stress(dev(pe.u), fi.MAT_FULL_D, dev(pe.mat_a))
+    assert rel(sig.cpu().numpy(), oracle.problem_stress(pe)) <= TOL64
+    pd = fi.make_problem(fi.DIVERGENCE, 2, (5, 4, 3), 18002)
+    md = gpu_mesh(pd)
+    re_, _ = md.residual(fi.DIVERGENCE, dev(pd.u), want_elem=True)
+    assert rel(re_.cpu().numpy(), oracle.problem_residual(pd)) <= TOL64
+    mp, mesh2, pf = _mixed(2, 1, (5, 4, 3), 18003)
+    v = mp.vel
+    ref = oracle.coupling_matrix(2, 1, 3, v.coords, v.conn)
+    assert rel(pf.coupling_matrices().cpu().numpy(), ref) <= TOL64
+
+
+def test_full_d_config_sampled():
+    """C3d (N4 bench workload: C3 with D[E][27][6][6]) at full size, in bench.py's launch
+    configuration: sampled element matrices and residuals vs the oracle cell by cell."""
+    import bench
+    pr = bench.build_problem("C3d")
+    mesh = gpu_mesh(pr)
+    a = dev(pr.mat_a)
+    K = mesh.element_matrices(fi.ELASTICITY, fi.MAT_FULL_D, a)
+    re_, _ = mesh.residual(fi.ELASTICITY, dev(pr.u), fi.MAT_FULL_D, a, want_elem=True)
+    idx = np.random.default_rng(7).choice(pr.n_elems, 24, replace=False)
+    sub = _sample_subproblem(pr, idx)
+    assert rel(K[torch.from_numpy(idx).cuda()].cpu().numpy(), oracle.problem_matrix(sub)) <= TOL64
+    assert rel(re_[torch.from_numpy(idx).cuda()].cpu().numpy(), oracle.problem_residual(sub)) <= TOL64
