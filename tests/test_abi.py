@@ -53,3 +53,26 @@ def test_product_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "fe_oracle" not in txt, f
+
+
+def test_new_entry_points_validate_on_host():
+    """N3 / N4 entry points reject bad arguments before touching the device."""
+    import paper_2107_04121_b200 as fe
+    lib = fe.lib()
+    INV = fe.FE_ERR_INVALID_ARG
+    assert lib.fe_eval_stress(None, None, None, 0, 0, None, None) == INV
+    out = ctypes.c_void_p()
+    assert lib.fe_create_field(None, 1, 8, None, None, ctypes.byref(out)) == INV
+    assert lib.fe_create_field(None, 1, 8, None, None, None) == INV
+    assert lib.fe_destroy_field(None) == fe.FE_OK
+    assert lib.fe_eval_coupling_matrices(None, None, 0, 0, 0, None, None) == INV
+    assert lib.fe_eval_coupling_residual(None, None, 0, None, 0, 0, None, None, None) == INV
+    assert lib.fe_eval_coupling_scalar(None, None, None, None, 0, 0, None, None) == INV
+    offs = (ctypes.c_int64 * 3)()
+    assert lib.fe_group_cells(None, 5, 2, None, offs, None) == INV      # NULL kind
+    assert lib.fe_group_cells(None, 0, 0, None, offs, None) == INV      # no kinds
+    assert lib.fe_group_cells(None, 0, 2, None, offs, None) == fe.FE_OK  # empty: offsets zero
+    assert list(offs) == [0, 0, 0]
+    assert lib.fe_gather_rows_f64(None, None, 3, None, 4, None, None) == INV
+    assert lib.fe_gather_rows_i32(None, None, 3, None, -1, None, None) == INV
+    assert lib.fe_gather_rows_i32(None, None, 3, None, 0, None, None) == fe.FE_OK
