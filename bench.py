@@ -342,6 +342,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                    help="N > 1 residual: interface planes by NCCL send/recv overlapped with the "
+                         "interior (default) or added by the residual kernel itself into the "
+                         "neighbours' vectors over peer memory (fe_eval_residual_peer)")
     ap.add_argument("--fused", action="store_true",
                     help="C2-type steps: fe_eval_matrix_residual (K_e and r_e = K_e u_e from one "
                          "pass) instead of the separate matrix and residual kernels")
@@ -398,7 +402,15 @@ def main():
     u_loc = np.ascontiguousarray(prob.u[sl.node_begin:sl.node_end])
     u = torch.from_numpy(u_loc).to(dev, tdt)
     K = torch.empty((El, D * nb, D * nb), dtype=torch.float64, device=dev) if "matrix" in modes else None
-    r = torch.zeros((sl.n_nodes, D), dtype=tdt, device=dev)
+    peer = None
+    if world > 1 and args.exchange == "peer" and "residual" in modes and not fused:
+        if args.dtype != "f64":
+            raise SystemExit("--exchange peer is built for fp64 residuals")
+        peer = slabs.PeerExchange(sl, prob.shape, prob.p, D, dev)
+        r = peer.r
+        tiny = torch.zeros(1, dtype=torch.float32, device=dev)
+    else:
+        r = torch.zeros((sl.n_nodes, D), dtype=tdt, device=dev)
     csr = fe.CSR(mesh, D) if "csr" in modes else None
     csr_vals = torch.zeros(csr.nnz, dtype=torch.float64, device=dev) if csr is not None else None
     stream = torch.cuda.current_stream(dev)
@@ -436,7 +448,20 @@ def main():
             csr.assemble(K, values=csr_vals, stream=stream)
             if record:
                 b = torch.cuda.Event(enable_timing=True); b.record(stream); ev["csr"].append((a, b))
-        if "residual" in modes:
+        if "residual" in modes and peer is not None:
+            if record:
+                a = torch.cuda.Event(enable_timing=True); a.record(stream)
+
+            def evaluate_peer(windows):
+                fe.fe_eval_residual_peer(mesh.handle, prob.form, prob.mat_kind, mat_a, mat_b, u, 0,
+                                         El, None, r, windows, stream)
+
+            # zero -> device barrier (tiny NCCL all-reduce) -> fused residual + exchange over
+            # peer memory -> device barrier
+            peer.residual(evaluate_peer, lambda: dist.all_reduce(tiny))
+            if record:
+                b = torch.cuda.Event(enable_timing=True); b.record(stream); ev["residual"].append((a, b))
+        elif "residual" in modes:
             r.zero_()
             if record:
                 a = torch.cuda.Event(enable_timing=True); a.record(stream)
@@ -680,7 +705,7 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": cfg, "desc": prob.meta.get("desc", ""), "cells": prob.n_elems,
                    "order": prob.p, "q1d": prob.q1d, "form": fi.FORM_NAMES[prob.form],
-                   "modes": list(modes), "parallelism": f"z-slabs x{world}",
+                   "modes": list(modes), "parallelism": f"z-slabs x{world}", "exchange": (args.exchange if world > 1 else None),
                    "l2": "no flush: every step writes/reads > L2 (C2 K = 1.53 GB)"},
         "modes": {m: {"kernel_ms": kern_ms[m], "cells_per_s": El / (kern_ms[m] * 1e-3),
                       "roofline": {k: rooflines[m][k] for k in ("bound", "achieved", "unit", "frac")}}

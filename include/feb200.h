@@ -157,6 +157,37 @@ fe_status fe_eval_residual(const fe_mesh *mesh, int32_t form, int32_t dtype,
                            const fe_material *mat, const void *u, int64_t elem_begin,
                            int64_t elem_end, void *r_elem, void *r_global, void *stream);
 
+/* ---- Fused residual + interface-plane exchange over peer memory ----
+ * Residual mode (FE_F64, the sum-factorised kernels) whose fused scatter also adds
+ * the contribution to every node n in a window's [node_begin, node_end) at
+ * dst[(n - node_begin + dst_node_offset) * D + a] with system-scope fp64 atomics.
+ * dst is any device pointer valid in the caller's context -- typically the
+ * neighbouring rank's residual vector opened with fe_ipc_open (NVLink peer
+ * memory), so the z-slab interface planes are summed inside the residual
+ * kernel with no separate collective.  The caller orders the ranks: every
+ * rank's r_global is zeroed before any rank's kernel starts, and no rank reads
+ * its vector before every rank's kernel has finished (a device-side barrier).
+ * 0..2 windows; FE_ERR_UNSUPPORTED with FEB200_RESIDUAL_IMPL=dense. */
+typedef struct {
+  int64_t node_begin, node_end;   /* local node range of the window */
+  double *dst;                    /* device (or peer-mapped) vector [..][D] */
+  int64_t dst_node_offset;        /* node index in dst of node_begin */
+} fe_peer_window;
+fe_status fe_eval_residual_peer(const fe_mesh *mesh, int32_t form, const fe_material *mat,
+                                const double *u, int64_t elem_begin, int64_t elem_end,
+                                double *r_elem, double *r_global, const fe_peer_window *windows,
+                                int32_t n_windows, void *stream);
+
+/* CUDA IPC helpers for the peer windows: fe_ipc_alloc allocates `bytes` of
+ * device memory on the current device (cudaMalloc) and returns its 64-byte IPC
+ * handle; fe_ipc_open maps another process's handle into this process (peer
+ * access enabled lazily; the same device or an NVLink peer); fe_ipc_close /
+ * fe_ipc_free release them. */
+fe_status fe_ipc_alloc(int64_t bytes, void **dev_ptr, unsigned char handle[64]);
+fe_status fe_ipc_free(void *dev_ptr);
+fe_status fe_ipc_open(const unsigned char handle[64], void **dev_ptr);
+fe_status fe_ipc_close(void *dev_ptr);
+
 /* Matrix mode and residual mode of a LINEAR scalar form (DIFFUSION, MASS,
  * MASS_DIFFUSION; order 1 or 2) in ONE pass: the element matrices K as in
  * fe_eval_element_matrices, and from the same K_e the residual r_e = K_e u_e

@@ -42,6 +42,11 @@ class fe_material(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("a", ctypes.c_void_p), ("b", ctypes.c_void_p)]
 
 
+class fe_peer_window(ctypes.Structure):
+    _fields_ = [("node_begin", ctypes.c_int64), ("node_end", ctypes.c_int64),
+                ("dst", ctypes.c_void_p), ("dst_node_offset", ctypes.c_int64)]
+
+
 class fe_info(ctypes.Structure):
     _fields_ = [("order", ctypes.c_int32), ("q1d", ctypes.c_int32), ("nb", ctypes.c_int32),
                 ("nq", ctypes.c_int32), ("n_vertices", ctypes.c_int64),
@@ -76,6 +81,12 @@ def _load():
     lib.fe_group_cells.argtypes = [P, i64, i32, P, P, P]
     lib.fe_gather_rows_i32.argtypes = [P, P, i32, P, i64, P, P]
     lib.fe_gather_rows_f64.argtypes = [P, P, i32, P, i64, P, P]
+    lib.fe_eval_residual_peer.argtypes = [P, i32, ctypes.POINTER(fe_material), P, i64, i64, P, P,
+                                          ctypes.POINTER(fe_peer_window), i32, P]
+    lib.fe_ipc_alloc.argtypes = [i64, ctypes.POINTER(P), ctypes.c_char_p]
+    lib.fe_ipc_free.argtypes = [P]
+    lib.fe_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(P)]
+    lib.fe_ipc_close.argtypes = [P]
     lib.fe_create_csr.argtypes = [P, i32, P, ctypes.POINTER(P)]
     lib.fe_csr_info.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     lib.fe_csr_arrays.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P)]
@@ -91,6 +102,7 @@ def _load():
               "fe_geometry", "fe_eval_scalar", "fe_eval_matrix_residual", "fe_eval_stress", "fe_create_field", "fe_destroy_field",
               "fe_eval_coupling_matrices", "fe_eval_coupling_residual", "fe_eval_coupling_scalar",
               "fe_group_cells", "fe_gather_rows_i32", "fe_gather_rows_f64",
+              "fe_eval_residual_peer", "fe_ipc_alloc", "fe_ipc_free", "fe_ipc_open", "fe_ipc_close",
               "fe_create_csr", "fe_csr_info", "fe_csr_arrays",
               "fe_csr_copy_arrays",
               "fe_assemble_matrix", "fe_destroy_csr"):
@@ -118,6 +130,7 @@ ABI_SYMBOLS = ("fe_create_mesh_geometry", "fe_destroy_mesh", "fe_mesh_info",
                "fe_create_field", "fe_destroy_field", "fe_eval_coupling_matrices",
                "fe_eval_coupling_residual", "fe_eval_coupling_scalar",
                "fe_group_cells", "fe_gather_rows_i32", "fe_gather_rows_f64",
+               "fe_eval_residual_peer", "fe_ipc_alloc", "fe_ipc_free", "fe_ipc_open", "fe_ipc_close",
                "fe_geometry", "fe_last_error", "fe_last_error_element", "fe_launch_count",
                "fe_create_csr", "fe_csr_info", "fe_csr_arrays", "fe_csr_copy_arrays",
                "fe_assemble_matrix", "fe_destroy_csr")
@@ -208,6 +221,55 @@ def fe_eval_residual(handle: int, form: int, dtype: int, mat_kind: int,
     m = _material(mat_kind, mat_a, mat_b)
     _check(_lib.fe_eval_residual(handle, form, dtype, ctypes.byref(m), _ptr(u), elem_begin,
                                  elem_end, _ptr(r_elem), _ptr(r_global), _stream(stream)))
+
+
+def fe_eval_residual_peer(handle: int, form: int, mat_kind: int, mat_a, mat_b, u: torch.Tensor,
+                          elem_begin: int, elem_end: int, r_elem, r_global, windows, stream=None):
+    """C-ABI fe_eval_residual_peer: fp64 residual whose fused scatter also adds the nodes of up
+    to two windows [(node_begin, node_end, dst_ptr, dst_node_offset), ...] into dst (peer memory
+    of a neighbouring rank: the z-slab interface exchange inside the residual kernel)."""
+    m = _material(mat_kind, mat_a, mat_b)
+    arr = (fe_peer_window * 2)()
+    for i, (lo, hi, dst, off) in enumerate(windows):
+        arr[i] = fe_peer_window(lo, hi, dst, off)
+    _check(_lib.fe_eval_residual_peer(handle, form, ctypes.byref(m), _ptr(u), elem_begin, elem_end,
+                                      _ptr(r_elem), _ptr(r_global), arr, len(windows),
+                                      _stream(stream)))
+
+
+class IpcVector:
+    """A device fp64 vector allocated with fe_ipc_alloc (shareable with other processes through
+    its 64-byte handle); `tensor` views it as a torch tensor (CUDA array interface)."""
+
+    def __init__(self, shape, device="cuda"):
+        n = 1
+        for s in shape:
+            n *= s
+        ptr = ctypes.c_void_p()
+        handle = ctypes.create_string_buffer(64)
+        with torch.cuda.device(device):
+            _check(_lib.fe_ipc_alloc(8 * n, ctypes.byref(ptr), handle))
+        self.ptr, self.handle, self.shape = ptr.value, handle.raw, tuple(shape)
+        self.__cuda_array_interface__ = {"shape": self.shape, "typestr": "<f8",
+                                         "data": (self.ptr, False), "version": 3, "strides": None}
+        self.tensor = torch.as_tensor(self, device=device)
+
+    def close(self):
+        if getattr(self, "ptr", None):
+            self.tensor = None
+            _lib.fe_ipc_free(self.ptr)
+            self.ptr = None
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map another process's fe_ipc_alloc buffer; returns the device pointer."""
+    ptr = ctypes.c_void_p()
+    _check(_lib.fe_ipc_open(handle, ctypes.byref(ptr)))
+    return ptr.value
+
+
+def ipc_close(ptr: int):
+    _check(_lib.fe_ipc_close(ptr))
 
 
 def fe_eval_matrix_residual(handle: int, form: int, dtype: int, mat_kind: int, mat_a, mat_b, u,

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <new>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -91,6 +92,7 @@ fe_status check_material(int form, const fe_material* mat) {
 }  // namespace
 
 namespace feb200 {
+thread_local PeerWin g_peer{};
 // error setter shared with the other ABI units (k_csr.cu)
 fe_status set_error(fe_status s, const char* msg) {
   if (s == FE_OK) return ok();
@@ -288,6 +290,72 @@ fe_status fe_eval_residual(const fe_mesh* mesh, int32_t form, int32_t dtype, con
                                         " / dtype " + std::to_string(dtype) + " at order " +
                                         std::to_string(mesh->order));
   if (e != cudaSuccess) return cuda_fail(e, "fe_eval_residual");
+  return ok();
+}
+
+fe_status fe_eval_residual_peer(const fe_mesh* mesh, int32_t form, const fe_material* mat,
+                                const double* u, int64_t elem_begin, int64_t elem_end,
+                                double* r_elem, double* r_global, const fe_peer_window* windows,
+                                int32_t n_windows, void* stream) {
+  if (n_windows < 0 || n_windows > 2 || (n_windows > 0 && !windows))
+    return fail(FE_ERR_INVALID_ARG, "fe_eval_residual_peer: 0..2 windows");
+  const char* impl = std::getenv("FEB200_RESIDUAL_IMPL");
+  if (impl && std::strcmp(impl, "dense") == 0)
+    return fail(FE_ERR_UNSUPPORTED, "fe_eval_residual_peer: not built for the dense residual kernels");
+  feb200::PeerWin pw{};
+  pw.n = n_windows;
+  for (int w = 0; w < n_windows; ++w) {
+    const fe_peer_window& x = windows[w];
+    if (!x.dst || x.node_begin < 0 || x.node_end < x.node_begin || x.dst_node_offset < 0)
+      return fail(FE_ERR_INVALID_ARG, "fe_eval_residual_peer: bad window");
+    pw.lo[w] = x.node_begin;
+    pw.hi[w] = x.node_end;
+    pw.off[w] = x.dst_node_offset;
+    pw.dst[w] = x.dst;
+  }
+  feb200::g_peer = pw;
+  const fe_status s = fe_eval_residual(mesh, form, FE_F64, mat, u, elem_begin, elem_end, r_elem,
+                                       r_global, stream);
+  feb200::g_peer = feb200::PeerWin{};
+  return s;
+}
+
+fe_status fe_ipc_alloc(int64_t bytes, void** dev_ptr, unsigned char handle[64]) {
+  if (!dev_ptr || !handle || bytes <= 0) return fail(FE_ERR_INVALID_ARG, "fe_ipc_alloc: bad argument");
+  *dev_ptr = nullptr;
+  cudaError_t e = cudaMalloc(dev_ptr, (size_t)bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "fe_ipc_alloc");
+  cudaIpcMemHandle_t h;
+  e = cudaIpcGetMemHandle(&h, *dev_ptr);
+  if (e != cudaSuccess) {
+    cudaFree(*dev_ptr);
+    *dev_ptr = nullptr;
+    return cuda_fail(e, "fe_ipc_alloc: cudaIpcGetMemHandle");
+  }
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  std::memcpy(handle, &h, 64);
+  return ok();
+}
+
+fe_status fe_ipc_free(void* dev_ptr) {
+  if (dev_ptr) cudaFree(dev_ptr);
+  return ok();
+}
+
+fe_status fe_ipc_open(const unsigned char handle[64], void** dev_ptr) {
+  if (!handle || !dev_ptr) return fail(FE_ERR_INVALID_ARG, "fe_ipc_open: bad argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e, "fe_ipc_open");
+  return ok();
+}
+
+fe_status fe_ipc_close(void* dev_ptr) {
+  if (dev_ptr) {
+    cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+    if (e != cudaSuccess) return cuda_fail(e, "fe_ipc_close");
+  }
   return ok();
 }
 

@@ -55,6 +55,25 @@ inline MeshView view_of(const fe_mesh* m) {
                   m->fwd, m->bwd, m->fwd_f, m->bwd_f, m->b1, m->d1};
 }
 
+// Peer scatter windows of the fused residual + interface exchange (fe_eval_residual_peer,
+// DESIGN.md 9): a scattered node n in [lo, hi) is also added (system-scope fp64 atomics,
+// NVLink peer memory or any device pointer) at dst[(n - lo + off) * D + a].
+struct PeerWin {
+  int n;
+  int64_t lo[2], hi[2], off[2];
+  double* dst[2];
+};
+// set by fe_eval_residual_peer around the launch (per host thread)
+extern thread_local PeerWin g_peer;
+
+template <int D>
+__device__ __forceinline__ void peer_scatter(const PeerWin& pw, int64_t n, int a, double v) {
+#pragma unroll
+  for (int w = 0; w < 2; ++w)
+    if (w < pw.n && n >= pw.lo[w] && n < pw.hi[w])
+      atomicAdd_system(pw.dst[w] + (n - pw.lo[w] + pw.off[w]) * D + a, v);
+}
+
 struct MatArgs {
   int kind;
   const void* a;

@@ -131,11 +131,11 @@ struct RSF {
                                 FORM == FE_FORM_ELASTICITY || FORM == FE_FORM_DIVERGENCE;
 };
 
-template <int P, int FORM, typename T>
+template <int P, int FORM, typename T, bool PEER = false>
 __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MINB)
     k_residual_sf(MeshView mv, int mat_kind, const T* __restrict__ ma, const T* __restrict__ mb,
                   const T* __restrict__ u, int64_t e0, int64_t e1, T* __restrict__ r_elem,
-                  T* __restrict__ r_global, double* __restrict__ eval_out) {
+                  T* __restrict__ r_global, double* __restrict__ eval_out, PeerWin pw) {
   using L = RSF<P, FORM, T>;
   constexpr int N1 = L::N1, Q1 = L::Q1, NB = L::NB, NQ = L::NQ, D = L::D, EB = L::EB;
   constexpr int Q2 = Q1 * Q1;
@@ -524,6 +524,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
           const int k = tx + N1 * ty + N1 * N1 * kz;
           if (r_elem) r_elem[(e - e0) * (int64_t)(D * NB) + a * NB + k] = v;
           if (r_global) atomicAdd(r_global + (int64_t)dcol[kz] * D + a, v);
+          if constexpr (PEER) peer_scatter<D>(pw, dcol[kz], a, (double)v);
           if (eval_out) ev = fma((double)s, (double)uc[a][kz], ev);
         }
     }
@@ -545,7 +546,11 @@ template <int P, int FORM, typename T>
 static cudaError_t launch_rsf_t(const fe_mesh* mh, MatArgs mat, const T* u, int64_t e0, int64_t e1,
                                 T* r_elem, T* r_global, double* eval_out, cudaStream_t st) {
   using L = RSF<P, FORM, T>;
+  const PeerWin pw = g_peer;
   auto kern = k_residual_sf<P, FORM, T>;
+  if constexpr (sizeof(T) == 8) {
+    if (pw.n > 0) kern = k_residual_sf<P, FORM, T, true>;
+  }
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
   if (err != cudaSuccess) return err;
   int nsm = 148, per_sm = 1, dev = 0;
@@ -558,7 +563,7 @@ static cudaError_t launch_rsf_t(const fe_mesh* mh, MatArgs mat, const T* u, int6
   grid = grid_cap(grid);
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, L::THREADS, L::BYTES, st>>>(view_of(mh), mat.kind, (const T*)mat.a, (const T*)mat.b,
-                                           u, e0, e1, r_elem, r_global, eval_out);
+                                           u, e0, e1, r_elem, r_global, eval_out, pw);
   count_launch();
   return cudaGetLastError();
 }

@@ -44,11 +44,11 @@ cudaError_t upload_const_tables_residual_t3(int order, const double* b1, const d
   return upload_tables_this_tu(order, b1, d1, x1, w1, st);
 }
 
-template <int FORM, bool EVAL>
+template <int FORM, bool EVAL, bool PEER = false>
 __global__ void __launch_bounds__(FEB200_T3_THREADS, FEB200_T3_MINB)
     k_residual_t3(MeshView mv, const double* __restrict__ ma, const double* __restrict__ mb,
                   const double* __restrict__ u, int64_t e0, int64_t e1, double* __restrict__ r_elem,
-                  double* __restrict__ r_global, double* __restrict__ eval_out) {
+                  double* __restrict__ r_global, double* __restrict__ eval_out, PeerWin pw) {
   constexpr int P = 2, N = 3, NB = 27, NQ = 27;
   constexpr bool VAL = FORM == FE_FORM_MASS || FORM == FE_FORM_MASS_DIFFUSION;
   constexpr bool GRAD = FORM != FE_FORM_MASS;
@@ -330,6 +330,7 @@ __global__ void __launch_bounds__(FEB200_T3_THREADS, FEB200_T3_MINB)
         if (valid) {
           if (r_elem) r_elem[le * NB + kx + N * ky + N * N * j] = rr;
           if (r_global) atomicAdd(r_global + dof[ky][kx], rr);
+          if constexpr (PEER) peer_scatter<1>(pw, dof[ky][kx], 0, rr);
           if (EVAL) ev = fma(rr, u[dof[ky][kx]], ev);
         }
       }
@@ -348,7 +349,9 @@ __global__ void __launch_bounds__(FEB200_T3_THREADS, FEB200_T3_MINB)
 template <int FORM>
 static cudaError_t launch_t3_t(const fe_mesh* mh, MatArgs mat, const double* u, int64_t e0, int64_t e1,
                                double* r_elem, double* r_global, double* eval_out, cudaStream_t st) {
-  auto kern = eval_out ? k_residual_t3<FORM, true> : k_residual_t3<FORM, false>;
+  const PeerWin pw = g_peer;
+  auto kern = eval_out ? k_residual_t3<FORM, true> : (pw.n > 0 ? k_residual_t3<FORM, false, true>
+                                                                : k_residual_t3<FORM, false>);
   constexpr int NCOEF = FORM == FE_FORM_MASS_DIFFUSION ? 2 : 1;
   const size_t smem = (size_t)FEB200_T3_THREADS * (8 * (3 * NCOEF * 9 + 2 * 9 + 2 * 8) + 4 * (3 * 9 + 3 * 8));
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -364,7 +367,7 @@ static cudaError_t launch_t3_t(const fe_mesh* mh, MatArgs mat, const double* u, 
   grid = grid_cap(grid);
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, FEB200_T3_THREADS, smem, st>>>(view_of(mh), (const double*)mat.a, (const double*)mat.b, u,
-                                              e0, e1, r_elem, r_global, eval_out);
+                                              e0, e1, r_elem, r_global, eval_out, pw);
   count_launch();
   return cudaGetLastError();
 }

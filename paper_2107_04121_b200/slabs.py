@@ -140,3 +140,51 @@ def residual_overlapped(evaluate, r: torch.Tensor, slab: Slab, shape, comm_strea
         evaluate(L, n_local - L)
     main.wait_stream(comm_stream)
     return bufs
+
+
+class PeerExchange:
+    """Fused residual + interface exchange over peer memory.
+
+    Every rank's residual vector lives in an IPC-shareable allocation (fe_ipc_alloc); each
+    rank maps its neighbours' vectors (fe_ipc_open: NVLink peer memory on a multi-GPU node, or
+    the same device) and passes two peer windows to fe_eval_residual_peer: its first node
+    plane is also added into rank g-1's last plane, its last plane into rank g+1's first plane,
+    by the residual kernel's own scatter (system-scope fp64 atomics).  No separate collective
+    moves data; the step is ordered by two barriers (all vectors zeroed before any kernel;
+    all kernels finished before any rank reads).  Plumbing only: the arithmetic is in the
+    library's residual kernels."""
+
+    def __init__(self, slab: Slab, shape, p: int, ncomp: int, device, group=None):
+        import paper_2107_04121_b200 as fe
+        self.fe, self.slab, self.group = fe, slab, group
+        self.vec = fe.IpcVector((slab.n_nodes, ncomp), device)
+        self.r = self.vec.tensor
+        handles = [None] * slab.world
+        dist.all_gather_object(handles, self.vec.handle, group=group)
+        self.peers = []
+        self.windows = []
+        pl = slab.plane
+        if slab.rank > 0:
+            prev = slab_of(shape, p, slab.world, slab.rank - 1)
+            ptr = fe.ipc_open(handles[slab.rank - 1])
+            self.peers.append(ptr)
+            self.windows.append((0, pl, ptr, prev.n_nodes - pl))
+        if slab.rank < slab.world - 1:
+            ptr = fe.ipc_open(handles[slab.rank + 1])
+            self.peers.append(ptr)
+            self.windows.append((slab.n_nodes - pl, slab.n_nodes, ptr, 0))
+
+    def residual(self, evaluate_peer, barrier):
+        """One step: zero the own vector, barrier, fused residual + exchange over all local
+        cells (evaluate_peer(windows) launches fe_eval_residual_peer), barrier."""
+        self.r.zero_()
+        barrier()
+        evaluate_peer(self.windows)
+        barrier()
+        return self.r
+
+    def close(self):
+        for ptr in self.peers:
+            self.fe.ipc_close(ptr)
+        self.peers = []
+        self.vec.close()
