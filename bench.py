@@ -387,6 +387,11 @@ def main():
     if cfg == "C5t":
         sl = slabs.Slab(0, 1, 0, prob.n_elems, 0, prob.coords.shape[0], 0, prob.n_nodes, 0)
         lc, lconn, ldc = prob.coords, prob.conn, prob.dof_conn
+    elif "csr" in modes and world > 1:
+        # N2 with row ownership: the slab plus the first cell layer above, so the rank's owned
+        # block rows of the global CSR matrix are complete without communication
+        sl = slabs.ghost_slab_of(prob.shape, prob.p, world, rank)
+        lc, lconn, ldc = slabs.local_arrays(sl, prob.coords, prob.conn, prob.dof_conn)
     else:
         sl = slabs.slab_of(prob.shape, prob.p, world, rank)
         lc, lconn, ldc = slabs.local_arrays(sl, prob.coords, prob.conn, prob.dof_conn)

@@ -188,3 +188,53 @@ class PeerExchange:
             self.fe.ipc_close(ptr)
         self.peers = []
         self.vec.close()
+
+
+@dataclass
+class GhostSlab:
+    """A z-slab extended by the first cell layer of the rank above (matrix mode + CSR with row
+    ownership): rank g owns the node rows of its planes p*z0+1 .. p*z1 (rank 0 also
+    plane 0), so every owned row's cells are local or in the ghost layer, and the rank's block
+    rows of the global CSR matrix are assembled without any communication; the ghost layer's
+    element matrices are computed twice (by the owner of the cells and by the rank below)."""
+    slab: Slab                # the rank's own cells
+    elem_begin: int           # extended element range (own + ghost layer)
+    elem_end: int
+    vert_begin: int
+    vert_end: int
+    node_begin: int           # extended node range
+    node_end: int
+    row_begin: int            # owned rows, in the extended local numbering
+    row_end: int
+
+    @property
+    def n_elems(self):
+        return self.elem_end - self.elem_begin
+
+    @property
+    def n_nodes(self):
+        return self.node_end - self.node_begin
+
+
+def ghost_slab_of(shape, p: int, world: int, rank: int) -> GhostSlab:
+    nx, ny, nz = shape
+    sl = slab_of(shape, p, world, rank)
+    z0, z1 = nz * rank // world, nz * (rank + 1) // world
+    zg = z1 + 1 if rank < world - 1 else z1
+    vplane = (nx + 1) * (ny + 1)
+    pl = sl.plane
+    row_begin = pl if rank > 0 else 0
+    row_end = (p * (z1 - z0) + 1) * pl
+    return GhostSlab(sl, z0 * nx * ny, zg * nx * ny, z0 * vplane, (zg + 1) * vplane,
+                     p * z0 * pl, (p * zg + 1) * pl, row_begin, row_end)
+
+
+def owned_block_rows(gs: GhostSlab, row_ptr, col, values, ncomp: int = 1):
+    """The rank's block rows of the global CSR matrix from the CSR of its ghost-extended mesh:
+    (global first row, row_ptr rebased to 0, GLOBAL column ids, values) of the owned rows.
+    row_ptr / col / values: the local CSR (scalar rows when ncomp = 1; interleaved node-major
+    rows node * ncomp + a otherwise, as fe_create_csr lays them out)."""
+    r0, r1 = gs.row_begin * ncomp, gs.row_end * ncomp
+    a, b = int(row_ptr[r0]), int(row_ptr[r1])
+    rp = row_ptr[r0:r1 + 1] - a
+    return gs.node_begin * ncomp + r0, rp, col[a:b] + gs.node_begin * ncomp, values[a:b]

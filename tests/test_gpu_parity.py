@@ -644,3 +644,43 @@ def test_full_d_config_sampled():
     sub = _sample_subproblem(pr, idx)
     assert rel(K[torch.from_numpy(idx).cuda()].cpu().numpy(), oracle.problem_matrix(sub)) <= TOL64
     assert rel(re_[torch.from_numpy(idx).cuda()].cpu().numpy(), oracle.problem_residual(sub)) <= TOL64
+
+
+@pytest.mark.parametrize("form,p,world", [(fi.DIFFUSION, 2, 2), (fi.DIFFUSION, 1, 4),
+                                          (fi.ELASTICITY, 2, 2), (fi.MASS_DIFFUSION, 2, 4)])
+def test_csr_row_ownership_ghost_layer(form, p, world):
+    """Multi-GPU CSR with row ownership: each rank evaluates its z-slab plus the
+    first cell layer of the rank above and assembles the CSR of that extended mesh; its owned
+    block rows (global column ids) equal the single-GPU global matrix's rows exactly in pattern
+    and to rounding in value, and the ranks' owned rows tile the global rows."""
+    from paper_2107_04121_b200 import slabs
+    m = fe()
+    shape = (3, 2, 4)
+    pr = fi.make_problem(form, p, shape, 22000 + 10 * form + p)
+    D = pr.ncomp
+    mat = lambda a, e0, e1: None if a is None else dev(a[e0:e1])
+    mesh = gpu_mesh(pr)
+    Kg = mesh.element_matrices(form, pr.mat_kind, dev(pr.mat_a), dev(pr.mat_b))
+    cg = m.CSR(mesh, D)
+    vg = cg.assemble(Kg).cpu().numpy()
+    rpg, colg = cg.arrays()
+    covered = 0
+    for rank in range(world):
+        gs = slabs.ghost_slab_of(shape, p, world, rank)
+        lc, lconn, ldc = slabs.local_arrays(gs, pr.coords, pr.conn, pr.dof_conn)
+        lm = m.Mesh(torch.from_numpy(lc), torch.from_numpy(lconn), p, dof_conn=torch.from_numpy(ldc),
+                    n_nodes=gs.n_nodes)
+        K = lm.element_matrices(form, pr.mat_kind, mat(pr.mat_a, gs.elem_begin, gs.elem_end),
+                                mat(pr.mat_b, gs.elem_begin, gs.elem_end))
+        c = m.CSR(lm, D)
+        v = c.assemble(K).cpu().numpy()
+        rp, col = c.arrays()
+        g0, rpo, colo, vo = slabs.owned_block_rows(gs, rp, col, v, D)
+        n = len(rpo) - 1
+        a, b = rpg[g0], rpg[g0 + n]
+        assert g0 == covered
+        assert np.array_equal(rpo, rpg[g0:g0 + n + 1] - a)
+        assert np.array_equal(colo, colg[a:b])
+        assert rel(vo, vg[a:b]) <= TOL64
+        covered += n
+    assert covered == pr.n_nodes * D
