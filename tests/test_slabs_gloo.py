@@ -133,3 +133,27 @@ def test_slab_bookkeeping():
         assert all(a[1] == b[0] for a, b in zip(elems[:-1], elems[1:]))
     with pytest.raises(ValueError):
         slabs.slab_of((4, 4, 6), 2, 4, 0)
+
+
+@pytest.mark.parametrize("world,p", [(2, 2), (4, 1), (4, 3)])
+def test_ghost_slabs_tile_rows(world, p):
+    """Row ownership bookkeeping (N2 on several ranks): owned rows tile the global node rows,
+    each extended slab holds its own cells plus exactly one layer above (not on the top rank),
+    and every cell touching an owned row is inside the extended slab."""
+    from paper_2107_04121_b200 import slabs
+    shape = (3, 2, 8)
+    pr = fi.make_problem(fi.DIFFUSION, p, shape, 5)
+    nxy = shape[0] * shape[1]
+    owner = np.full(pr.n_nodes, -1)
+    for g in range(world):
+        gs = slabs.ghost_slab_of(shape, p, world, g)
+        sl = gs.slab
+        assert gs.elem_begin == sl.elem_begin
+        assert gs.elem_end == sl.elem_end + (nxy if g < world - 1 else 0)
+        lo, hi = gs.node_begin + gs.row_begin, gs.node_begin + gs.row_end
+        assert np.all(owner[lo:hi] == -1)
+        owner[lo:hi] = g
+        slabs.local_arrays(gs, pr.coords, pr.conn, pr.dof_conn)  # index ranges consistent
+        touching = np.where(((pr.dof_conn >= lo) & (pr.dof_conn < hi)).any(axis=1))[0]
+        assert touching.min() >= gs.elem_begin and touching.max() < gs.elem_end
+    assert np.all(owner >= 0)
