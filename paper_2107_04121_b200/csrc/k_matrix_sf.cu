@@ -487,7 +487,7 @@ __device__ __forceinline__ void sfp_named_bar(int id, int nthreads) {
 }
 
 template <int P, int FORM, bool RES>
-__global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM != FE_FORM_DIFFUSION ? 1 : 0)>::THREADS, 1)
+__global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM != FE_FORM_DIFFUSION ? 1 : 0), RES>::THREADS, 1)
     k_matrix_sfp(MeshView mv, const double* __restrict__ ma, const double* __restrict__ mb,
                  int64_t e0, int64_t e1, double* __restrict__ K, const double* __restrict__ u,
                  double* __restrict__ r_elem, double* __restrict__ r_global) {
