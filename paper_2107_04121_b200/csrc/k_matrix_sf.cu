@@ -68,9 +68,12 @@ struct SFM {
   static constexpr int THREADS = ((M1 > M2 ? M1 : M2) + 31) / 32 * 32;
   // shared memory (doubles)
   static constexpr int KST = E * NB * NB;                       // one staging buffer
+  // K staging buffers: two (the TMA store of batch it overlaps batch it + 1), one at p = 4
+  // (K_e alone is 125 KB there)
+  static constexpr int NKB = P >= 4 ? 1 : 2;
   static constexpr int QQP = (Q1 * Q1 + 1) / 2 * 2;             // (qx,qy) padded for LDS.128
   static constexpr int OFF_K = 0;                               // 2 x KST (16-B aligned)
-  static constexpr int OFF_EDGE = OFF_K + 2 * KST;              // [E][3 dirs][4][3]
+  static constexpr int OFF_EDGE = OFF_K + NKB * KST;            // [E][3 dirs][4][3]
   static constexpr int OFF_COEF = OFF_EDGE + E * 36;            // [E][2][NQ] kappa, rho
   static constexpr int OFF_W = OFF_COEF + E * 2 * NQ;           // [E][NUP][NQ]
   static constexpr int OFF_T1 = (OFF_W + E * NUP * NQ + 1) / 2 * 2;  // [E][NUP][N1*N1][QQP]
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_D
   for (int64_t bidx = blockIdx.x; bidx < nbatch; bidx += gridDim.x, ++it) {
     const int64_t lb = bidx * E;                 // local index of the first cell
     const int ne = (int)((nloc - lb) < E ? (nloc - lb) : E);
-    double* Kst = sm + L::OFF_K + (it & 1) * L::KST;
+    double* Kst = sm + L::OFF_K + (L::NKB == 2 ? (it & 1) * L::KST : 0);
     // A. this batch's data from the prefetch registers; issue the next reads
     if (pe_on) edge[tid] = xb_cur - xa_cur;
     if (pk_on) {
@@ -252,8 +255,12 @@ __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_D
     ld_edge(cn0, cn1, xa_cur, xb_cur);
     ld_k(bidx + gridDim.x, k_cur, r_cur);
     ld_conn2(bidx + 2 * (int64_t)gridDim.x, cn0, cn1);
-    // the TMA store issued two batches ago read this staging buffer: wait for it
-    if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    // the TMA store issued two batches ago (one with a single buffer) read this staging
+    // buffer: wait for it
+    if (tid == 0) {
+      if constexpr (L::NKB == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
     __syncthreads();
     // B. geometry from the 12 edge vectors -> W^{mn}[q]
     if (tid < E * NQ) {
@@ -1111,6 +1118,7 @@ cudaError_t launch_matrix_sf(const fe_mesh* mh, int form, MatArgs mat, int64_t e
     SF_CASE(1)
     SF_CASE(2)
     SF_CASE(3)
+    SF_CASE(4)
   }
 #undef SF_CASE
   return cudaErrorNotSupported;

@@ -684,3 +684,17 @@ def test_csr_row_ownership_ghost_layer(form, p, world):
         assert rel(vo, vg[a:b]) <= TOL64
         covered += n
     assert covered == pr.n_nodes * D
+
+
+@pytest.mark.parametrize("form", [fi.DIFFUSION, fi.MASS, fi.MASS_DIFFUSION])
+def test_matrix_q4(form):
+    """Matrix mode at p = 4 (single-stage SF kernel, one cell per CTA iteration, single K
+    staging buffer of 125 KB), ragged cell count and a sub-range."""
+    pr = fi.make_problem(form, 4, (3, 2, 2), 23000 + form)
+    mesh = gpu_mesh(pr)
+    mat = (pr.mat_kind, dev(pr.mat_a), dev(pr.mat_b))
+    K = mesh.element_matrices(form, *mat)
+    Kref = oracle.problem_matrix(pr)
+    assert rel(K.cpu().numpy(), Kref) <= TOL64
+    Ks = mesh.element_matrices(form, *mat, elem_begin=5, elem_end=12)
+    assert rel(Ks.cpu().numpy(), Kref[5:12]) <= TOL64
