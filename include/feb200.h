@@ -140,8 +140,8 @@ fe_status fe_mesh_info(const fe_mesh *mesh, fe_info *info);
  *   state_u: CONVECTIVE only, the linearisation state [n_nodes][3]; the
  *   matrix is the Newton tangent of Eq. fe4 (both terms).  NULL otherwise.
  * Only FE_F64 is built for matrices.  Orders: scalar forms 1-4, vector forms
- * (VECTOR_MASS, ELASTICITY, CONVECTIVE, WEIGHTED_DOT) 1-2 (3 for the dense
- * kernels); other combinations FE_ERR_UNSUPPORTED.  DIVERGENCE has no matrix
+ * (VECTOR_MASS, ELASTICITY, CONVECTIVE, WEIGHTED_DOT) 1-2; other
+ * combinations FE_ERR_UNSUPPORTED.  DIVERGENCE has no matrix
  * mode (FE_ERR_UNSUPPORTED). */
 fe_status fe_eval_element_matrices(const fe_mesh *mesh, int32_t form, int32_t dtype,
                                    const fe_material *mat, const void *state_u,
