@@ -142,6 +142,19 @@ def residual_overlapped(evaluate, r: torch.Tensor, slab: Slab, shape, comm_strea
     return bufs
 
 
+def peer_windows(slab: Slab, shape, p: int, prev_ptr, next_ptr):
+    """fe_eval_residual_peer windows of rank g: its first node plane is rank g-1's last plane
+    (local offset n_prev - plane there), its last plane is rank g+1's first plane (offset 0)."""
+    pl = slab.plane
+    wins = []
+    if slab.rank > 0:
+        prev = slab_of(shape, p, slab.world, slab.rank - 1)
+        wins.append((0, pl, prev_ptr, prev.n_nodes - pl))
+    if slab.rank < slab.world - 1:
+        wins.append((slab.n_nodes - pl, slab.n_nodes, next_ptr, 0))
+    return wins
+
+
 class PeerExchange:
     """Fused residual + interface exchange over peer memory.
 
@@ -161,18 +174,10 @@ class PeerExchange:
         self.r = self.vec.tensor
         handles = [None] * slab.world
         dist.all_gather_object(handles, self.vec.handle, group=group)
-        self.peers = []
-        self.windows = []
-        pl = slab.plane
-        if slab.rank > 0:
-            prev = slab_of(shape, p, slab.world, slab.rank - 1)
-            ptr = fe.ipc_open(handles[slab.rank - 1])
-            self.peers.append(ptr)
-            self.windows.append((0, pl, ptr, prev.n_nodes - pl))
-        if slab.rank < slab.world - 1:
-            ptr = fe.ipc_open(handles[slab.rank + 1])
-            self.peers.append(ptr)
-            self.windows.append((slab.n_nodes - pl, slab.n_nodes, ptr, 0))
+        prev = fe.ipc_open(handles[slab.rank - 1]) if slab.rank > 0 else None
+        nxt = fe.ipc_open(handles[slab.rank + 1]) if slab.rank < slab.world - 1 else None
+        self.peers = [q for q in (prev, nxt) if q is not None]
+        self.windows = peer_windows(slab, shape, p, prev, nxt)
 
     def residual(self, evaluate_peer, barrier):
         """One step: zero the own vector, barrier, fused residual + exchange over all local

@@ -157,3 +157,20 @@ def test_ghost_slabs_tile_rows(world, p):
         touching = np.where(((pr.dof_conn >= lo) & (pr.dof_conn < hi)).any(axis=1))[0]
         assert touching.min() >= gs.elem_begin and touching.max() < gs.elem_end
     assert np.all(owner >= 0)
+
+
+@pytest.mark.parametrize("world,p", [(2, 2), (4, 1), (3, 3)])
+def test_peer_windows_map_shared_planes(world, p):
+    """The peer windows map every shared interface node to the same GLOBAL node on the
+    neighbour (index bookkeeping of the fused peer-memory exchange)."""
+    from paper_2107_04121_b200 import slabs
+    shape = (2, 3, 12)
+    for g in range(world):
+        sl = slabs.slab_of(shape, p, world, g)
+        wins = slabs.peer_windows(sl, shape, p, "prev", "next")
+        assert len(wins) == (g > 0) + (g < world - 1)
+        for lo, hi, dst, off in wins:
+            nb = slabs.slab_of(shape, p, world, g - 1 if dst == "prev" else g + 1)
+            assert hi - lo == sl.plane
+            for n in (lo, (lo + hi) // 2, hi - 1):
+                assert sl.node_begin + n == nb.node_begin + (n - lo + off)
