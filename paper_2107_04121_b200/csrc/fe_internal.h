@@ -124,6 +124,14 @@ cudaError_t launch_geometry_materialize(const fe_mesh* m, double* detw, double* 
                                         cudaStream_t st);
 
 void count_launch();
+// Per-(kernel, device) launch facts, computed on the first launch on each device and cached:
+// the max-dynamic-shared-memory attribute is set, the SM count and the resident CTAs per SM
+// queried (keeps the per-call host overhead of small launches low).
+struct LaunchFacts {
+  int nsm, per_sm;
+  cudaError_t err;
+};
+LaunchFacts launch_facts(const void* kern, int threads, size_t smem);
 cudaError_t launch_coupling(const fe_mesh* mh, const fe_field* f, int mode, bool trans,
                             const double* u, const double* p, int64_t e0, int64_t e1, double* out,
                             double* rg, double* val, cudaStream_t st);

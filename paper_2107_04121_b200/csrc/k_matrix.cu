@@ -227,13 +227,9 @@ static cudaError_t launch_matrix_t(const fe_mesh* mh, MatArgs mat, const double*
   using L = MatLayout<P, FORM>;
   if (L::BYTES > 227 * 1024) return cudaErrorNotSupported;
   auto kern = k_matrix<P, FORM>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
-  if (err != cudaSuccess) return err;
-  int nsm = 148, per_sm = 1, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, L::BYTES);
-  if (per_sm < 1) per_sm = 1;
+  const LaunchFacts lf = launch_facts((const void*)kern, 256, L::BYTES);
+  if (lf.err != cudaSuccess) return lf.err;
+  const int nsm = lf.nsm, per_sm = lf.per_sm;
   const int64_t n = e1 - e0;
   int grid = (int)std::min<int64_t>(n, (int64_t)nsm * per_sm);
   grid = grid_cap(grid);

@@ -1027,11 +1027,9 @@ static cudaError_t launch_sfp_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int6
                                 double* r_global = nullptr) {
   using L = SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM != FE_FORM_DIFFUSION ? 1 : 0), RES>;
   auto kern = k_matrix_sfp<P, FORM, RES>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
-  if (err != cudaSuccess) return err;
-  int nsm = 148, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const LaunchFacts lf = launch_facts((const void*)kern, L::THREADS, L::BYTES);
+  if (lf.err != cudaSuccess) return lf.err;
+  const int nsm = lf.nsm;
   const int64_t nbatch = (e1 - e0 + L::E - 1) / L::E;
   int grid = (int)(nbatch < nsm ? nbatch : nsm);
   grid = grid_cap(grid);
@@ -1070,13 +1068,9 @@ static cudaError_t launch_sf_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int64
   constexpr bool DIFF = FORM != FE_FORM_MASS, MASS = FORM != FE_FORM_DIFFUSION;
   using L = SFM<P, DIFF, MASS>;
   auto kern = k_matrix_sf<P, FORM>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
-  if (err != cudaSuccess) return err;
-  int nsm = 148, per_sm = 1, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::THREADS, L::BYTES);
-  if (per_sm < 1) per_sm = 1;
+  const LaunchFacts lf = launch_facts((const void*)kern, L::THREADS, L::BYTES);
+  if (lf.err != cudaSuccess) return lf.err;
+  const int nsm = lf.nsm, per_sm = lf.per_sm;
   const int64_t nbatch = (e1 - e0 + L::E - 1) / L::E;
   int grid = (int)((nbatch < (int64_t)nsm * per_sm) ? nbatch : (int64_t)nsm * per_sm);
   grid = grid_cap(grid);

@@ -775,11 +775,9 @@ static cudaError_t launch_vp_t(const fe_mesh* mh, MatArgs mat, const double* sta
   using L = VPL<P, FORM>;
   if (L::BYTES > 227 * 1024) return cudaErrorNotSupported;
   auto kern = k_matrix_vp<P, FORM>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
-  if (err != cudaSuccess) return err;
-  int nsm = 148, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const LaunchFacts lf = launch_facts((const void*)kern, L::THREADS, L::BYTES);
+  if (lf.err != cudaSuccess) return lf.err;
+  const int nsm = lf.nsm;
   const int64_t nbatch = (e1 - e0 + L::E - 1) / L::E;
   int grid = (int)(nbatch < nsm ? nbatch : nsm);
   grid = grid_cap(grid);

@@ -1,4 +1,7 @@
 // Geometry check / materialisation (step a1) and standalone assembly (step d).
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <algorithm>
 #include <atomic>
 
@@ -8,6 +11,30 @@
 #include <cstdlib>
 
 namespace feb200 {
+
+LaunchFacts launch_facts(const void* kern, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, size_t>, LaunchFacts> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(kern, dev, threads, smem);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  LaunchFacts f{148, 1, cudaSuccess};
+  if (smem > 48 * 1024)
+    f.err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (f.err != cudaSuccess) return f;  // not cached: the caller reports it
+  cudaDeviceGetAttribute(&f.nsm, cudaDevAttrMultiProcessorCount, dev);
+  int per = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, smem) != cudaSuccess || per < 1) per = 1;
+  f.per_sm = per;
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = f;
+  return f;
+}
 
 int grid_cap(int grid) {
   const char* v = std::getenv("FEB200_MAX_CTAS");  // read per launch: tests toggle it

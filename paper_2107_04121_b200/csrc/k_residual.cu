@@ -155,13 +155,9 @@ static cudaError_t launch_res_t(const fe_mesh* mh, MatArgs mat, const T* u, int6
   const size_t bytes = head + sizeof(T) * size_t(L::NB + L::M4) * L::NCOL;
   if (bytes > 227 * 1024) return cudaErrorNotSupported;
   auto kern = k_residual<P, FORM, T>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (err != cudaSuccess) return err;
-  int nsm = 148, per_sm = 1, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, bytes);
-  if (per_sm < 1) per_sm = 1;
+  const LaunchFacts lf = launch_facts((const void*)kern, 256, bytes);
+  if (lf.err != cudaSuccess) return lf.err;
+  const int nsm = lf.nsm, per_sm = lf.per_sm;
   const int64_t nbatch = (e1 - e0 + L::NE - 1) / L::NE;
   int grid = (int)std::min<int64_t>(nbatch, (int64_t)nsm * per_sm);
   grid = grid_cap(grid);

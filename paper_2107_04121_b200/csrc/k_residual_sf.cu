@@ -551,13 +551,9 @@ static cudaError_t launch_rsf_t(const fe_mesh* mh, MatArgs mat, const T* u, int6
   if constexpr (sizeof(T) == 8) {
     if (pw.n > 0) kern = k_residual_sf<P, FORM, T, true>;
   }
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
-  if (err != cudaSuccess) return err;
-  int nsm = 148, per_sm = 1, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::THREADS, L::BYTES);
-  if (per_sm < 1) per_sm = 1;
+  const LaunchFacts lf = launch_facts((const void*)kern, L::THREADS, L::BYTES);
+  if (lf.err != cudaSuccess) return lf.err;
+  const int nsm = lf.nsm, per_sm = lf.per_sm;
   const int64_t nbatch = (e1 - e0 + L::EB - 1) / L::EB;
   int grid = (int)((nbatch < (int64_t)nsm * per_sm) ? nbatch : (int64_t)nsm * per_sm);
   grid = grid_cap(grid);

@@ -354,13 +354,9 @@ static cudaError_t launch_t3_t(const fe_mesh* mh, MatArgs mat, const double* u, 
                                                                 : k_residual_t3<FORM, false>);
   constexpr int NCOEF = FORM == FE_FORM_MASS_DIFFUSION ? 2 : 1;
   const size_t smem = (size_t)FEB200_T3_THREADS * (8 * (3 * NCOEF * 9 + 2 * 9 + 2 * 8) + 4 * (3 * 9 + 3 * 8));
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (err != cudaSuccess) return err;
-  int nsm = 148, per_sm = 1, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FEB200_T3_THREADS, smem);
-  if (per_sm < 1) per_sm = 1;
+  const LaunchFacts lf = launch_facts((const void*)kern, FEB200_T3_THREADS, smem);
+  if (lf.err != cudaSuccess) return lf.err;
+  const int nsm = lf.nsm, per_sm = lf.per_sm;
   const int64_t ncg = (e1 - e0 + 9) / 10;                       // 10 cells per warp
   const int64_t nblk = (ncg + FEB200_T3_THREADS / 32 - 1) / (FEB200_T3_THREADS / 32);
   int grid = (int)(nblk < (int64_t)nsm * per_sm ? nblk : (int64_t)nsm * per_sm);
