@@ -19,6 +19,12 @@
 #ifndef FEB200_T3_THREADS
 #define FEB200_T3_THREADS 64
 #endif
+#ifndef FEB200_T3C
+#define FEB200_T3C 1
+#endif
+#ifndef FEB200_T3C_MINB
+#define FEB200_T3C_MINB 4
+#endif
 #ifndef FEB200_T3_MINB
 #define FEB200_T3_MINB 4
 #endif
@@ -368,6 +374,268 @@ static cudaError_t launch_t3_t(const fe_mesh* mh, MatArgs mat, const double* u, 
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------
+// Convective residual r_(a,k) = int phi_k sum_j (du_a/dx_j) u_j (Eq. fe2) at p = 2,
+// fp64, register-resident: NINE lanes per cell, lane (a, j) owning component a on z-plane j
+// (3 cells per warp, lanes 27-31 idle).  Each component runs the scalar forward pass of the
+// kernel above (x, y in registers, z by shuffles among the component's three plane lanes);
+// at the flux the velocity components u_b(q) come from the cell's other component lanes by
+// shuffle.  With t = C^T grad_ref u_a = det grad u_a (C the cofactors of J),
+//   detw f0_a = w det (1/det) sum_r t_r u_r = w sum_r t_r u_r      (det cancels).
+// The backward pass tests against v only (values), as in the shared-memory kernel.
+template <bool EVAL, bool PEER = false>
+__global__ void __launch_bounds__(FEB200_T3_THREADS, FEB200_T3C_MINB)
+    k_residual_t3c(MeshView mv, const double* __restrict__ u, int64_t e0, int64_t e1,
+                   double* __restrict__ r_elem, double* __restrict__ r_global,
+                   double* __restrict__ eval_out, PeerWin pw) {
+  constexpr int P = 2, N = 3, NB = 27;
+#define B0(q, k) c_tab1d[P][0][q][k]
+#define B1(q, k) c_tab1d[P][1][q][k]
+  const int lane = threadIdx.x & 31;
+  const int cl = lane / 9, rem = lane - 9 * cl, a = rem / 3, j = rem - 3 * a;
+  const bool lane_ok = lane < 27;
+  const int base = 9 * cl + 3 * a;  // the three plane lanes of (cell, component)
+  double f0[3], f1[3];
+  int srcf[3], srcb[3];
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    const int k = (j + s) % 3;
+    f0[s] = lane_ok ? c_tab1d[P][0][j][k] : 0.0;
+    f1[s] = lane_ok ? c_tab1d[P][1][j][k] : 0.0;
+    srcf[s] = lane_ok ? base + k : lane;
+    srcb[s] = lane_ok ? base + (j - s + 3) % 3 : lane;
+  }
+  const int srcu0 = lane_ok ? 9 * cl + j : lane, srcu1 = lane_ok ? 9 * cl + 3 + j : lane,
+            srcu2 = lane_ok ? 9 * cl + 6 + j : lane;  // component lanes of the same plane
+  const double tZ = lane_ok ? c_x1d[P][j] : 0.5, wz = lane_ok ? c_w1d[P][j] : 0.0;
+  const int64_t nloc = e1 - e0;
+  const int wpb = blockDim.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5), nw = (int64_t)gridDim.x * wpb;
+  constexpr int TH = FEB200_T3_THREADS;
+  extern __shared__ __align__(16) unsigned char t3s[];
+  double* s2u = reinterpret_cast<double*>(t3s);                 // [2][9][TH]
+  double* s2x = s2u + 2 * 9 * TH;                               // [2][8][TH]
+  int32_t* s1d = reinterpret_cast<int32_t*>(s2x + 2 * 8 * TH);  // [3][9][TH]
+  int32_t* s1c = s1d + 3 * 9 * TH;                              // [3][8][TH]
+  const int tid = threadIdx.x;
+  auto group_cell = [&](int64_t g, int64_t& le, bool& ok) {
+    le = (gw + g * nw) * 3 + cl;
+    ok = lane_ok && le < nloc;
+  };
+  auto issue_s1 = [&](int64_t g) {
+    int64_t le;
+    bool ok;
+    group_cell(g, le, ok);
+    if (ok) {
+      const int sl = (int)(g % 3);
+      const int64_t e = e0 + le;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) t3_cp4(&s1d[(sl * 9 + k) * TH + tid], mv.dof_conn + e * NB + N * N * j + k);
+      if (a == 0) {
+#pragma unroll
+        for (int v = 0; v < 8; ++v) t3_cp4(&s1c[(sl * 8 + v) * TH + tid], mv.conn + 8 * e + v);
+      }
+    }
+    t3_commit();
+  };
+  auto issue_s2 = [&](int64_t g) {
+    int64_t le;
+    bool ok;
+    group_cell(g, le, ok);
+    if (ok) {
+      const int s1 = (int)(g % 3), s2 = (int)(g & 1);
+#pragma unroll
+      for (int k = 0; k < 9; ++k)
+        t3_cp8(&s2u[(s2 * 9 + k) * TH + tid], u + 3 * (int64_t)s1d[(s1 * 9 + k) * TH + tid] + a);
+      if (a == 0) {
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const int pidx = 8 * j + h, v = pidx / 3, i = pidx - 3 * v;
+          t3_cp8(&s2x[(s2 * 8 + h) * TH + tid], mv.coords + 3 * (int64_t)s1c[(s1 * 8 + v) * TH + tid] + i);
+        }
+      }
+    }
+    t3_commit();
+  };
+  issue_s1(0);
+  issue_s1(1);
+  t3_wait<1>();
+  issue_s2(0);
+  for (int64_t g = 0;; ++g) {
+    int64_t le;
+    bool valid;
+    group_cell(g, le, valid);
+    if ((gw + g * nw) * 3 >= nloc) break;
+    t3_wait<0>();
+    __syncwarp();
+    issue_s2(g + 1);
+    issue_s1(g + 2);
+    const int s1 = (int)(g % 3), s2 = (int)(g & 1);
+    int dof[N][N];
+    double uv[N][N];
+#pragma unroll
+    for (int ky = 0; ky < N; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < N; ++kx) {
+        dof[ky][kx] = s1d[(s1 * 9 + kx + N * ky) * TH + tid];
+        uv[ky][kx] = valid ? s2u[(s2 * 9 + kx + N * ky) * TH + tid] : 0.0;
+      }
+    double c00[N][N], c01[N][N], c10[N][N];
+    {
+      double a0[N][N], a1[N][N];
+#pragma unroll
+      for (int ky = 0; ky < N; ++ky)
+#pragma unroll
+        for (int qx = 0; qx < N; ++qx) {
+          double s0 = 0.0, sd = 0.0;
+#pragma unroll
+          for (int kx = 0; kx < N; ++kx) {
+            s0 = fma(B0(qx, kx), uv[ky][kx], s0);
+            sd = fma(B1(qx, kx), uv[ky][kx], sd);
+          }
+          a0[ky][qx] = s0;
+          a1[ky][qx] = sd;
+        }
+#pragma unroll
+      for (int qy = 0; qy < N; ++qy)
+#pragma unroll
+        for (int qx = 0; qx < N; ++qx) {
+          double s00 = 0.0, s01 = 0.0, s10 = 0.0;
+#pragma unroll
+          for (int ky = 0; ky < N; ++ky) {
+            s00 = fma(B0(qy, ky), a0[ky][qx], s00);
+            s01 = fma(B1(qy, ky), a0[ky][qx], s01);
+            s10 = fma(B0(qy, ky), a1[ky][qx], s10);
+          }
+          c00[qy][qx] = s00;
+          c01[qy][qx] = s01;
+          c10[qy][qx] = s10;
+        }
+    }
+    double Uq[N][N], Gx[N][N], Gy[N][N], Gz[N][N];
+#pragma unroll
+    for (int qy = 0; qy < N; ++qy)
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        const double v00 = c00[qy][qx], v01 = c01[qy][qx], v10 = c10[qy][qx];
+        double uq = f0[0] * v00, gz = f1[0] * v00, gy = f0[0] * v01, gx = f0[0] * v10;
+#pragma unroll
+        for (int s = 1; s < 3; ++s) {
+          const double w00 = __shfl_sync(0xffffffffu, v00, srcf[s]);
+          const double w01 = __shfl_sync(0xffffffffu, v01, srcf[s]);
+          const double w10 = __shfl_sync(0xffffffffu, v10, srcf[s]);
+          uq = fma(f0[s], w00, uq);
+          gz = fma(f1[s], w00, gz);
+          gy = fma(f0[s], w01, gy);
+          gx = fma(f0[s], w10, gx);
+        }
+        Uq[qy][qx] = uq;
+        Gx[qy][qx] = gx;
+        Gy[qy][qx] = gy;
+        Gz[qy][qx] = gz;
+      }
+    double X[8][3];
+    const int wb = tid - lane;
+#pragma unroll
+    for (int pidx = 0; pidx < 24; ++pidx)
+      X[pidx / 3][pidx % 3] = valid ? s2x[(s2 * 8 + pidx % 8) * TH + wb + 9 * cl + pidx / 8] : 0.0;
+    double Fv[N][N];
+#pragma unroll
+    for (int qy = 0; qy < N; ++qy)
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        const double t0 = c_x1d[P][qx], t1 = c_x1d[P][qy], t2 = tZ;
+        double J[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          J[i][0] = (1 - t1) * (1 - t2) * (X[1][i] - X[0][i]) + t1 * (1 - t2) * (X[3][i] - X[2][i]) +
+                    (1 - t1) * t2 * (X[5][i] - X[4][i]) + t1 * t2 * (X[7][i] - X[6][i]);
+          J[i][1] = (1 - t0) * (1 - t2) * (X[2][i] - X[0][i]) + t0 * (1 - t2) * (X[3][i] - X[1][i]) +
+                    (1 - t0) * t2 * (X[6][i] - X[4][i]) + t0 * t2 * (X[7][i] - X[5][i]);
+          J[i][2] = (1 - t0) * (1 - t1) * (X[4][i] - X[0][i]) + t0 * (1 - t1) * (X[5][i] - X[1][i]) +
+                    (1 - t0) * t1 * (X[6][i] - X[2][i]) + t0 * t1 * (X[7][i] - X[3][i]);
+        }
+        const double C00 = J[1][1] * J[2][2] - J[1][2] * J[2][1], C01 = J[1][2] * J[2][0] - J[1][0] * J[2][2],
+                     C02 = J[1][0] * J[2][1] - J[1][1] * J[2][0], C10 = J[0][2] * J[2][1] - J[0][1] * J[2][2],
+                     C11 = J[0][0] * J[2][2] - J[0][2] * J[2][0], C12 = J[0][1] * J[2][0] - J[0][0] * J[2][1],
+                     C20 = J[0][1] * J[1][2] - J[0][2] * J[1][1], C21 = J[0][2] * J[1][0] - J[0][0] * J[1][2],
+                     C22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+        const double g0 = Gx[qy][qx], g1 = Gy[qy][qx], g2 = Gz[qy][qx];
+        const double tr0 = C00 * g0 + C01 * g1 + C02 * g2;  // det (grad u_a)_r
+        const double tr1 = C10 * g0 + C11 * g1 + C12 * g2;
+        const double tr2 = C20 * g0 + C21 * g1 + C22 * g2;
+        const double uq = Uq[qy][qx];
+        const double w0 = __shfl_sync(0xffffffffu, uq, srcu0);  // u_0, u_1, u_2 at the qp
+        const double w1 = __shfl_sync(0xffffffffu, uq, srcu1);
+        const double w2 = __shfl_sync(0xffffffffu, uq, srcu2);
+        const double wq = c_w1d[P][qx] * c_w1d[P][qy] * wz;
+        Fv[qy][qx] = valid ? wq * (tr0 * w0 + tr1 * w1 + tr2 * w2) : 0.0;
+      }
+    double Hv[N][N];
+#pragma unroll
+    for (int qy = 0; qy < N; ++qy)
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        const double fv = Fv[qy][qx];
+        double hv = f0[0] * fv;
+#pragma unroll
+        for (int s = 1; s < 3; ++s) hv += __shfl_sync(0xffffffffu, f0[s] * fv, srcb[s]);
+        Hv[qy][qx] = hv;
+      }
+    double ev = 0.0;
+#pragma unroll
+    for (int ky = 0; ky < N; ++ky) {
+      double Iv[N];
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        double sv = 0.0;
+#pragma unroll
+        for (int qy = 0; qy < N; ++qy) sv = fma(B0(qy, ky), Hv[qy][qx], sv);
+        Iv[qx] = sv;
+      }
+#pragma unroll
+      for (int kx = 0; kx < N; ++kx) {
+        double rr = 0.0;
+#pragma unroll
+        for (int qx = 0; qx < N; ++qx) rr = fma(B0(qx, kx), Iv[qx], rr);
+        if (valid) {
+          if (r_elem) r_elem[le * 3 * NB + a * NB + kx + N * ky + N * N * j] = rr;
+          if (r_global) atomicAdd(r_global + 3 * (int64_t)dof[ky][kx] + a, rr);
+          if constexpr (PEER) peer_scatter<3>(pw, dof[ky][kx], a, rr);
+          if (EVAL) ev = fma(rr, uv[ky][kx], ev);
+        }
+      }
+    }
+    if (EVAL) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
+      if (lane == 0 && ev != 0.0) atomicAdd(eval_out, ev);
+    }
+  }
+  t3_wait<0>();
+#undef B0
+#undef B1
+}
+
+static cudaError_t launch_t3c(const fe_mesh* mh, const double* u, int64_t e0, int64_t e1,
+                              double* r_elem, double* r_global, double* eval_out, cudaStream_t st) {
+  const PeerWin pw = g_peer;
+  auto kern = eval_out ? k_residual_t3c<true> : (pw.n > 0 ? k_residual_t3c<false, true>
+                                                            : k_residual_t3c<false>);
+  const size_t smem = (size_t)FEB200_T3_THREADS * (8 * (2 * 9 + 2 * 8) + 4 * (3 * 9 + 3 * 8));
+  const LaunchFacts lf = launch_facts((const void*)kern, FEB200_T3_THREADS, smem);
+  if (lf.err != cudaSuccess) return lf.err;
+  const int nsm = lf.nsm, per_sm = lf.per_sm;
+  const int64_t ncg = (e1 - e0 + 2) / 3;                        // 3 cells per warp
+  const int64_t nblk = (ncg + FEB200_T3_THREADS / 32 - 1) / (FEB200_T3_THREADS / 32);
+  int grid = (int)(nblk < (int64_t)nsm * per_sm ? nblk : (int64_t)nsm * per_sm);
+  grid = grid_cap(grid);
+  if (grid <= 0) return cudaSuccess;
+  kern<<<grid, FEB200_T3_THREADS, smem, st>>>(view_of(mh), u, e0, e1, r_elem, r_global, eval_out, pw);
+  count_launch();
+  return cudaGetLastError();
+}
+
 // Scalar forms at p = 2 in fp64; cudaErrorNotSupported otherwise (the smem kernel runs).
 cudaError_t launch_residual_t3(const fe_mesh* mh, int form, MatArgs mat, const double* u, int64_t e0,
                                int64_t e1, double* r_elem, double* r_global, cudaStream_t st,
@@ -378,6 +646,9 @@ cudaError_t launch_residual_t3(const fe_mesh* mh, int form, MatArgs mat, const d
     case FE_FORM_MASS: return launch_t3_t<FE_FORM_MASS>(mh, mat, u, e0, e1, r_elem, r_global, eval_out, st);
     case FE_FORM_MASS_DIFFUSION:
       return launch_t3_t<FE_FORM_MASS_DIFFUSION>(mh, mat, u, e0, e1, r_elem, r_global, eval_out, st);
+    case FE_FORM_CONVECTIVE:
+      if (FEB200_T3C) return launch_t3c(mh, u, e0, e1, r_elem, r_global, eval_out, st);
+      return cudaErrorNotSupported;
     default: return cudaErrorNotSupported;
   }
 }
