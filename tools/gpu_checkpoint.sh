@@ -13,3 +13,4 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 ncu --set full --clock-control none --import-source on -k regex:k_matrix_sfp -s 1 -c 1 -o gpurun_out/prof_ck_matrix $CMD > gpurun_out/ncu_ck_full.log 2>&1; echo ncu2=$?
 ncu --set full --clock-control none --import-source on -k regex:k_residual_t3 -s 1 -c 1 -o gpurun_out/prof_ck_residual $CMD > gpurun_out/ncu_ck_full_r.log 2>&1; echo ncu3=$?
 ncu --set full --clock-control none --import-source on -k regex:k_matrix_vp -s 1 -c 1 -o gpurun_out/prof_ck_c3_matrix python bench.py --config C3 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_ck_c3.log 2>&1; echo ncu4=$?
+ncu --set full --clock-control none --import-source on -k regex:k_residual_t3c -s 1 -c 1 -o gpurun_out/prof_ck_c5_residual python bench.py --config C5 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_ck_c5.log 2>&1; echo ncu5=$?
