@@ -19,6 +19,9 @@
 #ifndef FEB200_T3_THREADS
 #define FEB200_T3_THREADS 64
 #endif
+#ifndef FEB200_T3_SEPGEO
+#define FEB200_T3_SEPGEO 1
+#endif
 #ifndef FEB200_T3C
 #define FEB200_T3C 1
 #endif
@@ -221,21 +224,47 @@ __global__ void __launch_bounds__(FEB200_T3_THREADS, FEB200_T3_MINB)
 #pragma unroll
     for (int pidx = 0; pidx < 24; ++pidx)
       X[pidx / 3][pidx % 3] = valid ? s2x[(s2 * 8 + pidx % 8) * TH + wb + base + pidx / 8] : 0.0;
+    // separable trilinear Jacobian on this lane's plane (t2 = tZ fixed): column 0 is linear in
+    // t1, column 1 linear in t0, column 2 bilinear; the t2 interpolation is done once per cell
+    double gE0[3], gdE[3], gF0[3], gdF[3], gH0[N][3], gdH[N][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double e0 = (1 - tZ) * (X[1][i] - X[0][i]) + tZ * (X[5][i] - X[4][i]);
+      const double e1 = (1 - tZ) * (X[3][i] - X[2][i]) + tZ * (X[7][i] - X[6][i]);
+      const double f0_ = (1 - tZ) * (X[2][i] - X[0][i]) + tZ * (X[6][i] - X[4][i]);
+      const double f1_ = (1 - tZ) * (X[3][i] - X[1][i]) + tZ * (X[7][i] - X[5][i]);
+      gE0[i] = e0; gdE[i] = e1 - e0; gF0[i] = f0_; gdF[i] = f1_ - f0_;
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        const double t0 = c_x1d[P][qx];
+        const double h0 = (1 - t0) * (X[4][i] - X[0][i]) + t0 * (X[5][i] - X[1][i]);
+        const double h1 = (1 - t0) * (X[6][i] - X[2][i]) + t0 * (X[7][i] - X[3][i]);
+        gH0[qx][i] = h0;
+        gdH[qx][i] = h1 - h0;
+      }
+    }
     double Fv[N][N], Fx[N][N], Fy[N][N], Fz[N][N];
 #pragma unroll
     for (int qy = 0; qy < N; ++qy)
 #pragma unroll
       for (int qx = 0; qx < N; ++qx) {
-        const double t0 = c_x1d[P][qx], t1 = c_x1d[P][qy], t2 = tZ;
+        const double t0 = c_x1d[P][qx], t1 = c_x1d[P][qy];
         double J[3][3];
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-          J[i][0] = (1 - t1) * (1 - t2) * (X[1][i] - X[0][i]) + t1 * (1 - t2) * (X[3][i] - X[2][i]) +
-                    (1 - t1) * t2 * (X[5][i] - X[4][i]) + t1 * t2 * (X[7][i] - X[6][i]);
-          J[i][1] = (1 - t0) * (1 - t2) * (X[2][i] - X[0][i]) + t0 * (1 - t2) * (X[3][i] - X[1][i]) +
-                    (1 - t0) * t2 * (X[6][i] - X[4][i]) + t0 * t2 * (X[7][i] - X[5][i]);
-          J[i][2] = (1 - t0) * (1 - t1) * (X[4][i] - X[0][i]) + t0 * (1 - t1) * (X[5][i] - X[1][i]) +
-                    (1 - t0) * t1 * (X[6][i] - X[2][i]) + t0 * t1 * (X[7][i] - X[3][i]);
+          if (FEB200_T3_SEPGEO) {
+            J[i][0] = fma(t1, gdE[i], gE0[i]);
+            J[i][1] = fma(t0, gdF[i], gF0[i]);
+            J[i][2] = fma(t1, gdH[qx][i], gH0[qx][i]);
+          } else {
+            const double t2 = tZ;
+            J[i][0] = (1 - t1) * (1 - t2) * (X[1][i] - X[0][i]) + t1 * (1 - t2) * (X[3][i] - X[2][i]) +
+                      (1 - t1) * t2 * (X[5][i] - X[4][i]) + t1 * t2 * (X[7][i] - X[6][i]);
+            J[i][1] = (1 - t0) * (1 - t2) * (X[2][i] - X[0][i]) + t0 * (1 - t2) * (X[3][i] - X[1][i]) +
+                      (1 - t0) * t2 * (X[6][i] - X[4][i]) + t0 * t2 * (X[7][i] - X[5][i]);
+            J[i][2] = (1 - t0) * (1 - t1) * (X[4][i] - X[0][i]) + t0 * (1 - t1) * (X[5][i] - X[1][i]) +
+                      (1 - t0) * t1 * (X[6][i] - X[2][i]) + t0 * t1 * (X[7][i] - X[3][i]);
+          }
         }
         // cofactors C[r][c] of J; J^-1[m][r] = C[r][m] / det
         const double C00 = J[1][1] * J[2][2] - J[1][2] * J[2][1], C01 = J[1][2] * J[2][0] - J[1][0] * J[2][2],
@@ -539,21 +568,47 @@ __global__ void __launch_bounds__(FEB200_T3_THREADS, FEB200_T3C_MINB)
 #pragma unroll
     for (int pidx = 0; pidx < 24; ++pidx)
       X[pidx / 3][pidx % 3] = valid ? s2x[(s2 * 8 + pidx % 8) * TH + wb + 9 * cl + pidx / 8] : 0.0;
+    // separable trilinear Jacobian on this lane's plane (t2 = tZ fixed): column 0 is linear in
+    // t1, column 1 linear in t0, column 2 bilinear; the t2 interpolation is done once per cell
+    double gE0[3], gdE[3], gF0[3], gdF[3], gH0[N][3], gdH[N][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double e0 = (1 - tZ) * (X[1][i] - X[0][i]) + tZ * (X[5][i] - X[4][i]);
+      const double e1 = (1 - tZ) * (X[3][i] - X[2][i]) + tZ * (X[7][i] - X[6][i]);
+      const double f0_ = (1 - tZ) * (X[2][i] - X[0][i]) + tZ * (X[6][i] - X[4][i]);
+      const double f1_ = (1 - tZ) * (X[3][i] - X[1][i]) + tZ * (X[7][i] - X[5][i]);
+      gE0[i] = e0; gdE[i] = e1 - e0; gF0[i] = f0_; gdF[i] = f1_ - f0_;
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        const double t0 = c_x1d[P][qx];
+        const double h0 = (1 - t0) * (X[4][i] - X[0][i]) + t0 * (X[5][i] - X[1][i]);
+        const double h1 = (1 - t0) * (X[6][i] - X[2][i]) + t0 * (X[7][i] - X[3][i]);
+        gH0[qx][i] = h0;
+        gdH[qx][i] = h1 - h0;
+      }
+    }
     double Fv[N][N];
 #pragma unroll
     for (int qy = 0; qy < N; ++qy)
 #pragma unroll
       for (int qx = 0; qx < N; ++qx) {
-        const double t0 = c_x1d[P][qx], t1 = c_x1d[P][qy], t2 = tZ;
+        const double t0 = c_x1d[P][qx], t1 = c_x1d[P][qy];
         double J[3][3];
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-          J[i][0] = (1 - t1) * (1 - t2) * (X[1][i] - X[0][i]) + t1 * (1 - t2) * (X[3][i] - X[2][i]) +
-                    (1 - t1) * t2 * (X[5][i] - X[4][i]) + t1 * t2 * (X[7][i] - X[6][i]);
-          J[i][1] = (1 - t0) * (1 - t2) * (X[2][i] - X[0][i]) + t0 * (1 - t2) * (X[3][i] - X[1][i]) +
-                    (1 - t0) * t2 * (X[6][i] - X[4][i]) + t0 * t2 * (X[7][i] - X[5][i]);
-          J[i][2] = (1 - t0) * (1 - t1) * (X[4][i] - X[0][i]) + t0 * (1 - t1) * (X[5][i] - X[1][i]) +
-                    (1 - t0) * t1 * (X[6][i] - X[2][i]) + t0 * t1 * (X[7][i] - X[3][i]);
+          if (FEB200_T3_SEPGEO) {
+            J[i][0] = fma(t1, gdE[i], gE0[i]);
+            J[i][1] = fma(t0, gdF[i], gF0[i]);
+            J[i][2] = fma(t1, gdH[qx][i], gH0[qx][i]);
+          } else {
+            const double t2 = tZ;
+            J[i][0] = (1 - t1) * (1 - t2) * (X[1][i] - X[0][i]) + t1 * (1 - t2) * (X[3][i] - X[2][i]) +
+                      (1 - t1) * t2 * (X[5][i] - X[4][i]) + t1 * t2 * (X[7][i] - X[6][i]);
+            J[i][1] = (1 - t0) * (1 - t2) * (X[2][i] - X[0][i]) + t0 * (1 - t2) * (X[3][i] - X[1][i]) +
+                      (1 - t0) * t2 * (X[6][i] - X[4][i]) + t0 * t2 * (X[7][i] - X[5][i]);
+            J[i][2] = (1 - t0) * (1 - t1) * (X[4][i] - X[0][i]) + t0 * (1 - t1) * (X[5][i] - X[1][i]) +
+                      (1 - t0) * t1 * (X[6][i] - X[2][i]) + t0 * t1 * (X[7][i] - X[3][i]);
+          }
         }
         const double C00 = J[1][1] * J[2][2] - J[1][2] * J[2][1], C01 = J[1][2] * J[2][0] - J[1][0] * J[2][2],
                      C02 = J[1][0] * J[2][1] - J[1][1] * J[2][0], C10 = J[0][2] * J[2][1] - J[0][1] * J[2][2],
