@@ -421,14 +421,22 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
         } else if constexpr (!L::CONV) {
           const double lam = slot[L::LS_A + el * NQ + q];  // per-cell material replicated per qp by L
           const double mu = slot[L::LS_B + el * NQ + q];
+          // pre-scaled factors: Lm = dw lam Ji, Mu = dw mu Ji, Sd = Lm + Mu, Q = dw mu Ji Ji^T
+          double Lm[9], Mu[9];
+          const double dl = dw * lam, dm = dw * mu;
+#pragma unroll
+          for (int k = 0; k < 9; ++k) {
+            Lm[k] = dl * Ji[k];
+            Mu[k] = dm * Ji[k];
+          }
           // diagonal blocks (a,a), unique pairs m <= n: dw ((lam + mu) Ji[m][a] Ji[n][a] + mu (Ji Ji^T)_mn)
 #pragma unroll
           for (int u = 0; u < 6; ++u) {
             const int m = vp_um(u), n = vp_un(u);
-            const double g = mu * (Ji[3 * m] * Ji[3 * n] + Ji[3 * m + 1] * Ji[3 * n + 1] + Ji[3 * m + 2] * Ji[3 * n + 2]);
+            const double g = Mu[3 * m] * Ji[3 * n] + Mu[3 * m + 1] * Ji[3 * n + 1] + Mu[3 * m + 2] * Ji[3 * n + 2];
 #pragma unroll
             for (int a2 = 0; a2 < 3; ++a2)
-              Wq[(6 * a2 + u) * NQ] = dw * ((lam + mu) * Ji[3 * m + a2] * Ji[3 * n + a2] + g);
+              Wq[(6 * a2 + u) * NQ] = fma(Lm[3 * m + a2] + Mu[3 * m + a2], Ji[3 * n + a2], g);
           }
           // off-diagonal blocks (0,1) (0,2) (1,2): dw (lam Ji[m][a] Ji[n][b] + mu Ji[m][b] Ji[n][a])
 #pragma unroll
@@ -437,7 +445,7 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
 #pragma unroll
             for (int pp = 0; pp < 9; ++pp) {
               const int m = pp / 3, n = pp % 3;
-              Wq[(18 + 9 * ob + pp) * NQ] = dw * (lam * Ji[3 * m + a2] * Ji[3 * n + b2] + mu * Ji[3 * m + b2] * Ji[3 * n + a2]);
+              Wq[(18 + 9 * ob + pp) * NQ] = fma(Lm[3 * m + a2], Ji[3 * n + b2], Mu[3 * m + b2] * Ji[3 * n + a2]);
             }
           }
         } else {
