@@ -66,7 +66,7 @@ def _worker(rank, world, form, p, shape, port, out_dir):
 
 
 @pytest.mark.parametrize("form,p", [(fi.DIFFUSION, 2), (fi.ELASTICITY, 2), (fi.MASS_DIFFUSION, 4),
-                                    (fi.DIFFUSION, 1)])
+                                    (fi.DIFFUSION, 1), (fi.CONVECTIVE, 2)])
 def test_peer_exchange_two_ranks(form, p, tmp_path):
     shape = (3, 4, 4)
     world = 2
