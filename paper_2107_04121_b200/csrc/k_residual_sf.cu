@@ -54,7 +54,7 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 #define FEB200_RSF_PAD 1
 #endif
 #ifndef FEB200_RSF_EB3
-#define FEB200_RSF_EB3 12
+#define FEB200_RSF_EB3 14  // 126 of 128 lanes busy (aligned-superset fetch)
 #endif
 #ifndef FEB200_RSF_EB2
 #define FEB200_RSF_EB2 20
@@ -63,7 +63,7 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 #define FEB200_RSF_MINB2 2
 #endif
 #ifndef FEB200_RSF_EB4
-#define FEB200_RSF_EB4 4
+#define FEB200_RSF_EB4 5  // 125 of 128 lanes busy (needs the aligned-superset fetch: 5 cells are not 16-B multiples)
 #endif
 #ifndef FEB200_RSF_MINB4
 #define FEB200_RSF_MINB4 3
@@ -109,9 +109,11 @@ struct RSF {
   // vertex coordinates [EB][24]; plus two mbarriers
   static constexpr size_t SL_CONN = 0;
   static constexpr size_t SL_DOF = SL_CONN + size_t(EB) * 8 * 4;
-  static constexpr size_t SL_MA = (SL_DOF + size_t(EB) * NB * 4 + 15) / 16 * 16;
-  static constexpr size_t SL_MB = (SL_MA + size_t(EB) * NQ * sizeof(T) + 15) / 16 * 16;
-  static constexpr size_t SL_SIZE = (SL_MB + size_t(EB) * NQ * sizeof(T) + 15) / 16 * 16;
+  // dof / material regions carry 16 B of slack: a batch whose block does not start on a 16-B
+  // boundary is fetched as the enclosing 16-B-aligned range and read at its offset
+  static constexpr size_t SL_MA = (SL_DOF + size_t(EB) * NB * 4 + 16 + 15) / 16 * 16;
+  static constexpr size_t SL_MB = (SL_MA + size_t(EB) * NQ * sizeof(T) + 16 + 15) / 16 * 16;
+  static constexpr size_t SL_SIZE = (SL_MB + size_t(EB) * NQ * sizeof(T) + 16 + 15) / 16 * 16;
   static constexpr size_t OFF_X = (2 * Q1 * N1 * 8 + 15) / 16 * 16;
   static constexpr size_t OFF_XV = (OFF_X + size_t(EB) * XS * sizeof(T) + 15) / 16 * 16;
   static constexpr int XVS = 28;  // per-cell stride of the staged vertex coordinates (bank spread)
@@ -178,6 +180,8 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // byte offset of a block start within its 16-B line (the fetch and the readers agree on it)
+  auto misal = [](const void* p_) { return (uint32_t)(reinterpret_cast<uintptr_t>(p_) & 15u); };
   // TMA bulk loads of the contiguous per-batch blocks (conn, dof_conn, material) into slot j % NSLOT
   auto fetch_idx = [&](int64_t j) {
     const int64_t b = blockIdx.x + j * G;
@@ -201,22 +205,30 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
         if (al(gD, bD)) l2_prefetch_bulk(gD, bD);
       }
     }
-    const bool ok = al(gc, bc) && al(gd, bd) && (nma == 0 || (al(ga, bm) && (!has_mb || al(gb, bm))));
+    // 16-B-aligned enclosing ranges (the data lands at offset o* in the slot region)
+    const uint32_t od = misal(gd), oa = nma ? misal(ga) : 0u, ob = has_mb ? misal(gb) : 0u;
+    const uint32_t bd2 = (od + bd + 15u) & ~15u, ba2 = (oa + bm + 15u) & ~15u, bb2 = (ob + bm + 15u) & ~15u;
+    const char* dend = reinterpret_cast<const char*>(mv.dof_conn + mv.n_elems * NB);
+    const char* aend = reinterpret_cast<const char*>(ma + mv.n_elems * nma);
+    const char* bend = has_mb ? reinterpret_cast<const char*>(mb + mv.n_elems * nma) : nullptr;
+    const bool ok = al(gc, bc) && reinterpret_cast<const char*>(gd) - od + bd2 <= dend &&
+                    (nma == 0 || (reinterpret_cast<const char*>(ga) - oa + ba2 <= aend &&
+                                  (!has_mb || reinterpret_cast<const char*>(gb) - ob + bb2 <= bend)));
     if (ok) {
       if (tid == 0) {
-        mbar_expect_tx(&bars[sl], bc + bd + (nma ? bm * (has_mb ? 2 : 1) : 0));
+        mbar_expect_tx(&bars[sl], bc + bd2 + (nma ? ba2 + (has_mb ? bb2 : 0u) : 0u));
         tma_load(base + L::SL_CONN, gc, bc, &bars[sl]);
-        tma_load(base + L::SL_DOF, gd, bd, &bars[sl]);
+        tma_load(base + L::SL_DOF, reinterpret_cast<const char*>(gd) - od, bd2, &bars[sl]);
         if (nma) {
-          tma_load(base + L::SL_MA, ga, bm, &bars[sl]);
-          if (has_mb) tma_load(base + L::SL_MB, gb, bm, &bars[sl]);
+          tma_load(base + L::SL_MA, reinterpret_cast<const char*>(ga) - oa, ba2, &bars[sl]);
+          if (has_mb) tma_load(base + L::SL_MB, reinterpret_cast<const char*>(gb) - ob, bb2, &bars[sl]);
         }
       }
-    } else {  // unaligned range: plain copies, then a plain arrival
+    } else {  // range at the end of an array: plain copies (same offsets), then a plain arrival
       int32_t* cs = reinterpret_cast<int32_t*>(base + L::SL_CONN);
-      int32_t* ds = reinterpret_cast<int32_t*>(base + L::SL_DOF);
-      T* as_ = reinterpret_cast<T*>(base + L::SL_MA);
-      T* bs_ = reinterpret_cast<T*>(base + L::SL_MB);
+      int32_t* ds = reinterpret_cast<int32_t*>(base + L::SL_DOF + od);
+      T* as_ = reinterpret_cast<T*>(base + L::SL_MA + oa);
+      T* bs_ = reinterpret_cast<T*>(base + L::SL_MB + ob);
       for (int i = tid; i < ne * 8; i += blockDim.x) cs[i] = mv.conn[8 * eb + i];
       for (int i = tid; i < ne * NB; i += blockDim.x) ds[i] = mv.dof_conn[eb * NB + i];
       for (int i = tid; i < ne * nma; i += blockDim.x) {
@@ -235,8 +247,8 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
     const int sl = (int)(j % L::NSLOT);
     const unsigned char* base = slot_base(sl);
     const int32_t* cs = reinterpret_cast<const int32_t*>(base + L::SL_CONN);
-    const int32_t* ds = reinterpret_cast<const int32_t*>(base + L::SL_DOF);
     const int64_t eb = e0 + b * EB;
+    const int32_t* ds = reinterpret_cast<const int32_t*>(base + L::SL_DOF + misal(mv.dof_conn + eb * NB));
     const int ne = b < nbatch ? (int)((e1 - eb) < EB ? (e1 - eb) : EB) : 0;
     if (ne > 0) mbar_wait(&bars[sl], (uint32_t)((j / L::NSLOT) & 1));
     const bool v = active && el < ne;
@@ -271,9 +283,9 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
       const int i = tid + h * blockDim.x;
       if (i < EB * 24) xvs[(i / 24) * L::XVS + i % 24] = x_next[h];
     }
-    const int32_t* ds = reinterpret_cast<const int32_t*>(base + L::SL_DOF) + el * NB;
-    const T* msa = reinterpret_cast<const T*>(base + L::SL_MA) + el * nma;
-    const T* msb = reinterpret_cast<const T*>(base + L::SL_MB) + el * nma;
+    const int32_t* ds = reinterpret_cast<const int32_t*>(base + L::SL_DOF + misal(mv.dof_conn + eb * NB)) + el * NB;
+    const T* msa = reinterpret_cast<const T*>(base + L::SL_MA + (nma ? misal(ma + eb * nma) : 0u)) + el * nma;
+    const T* msb = reinterpret_cast<const T*>(base + L::SL_MB + (has_mb ? misal(mb + eb * nma) : 0u)) + el * nma;
     int dcol[N1];
     A uc[D][N1];
 #pragma unroll
