@@ -13,6 +13,9 @@
 // Assembly: values[pos(e, a k, b l)] += K_e[a k][b l] with fp64 atomics
 // (atomic order is the only run-to-run difference, as for the residual).
 #include <algorithm>
+#ifndef FEB200_CSR_CONST
+#define FEB200_CSR_CONST 1
+#endif
 #include <cstdlib>
 #include <cstring>
 #include <exception>
@@ -139,6 +142,26 @@ __global__ void __launch_bounds__(256) k_assemble_matrix(const int32_t* __restri
   }
 }
 
+
+// Same, with compile-time sizes and 32-bit index arithmetic (divisions by constants become
+// multiply-shifts; the generic kernel divides 64-bit indices per entry)
+template <typename PT, int NB, int D>
+__global__ void __launch_bounds__(256) k_assemble_matrix_c(const int32_t* __restrict__ dc, int64_t e0,
+                                                           uint32_t n, const int64_t* __restrict__ rpn,
+                                                           const PT* __restrict__ pos,
+                                                           const double* __restrict__ K,
+                                                           double* __restrict__ values) {
+  constexpr uint32_t ND = D * NB, NE = ND * ND;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t el = i / NE, rr = i - el * NE, row = rr / ND, cl = rr - row * ND;
+    const uint32_t a = row / NB, k = row - a * NB, b = cl / NB, l = cl - b * NB;
+    const int64_t e = e0 + el;
+    const int32_t rn = dc[e * NB + k];
+    const int64_t b0 = rpn[rn], nr = rpn[rn + 1] - b0;
+    const int64_t p = (int64_t)D * D * b0 + (int64_t)a * D * nr + (int64_t)pos[(e * NB + k) * NB + l] * D + b;
+    atomicAdd(values + p, K[i]);
+  }
+}
 
 // Gather ("row-owner") assembly, no atomics: one warp owns one node row r of the pattern,
 // accumulates in shared memory the rows k of every incident cell's K_e (node-to-cell list,
@@ -369,6 +392,16 @@ fe_status fe_assemble_matrix(const fe_csr* csr, const double* K, int64_t elem_be
   const int D = csr->ncomp;
   const size_t smem = (size_t)8 * D * D * csr->hmax * 8;  // 8 warps per block
   auto launch = [&](auto* pos) {
+    if (atomic && csr->mesh->nb == 27 && n < (int64_t(1) << 32) && FEB200_CSR_CONST) {
+      using PT = std::remove_const_t<std::remove_pointer_t<decltype(pos)>>;
+      if (D == 1)
+        feb200::k_assemble_matrix_c<PT, 27, 1><<<grid, 256, 0, (cudaStream_t)stream>>>(
+            csr->mesh->dof_conn, elem_begin, (uint32_t)n, csr->rowptr_node, pos, K, values);
+      else
+        feb200::k_assemble_matrix_c<PT, 27, 3><<<grid, 256, 0, (cudaStream_t)stream>>>(
+            csr->mesh->dof_conn, elem_begin, (uint32_t)n, csr->rowptr_node, pos, K, values);
+      return;
+    }
     if (atomic) {
       feb200::k_assemble_matrix<<<grid, 256, 0, (cudaStream_t)stream>>>(
           csr->mesh->dof_conn, csr->mesh->nb, csr->ncomp, elem_begin, elem_end, csr->rowptr_node, pos, K,
