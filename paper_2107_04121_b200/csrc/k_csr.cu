@@ -153,13 +153,17 @@ __global__ void __launch_bounds__(256) k_assemble_matrix_c(const int32_t* __rest
                                                            double* __restrict__ values) {
   constexpr uint32_t ND = D * NB, NE = ND * ND;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const uint32_t el = i / NE, rr = i - el * NE, row = rr / ND, cl = rr - row * ND;
-    const uint32_t a = row / NB, k = row - a * NB, b = cl / NB, l = cl - b * NB;
+    const uint32_t el = i / NE, rr = i - el * NE, row = rr / ND, j = rr - row * ND;
+    // D = 3: the column component b runs fastest over the lanes, so consecutive lanes add to
+    // consecutive CSR values (node-major interleaved columns) -- 4 lanes per 32-B sector
+    // instead of one -- while the K reads stay three runs of consecutive doubles
+    const uint32_t l = D == 1 ? j : j / D, b = D == 1 ? 0 : j - l * D;
+    const uint32_t a = row / NB, k = row - a * NB;
     const int64_t e = e0 + el;
     const int32_t rn = dc[e * NB + k];
     const int64_t b0 = rpn[rn], nr = rpn[rn + 1] - b0;
     const int64_t p = (int64_t)D * D * b0 + (int64_t)a * D * nr + (int64_t)pos[(e * NB + k) * NB + l] * D + b;
-    atomicAdd(values + p, K[i]);
+    atomicAdd(values + p, K[(uint64_t)el * NE + row * ND + b * NB + l]);
   }
 }
 
