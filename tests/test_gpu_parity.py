@@ -698,3 +698,33 @@ def test_matrix_q4(form):
     assert rel(K.cpu().numpy(), Kref) <= TOL64
     Ks = mesh.element_matrices(form, *mat, elem_begin=5, elem_end=12)
     assert rel(Ks.cpu().numpy(), Kref[5:12]) <= TOL64
+
+
+@pytest.mark.parametrize("form,p", [(fi.MASS_DIFFUSION, 4), (fi.ELASTICITY, 2), (fi.DIFFUSION, 2),
+                                    (fi.WEIGHTED_DOT, 2), (fi.MASS_DIFFUSION, 3)])
+@pytest.mark.parametrize("ctas", [0, 2])
+def test_residual_misaligned_inputs(form, p, ctas, monkeypatch):
+    """Material arrays passed as views that start 8 B past a 16-B boundary: the residual
+    kernels' block fetches take the enclosing aligned range and read at the offset (and fall
+    back to plain copies at the array end); results unchanged."""
+    if ctas:
+        monkeypatch.setenv("FEB200_MAX_CTAS", str(ctas))
+    pr = fi.make_problem(form, p, (5, 3, 3) if p <= 2 else (3, 2, 3), 24000 + 10 * form + p,
+                         mat_kind=fi.MAT_PER_QP if form == fi.ELASTICITY else None)
+    mesh = gpu_mesh(pr)
+
+    def shifted(a):
+        if a is None:
+            return None
+        flat = np.ascontiguousarray(a).ravel()
+        big = torch.zeros(flat.size + 1, dtype=torch.float64, device="cuda")
+        big[1:] = torch.from_numpy(flat).cuda()
+        v = big[1:].view(a.shape)
+        assert v.data_ptr() % 16 == 8
+        return v
+
+    r_elem, r_glob = mesh.residual(form, dev(pr.u), pr.mat_kind, shifted(pr.mat_a), shifted(pr.mat_b),
+                                   want_elem=True)
+    r_ref = oracle.problem_residual(pr)
+    assert rel(r_elem.cpu().numpy(), r_ref) <= TOL64
+    assert rel(r_glob.cpu().numpy().ravel(), oracle.assemble(r_ref, pr.dof_conn, pr.n_nodes, pr.ncomp)) <= TOL64
