@@ -129,6 +129,11 @@ __device__ __forceinline__ double hex_geometry(const double* __restrict__ xv, do
   return det;
 }
 
+// 32-byte read-only load (LDG.256 on sm_100): four consecutive doubles, 32-B aligned address
+__device__ __forceinline__ void ld_nc_v4(const double* p, double& x, double& y, double& z, double& w) {
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(x), "=d"(y), "=d"(z), "=d"(w) : "l"(p));
+}
+
 // Bulk prefetch of a contiguous global range into L2 (TMA engine; one instruction, no
 // completion tracking).  p and bytes must be 16-byte multiples; the caller checks.
 __device__ __forceinline__ void l2_prefetch_bulk(const void* p, uint32_t bytes) {

@@ -12,7 +12,11 @@
 //   weighted dot     f0_a = M_ab u_b, M per qp             ('ij,i,j')
 //   divergence       f1_aj = delta_aj (u does not enter)   ('i.i')
 #pragma once
+#include "fe_device.cuh"
 #include "feb200.h"
+#ifndef FEB200_FLUX_V4
+#define FEB200_FLUX_V4 1
+#endif
 
 namespace feb200 {
 
@@ -86,7 +90,21 @@ __device__ __forceinline__ void qp_flux_m(const double (&uq)[FormD<FORM>::D],
     double sig[6];
     if (mat_kind == FE_MAT_FULL_D) {
       const T* Dm = mq.Dm;
-      if (sizeof(T) == 8 && (reinterpret_cast<uintptr_t>(Dm) & 15u) == 0) {
+      if (sizeof(T) == 8 && FEB200_FLUX_V4 && (reinterpret_cast<uintptr_t>(Dm) & 31u) == 0) {
+        // 32-byte loads: one full sector per lane and instruction (the 288-B block of a qp is
+        // nine of them), so no sector is fetched twice through L1
+        const double* D8 = reinterpret_cast<const double*>(Dm);
+        double dv[36];
+#pragma unroll
+        for (int h = 0; h < 9; ++h) ld_nc_v4(D8 + 4 * h, dv[4 * h], dv[4 * h + 1], dv[4 * h + 2], dv[4 * h + 3]);
+#pragma unroll
+        for (int I = 0; I < 6; ++I) {
+          double s = 0.0;
+#pragma unroll
+          for (int K = 0; K < 6; ++K) s = fma(dv[6 * I + K], eps[K], s);
+          sig[I] = s;
+        }
+      } else if (sizeof(T) == 8 && (reinterpret_cast<uintptr_t>(Dm) & 15u) == 0) {
         // 16-byte loads: a warp's 36 scalar loads of 288-byte-strided blocks would each touch
         // 32 sectors for 8 useful bytes; pairs halve the sector re-fetches through L1
         const double2* D2 = reinterpret_cast<const double2*>(Dm);

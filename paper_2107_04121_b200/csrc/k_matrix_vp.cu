@@ -384,8 +384,13 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
           // W^{ab}_{mn} = dw sum_{j,l} Ji[m][j] D[v(a,j)][v(b,l)] Ji[n][l]
           double Dm[36];
           const double* Dg = ma + ((e0 + lb + el) * NQ + q) * 36;
+          if (on && (reinterpret_cast<uintptr_t>(Dg) & 31u) == 0) {  // nine 32-B loads
 #pragma unroll
-          for (int i = 0; i < 36; ++i) Dm[i] = on ? __ldg(Dg + i) : 0.0;
+            for (int h = 0; h < 9; ++h) ld_nc_v4(Dg + 4 * h, Dm[4 * h], Dm[4 * h + 1], Dm[4 * h + 2], Dm[4 * h + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 36; ++i) Dm[i] = on ? __ldg(Dg + i) : 0.0;
+          }
           auto Dv = [&](int a, int j, int b, int l) {
             const int I = vp_voigt(a, j), Kk = vp_voigt(b, l);
             return I <= Kk ? Dm[6 * I + Kk] : Dm[6 * Kk + I];
