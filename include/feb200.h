@@ -88,10 +88,14 @@ typedef enum { FE_F64 = 0, FE_F32 = 1 } fe_dtype;
  *   ELASTICITY      PER_ELEM: a = lambda[E], b = mu[E];
  *                   PER_QP:   a = lambda[E][n_q], b = mu[E][n_q];
  *                   FULL_D:   a = D[E][n_q][6][6] (Voigt xx,yy,zz,xy,xz,yz,
- *                             engineering shears; 'cqIK' operand);
- *                             symmetric (major symmetry of the elasticity
- *                             tensor, reading 23): the pipelined Q2
- *                             matrix kernel reads its upper triangle only
+ *                             engineering shears; 'cqIK' operand),
+ *                             read as given by every mode (DESIGN.md reading
+ *                             23).  A non-symmetric D gives a non-symmetric K.
+ *                             At p = 2 matrix mode checks the symmetry on the
+ *                             device (one extra read of D) and runs the
+ *                             pipelined kernel (which derives K_ba = K_ab^T)
+ *                             only for a D symmetric to 8 ulps; otherwise the
+ *                             general 9-block kernel
  *   CONVECTIVE      unused (kind ignored)                                  */
 typedef enum { FE_MAT_PER_QP = 0, FE_MAT_PER_ELEM = 1, FE_MAT_FULL_D = 2 } fe_material_kind;
 
@@ -128,8 +132,12 @@ fe_status fe_create_mesh_geometry(int64_t n_vertices, const double *coords, int6
                                   int64_t n_nodes, const int32_t *dof_conn, void *stream,
                                   fe_mesh **out);
 
-/* Release the handle and its device memory (synchronises the device). NULL is a no-op. */
-fe_status fe_destroy_mesh(fe_mesh *mesh);
+/* Release the handle and its device memory, stream-ordered: the memory is returned
+ * (cudaFreeAsync) after the work already queued on `stream`; the device is NOT
+ * synchronised.  Work on other streams that uses the handle must be ordered
+ * before this call by the caller (events), as for any stream-ordered free.
+ * NULL is a no-op. */
+fe_status fe_destroy_mesh(fe_mesh *mesh, void *stream);
 
 /* Sizes of the handle (host struct). */
 fe_status fe_mesh_info(const fe_mesh *mesh, fe_info *info);
@@ -228,6 +236,15 @@ fe_status fe_eval_scalar(const fe_mesh *mesh, int32_t form, int32_t dtype, const
 fe_status fe_eval_stress(const fe_mesh *mesh, const fe_material *mat, const double *u,
                          int64_t elem_begin, int64_t elem_end, double *sigma, void *stream);
 
+/* The Cauchy stress in the paper's 'eval' mode, "returning the integral value":
+ * per cell, sigma_int[e - elem_begin][I] = int_e sigma_I dx = sum_q w_q det J_q sigma[e][q][I]
+ * (the domain integral is the sum over cells).  Arguments as fe_eval_stress; sigma_int
+ * [elem_end - elem_begin][6] fp64, caller owned, overwritten.  Deterministic (fixed qp order,
+ * no atomics). */
+fe_status fe_eval_stress_integral(const fe_mesh *mesh, const fe_material *mat, const double *u,
+                                  int64_t elem_begin, int64_t elem_end, double *sigma_int,
+                                  void *stream);
+
 /* ---- Element-kind grouping ---------------------------
  * One evaluation call covers cells of one kind (order); a p-/hp-mixed mesh is
  * evaluated group by group.  fe_group_cells is a stable GPU sort of the cell
@@ -266,7 +283,8 @@ typedef struct fe_field fe_field;
  * (3,3) (4,3) (4,4); others FE_ERR_UNSUPPORTED. */
 fe_status fe_create_field(const fe_mesh *mesh, int32_t order, int64_t n_nodes,
                           const int32_t *dof_conn, void *stream, fe_field **out);
-fe_status fe_destroy_field(fe_field *field);
+/* Stream-ordered release, as fe_destroy_mesh. */
+fe_status fe_destroy_field(fe_field *field, void *stream);
 
 /* Matrix mode of the coupling over cells [elem_begin, elem_end):
  *   transposed = 0: B[e'][a*n_bv + k][l] = int dphi_k/dx_a psi_l   (test v, trial p)
@@ -330,8 +348,8 @@ fe_status fe_csr_copy_arrays(const fe_csr *csr, int64_t *row_ptr, int32_t *col_i
 fe_status fe_assemble_matrix(const fe_csr *csr, const double *K, int64_t elem_begin,
                              int64_t elem_end, double *values, void *stream);
 
-/* Release the CSR object (synchronises the device).  NULL is a no-op. */
-fe_status fe_destroy_csr(fe_csr *csr);
+/* Release the CSR object, stream-ordered as fe_destroy_mesh.  NULL is a no-op. */
+fe_status fe_destroy_csr(fe_csr *csr, void *stream);
 
 /* Test mode: materialise the geometry of step a1 (fp64):
  *   detw[E][n_q] = w_q det J,  jinv[E][n_q][3][3] = J^-1 (row-major).
@@ -346,6 +364,33 @@ int64_t fe_last_error_element(void);
 
 /* Number of kernels this library launched since load (all threads). */
 int64_t fe_launch_count(void);
+
+/* ---- Process-wide implementation options ------------------------------------
+ * Alternative kernels kept as measured baselines and test hooks.  Defaults are
+ * read ONCE, when the library is loaded, from the environment variables named
+ * below (FE_OPT_* = 0 when unset); afterwards only fe_set_option changes them
+ * (no per-launch getenv).  Values are relaxed atomics: set them while no
+ * evaluation is in flight on another thread.  Out-of-range values give
+ * FE_ERR_INVALID_ARG.
+ *   FE_OPT_MATRIX_IMPL   (FEB200_MATRIX_IMPL = sf1 | dense)  0 default (sum-factorised,
+ *                        warp-specialised pipelines where built), 1 single-stage
+ *                        sum-factorised kernels, 2 dense DMMA kernels
+ *   FE_OPT_RESIDUAL_IMPL (FEB200_RESIDUAL_IMPL = sf | dense) 0 default (register-resident
+ *                        kernels at p = 2, sum-factorised otherwise), 1 shared-memory
+ *                        sum-factorised kernels for every form, 2 dense DMMA kernels
+ *   FE_OPT_CSR_IMPL      (FEB200_CSR_IMPL = gather)          0 fp64 atomics, 1 atomic-free
+ *                        row-owner gather (bitwise reproducible, p <= 2)
+ *   FE_OPT_MAX_CTAS      (FEB200_MAX_CTAS = n)               0 no cap, else the grid cap of
+ *                        the persistent kernels (test hook: many batches per CTA) */
+typedef enum {
+  FE_OPT_MATRIX_IMPL = 0,
+  FE_OPT_RESIDUAL_IMPL = 1,
+  FE_OPT_CSR_IMPL = 2,
+  FE_OPT_MAX_CTAS = 3,
+  FE_OPT_COUNT = 4
+} fe_option;
+fe_status fe_set_option(int32_t option, int64_t value);
+fe_status fe_get_option(int32_t option, int64_t *value);
 
 #ifdef __cplusplus
 }

@@ -56,6 +56,8 @@ def lib():
         _lib.oracle_eval_scalar.restype = ci
         _lib.oracle_eval_stress.argtypes = [ci, ci, i64, P, P, P, ci, P, P, P, i64, i64, P]
         _lib.oracle_eval_stress.restype = ci
+        _lib.oracle_eval_stress_integral.argtypes = [ci, ci, i64, P, P, P, ci, P, P, P, i64, i64, P]
+        _lib.oracle_eval_stress_integral.restype = ci
         _lib.oracle_coupling_matrix.argtypes = [ci, ci, ci, ci, i64, P, P, i64, i64, P]
         _lib.oracle_coupling_residual.argtypes = [ci, ci, ci, ci, i64, P, P, P, P, P, P, i64, i64, P]
         _lib.oracle_coupling_eval.argtypes = [ci, ci, ci, i64, P, P, P, P, P, P, i64, i64, P]
@@ -196,6 +198,20 @@ def eval_stress(p, q1d, coords, conn, dof_conn, u, mat_kind=1, mat_a=None, mat_b
     _check(lib().oracle_eval_stress(p, q1d, E, _ptr(coords), _ptr(conn), _ptr(dof_conn), mat_kind,
                                     _ptr(mat_a), _ptr(mat_b), _ptr(u), elem_begin, elem_end,
                                     _ptr(sig)))
+    return sig
+
+
+def eval_stress_integral(p, q1d, coords, conn, dof_conn, u, mat_kind=1, mat_a=None, mat_b=None,
+                         elem_begin=0, elem_end=None):
+    """Cauchy stress in 'eval' mode: per cell int_e sigma dx, [E'][6] (Voigt)."""
+    coords, conn, dof_conn = _f64(coords), _i32(conn), _i32(dof_conn)
+    mat_a, mat_b, u = _f64(mat_a), _f64(mat_b), _f64(u)
+    E = conn.shape[0]
+    elem_end = E if elem_end is None else elem_end
+    sig = np.zeros((max(elem_end - elem_begin, 0), 6))
+    _check(lib().oracle_eval_stress_integral(p, q1d, E, _ptr(coords), _ptr(conn), _ptr(dof_conn),
+                                             mat_kind, _ptr(mat_a), _ptr(mat_b), _ptr(u),
+                                             elem_begin, elem_end, _ptr(sig)))
     return sig
 
 

@@ -661,10 +661,10 @@ int oracle_set_threads(int n) {
  * point of cells [elem_begin, elem_end), Voigt order (xx, yy, zz, xy, xz, yz), engineering
  * shear strains (reading 7); "evaluated only" (no test variable):
  *   sigma[e - elem_begin][q][6]. */
-int oracle_eval_stress(int p, int q1d, int64_t n_elems, const double *coords, const int32_t *conn,
+static int stress_impl(int p, int q1d, int64_t n_elems, const double *coords, const int32_t *conn,
                        const int32_t *dof_conn, int mat_kind, const double *mat_a,
                        const double *mat_b, const double *u, int64_t elem_begin, int64_t elem_end,
-                       double *sigma) {
+                       double *sigma, int integ) {
   if (p < 1 || p > 8 || q1d < 1 || q1d > 16 || n_elems < 0 || !u || !sigma) return OR_ERR_ARG;
   if (elem_begin < 0 || elem_end > n_elems || elem_begin > elem_end) return OR_ERR_ARG;
   const int n1 = p + 1, nb = n1 * n1 * n1, nq = q1d * q1d * q1d;
@@ -697,16 +697,39 @@ int oracle_eval_stress(int p, int q1d, int64_t n_elems, const double *coords, co
         for (int r = 0; r < 3; ++r)
           for (int l = 0; l < 3; ++l) eps[I] += Psg[r][l][I] * gu[r][l];
       }
-      double *out = sigma + ((e - elem_begin) * nq + q) * 6;
       for (int I = 0; I < 6; ++I) {
         double sI = 0.0;
         for (int K = 0; K < 6; ++K) sI += Dm[6 * I + K] * eps[K];
-        out[I] = sI;
+        if (integ)  /* 'eval' mode: int_e sigma = sum_q w_q det J sigma */
+          sigma[(e - elem_begin) * 6 + I] += w[q] * det * sI;
+        else
+          sigma[((e - elem_begin) * nq + q) * 6 + I] = sI;
       }
     }
   }
   free(xi); free(w); free(Phi); free(dPhi);
   return status;
+}
+
+/* Cauchy stress at every qp: sigma[e - elem_begin][q][6]. */
+int oracle_eval_stress(int p, int q1d, int64_t n_elems, const double *coords, const int32_t *conn,
+                       const int32_t *dof_conn, int mat_kind, const double *mat_a,
+                       const double *mat_b, const double *u, int64_t elem_begin, int64_t elem_end,
+                       double *sigma) {
+  return stress_impl(p, q1d, n_elems, coords, conn, dof_conn, mat_kind, mat_a, mat_b, u,
+                     elem_begin, elem_end, sigma, 0);
+}
+
+/* The Cauchy stress in 'eval' mode ("the integral value"): per cell
+ * sigma_int[e - elem_begin][6] = int_e sigma dx (quadrature as everywhere: w_q det J). */
+int oracle_eval_stress_integral(int p, int q1d, int64_t n_elems, const double *coords,
+                                const int32_t *conn, const int32_t *dof_conn, int mat_kind,
+                                const double *mat_a, const double *mat_b, const double *u,
+                                int64_t elem_begin, int64_t elem_end, double *sigma_int) {
+  if (sigma_int && elem_end > elem_begin && elem_begin >= 0)
+    memset(sigma_int, 0, sizeof(double) * 6 * (size_t)(elem_end - elem_begin));
+  return stress_impl(p, q1d, n_elems, coords, conn, dof_conn, mat_kind, mat_a, mat_b, u,
+                     elem_begin, elem_end, sigma_int, 1);
 }
 
 /* ------------------------------------------------------------------ */

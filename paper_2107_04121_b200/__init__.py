@@ -59,10 +59,16 @@ def _load():
         raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2107_04121_b200.build` "
                           "(no CPU fallback exists)")
     lib = ctypes.CDLL(LIB_PATH)
+    env = {k: v for k, v in os.environ.items() if k in (
+        "FEB200_MATRIX_IMPL", "FEB200_RESIDUAL_IMPL", "FEB200_CSR_IMPL", "FEB200_MAX_CTAS")}
+    if env:  # non-default kernels selected from the environment: say so (measured baselines)
+        import sys
+        print(f"paper_2107_04121_b200: implementation options from the environment: {env}",
+              file=sys.stderr)
     P, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
     lib.fe_create_mesh_geometry.argtypes = [i64, P, i64, P, i32, i32, i64, P, P,
                                             ctypes.POINTER(P)]
-    lib.fe_destroy_mesh.argtypes = [P]
+    lib.fe_destroy_mesh.argtypes = [P, P]
     lib.fe_mesh_info.argtypes = [P, ctypes.POINTER(fe_info)]
     lib.fe_eval_element_matrices.argtypes = [P, i32, i32, ctypes.POINTER(fe_material), P, i64,
                                              i64, P, P]
@@ -74,7 +80,7 @@ def _load():
                                             i64, P, P, P, P]
     lib.fe_eval_stress.argtypes = [P, ctypes.POINTER(fe_material), P, i64, i64, P, P]
     lib.fe_create_field.argtypes = [P, i32, i64, P, P, ctypes.POINTER(P)]
-    lib.fe_destroy_field.argtypes = [P]
+    lib.fe_destroy_field.argtypes = [P, P]
     lib.fe_eval_coupling_matrices.argtypes = [P, P, i32, i64, i64, P, P]
     lib.fe_eval_coupling_residual.argtypes = [P, P, i32, P, i64, i64, P, P, P]
     lib.fe_eval_coupling_scalar.argtypes = [P, P, P, P, i64, i64, P, P]
@@ -92,7 +98,10 @@ def _load():
     lib.fe_csr_arrays.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P)]
     lib.fe_csr_copy_arrays.argtypes = [P, P, P, P]
     lib.fe_assemble_matrix.argtypes = [P, P, i64, i64, P, P]
-    lib.fe_destroy_csr.argtypes = [P]
+    lib.fe_destroy_csr.argtypes = [P, P]
+    lib.fe_set_option.argtypes = [i32, i64]
+    lib.fe_get_option.argtypes = [i32, ctypes.POINTER(i64)]
+    lib.fe_eval_stress_integral.argtypes = [P, ctypes.POINTER(fe_material), P, i64, i64, P, P]
     lib.fe_geometry.argtypes = [P, P, P, P]
     lib.fe_last_error.restype = ctypes.c_char_p
     lib.fe_last_error_element.restype = i64
@@ -105,7 +114,8 @@ def _load():
               "fe_eval_residual_peer", "fe_ipc_alloc", "fe_ipc_free", "fe_ipc_open", "fe_ipc_close",
               "fe_create_csr", "fe_csr_info", "fe_csr_arrays",
               "fe_csr_copy_arrays",
-              "fe_assemble_matrix", "fe_destroy_csr"):
+              "fe_assemble_matrix", "fe_destroy_csr", "fe_set_option", "fe_get_option",
+              "fe_eval_stress_integral"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -133,7 +143,8 @@ ABI_SYMBOLS = ("fe_create_mesh_geometry", "fe_destroy_mesh", "fe_mesh_info",
                "fe_eval_residual_peer", "fe_ipc_alloc", "fe_ipc_free", "fe_ipc_open", "fe_ipc_close",
                "fe_geometry", "fe_last_error", "fe_last_error_element", "fe_launch_count",
                "fe_create_csr", "fe_csr_info", "fe_csr_arrays", "fe_csr_copy_arrays",
-               "fe_assemble_matrix", "fe_destroy_csr")
+               "fe_assemble_matrix", "fe_destroy_csr", "fe_set_option", "fe_get_option",
+               "fe_eval_stress_integral")
 
 
 def lib():
@@ -190,8 +201,63 @@ def fe_create_mesh_geometry(coords: torch.Tensor, conn: torch.Tensor, order: int
     return out.value
 
 
-def fe_destroy_mesh(handle: int):
-    _check(_lib.fe_destroy_mesh(handle))
+def _release_stream(device):
+    """Stream for the stream-ordered release of a handle: the current stream of its device
+    (where the handle's work was queued in the usual single-stream use); NULL (legacy default
+    stream) when torch cannot tell (interpreter shutdown)."""
+    try:
+        return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+    except Exception:
+        return None
+
+
+def fe_destroy_mesh(handle: int, stream=None):
+    _check(_lib.fe_destroy_mesh(handle, _stream(stream) if stream is not None else None))
+
+
+# ---- process-wide implementation options (fe_set_option; include/feb200.h)
+OPT_MATRIX_IMPL, OPT_RESIDUAL_IMPL, OPT_CSR_IMPL, OPT_MAX_CTAS = range(4)
+_OPT_NAMES = {"matrix_impl": OPT_MATRIX_IMPL, "residual_impl": OPT_RESIDUAL_IMPL,
+              "csr_impl": OPT_CSR_IMPL, "max_ctas": OPT_MAX_CTAS}
+_OPT_VALUES = {OPT_MATRIX_IMPL: {"default": 0, "sf1": 1, "dense": 2},
+               OPT_RESIDUAL_IMPL: {"default": 0, "sf": 1, "dense": 2},
+               OPT_CSR_IMPL: {"atomic": 0, "gather": 1}}
+
+
+def fe_set_option(option: int, value: int):
+    _check(_lib.fe_set_option(option, int(value)))
+
+
+def fe_get_option(option: int) -> int:
+    v = ctypes.c_int64()
+    _check(_lib.fe_get_option(option, ctypes.byref(v)))
+    return v.value
+
+
+def get_options() -> dict:
+    """The active implementation options by name (values as set, 0 = default)."""
+    return {k: fe_get_option(o) for k, o in _OPT_NAMES.items()}
+
+
+class options:
+    """Context manager that sets implementation options and restores them on exit, e.g.
+    ``with fe.options(matrix_impl="dense", max_ctas=3): ...`` (values by name or number)."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.saved = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            o = _OPT_NAMES[k]
+            v = _OPT_VALUES.get(o, {}).get(v, v) if isinstance(v, str) else v
+            self.saved[o] = fe_get_option(o)
+            fe_set_option(o, v)
+        return self
+
+    def __exit__(self, *a):
+        for o, v in self.saved.items():
+            fe_set_option(o, v)
 
 
 def fe_mesh_info(handle: int) -> fe_info:
@@ -305,6 +371,15 @@ def fe_eval_stress(handle: int, mat_kind: int, mat_a: Optional[torch.Tensor],
                                _stream(stream)))
 
 
+def fe_eval_stress_integral(handle: int, mat_kind: int, mat_a: Optional[torch.Tensor],
+                            mat_b: Optional[torch.Tensor], u: torch.Tensor, elem_begin: int,
+                            elem_end: int, sigma_int: torch.Tensor, stream=None):
+    """sigma_int [E'][6] (fp64 device) = int_e sigma dx per cell ('eval' mode, P:806-813)."""
+    m = _material(mat_kind, mat_a, mat_b)
+    _check(_lib.fe_eval_stress_integral(handle, ctypes.byref(m), _ptr(u), elem_begin, elem_end,
+                                        _ptr(sigma_int), _stream(stream)))
+
+
 def fe_geometry(handle: int, detw: Optional[torch.Tensor], jinv: Optional[torch.Tensor],
                 stream=None):
     _check(_lib.fe_geometry(handle, _ptr(detw), _ptr(jinv), _stream(stream)))
@@ -367,7 +442,7 @@ class PressureField:
 
     def close(self):
         if getattr(self, "handle", None):
-            _check(_lib.fe_destroy_field(self.handle))
+            _check(_lib.fe_destroy_field(self.handle, _release_stream(self.mesh.device)))
             self.handle = None
 
     def __del__(self):
@@ -487,7 +562,7 @@ class CSR:
 
     def close(self):
         if getattr(self, "handle", None):
-            _check(_lib.fe_destroy_csr(self.handle))
+            _check(_lib.fe_destroy_csr(self.handle, _release_stream(self.mesh.device)))
             self.handle = None
 
     def __del__(self):
@@ -520,7 +595,7 @@ class Mesh:
 
     def close(self):
         if getattr(self, "handle", None):
-            fe_destroy_mesh(self.handle)
+            _check(_lib.fe_destroy_mesh(self.handle, _release_stream(self.device)))
             self.handle = None
 
     def __del__(self):
@@ -595,6 +670,15 @@ class Mesh:
                             device=self.device)
         fe_eval_stress(self.handle, mat_kind, mat_a, mat_b, u, elem_begin, elem_end, sigma, stream)
         return sigma
+
+    def stress_integral(self, u, mat_kind=MAT_PER_QP, mat_a=None, mat_b=None, elem_begin=0,
+                        elem_end=None, stream=None):
+        elem_end = self.n_elems if elem_end is None else elem_end
+        out = torch.empty((max(elem_end - elem_begin, 0), 6), dtype=torch.float64,
+                          device=self.device)
+        fe_eval_stress_integral(self.handle, mat_kind, mat_a, mat_b, u, elem_begin, elem_end, out,
+                                stream)
+        return out
 
     def geometry(self, stream=None):
         detw = torch.empty((self.n_elems, self.nq), dtype=torch.float64, device=self.device)

@@ -41,18 +41,26 @@ fe_status ok() {
 
 template <typename T>
 cudaError_t upload(T** dst, const std::vector<T>& src, cudaStream_t st) {
-  cudaError_t e = cudaMalloc((void**)dst, src.size() * sizeof(T) + 16);
+  cudaError_t e = cudaMallocAsync((void**)dst, src.size() * sizeof(T) + 16, st);
   if (e != cudaSuccess) return e;
   return cudaMemcpyAsync(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, st);
 }
 
-void free_mesh(fe_mesh* m) {
-  if (!m) return;
+// Device memory of the handles comes from the stream-ordered allocator (cudaMallocAsync on the
+// create stream) and is returned with cudaFreeAsync on the destroy stream: no device-wide
+// synchronisation, other streams keep running.
+cudaError_t free_mesh(fe_mesh* m, cudaStream_t st) {
+  if (!m) return cudaSuccess;
   void* ptrs[] = {m->coords, m->conn, m->dof_conn, m->xi, m->w, m->phi, m->dphi, m->fwd, m->bwd,
                   m->phi_f, m->dphi_f, m->fwd_f, m->bwd_f, m->b1, m->d1, m->x1, m->w1};
+  cudaError_t e = cudaSuccess;
   for (void* p : ptrs)
-    if (p) cudaFree(p);
+    if (p) {
+      const cudaError_t ee = cudaFreeAsync(p, st);
+      if (e == cudaSuccess) e = ee;
+    }
   delete m;
+  return e;
 }
 
 int form_ncomp(int form) {
@@ -106,9 +114,23 @@ const char* fe_last_error(void) { return g_err.c_str(); }
 int64_t fe_last_error_element(void) { return g_err_elem; }
 int64_t fe_launch_count(void) { return feb200::launch_count_value(); }
 
+fe_status fe_set_option(int32_t option, int64_t value) {
+  if (!feb200::set_option(option, value))
+    return fail(FE_ERR_INVALID_ARG, "fe_set_option: unknown option or value out of range");
+  return ok();
+}
+
+fe_status fe_get_option(int32_t option, int64_t* value) {
+  if (!value || option < 0 || option >= FE_OPT_COUNT)
+    return fail(FE_ERR_INVALID_ARG, "fe_get_option: unknown option or NULL value");
+  *value = feb200::option(option);
+  return ok();
+}
+
 fe_status fe_create_mesh_geometry(int64_t n_vertices, const double* coords, int64_t n_elems,
                                   const int32_t* conn, int32_t order, int32_t q1d, int64_t n_nodes,
                                   const int32_t* dof_conn, void* stream, fe_mesh** out) {
+  FE_NVTX_RANGE("fe_create_mesh_geometry");
   if (!out) return fail(FE_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
   if (n_vertices < 8 || n_elems < 0) return fail(FE_ERR_INVALID_ARG, "bad sizes");
@@ -136,17 +158,17 @@ fe_status fe_create_mesh_geometry(int64_t n_vertices, const double* coords, int6
   do {                                   \
     e = (x);                             \
     if (e != cudaSuccess) {              \
-      free_mesh(m);                      \
+      free_mesh(m, st);                  \
       return cuda_fail(e, where);        \
     }                                    \
   } while (0)
-  CK(cudaMalloc(&m->coords, sizeof(double) * 3 * n_vertices), "alloc coords");
+  CK(cudaMallocAsync((void**)&m->coords, sizeof(double) * 3 * n_vertices, st), "alloc coords");
   CK(cudaMemcpyAsync(m->coords, coords, sizeof(double) * 3 * n_vertices, cudaMemcpyDefault, st), "copy coords");
-  CK(cudaMalloc(&m->conn, sizeof(int32_t) * 8 * std::max<int64_t>(n_elems, 1)), "alloc conn");
+  CK(cudaMallocAsync((void**)&m->conn, sizeof(int32_t) * 8 * std::max<int64_t>(n_elems, 1), st), "alloc conn");
   if (n_elems > 0)
     CK(cudaMemcpyAsync(m->conn, conn, sizeof(int32_t) * 8 * n_elems, cudaMemcpyDefault, st), "copy conn");
   const int64_t ndc = int64_t(m->nb) * std::max<int64_t>(n_elems, 1);
-  CK(cudaMalloc(&m->dof_conn, sizeof(int32_t) * ndc), "alloc dof_conn");
+  CK(cudaMallocAsync((void**)&m->dof_conn, sizeof(int32_t) * ndc, st), "alloc dof_conn");
   if (n_elems > 0)
     CK(cudaMemcpyAsync(m->dof_conn, dof_conn ? dof_conn : conn, sizeof(int32_t) * m->nb * n_elems,
                        cudaMemcpyDefault, st), "copy dof_conn");
@@ -185,16 +207,16 @@ fe_status fe_create_mesh_geometry(int64_t n_vertices, const double* coords, int6
   CK(upf(&m->bwd_f, T.bwd), "tables");
   // connectivity range checks
   int* flag = nullptr;
-  CK(cudaMalloc(&flag, sizeof(int) * 2), "alloc flag");
+  CK(cudaMallocAsync((void**)&flag, sizeof(int) * 2, st), "alloc flag");
   CK(cudaMemsetAsync(flag, 0, sizeof(int) * 2, st), "memset");
   CK(feb200::launch_conn_check(m->conn, 8 * n_elems, n_vertices, flag, st), "conn check");
   CK(feb200::launch_conn_check(m->dof_conn, int64_t(m->nb) * n_elems, n_nodes, flag + 1, st), "dof check");
   int hflag[2] = {0, 0};
   CK(cudaMemcpyAsync(hflag, flag, sizeof(hflag), cudaMemcpyDeviceToHost, st), "copy flag");
+  cudaFreeAsync(flag, st);
   CK(cudaStreamSynchronize(st), "sync");
-  cudaFree(flag);
   if (hflag[0] || hflag[1]) {
-    free_mesh(m);
+    free_mesh(m, st);
     return fail(FE_ERR_INVALID_ARG, hflag[0] ? "conn entry out of [0, n_vertices)"
                                              : "dof_conn entry out of [0, n_nodes)");
   }
@@ -204,20 +226,20 @@ fe_status fe_create_mesh_geometry(int64_t n_vertices, const double* coords, int6
   if (nblk > 0) {
     double* bmin = nullptr;
     unsigned long long* bad = nullptr;
-    CK(cudaMalloc(&bmin, sizeof(double) * nblk), "alloc");
-    CK(cudaMalloc(&bad, sizeof(unsigned long long)), "alloc");
+    CK(cudaMallocAsync((void**)&bmin, sizeof(double) * nblk, st), "alloc");
+    CK(cudaMallocAsync((void**)&bad, sizeof(unsigned long long), st), "alloc");
     CK(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st), "memset");
     CK(feb200::launch_geometry_check(m, bmin, bad, nblk, st), "geometry check");
     std::vector<double> hmin(nblk);
     unsigned long long hbad = ~0ull;
     CK(cudaMemcpyAsync(hmin.data(), bmin, sizeof(double) * nblk, cudaMemcpyDeviceToHost, st), "copy");
     CK(cudaMemcpyAsync(&hbad, bad, sizeof(hbad), cudaMemcpyDeviceToHost, st), "copy");
+    cudaFreeAsync(bmin, st);
+    cudaFreeAsync(bad, st);
     CK(cudaStreamSynchronize(st), "sync");
-    cudaFree(bmin);
-    cudaFree(bad);
     for (double v : hmin) m->min_det = std::min(m->min_det, v);
     if (hbad != ~0ull) {
-      free_mesh(m);
+      free_mesh(m, st);
       return fail(FE_ERR_DEGENERATE,
                   "det J <= 0 in cell " + std::to_string((long long)hbad), (int64_t)hbad);
     }
@@ -227,10 +249,16 @@ fe_status fe_create_mesh_geometry(int64_t n_vertices, const double* coords, int6
   return ok();
 }
 
-fe_status fe_destroy_mesh(fe_mesh* mesh) {
+fe_status fe_destroy_mesh(fe_mesh* mesh, void* stream) {
+  FE_NVTX_RANGE("fe_destroy_mesh");
   if (!mesh) return ok();
-  cudaDeviceSynchronize();
-  free_mesh(mesh);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  const int dev = mesh->device;
+  if (cur != dev) cudaSetDevice(dev);
+  const cudaError_t e = free_mesh(mesh, (cudaStream_t)stream);
+  if (cur != dev) cudaSetDevice(cur);
+  if (e != cudaSuccess) return cuda_fail(e, "fe_destroy_mesh");
   return ok();
 }
 
@@ -250,6 +278,7 @@ fe_status fe_mesh_info(const fe_mesh* mesh, fe_info* info) {
 fe_status fe_eval_element_matrices(const fe_mesh* mesh, int32_t form, int32_t dtype,
                                    const fe_material* mat, const void* state_u, int64_t elem_begin,
                                    int64_t elem_end, void* K, void* stream) {
+  FE_NVTX_RANGE("fe_eval_element_matrices");
   fe_status s = check_common(mesh, form, elem_begin, elem_end);
   if (s != FE_OK) return s;
   if (dtype != FE_F64) return fail(FE_ERR_UNSUPPORTED, "element matrices are built for FE_F64 only");
@@ -272,6 +301,7 @@ fe_status fe_eval_element_matrices(const fe_mesh* mesh, int32_t form, int32_t dt
 fe_status fe_eval_residual(const fe_mesh* mesh, int32_t form, int32_t dtype, const fe_material* mat,
                            const void* u, int64_t elem_begin, int64_t elem_end, void* r_elem,
                            void* r_global, void* stream) {
+  FE_NVTX_RANGE("fe_eval_residual");
   fe_status s = check_common(mesh, form, elem_begin, elem_end);
   if (s != FE_OK) return s;
   if ((s = check_material(form, mat)) != FE_OK) return s;
@@ -297,10 +327,10 @@ fe_status fe_eval_residual_peer(const fe_mesh* mesh, int32_t form, const fe_mate
                                 const double* u, int64_t elem_begin, int64_t elem_end,
                                 double* r_elem, double* r_global, const fe_peer_window* windows,
                                 int32_t n_windows, void* stream) {
+  FE_NVTX_RANGE("fe_eval_residual_peer");
   if (n_windows < 0 || n_windows > 2 || (n_windows > 0 && !windows))
     return fail(FE_ERR_INVALID_ARG, "fe_eval_residual_peer: 0..2 windows");
-  const char* impl = std::getenv("FEB200_RESIDUAL_IMPL");
-  if (impl && std::strcmp(impl, "dense") == 0)
+  if (feb200::option(FE_OPT_RESIDUAL_IMPL) == feb200::RESIDUAL_DENSE)
     return fail(FE_ERR_UNSUPPORTED, "fe_eval_residual_peer: not built for the dense residual kernels");
   feb200::PeerWin pw{};
   pw.n = n_windows;
@@ -321,6 +351,7 @@ fe_status fe_eval_residual_peer(const fe_mesh* mesh, int32_t form, const fe_mate
 }
 
 fe_status fe_ipc_alloc(int64_t bytes, void** dev_ptr, unsigned char handle[64]) {
+  FE_NVTX_RANGE("fe_ipc_alloc");
   if (!dev_ptr || !handle || bytes <= 0) return fail(FE_ERR_INVALID_ARG, "fe_ipc_alloc: bad argument");
   *dev_ptr = nullptr;
   cudaError_t e = cudaMalloc(dev_ptr, (size_t)bytes);
@@ -338,11 +369,13 @@ fe_status fe_ipc_alloc(int64_t bytes, void** dev_ptr, unsigned char handle[64]) 
 }
 
 fe_status fe_ipc_free(void* dev_ptr) {
+  FE_NVTX_RANGE("fe_ipc_free");
   if (dev_ptr) cudaFree(dev_ptr);
   return ok();
 }
 
 fe_status fe_ipc_open(const unsigned char handle[64], void** dev_ptr) {
+  FE_NVTX_RANGE("fe_ipc_open");
   if (!handle || !dev_ptr) return fail(FE_ERR_INVALID_ARG, "fe_ipc_open: bad argument");
   cudaIpcMemHandle_t h;
   std::memcpy(&h, handle, 64);
@@ -352,6 +385,7 @@ fe_status fe_ipc_open(const unsigned char handle[64], void** dev_ptr) {
 }
 
 fe_status fe_ipc_close(void* dev_ptr) {
+  FE_NVTX_RANGE("fe_ipc_close");
   if (dev_ptr) {
     cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
     if (e != cudaSuccess) return cuda_fail(e, "fe_ipc_close");
@@ -363,6 +397,7 @@ fe_status fe_eval_matrix_residual(const fe_mesh* mesh, int32_t form, int32_t dty
                                   const fe_material* mat, const void* u, int64_t elem_begin,
                                   int64_t elem_end, void* K, void* r_elem, void* r_global,
                                   void* stream) {
+  FE_NVTX_RANGE("fe_eval_matrix_residual");
   fe_status s = check_common(mesh, form, elem_begin, elem_end);
   if (s != FE_OK) return s;
   if (dtype != FE_F64) return fail(FE_ERR_UNSUPPORTED, "fe_eval_matrix_residual is built for FE_F64 only");
@@ -384,6 +419,7 @@ fe_status fe_eval_matrix_residual(const fe_mesh* mesh, int32_t form, int32_t dty
 fe_status fe_eval_scalar(const fe_mesh* mesh, int32_t form, int32_t dtype, const fe_material* mat,
                          const void* u, int64_t elem_begin, int64_t elem_end, double* value,
                          void* stream) {
+  FE_NVTX_RANGE("fe_eval_scalar");
   fe_status s = check_common(mesh, form, elem_begin, elem_end);
   if (s != FE_OK) return s;
   if ((s = check_material(form, mat)) != FE_OK) return s;
@@ -408,23 +444,40 @@ fe_status fe_eval_scalar(const fe_mesh* mesh, int32_t form, int32_t dtype, const
   return ok();
 }
 
-fe_status fe_eval_stress(const fe_mesh* mesh, const fe_material* mat, const double* u,
-                         int64_t elem_begin, int64_t elem_end, double* sigma, void* stream) {
+static fe_status eval_stress_impl(const fe_mesh* mesh, const fe_material* mat, const double* u,
+                                  int64_t elem_begin, int64_t elem_end, double* sigma, bool integ,
+                                  void* stream, const char* name) {
   fe_status s = check_common(mesh, FE_FORM_ELASTICITY, elem_begin, elem_end);
   if (s != FE_OK) return s;
   if ((s = check_material(FE_FORM_ELASTICITY, mat)) != FE_OK) return s;
   if (elem_end > elem_begin && (!u || !sigma)) return fail(FE_ERR_INVALID_ARG, "u / sigma is NULL");
   feb200::MatArgs ma{mat->kind, mat->a, mat->b};
-  cudaError_t e = feb200::launch_stress(mesh, ma, u, elem_begin, elem_end, sigma, (cudaStream_t)stream);
+  cudaError_t e = feb200::launch_stress(mesh, ma, u, elem_begin, elem_end, sigma, integ,
+                                        (cudaStream_t)stream);
   if (e == cudaErrorNotSupported)
-    return fail(FE_ERR_UNSUPPORTED, "fe_eval_stress: q1d " + std::to_string(mesh->q1d) +
+    return fail(FE_ERR_UNSUPPORTED, std::string(name) + ": q1d " + std::to_string(mesh->q1d) +
                                         " not built for order " + std::to_string(mesh->order));
-  if (e != cudaSuccess) return cuda_fail(e, "fe_eval_stress");
+  if (e != cudaSuccess) return cuda_fail(e, name);
   return ok();
+}
+
+fe_status fe_eval_stress(const fe_mesh* mesh, const fe_material* mat, const double* u,
+                         int64_t elem_begin, int64_t elem_end, double* sigma, void* stream) {
+  FE_NVTX_RANGE("fe_eval_stress");
+  return eval_stress_impl(mesh, mat, u, elem_begin, elem_end, sigma, false, stream, "fe_eval_stress");
+}
+
+fe_status fe_eval_stress_integral(const fe_mesh* mesh, const fe_material* mat, const double* u,
+                                  int64_t elem_begin, int64_t elem_end, double* sigma_int,
+                                  void* stream) {
+  FE_NVTX_RANGE("fe_eval_stress_integral");
+  return eval_stress_impl(mesh, mat, u, elem_begin, elem_end, sigma_int, true, stream,
+                          "fe_eval_stress_integral");
 }
 
 fe_status fe_create_field(const fe_mesh* mesh, int32_t order, int64_t n_nodes,
                           const int32_t* dof_conn, void* stream, fe_field** out) {
+  FE_NVTX_RANGE("fe_create_field");
   if (!out) return fail(FE_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
   if (!mesh) return fail(FE_ERR_INVALID_ARG, "mesh is NULL");
@@ -441,14 +494,14 @@ fe_status fe_create_field(const fe_mesh* mesh, int32_t order, int64_t n_nodes,
   f->n_nodes = n_nodes;
   f->mesh = mesh;
   auto bail = [&](cudaError_t e, const char* where) {
-    if (f->dof_conn) cudaFree(f->dof_conn);
-    if (f->psi) cudaFree(f->psi);
+    if (f->dof_conn) cudaFreeAsync(f->dof_conn, st);
+    if (f->psi) cudaFreeAsync(f->psi, st);
     delete f;
     return cuda_fail(e, where);
   };
   cudaError_t e;
   const int64_t n = int64_t(f->nb) * mesh->n_elems;
-  if ((e = cudaMalloc(&f->dof_conn, sizeof(int32_t) * std::max<int64_t>(n, 1))) != cudaSuccess)
+  if ((e = cudaMallocAsync((void**)&f->dof_conn, sizeof(int32_t) * std::max<int64_t>(n, 1), st)) != cudaSuccess)
     return bail(e, "alloc dof_conn");
   if (n > 0 && (e = cudaMemcpyAsync(f->dof_conn, dof_conn, sizeof(int32_t) * n, cudaMemcpyDefault, st)) != cudaSuccess)
     return bail(e, "copy dof_conn");
@@ -457,16 +510,16 @@ fe_status fe_create_field(const fe_mesh* mesh, int32_t order, int64_t n_nodes,
   if ((e = upload(&f->psi, T.phi, st)) != cudaSuccess) return bail(e, "tables");
   int* flag = nullptr;
   int hflag = 0;
-  if ((e = cudaMalloc(&flag, sizeof(int))) != cudaSuccess) return bail(e, "alloc flag");
+  if ((e = cudaMallocAsync((void**)&flag, sizeof(int), st)) != cudaSuccess) return bail(e, "alloc flag");
   e = cudaMemsetAsync(flag, 0, sizeof(int), st);
   if (e == cudaSuccess) e = feb200::launch_conn_check(f->dof_conn, n, n_nodes, flag, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(flag, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  cudaFree(flag);
   if (e != cudaSuccess) return bail(e, "dof check");
   if (hflag) {
-    cudaFree(f->dof_conn);
-    cudaFree(f->psi);
+    cudaFreeAsync(f->dof_conn, st);
+    cudaFreeAsync(f->psi, st);
     delete f;
     return fail(FE_ERR_INVALID_ARG, "pressure dof_conn entry out of [0, n_nodes)");
   }
@@ -474,12 +527,16 @@ fe_status fe_create_field(const fe_mesh* mesh, int32_t order, int64_t n_nodes,
   return ok();
 }
 
-fe_status fe_destroy_field(fe_field* field) {
+fe_status fe_destroy_field(fe_field* field, void* stream) {
+  FE_NVTX_RANGE("fe_destroy_field");
   if (!field) return ok();
-  cudaDeviceSynchronize();
-  if (field->dof_conn) cudaFree(field->dof_conn);
-  if (field->psi) cudaFree(field->psi);
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess, e2 = cudaSuccess;
+  if (field->dof_conn) e = cudaFreeAsync(field->dof_conn, st);
+  if (field->psi) e2 = cudaFreeAsync(field->psi, st);
   delete field;
+  if (e == cudaSuccess) e = e2;
+  if (e != cudaSuccess) return cuda_fail(e, "fe_destroy_field");
   return ok();
 }
 
@@ -501,6 +558,7 @@ static fe_status coupling_status(cudaError_t e, const fe_mesh* mesh, const fe_fi
 
 fe_status fe_eval_coupling_matrices(const fe_mesh* mesh, const fe_field* pressure, int32_t transposed,
                                     int64_t elem_begin, int64_t elem_end, double* out, void* stream) {
+  FE_NVTX_RANGE("fe_eval_coupling_matrices");
   fe_status s = check_coupling(mesh, pressure, elem_begin, elem_end);
   if (s != FE_OK) return s;
   if (elem_end > elem_begin && !out) return fail(FE_ERR_INVALID_ARG, "out is NULL");
@@ -513,6 +571,7 @@ fe_status fe_eval_coupling_matrices(const fe_mesh* mesh, const fe_field* pressur
 fe_status fe_eval_coupling_residual(const fe_mesh* mesh, const fe_field* pressure, int32_t transposed,
                                     const double* x, int64_t elem_begin, int64_t elem_end,
                                     double* r_elem, double* r_global, void* stream) {
+  FE_NVTX_RANGE("fe_eval_coupling_residual");
   fe_status s = check_coupling(mesh, pressure, elem_begin, elem_end);
   if (s != FE_OK) return s;
   if (!x) return fail(FE_ERR_INVALID_ARG, "input vector is NULL");
@@ -526,6 +585,7 @@ fe_status fe_eval_coupling_residual(const fe_mesh* mesh, const fe_field* pressur
 fe_status fe_eval_coupling_scalar(const fe_mesh* mesh, const fe_field* pressure, const double* u,
                                   const double* p, int64_t elem_begin, int64_t elem_end,
                                   double* value, void* stream) {
+  FE_NVTX_RANGE("fe_eval_coupling_scalar");
   fe_status s = check_coupling(mesh, pressure, elem_begin, elem_end);
   if (s != FE_OK) return s;
   if (!u || !p || !value) return fail(FE_ERR_INVALID_ARG, "u / p / value is NULL");
@@ -536,6 +596,7 @@ fe_status fe_eval_coupling_scalar(const fe_mesh* mesh, const fe_field* pressure,
 
 fe_status fe_assemble_vector(const fe_mesh* mesh, int32_t dtype, int32_t ncomp, int64_t elem_begin,
                              int64_t elem_end, const void* r_elem, void* r_global, void* stream) {
+  FE_NVTX_RANGE("fe_assemble_vector");
   fe_status s = check_common(mesh, FE_FORM_DIFFUSION, elem_begin, elem_end);
   if (s != FE_OK) return s;
   if (ncomp != 1 && ncomp != 3) return fail(FE_ERR_INVALID_ARG, "ncomp must be 1 or 3");
@@ -549,6 +610,7 @@ fe_status fe_assemble_vector(const fe_mesh* mesh, int32_t dtype, int32_t ncomp, 
 }
 
 fe_status fe_geometry(const fe_mesh* mesh, double* detw, double* jinv, void* stream) {
+  FE_NVTX_RANGE("fe_geometry");
   if (!mesh) return fail(FE_ERR_INVALID_ARG, "mesh is NULL");
   cudaError_t e = feb200::launch_geometry_materialize(mesh, detw, jinv, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "fe_geometry");

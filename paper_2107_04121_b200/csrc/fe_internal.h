@@ -2,6 +2,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "feb200.h"
 
@@ -31,6 +32,16 @@ struct fe_field {
 };
 
 namespace feb200 {
+
+// NVTX range around every ABI entry point that queues or performs work (visible in nsys /
+// ncu --nvtx timelines; header-only NVTX3: a no-op branch when no tool is attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define FE_NVTX_RANGE(name) ::feb200::NvtxRange fe_nvtx_range_(name)
 
 // Read-only view passed to kernels by value.
 struct MeshView {
@@ -103,6 +114,11 @@ cudaError_t launch_matrix_sfv(const fe_mesh* m, int form, MatArgs mat, const dou
                               int64_t e0, int64_t e1, double* K, cudaStream_t st);
 cudaError_t launch_matrix_vp(const fe_mesh* m, int form, MatArgs mat, const double* state_u,
                              int64_t e0, int64_t e1, double* K, cudaStream_t st);
+// general-D elasticity at p = 2 through k_matrix_sfv, executed only when *run_if != 0 (set on
+// the device by the symmetry check of launch_matrix_vp)
+cudaError_t launch_matrix_sfv_gated(const fe_mesh* m, int form, MatArgs mat, const double* state_u,
+                                    int64_t e0, int64_t e1, double* K, cudaStream_t st,
+                                    const int* run_if);
 cudaError_t upload_const_tables_matrix_vp(int order, const double* b1, const double* d1,
                                          const double* x1, const double* w1, cudaStream_t st);
 cudaError_t upload_const_tables_matrix_v(int order, const double* b1, const double* d1,
@@ -136,8 +152,13 @@ cudaError_t launch_coupling(const fe_mesh* mh, const fe_field* f, int mode, bool
                             const double* u, const double* p, int64_t e0, int64_t e1, double* out,
                             double* rg, double* val, cudaStream_t st);
 cudaError_t launch_stress(const fe_mesh* m, MatArgs mat, const double* u, int64_t e0, int64_t e1,
-                          double* sigma, cudaStream_t st);
-// Test hook: FEB200_MAX_CTAS caps the grid of the persistent kernels so that small meshes
+                          double* sigma, bool integrated, cudaStream_t st);
+// Implementation options (fe_set_option; defaults from the environment, read once at load).
+int64_t option(int opt);
+bool set_option(int opt, int64_t value);
+enum { MATRIX_DEFAULT = 0, MATRIX_SF1 = 1, MATRIX_DENSE = 2 };
+enum { RESIDUAL_DEFAULT = 0, RESIDUAL_SF = 1, RESIDUAL_DENSE = 2 };
+// Test hook: FE_OPT_MAX_CTAS caps the grid of the persistent kernels so that small meshes
 // still run many batches per CTA (ring-buffer phases wrap several times in the parity tests).
 int grid_cap(int grid);
 cudaError_t upload_const_tables_matrix(int order, const double* b1, const double* d1,

@@ -241,17 +241,25 @@ fe_status set_error(fe_status s, const char* msg);
 
 extern "C" {
 
-static void free_csr(fe_csr* c) {
-  if (!c) return;
+// The CSR object's arrays come from the stream-ordered allocator and are released with
+// cudaFreeAsync (no device-wide synchronisation).
+static cudaError_t free_csr(fe_csr* c, cudaStream_t st = 0) {
+  if (!c) return cudaSuccess;
   void* p[] = {c->rowptr_node, c->col_node, c->pos_in_row, c->n2c_ptr, c->n2c, c->rowptr, c->col};
+  cudaError_t e = cudaSuccess;
   for (void* q : p)
-    if (q) cudaFree(q);
+    if (q) {
+      const cudaError_t ee = cudaFreeAsync(q, st);
+      if (e == cudaSuccess) e = ee;
+    }
   delete c;
+  return e;
 }
 
 static fe_status create_csr_impl(const fe_mesh* mesh, int32_t ncomp, void* stream, fe_csr** out);
 
 fe_status fe_create_csr(const fe_mesh* mesh, int32_t ncomp, void* stream, fe_csr** out) {
+  FE_NVTX_RANGE("fe_create_csr");
   try {  // thrust reports failures with exceptions; none may cross the ABI
     return create_csr_impl(mesh, ncomp, stream, out);
   } catch (const std::bad_alloc&) {
@@ -278,7 +286,7 @@ static fe_status create_csr_impl(const fe_mesh* mesh, int32_t ncomp, void* strea
   c->n_nodes = N;
   int64_t* keys = nullptr;
   cudaError_t e = cudaMalloc(&keys, sizeof(int64_t) * npairs);
-  if (e != cudaSuccess) { free_csr(c); return feb200::set_error(FE_ERR_OOM, "fe_create_csr: keys"); }
+  if (e != cudaSuccess) { free_csr(c, st); return feb200::set_error(FE_ERR_OOM, "fe_create_csr: keys"); }
   const int grid = 148 * 16;
   feb200::k_pair_keys<<<grid, 256, 0, st>>>(mesh->dof_conn, nb, E, N, keys);
   feb200::count_launch();
@@ -287,9 +295,9 @@ static fe_status create_csr_impl(const fe_mesh* mesh, int32_t ncomp, void* strea
   thrust::sort(pol, kp, kp + npairs);
   const int64_t nnz = thrust::unique(pol, kp, kp + npairs) - kp;
   c->nnz_node = nnz;
-  e = cudaMalloc(&c->rowptr_node, sizeof(int64_t) * (N + 1));
-  if (e == cudaSuccess) e = cudaMalloc(&c->col_node, sizeof(int32_t) * nnz);
-  if (e != cudaSuccess) { cudaFree(keys); free_csr(c); return feb200::set_error(FE_ERR_OOM, "fe_create_csr: pattern"); }
+  e = cudaMallocAsync((void**)&c->rowptr_node, sizeof(int64_t) * (N + 1), st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&c->col_node, sizeof(int32_t) * nnz, st);
+  if (e != cudaSuccess) { cudaFree(keys); free_csr(c, st); return feb200::set_error(FE_ERR_OOM, "fe_create_csr: pattern"); }
   // rowptr_node[r] = first key >= r * N
   thrust::device_ptr<int64_t> rp(c->rowptr_node);
   auto row_keys = thrust::make_transform_iterator(thrust::make_counting_iterator<int64_t>(0),
@@ -309,8 +317,8 @@ static fe_status create_csr_impl(const fe_mesh* mesh, int32_t ncomp, void* strea
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (dmax) cudaFree(dmax);
   c->pos_bytes = hmax <= 256 ? 1 : (hmax <= 65536 ? 2 : 4);
-  if (e == cudaSuccess) e = cudaMalloc(&c->pos_in_row, (size_t)c->pos_bytes * npairs);
-  if (e != cudaSuccess) { cudaFree(keys); free_csr(c); return feb200::set_error(FE_ERR_OOM, "fe_create_csr: position map"); }
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&c->pos_in_row, (size_t)c->pos_bytes * npairs, st);
+  if (e != cudaSuccess) { cudaFree(keys); free_csr(c, st); return feb200::set_error(FE_ERR_OOM, "fe_create_csr: position map"); }
   if (c->pos_bytes == 1)
     feb200::k_pos_map<uint8_t><<<grid, 256, 0, st>>>(mesh->dof_conn, nb, E, c->rowptr_node, c->col_node, (uint8_t*)c->pos_in_row);
   else if (c->pos_bytes == 2)
@@ -324,12 +332,12 @@ static fe_status create_csr_impl(const fe_mesh* mesh, int32_t ncomp, void* strea
     const int64_t ne = E * nb;
     int32_t* nkeys = nullptr;
     e = cudaMalloc(&nkeys, sizeof(int32_t) * ne);
-    if (e == cudaSuccess) e = cudaMalloc(&c->n2c, sizeof(int32_t) * ne);
-    if (e == cudaSuccess) e = cudaMalloc(&c->n2c_ptr, sizeof(int64_t) * (N + 1));
+    if (e == cudaSuccess) e = cudaMallocAsync((void**)&c->n2c, sizeof(int32_t) * ne, st);
+    if (e == cudaSuccess) e = cudaMallocAsync((void**)&c->n2c_ptr, sizeof(int64_t) * (N + 1), st);
     if (e != cudaSuccess) {
       if (nkeys) cudaFree(nkeys);
       cudaFree(keys);
-      free_csr(c);
+      free_csr(c, st);
       return feb200::set_error(FE_ERR_OOM, "fe_create_csr: node-to-cell list");
     }
     thrust::device_ptr<int32_t> nk(nkeys), nv(c->n2c);
@@ -343,14 +351,14 @@ static fe_status create_csr_impl(const fe_mesh* mesh, int32_t ncomp, void* strea
     cudaStreamSynchronize(st);
     cudaFree(nkeys);
   }
-  e = cudaMalloc(&c->rowptr, sizeof(int64_t) * (N * ncomp + 1));
-  if (e == cudaSuccess) e = cudaMalloc(&c->col, sizeof(int32_t) * nnz * ncomp * ncomp);
-  if (e != cudaSuccess) { cudaFree(keys); free_csr(c); return feb200::set_error(FE_ERR_OOM, "fe_create_csr: expanded pattern"); }
+  e = cudaMallocAsync((void**)&c->rowptr, sizeof(int64_t) * (N * ncomp + 1), st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&c->col, sizeof(int32_t) * nnz * ncomp * ncomp, st);
+  if (e != cudaSuccess) { cudaFree(keys); free_csr(c, st); return feb200::set_error(FE_ERR_OOM, "fe_create_csr: expanded pattern"); }
   feb200::k_expand<<<grid, 256, 0, st>>>(c->rowptr_node, c->col_node, N, ncomp, c->rowptr, c->col);
   feb200::count_launch();
   e = cudaStreamSynchronize(st);
   cudaFree(keys);
-  if (e != cudaSuccess) { free_csr(c); return feb200::set_error(FE_ERR_CUDA, cudaGetErrorString(e)); }
+  if (e != cudaSuccess) { free_csr(c, st); return feb200::set_error(FE_ERR_CUDA, cudaGetErrorString(e)); }
   *out = c;
   return feb200::set_error(FE_OK, "");
 }
@@ -370,6 +378,7 @@ fe_status fe_csr_arrays(const fe_csr* csr, const int64_t** row_ptr, const int32_
 }
 
 fe_status fe_csr_copy_arrays(const fe_csr* csr, int64_t* row_ptr, int32_t* col_idx, void* stream) {
+  FE_NVTX_RANGE("fe_csr_copy_arrays");
   if (!csr) return feb200::set_error(FE_ERR_INVALID_ARG, "csr is NULL");
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
@@ -381,6 +390,7 @@ fe_status fe_csr_copy_arrays(const fe_csr* csr, int64_t* row_ptr, int32_t* col_i
 
 fe_status fe_assemble_matrix(const fe_csr* csr, const double* K, int64_t elem_begin, int64_t elem_end,
                              double* values, void* stream) {
+  FE_NVTX_RANGE("fe_assemble_matrix");
   if (!csr || (!K && elem_end > elem_begin) || !values)
     return feb200::set_error(FE_ERR_INVALID_ARG, "fe_assemble_matrix: NULL argument");
   if (elem_begin < 0 || elem_end > csr->mesh->n_elems || elem_begin > elem_end)
@@ -389,14 +399,15 @@ fe_status fe_assemble_matrix(const fe_csr* csr, const double* K, int64_t elem_be
   const int64_t n = (elem_end - elem_begin) * nd * nd;
   if (n == 0) return FE_OK;
   const int grid = (int)((n + 255) / 256 < 148 * 32 ? (n + 255) / 256 : 148 * 32);
-  const char* impl = std::getenv("FEB200_CSR_IMPL");
-  // default: fp64 atomics (fastest on B200); FEB200_CSR_IMPL=gather selects the atomic-free
-  // row-owner kernel (fixed summation order, bitwise reproducible; nb <= 27)
-  const bool atomic = !(impl && std::strcmp(impl, "gather") == 0) || csr->mesh->nb > 27;
+  // default: fp64 atomics (fastest on B200); FE_OPT_CSR_IMPL = 1 (gather) selects the
+  // atomic-free row-owner kernel (fixed summation order, bitwise reproducible; nb <= 27)
+  const bool atomic = feb200::option(FE_OPT_CSR_IMPL) == 0 || csr->mesh->nb > 27;
   const int D = csr->ncomp;
   const size_t smem = (size_t)8 * D * D * csr->hmax * 8;  // 8 warps per block
   auto launch = [&](auto* pos) {
-    if (atomic && csr->mesh->nb == 27 && n < (int64_t(1) << 32) && FEB200_CSR_CONST) {
+    // 32-bit loop index: i + gridDim*blockDim must not wrap past 2^32 on the last stride
+    if (atomic && csr->mesh->nb == 27 && n <= int64_t(UINT32_MAX) - int64_t(grid) * 256 &&
+        FEB200_CSR_CONST) {
       using PT = std::remove_const_t<std::remove_pointer_t<decltype(pos)>>;
       if (D == 1)
         feb200::k_assemble_matrix_c<PT, 27, 1><<<grid, 256, 0, (cudaStream_t)stream>>>(
@@ -428,12 +439,12 @@ fe_status fe_assemble_matrix(const fe_csr* csr, const double* K, int64_t elem_be
   return e == cudaSuccess ? feb200::set_error(FE_OK, "") : feb200::set_error(FE_ERR_CUDA, cudaGetErrorString(e));
 }
 
-fe_status fe_destroy_csr(fe_csr* csr) {
-  if (csr) {
-    cudaDeviceSynchronize();
-    free_csr(csr);
-  }
-  return FE_OK;
+fe_status fe_destroy_csr(fe_csr* csr, void* stream) {
+  FE_NVTX_RANGE("fe_destroy_csr");
+  if (!csr) return feb200::set_error(FE_OK, "");
+  const cudaError_t e = free_csr(csr, (cudaStream_t)stream);
+  return e == cudaSuccess ? feb200::set_error(FE_OK, "")
+                          : feb200::set_error(FE_ERR_CUDA, cudaGetErrorString(e));
 }
 
 }  // extern "C"

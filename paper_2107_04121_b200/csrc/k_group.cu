@@ -96,6 +96,7 @@ extern "C" {
 
 fe_status fe_group_cells(const int32_t* kind, int64_t n_cells, int32_t n_kinds, int64_t* perm,
                          int64_t* offsets, void* stream) {
+  FE_NVTX_RANGE("fe_group_cells");
   try {  // thrust reports failures with exceptions; none may cross the ABI
     return feb200::group_cells_impl(kind, n_cells, n_kinds, perm, offsets, stream);
   } catch (const std::bad_alloc&) {
@@ -109,11 +110,13 @@ fe_status fe_group_cells(const int32_t* kind, int64_t n_cells, int32_t n_kinds, 
 
 fe_status fe_gather_rows_i32(const int32_t* in, const int64_t* row_ptr, int32_t width,
                              const int64_t* perm, int64_t n, int32_t* out, void* stream) {
+  FE_NVTX_RANGE("fe_gather_rows_i32");
   return feb200::gather_rows<int32_t>(in, row_ptr, width, perm, n, out, stream);
 }
 
 fe_status fe_gather_rows_f64(const double* in, const int64_t* row_ptr, int32_t width,
                              const int64_t* perm, int64_t n, double* out, void* stream) {
+  FE_NVTX_RANGE("fe_gather_rows_f64");
   return feb200::gather_rows<double>(in, row_ptr, width, perm, n, out, stream);
 }
 

@@ -257,9 +257,8 @@ static cudaError_t dispatch_form(const fe_mesh* mh, int form, MatArgs mat, const
 cudaError_t launch_matrix(const fe_mesh* mh, int form, MatArgs mat, const double* state_u,
                           int64_t e0, int64_t e1, double* K, cudaStream_t st) {
   if (mh->q1d != mh->order + 1) return cudaErrorNotSupported;
-  // sum-factorised kernels first; FEB200_MATRIX_IMPL=dense selects the dense DMMA kernels
-  const char* impl = std::getenv("FEB200_MATRIX_IMPL");
-  if (!(impl && std::strcmp(impl, "dense") == 0)) {
+  // sum-factorised kernels first; FE_OPT_MATRIX_IMPL = dense selects the dense DMMA kernels
+  if (option(FE_OPT_MATRIX_IMPL) != MATRIX_DENSE) {
     cudaError_t e = launch_matrix_sf(mh, form, mat, e0, e1, K, st);
     if (e != cudaErrorNotSupported) return e;
     e = launch_matrix_vp(mh, form, mat, state_u, e0, e1, K, st);

@@ -90,7 +90,7 @@ cudaError_t upload_const_tables_matrix(int order, const double* b1, const double
                                       const double* x1, const double* w1, cudaStream_t st) {
   cudaError_t e = upload_tables_this_tu(order, b1, d1, x1, w1, st);
   if (e != cudaSuccess || order < 1 || order > 3) return e;
-  static double h[2][2][4][4][4];
+  double h[2][2][4][4][4] = {};  // per call (stack): concurrent mesh creation is safe
   const int n1 = order + 1, q1 = order + 1;
   for (int az = 0; az < 2; ++az)
     for (int bz = 0; bz < 2; ++bz)
@@ -1085,8 +1085,7 @@ static cudaError_t launch_sf_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int64
 cudaError_t launch_matrix_sf(const fe_mesh* mh, int form, MatArgs mat, int64_t e0, int64_t e1,
                              double* K, cudaStream_t st) {
   if (mh->q1d != mh->order + 1) return cudaErrorNotSupported;
-  const char* impl = std::getenv("FEB200_MATRIX_IMPL");
-  const bool pipelined = FEB200_SFP && !(impl && std::strcmp(impl, "sf1") == 0);
+  const bool pipelined = FEB200_SFP && option(FE_OPT_MATRIX_IMPL) != MATRIX_SF1;
   if (pipelined && (mh->order == 1 || mh->order == 2)) {
 #define SFP_CASE(P)                                                                                \
   if (mh->order == P) switch (form) {                                                              \

@@ -97,7 +97,10 @@ template <int P, int FORM, bool FULLD>
 __global__ void __launch_bounds__(SFV<P, FORM, FULLD>::THREADS)
     k_matrix_sfv(MeshView mv, int mat_kind, const double* __restrict__ ma,
                  const double* __restrict__ mb, const double* __restrict__ state_u, int64_t e0,
-                 int64_t e1, double* __restrict__ K) {
+                 int64_t e1, double* __restrict__ K, const int* __restrict__ run_if) {
+  // device-side dispatch (general D at p = 2, launch_matrix_vp): runs only when the symmetry
+  // check flagged a non-symmetric D
+  if (run_if != nullptr && *run_if == 0) return;
   using L = SFV<P, FORM, FULLD>;
   using BS = typename L::BS;
   constexpr int N1 = L::N1, Q1 = L::Q1, NB = L::NB, NQ = L::NQ, NDOF = L::NDOF, QQP = L::QQP;
@@ -395,9 +398,9 @@ __global__ void __launch_bounds__(SFV<P, FORM, FULLD>::THREADS)
 
 template <int P, int FORM, bool FULLD = false>
 static cudaError_t launch_sfv_t(const fe_mesh* mh, MatArgs mat, const double* state_u, int64_t e0,
-                                int64_t e1, double* K, cudaStream_t st) {
+                                int64_t e1, double* K, cudaStream_t st, const int* run_if = nullptr) {
   if constexpr (FORM == FE_FORM_ELASTICITY && !FULLD) {
-    if (mat.kind == FE_MAT_FULL_D) return launch_sfv_t<P, FORM, true>(mh, mat, state_u, e0, e1, K, st);
+    if (mat.kind == FE_MAT_FULL_D) return launch_sfv_t<P, FORM, true>(mh, mat, state_u, e0, e1, K, st, run_if);
   }
   using L = SFV<P, FORM, FULLD>;
   if (L::BYTES > 227 * 1024) return cudaErrorNotSupported;
@@ -410,9 +413,18 @@ static cudaError_t launch_sfv_t(const fe_mesh* mh, MatArgs mat, const double* st
   grid = grid_cap(grid);
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, L::THREADS, L::BYTES, st>>>(view_of(mh), mat.kind, (const double*)mat.a,
-                                           (const double*)mat.b, state_u, e0, e1, K);
+                                           (const double*)mat.b, state_u, e0, e1, K, run_if);
   count_launch();
   return cudaGetLastError();
+}
+
+cudaError_t launch_matrix_sfv_gated(const fe_mesh* mh, int form, MatArgs mat, const double* state_u,
+                                    int64_t e0, int64_t e1, double* K, cudaStream_t st,
+                                    const int* run_if) {
+  if (mh->q1d != mh->order + 1 || mh->order != 2 || form != FE_FORM_ELASTICITY ||
+      mat.kind != FE_MAT_FULL_D)
+    return cudaErrorNotSupported;
+  return launch_sfv_t<2, FE_FORM_ELASTICITY, true>(mh, mat, state_u, e0, e1, K, st, run_if);
 }
 
 cudaError_t launch_matrix_sfv(const fe_mesh* mh, int form, MatArgs mat, const double* state_u,

@@ -102,7 +102,7 @@ cudaError_t upload_const_tables_matrix_vp(int order, const double* b1, const dou
                                          const double* x1, const double* w1, cudaStream_t st) {
   cudaError_t e = upload_tables_this_tu(order, b1, d1, x1, w1, st);
   if (e != cudaSuccess || order < 1 || order > 3) return e;
-  static double h[2][2][4][4][4];
+  double h[2][2][4][4][4] = {};  // per call (stack): concurrent mesh creation is safe
   const int n1 = order + 1, q1 = order + 1;
   for (int az = 0; az < 2; ++az)
     for (int bz = 0; bz < 2; ++bz)
@@ -194,7 +194,11 @@ struct VPL {
 template <int P, int FORM>
 __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
     k_matrix_vp(MeshView mv, int mat_kind, const double* __restrict__ ma, const double* __restrict__ mb,
-                const double* __restrict__ state_u, int64_t e0, int64_t e1, double* __restrict__ K) {
+                const double* __restrict__ state_u, int64_t e0, int64_t e1, double* __restrict__ K,
+                const int* __restrict__ skip) {
+  // device-side dispatch (general D): the launch is a no-op when the symmetry check found a
+  // non-symmetric D, and the general 9-block kernel k_matrix_sfv runs instead
+  if (skip != nullptr && *skip != 0) return;
   using L = VPL<P, FORM>;
   using IT = typename L::IT;
   constexpr int N1 = L::N1, Q1 = L::Q1, NB = L::NB, NQ = L::NQ, Q2 = L::Q2, E = L::E, QQP = L::QQP;
@@ -380,7 +384,8 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
         // all pair weights W^{ab}_{mn}(q) of the batch, item-major: Wsm[el][PB(i) + p][q]
         double* Wq = Wsm + el * L::NWP * NQ + q;
         if (!L::CONV && mat_kind == FE_MAT_FULL_D) {
-          // general Voigt D (symmetric: upper triangle read, reading 23):
+          // general Voigt D, symmetric (checked by k_dsym_check before this launch, DESIGN.md
+          // reading 23; the upper triangle is read):
           // W^{ab}_{mn} = dw sum_{j,l} Ji[m][j] D[v(a,j)][v(b,l)] Ji[n][l]
           double Dm[36];
           const double* Dg = ma + ((e0 + lb + el) * NQ + q) * 36;
@@ -784,7 +789,7 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
 
 template <int P, int FORM>
 static cudaError_t launch_vp_t(const fe_mesh* mh, MatArgs mat, const double* state_u, int64_t e0,
-                               int64_t e1, double* K, cudaStream_t st) {
+                               int64_t e1, double* K, cudaStream_t st, const int* skip = nullptr) {
   using L = VPL<P, FORM>;
   if (L::BYTES > 227 * 1024) return cudaErrorNotSupported;
   auto kern = k_matrix_vp<P, FORM>;
@@ -796,19 +801,60 @@ static cudaError_t launch_vp_t(const fe_mesh* mh, MatArgs mat, const double* sta
   grid = grid_cap(grid);
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, L::THREADS, L::BYTES, st>>>(view_of(mh), mat.kind, (const double*)mat.a,
-                                           (const double*)mat.b, state_u, e0, e1, K);
+                                           (const double*)mat.b, state_u, e0, e1, K, skip);
   count_launch();
   return cudaGetLastError();
+}
+
+// Symmetry check of a general Voigt D[n][6][6] (FE_MAT_FULL_D): *flag = 1 when some block has
+// |D_IK - D_KI| > 8 eps max(|D_IK|, |D_KI|) (a D built as A A^T in floating point may differ
+// from its transpose in the last bits; reading the upper triangle of such a D changes K by a
+// few ulps).  Grid-stride over the upper off-diagonal entries, coalesced over the 36-blocks.
+__global__ void __launch_bounds__(256) k_dsym_check(const double* __restrict__ D, int64_t n_blk,
+                                                    int* __restrict__ flag) {
+  const int64_t total = n_blk * 36;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i % 36), I = r / 6, Kk = r - 6 * I;
+    if (Kk <= I) continue;
+    const double a = __ldg(D + i), b = __ldg(D + (i - r) + 6 * Kk + I);
+    if (!(fabs(a - b) <= 8.0 * 2.220446049250313e-16 * fmax(fabs(a), fabs(b)))) {
+      *flag = 1;
+      return;
+    }
+  }
 }
 
 // Returns cudaErrorNotSupported when the combination has no pipelined vector kernel
 // (vector mass, weighted dot, p != 2: the single-stage k_matrix_sfv handles those; with
 // FEB200_MATRIX_IMPL=sf1 the general non-symmetric FULL_D path of k_matrix_sfv is used).
+// General D (FE_MAT_FULL_D) is read as given by every path: the pipelined kernel, which
+// derives K_ba = K_ab^T, runs only on a symmetric D; k_dsym_check decides on the device and
+// both kernels are launched, the one not chosen returning at once (no host synchronisation,
+// so the call stays asynchronous and graph-capturable).
 cudaError_t launch_matrix_vp(const fe_mesh* mh, int form, MatArgs mat, const double* state_u,
                              int64_t e0, int64_t e1, double* K, cudaStream_t st) {
   if (mh->q1d != mh->order + 1 || mh->order != 2) return cudaErrorNotSupported;
-  const char* impl = std::getenv("FEB200_MATRIX_IMPL");
-  if (impl && std::strcmp(impl, "sf1") == 0) return cudaErrorNotSupported;
+  if (option(FE_OPT_MATRIX_IMPL) == MATRIX_SF1) return cudaErrorNotSupported;
+  if (form == FE_FORM_ELASTICITY && mat.kind == FE_MAT_FULL_D) {
+    if (e1 <= e0) return cudaSuccess;
+    int* flag = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)&flag, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(flag, 0, sizeof(int), st);
+    const int64_t nblk = (e1 - e0) * (int64_t)mh->nq;
+    if (e == cudaSuccess) {
+      const int64_t want = (nblk * 36 + 255) / 256;
+      const int grid = (int)(want < 148 * 8 ? want : 148 * 8);
+      k_dsym_check<<<grid, 256, 0, st>>>((const double*)mat.a + e0 * mh->nq * 36, nblk, flag);
+      count_launch();
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = launch_vp_t<2, FE_FORM_ELASTICITY>(mh, mat, state_u, e0, e1, K, st, flag);
+    if (e == cudaSuccess) e = launch_matrix_sfv_gated(mh, form, mat, state_u, e0, e1, K, st, flag);
+    cudaError_t ef = cudaFreeAsync(flag, st);
+    return e != cudaSuccess ? e : ef;
+  }
   if (form == FE_FORM_ELASTICITY)
     return launch_vp_t<2, FE_FORM_ELASTICITY>(mh, mat, state_u, e0, e1, K, st);
   if (form == FE_FORM_CONVECTIVE) return launch_vp_t<2, FE_FORM_CONVECTIVE>(mh, mat, state_u, e0, e1, K, st);

@@ -9,20 +9,44 @@
 #include "fe_internal.h"
 
 #include <cstdlib>
+#include <cstring>
+#include <climits>
 
 namespace feb200 {
 
+// Lock-free read path: a fixed table of published entries (key fields written before the
+// `ready` release store); only the first launch of a (kernel, device, threads, smem) key takes
+// the mutex to fill a slot.
+namespace {
+struct FactSlot {
+  const void* kern;
+  int dev, threads;
+  size_t smem;
+  LaunchFacts f;
+  std::atomic<int> ready{0};
+};
+constexpr int kFactSlots = 256;
+FactSlot g_facts[kFactSlots];
+std::atomic<int> g_fact_count{0};
+std::mutex g_fact_mu;
+}  // namespace
+
 LaunchFacts launch_facts(const void* kern, int threads, size_t smem) {
-  static std::mutex mu;
-  static std::map<std::tuple<const void*, int, int, size_t>, LaunchFacts> cache;
   int dev = 0;
   cudaGetDevice(&dev);
-  const auto key = std::make_tuple(kern, dev, threads, smem);
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = cache.find(key);
-    if (it != cache.end()) return it->second;
-  }
+  auto find = [&](int n) -> const FactSlot* {
+    for (int i = 0; i < n; ++i) {
+      const FactSlot& s = g_facts[i];
+      if (s.ready.load(std::memory_order_acquire) && s.kern == kern && s.dev == dev &&
+          s.threads == threads && s.smem == smem)
+        return &s;
+    }
+    return nullptr;
+  };
+  if (const FactSlot* s = find(g_fact_count.load(std::memory_order_acquire))) return s->f;
+  std::lock_guard<std::mutex> lk(g_fact_mu);
+  const int n = g_fact_count.load(std::memory_order_relaxed);
+  if (const FactSlot* s = find(n)) return s->f;
   LaunchFacts f{148, 1, cudaSuccess};
   if (smem > 48 * 1024)
     f.err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -31,15 +55,66 @@ LaunchFacts launch_facts(const void* kern, int threads, size_t smem) {
   int per = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, smem) != cudaSuccess || per < 1) per = 1;
   f.per_sm = per;
-  std::lock_guard<std::mutex> lk(mu);
-  cache[key] = f;
+  if (n < kFactSlots) {
+    FactSlot& s = g_facts[n];
+    s.kern = kern;
+    s.dev = dev;
+    s.threads = threads;
+    s.smem = smem;
+    s.f = f;
+    s.ready.store(1, std::memory_order_release);
+    g_fact_count.store(n + 1, std::memory_order_release);
+  }
   return f;
 }
 
+namespace {
+int64_t env_default(int opt) {
+  auto is = [](const char* v, const char* w) { return v && std::strcmp(v, w) == 0; };
+  switch (opt) {
+    case FE_OPT_MATRIX_IMPL: {
+      const char* v = std::getenv("FEB200_MATRIX_IMPL");
+      return is(v, "sf1") ? MATRIX_SF1 : is(v, "dense") ? MATRIX_DENSE : MATRIX_DEFAULT;
+    }
+    case FE_OPT_RESIDUAL_IMPL: {
+      const char* v = std::getenv("FEB200_RESIDUAL_IMPL");
+      return is(v, "sf") ? RESIDUAL_SF : is(v, "dense") ? RESIDUAL_DENSE : RESIDUAL_DEFAULT;
+    }
+    case FE_OPT_CSR_IMPL: return is(std::getenv("FEB200_CSR_IMPL"), "gather") ? 1 : 0;
+    case FE_OPT_MAX_CTAS: {
+      const char* v = std::getenv("FEB200_MAX_CTAS");
+      const long long n = v ? std::atoll(v) : 0;
+      return n > 0 ? n : 0;
+    }
+  }
+  return 0;
+}
+
+struct Options {
+  std::atomic<int64_t> v[FE_OPT_COUNT];
+  Options() {
+    for (int i = 0; i < FE_OPT_COUNT; ++i) v[i].store(env_default(i), std::memory_order_relaxed);
+  }
+};
+Options& options() {
+  static Options o;  // initialised once (thread-safe static), from the environment
+  return o;
+}
+const Options& g_options_at_load = options();
+}  // namespace
+
+int64_t option(int opt) { return options().v[opt].load(std::memory_order_relaxed); }
+
+bool set_option(int opt, int64_t value) {
+  static const int64_t hi[FE_OPT_COUNT] = {2, 2, 1, INT32_MAX};
+  if (opt < 0 || opt >= FE_OPT_COUNT || value < 0 || value > hi[opt]) return false;
+  options().v[opt].store(value, std::memory_order_relaxed);
+  return true;
+}
+
 int grid_cap(int grid) {
-  const char* v = std::getenv("FEB200_MAX_CTAS");  // read per launch: tests toggle it
-  const int cap = v ? std::atoi(v) : 0;
-  return (cap > 0 && grid > cap) ? cap : grid;
+  const int64_t cap = option(FE_OPT_MAX_CTAS);
+  return (cap > 0 && grid > cap) ? (int)cap : grid;
 }
 
 namespace {

@@ -203,17 +203,11 @@ static cudaError_t res_dispatch(const fe_mesh* mh, int form, MatArgs mat, const 
   return cudaErrorNotSupported;
 }
 
-// sum-factorised kernels first; FEB200_RESIDUAL_IMPL=dense selects the dense DMMA kernels
-static bool want_dense_residual() {
-  const char* impl = std::getenv("FEB200_RESIDUAL_IMPL");
-  return impl && std::strcmp(impl, "dense") == 0;
-}
+// sum-factorised kernels first; FE_OPT_RESIDUAL_IMPL = dense selects the dense DMMA kernels
+static bool want_dense_residual() { return option(FE_OPT_RESIDUAL_IMPL) == RESIDUAL_DENSE; }
 
-// FEB200_RESIDUAL_IMPL=sf keeps the shared-memory sum-factorised kernel for every form
-bool want_residual_t3() {
-  const char* impl = std::getenv("FEB200_RESIDUAL_IMPL");
-  return !(impl && (std::strcmp(impl, "sf") == 0 || std::strcmp(impl, "dense") == 0));
-}
+// FE_OPT_RESIDUAL_IMPL = sf keeps the shared-memory sum-factorised kernel for every form
+bool want_residual_t3() { return option(FE_OPT_RESIDUAL_IMPL) == RESIDUAL_DEFAULT; }
 
 cudaError_t launch_residual_f64(const fe_mesh* m, int form, MatArgs mat, const double* u,
                                 int64_t e0, int64_t e1, double* r_elem, double* r_global,

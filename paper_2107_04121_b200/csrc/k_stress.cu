@@ -9,6 +9,11 @@
 // of the cell); the reference-gradient table dphi[q][m][k] is read through L1 (shared by
 // all cells).  Output rows of 6 doubles are contiguous in (cell, qp) order, so the stores
 // of a warp cover one contiguous 48 B-per-thread range.
+//
+// INTEG: the paper's only mode for this form is 'eval', "returning the integral value"
+// (P:806-813): sigma_int[e][I] = sum_q w_q det J_q sigma[e][q][I] (the integral of sigma over
+// cell e; the domain integral is their sum).  The weighted per-qp values are staged in shared
+// memory and summed over q in ascending order by one thread per (cell, I): deterministic.
 #include "fe_device.cuh"
 #include "fe_internal.h"
 
@@ -21,7 +26,7 @@ struct StressL {
   static constexpr int NT = (CB * NQ + 31) / 32 * 32;           // threads used
 };
 
-template <int NB, int NQ>
+template <int NB, int NQ, bool INTEG>
 __global__ void __launch_bounds__(128)
     k_stress(MeshView mv, int mat_kind, const double* __restrict__ ma, const double* __restrict__ mb,
              const double* __restrict__ u, int64_t e0, int64_t e1, double* __restrict__ sigma) {
@@ -29,6 +34,7 @@ __global__ void __launch_bounds__(128)
   constexpr int CB = L::CB;
   __shared__ double xv[CB][24];
   __shared__ double ue[CB][3][NB];
+  __shared__ double acc[INTEG ? L::NT : 1][6];
   const int tid = threadIdx.x;
   for (int64_t eb = e0 + (int64_t)blockIdx.x * CB; eb < e1; eb += (int64_t)gridDim.x * CB) {
     const int ne = (int)((e1 - eb) < CB ? (e1 - eb) : CB);
@@ -46,10 +52,10 @@ __global__ void __launch_bounds__(128)
     }
     __syncthreads();
     const int c = tid / NQ, q = tid - c * NQ;
-    if (c >= ne) continue;
+    if (c < ne) {
     const int64_t e = eb + c;
     double Ji[9];
-    hex_geometry(xv[c], mv.xi[3 * q], mv.xi[3 * q + 1], mv.xi[3 * q + 2], Ji);
+    const double det = hex_geometry(xv[c], mv.xi[3 * q], mv.xi[3 * q + 1], mv.xi[3 * q + 2], Ji);
     // reference gradient r[a][m] = sum_k dphi[q][m][k] u_e[a][k]
     double r[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
     const double* dp = mv.dphi + (int64_t)q * 3 * NB;
@@ -93,23 +99,37 @@ __global__ void __launch_bounds__(128)
       s[4] = mu * eps[4];
       s[5] = mu * eps[5];
     }
-    double* o = sigma + ((e - e0) * NQ + q) * 6;
+    if constexpr (INTEG) {
+      const double dw = mv.w[q] * det;
 #pragma unroll
-    for (int I = 0; I < 6; ++I) o[I] = s[I];
+      for (int I = 0; I < 6; ++I) acc[tid][I] = dw * s[I];
+    } else {
+      double* o = sigma + ((e - e0) * NQ + q) * 6;
+#pragma unroll
+      for (int I = 0; I < 6; ++I) o[I] = s[I];
+    }
+    }  // c < ne
+    if constexpr (INTEG) {
+      __syncthreads();
+      for (int i = tid; i < ne * 6; i += blockDim.x) {
+        const int cc = i / 6, I = i - 6 * cc;
+        double t = 0.0;
+        for (int qq = 0; qq < NQ; ++qq) t += acc[cc * NQ + qq][I];
+        sigma[(eb + cc - e0) * 6 + I] = t;
+      }
+    }
   }
 }
 
 template <int P, int Q>
 static cudaError_t launch_stress_t(const fe_mesh* mh, MatArgs mat, const double* u, int64_t e0,
-                                   int64_t e1, double* sigma, cudaStream_t st) {
+                                   int64_t e1, double* sigma, bool integ, cudaStream_t st) {
   constexpr int NB = (P + 1) * (P + 1) * (P + 1), NQ = Q * Q * Q;
   using L = StressL<NB, NQ>;
-  auto kern = k_stress<NB, NQ>;
-  int nsm = 148, per_sm = 1, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::NT, 0);
-  if (per_sm < 1) per_sm = 1;
+  auto kern = integ ? k_stress<NB, NQ, true> : k_stress<NB, NQ, false>;
+  const LaunchFacts lf = launch_facts((const void*)kern, L::NT, 0);
+  if (lf.err != cudaSuccess) return lf.err;
+  const int nsm = lf.nsm, per_sm = lf.per_sm;
   const int64_t nb = (e1 - e0 + L::CB - 1) / L::CB;
   int grid = (int)(nb < (int64_t)nsm * per_sm ? nb : (int64_t)nsm * per_sm);
   grid = grid_cap(grid);
@@ -121,10 +141,10 @@ static cudaError_t launch_stress_t(const fe_mesh* mh, MatArgs mat, const double*
 }
 
 cudaError_t launch_stress(const fe_mesh* mh, MatArgs mat, const double* u, int64_t e0, int64_t e1,
-                          double* sigma, cudaStream_t st) {
+                          double* sigma, bool integ, cudaStream_t st) {
   // the mesh's own quadrature (meshes are built with q1d = order + 1)
 #define ST_CASE(P) \
-  if (mh->order == P && mh->q1d == P + 1) return launch_stress_t<P, P + 1>(mh, mat, u, e0, e1, sigma, st);
+  if (mh->order == P && mh->q1d == P + 1) return launch_stress_t<P, P + 1>(mh, mat, u, e0, e1, sigma, integ, st);
   ST_CASE(1) ST_CASE(2) ST_CASE(3) ST_CASE(4)
 #undef ST_CASE
   return cudaErrorNotSupported;

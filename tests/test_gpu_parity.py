@@ -51,13 +51,13 @@ RESIDUAL_CASES = [(f, p) for f in (0, 1, 2, 3, 4, 5) for p in (1, 2, 3)] + \
 
 
 @pytest.fixture(params=["default", "sf1", "dense"])
-def matrix_impl(request, monkeypatch):
+def matrix_impl(request, fe_opts):
     """default = sum-factorised kernels where built (warp-specialised pipeline for the scalar
     forms at p <= 2); sf1 = the single-stage sum-factorised kernel; dense = the DMMA kernels."""
     if request.param in ("dense", "sf1"):
-        monkeypatch.setenv("FEB200_MATRIX_IMPL", request.param)
+        fe_opts(matrix_impl=request.param)
     else:
-        monkeypatch.delenv("FEB200_MATRIX_IMPL", raising=False)
+        fe_opts(matrix_impl="default")
     return request.param
 
 
@@ -224,13 +224,10 @@ def test_config_full_size(name):
     r_elem, r_glob = mesh.residual(pr.form, u, *mat, want_elem=True)
     r_ref = oracle.problem_residual(sub)
     assert rel(r_elem[torch.from_numpy(idx).cuda()].cpu().numpy(), r_ref) <= TOL64
-    if name in ("C1", "C2", "C3", "C4"):
-        R_ref = oracle.problem_assembled_residual(pr)
-        assert rel(r_glob.cpu().numpy().ravel(), R_ref) <= TOL64
-    else:
-        # assembled vector == assemble of the GPU's own element residuals (atomics only)
-        R2 = mesh.assemble(r_elem, pr.ncomp)
-        assert rel(r_glob.cpu().numpy(), R2.cpu().numpy()) <= 1e-14
+    # the assembled global vector in full against the oracle's (C5: 2.1 M cells, 50.9 M
+    # values; the OpenMP oracle does it in seconds)
+    R_ref = oracle.problem_assembled_residual(pr)
+    assert rel(r_glob.cpu().numpy().ravel(), R_ref) <= TOL64
     if name == "C4":
         r_elem32, r_glob32 = mesh.residual(pr.form, dev(pr.u, torch.float32), pr.mat_kind,
                                            dev(pr.mat_a, torch.float32),
@@ -313,11 +310,11 @@ def test_csr_full_size_c2():
 @pytest.mark.parametrize("form,p,shape", [(0, 2, (6, 5, 4)), (3, 2, (5, 5, 3)), (1, 1, (9, 8, 7)),
                                           (4, 2, (4, 3, 5)), (5, 2, (4, 4, 3)), (0, 4, (4, 3, 3))])
 @pytest.mark.parametrize("ctas", [1, 3])
-def test_pipelined_many_batches_per_cta(form, p, shape, ctas, monkeypatch):
+def test_pipelined_many_batches_per_cta(form, p, shape, ctas, fe_opts):
     """FEB200_MAX_CTAS caps the persistent grids so that each CTA runs many batches: every
     ring slot and mbarrier phase of the warp-specialised kernels wraps several times (plus a
     ragged last batch); matrices and residuals still match the oracle in full."""
-    monkeypatch.setenv("FEB200_MAX_CTAS", str(ctas))
+    fe_opts(max_ctas=ctas)
     pr = fi.make_problem(form, p, shape, 6000 + 10 * form + p)
     mesh = gpu_mesh(pr)
     mat = (pr.mat_kind, dev(pr.mat_a), dev(pr.mat_b))
@@ -332,7 +329,7 @@ def test_pipelined_many_batches_per_cta(form, p, shape, ctas, monkeypatch):
 
 
 @pytest.mark.parametrize("form,p", [(0, 1), (0, 2), (3, 2), (4, 2)])
-def test_csr_gather_deterministic(form, p, monkeypatch):
+def test_csr_gather_deterministic(form, p, fe_opts):
     """FEB200_CSR_IMPL=gather: atomic-free row-owner assembly == the atomic one, and two runs
     are bitwise identical (fixed summation order)."""
     pr = fi.make_problem(form, p, (4, 3, 5), 8000 + form)
@@ -341,7 +338,7 @@ def test_csr_gather_deterministic(form, p, monkeypatch):
                               dev(pr.u) if form == fi.CONVECTIVE else None)
     csr = fe().CSR(mesh, pr.ncomp)
     ref = csr.assemble(K)
-    monkeypatch.setenv("FEB200_CSR_IMPL", "gather")
+    fe_opts(csr_impl="gather")
     a = csr.assemble(K)
     b = csr.assemble(K)
     assert torch.equal(a, b)
@@ -355,11 +352,11 @@ def test_csr_gather_deterministic(form, p, monkeypatch):
 
 @pytest.mark.parametrize("form,p", [(0, 1), (0, 2), (1, 2), (3, 2), (3, 1)])
 @pytest.mark.parametrize("ctas", [0, 2])
-def test_matrix_residual_fused(form, p, ctas, monkeypatch):
+def test_matrix_residual_fused(form, p, ctas, fe_opts):
     """fe_eval_matrix_residual: K as fe_eval_element_matrices and r_e = K_e u_e (Alg. 1 for a
     bilinear form, pin P8) with the fused scatter, against the oracle's direct residual."""
     if ctas:
-        monkeypatch.setenv("FEB200_MAX_CTAS", str(ctas))
+        fe_opts(max_ctas=ctas)
     pr = fi.make_problem(form, p, (6, 4, 5), 9000 + 10 * form + p)
     mesh = gpu_mesh(pr)
     K, r_elem, r_glob = mesh.matrix_residual(form, dev(pr.u), pr.mat_kind, dev(pr.mat_a),
@@ -441,11 +438,11 @@ def test_weighted_dot_matrix(p, shape):
 @pytest.mark.parametrize("form", [fi.WEIGHTED_DOT, fi.DIVERGENCE])
 @pytest.mark.parametrize("p", [1, 2, 3, 4])
 @pytest.mark.parametrize("impl", ["default", "dense"])
-def test_n3_residual(form, p, impl, monkeypatch):
+def test_n3_residual(form, p, impl, fe_opts):
     """Residual mode of 'ij,i,j' (f0 = M u) and 'i.i' (r_k = int dphi_k/dx_a), sum-factorised
     and dense kernels, ragged cell counts."""
     if impl == "dense":
-        monkeypatch.setenv("FEB200_RESIDUAL_IMPL", "dense")
+        fe_opts(residual_impl="dense")
     pr = fi.make_problem(form, p, (5, 3, 4) if p <= 2 else (3, 2, 3), 14000 + 10 * form + p)
     r_ref = oracle.problem_residual(pr)
     R_ref = oracle.assemble(r_ref, pr.dof_conn, pr.n_nodes, pr.ncomp)
@@ -493,6 +490,14 @@ def test_stress(kind, p):
     assert rel(sub.cpu().numpy(), ref[5:17]) <= TOL64
     empty = mesh.stress(dev(pr.u), *mat, elem_begin=3, elem_end=3)
     assert empty.shape[0] == 0
+    # 'eval' mode of the Cauchy stress: the per-cell integral
+    ref_i = oracle.eval_stress_integral(p, p + 1, pr.coords, pr.conn, pr.dof_conn, pr.u, kind,
+                                        pr.mat_a, pr.mat_b)
+    si = mesh.stress_integral(dev(pr.u), *mat)
+    assert rel(si.cpu().numpy(), ref_i) <= TOL64
+    si_sub = mesh.stress_integral(dev(pr.u), *mat, elem_begin=5, elem_end=17)
+    assert rel(si_sub.cpu().numpy(), ref_i[5:17]) <= TOL64
+    assert mesh.stress_integral(dev(pr.u), *mat, elem_begin=3, elem_end=3).shape[0] == 0
 
 
 # ---- N3: Stokes coupling pair -------------------------------------------------
@@ -605,10 +610,10 @@ def test_mixed_order_mesh():
 
 
 @pytest.mark.parametrize("ctas", [1, 3])
-def test_n3_n4_many_batches_per_cta(ctas, monkeypatch):
+def test_n3_n4_many_batches_per_cta(ctas, fe_opts):
     """Grid caps force many batches per CTA through the N3 / N4 kernels (weighted-dot matrix,
     FULL_D pipelined matrix and its D prefetch, divergence residual, stress, Stokes coupling)."""
-    monkeypatch.setenv("FEB200_MAX_CTAS", str(ctas))
+    fe_opts(max_ctas=ctas)
     pr = fi.make_problem(fi.WEIGHTED_DOT, 2, (5, 4, 3), 18000)
     mesh = gpu_mesh(pr)
     K = mesh.element_matrices(fi.WEIGHTED_DOT, pr.mat_kind, dev(pr.mat_a))
@@ -703,12 +708,12 @@ def test_matrix_q4(form):
 @pytest.mark.parametrize("form,p", [(fi.MASS_DIFFUSION, 4), (fi.ELASTICITY, 2), (fi.DIFFUSION, 2),
                                     (fi.WEIGHTED_DOT, 2), (fi.MASS_DIFFUSION, 3)])
 @pytest.mark.parametrize("ctas", [0, 2])
-def test_residual_misaligned_inputs(form, p, ctas, monkeypatch):
+def test_residual_misaligned_inputs(form, p, ctas, fe_opts):
     """Material arrays passed as views that start 8 B past a 16-B boundary: the residual
     kernels' block fetches take the enclosing aligned range and read at the offset (and fall
     back to plain copies at the array end); results unchanged."""
     if ctas:
-        monkeypatch.setenv("FEB200_MAX_CTAS", str(ctas))
+        fe_opts(max_ctas=ctas)
     pr = fi.make_problem(form, p, (5, 3, 3) if p <= 2 else (3, 2, 3), 24000 + 10 * form + p,
                          mat_kind=fi.MAT_PER_QP if form == fi.ELASTICITY else None)
     mesh = gpu_mesh(pr)
@@ -728,3 +733,103 @@ def test_residual_misaligned_inputs(form, p, ctas, monkeypatch):
     r_ref = oracle.problem_residual(pr)
     assert rel(r_elem.cpu().numpy(), r_ref) <= TOL64
     assert rel(r_glob.cpu().numpy().ravel(), oracle.assemble(r_ref, pr.dof_conn, pr.n_nodes, pr.ncomp)) <= TOL64
+
+
+# ---- general D read as given (reading 23) -----------------------------------------
+
+def _nonsym_D(pr, seed, scale=0.3):
+    """The problem's SPD D plus a random skew part: a non-symmetric Voigt matrix per qp."""
+    rng = np.random.default_rng(seed)
+    S = rng.uniform(-1, 1, size=pr.mat_a.shape)
+    return pr.mat_a + scale * (S - np.swapaxes(S, -1, -2))
+
+
+@pytest.mark.parametrize("p", [1, 2])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_full_d_nonsymmetric(p, shape, fe_opts):
+    """A non-symmetric D[E][n_q][6][6] is read as given by matrix and residual mode at p = 1
+    and 2 (at p = 2 the device-side symmetry check routes the matrix to the general 9-block
+    kernel): K == oracle, K not symmetric, and K_e u_e == r_e (P8).  With many batches per
+    CTA, and a symmetric-to-rounding D keeps the pipelined kernel's result within 1e-12."""
+    pr = fi.make_problem(fi.ELASTICITY, p, shape, 17000 + p, mat_kind=fi.MAT_FULL_D)
+    D = _nonsym_D(pr, 5 + p)
+    pr_ns = fi.Problem(pr.name, pr.form, pr.p, pr.q1d, pr.shape, pr.coords, pr.conn, pr.dof_conn,
+                       pr.n_nodes, pr.mat_kind, D, None, pr.u)
+    Kref = oracle.problem_matrix(pr_ns)
+    rref = oracle.problem_residual(pr_ns)
+    assert rel(Kref, Kref.transpose(0, 2, 1)) > 1e-3
+    mesh = gpu_mesh(pr)
+    for ctas in (0, 2):
+        fe_opts(max_ctas=ctas)
+        K = mesh.element_matrices(fi.ELASTICITY, fi.MAT_FULL_D, dev(D), None).cpu().numpy()
+        assert rel(K, Kref) <= TOL64
+        re_, _ = mesh.residual(fi.ELASTICITY, dev(pr.u), fi.MAT_FULL_D, dev(D), None,
+                               want_elem=True, want_global=False)
+        re_ = re_.cpu().numpy()
+        assert rel(re_, rref) <= TOL64
+        ue = pr.u[pr.dof_conn].transpose(0, 2, 1).reshape(pr.n_elems, -1)
+        assert rel(np.einsum("eij,ej->ei", K, ue), re_) <= 1e-12
+    # one non-symmetric qp block among symmetric ones still routes the whole call
+    D1 = pr.mat_a.copy()
+    D1[-1, -1, 0, 5] += 0.5
+    pr1 = fi.Problem(pr.name, pr.form, pr.p, pr.q1d, pr.shape, pr.coords, pr.conn, pr.dof_conn,
+                     pr.n_nodes, pr.mat_kind, D1, None, pr.u)
+    K1 = mesh.element_matrices(fi.ELASTICITY, fi.MAT_FULL_D, dev(D1), None).cpu().numpy()
+    assert rel(K1, oracle.problem_matrix(pr1)) <= TOL64
+    # a D whose transpose differs in the last bits only: the pipelined kernel (upper triangle)
+    # stays within the parity tolerance
+    Dr = pr.mat_a * (1 + 2.2e-16 * np.random.default_rng(3).integers(-2, 3, pr.mat_a.shape))
+    prr = fi.Problem(pr.name, pr.form, pr.p, pr.q1d, pr.shape, pr.coords, pr.conn, pr.dof_conn,
+                     pr.n_nodes, pr.mat_kind, Dr, None, pr.u)
+    Kr = mesh.element_matrices(fi.ELASTICITY, fi.MAT_FULL_D, dev(Dr), None).cpu().numpy()
+    assert rel(Kr, oracle.problem_matrix(prr)) <= TOL64
+
+
+def test_concurrent_mesh_creation():
+    """Two host threads create meshes of different orders at the same time (the per-order
+    __constant__ tables are uploaded from per-call stack buffers) and evaluate them on their
+    own streams; every result equals the oracle."""
+    import threading
+    probs = [fi.make_problem(fi.DIFFUSION, p, (4, 3, 3), 18000 + p) for p in (1, 2, 1, 2)]
+    refs = [oracle.problem_matrix(pr) for pr in probs]
+    errs, out = [], [None] * len(probs)
+
+    def work(i):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                for _ in range(5):
+                    m = gpu_mesh(probs[i])
+                    K = m.element_matrices(fi.DIFFUSION, 0, dev(probs[i].mat_a), None)
+                    st.synchronize()
+                    out[i] = K.cpu().numpy()
+                    m.close()
+        except Exception as ex:  # pragma: no cover - reported below
+            errs.append(ex)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(len(probs))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for K, Kr in zip(out, refs):
+        assert rel(K, Kr) <= TOL64
+
+
+def test_stream_ordered_destroy():
+    """fe_destroy_mesh / fe_destroy_csr release on the caller's stream without a device
+    synchronisation: work queued before on that stream still sees valid memory, and a
+    mesh created right after works."""
+    pr = fi.make_problem(fi.DIFFUSION, 2, (6, 5, 4), 18100)
+    ref = oracle.problem_assembled_residual(pr)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            m = gpu_mesh(pr)
+            csr = fe().CSR(m, 1)
+            _, rg = m.residual(fi.DIFFUSION, dev(pr.u), 0, dev(pr.mat_a), None)
+            csr.close()
+            m.close()          # queued behind the residual on st
+            st.synchronize()
+            assert rel(rg.cpu().numpy().ravel(), ref) <= TOL64

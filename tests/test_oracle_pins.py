@@ -764,3 +764,137 @@ def test_N3_stokes_coupling_linear_fields(pv, pp):
     args = (pv, pp, pv + 1, v.coords, v.conn, v.dof_conn, mp.p_dof_conn)
     assert abs(oracle.coupling_eval(*args, X, pl) - 3.0) < 1e-13
     assert abs(oracle.coupling_eval(*args, X, np.ones(mp.n_p_nodes)) - 3.0) < 1e-13
+
+
+# ---------------------------------------------------------------- geometry output layout
+def _corners01():
+    """Reference corners of [0,1]^3 in the lexicographic vertex order v = a + 2b + 4c."""
+    return np.array([[a, b, c] for c in (0, 1) for b in (0, 1) for a in (0, 1)], dtype=float)
+
+
+def _trilinear(xv, xi):
+    """x(xi) of the trilinear map with vertex coordinates xv[8][3] (reading 4)."""
+    w = np.array([(xi[0] if a else 1 - xi[0]) * (xi[1] if b else 1 - xi[1]) *
+                  (xi[2] if c else 1 - xi[2]) for c in (0, 1) for b in (0, 1) for a in (0, 1)])
+    return w @ xv
+
+
+@pytest.mark.parametrize("q1d", [2, 3, 5])
+def test_geometry_affine_closed_form(q1d):
+    """Affine cell x = A xi + b: J = A at every qp, so the stored J^-1 is A^-1 (row-major,
+    J_ij = dx_i/dxi_j) and detw = w_q det A.  A is non-symmetric, so a transposed
+    J^-1 store, a permuted qp order or a dropped weight fails."""
+    A = np.array([[0.9, 0.2, -0.1], [0.05, 1.3, 0.3], [-0.2, 0.1, 0.7]])
+    b = np.array([0.1, -0.4, 2.0])
+    coords = _corners01() @ A.T + b
+    conn = np.arange(8, dtype=np.int32)[None]
+    detw, Jinv = oracle.geometry(q1d, coords, conn)
+    t, w = np.polynomial.legendre.leggauss(q1d)
+    w = w / 2.0
+    W = np.einsum("c,b,a->cba", w, w, w).ravel()          # q = a + q1d (b + q1d c)
+    Ainv = np.linalg.inv(A)
+    assert np.abs(Jinv[0] - Ainv[None]).max() <= 1e-14 * np.abs(Ainv).max()
+    np.testing.assert_allclose(detw[0], W * np.linalg.det(A), rtol=1e-14)
+
+
+def test_geometry_jinv_perturbed():
+    """Perturbed cells: J from exact central differences of the trilinear map (linear in each
+    xi_j separately, so the difference quotient is exact up to rounding) times the oracle's
+    J^-1 is the identity at every qp; J^-1 also equals numpy.linalg.inv of the einsum oracle's
+    Jacobian (tests/einsum_oracle.py) in the same [E][q][3][3] layout."""
+    pr = fi.make_problem(fi.DIFFUSION, 2, (3, 2, 2), 31)
+    q1d = 3
+    detw, Jinv = oracle.geometry(q1d, pr.coords, pr.conn)
+    t, w = np.polynomial.legendre.leggauss(q1d)
+    x = (t + 1) / 2
+    qps = [(x[a], x[b], x[c]) for c in range(q1d) for b in range(q1d) for a in range(q1d)]
+    h = 0.25
+    for e in range(pr.n_elems):
+        xv = pr.coords[pr.conn[e]]
+        for q, xi in enumerate(qps):
+            J = np.zeros((3, 3))
+            for j in range(3):
+                d = np.zeros(3)
+                d[j] = h
+                J[:, j] = (_trilinear(xv, np.add(xi, d)) - _trilinear(xv, np.subtract(xi, d))) / (2 * h)
+            assert np.abs(J @ Jinv[e, q] - np.eye(3)).max() <= 1e-13
+            assert abs(detw[e, q] - np.linalg.det(J) * w[q % 3] * w[(q // 3) % 3] * w[q // 9] / 8) \
+                <= 1e-14 * abs(detw[e, q])
+    det2, Jinv2 = eo.mapping(pr.coords, pr.conn, q1d)
+    assert rel(Jinv, Jinv2) < 1e-14
+    assert rel(detw, det2) < 1e-14
+
+
+# ---------------------------------------------------------------- D = 3 gather / scatter
+@pytest.mark.parametrize("p", [1, 2])
+def test_P5_vector_patch_test(p):
+    """Vector patch test (the D = 3 analogue of P5, gather/scatter through the connectivity,
+    P:1093-1095): u = A x + b at the nodes with constant lambda, mu gives a constant stress, so
+    the assembled elasticity residual int sigma : grad v vanishes at every interior node of a
+    perturbed mesh (div sigma = 0, and the integrand sigma : cof(J)^T grad phi is integrated
+    exactly by q1d = p + 1).  Global vector node-major interleaved [n_nodes][3] (reading 9): a
+    component-major scatter or gather puts boundary values on interior rows and fails."""
+    pr = fi.make_problem(fi.ELASTICITY, p, (3, 3, 3), 41)
+    X = node_coords(pr)
+    A = np.array([[0.3, -0.7, 0.2], [0.5, 0.1, -0.4], [-0.6, 0.8, 0.25]])
+    u = X @ A.T + np.array([0.2, -0.1, 0.4])
+    lam = np.full(pr.n_elems, 1.3)
+    mu = np.full(pr.n_elems, 0.8)
+    r = oracle.eval_residual(fi.ELASTICITY, p, p + 1, pr.coords, pr.conn, pr.dof_conn, u,
+                             fi.MAT_PER_ELEM, lam, mu)
+    R = oracle.assemble(r, pr.dof_conn, pr.n_nodes, 3).reshape(pr.n_nodes, 3)
+    M = 3 * p + 1
+    idx = np.arange(pr.n_nodes)
+    ix, iy, iz = idx % M, (idx // M) % M, idx // (M * M)
+    interior = (ix > 0) & (ix < M - 1) & (iy > 0) & (iy < M - 1) & (iz > 0) & (iz < M - 1)
+    assert np.abs(R[interior]).max() <= 1e-13 * np.abs(R).max()
+    assert (np.abs(R[~interior]).max(axis=0) > 1e-3).all()
+    # the per-component boundary tractions balance: sum over all nodes of R[:, a] = 0
+    assert np.abs(R.sum(axis=0)).max() <= 1e-13 * np.abs(R).max()
+
+
+def test_vector_assembly_component_sums():
+    """Vector mass with rho = 1 and u = c (constant vector): sum_nodes R[:, a] = c_a vol (= c_a
+    on the unit cube), per component, through the interleaved scatter (reading 9)."""
+    pr = fi.make_problem(fi.VECTOR_MASS, 2, (3, 2, 2), 43)
+    c = np.array([1.0, -2.0, 3.5])
+    u = np.tile(c, (pr.n_nodes, 1))
+    r = oracle.eval_residual(fi.VECTOR_MASS, 2, 3, pr.coords, pr.conn, pr.dof_conn, u, 0,
+                             np.ones((pr.n_elems, pr.nq)))
+    R = oracle.assemble(r, pr.dof_conn, pr.n_nodes, 3).reshape(pr.n_nodes, 3)
+    np.testing.assert_allclose(R.sum(axis=0), c, rtol=1e-13)
+    # and each node's three entries are c times the same lumped mass
+    lumped = R[:, 0] / c[0]
+    np.testing.assert_allclose(R, lumped[:, None] * c[None], rtol=1e-12, atol=1e-16)
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_N3_cauchy_stress_integral(p):
+    """Cauchy stress in 'eval' mode, "returning the integral value": for an affine
+    u and constant lambda, mu, sigma is the constant D eps(A), so int_e sigma = D eps(A) vol(e)
+    with vol(e) from the mass-matrix pin (P4), and the cells sum to D eps(A) on the unit cube."""
+    pr = fi.make_problem(fi.ELASTICITY, p, (3, 2, 2), 45)
+    X = node_coords(pr)
+    A = np.array([[0.3, -0.2, 0.1], [0.05, -0.4, 0.25], [0.2, 0.15, 0.6]])
+    u = X @ A.T + np.array([0.1, -0.3, 0.2])
+    lam = np.full(pr.n_elems, 1.1)
+    mu = np.full(pr.n_elems, 0.7)
+    si = oracle.eval_stress_integral(p, p + 1, pr.coords, pr.conn, pr.dof_conn, u,
+                                     fi.MAT_PER_ELEM, lam, mu)
+    eps = np.array([A[0, 0], A[1, 1], A[2, 2], A[0, 1] + A[1, 0], A[0, 2] + A[2, 0],
+                    A[1, 2] + A[2, 1]])
+    ref = oracle.isotropic_D(1.1, 0.7) @ eps
+    M = oracle.eval_matrix(fi.MASS, p, p + 1, pr.coords, pr.conn, pr.dof_conn, 0,
+                           np.ones((pr.n_elems, pr.nq)))
+    vol = M.sum(axis=(1, 2))
+    np.testing.assert_allclose(si, vol[:, None] * ref[None, :], rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(si.sum(axis=0), ref, rtol=1e-13)
+    # with random materials: the integral is the quadrature sum of the per-qp oracle stress
+    # weighted by detw (two oracle entry points, same definition, different loops)
+    pr2 = fi.make_problem(fi.ELASTICITY, p, (2, 2, 2), 46, mat_kind=fi.MAT_PER_QP)
+    si2 = oracle.eval_stress_integral(p, p + 1, pr2.coords, pr2.conn, pr2.dof_conn, pr2.u,
+                                      pr2.mat_kind, pr2.mat_a, pr2.mat_b, 2, 7)
+    sq = oracle.eval_stress(p, p + 1, pr2.coords, pr2.conn, pr2.dof_conn, pr2.u, pr2.mat_kind,
+                            pr2.mat_a, pr2.mat_b, 2, 7)
+    detw, _ = oracle.geometry(p + 1, pr2.coords, pr2.conn)
+    np.testing.assert_allclose(si2, np.einsum("eq,eqi->ei", detw[2:7], sq), rtol=1e-12, atol=1e-18)
