@@ -12,10 +12,20 @@ perturbed cells, matrix + residual).  Metric: cells evaluated per second
 (each cell gets its element matrix AND its residual every step).
 
 Timing: W warm-up steps, then K steps bracketed by barrier + synchronize,
-CUDA events on the launching stream, max over ranks.  The C2 matrix output
-(1.53 GB) is larger than L2 (126 MB), so every step starts L2-cold.
-Kernel durations are measured with CUDA events around each ABI call on the
-same stream.  Clocks are sampled with nvidia-smi during the timed region.
+CUDA events on the launching stream (per-step and per-kernel events
+preallocated), max over ranks.  Every step writes or reads more than the
+126 MB L2 (C2: K = 1.53 GB), so no explicit flush.  Reported per step and
+per kernel: mean, the paper's mean without the worst call T^ww,
+median and minimum, plus the result throughput |K| or |r| / T^ww in MB/s
+(P:1566-1572).  Clocks are sampled with nvidia-smi every 20 ms over a window
+of >= 1.2 s that contains the timed region (untimed repeats of the same step
+before and after it), so the record has samples even when K steps take a few
+milliseconds.
+
+The default line (--config C2) also carries `configs`: every other BASELINE
+form and mode (C3 elasticity matrix + residual, C4 mass+Laplace residual in
+fp64 and fp32, C5 convective residual, C5t convective tangent), each measured
+the same way with its own kernel statistics, rooflines and clock record.
 """
 from __future__ import annotations
 
@@ -174,6 +184,14 @@ WORKLOADS = {
     "C3csr": dict(modes=("matrix", "csr")),
     "C3d": dict(modes=("matrix", "residual")),  # N4: C3 with a general Voigt D[E][n_q][6][6]
 }
+# per-form sub-results carried by the default (C2) line: every BASELINE.json form and mode
+SUB_CONFIGS = ("C3", "C4", "C4f32", "C5", "C5t")
+L2_NOTE = "no flush: every step writes/reads more than the 126 MB L2"
+
+
+def split_cfg(name):
+    """'C4f32' -> ('C4', 'f32'); 'C3' -> ('C3', None)."""
+    return (name[:-3], "f32") if name.endswith("f32") else (name, None)
 
 
 def build_problem(name):
@@ -190,6 +208,32 @@ def build_problem(name):
     return fi.make_config(name)
 
 
+def config_dict(cfg, prob, modes, world, exchange, dtype):
+    """The `config` object of the JSON line -- identical in both arms (ours / reference)."""
+    return {"workload": cfg, "desc": prob.meta.get("desc", ""), "cells": prob.n_elems,
+            "order": prob.p, "q1d": prob.q1d, "form": fi.FORM_NAMES[prob.form],
+            "modes": list(modes), "dtype": dtype, "parallelism": f"z-slabs x{world}",
+            "exchange": exchange if world > 1 else None, "l2": L2_NOTE}
+
+
+def step_stats(xs):
+    """Timing statistics of repeated calls: mean, the paper's mean without the worst call
+    T^ww, median and minimum."""
+    xs = np.asarray(xs, dtype=np.float64)
+    tww = float((xs.sum() - xs.max()) / (len(xs) - 1)) if len(xs) > 1 else float(xs[0])
+    return {"mean": float(xs.mean()), "tww": tww, "median": float(np.median(xs)),
+            "min": float(xs.min()), "n": int(len(xs))}
+
+
+def result_bytes(prob, mode, esize):
+    """Size of the resulting array the paper's throughput divides by T^ww:
+    the element matrices (matrix mode) or the element residual vectors (residual mode)."""
+    nd = prob.ncomp * prob.nb
+    if mode == "residual":
+        return prob.n_elems * nd * esize
+    return prob.n_elems * nd * nd * 8
+
+
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -199,8 +243,10 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.t0 = self.t1 = None
 
     def __enter__(self):
+        self.t0 = time.perf_counter()
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -217,6 +263,7 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.t1 = time.perf_counter()
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -239,10 +286,14 @@ class ClockSampler:
             for nm, v in zip(names, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
+        win = None if self.t1 is None else round(self.t1 - self.t0, 3)
         if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "window_s": win}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window_s": win,
+                "note": "sampled every 20 ms over the timed region plus untimed repeats of the "
+                        "same step before and after it (window >= 1.2 s)"}
 
 
 # ----------------------------------------------------------------------------
@@ -291,7 +342,7 @@ def cpu_baseline(prob, modes, budget_s=12.0):
                      f"modes {'+'.join(modes)}, plain C oracle (-O2, OpenMP over cells), {t:.1f} s"}
     # the same oracle on one core, on a smaller prefix
     import oracle
-    nthr = oracle.set_threads(1)
+    oracle.set_threads(1)
     try:
         n1 = max(1, n // max(1, cpu_cores()))
         t1 = oracle_step(prob, n1, modes)
@@ -299,14 +350,15 @@ def cpu_baseline(prob, modes, budget_s=12.0):
         out["sample_1core"] = f"first {n1} cells, 1 thread, {t1:.1f} s"
     finally:
         oracle.set_threads(cpu_cores())
-    del nthr
     return out
 
 
 def run_reference(args, cfg):
+    """--impl reference: the oracle (this tier's reference arm) on the host cores, rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     prob = build_problem(cfg)
     modes = WORKLOADS[cfg]["modes"]
     per_step_budget = max(0.5, min(6.0, 150.0 / max(1, args.steps + args.warmup)))
@@ -320,28 +372,362 @@ def run_reference(args, cfg):
         "impl": "reference", "metric": f"{cfg} cells evaluated per second ({'+'.join(modes)})",
         "value": value, "unit": "cells/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg, "cells": prob.n_elems, "order": prob.p,
-                   "form": fi.FORM_NAMES[prob.form], "modes": list(modes),
-                   "sample_cells_per_step": n},
+        "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": config_dict(cfg, prob, modes, world, args.exchange, args.dtype),
+        "stats": {"step_ms_full_workload_equiv": step_stats(
+            [1e3 * t * prob.n_elems / n for t in times])},
         "cpu_baseline": {"value": value, "unit": "cells/s", "cores": cpu_cores(), "kind": "oracle",
-                         "sample": f"first {n} of {prob.n_elems} cells per step"},
+                         "sample": f"first {n} of {prob.n_elems} cells per step (plain C oracle, "
+                                   f"-O2, OpenMP over cells)"},
         "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------
+class Runner:
+    """One config set up on this rank: mesh (z-slab for N > 1), inputs and outputs in HBM, and
+    step() = one pass of the config's modes through the C ABI (plus, for N > 1, the interface
+    exchange).  Kernel events are preallocated by the caller and passed in `rec`."""
+
+    def __init__(self, cfg, dtype, world, rank, dev, exchange="nccl", fused=False):
+        import torch
+
+        import paper_2107_04121_b200 as fe
+        from paper_2107_04121_b200 import slabs
+        self.torch, self.fe, self.slabs = torch, fe, slabs
+        self.cfg, self.world, self.rank, self.dev, self.dtype = cfg, world, rank, dev, dtype
+        self.modes = WORKLOADS[cfg]["modes"]
+        self.prob = prob = build_problem(cfg)
+        self.fused = (fused and tuple(self.modes) == ("matrix", "residual") and dtype == "f64"
+                      and prob.form in (fi.DIFFUSION, fi.MASS, fi.MASS_DIFFUSION) and prob.p <= 2)
+        self.kmodes = ("matrix+residual",) if self.fused else tuple(self.modes)
+        if cfg == "C5t" and world > 1:
+            raise SystemExit("C5t (corner tangent) is single-GPU")
+        if dtype == "f32" and "matrix" in self.modes:
+            raise SystemExit("fp32 is built for residual mode only")
+        self.tdt = torch.float64 if dtype == "f64" else torch.float32
+        self.dtc = fe.F64 if dtype == "f64" else fe.F32
+        D, nb = prob.ncomp, prob.nb
+        if cfg == "C5t":
+            sl = slabs.Slab(0, 1, 0, prob.n_elems, 0, prob.coords.shape[0], 0, prob.n_nodes, 0)
+            lc, lconn, ldc = prob.coords, prob.conn, prob.dof_conn
+        elif "csr" in self.modes and world > 1:
+            # N2 with row ownership: the slab plus the first cell layer above, so the rank's owned
+            # block rows of the global CSR matrix are complete without communication
+            sl = slabs.ghost_slab_of(prob.shape, prob.p, world, rank)
+            lc, lconn, ldc = slabs.local_arrays(sl, prob.coords, prob.conn, prob.dof_conn)
+        else:
+            sl = slabs.slab_of(prob.shape, prob.p, world, rank)
+            lc, lconn, ldc = slabs.local_arrays(sl, prob.coords, prob.conn, prob.dof_conn)
+        self.sl = sl
+        e0, e1 = sl.elem_begin, sl.elem_end
+        self.El = El = e1 - e0
+        self.mesh = fe.Mesh(torch.from_numpy(lc), torch.from_numpy(lconn), prob.p, prob.q1d,
+                            dof_conn=torch.from_numpy(ldc), n_nodes=sl.n_nodes, device=dev)
+
+        def dslice(a):
+            return None if a is None else torch.from_numpy(np.ascontiguousarray(a[e0:e1])).to(dev, self.tdt)
+
+        self.mat_a, self.mat_b = dslice(prob.mat_a), dslice(prob.mat_b)
+        self.u_loc = np.ascontiguousarray(prob.u[sl.node_begin:sl.node_end])
+        self.u = torch.from_numpy(self.u_loc).to(dev, self.tdt)
+        self.K = (torch.empty((El, D * nb, D * nb), dtype=torch.float64, device=dev)
+                  if "matrix" in self.modes else None)
+        self.peer = None
+        if world > 1 and exchange == "peer" and "residual" in self.modes and not self.fused:
+            if dtype != "f64":
+                raise SystemExit("--exchange peer is built for fp64 residuals")
+            self.peer = slabs.PeerExchange(sl, prob.shape, prob.p, D, dev)
+            self.r = self.peer.r
+            self.tiny = torch.zeros(1, dtype=torch.float32, device=dev)
+        else:
+            self.r = torch.zeros((sl.n_nodes, D), dtype=self.tdt, device=dev)
+        self.csr = fe.CSR(self.mesh, D) if "csr" in self.modes else None
+        self.csr_vals = (torch.zeros(self.csr.nnz, dtype=torch.float64, device=dev)
+                         if self.csr is not None else None)
+        self.stream = torch.cuda.current_stream(dev)
+        self.comm_stream = torch.cuda.Stream(dev) if world > 1 else None
+        self.bufs = [None]
+
+    def events(self, n):
+        """Preallocated kernel events: rec[i][mode] = (start, end) for step i."""
+        E = self.torch.cuda.Event
+        return [{m: (E(enable_timing=True), E(enable_timing=True)) for m in self.kmodes}
+                for _ in range(n)]
+
+    def step(self, rec=None):
+        fe, prob, mesh, st = self.fe, self.prob, self.mesh, self.stream
+        mat = (prob.mat_kind, self.mat_a, self.mat_b)
+        u, r, El, K = self.u, self.r, self.El, self.K
+        comm = self.comm_stream if self.world > 1 else None
+        if self.fused:
+            r.zero_()
+            if rec:
+                rec["matrix+residual"][0].record(st)
+
+            def evaluate_f(lo, hi):
+                fe.fe_eval_matrix_residual(mesh.handle, prob.form, fe.F64, *mat, u, lo, hi,
+                                           K[lo:hi], None, r, st)
+
+            self.bufs[0] = self.slabs.residual_overlapped(evaluate_f, r, self.sl, prob.shape, comm,
+                                                          self.bufs[0])
+            if rec:
+                rec["matrix+residual"][1].record(st)
+            return
+        if "matrix" in self.modes:
+            if rec:
+                rec["matrix"][0].record(st)
+            fe.fe_eval_element_matrices(mesh.handle, prob.form, fe.F64, *mat,
+                                        u if prob.form == fi.CONVECTIVE else None, 0, El, K, st)
+            if rec:
+                rec["matrix"][1].record(st)
+        if "csr" in self.modes:
+            self.csr_vals.zero_()
+            if rec:
+                rec["csr"][0].record(st)
+            self.csr.assemble(K, values=self.csr_vals, stream=st)
+            if rec:
+                rec["csr"][1].record(st)
+        if "residual" in self.modes and self.peer is not None:
+            if rec:
+                rec["residual"][0].record(st)
+
+            def evaluate_peer(windows):
+                fe.fe_eval_residual_peer(mesh.handle, prob.form, *mat, u, 0, El, None, r, windows, st)
+
+            # zero -> device barrier (tiny NCCL all-reduce) -> fused residual + exchange over
+            # peer memory -> device barrier
+            import torch.distributed as dist
+            self.peer.residual(evaluate_peer, lambda: dist.all_reduce(self.tiny))
+            if rec:
+                rec["residual"][1].record(st)
+        elif "residual" in self.modes:
+            r.zero_()
+            if rec:
+                rec["residual"][0].record(st)
+
+            def evaluate(lo, hi):
+                fe.fe_eval_residual(mesh.handle, prob.form, self.dtc, *mat, u, lo, hi, None, r, st)
+
+            # boundary-first residual; for N > 1 the interface exchange overlaps the interior
+            self.bufs[0] = self.slabs.residual_overlapped(evaluate, r, self.sl, prob.shape, comm,
+                                                          self.bufs[0])
+            if rec:
+                rec["residual"][1].record(st)
+
+    def close(self):
+        if self.peer is not None:
+            self.peer.close()
+        if self.csr is not None:
+            self.csr.close()
+        self.mesh.close()
+
+
+def _barrier(torch, dist, world, local_rank, dev):
+    if world > 1:
+        dist.barrier(device_ids=[local_rank])
+    torch.cuda.synchronize(dev)
+
+
+def timed_run(run, steps, warmup, world, local_rank, window_s=1.2):
+    """W warm-up steps; then, under the clock sampler, untimed repeats (>= 0.25 s), EXACTLY K
+    timed steps bracketed by barrier + synchronize with CUDA events on the launching stream
+    (per-step and per-kernel events preallocated), and untimed repeats until the sampler
+    window is >= window_s.  Returns the max-over-ranks timings."""
+    import torch
+    import torch.distributed as dist
+    dev, st = run.dev, run.stream
+    for _ in range(warmup):
+        run.step()
+    _barrier(torch, dist, world, local_rank, dev)
+    # step-time estimate (same on every rank: NCCL steps must match in count)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for _ in range(2):
+        run.step()
+    b.record(st)
+    _barrier(torch, dist, world, local_rank, dev)
+    est = a.elapsed_time(b) / 2
+    if world > 1:
+        t = torch.tensor([est], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        est = float(t[0])
+    est = max(est, 1e-3)
+    n_pre = int(np.ceil(250.0 / est))
+    n_post = max(0, int(np.ceil((window_s * 1e3 - 250.0 - steps * est) / est)))
+    ev_step = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    rec = run.events(steps)
+    fe = run.fe
+    with ClockSampler(local_rank) as clk:
+        for _ in range(n_pre):
+            run.step()
+        _barrier(torch, dist, world, local_rank, dev)
+        n_launch0 = fe.fe_launch_count()
+        ev_step[0].record(st)
+        for i in range(steps):
+            run.step(rec[i])
+            ev_step[i + 1].record(st)
+        _barrier(torch, dist, world, local_rank, dev)
+        launches = fe.fe_launch_count() - n_launch0
+        for _ in range(n_post):
+            run.step()
+        _barrier(torch, dist, world, local_rank, dev)
+    total = ev_step[0].elapsed_time(ev_step[steps])
+    per_step = [ev_step[i].elapsed_time(ev_step[i + 1]) for i in range(steps)]
+    per_kern = {m: [rec[i][m][0].elapsed_time(rec[i][m][1]) for i in range(steps)]
+                for m in run.kmodes}
+    if world > 1:
+        vec = [total] + per_step + [x for m in run.kmodes for x in per_kern[m]]
+        t = torch.tensor(vec, device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = t.tolist()
+        total, per_step = t[0], t[1:1 + steps]
+        off = 1 + steps
+        for m in run.kmodes:
+            per_kern[m], off = t[off:off + steps], off + steps
+    return {"total_ms": total, "per_step": per_step, "per_kern": per_kern,
+            "launches": launches, "clocks": clk.summary(),
+            "untimed_repeats": {"before": n_pre, "after": n_post}}
+
+
+def roofline_for(prob, mode, kern_ms, El, dtype, csr_nnz=0.0, cfg=""):
+    """Roofline of one kernel of the step: algorithmic bytes and flops per cell
+    x cells per launch / the kernel's mean launch duration, against the measured HBM copy
+    bandwidth or the measured FP64 (DFMA / DMMA) peak, whichever bounds it."""
+    nb, nq, D = prob.nb, prob.nq, prob.ncomp
+    esize = 8 if dtype == "f64" else 4
+    pk_b, src_b = hbm_peak_gbs()
+    t_s = kern_ms * 1e-3
+    if mode == "matrix+residual":
+        rf = roofline_for(prob, "matrix", kern_ms, El, dtype, csr_nnz, cfg)
+        by = rf["alg_bytes_per_cell"] * El + (4 * nb + 3 * D * prob.p ** 3 * 8) * El
+        fl = rf["alg_flops_per_cell"] * El + 2 * nb * nb * El      # r_e = K_e u_e
+        fpk, fsrc = fp64_peak_tflops("dfma_tflops_sustained")
+        if fl / (fpk * 1e12) >= by / (pk_b * 1e9):
+            base = {"bound": "alu", "achieved": fl / t_s / 1e12, "peak": fpk, "unit": "TFLOP/s",
+                    "frac": fl / t_s / 1e12 / fpk, "peak_source": fsrc}
+        else:
+            base = {"bound": "hbm", "achieved": by / t_s / 1e9, "peak": pk_b, "unit": "GB/s",
+                    "frac": by / t_s / 1e9 / pk_b, "peak_source": src_b}
+        rf.update(base)
+        rf.update({"kernel": f"matrix+residual fused ({fi.FORM_NAMES[prob.form]}, Q{prob.p}, "
+                             "sum-factorised, r_e = K_e u_e)",
+                   "kernel_ms": kern_ms, "alg_flops_per_cell": fl / El,
+                   "alg_bytes_per_cell": by / El, "achieved_gbs": by / t_s / 1e9,
+                   "achieved_tflops": fl / t_s / 1e12, "traffic": None})
+        return rf
+    fl_lean = alg_flops(prob.form, mode, nb, nq) * El
+    if mode == "matrix":
+        sf = uses_sf_matrix(prob.form, prob.p) or (
+            prob.form in (fi.ELASTICITY, fi.CONVECTIVE, fi.VECTOR_MASS) and prob.p <= 2
+            and os.environ.get("FEB200_MATRIX_IMPL", "") != "dense")
+    elif mode == "residual":
+        sf = uses_sf_residual(prob.p)
+    else:
+        sf = False
+    impl = "atomic-scatter" if mode == "csr" else ("sum-factorised" if sf else "dense-table")
+    if not sf:
+        fl = fl_lean
+    elif mode == "matrix" and uses_sf_matrix(prob.form, prob.p):
+        fl = sf_matrix_flops(prob.form, prob.p) * El
+    elif mode == "matrix" and prob.form in (fi.ELASTICITY, fi.CONVECTIVE) and prob.p == 2:
+        fl = sf_vector_matrix_flops(prob.form, prob.p) * El
+        impl = "sum-factorised, pipelined"
+    elif mode == "matrix":
+        fl = fl_lean  # single-stage vector SF kernel: flop count not modelled, lean dense count
+    else:
+        fl = sf_residual_flops(prob.form, prob.p) * El
+    by = alg_bytes(prob.form, mode, prob.p, nb, nq, D, prob.mat_kind, esize, csr_nnz) * El
+    if dtype == "f32":
+        pk_f, src_f, fbound = 74.4, "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz", "alu"
+    elif impl.startswith("sum-factorised") or mode == "csr":
+        pk_f, src_f = fp64_peak_tflops("dfma_tflops_sustained")
+        fbound = "alu"
+    else:
+        pk_f, src_f = fp64_peak_tflops("dmma_m16n8k4_tflops_sustained")
+        fbound = "tensor"
+    if fl / (pk_f * 1e12) >= by / (pk_b * 1e9):
+        rf = {"bound": fbound, "achieved": fl / t_s / 1e12, "peak": pk_f, "unit": "TFLOP/s",
+              "frac": (fl / t_s / 1e12) / pk_f, "peak_source": src_f}
+    else:
+        rf = {"bound": "hbm", "achieved": by / t_s / 1e9, "peak": pk_b, "unit": "GB/s",
+              "frac": (by / t_s / 1e9) / pk_b, "peak_source": src_b}
+    rf.update({"kernel": f"{mode} ({fi.FORM_NAMES[prob.form]}, Q{prob.p}, {impl})",
+               "lean_dense_flops_per_cell": fl_lean / El,
+               "effective_lean_tflops": fl_lean / t_s / 1e12,
+               "kernel_ms": kern_ms, "alg_flops_per_cell": fl / El,
+               "alg_bytes_per_cell": by / El, "cells_per_launch": El,
+               "achieved_gbs": by / t_s / 1e9, "achieved_tflops": fl / t_s / 1e12,
+               "traffic": None})
+    prof_ = os.path.join(ROOT, "profiles", f"traffic_{cfg}_{mode}.json")
+    if os.path.exists(prof_):
+        try:
+            rf["traffic"] = json.load(open(prof_)).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    return rf
+
+
+def summarize(run, res, dtype):
+    """Per-mode kernel statistics, result throughput and rooflines of a run."""
+    prob, El = run.prob, run.El
+    esize = 8 if dtype == "f64" else 4
+    csr_nnz = (run.csr.nnz / El) if run.csr is not None else 0.0
+    modes = {}
+    for m in run.kmodes:
+        ks = step_stats(res["per_kern"][m])
+        rf = roofline_for(prob, m, ks["mean"], El, dtype, csr_nnz, run.cfg)
+        rb = sum(result_bytes(prob, mm, esize) for mm in m.split("+") if mm != "csr")
+        modes[m] = {"kernel_ms": ks, "cells_per_s": El / (ks["mean"] * 1e-3),
+                    "result_mb_per_s": (rb * El / prob.n_elems) / (ks["tww"] * 1e-3) / 1e6,
+                    "roofline": rf}
+    return modes
+
+
+def measure_sub(cfg_name, args, world, rank, local_rank, dev):
+    """A sub-result of the default line: one more BASELINE form / mode measured like the
+    headline (warm-up, K timed steps, clocks over >= 1.2 s)."""
+    import torch
+    cfg, dt = split_cfg(cfg_name)
+    dtype = dt or "f64"
+    run = Runner(cfg, dtype, world, rank, dev, args.exchange)
+    try:
+        res = timed_run(run, args.steps, args.warmup, world, local_rank)
+        modes = summarize(run, res, dtype)
+        st = step_stats(res["per_step"])
+        out = {"config": config_dict(cfg, run.prob, run.modes, world, args.exchange, dtype),
+               "ms_per_step": res["total_ms"] / args.steps, "step_ms": st,
+               "cells_per_s": run.prob.n_elems / (res["total_ms"] / args.steps * 1e-3),
+               "modes": {m: {"kernel_ms": v["kernel_ms"], "cells_per_s": v["cells_per_s"],
+                             "result_mb_per_s": v["result_mb_per_s"],
+                             "roofline": {k: v["roofline"][k] for k in (
+                                 "bound", "achieved", "peak", "unit", "frac", "kernel",
+                                 "alg_bytes_per_cell", "alg_flops_per_cell", "traffic")}}
+                         for m, v in modes.items()},
+               "gpu_launches": int(res["launches"]), "clocks": res["clocks"]}
+    finally:
+        run.close()
+        del run
+        torch.cuda.synchronize(dev)
+        torch.cuda.empty_cache()
+    return out
+
+
+# ----------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sub-configs", default=None,
+                    help="comma-separated per-form sub-results for the line (default with "
+                         f"--config C2: {','.join(SUB_CONFIGS)}; 'none' to skip)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
                     help="N > 1 residual: interface planes by NCCL send/recv overlapped with the "
                          "interior (default) or added by the residual kernel itself into the "
@@ -357,9 +743,6 @@ def main():
     import torch
     import torch.distributed as dist
 
-    import paper_2107_04121_b200 as fe
-    from paper_2107_04121_b200 import slabs
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -367,197 +750,62 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     dev = torch.device("cuda", local_rank)
-
     cfg = args.config
-    modes = WORKLOADS[cfg]["modes"]
-    prob = build_problem(cfg)
-    # linear scalar forms at p <= 2: matrix + residual in one kernel (r_e = K_e u_e, pin P8)
-    fused = (args.fused and tuple(modes) == ("matrix", "residual") and args.dtype == "f64"
-             and prob.form in (fi.DIFFUSION, fi.MASS, fi.MASS_DIFFUSION) and prob.p <= 2)
-    kmodes = ("matrix+residual",) if fused else tuple(modes)
-    if cfg == "C5t" and world > 1:
-        raise SystemExit("C5t (corner tangent) is single-GPU")
-    tdt = torch.float64 if args.dtype == "f64" else torch.float32
-    dtc = fe.F64 if args.dtype == "f64" else fe.F32
-    if args.dtype == "f32" and "matrix" in modes:
-        raise SystemExit("fp32 is built for residual mode only")
-    D = prob.ncomp
-    nb, nq = prob.nb, prob.nq
+    run = Runner(cfg, args.dtype, world, rank, dev, args.exchange, args.fused)
+    prob, modes, El = run.prob, run.modes, run.El
+    fe = run.fe
 
-    if cfg == "C5t":
-        sl = slabs.Slab(0, 1, 0, prob.n_elems, 0, prob.coords.shape[0], 0, prob.n_nodes, 0)
-        lc, lconn, ldc = prob.coords, prob.conn, prob.dof_conn
-    elif "csr" in modes and world > 1:
-        # N2 with row ownership: the slab plus the first cell layer above, so the rank's owned
-        # block rows of the global CSR matrix are complete without communication
-        sl = slabs.ghost_slab_of(prob.shape, prob.p, world, rank)
-        lc, lconn, ldc = slabs.local_arrays(sl, prob.coords, prob.conn, prob.dof_conn)
-    else:
-        sl = slabs.slab_of(prob.shape, prob.p, world, rank)
-        lc, lconn, ldc = slabs.local_arrays(sl, prob.coords, prob.conn, prob.dof_conn)
-    e0, e1 = sl.elem_begin, sl.elem_end
-    El = e1 - e0
-    mesh = fe.Mesh(torch.from_numpy(lc), torch.from_numpy(lconn), prob.p, prob.q1d,
-                   dof_conn=torch.from_numpy(ldc), n_nodes=sl.n_nodes, device=dev)
+    res = timed_run(run, args.steps, args.warmup, world, local_rank)
+    ms_step = res["total_ms"] / args.steps
+    value = prob.n_elems / (ms_step * 1e-3)
+    mode_sum = summarize(run, res, args.dtype)
 
-    def dslice(a):
-        return None if a is None else torch.from_numpy(np.ascontiguousarray(a[e0:e1])).to(dev, tdt)
-
-    mat_a, mat_b = dslice(prob.mat_a), dslice(prob.mat_b)
-    u_loc = np.ascontiguousarray(prob.u[sl.node_begin:sl.node_end])
-    u = torch.from_numpy(u_loc).to(dev, tdt)
-    K = torch.empty((El, D * nb, D * nb), dtype=torch.float64, device=dev) if "matrix" in modes else None
-    peer = None
-    if world > 1 and args.exchange == "peer" and "residual" in modes and not fused:
-        if args.dtype != "f64":
-            raise SystemExit("--exchange peer is built for fp64 residuals")
-        peer = slabs.PeerExchange(sl, prob.shape, prob.p, D, dev)
-        r = peer.r
-        tiny = torch.zeros(1, dtype=torch.float32, device=dev)
-    else:
-        r = torch.zeros((sl.n_nodes, D), dtype=tdt, device=dev)
-    csr = fe.CSR(mesh, D) if "csr" in modes else None
-    csr_vals = torch.zeros(csr.nnz, dtype=torch.float64, device=dev) if csr is not None else None
-    stream = torch.cuda.current_stream(dev)
-    comm_stream = torch.cuda.Stream(dev) if world > 1 else None
-    bufs = [None]
-    ev = {m: [] for m in kmodes}
-
-    def step(record=False):
-        if fused:
-            r.zero_()
-            if record:
-                a = torch.cuda.Event(enable_timing=True); a.record(stream)
-
-            def evaluate_f(lo, hi):
-                fe.fe_eval_matrix_residual(mesh.handle, prob.form, fe.F64, prob.mat_kind, mat_a,
-                                           mat_b, u, lo, hi, K[lo:hi], None, r, stream)
-
-            bufs[0] = slabs.residual_overlapped(evaluate_f, r, sl, prob.shape,
-                                                comm_stream if world > 1 else None, bufs[0])
-            if record:
-                b = torch.cuda.Event(enable_timing=True); b.record(stream)
-                ev["matrix+residual"].append((a, b))
-            return
-        if "matrix" in modes:
-            if record:
-                a = torch.cuda.Event(enable_timing=True); a.record(stream)
-            fe.fe_eval_element_matrices(mesh.handle, prob.form, fe.F64, prob.mat_kind, mat_a, mat_b,
-                                        u if prob.form == fi.CONVECTIVE else None, 0, El, K, stream)
-            if record:
-                b = torch.cuda.Event(enable_timing=True); b.record(stream); ev["matrix"].append((a, b))
-        if "csr" in modes:
-            csr_vals.zero_()
-            if record:
-                a = torch.cuda.Event(enable_timing=True); a.record(stream)
-            csr.assemble(K, values=csr_vals, stream=stream)
-            if record:
-                b = torch.cuda.Event(enable_timing=True); b.record(stream); ev["csr"].append((a, b))
-        if "residual" in modes and peer is not None:
-            if record:
-                a = torch.cuda.Event(enable_timing=True); a.record(stream)
-
-            def evaluate_peer(windows):
-                fe.fe_eval_residual_peer(mesh.handle, prob.form, prob.mat_kind, mat_a, mat_b, u, 0,
-                                         El, None, r, windows, stream)
-
-            # zero -> device barrier (tiny NCCL all-reduce) -> fused residual + exchange over
-            # peer memory -> device barrier
-            peer.residual(evaluate_peer, lambda: dist.all_reduce(tiny))
-            if record:
-                b = torch.cuda.Event(enable_timing=True); b.record(stream); ev["residual"].append((a, b))
-        elif "residual" in modes:
-            r.zero_()
-            if record:
-                a = torch.cuda.Event(enable_timing=True); a.record(stream)
-
-            def evaluate(lo, hi):
-                fe.fe_eval_residual(mesh.handle, prob.form, dtc, prob.mat_kind, mat_a, mat_b, u, lo,
-                                    hi, None, r, stream)
-
-            # boundary-first residual; for N > 1 the interface exchange overlaps the interior
-            bufs[0] = slabs.residual_overlapped(evaluate, r, sl, prob.shape,
-                                                comm_stream if world > 1 else None, bufs[0])
-            if record:
-                b = torch.cuda.Event(enable_timing=True); b.record(stream); ev["residual"].append((a, b))
-
-    def barrier():
-        if world > 1:
-            dist.barrier(device_ids=[local_rank])
-        torch.cuda.synchronize(dev)
-
-    for _ in range(args.warmup):
-        step()
-    barrier()
-    n_launch0 = fe.fe_launch_count()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
-        barrier()
-        t0.record(stream)
-        for _ in range(args.steps):
-            step(record=True)
-        t1.record(stream)
-        barrier()
-    launches = fe.fe_launch_count() - n_launch0
-    ms = t0.elapsed_time(t1)
-    kern_ms = {m: float(np.mean([a.elapsed_time(b) for a, b in ev[m]])) for m in kmodes}
-    if world > 1:
-        tt = torch.tensor([ms] + [kern_ms[m] for m in kmodes], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt[0])
-        kern_ms = {m: float(tt[1 + i]) for i, m in enumerate(kmodes)}
     # alternative path of the same step, timed outside the timed region for the record:
     # the fused kernel when the step ran unfused, the two kernels when it ran fused
     fusable = (tuple(modes) == ("matrix", "residual") and args.dtype == "f64" and world == 1
                and prob.form in (fi.DIFFUSION, fi.MASS, fi.MASS_DIFFUSION) and prob.p <= 2)
-    fused_alt = None
-    if fusable and not fused:
+    mesh, st, u, r, K = run.mesh, run.stream, run.u, run.r, run.K
+    mat = (prob.mat_kind, run.mat_a, run.mat_b)
+    fused_alt = unfused = None
+    if fusable and not run.fused:
         n_f = 20
         fa, fb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        fe.fe_eval_matrix_residual(mesh.handle, prob.form, fe.F64, prob.mat_kind, mat_a, mat_b, u,
-                                   0, El, K, None, r, stream)
+        fe.fe_eval_matrix_residual(mesh.handle, prob.form, fe.F64, *mat, u, 0, El, K, None, r, st)
         torch.cuda.synchronize(dev)
-        fa.record(stream)
+        fa.record(st)
         for _ in range(n_f):
             r.zero_()
-            fe.fe_eval_matrix_residual(mesh.handle, prob.form, fe.F64, prob.mat_kind, mat_a, mat_b,
-                                       u, 0, El, K, None, r, stream)
-        fb.record(stream)
+            fe.fe_eval_matrix_residual(mesh.handle, prob.form, fe.F64, *mat, u, 0, El, K, None, r, st)
+        fb.record(st)
         torch.cuda.synchronize(dev)
         f_ms = fa.elapsed_time(fb) / n_f
         fused_alt = {"step_ms": f_ms, "cells_per_s": prob.n_elems / (f_ms * 1e-3),
                      "note": "fe_eval_matrix_residual: K_e and r_e = K_e u_e from one kernel pass "
                              "(linear form, pin P8), r zeroing included; not the timed step "
                              "(bench.py --fused times it)"}
-    unfused = None
-    if fused and world == 1:
+    if run.fused and world == 1:
         n_u = 20
         ea = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        tm, tr = 0.0, 0.0
+        tm = tr = 0.0
         for _ in range(n_u):
-            ea[0].record(stream)
-            fe.fe_eval_element_matrices(mesh.handle, prob.form, fe.F64, prob.mat_kind, mat_a, mat_b,
-                                        None, 0, El, K, stream)
-            ea[1].record(stream)
+            ea[0].record(st)
+            fe.fe_eval_element_matrices(mesh.handle, prob.form, fe.F64, *mat, None, 0, El, K, st)
+            ea[1].record(st)
             r.zero_()
-            fe.fe_eval_residual(mesh.handle, prob.form, dtc, prob.mat_kind, mat_a, mat_b, u, 0, El,
-                                None, r, stream)
-            ea[2].record(stream)
+            fe.fe_eval_residual(mesh.handle, prob.form, run.dtc, *mat, u, 0, El, None, r, st)
+            ea[2].record(st)
             torch.cuda.synchronize(dev)
             tm += ea[0].elapsed_time(ea[1])
             tr += ea[1].elapsed_time(ea[2])
         unfused = {"matrix_ms": tm / n_u, "residual_ms": tr / n_u, "step_ms": (tm + tr) / n_u,
                    "note": "separate fe_eval_element_matrices + fe_eval_residual, not the timed step"}
-    ms_step = ms / args.steps
-    value = prob.n_elems / (ms_step * 1e-3)
 
     # ---- end-to-end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        h_u = torch.from_numpy(u_loc).to(tdt).pin_memory()
-        h_a = None if mat_a is None else mat_a.cpu().pin_memory()
-        h_b = None if mat_b is None else mat_b.cpu().pin_memory()
+        h_u = torch.from_numpy(run.u_loc).to(run.tdt).pin_memory()
+        h_a = None if run.mat_a is None else run.mat_a.cpu().pin_memory()
+        h_b = None if run.mat_b is None else run.mat_b.cpu().pin_memory()
         h_r = torch.empty_like(r, device="cpu").pin_memory()
         h_K = torch.empty(K.shape, dtype=K.dtype).pin_memory() if K is not None else None
         n_e2e = max(3, min(args.steps, 10))
@@ -565,33 +813,32 @@ def main():
         def e2e_step():
             u.copy_(h_u, non_blocking=True)
             if h_a is not None:
-                mat_a.copy_(h_a, non_blocking=True)
+                run.mat_a.copy_(h_a, non_blocking=True)
             if h_b is not None:
-                mat_b.copy_(h_b, non_blocking=True)
-            step()
+                run.mat_b.copy_(h_b, non_blocking=True)
+            run.step()
             if h_K is not None:
                 h_K.copy_(K, non_blocking=True)
             h_r.copy_(r, non_blocking=True)
 
         e2e_step()
-        barrier()
+        _barrier(torch, dist, world, local_rank, dev)
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
+        a.record(st)
         for _ in range(n_e2e):
             e2e_step()
-        b.record(stream)
-        barrier()
+        b.record(st)
+        _barrier(torch, dist, world, local_rank, dev)
         e_ms = a.elapsed_time(b)
-        if world > 1:
-            tt = torch.tensor([e_ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e_ms = float(tt[0])
         h2d = h_u.numel() * h_u.element_size() + sum(
             x.numel() * x.element_size() for x in (h_a, h_b) if x is not None)
         d2h = h_r.numel() * h_r.element_size() + (
             h_K.numel() * h_K.element_size() if h_K is not None else 0)
         if world > 1:
+            tt = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e_ms = float(tt[0])
             tt = torch.tensor([h2d, d2h], device=dev, dtype=torch.float64)
             dist.all_reduce(tt)
             h2d, d2h = int(tt[0]), int(tt[1])
@@ -600,105 +847,29 @@ def main():
                "ms_per_step": e_ms / n_e2e, "steps": n_e2e,
                "note": "pinned host inputs (u, material) H2D + step + D2H of r"
                        + (" and K" if K is not None else "")}
+        del h_K
+    launches = int(res["launches"])
+    run.close()
+    del run, mesh, K, r, u
+    torch.cuda.synchronize(dev)
+    torch.cuda.empty_cache()
+
+    # ---- the other BASELINE forms / modes, each measured like the headline
+    subs_req = args.sub_configs if args.sub_configs is not None else (
+        ",".join(SUB_CONFIGS) if cfg == "C2" and not args.fused else "none")
+    subs = {}
+    for name in [s for s in subs_req.split(",") if s and s != "none"]:
+        if name == "C5t" and world > 1:
+            continue
+        subs[name] = measure_sub(name, args, world, rank, local_rank, dev)
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
 
-    # ---- roofline of every kernel of the step; the dominant one is the headline
-    esize = 8 if args.dtype == "f64" else 4
-    pk_b, src_b = hbm_peak_gbs()
-
-    def roofline_for(mode):
-        if mode == "matrix+residual":
-            kern_ms["matrix"] = kern_ms[mode]       # per-cell work of the matrix part only
-            rf = roofline_for("matrix")
-            del kern_ms["matrix"]
-            extra_b = (4 * nb + 3 * D * prob.p ** 3 * 8) * El      # dof ids, u gather, r RMW
-            extra_f = 2 * nb * nb * El                             # r_e = K_e u_e
-            t_s = kern_ms[mode] * 1e-3
-            by = rf["alg_bytes_per_cell"] * El + extra_b
-            fl = rf["alg_flops_per_cell"] * El + extra_f
-            hb, hsrc = hbm_peak_gbs()
-            fpk, fsrc = fp64_peak_tflops("dfma_tflops_sustained")
-            if fl / (fpk * 1e12) >= by / (hb * 1e9):
-                base = {"bound": "alu", "achieved": fl / t_s / 1e12, "peak": fpk, "unit": "TFLOP/s",
-                        "frac": fl / t_s / 1e12 / fpk, "peak_source": fsrc}
-            else:
-                base = {"bound": "hbm", "achieved": by / t_s / 1e9, "peak": hb, "unit": "GB/s",
-                        "frac": by / t_s / 1e9 / hb, "peak_source": hsrc}
-            rf.update(base)
-            rf.update({"kernel": f"matrix+residual fused ({fi.FORM_NAMES[prob.form]}, Q{prob.p}, "
-                                 "sum-factorised, r_e = K_e u_e)",
-                       "kernel_ms": kern_ms[mode], "alg_flops_per_cell": fl / El,
-                       "alg_bytes_per_cell": by / El, "achieved_gbs": by / t_s / 1e9,
-                       "achieved_tflops": fl / t_s / 1e12, "traffic": None})
-            prof_ = os.path.join(ROOT, "profiles", f"traffic_{cfg}_{mode}.json")
-            if os.path.exists(prof_):
-                try:
-                    rf["traffic"] = json.load(open(prof_)).get("dram_bytes_per_launch")
-                except Exception:
-                    pass
-            return rf
-        fl_lean = alg_flops(prob.form, mode, nb, nq) * El
-        if mode == "matrix":
-            sf = uses_sf_matrix(prob.form, prob.p) or (
-                prob.form in (fi.ELASTICITY, fi.CONVECTIVE, fi.VECTOR_MASS) and prob.p <= 2
-                and os.environ.get("FEB200_MATRIX_IMPL", "") != "dense")
-        elif mode == "residual":
-            sf = uses_sf_residual(prob.p)
-        else:
-            sf = False
-        impl = "atomic-scatter" if mode == "csr" else ("sum-factorised" if sf else "dense-table")
-        if not sf:
-            fl = fl_lean
-        elif mode == "matrix" and uses_sf_matrix(prob.form, prob.p):
-            fl = sf_matrix_flops(prob.form, prob.p) * El
-        elif mode == "matrix" and prob.form in (fi.ELASTICITY, fi.CONVECTIVE) and prob.p == 2:
-            fl = sf_vector_matrix_flops(prob.form, prob.p) * El
-            impl = "sum-factorised, pipelined"
-        elif mode == "matrix":
-            fl = fl_lean  # single-stage vector SF kernel: flop count not modelled, lean dense count
-        else:
-            fl = sf_residual_flops(prob.form, prob.p) * El
-        by = alg_bytes(prob.form, mode, prob.p, nb, nq, D, prob.mat_kind, esize,
-                       (csr.nnz / El) if csr is not None else 0.0) * El
-        t_s = kern_ms[mode] * 1e-3
-        if args.dtype == "f32":
-            pk_f, src_f, fbound = 74.4, "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz", "alu"
-        elif impl == "sum-factorised" or mode == "csr":
-            pk_f, src_f = fp64_peak_tflops("dfma_tflops_sustained")
-            fbound = "alu"
-        else:
-            pk_f, src_f = fp64_peak_tflops("dmma_m16n8k4_tflops_sustained")
-            fbound = "tensor"
-        t_flop = fl / (pk_f * 1e12)
-        t_mem = by / (pk_b * 1e9)
-        if t_flop >= t_mem:
-            rf = {"bound": fbound, "achieved": fl / t_s / 1e12, "peak": pk_f, "unit": "TFLOP/s",
-                  "frac": (fl / t_s / 1e12) / pk_f, "peak_source": src_f}
-        else:
-            rf = {"bound": "hbm", "achieved": by / t_s / 1e9, "peak": pk_b, "unit": "GB/s",
-                  "frac": (by / t_s / 1e9) / pk_b, "peak_source": src_b}
-        rf.update({"kernel": f"{mode} ({fi.FORM_NAMES[prob.form]}, Q{prob.p}, {impl})",
-                   "lean_dense_flops_per_cell": fl_lean / El,
-                   "effective_lean_tflops": fl_lean / t_s / 1e12,
-                   "kernel_ms": kern_ms[mode], "alg_flops_per_cell": fl / El,
-                   "alg_bytes_per_cell": by / El, "cells_per_launch": El,
-                   "achieved_gbs": by / t_s / 1e9, "achieved_tflops": fl / t_s / 1e12,
-                   "traffic": None})
-        prof_ = os.path.join(ROOT, "profiles", f"traffic_{cfg}_{mode}.json")
-        if os.path.exists(prof_):
-            try:
-                rf["traffic"] = json.load(open(prof_)).get("dram_bytes_per_launch")
-            except Exception:
-                pass
-        return rf
-
-    dom = max(kmodes, key=lambda m: kern_ms[m])
-    rooflines = {m: roofline_for(m) for m in kmodes}
-    roof = rooflines[dom]
+    dom = max(mode_sum, key=lambda m: mode_sum[m]["kernel_ms"]["mean"])
+    roof = mode_sum[dom]["roofline"]
     cb = None
     if not args.no_cpu_baseline and world == 1:
         cb = cpu_baseline(prob, modes)
@@ -708,20 +879,24 @@ def main():
         "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-        "config": {"workload": cfg, "desc": prob.meta.get("desc", ""), "cells": prob.n_elems,
-                   "order": prob.p, "q1d": prob.q1d, "form": fi.FORM_NAMES[prob.form],
-                   "modes": list(modes), "parallelism": f"z-slabs x{world}", "exchange": (args.exchange if world > 1 else None),
-                   "l2": "no flush: every step writes/reads > L2 (C2 K = 1.53 GB)"},
-        "modes": {m: {"kernel_ms": kern_ms[m], "cells_per_s": El / (kern_ms[m] * 1e-3),
-                      "roofline": {k: rooflines[m][k] for k in ("bound", "achieved", "unit", "frac")}}
-                  for m in kmodes},
+        "config": config_dict(cfg, prob, modes, world, args.exchange, args.dtype),
+        "stats": {"step_ms": step_stats(res["per_step"]),
+                  "note": "per-step CUDA-event times (max over ranks); tww = mean without the "
+                          "worst call (P:1158-1163)"},
+        "modes": {m: {"kernel_ms": v["kernel_ms"], "cells_per_s": v["cells_per_s"],
+                      "result_mb_per_s": v["result_mb_per_s"],
+                      "roofline": {k: v["roofline"][k] for k in ("bound", "achieved", "unit", "frac")}}
+                  for m, v in mode_sum.items()},
         "roofline": roof,
         "unfused": unfused,
         "fused": fused_alt,
         "cpu_baseline": cb,
         "e2e": e2e,
-        "gpu_launches": int(launches),
-        "clocks": clk.summary(),
+        "gpu_launches": launches,
+        "clocks": res["clocks"],
+        "untimed_repeats": res["untimed_repeats"],
+        "configs": subs,
+        "options": fe.get_options(),
     }
     print(json.dumps(line), flush=True)
     if world > 1:
