@@ -554,8 +554,8 @@ def timed_run(run, steps, warmup, world, local_rank, window_s=1.2):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         est = float(t[0])
     est = max(est, 1e-3)
-    n_pre = int(np.ceil(250.0 / est))
-    n_post = max(0, int(np.ceil((window_s * 1e3 - 250.0 - steps * est) / est)))
+    n_pre = int(np.ceil(250.0 / est)) if window_s > 0 else 0
+    n_post = max(0, int(np.ceil((window_s * 1e3 - 250.0 - steps * est) / est))) if window_s > 0 else 0
     ev_step = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
     rec = run.events(steps)
     fe = run.fe
@@ -693,7 +693,7 @@ def measure_sub(cfg_name, args, world, rank, local_rank, dev):
     dtype = dt or "f64"
     run = Runner(cfg, dtype, world, rank, dev, args.exchange)
     try:
-        res = timed_run(run, args.steps, args.warmup, world, local_rank)
+        res = timed_run(run, args.steps, args.warmup, world, local_rank, args.clock_window)
         modes = summarize(run, res, dtype)
         st = step_stats(res["per_step"])
         out = {"config": config_dict(cfg, run.prob, run.modes, world, args.exchange, dtype),
@@ -725,6 +725,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--clock-window", type=float, default=1.2,
+                    help="seconds of the clock-sampling window around the timed region (untimed "
+                         "repeats before/after it); 0 = timed region only (profiler runs)")
     ap.add_argument("--sub-configs", default=None,
                     help="comma-separated per-form sub-results for the line (default with "
                          f"--config C2: {','.join(SUB_CONFIGS)}; 'none' to skip)")
@@ -755,7 +758,7 @@ def main():
     prob, modes, El = run.prob, run.modes, run.El
     fe = run.fe
 
-    res = timed_run(run, args.steps, args.warmup, world, local_rank)
+    res = timed_run(run, args.steps, args.warmup, world, local_rank, args.clock_window)
     ms_step = res["total_ms"] / args.steps
     value = prob.n_elems / (ms_step * 1e-3)
     mode_sum = summarize(run, res, args.dtype)

@@ -25,6 +25,14 @@ KEYS = [
 ]
 
 
+EXTRA_PREFIXES = ("l1tex__data_pipe_lsu_wavefronts", "smsp__issue_active.avg.pct",
+                  "sm__inst_executed_pipe_lsu", "smsp__warps_active.avg.per_cycle_active",
+                  "l1tex__t_bytes_pipe_lsu_mem_global_op_ld", "lts__t_bytes.sum",
+                  "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_elapsed",
+                  "sm__pipe_fma_cycles_active", "sm__pipe_alu_cycles_active",
+                  "local_load", "local_store", "l1tex__t_sectors_pipe_lsu_mem_local")
+
+
 def main(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
@@ -38,6 +46,21 @@ def main(path):
         for k in KEYS:
             if k in d:
                 print(f"{k} = {d[k]} {u.get(k, '')}".rstrip())
+        for k in sorted(d):
+            if k.startswith(EXTRA_PREFIXES) or any(p in k for p in ("_mem_local",)):
+                if k not in KEYS and d[k] not in ("", "n/a"):
+                    print(f"{k} = {d[k]} {u.get(k, '')}".rstrip())
+        # warp stall breakdown: stalls per issued instruction, largest first
+        st = []
+        for k in d:
+            if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
+                try:
+                    st.append((float(d[k].replace(",", "")), k[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+                except ValueError:
+                    pass
+        if st:
+            st.sort(reverse=True)
+            print("stalls_per_issue = " + ", ".join(f"{n} {v:.2f}" for v, n in st if v >= 0.05))
         rd = d.get("dram__bytes_read.sum")
         if rd is not None:
             def tobytes(k):
