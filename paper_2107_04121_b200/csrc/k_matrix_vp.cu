@@ -35,17 +35,31 @@
 #ifndef FEB200_VP_E
 #define FEB200_VP_E 2
 #endif
-#ifndef FEB200_VP_XG
-#define FEB200_VP_XG 2
-#endif
-#ifndef FEB200_VP_S
-#define FEB200_VP_S 4
-#endif
 #ifndef FEB200_VP_TASKMAP
 #define FEB200_VP_TASKMAP 1
 #endif
-#ifndef FEB200_VP_GH
-#define FEB200_VP_GH 3
+// per-form role sizes (elasticity / convective): X groups, G pair groups, T1 ring depth.
+// Measured (B200, C3 / C5t): 4 G groups for elasticity (1.96 vs 2.10 ms with 3; 17 warps at
+// 96 registers), 2 for the convective tangent (3.69 vs 3.71 ms).  An X role with register
+// reuse (one thread per (cell, z pair, iy) over the three jy: a third of the T1 loads) was
+// 20-70 % slower in every X / G split tried -- the role becomes latency-bound.
+#ifndef FEB200_VP_XG_EL
+#define FEB200_VP_XG_EL 2
+#endif
+#ifndef FEB200_VP_XG_CV
+#define FEB200_VP_XG_CV 2
+#endif
+#ifndef FEB200_VP_GH_EL
+#define FEB200_VP_GH_EL 4
+#endif
+#ifndef FEB200_VP_GH_CV
+#define FEB200_VP_GH_CV 2
+#endif
+#ifndef FEB200_VP_S_EL
+#define FEB200_VP_S_EL 4
+#endif
+#ifndef FEB200_VP_S_CV
+#define FEB200_VP_S_CV 4
 #endif
 
 namespace feb200 {
@@ -161,8 +175,9 @@ struct VPL {
   using IT = VItems<FORM>;
   static constexpr int N1 = P + 1, Q1 = P + 1, NB = N1 * N1 * N1, NQ = Q1 * Q1 * Q1, Q2 = Q1 * Q1;
   static constexpr int NDOF = 3 * NB;
+  static constexpr bool EL = FORM == FE_FORM_ELASTICITY;
   static constexpr int E = FEB200_VP_E;                  // cells per batch
-  static constexpr int GH = FEB200_VP_GH;                // G threads per column (pair split)
+  static constexpr int GH = EL ? FEB200_VP_GH_EL : FEB200_VP_GH_CV;  // G pair groups
   static constexpr int QQP = (Q2 + 1) / 2 * 2;
   static constexpr int NWP = IT::NWP;                    // pair weights per qp (all items)
   static constexpr int G1T = E * NQ;                     // phase-1 tasks (per qp)
@@ -170,11 +185,11 @@ struct VPL {
   static constexpr int NG = ((G1T + 31) / 32 > GH * G2W) ? (G1T + 31) / 32 : GH * G2W;
   static constexpr int NFULL = N1 * N1 * N1 * N1;        // (z pair, y pair) tasks, ordered
   static constexpr int NSYM = N1 * N1 * (N1 * (N1 - 1) / 2) + N1 * (N1 * (N1 + 1) / 2);
-  static constexpr int XG = FEB200_VP_XG;                // X groups working on alternate items
+  static constexpr int XG = EL ? FEB200_VP_XG_EL : FEB200_VP_XG_CV;  // X groups (alternate items)
   static constexpr int NXW = (E * NFULL + 31) / 32;      // warps per X group
   static constexpr int NX = XG * NXW;
   static constexpr int THREADS = 32 * (1 + NG + NX);
-  static constexpr int S = FEB200_VP_S;                  // T1 ring depth (items)
+  static constexpr int S = EL ? FEB200_VP_S_EL : FEB200_VP_S_CV;  // T1 ring depth (items)
   static constexpr bool TASKMAP = FEB200_VP_TASKMAP && P == 2 && E == 2 && NXW == 6;
   static constexpr bool CONV = FORM == FE_FORM_CONVECTIVE;
   // L slot (doubles): coords [E][24], material a/b [E][NQ] | state [E][3][NB]
@@ -188,7 +203,7 @@ struct VPL {
   static constexpr size_t OFF_L = OFF_QD + size_t(E) * IT::NWP * NQ * 8;
   static constexpr size_t OFF_IDX = OFF_L + 2 * size_t(LSLOT) * 8;       // [2][E][8 + NB] int32
   static constexpr size_t OFF_BAR = (OFF_IDX + 2 * size_t(E) * (8 + NB) * 4 + 15) / 16 * 16;
-  static constexpr size_t BYTES = OFF_BAR + (4 + 2 * S) * 8;
+  static constexpr size_t BYTES = OFF_BAR + (6 + 2 * S) * 8;
 };
 
 template <int P, int FORM>
@@ -209,6 +224,12 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
   uint64_t* emptyL = bars + 2;  // [2]
   uint64_t* fullT = bars + 4;          // [S]
   uint64_t* emptyT = bars + 4 + L::S;  // [S]
+  // K staging handshake (single buffer): every X thread arrives on kfull after its last K
+  // write of a batch; the L warp then issues the TMA bulk store and arrives on kfree once the
+  // store has read the buffer; X threads wait on kfree before their first K write of the next
+  // batch (no CTA-wide barrier couples the two X groups or the store to the X warps)
+  uint64_t* kfull = bars + 4 + 2 * L::S;
+  uint64_t* kfree = bars + 5 + 2 * L::S;
   double* Kst = reinterpret_cast<double*>(smv + L::OFF_K);
   double* Wsm = reinterpret_cast<double*>(smv + L::OFF_QD);  // [E][NWP][NQ] pair weights
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -227,6 +248,8 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
       vp_bar_init(&fullT[s], 32 * L::NG);
       vp_bar_init(&emptyT[s], 32 * L::NXW);
     }
+    vp_bar_init(kfull, 32 * L::NX);
+    vp_bar_init(kfree, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -262,13 +285,39 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
     constexpr int XPL = (E * 24 + 31) / 32;
     constexpr int MPL = L::CONV ? 0 : (E * NQ + 31) / 32;
     constexpr int UPL = L::CONV ? (E * 3 * NB + 31) / 32 : 0;
+    // K store of batch j (after every X thread's last K write of it), then kfree
+    auto store_batch = [&](int64_t j) {
+      int64_t lbj;
+      int nej;
+      batch_of(j, lbj, nej);
+      if (nej <= 0) return;
+      VP_T(6, vp_wait(kfull, (uint32_t)(j & 1)));
+      const uint32_t bytes = (uint32_t)((size_t)nej * NDOF * NDOF * 8);
+      double* gdst = K + lbj * NDOF * NDOF;
+      if (((reinterpret_cast<uintptr_t>(gdst) | bytes) & 15u) == 0) {
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                       :: "l"(gdst), "r"(vp_u32(Kst)), "r"(bytes) : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+      } else {
+        for (int i = lane; i < nej * NDOF * NDOF; i += 32) gdst[i] = Kst[i];
+      }
+      __syncwarp();
+      if (lane == 0) vp_arrive(kfree);
+    };
     load_idx(0);
     __syncwarp();
+    int64_t nit = 0;  // batches of this CTA
     for (int64_t it = 0;; ++it) {
       int64_t lb;
       int ne;
       batch_of(it, lb, ne);
-      if (ne <= 0) break;
+      if (ne <= 0) {
+        nit = it;
+        break;
+      }
       const int sl = (int)(it & 1);
       const int32_t* ib = idxb + sl * E * (8 + NB);
       double xr[XPL], mra[MPL > 0 ? MPL : 1], mrb[MPL > 0 ? MPL : 1], ur[UPL > 0 ? UPL : 1];
@@ -304,6 +353,7 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
       }
       __syncwarp();
       load_idx(it + 1);  // other half of the index ring (read in iteration it - 1)
+      if (it >= 2) store_batch(it - 2);  // overlaps the latency of the gathers above
       VP_T(1, vp_wait(&emptyL[sl], (uint32_t)(((it >> 1) & 1) ^ 1)));
       double* slot = reinterpret_cast<double*>(smv + L::OFF_L) + sl * L::LSLOT;
 #pragma unroll
@@ -330,6 +380,9 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
       __syncwarp();
       vp_arrive(&fullL[sl]);
     }
+    if (nit >= 2) store_batch(nit - 2);
+    if (nit >= 1) store_batch(nit - 1);
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else if (warp <= L::NG) {
     // ======================= G: per-qp data, pair weights, stage z =======================
     const int gtid = tid - 32;
@@ -561,7 +614,6 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
     // ======================= X: stages y and x per item, K staging, TMA store =======================
     const int xall = tid - 32 * (1 + L::NG);
     const int xg = xall / (32 * L::NXW), xtid = xall - xg * 32 * L::NXW;  // group, thread in group
-    constexpr int NXA = 32 * L::NX;
     int task_full = -1, task_sym = -1;
     if constexpr (L::TASKMAP) {
       task_full = vp_tasks_full[xtid];
@@ -723,10 +775,10 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
           }
         }
         vp_arrive(&emptyT[s]);
-        if (I == xg) {
-          // first item of this group in the batch: the store of batch it-1 has finished reading
-          // K staging (elected thread, before this barrier of all X threads)
-          VP_T(5, vp_named_bar(2, NXA));
+        if (I == xg && it > 0) {
+          // first K write of this thread in the batch: the store of batch it-1 has read the
+          // staging buffer
+          VP_T(5, vp_wait(kfree, (uint32_t)((it - 1) & 1)));
         }
         if (ADV && xact && el < ne) {  // K_aa = A + R_aa for a = 0, 1, 2
           double* Kc = Kst + el * NDOF * NDOF;
@@ -758,23 +810,10 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
         if (IT::sym(i)) item(std::true_type{}, i, IT::a(i), IT::b(i));
         else item(std::false_type{}, i, IT::a(i), IT::b(i));
       }
-      // ---- store the batch
+      // ---- hand the batch's K staging to the store (L warp)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      VP_T(6, vp_named_bar(3, NXA));
-      const uint32_t bytes = (uint32_t)((size_t)ne * NDOF * NDOF * 8);
-      double* gdst = K + lb * NDOF * NDOF;
-      if (((reinterpret_cast<uintptr_t>(gdst) | bytes) & 15u) == 0) {
-        if (xall == 0) {
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                       :: "l"(gdst), "r"(vp_u32(Kst)), "r"(bytes) : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        }
-      } else {
-        for (int i = xall; i < ne * NDOF * NDOF; i += NXA) gdst[i] = Kst[i];
-      }
+      vp_arrive(kfull);
     }
-    if (xall == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
 #ifdef FEB200_VP_PROF
   if (lane == 0) {
