@@ -449,6 +449,7 @@ class Runner:
         self.stream = torch.cuda.current_stream(dev)
         self.comm_stream = torch.cuda.Stream(dev) if world > 1 else None
         self.bufs = [None]
+        self.bev = torch.cuda.Event()   # boundary -> exchange dependency (preallocated)
 
     def events(self, n):
         """Preallocated kernel events: rec[i][mode] = (start, end) for step i."""
@@ -457,7 +458,9 @@ class Runner:
                 for _ in range(n)]
 
     def step(self, rec=None):
-        fe, prob, mesh, st = self.fe, self.prob, self.mesh, self.stream
+        # every call goes to the CURRENT stream (the capture stream under --graph)
+        fe, prob, mesh = self.fe, self.prob, self.mesh
+        st = self.torch.cuda.current_stream(self.dev)
         mat = (prob.mat_kind, self.mat_a, self.mat_b)
         u, r, El, K = self.u, self.r, self.El, self.K
         comm = self.comm_stream if self.world > 1 else None
@@ -471,7 +474,7 @@ class Runner:
                                            K[lo:hi], None, r, st)
 
             self.bufs[0] = self.slabs.residual_overlapped(evaluate_f, r, self.sl, prob.shape, comm,
-                                                          self.bufs[0])
+                                                          self.bufs[0], events=self.bev)
             if rec:
                 rec["matrix+residual"][1].record(st)
             return
@@ -512,7 +515,7 @@ class Runner:
 
             # boundary-first residual; for N > 1 the interface exchange overlaps the interior
             self.bufs[0] = self.slabs.residual_overlapped(evaluate, r, self.sl, prob.shape, comm,
-                                                          self.bufs[0])
+                                                          self.bufs[0], events=self.bev)
             if rec:
                 rec["residual"][1].record(st)
 
@@ -530,7 +533,7 @@ def _barrier(torch, dist, world, local_rank, dev):
     torch.cuda.synchronize(dev)
 
 
-def timed_run(run, steps, warmup, world, local_rank, window_s=1.2):
+def timed_run(run, steps, warmup, world, local_rank, window_s=1.2, graph=False):
     """W warm-up steps; then, under the clock sampler, untimed repeats (>= 0.25 s), EXACTLY K
     timed steps bracketed by barrier + synchronize with CUDA events on the launching stream
     (per-step and per-kernel events preallocated), and untimed repeats until the sampler
@@ -541,6 +544,14 @@ def timed_run(run, steps, warmup, world, local_rank, window_s=1.2):
     for _ in range(warmup):
         run.step()
     _barrier(torch, dist, world, local_rank, dev)
+    if graph:
+        # the whole step captured once into a CUDA graph (slabs.StepGraph); the timed loop
+        # replays it (per-kernel events are not recorded inside the graph: kernel times come
+        # from an eager pass after the timed region)
+        gr = run.slabs.StepGraph(run.step, dev)
+        eager_step = run.step
+        run.step = lambda rec=None: gr.replay()
+        _barrier(torch, dist, world, local_rank, dev)
     # step-time estimate (same on every rank: NCCL steps must match in count)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(st)
@@ -564,14 +575,27 @@ def timed_run(run, steps, warmup, world, local_rank, window_s=1.2):
             run.step()
         _barrier(torch, dist, world, local_rank, dev)
         n_launch0 = fe.fe_launch_count()
+        h0 = time.perf_counter()
         ev_step[0].record(st)
         for i in range(steps):
             run.step(rec[i])
             ev_step[i + 1].record(st)
+        h1 = time.perf_counter()
         _barrier(torch, dist, world, local_rank, dev)
         launches = fe.fe_launch_count() - n_launch0
         for _ in range(n_post):
             run.step()
+        _barrier(torch, dist, world, local_rank, dev)
+    host_us = (h1 - h0) / steps * 1e6
+    if graph:
+        run.step = eager_step
+        # graph nodes: count the kernels of one eager step (the graph replays exactly these)
+        n0 = fe.fe_launch_count()
+        run.step()
+        launches = (fe.fe_launch_count() - n0) * steps
+        _barrier(torch, dist, world, local_rank, dev)
+        for i in range(steps):
+            run.step(rec[i])
         _barrier(torch, dist, world, local_rank, dev)
     total = ev_step[0].elapsed_time(ev_step[steps])
     per_step = [ev_step[i].elapsed_time(ev_step[i + 1]) for i in range(steps)]
@@ -587,7 +611,7 @@ def timed_run(run, steps, warmup, world, local_rank, window_s=1.2):
         for m in run.kmodes:
             per_kern[m], off = t[off:off + steps], off + steps
     return {"total_ms": total, "per_step": per_step, "per_kern": per_kern,
-            "launches": launches, "clocks": clk.summary(),
+            "launches": launches, "clocks": clk.summary(), "host_us_per_step": host_us,
             "untimed_repeats": {"before": n_pre, "after": n_post}}
 
 
@@ -693,7 +717,8 @@ def measure_sub(cfg_name, args, world, rank, local_rank, dev):
     dtype = dt or "f64"
     run = Runner(cfg, dtype, world, rank, dev, args.exchange)
     try:
-        res = timed_run(run, args.steps, args.warmup, world, local_rank, args.clock_window)
+        res = timed_run(run, args.steps, args.warmup, world, local_rank, args.clock_window,
+                        graph=args.graph)
         modes = summarize(run, res, dtype)
         st = step_stats(res["per_step"])
         out = {"config": config_dict(cfg, run.prob, run.modes, world, args.exchange, dtype),
@@ -705,7 +730,8 @@ def measure_sub(cfg_name, args, world, rank, local_rank, dev):
                                  "bound", "achieved", "peak", "unit", "frac", "kernel",
                                  "alg_bytes_per_cell", "alg_flops_per_cell", "traffic")}}
                          for m, v in modes.items()},
-               "gpu_launches": int(res["launches"]), "clocks": res["clocks"]}
+               "gpu_launches": int(res["launches"]), "clocks": res["clocks"],
+               "host_us_per_step": res["host_us_per_step"], "graph": bool(args.graph)}
     finally:
         run.close()
         del run
@@ -735,6 +761,10 @@ def main():
                     help="N > 1 residual: interface planes by NCCL send/recv overlapped with the "
                          "interior (default) or added by the residual kernel itself into the "
                          "neighbours' vectors over peer memory (fe_eval_residual_peer)")
+    ap.add_argument("--graph", action="store_true",
+                    help="capture each rank's whole step (boundary cells, exchange on the comm "
+                         "stream, interior cells, plane adds) into a CUDA graph and time its "
+                         "replays (kernel times from an eager pass)")
     ap.add_argument("--fused", action="store_true",
                     help="C2-type steps: fe_eval_matrix_residual (K_e and r_e = K_e u_e from one "
                          "pass) instead of the separate matrix and residual kernels")
@@ -758,7 +788,8 @@ def main():
     prob, modes, El = run.prob, run.modes, run.El
     fe = run.fe
 
-    res = timed_run(run, args.steps, args.warmup, world, local_rank, args.clock_window)
+    res = timed_run(run, args.steps, args.warmup, world, local_rank, args.clock_window,
+                    graph=args.graph)
     ms_step = res["total_ms"] / args.steps
     value = prob.n_elems / (ms_step * 1e-3)
     mode_sum = summarize(run, res, args.dtype)
@@ -898,6 +929,8 @@ def main():
         "gpu_launches": launches,
         "clocks": res["clocks"],
         "untimed_repeats": res["untimed_repeats"],
+        "graph": bool(args.graph),
+        "host_us_per_step": res["host_us_per_step"],
         "configs": subs,
         "options": fe.get_options(),
     }

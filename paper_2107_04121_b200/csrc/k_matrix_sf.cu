@@ -37,6 +37,9 @@
 #ifndef FEB200_SFP_NOX
 #define FEB200_SFP_NOX 0
 #endif
+#ifndef FEB200_SFP_NOG
+#define FEB200_SFP_NOG 0  // experiment: G skips geometry and stage z (X reads stale T1)
+#endif
 #ifndef FEB200_SFP_GH
 #define FEB200_SFP_GH 1
 #endif
@@ -782,7 +785,7 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
       // stage z into T1 slot it % 2 once X has released it
       SFP_T(3, sfp_wait(&emptyT[sl], par ^ 1u));
       double* T1 = reinterpret_cast<double*>(smp + L::OFF_T1 + sl * L::T1SLOT);
-      if (gact) {
+      if (gact && !FEB200_SFP_NOG) {
 #pragma unroll
         for (int ul = 0; ul < NUP; ++ul) {
           if (L::GH > 1 && (ul < ulo || ul >= uhi)) continue;

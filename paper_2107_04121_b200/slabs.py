@@ -101,14 +101,18 @@ def layer_cells(shape, world: int) -> int:
     return shape[0] * shape[1]
 
 
-def residual_overlapped(evaluate, r: torch.Tensor, slab: Slab, shape, comm_stream=None, bufs=None):
+def residual_overlapped(evaluate, r: torch.Tensor, slab: Slab, shape, comm_stream=None, bufs=None,
+                        exchange=None, events=None):
     """Boundary-first residual step with the interface exchange overlapped.
 
     evaluate(a, b) launches the fused residual kernel for local cells [a, b) on the current
     stream.  The two boundary z-layers are evaluated first; their node planes are then final,
-    so the NCCL exchange of those planes runs on `comm_stream` while the interior layers are
-    evaluated (the interior cells never touch the interface planes).  The current stream
-    waits for the exchange before returning."""
+    so the exchange of those planes (`exchange(r, slab, group, bufs)`, default the NCCL / gloo
+    exchange_planes) runs on `comm_stream` while the interior layers are evaluated (the
+    interior cells never touch the interface planes).  The current stream waits for the
+    exchange before returning.  `events`: a preallocated torch.cuda.Event for the
+    boundary -> exchange dependency (none is created per step when it is given)."""
+    exchange = exchange_planes if exchange is None else exchange
     n_local = slab.n_elems
     if slab.world == 1:
         evaluate(0, n_local)
@@ -117,10 +121,10 @@ def residual_overlapped(evaluate, r: torch.Tensor, slab: Slab, shape, comm_strea
     if comm_stream is None:  # CPU / gloo: same boundary-first order, no concurrency
         if n_local <= 2 * L:
             evaluate(0, n_local)
-            return exchange_planes(r, slab, None, bufs)
+            return exchange(r, slab, None, bufs)
         evaluate(0, L)
         evaluate(n_local - L, n_local)
-        bufs = exchange_planes(r, slab, None, bufs)
+        bufs = exchange(r, slab, None, bufs)
         evaluate(L, n_local - L)
         return bufs
     main = torch.cuda.current_stream(r.device)
@@ -131,15 +135,140 @@ def residual_overlapped(evaluate, r: torch.Tensor, slab: Slab, shape, comm_strea
         evaluate(0, L)
         evaluate(n_local - L, n_local)
         lo_hi_done = None
-    ev = torch.cuda.Event()
+    ev = torch.cuda.Event() if events is None else events
     ev.record(main)
     comm_stream.wait_event(ev)
     with torch.cuda.stream(comm_stream):
-        bufs = exchange_planes(r, slab, None, bufs)
+        bufs = exchange(r, slab, None, bufs)
     if lo_hi_done is None:
         evaluate(L, n_local - L)
     main.wait_stream(comm_stream)
     return bufs
+
+
+class VirtualWorld:
+    """P z-slab "ranks" on ONE device in one process (one host thread per rank): the
+    interface exchange of exchange_planes done by device copies instead of NCCL, so the
+    multi-rank code path (residual_overlapped's comm-stream exchange, boundary-first order,
+    plane adds, CUDA-graph capture) runs and is checked on a single GPU.
+
+    exchange(r, slab, group, bufs) for rank g, on its comm stream: "send" = copy its first /
+    last plane into the receive buffer that rank g-1 / g+1 owns, record an event; a host
+    barrier (every rank has enqueued its sends and recorded its event); "receive" = wait for
+    the neighbours' send events, add the buffers into its own planes -- the order of the NCCL
+    send/recv + add.  No kernel waits on another rank's kernel (only stream-event order)."""
+
+    def __init__(self, slabs_, ncomp, device, dtype=torch.float64):
+        import threading
+        self.slabs = slabs_
+        P = len(slabs_)
+        self.barrier = threading.Barrier(P, timeout=120)
+        D = ncomp
+        # recv[g] = [from g-1 (into my first plane), from g+1 (into my last plane)]
+        self.recv = [[torch.empty(s.plane * D, dtype=dtype, device=device) for _ in range(2)]
+                     for s in slabs_]
+        self.sent = [torch.cuda.Event() for _ in range(P)]
+
+    def exchange_for(self, rank):
+        def exchange(r, slab, group, bufs):
+            P = len(self.slabs)
+            pl = slab.plane
+            D = r.shape[1] if r.dim() > 1 else 1
+            flat = r.view(-1)
+            lo = flat[: pl * D]
+            hi = flat[flat.numel() - pl * D:]
+            if rank > 0:
+                self.recv[rank - 1][1].copy_(lo)
+            if rank < P - 1:
+                self.recv[rank + 1][0].copy_(hi)
+            self.sent[rank].record(torch.cuda.current_stream(r.device))
+            self.barrier.wait()
+            st = torch.cuda.current_stream(r.device)
+            if rank > 0:
+                st.wait_event(self.sent[rank - 1])
+                lo.add_(self.recv[rank][0])
+            if rank < P - 1:
+                st.wait_event(self.sent[rank + 1])
+                hi.add_(self.recv[rank][1])
+            self.barrier.wait()  # no rank reuses a receive buffer of this step early
+            return bufs
+        return exchange
+
+
+def virtual_world_step(slabs_, evaluators, rs, mains, comms, world: VirtualWorld, shape,
+                       events=None):
+    """One residual step of every virtual rank enqueued from ONE host thread, so that the
+    whole world's step can be captured into a single CUDA graph: per rank, zero r and the
+    boundary layers on its main stream; then the sends (device copies) on its comm stream;
+    then the interior layers on the main stream while the comm stream adds the received
+    planes; the main stream joins the comm stream.  The same order as residual_overlapped +
+    exchange_planes, phase by phase over the ranks.  All streams must have been forked from
+    the caller's current stream (mains[g] / comms[g] wait on it); the caller joins them."""
+    P = len(slabs_)
+    if events is None:
+        events = [torch.cuda.Event() for _ in range(P)]
+    L = layer_cells(shape, P)
+    for g in range(P):
+        with torch.cuda.stream(mains[g]):
+            rs[g].zero_()
+            n = slabs_[g].n_elems
+            if n <= 2 * L:
+                evaluators[g](0, n)
+            else:
+                evaluators[g](0, L)
+                evaluators[g](n - L, n)
+            events[g].record(mains[g])
+    for g in range(P):
+        comms[g].wait_event(events[g])
+        with torch.cuda.stream(comms[g]):
+            sl, r = slabs_[g], rs[g]
+            D = r.shape[1] if r.dim() > 1 else 1
+            flat = r.view(-1)
+            if g > 0:
+                world.recv[g - 1][1].copy_(flat[: sl.plane * D])
+            if g < P - 1:
+                world.recv[g + 1][0].copy_(flat[flat.numel() - sl.plane * D:])
+            world.sent[g].record(comms[g])
+    for g in range(P):
+        n = slabs_[g].n_elems
+        with torch.cuda.stream(mains[g]):
+            if n > 2 * L:
+                evaluators[g](L, n - L)
+        with torch.cuda.stream(comms[g]):
+            sl, r = slabs_[g], rs[g]
+            D = r.shape[1] if r.dim() > 1 else 1
+            flat = r.view(-1)
+            if g > 0:
+                comms[g].wait_event(world.sent[g - 1])
+                flat[: sl.plane * D].add_(world.recv[g][0])
+            if g < P - 1:
+                comms[g].wait_event(world.sent[g + 1])
+                flat[flat.numel() - sl.plane * D:].add_(world.recv[g][1])
+        mains[g].wait_stream(comms[g])
+
+
+class StepGraph:
+    """A rank's whole step (e.g. zero r, boundary cells, exchange on the comm stream,
+    interior cells, plane adds) captured once into a CUDA graph and replayed: one host call
+    per step instead of ~10.  `step()` must issue its work on the current
+    stream (torch.cuda.current_stream()), which is the capture stream while capturing; NCCL
+    P2P inside the step is captured as well (NCCL >= 2.9.6).  warmup: eager runs on the
+    capture stream before capturing (libraries / NCCL set up lazily)."""
+
+    def __init__(self, step, device, warmup=2):
+        self.device = device
+        self.stream = torch.cuda.Stream(device)
+        self.stream.wait_stream(torch.cuda.current_stream(device))
+        with torch.cuda.stream(self.stream):
+            for _ in range(warmup):
+                step()
+        torch.cuda.current_stream(device).wait_stream(self.stream)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            step()
+
+    def replay(self):
+        self.graph.replay()
 
 
 def peer_windows(slab: Slab, shape, p: int, prev_ptr, next_ptr):
