@@ -55,12 +55,28 @@ def slab_of(shape, p: int, world: int, rank: int) -> Slab:
                 p * z0 * plane, (p * z1 + 1) * plane, plane)
 
 
-def local_arrays(slab: Slab, coords, conn, dof_conn):
-    """Rank-local mesh arrays: vertex/node ids renumbered into the slab's ranges."""
+def boundary_first_order(slab: Slab, shape) -> np.ndarray:
+    """Local cell order with the slab's two boundary z-layers first (first layer, last
+    layer, then the interior layers in order): the boundary cells are then ONE contiguous
+    range [0, 2 L) and the step of residual_overlapped(boundary_first=True) needs two
+    launches instead of three.  Returns the permutation of the slab's local cell ids."""
+    L = layer_cells(shape, slab.world)
+    n = slab.n_elems
+    idx = np.arange(n)
+    if slab.world == 1 or n <= 2 * L:
+        return idx
+    return np.concatenate([idx[:L], idx[n - L:], idx[L:n - L]])
+
+
+def local_arrays(slab: Slab, coords, conn, dof_conn, order=None):
+    """Rank-local mesh arrays: vertex/node ids renumbered into the slab's ranges; `order`
+    (e.g. boundary_first_order) permutes the slab's cells (per-cell inputs such as the
+    material must be permuted the same way)."""
     e0, e1 = slab.elem_begin, slab.elem_end
     lc = np.ascontiguousarray(coords[slab.vert_begin:slab.vert_end])
-    lconn = np.ascontiguousarray(conn[e0:e1] - slab.vert_begin).astype(np.int32)
-    ldc = np.ascontiguousarray(dof_conn[e0:e1] - slab.node_begin).astype(np.int32)
+    cells = np.arange(e0, e1) if order is None else e0 + np.asarray(order)
+    lconn = np.ascontiguousarray(conn[cells] - slab.vert_begin).astype(np.int32)
+    ldc = np.ascontiguousarray(dof_conn[cells] - slab.node_begin).astype(np.int32)
     assert lconn.min() >= 0 and lconn.max() < slab.vert_end - slab.vert_begin
     assert ldc.min() >= 0 and ldc.max() < slab.n_nodes
     return lc, lconn, ldc
@@ -102,7 +118,7 @@ def layer_cells(shape, world: int) -> int:
 
 
 def residual_overlapped(evaluate, r: torch.Tensor, slab: Slab, shape, comm_stream=None, bufs=None,
-                        exchange=None, events=None):
+                        exchange=None, events=None, boundary_first=False):
     """Boundary-first residual step with the interface exchange overlapped.
 
     evaluate(a, b) launches the fused residual kernel for local cells [a, b) on the current
@@ -111,7 +127,9 @@ def residual_overlapped(evaluate, r: torch.Tensor, slab: Slab, shape, comm_strea
     exchange_planes) runs on `comm_stream` while the interior layers are evaluated (the
     interior cells never touch the interface planes).  The current stream waits for the
     exchange before returning.  `events`: a preallocated torch.cuda.Event for the
-    boundary -> exchange dependency (none is created per step when it is given)."""
+    boundary -> exchange dependency (none is created per step when it is given).
+    boundary_first: the local cells are in boundary_first_order (boundary cells = [0, 2L),
+    one launch instead of two)."""
     exchange = exchange_planes if exchange is None else exchange
     n_local = slab.n_elems
     if slab.world == 1:
@@ -131,6 +149,9 @@ def residual_overlapped(evaluate, r: torch.Tensor, slab: Slab, shape, comm_strea
     if n_local <= 2 * L:
         evaluate(0, n_local)
         lo_hi_done = [(0, n_local)]
+    elif boundary_first:
+        evaluate(0, 2 * L)
+        lo_hi_done = None
     else:
         evaluate(0, L)
         evaluate(n_local - L, n_local)
@@ -141,7 +162,10 @@ def residual_overlapped(evaluate, r: torch.Tensor, slab: Slab, shape, comm_strea
     with torch.cuda.stream(comm_stream):
         bufs = exchange(r, slab, None, bufs)
     if lo_hi_done is None:
-        evaluate(L, n_local - L)
+        if boundary_first:
+            evaluate(2 * L, n_local)
+        else:
+            evaluate(L, n_local - L)
     main.wait_stream(comm_stream)
     return bufs
 
@@ -264,7 +288,8 @@ class StepGraph:
                 step()
         torch.cuda.current_stream(device).wait_stream(self.stream)
         self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph, stream=self.stream):
+        # thread_local: CUDA calls of other host threads (the NCCL watchdog) stay legal
+        with torch.cuda.graph(self.graph, stream=self.stream, capture_error_mode="thread_local"):
             step()
 
     def replay(self):

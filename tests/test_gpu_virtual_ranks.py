@@ -23,7 +23,7 @@ CASES = {"md_q4": (fi.MASS_DIFFUSION, 4, (3, 2, 8)), "diff_q2": (fi.DIFFUSION, 2
          "elas_q2": (fi.ELASTICITY, 2, (3, 3, 4)), "conv_q2": (fi.CONVECTIVE, 2, (2, 3, 4))}
 
 
-def _setup(case, P, seed=777):
+def _setup(case, P, seed=777, boundary_first=False):
     import paper_2107_04121_b200 as fe
     from paper_2107_04121_b200 import slabs
     form, p, shape = CASES[case]
@@ -32,12 +32,14 @@ def _setup(case, P, seed=777):
     sls = [slabs.slab_of(shape, p, P, g) for g in range(P)]
     ranks = []
     for sl in sls:
-        lc, lconn, ldc = slabs.local_arrays(sl, pr.coords, pr.conn, pr.dof_conn)
+        order = slabs.boundary_first_order(sl, shape) if boundary_first else None
+        lc, lconn, ldc = slabs.local_arrays(sl, pr.coords, pr.conn, pr.dof_conn, order)
         e0, e1 = sl.elem_begin, sl.elem_end
+        cells = np.arange(e0, e1) if order is None else e0 + order
         mesh = fe.Mesh(torch.from_numpy(lc), torch.from_numpy(lconn), p, p + 1,
                        dof_conn=torch.from_numpy(ldc), n_nodes=sl.n_nodes)
         cut = (lambda a: None if a is None else torch.from_numpy(
-            np.ascontiguousarray(a[e0:e1])).cuda())
+            np.ascontiguousarray(a[cells])).cuda())
         u = torch.from_numpy(np.ascontiguousarray(pr.u[sl.node_begin:sl.node_end])).cuda()
         r = torch.zeros((sl.n_nodes, pr.ncomp), dtype=torch.float64, device="cuda")
         ranks.append(dict(sl=sl, mesh=mesh, ma=cut(pr.mat_a), mb=cut(pr.mat_b), u=u, r=r,
@@ -63,13 +65,16 @@ def _check(pr, ref, ranks):
             assert np.array_equal(R[-sl.plane:], Rn[:sl.plane])  # both copies bitwise equal
 
 
-@pytest.mark.parametrize("case,P", [("md_q4", 2), ("md_q4", 4), ("md_q4", 8), ("diff_q2", 4),
-                                    ("elas_q2", 2), ("conv_q2", 4)])
-def test_virtual_ranks_threaded(case, P):
+@pytest.mark.parametrize("case,P,bf", [("md_q4", 2, False), ("md_q4", 4, False),
+                                       ("md_q4", 8, False), ("diff_q2", 4, False),
+                                       ("elas_q2", 2, False), ("conv_q2", 4, False),
+                                       ("md_q4", 4, True), ("diff_q2", 2, True)])
+def test_virtual_ranks_threaded(case, P, bf):
     """One host thread per virtual rank runs slabs.residual_overlapped (boundary layers,
     exchange on the comm stream, interior layers) with the device-copy exchange; two steps
-    (re-zeroing and buffer reuse)."""
-    fe, slabs, pr, ref, sls, ranks = _setup(case, P)
+    (re-zeroing and buffer reuse).  bf: cells in boundary_first_order (boundary layers in
+    one launch)."""
+    fe, slabs, pr, ref, sls, ranks = _setup(case, P, boundary_first=bf)
     world = slabs.VirtualWorld(sls, pr.ncomp, "cuda")
     errs = []
 
@@ -82,7 +87,8 @@ def test_virtual_ranks_threaded(case, P):
                     rk["r"].zero_()
                     slabs.residual_overlapped(_evaluator(fe, pr, rk_), rk["r"], rk["sl"],
                                               CASES[case][2], rk["comm"],
-                                              exchange=world.exchange_for(g), events=ev)
+                                              exchange=world.exchange_for(g), events=ev,
+                                              boundary_first=bf)
                     rk["main"].synchronize()
                     world.barrier.wait()  # nobody zeroes before everybody finished the step
         except Exception as ex:  # pragma: no cover - reported below

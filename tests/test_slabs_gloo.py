@@ -174,3 +174,26 @@ def test_peer_windows_map_shared_planes(world, p):
             assert hi - lo == sl.plane
             for n in (lo, (lo + hi) // 2, hi - 1):
                 assert sl.node_begin + n == nb.node_begin + (n - lo + off)
+
+
+def test_boundary_first_order():
+    """Boundary layers first: a permutation whose first 2L cells are the slab's first and last
+    z-layers and whose rest is the interior in order (host bookkeeping, no exchange)."""
+    shape, p = (3, 2, 8), 2
+    for world in (1, 2, 4):
+        for rank in range(world):
+            sl = slabs.slab_of(shape, p, world, rank)
+            o = slabs.boundary_first_order(sl, shape)
+            assert sorted(o.tolist()) == list(range(sl.n_elems))
+            L = shape[0] * shape[1]
+            if world > 1 and sl.n_elems > 2 * L:
+                ez = o // L
+                nl = sl.n_elems // L
+                assert set(ez[:2 * L].tolist()) == {0, nl - 1}
+                assert (np.diff(o[2 * L:]) == 1).all()
+    pr = fi.make_problem(fi.DIFFUSION, p, shape, 3)
+    sl = slabs.slab_of(shape, p, 2, 1)
+    o = slabs.boundary_first_order(sl, shape)
+    lc, lconn, ldc = slabs.local_arrays(sl, pr.coords, pr.conn, pr.dof_conn, o)
+    lc0, lconn0, ldc0 = slabs.local_arrays(sl, pr.coords, pr.conn, pr.dof_conn)
+    assert (lconn == lconn0[o]).all() and (ldc == ldc0[o]).all()

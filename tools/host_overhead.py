@@ -121,6 +121,50 @@ def main():
     res["graph"] = {"device_ms_per_step": graph_ms, "host_us_per_step": graph_host_us}
     res["graph_over_kernel"] = graph_ms / kern_ms
     res["eager_over_kernel"] = eager_ms / kern_ms
+    # variants of the same step, graph-replayed: (b) the rank's cells in boundary-first order
+    # (boundary layers one launch), (c) no overlap: all cells in one launch, then the exchange
+    order = slabs.boundary_first_order(sl, pr.shape)
+    lc, lconn, ldc = slabs.local_arrays(sl, pr.coords, pr.conn, pr.dof_conn, order)
+    e0 = sl.elem_begin
+    mesh_b = fe.Mesh(torch.from_numpy(lc), torch.from_numpy(lconn), pr.p, pr.q1d,
+                     dof_conn=torch.from_numpy(ldc), n_nodes=sl.n_nodes)
+    cutb = (lambda a: None if a is None else torch.from_numpy(
+        np.ascontiguousarray(a[e0 + order])).to("cuda", tdt))
+    rkb = dict(rk, mesh=mesh_b, ma=cutb(pr.mat_a), mb=cutb(pr.mat_b))
+    evb = evaluator(rkb)
+
+    def step_b():
+        rk["r"].zero_()
+        slabs.residual_overlapped(evb, rk["r"], sl, pr.shape, rk["comm"], exchange=one_rank_exchange,
+                                  events=bufs_ev, boundary_first=True)
+
+    def step_c():
+        rk["r"].zero_()
+        evg(0, sl.n_elems)
+        one_rank_exchange(rk["r"], sl, None, None)
+
+    # (d) the fused residual + exchange (fe_eval_residual_peer): the kernel's own scatter adds
+    # the interface planes into the neighbours' vectors (here: the other virtual ranks' r on the
+    # same GPU; NVLink peer memory across GPUs) -- one kernel per step plus the zeroing (the
+    # two device barriers of the multi-GPU step, tiny NCCL all-reduces, are not in this number)
+    prev_ptr = ranks[g - 1]["r"].data_ptr() if g > 0 else None
+    next_ptr = ranks[g + 1]["r"].data_ptr() if g < P - 1 else None
+    wins = slabs.peer_windows(sl, pr.shape, pr.p, prev_ptr, next_ptr)
+
+    def step_d():
+        rk["r"].zero_()
+        fe.fe_eval_residual_peer(rk["mesh"].handle, pr.form, pr.mat_kind, rk["ma"], rk["mb"],
+                                 rk["u"], 0, sl.n_elems, None, rk["r"], wins,
+                                 torch.cuda.current_stream())
+
+    variants = [("graph_boundary_first", step_b), ("graph_no_overlap", step_c)]
+    if args.dtype == "f64":
+        variants.append(("graph_peer_fused", step_d))
+    for name, fn in variants:
+        gx = slabs.StepGraph(fn, torch.device("cuda"))
+        ms, hus = timed(gx.replay, args.steps)
+        res[name] = {"device_ms_per_step": ms, "host_us_per_step": hus,
+                     "over_kernel": ms / kern_ms}
     # the whole P-rank world in one graph (P slabs on one GPU: device time ~ P x one slab)
     evs = [evaluator(x) for x in ranks]
     rs = [x["r"] for x in ranks]
@@ -138,7 +182,6 @@ def main():
 
     wg = slabs.StepGraph(world_step, torch.device("cuda"))
     w_ms, w_host = timed(wg.replay, max(10, args.steps // 4))
-    full_ms, _ = timed(lambda: None, 1)
     res["world_graph"] = {"device_ms_per_step": w_ms, "host_us_per_step": w_host,
                           "note": f"all {P} virtual ranks' steps (one GPU) in one graph"}
     print(json.dumps(res))
