@@ -1,16 +1,11 @@
-# Full checkpoint on one GPU: tests, default bench (with e2e + cpu baseline), all configs,
-# reference arm, ncu launch list and one --set full capture of the dominant kernel.
+# Full checkpoint on one GPU: tests, smoke, default bench (all forms as sub-results, e2e, cpu
+# baseline), reference arm, host-overhead tool, launch list, ncu captures.  usage: bash tools/gpu_checkpoint.sh TAG
+T=${1:-ck}
 set -x
-timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -3
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -4
 python __graft_entry__.py smoke 2>&1 | tail -1
-python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo bench_rc=$?
-cat gpurun_out/bench_default.json
-bash tools/gpu_all_configs.sh
-python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.json 2>&1; echo ref_rc=$?
-CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
-$CMD > gpurun_out/plain_ck.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_ck.csv $CMD > gpurun_out/ncu_ck_launch.log 2>&1; echo ncu1=$?
-ncu --set full --clock-control none --import-source on -k regex:k_matrix_sfp -s 1 -c 1 -o gpurun_out/prof_ck_matrix $CMD > gpurun_out/ncu_ck_full.log 2>&1; echo ncu2=$?
-ncu --set full --clock-control none --import-source on -k regex:k_residual_t3 -s 1 -c 1 -o gpurun_out/prof_ck_residual $CMD > gpurun_out/ncu_ck_full_r.log 2>&1; echo ncu3=$?
-ncu --set full --clock-control none --import-source on -k regex:k_matrix_vp -s 1 -c 1 -o gpurun_out/prof_ck_c3_matrix python bench.py --config C3 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_ck_c3.log 2>&1; echo ncu4=$?
-ncu --set full --clock-control none --import-source on -k regex:k_residual_t3c -s 1 -c 1 -o gpurun_out/prof_ck_c5_residual python bench.py --config C5 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_ck_c5.log 2>&1; echo ncu5=$?
+python bench.py > gpurun_out/bench_$T.json 2> gpurun_out/bench_$T.err; echo bench_rc=$?
+python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/reference_$T.json 2>&1; echo ref_rc=$?
+python tools/host_overhead.py > gpurun_out/host_overhead_C4_P8_$T.json 2>/dev/null; echo ho=$?
+python tools/host_overhead.py --config C5 > gpurun_out/host_overhead_C5_P8_$T.json 2>/dev/null
+KEEP="${KEEP:-}" bash tools/gpu_ncu_all.sh $T > gpurun_out/ncu_all_$T.log 2>&1; tail -12 gpurun_out/ncu_all_$T.log
