@@ -92,6 +92,17 @@ __device__ __forceinline__ void seg_gemm_simt(const T* const* As, const T* const
 
 // Jacobian of the trilinear map x(xi) = sum_v x_v psi_v(xi) at xi, vertices
 // xv[v][3] with v = a + 2b + 4c.  Returns det J; Jinv row-major Jinv[m][j].
+// 1/x for x > 0 (det J): rcp.approx + two Newton steps, within ~1 ulp of the IEEE quotient
+// and a few instructions instead of the division's slow-path-guarded sequence
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 __device__ __forceinline__ double hex_geometry(const double* __restrict__ xv, double x0, double x1,
                                                double x2, double Jinv[9]) {
   double J[9];

@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_D
       double* Wel = W + el * NUP * NQ;
       if constexpr (DIFF) {
         // W^{mn} = detw kappa sum_k Jinv[m][k] Jinv[n][k] = w kappa / det * sum_k cof[k][m] cof[k][n]
-        const double s = wq * coef[(el * 2) * NQ + q] / det;
+        const double s = wq * coef[(el * 2) * NQ + q] * rcp_nr(det);
         const double C[3][3] = {{c00, c01, c02}, {c10, c11, c12}, {c20, c21, c22}};
 #pragma unroll
         for (int u = 0; u < 6; ++u) {

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(SFV<P, FORM, FULLD>::THREADS)
       const double c21 = J[0][2] * J[1][0] - J[0][0] * J[1][2];
       const double c22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
       const double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
-      const double id = 1.0 / det;
+      const double id = rcp_nr(det);
       double* o = qd + q * QD;
       // Jinv[m][j] = cof[j][m] / det
       o[0] = c00 * id; o[1] = c10 * id; o[2] = c20 * id;

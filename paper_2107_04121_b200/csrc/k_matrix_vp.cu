@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
         const double c22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
         const double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
         const bool on = el < ne;
-        const double id = on ? 1.0 / det : 0.0;
+        const double id = on ? rcp_nr(det) : 0.0;
         // Ji[m][j] = cof[j][m] / det
         const double Ji[9] = {c00 * id, c10 * id, c20 * id, c01 * id, c11 * id, c21 * id, c02 * id, c12 * id, c22 * id};
         const double dw = on ? c_w1d[P][qx] * c_w1d[P][qy] * c_w1d[P][qz] * det : 0.0;

@@ -80,6 +80,9 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 #ifndef FEB200_RSF_PADP
 #define FEB200_RSF_PADP 4
 #endif
+#ifndef FEB200_RSF_COF
+#define FEB200_RSF_COF 1
+#endif
 template <int P, int FORM, typename T>
 struct RSF {
   static constexpr int N1 = P + 1, Q1 = P + 1, NB = N1 * N1 * N1, NQ = Q1 * Q1 * Q1;
@@ -145,6 +148,9 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
   // the backward pass tests against grad v only where the flux has an f1 part
   // (the convective residual v . (grad u) u has f0 only, Eq. fe2)
   constexpr bool BGRAD = L::BGRAD;
+  // scalar per-qp forms: the flux in cofactor form (FEB200_RSF_COF)
+  constexpr bool SCALARF = FEB200_RSF_COF && D == 1 &&
+                           (FORM == FE_FORM_DIFFUSION || FORM == FE_FORM_MASS || FORM == FE_FORM_MASS_DIFFUSION);
   using A = T;  // contraction arithmetic in the call's precision (geometry and flux stay fp64)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Bs = reinterpret_cast<T*>(smem_raw);  // [2][Q1][N1] in the arithmetic type
@@ -435,7 +441,42 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
       const double c21g = J[0][2] * J[1][0] - J[0][0] * J[1][2];
       const double c22g = J[0][0] * J[1][1] - J[0][1] * J[1][0];
       const double det = J[0][0] * c00g + J[0][1] * c01g + J[0][2] * c02g;
-      const double id = 1.0 / det;
+      if constexpr (SCALARF) {
+        // scalar forms in cofactor form (as k_residual_t3): with t = C g (C the cofactors,
+        // t = det grad u), F = detw J^-1 kappa grad u = (w kappa / det) C^T t and
+        // F0 = w det rho u -- no J^-1, and 1/det by rcp.approx + two Newton steps (~1 ulp)
+        const int q = tx + Q1 * ty + Q2 * qz;
+        const double w = mv.w[q];
+        double F0d = 0.0, Fxd = 0.0, Fyd = 0.0, Fzd = 0.0;
+        if (valid) {
+          if constexpr (VAL) F0d = w * det * mq[qz].a * uq[0];
+          if constexpr (GRAD) {
+            const double kap = FORM == FE_FORM_MASS_DIFFUSION ? mq[qz].b : mq[qz].a;
+            const double g0 = gr[0][0], g1 = gr[0][1], g2 = gr[0][2];
+            const double t0 = c00g * g0 + c01g * g1 + c02g * g2;
+            const double t1 = c10g * g0 + c11g * g1 + c12g * g2;
+            const double t2 = c20g * g0 + c21g * g1 + c22g * g2;
+            const double sc = w * kap * rcp_nr(det);
+            Fxd = sc * (c00g * t0 + c10g * t1 + c20g * t2);
+            Fyd = sc * (c01g * t0 + c11g * t1 + c21g * t2);
+            Fzd = sc * (c02g * t0 + c12g * t1 + c22g * t2);
+          }
+        }
+        const A F0 = (A)F0d, Fx = (A)Fxd, Fy = (A)Fyd, Fz = (A)Fzd;
+#pragma unroll
+        for (int kz = 0; kz < N1; ++kz) {
+          A hv = A(0);
+          if (VAL) hv = B(0, qz, kz) * F0;
+          if (BGRAD) {
+            hv = fma(B(1, qz, kz), Fz, hv);
+            Hx[0][kz] = fma(B(0, qz, kz), Fx, Hx[0][kz]);
+            Hy[0][kz] = fma(B(0, qz, kz), Fy, Hy[0][kz]);
+          }
+          Hv[0][kz] += hv;
+        }
+        continue;
+      }
+      const double id = rcp_nr(det);
       // Jinv[m][j] = cof[j][m] / det
       const double Ji[9] = {c00g * id, c10g * id, c20g * id, c01g * id, c11g * id,
                             c21g * id, c02g * id, c12g * id, c22g * id};

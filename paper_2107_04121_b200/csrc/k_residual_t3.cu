@@ -14,6 +14,7 @@
 //   backward  [z^T, shuffles] -> [y^T] -> [x^T] -> r(kx,ky,kz=j) -> atomic scatter
 // 10 cells per warp (lanes 30, 31 idle).
 #include "fe_const.cuh"
+#include "fe_device.cuh"
 #include "fe_internal.h"
 
 #ifndef FEB200_T3_THREADS
@@ -289,7 +290,7 @@ __global__ void __launch_bounds__(FEB200_T3_THREADS, FEB200_T3_MINB)
             const double tr0 = C00 * g0 + C01 * g1 + C02 * g2;
             const double tr1 = C10 * g0 + C11 * g1 + C12 * g2;
             const double tr2 = C20 * g0 + C21 * g1 + C22 * g2;
-            const double sc = wq * kap / det;
+            const double sc = wq * kap * rcp_nr(det);
             fx = sc * (C00 * tr0 + C10 * tr1 + C20 * tr2);
             fy = sc * (C01 * tr0 + C11 * tr1 + C21 * tr2);
             fz = sc * (C02 * tr0 + C12 * tr1 + C22 * tr2);
