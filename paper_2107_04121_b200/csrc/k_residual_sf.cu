@@ -151,6 +151,9 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
   // scalar per-qp forms: the flux in cofactor form (FEB200_RSF_COF)
   constexpr bool SCALARF = FEB200_RSF_COF && D == 1 &&
                            (FORM == FE_FORM_DIFFUSION || FORM == FE_FORM_MASS || FORM == FE_FORM_MASS_DIFFUSION);
+  // forms whose flux is linear in grad u (f0 of the convective form, f1 of elasticity): the
+  // flux evaluated at det grad u in cofactor form (FEB200_RSF_COF)
+  constexpr bool COFV = FEB200_RSF_COF && (FORM == FE_FORM_ELASTICITY || FORM == FE_FORM_CONVECTIVE);
   using A = T;  // contraction arithmetic in the call's precision (geometry and flux stay fp64)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Bs = reinterpret_cast<T*>(smem_raw);  // [2][Q1][N1] in the arithmetic type
@@ -473,6 +476,49 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
             Hy[0][kz] = fma(B(0, qz, kz), Fy, Hy[0][kz]);
           }
           Hv[0][kz] += hv;
+        }
+        continue;
+      }
+      if constexpr (COFV) {
+        // elasticity / convective: the flux is linear in grad u, so it is evaluated at
+        // t = det grad u (t[a][j] = sum_m C[j][m] g[a][m], C the cofactors) and scaled back:
+        // F1[a][m] = (w / det) sum_j C[j][m] f1(t)[a][j], F0[a] = w f0(t)[a] -- no J^-1
+        const int q = tx + Q1 * ty + Q2 * qz;
+        const double w = mv.w[q];
+        const double C[3][3] = {{c00g, c01g, c02g}, {c10g, c11g, c12g}, {c20g, c21g, c22g}};
+        double tg[D][3];
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int j = 0; j < 3; ++j) tg[a][j] = C[j][0] * gr[a][0] + C[j][1] * gr[a][1] + C[j][2] * gr[a][2];
+        double f0[D], f1[D][3];
+        if (valid) {
+          qp_flux_m<FORM, T>(uq, tg, mq[qz], mat_kind, f0, f1);
+        } else {
+#pragma unroll
+          for (int a = 0; a < D; ++a) f0[a] = f1[a][0] = f1[a][1] = f1[a][2] = 0.0;
+        }
+        const double sw = BGRAD ? w * rcp_nr(det) : 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const A F0 = (A)(w * f0[a]);
+          A Fx = A(0), Fy = A(0), Fz = A(0);
+          if (BGRAD) {
+            Fx = (A)(sw * (C[0][0] * f1[a][0] + C[1][0] * f1[a][1] + C[2][0] * f1[a][2]));
+            Fy = (A)(sw * (C[0][1] * f1[a][0] + C[1][1] * f1[a][1] + C[2][1] * f1[a][2]));
+            Fz = (A)(sw * (C[0][2] * f1[a][0] + C[1][2] * f1[a][1] + C[2][2] * f1[a][2]));
+          }
+#pragma unroll
+          for (int kz = 0; kz < N1; ++kz) {
+            A hv = A(0);
+            if (VAL) hv = B(0, qz, kz) * F0;
+            if (BGRAD) {
+              hv = fma(B(1, qz, kz), Fz, hv);
+              Hx[a][kz] = fma(B(0, qz, kz), Fx, Hx[a][kz]);
+              Hy[a][kz] = fma(B(0, qz, kz), Fy, Hy[a][kz]);
+            }
+            Hv[a][kz] += hv;
+          }
         }
         continue;
       }
