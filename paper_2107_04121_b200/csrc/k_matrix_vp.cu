@@ -38,6 +38,9 @@
 #ifndef FEB200_VP_TASKMAP
 #define FEB200_VP_TASKMAP 1
 #endif
+#ifndef FEB200_VP_GMAP
+#define FEB200_VP_GMAP 1
+#endif
 // per-form role sizes (elasticity / convective): X groups, G pair groups, T1 ring depth.
 // Measured (B200, C3 / C5t): 4 G groups for elasticity (1.96 vs 2.10 ms with 3; 17 warps at
 // 96 registers), 2 for the convective tangent (3.69 vs 3.71 ms).  An X role with register
@@ -389,9 +392,16 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
     constexpr int NGT = 32 * L::NG;
     // phase-2 mapping: warp-uniform pair group h (pairs p with p % GH == h), column (el, qxy)
     const int h2 = gtid / (32 * L::G2W), r2 = gtid - h2 * (32 * L::G2W);
-    const int el2 = r2 / Q2, qxy = r2 - el2 * Q2;
+    // column of this lane.  E = 2: the second cell's columns whose T1 stores would share a bank
+    // with the first cell's in half-warp 0 (per-cell T1 stride S mod 16: banks (S + qxy) mod 16
+    // against 0..8) move to half-warp 1, behind idle lanes -- 2 instead of 3 wavefronts per store
+    constexpr int S16 = (IT::NPMAX * N1 * N1 * QQP) % 16;
+    constexpr int KOK = (S16 >= 9 && FEB200_VP_GMAP) ? 16 - S16 : Q2;  // second-cell columns in half-warp 0
+    int col2 = r2;
+    if (E == 2 && Q2 == 9 && KOK < Q2) col2 = r2 < Q2 + KOK ? r2 : (r2 < 16 ? -1 : r2 - 16 + Q2 + KOK);
+    const int el2 = col2 >= 0 ? col2 / Q2 : 0, qxy = col2 >= 0 ? col2 - el2 * Q2 : 0;
     const int tx = qxy / Q1, ty = qxy - tx * Q1;  // T1's inner index is qx * Q1 + qy
-    const bool act2 = h2 < GH && r2 < E * Q2;
+    const bool act2 = h2 < GH && col2 >= 0 && col2 < E * Q2;
     int64_t gi = 0;  // global item counter (T1 ring position)
     for (int64_t it = 0;; ++it) {
       int64_t lb;
