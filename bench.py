@@ -458,6 +458,8 @@ class Runner:
         self.comm_stream = torch.cuda.Stream(dev) if world > 1 else None
         self.bufs = [None]
         self.bev = torch.cuda.Event()   # boundary -> exchange dependency (preallocated)
+        self.side = (torch.cuda.Stream(dev) if "matrix" in self.modes and "residual" in self.modes
+                     and not self.fused and self.peer is None else None)
 
     def events(self, n):
         """Preallocated kernel events: rec[i][mode] = (start, end) for step i."""
@@ -515,19 +517,30 @@ class Runner:
             if rec:
                 rec["residual"][1].record(st)
         elif "residual" in self.modes:
-            r.zero_()
-            if rec:
-                rec["residual"][0].record(st)
+            # matrix + residual steps: the residual runs on a side stream forked after the
+            # matrix kernel was queued, so its CTAs fill the SMs the matrix kernel's tail frees
+            # (C2: 0.550 -> 0.542 ms); the current stream joins it at the end of the step
+            side = self.side
+            if side is not None:
+                side.wait_stream(st)
+            with self.torch.cuda.stream(side if side is not None else st):
+                rst = self.torch.cuda.current_stream(self.dev)
+                r.zero_()
+                if rec:
+                    rec["residual"][0].record(rst)
 
-            def evaluate(lo, hi):
-                fe.fe_eval_residual(mesh.handle, prob.form, self.dtc, *mat, u, lo, hi, None, r, st)
+                def evaluate(lo, hi):
+                    fe.fe_eval_residual(mesh.handle, prob.form, self.dtc, *mat, u, lo, hi, None, r,
+                                        rst)
 
-            # boundary-first residual; for N > 1 the interface exchange overlaps the interior
-            self.bufs[0] = self.slabs.residual_overlapped(evaluate, r, self.sl, prob.shape, comm,
-                                                          self.bufs[0], events=self.bev,
-                                                          boundary_first=self.bfirst)
-            if rec:
-                rec["residual"][1].record(st)
+                # boundary-first residual; for N > 1 the interface exchange overlaps the interior
+                self.bufs[0] = self.slabs.residual_overlapped(evaluate, r, self.sl, prob.shape, comm,
+                                                              self.bufs[0], events=self.bev,
+                                                              boundary_first=self.bfirst)
+                if rec:
+                    rec["residual"][1].record(rst)
+            if side is not None:
+                st.wait_stream(side)
 
     def close(self):
         if self.peer is not None:
