@@ -178,7 +178,7 @@ fe_status fe_eval_residual(const fe_mesh *mesh, int32_t form, int32_t dtype,
  * kernel with no separate collective.  The caller orders the ranks: every
  * rank's r_global is zeroed before any rank's kernel starts, and no rank reads
  * its vector before every rank's kernel has finished (a device-side barrier).
- * 0..2 windows; FE_ERR_UNSUPPORTED with FEB200_RESIDUAL_IMPL=dense. */
+ * 0..2 windows; FE_ERR_UNSUPPORTED with FE_OPT_RESIDUAL_IMPL = 2 (dense). */
 typedef struct {
   int64_t node_begin, node_end;   /* local node range of the window */
   double *dst;                    /* device (or peer-mapped) vector [..][D] */
@@ -344,7 +344,8 @@ fe_status fe_csr_copy_arrays(const fe_csr *csr, int64_t *row_ptr, int32_t *col_i
  * fp atomics: the caller zeroes `values`; summation order is run-dependent.  With the
  * environment variable FEB200_CSR_IMPL=gather (p <= 2) a row-owner kernel without atomics
  * is used instead: each node row sums its incident cells in ascending cell order, so the
- * result is bitwise reproducible (slower on B200: 1.9 vs 1.1 ms for C2). */
+ * result is bitwise reproducible (slower on B200: 1.9 vs 1.1 ms for C2).  (The variable is read
+ * at library load only; fe_set_option(FE_OPT_CSR_IMPL, 1) selects it at run time.) */
 fe_status fe_assemble_matrix(const fe_csr *csr, const double *K, int64_t elem_begin,
                              int64_t elem_end, double *values, void *stream);
 
