@@ -186,7 +186,8 @@ WORKLOADS = {
 }
 # per-form sub-results carried by the default (C2) line: every BASELINE.json form and mode
 SUB_CONFIGS = ("C3", "C4", "C4f32", "C5", "C5t")
-L2_NOTE = "no flush: every step writes/reads more than the 126 MB L2"
+L2_NOTE = ("no flush when a step moves more than 4 x the 126 MB L2 (C2: K = 1.53 GB); smaller "
+           "steps (C4) flush L2 between timed steps: see l2_flush")
 
 
 def split_cfg(name):
@@ -556,6 +557,23 @@ def _barrier(torch, dist, world, local_rank, dev):
     torch.cuda.synchronize(dev)
 
 
+L2_BYTES = 126 * 2 ** 20
+
+
+def step_bytes(run):
+    """Algorithmic HBM bytes of one step of a Runner (all its modes): when they do not exceed a
+    few L2 capacities, the timed loop flushes L2 between steps (timing rules)."""
+    prob = run.prob
+    esize = 8 if run.dtype == "f64" else 4
+    tot = 0.0
+    for m in run.modes:
+        if m == "csr":
+            continue
+        tot += alg_bytes(prob.form, m, prob.p, prob.nb, prob.nq, prob.ncomp, prob.mat_kind,
+                         esize) * run.El
+    return tot
+
+
 def timed_run(run, steps, warmup, world, local_rank, window_s=1.2, graph=False):
     """W warm-up steps; then, under the clock sampler, untimed repeats (>= 0.25 s), EXACTLY K
     timed steps bracketed by barrier + synchronize with CUDA events on the launching stream
@@ -598,6 +616,12 @@ def timed_run(run, steps, warmup, world, local_rank, window_s=1.2, graph=False):
     n_pre = int(np.ceil(250.0 / est)) if window_s > 0 else 0
     n_post = max(0, int(np.ceil((window_s * 1e3 - 250.0 - steps * est) / est))) if window_s > 0 else 0
     ev_step = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    # L2 flush between timed steps when a step's working set is small (C4: ~260 MB f64, ~150 MB
+    # f32): a write of 2 x L2 outside the per-step events; the step time is then the sum of the
+    # per-step event times
+    flush = step_bytes(run) < 4 * L2_BYTES
+    fbuf = torch.empty(2 * L2_BYTES // 8, dtype=torch.float64, device=dev) if flush else None
+    ev_beg = [torch.cuda.Event(enable_timing=True) for _ in range(steps)] if flush else None
     rec = run.events(steps)
     fe = run.fe
     with ClockSampler(local_rank) as clk:
@@ -608,6 +632,9 @@ def timed_run(run, steps, warmup, world, local_rank, window_s=1.2, graph=False):
         h0 = time.perf_counter()
         ev_step[0].record(st)
         for i in range(steps):
+            if flush:
+                fbuf.zero_()
+                ev_beg[i].record(st)
             run.step(rec[i])
             ev_step[i + 1].record(st)
         h1 = time.perf_counter()
@@ -627,8 +654,12 @@ def timed_run(run, steps, warmup, world, local_rank, window_s=1.2, graph=False):
         for i in range(steps):
             run.step(rec[i])
         _barrier(torch, dist, world, local_rank, dev)
-    total = ev_step[0].elapsed_time(ev_step[steps])
-    per_step = [ev_step[i].elapsed_time(ev_step[i + 1]) for i in range(steps)]
+    if flush:
+        per_step = [ev_beg[i].elapsed_time(ev_step[i + 1]) for i in range(steps)]
+        total = float(sum(per_step))
+    else:
+        total = ev_step[0].elapsed_time(ev_step[steps])
+        per_step = [ev_step[i].elapsed_time(ev_step[i + 1]) for i in range(steps)]
     per_kern = {m: [rec[i][m][0].elapsed_time(rec[i][m][1]) for i in range(steps)]
                 for m in run.kmodes}
     if world > 1:
@@ -640,7 +671,7 @@ def timed_run(run, steps, warmup, world, local_rank, window_s=1.2, graph=False):
         off = 1 + steps
         for m in run.kmodes:
             per_kern[m], off = t[off:off + steps], off + steps
-    return {"total_ms": total, "per_step": per_step, "per_kern": per_kern,
+    return {"total_ms": total, "per_step": per_step, "per_kern": per_kern, "l2_flush": flush,
             "launches": launches, "clocks": clk.summary(), "host_us_per_step": host_us,
             "graph": graph, "graph_error": graph_error,
             "untimed_repeats": {"before": n_pre, "after": n_post}}
@@ -753,6 +784,7 @@ def measure_sub(cfg_name, args, world, rank, local_rank, dev):
         modes = summarize(run, res, dtype)
         st = step_stats(res["per_step"])
         out = {"config": config_dict(cfg, run.prob, run.modes, world, args.exchange, dtype),
+               "l2_flush": res["l2_flush"],
                "ms_per_step": res["total_ms"] / args.steps, "step_ms": st,
                "cells_per_s": run.prob.n_elems / (res["total_ms"] / args.steps * 1e-3),
                "modes": {m: {"kernel_ms": v["kernel_ms"], "cells_per_s": v["cells_per_s"],
@@ -991,6 +1023,7 @@ def main():
         "untimed_repeats": res["untimed_repeats"],
         "graph": bool(res["graph"]),
         "graph_error": res["graph_error"],
+        "l2_flush": res["l2_flush"],
         "host_us_per_step": res["host_us_per_step"],
         "configs": subs,
         "options": fe.get_options(),
