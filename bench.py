@@ -144,7 +144,7 @@ def alg_bytes(form: int, mode: str, p: int, nb: int, nq: int, D: int, mat_kind: 
         mat = nq * esize
     geo = 24 + 32                               # one vertex + 8 conn ids per cell
     if mode == "matrix":
-        b = geo + mat + (D * nb) ** 2 * 8
+        b = geo + mat + (D * nb) ** 2 * esize       # K in the call's type (fp32: FE_F32 path)
         if form == fi.CONVECTIVE:
             b += 4 * nb + D * p ** 3 * 8        # gather of the state
         return b
@@ -405,8 +405,11 @@ class Runner:
         self.kmodes = ("matrix+residual",) if self.fused else tuple(self.modes)
         if cfg == "C5t" and world > 1:
             raise SystemExit("C5t (corner tangent) is single-GPU")
-        if dtype == "f32" and "matrix" in self.modes:
-            raise SystemExit("fp32 is built for residual mode only")
+        if dtype == "f32" and "matrix" in self.modes and not (
+                prob.form in (fi.DIFFUSION, fi.MASS, fi.MASS_DIFFUSION) and prob.p <= 2):
+            raise SystemExit("fp32 matrices are built for the scalar forms at p <= 2")
+        if dtype == "f32" and "csr" in self.modes:
+            raise SystemExit("CSR assembly is built for fp64 element matrices")
         self.tdt = torch.float64 if dtype == "f64" else torch.float32
         self.dtc = fe.F64 if dtype == "f64" else fe.F32
         D, nb = prob.ncomp, prob.nb
@@ -441,7 +444,7 @@ class Runner:
         self.mat_a, self.mat_b = dslice(prob.mat_a), dslice(prob.mat_b)
         self.u_loc = np.ascontiguousarray(prob.u[sl.node_begin:sl.node_end])
         self.u = torch.from_numpy(self.u_loc).to(dev, self.tdt)
-        self.K = (torch.empty((El, D * nb, D * nb), dtype=torch.float64, device=dev)
+        self.K = (torch.empty((El, D * nb, D * nb), dtype=self.tdt, device=dev)
                   if "matrix" in self.modes else None)
         self.peer = None
         if world > 1 and exchange == "peer" and "residual" in self.modes and not self.fused:
@@ -493,7 +496,7 @@ class Runner:
         if "matrix" in self.modes:
             if rec:
                 rec["matrix"][0].record(st)
-            fe.fe_eval_element_matrices(mesh.handle, prob.form, fe.F64, *mat,
+            fe.fe_eval_element_matrices(mesh.handle, prob.form, self.dtc, *mat,
                                         u if prob.form == fi.CONVECTIVE else None, 0, El, K, st)
             if rec:
                 rec["matrix"][1].record(st)
@@ -725,7 +728,7 @@ def roofline_for(prob, mode, kern_ms, El, dtype, csr_nnz=0.0, cfg=""):
     else:
         fl = sf_residual_flops(prob.form, prob.p) * El
     by = alg_bytes(prob.form, mode, prob.p, nb, nq, D, prob.mat_kind, esize, csr_nnz) * El
-    if dtype == "f32":
+    if dtype == "f32" and mode != "matrix":   # fp32 matrices contract in fp64
         pk_f, src_f, fbound = 74.4, "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz", "alu"
     elif impl.startswith("sum-factorised") or mode == "csr":
         pk_f, src_f = fp64_peak_tflops("dfma_tflops_sustained")

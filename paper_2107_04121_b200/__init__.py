@@ -606,13 +606,15 @@ class Mesh:
 
     def element_matrices(self, form, mat_kind=MAT_PER_QP, mat_a=None, mat_b=None, state_u=None,
                          elem_begin=0, elem_end=None, out=None, stream=None):
+        """K [E'][ndof][ndof]; fp32 coefficient arrays select the FE_F32 path (fp32 K)."""
         elem_end = self.n_elems if elem_end is None else elem_end
         ndof = NCOMP[form] * self.nb
+        f32 = mat_a is not None and mat_a.dtype == torch.float32
         if out is None:
-            out = torch.empty((elem_end - elem_begin, ndof, ndof), dtype=torch.float64,
-                              device=self.device)
-        fe_eval_element_matrices(self.handle, form, F64, mat_kind, mat_a, mat_b, state_u,
-                                 elem_begin, elem_end, out, stream)
+            out = torch.empty((elem_end - elem_begin, ndof, ndof),
+                              dtype=torch.float32 if f32 else torch.float64, device=self.device)
+        fe_eval_element_matrices(self.handle, form, F32 if f32 else F64, mat_kind, mat_a, mat_b,
+                                 state_u, elem_begin, elem_end, out, stream)
         return out
 
     def residual(self, form, u, mat_kind=MAT_PER_QP, mat_a=None, mat_b=None, elem_begin=0,

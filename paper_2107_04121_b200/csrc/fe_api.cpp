@@ -281,8 +281,21 @@ fe_status fe_eval_element_matrices(const fe_mesh* mesh, int32_t form, int32_t dt
   FE_NVTX_RANGE("fe_eval_element_matrices");
   fe_status s = check_common(mesh, form, elem_begin, elem_end);
   if (s != FE_OK) return s;
-  if (dtype != FE_F64) return fail(FE_ERR_UNSUPPORTED, "element matrices are built for FE_F64 only");
+  if (dtype != FE_F64 && dtype != FE_F32) return fail(FE_ERR_INVALID_ARG, "unknown dtype");
   if ((s = check_material(form, mat)) != FE_OK) return s;
+  if (dtype == FE_F32) {
+    if (elem_end > elem_begin && !K) return fail(FE_ERR_INVALID_ARG, "K is NULL");
+    if (feb200::option(FE_OPT_MATRIX_IMPL) != feb200::MATRIX_DEFAULT)
+      return fail(FE_ERR_UNSUPPORTED, "FE_F32 element matrices: the pipelined kernels only");
+    feb200::MatArgs ma{mat->kind, mat->a, mat->b};
+    cudaError_t e = feb200::launch_matrix_sf_f32(mesh, form, ma, elem_begin, elem_end, (float*)K,
+                                                 (cudaStream_t)stream);
+    if (e == cudaErrorNotSupported)
+      return fail(FE_ERR_UNSUPPORTED, "FE_F32 element matrices are built for the scalar forms "
+                                      "(diffusion, mass, mass + diffusion) at order 1 and 2");
+    if (e != cudaSuccess) return cuda_fail(e, "fe_eval_element_matrices");
+    return ok();
+  }
   if (form == FE_FORM_CONVECTIVE && !state_u)
     return fail(FE_ERR_INVALID_ARG, "convective tangent needs state_u");
   if (form == FE_FORM_DIVERGENCE)

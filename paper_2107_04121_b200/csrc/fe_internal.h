@@ -97,6 +97,8 @@ cudaError_t launch_matrix(const fe_mesh* m, int form, MatArgs mat, const double*
                           int64_t e0, int64_t e1, double* K, cudaStream_t st);
 cudaError_t launch_matrix_sf(const fe_mesh* m, int form, MatArgs mat, int64_t e0, int64_t e1,
                              double* K, cudaStream_t st);
+cudaError_t launch_matrix_sf_f32(const fe_mesh* m, int form, MatArgs mat, int64_t e0, int64_t e1,
+                                 float* K, cudaStream_t st);
 cudaError_t launch_matrix_residual_sf(const fe_mesh* m, int form, MatArgs mat, const double* u,
                                       int64_t e0, int64_t e1, double* K, double* r_elem,
                                       double* r_global, cudaStream_t st);

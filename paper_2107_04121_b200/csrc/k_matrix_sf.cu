@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_D
 //                  (b, c1) -> K staging slot [it % 2] -> one TMA bulk store
 // The geometry + stage-z thread uses compile-time pair indices, so every 1D
 // table operand is a constant-bank operand.
-template <int P, int NUPMAX, bool RES = false>
+template <int P, int NUPMAX, bool RES = false, int KB = 8>
 struct SFP {
   static constexpr int N1 = P + 1, Q1 = P + 1, NB = N1 * N1 * N1, NQ = Q1 * Q1 * Q1, Q2 = Q1 * Q1;
   static constexpr int YP = N1 * N1, YPS = N1 * (N1 + 1) / 2;
@@ -441,7 +441,7 @@ struct SFP {
   static constexpr int T1PAD = FEB200_SFP_T1PAD;
   static constexpr int T1CELL = NUPMAX * N1 * N1 * QQP + T1PAD;
   static constexpr size_t T1SLOT = size_t(E) * T1CELL * 8;
-  static constexpr size_t KSLOT = size_t(E) * NB * NB * 8;
+  static constexpr size_t KSLOT = size_t(E) * NB * NB * KB;  // K staging in the output type
   static constexpr size_t OFF_K = 0;                                  // [2][KSLOT]
   static constexpr size_t OFF_T1 = OFF_K + 2 * KSLOT;                 // [2][T1SLOT]
   static constexpr size_t OFF_L = OFF_T1 + 2 * T1SLOT;                // [2][LSLOT]
@@ -496,14 +496,17 @@ __device__ __forceinline__ void sfp_named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <int P, int FORM, bool RES>
-__global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM != FE_FORM_DIFFUSION ? 1 : 0), RES>::THREADS, 1)
-    k_matrix_sfp(MeshView mv, const double* __restrict__ ma, const double* __restrict__ mb,
-                 int64_t e0, int64_t e1, double* __restrict__ K, const double* __restrict__ u,
+// KT: element type of the material arrays and of K (double, or float for the FE_F32 matrix
+// path: the contraction runs in fp64 on the fp32 inputs and K is rounded to fp32 when staged)
+template <int P, int FORM, bool RES, typename KT = double>
+__global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM != FE_FORM_DIFFUSION ? 1 : 0), RES, (int)sizeof(KT)>::THREADS, 1)
+    k_matrix_sfp(MeshView mv, const KT* __restrict__ ma, const KT* __restrict__ mb,
+                 int64_t e0, int64_t e1, KT* __restrict__ K, const double* __restrict__ u,
                  double* __restrict__ r_elem, double* __restrict__ r_global) {
+  static_assert(!RES || sizeof(KT) == 8, "the fused matrix + residual kernel is fp64");
   constexpr bool DIFF = FORM != FE_FORM_MASS, MASS = FORM != FE_FORM_DIFFUSION;
   constexpr int NUP = (DIFF ? 6 : 0) + (MASS ? 1 : 0);
-  using L = SFP<P, NUP, RES>;
+  using L = SFP<P, NUP, RES, (int)sizeof(KT)>;
   constexpr int N1 = L::N1, Q1 = L::Q1, NB = L::NB, NQ = L::NQ, Q2 = L::Q2, E = L::E;
   constexpr int QQP = L::QQP;
   constexpr int NOP = (DIFF ? 9 : 0) + (MASS ? 1 : 0);
@@ -657,9 +660,9 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
       if (lane == 0) conn_issue(it + 2);  // ring slot (it+2)%3 was last read in iteration it-2
       SFP_T(1, sfp_wait(&emptyL[sl], (uint32_t)(((it >> 1) & 1) ^ 1)));
       double* slot = reinterpret_cast<double*>(smp + L::OFF_L + sl * L::LSLOT);
-      const double* ga = ma + (e0 + lb) * NQ;
-      const double* gb = NCOEF == 2 ? mb + (e0 + lb) * NQ : nullptr;
-      const uint32_t kbytes = (uint32_t)ne * NQ * 8u;
+      const KT* ga = ma + (e0 + lb) * NQ;
+      const KT* gb = NCOEF == 2 ? mb + (e0 + lb) * NQ : nullptr;
+      const uint32_t kbytes = (uint32_t)ne * NQ * (uint32_t)sizeof(KT);
       const bool tma_ok = (((reinterpret_cast<uintptr_t>(ga) | (NCOEF == 2 ? reinterpret_cast<uintptr_t>(gb) : 0) |
                              kbytes) & 15u) == 0);
       if (tma_ok) {
@@ -672,9 +675,9 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
 #pragma unroll
         for (int h = 0; h < KPL; ++h) {
           const int i = lane + 32 * h;
-          if (i < ne * NQ) {
-            slot[E * 24 + i] = ga[i];
-            if (NCOEF == 2) slot[E * 24 + E * NQ + i] = gb[i];
+          if (i < ne * NQ) {  // the coefficient blocks keep the input type (as the TMA copy)
+            reinterpret_cast<KT*>(slot + E * 24)[i] = ga[i];
+            if (NCOEF == 2) reinterpret_cast<KT*>(slot + E * 24 + E * NQ)[i] = gb[i];
           }
         }
       }
@@ -737,8 +740,8 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
 #pragma unroll
         for (int qz = 0; qz < Q1; ++qz) {
           const int q = tx + Q1 * ty + Q2 * qz;
-          ca[qz] = on ? slot[E * 24 + el * NQ + q] : 0.0;
-          cb[qz] = (on && NCOEF == 2) ? slot[E * 24 + E * NQ + el * NQ + q] : 0.0;
+          ca[qz] = on ? (double)reinterpret_cast<const KT*>(slot + E * 24)[el * NQ + q] : 0.0;
+          cb[qz] = (on && NCOEF == 2) ? (double)reinterpret_cast<const KT*>(slot + E * 24 + E * NQ)[el * NQ + q] : 0.0;
         }
       }
       sfp_arrive(&emptyL[sl]);
@@ -944,18 +947,18 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
       } else {
         sfp_arrive(&emptyT[sl]);
       }
-      double* Kst = reinterpret_cast<double*>(smp + L::OFF_K + sl * L::KSLOT);
+      KT* Kst = reinterpret_cast<KT*>(smp + L::OFF_K + sl * L::KSLOT);
       const int su = (int)(it % L::SU);
       if constexpr (RES) SFP_T(7, sfp_wait(&fullU[su], (uint32_t)((it / L::SU) & 1)));
       if (xact && yx_el < ne) {
-        double* Ke = Kst + yx_el * NB * NB;
+        KT* Ke = Kst + yx_el * NB * NB;
         const int ib = N1 * (iy + N1 * iz), jb = N1 * (jy + N1 * jz);
 #pragma unroll
         for (int a = 0; a < N1; ++a)
 #pragma unroll
           for (int bb = 0; bb < N1; ++bb) {
-            Ke[(ib + a) * NB + jb + bb] = acc[a][bb];
-            if (mirror) Ke[(jb + bb) * NB + ib + a] = acc[a][bb];
+            Ke[(ib + a) * NB + jb + bb] = (KT)acc[a][bb];
+            if (mirror) Ke[(jb + bb) * NB + ib + a] = (KT)acc[a][bb];
           }
         if constexpr (RES) {
           // r_e = K_e u_e (Alg. 1 for a linear form, pin P8).  Row (ix, iy, iz) of K_e is
@@ -997,8 +1000,8 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
         }
         sfp_arrive(&doneR[su]);
       }
-      const uint32_t bytes = (uint32_t)ne * NB * NB * 8;
-      double* gdst = K + lb * NB * NB;
+      const uint32_t bytes = (uint32_t)ne * NB * NB * (uint32_t)sizeof(KT);
+      KT* gdst = K + lb * NB * NB;
       if (FEB200_SFP_NOSTORE) {
       } else if (((reinterpret_cast<uintptr_t>(gdst) | bytes) & 15u) == 0) {
         if (xtid == 0) {
@@ -1024,12 +1027,12 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
 #undef Bt
 }
 
-template <int P, int FORM, bool RES = false>
-static cudaError_t launch_sfp_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int64_t e1, double* K,
+template <int P, int FORM, bool RES = false, typename KT = double>
+static cudaError_t launch_sfp_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int64_t e1, KT* K,
                                 cudaStream_t st, const double* u = nullptr, double* r_elem = nullptr,
                                 double* r_global = nullptr) {
-  using L = SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM != FE_FORM_DIFFUSION ? 1 : 0), RES>;
-  auto kern = k_matrix_sfp<P, FORM, RES>;
+  using L = SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM != FE_FORM_DIFFUSION ? 1 : 0), RES, (int)sizeof(KT)>;
+  auto kern = k_matrix_sfp<P, FORM, RES, KT>;
   const LaunchFacts lf = launch_facts((const void*)kern, L::THREADS, L::BYTES);
   if (lf.err != cudaSuccess) return lf.err;
   const int nsm = lf.nsm;
@@ -1037,7 +1040,7 @@ static cudaError_t launch_sfp_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int6
   int grid = (int)(nbatch < nsm ? nbatch : nsm);
   grid = grid_cap(grid);
   if (grid <= 0) return cudaSuccess;
-  kern<<<grid, L::THREADS, L::BYTES, st>>>(view_of(mh), (const double*)mat.a, (const double*)mat.b,
+  kern<<<grid, L::THREADS, L::BYTES, st>>>(view_of(mh), (const KT*)mat.a, (const KT*)mat.b,
                                            e0, e1, K, u, r_elem, r_global);
   count_launch();
   return cudaGetLastError();
@@ -1082,6 +1085,25 @@ static cudaError_t launch_sf_t(const fe_mesh* mh, MatArgs mat, int64_t e0, int64
                                           e0, e1, K);
   count_launch();
   return cudaGetLastError();
+}
+
+// fp32 element matrices of the scalar forms (FE_F32: fp32 coefficients and K, contraction in
+// fp64) through the pipelined kernel, p = 1, 2; cudaErrorNotSupported otherwise.
+cudaError_t launch_matrix_sf_f32(const fe_mesh* mh, int form, MatArgs mat, int64_t e0, int64_t e1,
+                                 float* K, cudaStream_t st) {
+  if (mh->q1d != mh->order + 1 || !FEB200_SFP) return cudaErrorNotSupported;
+#define SFP32_CASE(P)                                                                                          \
+  if (mh->order == P) switch (form) {                                                                          \
+      case FE_FORM_DIFFUSION: return launch_sfp_t<P, FE_FORM_DIFFUSION, false, float>(mh, mat, e0, e1, K, st); \
+      case FE_FORM_MASS: return launch_sfp_t<P, FE_FORM_MASS, false, float>(mh, mat, e0, e1, K, st);           \
+      case FE_FORM_MASS_DIFFUSION:                                                                             \
+        return launch_sfp_t<P, FE_FORM_MASS_DIFFUSION, false, float>(mh, mat, e0, e1, K, st);                  \
+      default: return cudaErrorNotSupported;                                                                   \
+    }
+  SFP32_CASE(1)
+  SFP32_CASE(2)
+#undef SFP32_CASE
+  return cudaErrorNotSupported;
 }
 
 // Returns cudaErrorNotSupported when the combination has no sum-factorised kernel.

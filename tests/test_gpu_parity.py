@@ -833,3 +833,35 @@ def test_stream_ordered_destroy():
             m.close()          # queued behind the residual on st
             st.synchronize()
             assert rel(rg.cpu().numpy().ravel(), ref) <= TOL64
+
+
+# ---- FE_F32 element matrices (scalar forms, p = 1, 2; reading 15) -------------------------
+
+@pytest.mark.parametrize("form,p", [(fi.DIFFUSION, 1), (fi.DIFFUSION, 2), (fi.MASS, 2),
+                                    (fi.MASS_DIFFUSION, 1), (fi.MASS_DIFFUSION, 2)])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_matrix_fp32(form, p, shape, fe_opts):
+    """fp32 coefficients -> fp32 K within 1e-5 of the fp64 oracle (also with many batches per
+    CTA and an element sub-range); other forms / orders are FE_ERR_UNSUPPORTED."""
+    pr = fi.make_problem(form, p, shape, 19000 + 10 * form + p)
+    Kref = oracle.problem_matrix(pr)
+    mesh = gpu_mesh(pr)
+    for ctas in (0, 2):
+        fe_opts(max_ctas=ctas)
+        K = mesh.element_matrices(form, pr.mat_kind, dev(pr.mat_a, torch.float32),
+                                  dev(pr.mat_b, torch.float32))
+        assert K.dtype == torch.float32
+        assert rel(K.cpu().numpy(), Kref) <= TOL32
+    Ks = mesh.element_matrices(form, pr.mat_kind, dev(pr.mat_a, torch.float32),
+                               dev(pr.mat_b, torch.float32), elem_begin=3, elem_end=pr.n_elems - 2)
+    assert rel(Ks.cpu().numpy(), Kref[3:pr.n_elems - 2]) <= TOL32
+
+
+def test_matrix_fp32_unsupported():
+    m = fe()
+    pr = fi.make_problem(fi.ELASTICITY, 2, (2, 2, 2), 19100)
+    mesh = gpu_mesh(pr)
+    with pytest.raises(m.FEError) as ei:
+        mesh.element_matrices(fi.ELASTICITY, pr.mat_kind, dev(pr.mat_a, torch.float32),
+                              dev(pr.mat_b, torch.float32))
+    assert ei.value.status == m.FE_ERR_UNSUPPORTED
