@@ -148,8 +148,8 @@ fe_status fe_mesh_info(const fe_mesh *mesh, fe_info *info);
  *   state_u: CONVECTIVE only, the linearisation state [n_nodes][3]; the
  *   matrix is the Newton tangent of Eq. fe4 (both terms).  NULL otherwise.
  * FE_F64: orders scalar forms 1-4, vector forms
- * (VECTOR_MASS, ELASTICITY, CONVECTIVE, WEIGHTED_DOT) 1-2; other
- * combinations FE_ERR_UNSUPPORTED.  DIVERGENCE has no matrix
+ * (VECTOR_MASS, ELASTICITY, CONVECTIVE, WEIGHTED_DOT) 1-3 (order 3 through the
+ * dense tensor-core kernel); other combinations FE_ERR_UNSUPPORTED.  DIVERGENCE has no matrix
  * mode (FE_ERR_UNSUPPORTED).  FE_F32 (DIFFUSION, MASS, MASS_DIFFUSION at order 1, 2; default
  * matrix implementation): fp32 coefficient arrays and fp32 K, the contraction in fp64 and K
  * rounded once (within 1e-5 of the fp64 oracle, reading 15). */

@@ -31,14 +31,15 @@ __device__ __forceinline__ int voigt_index(int a, int j) {
 template <int FORM>
 struct FormInfo {
   static constexpr int D = (FORM == FE_FORM_VECTOR_MASS || FORM == FE_FORM_ELASTICITY ||
-                            FORM == FE_FORM_CONVECTIVE) ? 3 : 1;
+                            FORM == FE_FORM_CONVECTIVE || FORM == FE_FORM_WEIGHTED_DOT) ? 3 : 1;
 };
 
 template <int P, int FORM>
 struct MatLayout {
   static constexpr int Q = P + 1, NB = (P + 1) * (P + 1) * (P + 1), NQ = Q * Q * Q;
   static constexpr int D = FormInfo<FORM>::D, NDOF = D * NB;
-  static constexpr bool NEED_G = FORM != FE_FORM_MASS && FORM != FE_FORM_VECTOR_MASS;
+  static constexpr bool NEED_G = FORM != FE_FORM_MASS && FORM != FE_FORM_VECTOR_MASS &&
+                                 FORM != FE_FORM_WEIGHTED_DOT;
   // offsets in doubles
   static constexpr int XV = 0;
   static constexpr int JINV = XV + 24;
@@ -46,7 +47,8 @@ struct MatLayout {
   static constexpr int WT = DETW + NQ;                      // row weights, 4 NQ
   static constexpr int G = WT + 4 * NQ;                     // [NQ][3][NB]
   static constexpr int X1 = G + (NEED_G ? 3 * NQ * NB : 0); // form scratch 1
-  static constexpr int X1_SIZE = FORM == FE_FORM_ELASTICITY ? 81 * NQ
+  // elasticity: the C_ajbl of one block (a, b) at a time, [NQ][9]
+  static constexpr int X1_SIZE = FORM == FE_FORM_ELASTICITY ? 9 * NQ
                                  : FORM == FE_FORM_CONVECTIVE ? (3 * NB + 12 * NQ + NQ * NB) : 0;
   static constexpr int X2 = X1 + X1_SIZE;                   // form scratch 2
   static constexpr int X2_SIZE = FORM == FE_FORM_ELASTICITY ? 3 * NQ * NB
@@ -137,30 +139,41 @@ __global__ void __launch_bounds__(256) k_matrix(MeshView m, int mat_kind, const 
                     [&](int r, int c, double v) { Ke[(int64_t)r * NDOF + c] = v; });
       }
       __syncthreads();
-    } else if constexpr (FORM == FE_FORM_ELASTICITY) {
-      double* Cten = X1;  // [NQ][81], C[a][j][b][l] = detw D[I(a,j)][I(b,l)]
-      double* H = X2;     // [NQ][3][NB]
-      for (int idx = tid; idx < NQ * 81; idx += nthr) {
-        const int q = idx / 81, r = idx - q * 81;
-        const int a = r / 27, j = (r / 9) % 3, b = (r / 3) % 3, l = r % 3;
-        const int I = voigt_index(a, j), Kv = voigt_index(b, l);
-        double dik;
-        if (mat_kind == FE_MAT_FULL_D) {
-          dik = ma[(e * NQ + q) * 36 + 6 * I + Kv];
-        } else {
-          const double lam = mat_kind == FE_MAT_PER_ELEM ? ma[e] : ma[e * NQ + q];
-          const double mu = mat_kind == FE_MAT_PER_ELEM ? mb[e] : mb[e * NQ + q];
-          dik = (I < 3 && Kv < 3 ? lam : 0.0) + (I == Kv ? (I < 3 ? 2.0 * mu : mu) : 0.0);
-        }
-        Cten[idx] = detw[q] * dik;
-      }
-      __syncthreads();
+    } else if constexpr (FORM == FE_FORM_WEIGHTED_DOT) {
+      // K_ab = sum_q detw M_ab(q) phi phi^T ('ij,i,j'): nine weighted mass blocks
       for (int a = 0; a < 3; ++a)
         for (int b = 0; b < 3; ++b) {
+          for (int q = tid; q < NQ; q += nthr) wt[q] = detw[q] * ma[(e * NQ + q) * 9 + 3 * a + b];
+          __syncthreads();
+          Seg s{m.phi, m.phi, wt, NB, NB, NQ};
+          seg_gemm<2>(&s, 1, NB, NB, warp, nwarps, lane, [&](int r, int c, double v) {
+            Ke[(int64_t)(a * NB + r) * NDOF + b * NB + c] = v;
+          });
+          __syncthreads();
+        }
+    } else if constexpr (FORM == FE_FORM_ELASTICITY) {
+      double* Cab = X1;  // [NQ][9]: C[a][j][b][l] = detw D[I(a,j)][I(b,l)] of the current (a, b)
+      double* H = X2;    // [NQ][3][NB]
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) {
+          for (int idx = tid; idx < NQ * 9; idx += nthr) {
+            const int q = idx / 9, j = (idx / 3) % 3, l = idx % 3;
+            const int I = voigt_index(a, j), Kv = voigt_index(b, l);
+            double dik;
+            if (mat_kind == FE_MAT_FULL_D) {
+              dik = ma[(e * NQ + q) * 36 + 6 * I + Kv];
+            } else {
+              const double lam = mat_kind == FE_MAT_PER_ELEM ? ma[e] : ma[e * NQ + q];
+              const double mu = mat_kind == FE_MAT_PER_ELEM ? mb[e] : mb[e * NQ + q];
+              dik = (I < 3 && Kv < 3 ? lam : 0.0) + (I == Kv ? (I < 3 ? 2.0 * mu : mu) : 0.0);
+            }
+            Cab[idx] = detw[q] * dik;
+          }
+          __syncthreads();
           for (int idx = tid; idx < NQ * 3 * NB; idx += nthr) {
             const int q = idx / (3 * NB), r = idx - q * 3 * NB;
             const int j = r / NB, k = r - j * NB;
-            const double* C = Cten + q * 81 + a * 27 + j * 9 + b * 3;
+            const double* C = Cab + q * 9 + j * 3;
             const double* Gq = G + 3 * q * NB + k;
             H[idx] = C[0] * Gq[0] + C[1] * Gq[NB] + C[2] * Gq[2 * NB];
           }
@@ -250,6 +263,7 @@ static cudaError_t dispatch_form(const fe_mesh* mh, int form, MatArgs mat, const
     case FE_FORM_MASS_DIFFUSION: return launch_matrix_t<P, FE_FORM_MASS_DIFFUSION>(mh, mat, state_u, e0, e1, K, st);
     case FE_FORM_ELASTICITY: return launch_matrix_t<P, FE_FORM_ELASTICITY>(mh, mat, state_u, e0, e1, K, st);
     case FE_FORM_CONVECTIVE: return launch_matrix_t<P, FE_FORM_CONVECTIVE>(mh, mat, state_u, e0, e1, K, st);
+    case FE_FORM_WEIGHTED_DOT: return launch_matrix_t<P, FE_FORM_WEIGHTED_DOT>(mh, mat, state_u, e0, e1, K, st);
   }
   return cudaErrorNotSupported;
 }

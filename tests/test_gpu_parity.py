@@ -45,7 +45,8 @@ def dev(a, dtype=torch.float64):
 
 # ragged element counts: several CTA batches plus a partial tail
 SHAPES = [(5, 3, 4), (7, 2, 3)]
-MATRIX_CASES = [(f, p) for f in (0, 1, 2, 3, 4, 5) for p in (1, 2)] + [(0, 3), (1, 3), (3, 3)]
+MATRIX_CASES = [(f, p) for f in (0, 1, 2, 3, 4, 5) for p in (1, 2)] + [(0, 3), (1, 3), (3, 3)] + \
+               [(2, 3), (4, 3), (5, 3)]   # vector forms at p = 3: the dense DMMA kernel
 RESIDUAL_CASES = [(f, p) for f in (0, 1, 2, 3, 4, 5) for p in (1, 2, 3)] + \
                  [(0, 4), (1, 4), (3, 4), (2, 4), (4, 4), (5, 4)]
 
@@ -420,7 +421,7 @@ def test_unaligned_outputs(form, p):
 
 # ---- N3: the remaining Tab. 2 forms --------------------------------------------
 
-@pytest.mark.parametrize("p", [1, 2])
+@pytest.mark.parametrize("p", [1, 2, 3])
 @pytest.mark.parametrize("shape", SHAPES)
 def test_weighted_dot_matrix(p, shape):
     """'ij,i,j' matrix mode: 9 blocks of weight detw M_ab, M non-symmetric."""
