@@ -124,12 +124,20 @@ __global__ void __launch_bounds__(FEB200_T3_THREADS, FEB200_T3_MINB)
     group_cell(g, le, ok);
     if (ok) {
       const int s1 = (int)(g % 3), s2 = (int)(g & 1);
+      // all staged indices first (the copies' asm memory clobbers would otherwise serialise
+      // each index load behind the previous copy), then the copies
+      int dd[9], vv[8];
 #pragma unroll
-      for (int k = 0; k < 9; ++k) t3_cp8(&s2u[(s2 * 9 + k) * TH + tid], u + s1d[(s1 * 9 + k) * TH + tid]);
+      for (int k = 0; k < 9; ++k) dd[k] = s1d[(s1 * 9 + k) * TH + tid];
+#pragma unroll
+      for (int h = 0; h < 8; ++h) vv[h] = s1c[(s1 * 8 + (8 * j + h) / 3) * TH + tid];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) t3_cp8(&s2u[(s2 * 9 + k) * TH + tid], u + dd[k]);
 #pragma unroll
       for (int h = 0; h < 8; ++h) {  // coordinate p = 8 j + h of the cell: vertex p / 3, component p % 3
         const int pidx = 8 * j + h, v = pidx / 3, i = pidx - 3 * v;
-        t3_cp8(&s2x[(s2 * 8 + h) * TH + tid], mv.coords + 3 * (int64_t)s1c[(s1 * 8 + v) * TH + tid] + i);
+        t3_cp8(&s2x[(s2 * 8 + h) * TH + tid], mv.coords + 3 * (int64_t)vv[h] + i);
+        (void)v;
       }
     }
     t3_commit();
@@ -474,14 +482,20 @@ __global__ void __launch_bounds__(FEB200_T3_THREADS, FEB200_T3C_MINB)
     group_cell(g, le, ok);
     if (ok) {
       const int s1 = (int)(g % 3), s2 = (int)(g & 1);
+      // staged indices first, then the copies (see the scalar kernel)
+      int dd[9];
 #pragma unroll
-      for (int k = 0; k < 9; ++k)
-        t3_cp8(&s2u[(s2 * 9 + k) * TH + tid], u + 3 * (int64_t)s1d[(s1 * 9 + k) * TH + tid] + a);
+      for (int k = 0; k < 9; ++k) dd[k] = s1d[(s1 * 9 + k) * TH + tid];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) t3_cp8(&s2u[(s2 * 9 + k) * TH + tid], u + 3 * (int64_t)dd[k] + a);
       if (a == 0) {
+        int vv[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) vv[h] = s1c[(s1 * 8 + (8 * j + h) / 3) * TH + tid];
 #pragma unroll
         for (int h = 0; h < 8; ++h) {
-          const int pidx = 8 * j + h, v = pidx / 3, i = pidx - 3 * v;
-          t3_cp8(&s2x[(s2 * 8 + h) * TH + tid], mv.coords + 3 * (int64_t)s1c[(s1 * 8 + v) * TH + tid] + i);
+          const int pidx = 8 * j + h, i = pidx % 3;
+          t3_cp8(&s2x[(s2 * 8 + h) * TH + tid], mv.coords + 3 * (int64_t)vv[h] + i);
         }
       }
     }
