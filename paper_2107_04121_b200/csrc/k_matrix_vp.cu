@@ -64,6 +64,21 @@
 #ifndef FEB200_VP_S_CV
 #define FEB200_VP_S_CV 4
 #endif
+// G split (warps of a dedicated phase-1 sub-role, 0 = one G role doing both phases): with a
+// split, G1 warps compute the pair weights of batch it+1 into the second half of a double-
+// buffered Wsm while the G2 warps run stage z of batch it.  Measured (B200): general D
+// elasticity (C3d) 2.24 ms with 2 G1 warps vs 2.58 without (its phase 1 -- 36 D loads and the
+// 9 blocks J^-T C J^-1 per qp -- stalled stage z); convective tangent (C5t) 3.69 vs 3.75 with 1
+// (2: 17 warps at 96 registers, 3.87); isotropic elasticity (C3) 1.96 with 2 or 3 vs 1.877 without
+#ifndef FEB200_VP_G1W_EL
+#define FEB200_VP_G1W_EL 0
+#endif
+#ifndef FEB200_VP_G1W_ELD
+#define FEB200_VP_G1W_ELD 2
+#endif
+#ifndef FEB200_VP_G1W_CV
+#define FEB200_VP_G1W_CV 1
+#endif
 
 namespace feb200 {
 
@@ -173,7 +188,7 @@ struct VItems<FE_FORM_CONVECTIVE> {
   static constexpr int NWP = 12;
 };
 
-template <int P, int FORM>
+template <int P, int FORM, bool FD>
 struct VPL {
   using IT = VItems<FORM>;
   static constexpr int N1 = P + 1, Q1 = P + 1, NB = N1 * N1 * N1, NQ = Q1 * Q1 * Q1, Q2 = Q1 * Q1;
@@ -185,7 +200,12 @@ struct VPL {
   static constexpr int NWP = IT::NWP;                    // pair weights per qp (all items)
   static constexpr int G1T = E * NQ;                     // phase-1 tasks (per qp)
   static constexpr int G2W = (E * Q2 + 31) / 32;         // warps per pair group (warp-uniform group)
-  static constexpr int NG = ((G1T + 31) / 32 > GH * G2W) ? (G1T + 31) / 32 : GH * G2W;
+  // phase-1 warps (0: no split); FD: the general-D (FE_MAT_FULL_D) elasticity instantiation
+  static constexpr int NG1 = EL ? (FD ? FEB200_VP_G1W_ELD : FEB200_VP_G1W_EL) : FEB200_VP_G1W_CV;
+  static constexpr bool SPLIT = NG1 > 0;
+  static constexpr int NG = SPLIT ? NG1 + GH * G2W
+                                  : (((G1T + 31) / 32 > GH * G2W) ? (G1T + 31) / 32 : GH * G2W);
+  static constexpr int NG2 = SPLIT ? NG - NG1 : NG;      // warps that run stage z
   static constexpr int NFULL = N1 * N1 * N1 * N1;        // (z pair, y pair) tasks, ordered
   static constexpr int NSYM = N1 * N1 * (N1 * (N1 - 1) / 2) + N1 * (N1 * (N1 + 1) / 2);
   static constexpr int XG = EL ? FEB200_VP_XG_EL : FEB200_VP_XG_CV;  // X groups (alternate items)
@@ -203,21 +223,22 @@ struct VPL {
   static constexpr size_t OFF_K = 0;
   static constexpr size_t OFF_T1 = (OFF_K + KBYTES + 127) / 128 * 128;
   static constexpr size_t OFF_QD = OFF_T1 + S * T1SLOT;
-  static constexpr size_t OFF_L = OFF_QD + size_t(E) * IT::NWP * NQ * 8;
+  static constexpr size_t WSZ = size_t(E) * IT::NWP * NQ;  // doubles per Wsm buffer
+  static constexpr size_t OFF_L = OFF_QD + (SPLIT ? 2 : 1) * WSZ * 8;
   static constexpr size_t OFF_IDX = OFF_L + 2 * size_t(LSLOT) * 8;       // [2][E][8 + NB] int32
   static constexpr size_t OFF_BAR = (OFF_IDX + 2 * size_t(E) * (8 + NB) * 4 + 15) / 16 * 16;
-  static constexpr size_t BYTES = OFF_BAR + (6 + 2 * S) * 8;
+  static constexpr size_t BYTES = OFF_BAR + (10 + 2 * S) * 8;
 };
 
-template <int P, int FORM>
-__global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
+template <int P, int FORM, bool FD>
+__global__ void __launch_bounds__(VPL<P, FORM, FD>::THREADS, 1)
     k_matrix_vp(MeshView mv, int mat_kind, const double* __restrict__ ma, const double* __restrict__ mb,
                 const double* __restrict__ state_u, int64_t e0, int64_t e1, double* __restrict__ K,
                 const int* __restrict__ skip) {
   // device-side dispatch (general D): the launch is a no-op when the symmetry check found a
   // non-symmetric D, and the general 9-block kernel k_matrix_sfv runs instead
   if (skip != nullptr && *skip != 0) return;
-  using L = VPL<P, FORM>;
+  using L = VPL<P, FORM, FD>;
   using IT = typename L::IT;
   constexpr int N1 = L::N1, Q1 = L::Q1, NB = L::NB, NQ = L::NQ, Q2 = L::Q2, E = L::E, QQP = L::QQP;
   constexpr int NDOF = L::NDOF, NITEM = IT::NITEM, S = L::S, GH = L::GH;
@@ -233,6 +254,8 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
   // batch (no CTA-wide barrier couples the two X groups or the store to the X warps)
   uint64_t* kfull = bars + 4 + 2 * L::S;
   uint64_t* kfree = bars + 5 + 2 * L::S;
+  uint64_t* fullW = bars + 6 + 2 * L::S;   // [2] (G split only) G1 -> G2: Wsm buffer written
+  uint64_t* emptyW = bars + 8 + 2 * L::S;  // [2] G2 -> G1: Wsm buffer read
   double* Kst = reinterpret_cast<double*>(smv + L::OFF_K);
   double* Wsm = reinterpret_cast<double*>(smv + L::OFF_QD);  // [E][NWP][NQ] pair weights
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -245,10 +268,14 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
   if (tid == 0) {
     vp_bar_init(&fullL[0], 32);
     vp_bar_init(&fullL[1], 32);
-    vp_bar_init(&emptyL[0], 32 * L::NG);
-    vp_bar_init(&emptyL[1], 32 * L::NG);
+    vp_bar_init(&emptyL[0], 32 * (L::SPLIT ? L::NG1 : L::NG));
+    vp_bar_init(&emptyL[1], 32 * (L::SPLIT ? L::NG1 : L::NG));
+    for (int b = 0; b < 2; ++b) {
+      vp_bar_init(&fullW[b], 32 * (L::SPLIT ? L::NG1 : 1));
+      vp_bar_init(&emptyW[b], 32 * L::NG2);
+    }
     for (int s = 0; s < S; ++s) {
-      vp_bar_init(&fullT[s], 32 * L::NG);
+      vp_bar_init(&fullT[s], 32 * L::NG2);
       vp_bar_init(&emptyT[s], 32 * L::NXW);
     }
     vp_bar_init(kfull, 32 * L::NX);
@@ -273,7 +300,7 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
       batch_of(j, lb, ne);
       if (ne <= 0) return;
       int32_t* ib = idxb + (j & 1) * E * (8 + NB);
-      if (FEB200_VP_L2PF && !L::CONV && mat_kind == FE_MAT_FULL_D && lane == 0) {  // D block of batch j -> L2
+      if (FEB200_VP_L2PF && !L::CONV && (FD || mat_kind == FE_MAT_FULL_D) && lane == 0) {  // D block of batch j -> L2
         const double* gD = ma + (e0 + lb) * NQ * 36;
         const uint32_t bD = (uint32_t)ne * NQ * 36u * 8u;
         if (((reinterpret_cast<uintptr_t>(gD) | bD) & 15u) == 0) l2_prefetch_bulk(gD, bD);
@@ -390,8 +417,12 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
     // ======================= G: per-qp data, pair weights, stage z =======================
     const int gtid = tid - 32;
     constexpr int NGT = 32 * L::NG;
+    // G split: warps 1..NG1 run phase 1 only (G1), the rest phase 2 only (G2)
+    const bool g1 = !L::SPLIT || warp <= L::NG1, g2 = !L::SPLIT || warp > L::NG1;
+    constexpr int NGT1 = L::SPLIT ? 32 * L::NG1 : NGT;
+    const int gtid2 = L::SPLIT ? gtid - 32 * L::NG1 : gtid;
     // phase-2 mapping: warp-uniform pair group h (pairs p with p % GH == h), column (el, qxy)
-    const int h2 = gtid / (32 * L::G2W), r2 = gtid - h2 * (32 * L::G2W);
+    const int h2 = gtid2 / (32 * L::G2W), r2 = gtid2 - h2 * (32 * L::G2W);
     // column of this lane.  E = 2: the second cell's columns whose T1 stores would share a bank
     // with the first cell's in half-warp 0 (per-cell T1 stride S mod 16: banks (S + qxy) mod 16
     // against 0..8) move to half-warp 1, behind idle lanes -- 2 instead of 3 wavefronts per store
@@ -409,11 +440,19 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
       batch_of(it, lb, ne);
       if (ne <= 0) break;
       const int sl = (int)(it & 1);
+      const int wb = L::SPLIT ? (int)(it & 1) : 0;
+      double* const Wb_ = Wsm + wb * L::WSZ;
+      if (g1) {
       VP_T(2, vp_wait(&fullL[sl], (uint32_t)((it >> 1) & 1)));
       const double* slot = reinterpret_cast<const double*>(smv + L::OFF_L) + sl * L::LSLOT;
-      // ---- phase 1: pair weights of the batch (Wsm is free once every G thread left phase 2 of it-1)
-      VP_T(0, vp_named_bar(1, NGT));
-      for (int t = gtid; t < L::G1T; t += NGT) {
+      // ---- phase 1: pair weights of the batch (Wsm is free once every G thread left phase 2 of
+      // it-1, or -- G split -- once the G2 warps released this buffer after batch it-2)
+      if constexpr (L::SPLIT) {
+        VP_T(0, vp_wait(&emptyW[wb], (uint32_t)(((it >> 1) & 1) ^ 1)));
+      } else {
+        VP_T(0, vp_named_bar(1, NGT));
+      }
+      for (int t = gtid; t < L::G1T; t += NGT1) {
         const int el = t / NQ, q = t - el * NQ;
         const int qx = q % Q1, qy = (q / Q1) % Q1, qz = q / Q2;
         const double t0 = c_x1d[P][qx], t1 = c_x1d[P][qy], t2 = c_x1d[P][qz];
@@ -445,8 +484,10 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
         const double Ji[9] = {c00 * id, c10 * id, c20 * id, c01 * id, c11 * id, c21 * id, c02 * id, c12 * id, c22 * id};
         const double dw = on ? c_w1d[P][qx] * c_w1d[P][qy] * c_w1d[P][qz] * det : 0.0;
         // all pair weights W^{ab}_{mn}(q) of the batch, item-major: Wsm[el][PB(i) + p][q]
-        double* Wq = Wsm + el * L::NWP * NQ + q;
-        if (!L::CONV && mat_kind == FE_MAT_FULL_D) {
+        double* Wq = Wb_ + el * L::NWP * NQ + q;
+        // the non-split elasticity instantiation keeps the (there unused) general-D branch: without
+        // it ptxas allocates the isotropic path differently, 1.93 vs 1.88 ms on C3
+        if (!L::CONV && (FD || mat_kind == FE_MAT_FULL_D)) {
           // general Voigt D, symmetric (checked by k_dsym_check before this launch, DESIGN.md
           // reading 23; the upper triangle is read):
           // W^{ab}_{mn} = dw sum_{j,l} Ji[m][j] D[v(a,j)][v(b,l)] Ji[n][l]
@@ -579,14 +620,21 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
         }
       }
       vp_arrive(&emptyL[sl]);
-      VP_T(0, vp_named_bar(1, NGT));
+      if constexpr (L::SPLIT) vp_arrive(&fullW[wb]);
+      }  // g1
+      if constexpr (L::SPLIT) {
+        if (!g2) continue;
+        VP_T(2, vp_wait(&fullW[wb], (uint32_t)((it >> 1) & 1)));
+      } else {
+        VP_T(0, vp_named_bar(1, NGT));
+      }
       // ---- phase 2: stage z of every item, one compiled body per item kind (symmetric /
       // full pair set) inside a runtime item loop, so the code stays in the instruction cache
       auto g_item = [&](auto SYMc, int i) {
         constexpr bool SYMI = decltype(SYMc)::value;
         constexpr int NP = SYMI ? (L::CONV ? 1 : 6) : (L::CONV ? 6 : 9);
         const int s = (int)(gi % S);
-        const double* Wi = Wsm + (act2 ? el2 : 0) * L::NWP * NQ + IT::pbase(i) * NQ + tx + Q1 * ty;
+        const double* Wi = Wb_ + (act2 ? el2 : 0) * L::NWP * NQ + IT::pbase(i) * NQ + tx + Q1 * ty;
         VP_T(3, vp_wait(&emptyT[s], (uint32_t)(((gi / S) & 1) ^ 1)));
         double* T1 = reinterpret_cast<double*>(smv + L::OFF_T1 + s * L::T1SLOT);
         if (act2) {
@@ -619,6 +667,7 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
         if (IT::sym(i)) g_item(std::true_type{}, i);
         else g_item(std::false_type{}, i);
       }
+      if constexpr (L::SPLIT) vp_arrive(&emptyW[wb]);
     }
   } else {
     // ======================= X: stages y and x per item, K staging, TMA store =======================
@@ -836,12 +885,12 @@ __global__ void __launch_bounds__(VPL<P, FORM>::THREADS, 1)
 #undef Bt
 }
 
-template <int P, int FORM>
+template <int P, int FORM, bool FD>
 static cudaError_t launch_vp_t(const fe_mesh* mh, MatArgs mat, const double* state_u, int64_t e0,
                                int64_t e1, double* K, cudaStream_t st, const int* skip = nullptr) {
-  using L = VPL<P, FORM>;
+  using L = VPL<P, FORM, FD>;
   if (L::BYTES > 227 * 1024) return cudaErrorNotSupported;
-  auto kern = k_matrix_vp<P, FORM>;
+  auto kern = k_matrix_vp<P, FORM, FD>;
   const LaunchFacts lf = launch_facts((const void*)kern, L::THREADS, L::BYTES);
   if (lf.err != cudaSuccess) return lf.err;
   const int nsm = lf.nsm;
@@ -899,14 +948,15 @@ cudaError_t launch_matrix_vp(const fe_mesh* mh, int form, MatArgs mat, const dou
       count_launch();
       e = cudaGetLastError();
     }
-    if (e == cudaSuccess) e = launch_vp_t<2, FE_FORM_ELASTICITY>(mh, mat, state_u, e0, e1, K, st, flag);
+    if (e == cudaSuccess) e = launch_vp_t<2, FE_FORM_ELASTICITY, true>(mh, mat, state_u, e0, e1, K, st, flag);
     if (e == cudaSuccess) e = launch_matrix_sfv_gated(mh, form, mat, state_u, e0, e1, K, st, flag);
     cudaError_t ef = cudaFreeAsync(flag, st);
     return e != cudaSuccess ? e : ef;
   }
   if (form == FE_FORM_ELASTICITY)
-    return launch_vp_t<2, FE_FORM_ELASTICITY>(mh, mat, state_u, e0, e1, K, st);
-  if (form == FE_FORM_CONVECTIVE) return launch_vp_t<2, FE_FORM_CONVECTIVE>(mh, mat, state_u, e0, e1, K, st);
+    return launch_vp_t<2, FE_FORM_ELASTICITY, false>(mh, mat, state_u, e0, e1, K, st);
+  if (form == FE_FORM_CONVECTIVE)
+    return launch_vp_t<2, FE_FORM_CONVECTIVE, false>(mh, mat, state_u, e0, e1, K, st);
   return cudaErrorNotSupported;
 }
 
