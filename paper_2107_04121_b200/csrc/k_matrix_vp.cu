@@ -55,6 +55,9 @@
 #ifndef FEB200_VP_GH_EL
 #define FEB200_VP_GH_EL 4
 #endif
+#ifndef FEB200_VP_GH_ELD
+#define FEB200_VP_GH_ELD 3
+#endif
 #ifndef FEB200_VP_GH_CV
 #define FEB200_VP_GH_CV 2
 #endif
@@ -68,10 +71,12 @@
 // split, G1 warps compute the pair weights of batch it+1 into the second half of a double-
 // buffered Wsm while the G2 warps run stage z of batch it.  Measured (B200): general D
 // elasticity (C3d) 2.24 ms with 2 G1 warps vs 2.58 without (its phase 1 -- 36 D loads and the
-// 9 blocks J^-T C J^-1 per qp -- stalled stage z); convective tangent (C5t) 3.69 vs 3.75 with 1
-// (2: 17 warps at 96 registers, 3.87); isotropic elasticity (C3) 1.96 with 2 or 3 vs 1.877 without
+// 9 blocks J^-T C J^-1 per qp -- stalled stage z; 2.20 with 3 stage-z groups instead of 4);
+// convective tangent (C5t) 3.69 vs 3.75 with 1
+// (2: 17 warps at 96 registers, 3.87); isotropic elasticity (C3) 1.873 with 1, 1.877 without,
+// 1.96 with 2 or 3
 #ifndef FEB200_VP_G1W_EL
-#define FEB200_VP_G1W_EL 0
+#define FEB200_VP_G1W_EL 1
 #endif
 #ifndef FEB200_VP_G1W_ELD
 #define FEB200_VP_G1W_ELD 2
@@ -195,7 +200,7 @@ struct VPL {
   static constexpr int NDOF = 3 * NB;
   static constexpr bool EL = FORM == FE_FORM_ELASTICITY;
   static constexpr int E = FEB200_VP_E;                  // cells per batch
-  static constexpr int GH = EL ? FEB200_VP_GH_EL : FEB200_VP_GH_CV;  // G pair groups
+  static constexpr int GH = EL ? (FD ? FEB200_VP_GH_ELD : FEB200_VP_GH_EL) : FEB200_VP_GH_CV;  // G pair groups
   static constexpr int QQP = (Q2 + 1) / 2 * 2;
   static constexpr int NWP = IT::NWP;                    // pair weights per qp (all items)
   static constexpr int G1T = E * NQ;                     // phase-1 tasks (per qp)
@@ -485,8 +490,8 @@ __global__ void __launch_bounds__(VPL<P, FORM, FD>::THREADS, 1)
         const double dw = on ? c_w1d[P][qx] * c_w1d[P][qy] * c_w1d[P][qz] * det : 0.0;
         // all pair weights W^{ab}_{mn}(q) of the batch, item-major: Wsm[el][PB(i) + p][q]
         double* Wq = Wb_ + el * L::NWP * NQ + q;
-        // the non-split elasticity instantiation keeps the (there unused) general-D branch: without
-        // it ptxas allocates the isotropic path differently, 1.93 vs 1.88 ms on C3
+        // the isotropic elasticity instantiation keeps the (there unused) general-D branch:
+        // without it ptxas allocated the isotropic path differently (1.93 vs 1.88 ms on C3)
         if (!L::CONV && (FD || mat_kind == FE_MAT_FULL_D)) {
           // general Voigt D, symmetric (checked by k_dsym_check before this launch, DESIGN.md
           // reading 23; the upper triangle is read):
