@@ -137,14 +137,23 @@ def pack(t):
 
 
 def main():
-    iters = int(sys.argv[1]) if len(sys.argv) > 1 else 30000
+    """usage: gen_vp_tasks.py [ITERS] [--full ITERS:SEED] [--sym ITERS:SEED]
+    (the committed header: --full 900000:21 --sym 400000:2107, about 1.5 h / 0.5 h of CPU)"""
+    args = sys.argv[1:]
+    iters = int(args.pop(0)) if args and not args[0].startswith("--") else 30000
+    params = {"full": (iters, 2107), "sym": (iters, 2107)}
+    while args:
+        k, v = args.pop(0).lstrip("-"), args.pop(0)
+        params[k] = tuple(int(x) for x in v.split(":"))
     lines = ["// Generated by tools/gen_vp_tasks.py -- X-thread task maps of k_matrix_vp.cu (p = 2, E = 2).",
              "// entry = el | iz << 4 | jz << 8 | iy << 12 | jy << 16, -1 = idle lane.", "#pragma once", ""]
     for name, tasks, sym in (("full", full_tasks(), False), ("sym", sym_tasks(), True)):
-        s, c, slots = anneal(tasks, sym, iters, 2107)
+        it, seed = params[name]
+        s, c, slots = anneal(tasks, sym, it, seed)
         print(f"{name}: shared wavefronts per item {s} -> {c}")
         vals = ", ".join(str(pack(t)) for t in slots)
-        lines.append(f"// {name}: modelled shared wavefronts (T1 loads + K stores) per item {s} (natural order) -> {c}")
+        lines.append(f"// {name}: modelled shared wavefronts (T1 loads + K stores) per item {s} (natural order) -> {c}"
+                     f" ({it} iterations, seed {seed})")
         lines.append(f"__device__ const int vp_tasks_{name}[{LANES}] = {{{vals}}};")
     out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                        "paper_2107_04121_b200", "csrc", "vp_tasks.h")
