@@ -18,6 +18,7 @@ cap "k_residual_sf" C4_residual_f64 --config C4
 cap "k_residual_sf" C4_residual_f32 --config C4 --dtype f32
 cap "k_residual_t3c" C5_residual --config C5
 cap "k_matrix_vp" C5t_matrix --config C5t
+cap "k_matrix_vp" C3d_matrix --config C3d
 cap "k_assemble_matrix" C2csr_assembly --config C2csr
 cap "k_assemble_matrix" C3csr_assembly --config C3csr
 # summaries (and the raw csv pages) come back; the reports stay in /tmp except the ones named
