@@ -239,10 +239,10 @@ template <int P, int FORM, bool FD>
 __global__ void __launch_bounds__(VPL<P, FORM, FD>::THREADS, 1)
     k_matrix_vp(MeshView mv, int mat_kind, const double* __restrict__ ma, const double* __restrict__ mb,
                 const double* __restrict__ state_u, int64_t e0, int64_t e1, double* __restrict__ K,
-                const int* __restrict__ skip) {
-  // device-side dispatch (general D): the launch is a no-op when the symmetry check found a
-  // non-symmetric D, and the general 9-block kernel k_matrix_sfv runs instead
-  if (skip != nullptr && *skip != 0) return;
+                int* __restrict__ nonsym) {
+  // general D (FD): the kernel reads the upper triangle of each 6x6 block and sets *nonsym when
+  // a block is not symmetric; the general 9-block kernel k_matrix_sfv, launched next and gated
+  // on the flag, then recomputes K (reading 23)
   using L = VPL<P, FORM, FD>;
   using IT = typename L::IT;
   constexpr int N1 = L::N1, Q1 = L::Q1, NB = L::NB, NQ = L::NQ, Q2 = L::Q2, E = L::E, QQP = L::QQP;
@@ -493,8 +493,7 @@ __global__ void __launch_bounds__(VPL<P, FORM, FD>::THREADS, 1)
         // the isotropic elasticity instantiation keeps the (there unused) general-D branch:
         // without it ptxas allocated the isotropic path differently (1.93 vs 1.88 ms on C3)
         if (!L::CONV && (FD || mat_kind == FE_MAT_FULL_D)) {
-          // general Voigt D, symmetric (checked by k_dsym_check before this launch, DESIGN.md
-          // reading 23; the upper triangle is read):
+          // general Voigt D, the upper triangle read (symmetry checked below, reading 23):
           // W^{ab}_{mn} = dw sum_{j,l} Ji[m][j] D[v(a,j)][v(b,l)] Ji[n][l]
           double Dm[36];
           const double* Dg = ma + ((e0 + lb + el) * NQ + q) * 36;
@@ -504,6 +503,19 @@ __global__ void __launch_bounds__(VPL<P, FORM, FD>::THREADS, 1)
           } else {
 #pragma unroll
             for (int i = 0; i < 36; ++i) Dm[i] = on ? __ldg(Dg + i) : 0.0;
+          }
+          if constexpr (FD) {
+            // |D_IK - D_KI| > 8 eps max(|D_IK|, |D_KI|) (or NaN): not symmetric (a D formed as
+            // A A^T in floating point may differ from its transpose in the last bits)
+            bool ns = false;
+#pragma unroll
+            for (int I = 0; I < 6; ++I)
+#pragma unroll
+              for (int Kk = I + 1; Kk < 6; ++Kk) {
+                const double a = Dm[6 * I + Kk], b = Dm[6 * Kk + I];
+                ns |= !(fabs(a - b) <= 8.0 * 2.220446049250313e-16 * fmax(fabs(a), fabs(b)));
+              }
+            if (ns && nonsym != nullptr) *nonsym = 1;
           }
           auto Dv = [&](int a, int j, int b, int l) {
             const int I = vp_voigt(a, j), Kk = vp_voigt(b, l);
@@ -892,7 +904,7 @@ __global__ void __launch_bounds__(VPL<P, FORM, FD>::THREADS, 1)
 
 template <int P, int FORM, bool FD>
 static cudaError_t launch_vp_t(const fe_mesh* mh, MatArgs mat, const double* state_u, int64_t e0,
-                               int64_t e1, double* K, cudaStream_t st, const int* skip = nullptr) {
+                               int64_t e1, double* K, cudaStream_t st, int* nonsym = nullptr) {
   using L = VPL<P, FORM, FD>;
   if (L::BYTES > 227 * 1024) return cudaErrorNotSupported;
   auto kern = k_matrix_vp<P, FORM, FD>;
@@ -904,37 +916,19 @@ static cudaError_t launch_vp_t(const fe_mesh* mh, MatArgs mat, const double* sta
   grid = grid_cap(grid);
   if (grid <= 0) return cudaSuccess;
   kern<<<grid, L::THREADS, L::BYTES, st>>>(view_of(mh), mat.kind, (const double*)mat.a,
-                                           (const double*)mat.b, state_u, e0, e1, K, skip);
+                                           (const double*)mat.b, state_u, e0, e1, K, nonsym);
   count_launch();
   return cudaGetLastError();
-}
-
-// Symmetry check of a general Voigt D[n][6][6] (FE_MAT_FULL_D): *flag = 1 when some block has
-// |D_IK - D_KI| > 8 eps max(|D_IK|, |D_KI|) (a D built as A A^T in floating point may differ
-// from its transpose in the last bits; reading the upper triangle of such a D changes K by a
-// few ulps).  Grid-stride over the upper off-diagonal entries, coalesced over the 36-blocks.
-__global__ void __launch_bounds__(256) k_dsym_check(const double* __restrict__ D, int64_t n_blk,
-                                                    int* __restrict__ flag) {
-  const int64_t total = n_blk * 36;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(i % 36), I = r / 6, Kk = r - 6 * I;
-    if (Kk <= I) continue;
-    const double a = __ldg(D + i), b = __ldg(D + (i - r) + 6 * Kk + I);
-    if (!(fabs(a - b) <= 8.0 * 2.220446049250313e-16 * fmax(fabs(a), fabs(b)))) {
-      *flag = 1;
-      return;
-    }
-  }
 }
 
 // Returns cudaErrorNotSupported when the combination has no pipelined vector kernel
 // (vector mass, weighted dot, p != 2: the single-stage k_matrix_sfv handles those; with
 // FEB200_MATRIX_IMPL=sf1 the general non-symmetric FULL_D path of k_matrix_sfv is used).
 // General D (FE_MAT_FULL_D) is read as given by every path: the pipelined kernel, which
-// derives K_ba = K_ab^T, runs only on a symmetric D; k_dsym_check decides on the device and
-// both kernels are launched, the one not chosen returning at once (no host synchronisation,
-// so the call stays asynchronous and graph-capturable).
+// derives K_ba = K_ab^T, is exact only for a symmetric D; it flags a non-symmetric block on
+// the device, and the general kernel launched after it recomputes K when the flag is set and
+// returns at once otherwise (no host synchronisation, so the call stays asynchronous and
+// graph-capturable; the symmetric case costs one empty launch, not a second read of D).
 cudaError_t launch_matrix_vp(const fe_mesh* mh, int form, MatArgs mat, const double* state_u,
                              int64_t e0, int64_t e1, double* K, cudaStream_t st) {
   if (mh->q1d != mh->order + 1 || mh->order != 2) return cudaErrorNotSupported;
@@ -945,14 +939,6 @@ cudaError_t launch_matrix_vp(const fe_mesh* mh, int form, MatArgs mat, const dou
     cudaError_t e = cudaMallocAsync((void**)&flag, sizeof(int), st);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(flag, 0, sizeof(int), st);
-    const int64_t nblk = (e1 - e0) * (int64_t)mh->nq;
-    if (e == cudaSuccess) {
-      const int64_t want = (nblk * 36 + 255) / 256;
-      const int grid = (int)(want < 148 * 8 ? want : 148 * 8);
-      k_dsym_check<<<grid, 256, 0, st>>>((const double*)mat.a + e0 * mh->nq * 36, nblk, flag);
-      count_launch();
-      e = cudaGetLastError();
-    }
     if (e == cudaSuccess) e = launch_vp_t<2, FE_FORM_ELASTICITY, true>(mh, mat, state_u, e0, e1, K, st, flag);
     if (e == cudaSuccess) e = launch_matrix_sfv_gated(mh, form, mat, state_u, e0, e1, K, st, flag);
     cudaError_t ef = cudaFreeAsync(flag, st);
