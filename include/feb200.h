@@ -91,11 +91,12 @@ typedef enum { FE_F64 = 0, FE_F32 = 1 } fe_dtype;
  *                             engineering shears; 'cqIK' operand),
  *                             read as given by every mode (DESIGN.md reading
  *                             23).  A non-symmetric D gives a non-symmetric K.
- *                             At p = 2 matrix mode checks the symmetry on the
- *                             device (one extra read of D) and runs the
- *                             pipelined kernel (which derives K_ba = K_ab^T)
- *                             only for a D symmetric to 8 ulps; otherwise the
- *                             general 9-block kernel
+ *                             At p = 2 matrix mode runs the pipelined kernel
+ *                             (which derives K_ba = K_ab^T) and checks the
+ *                             symmetry of D (to 8 ulps) on the device while
+ *                             it loads D; for a non-symmetric D the general
+ *                             9-block kernel then recomputes K (same stream,
+ *                             no host synchronisation)
  *   CONVECTIVE      unused (kind ignored)                                  */
 typedef enum { FE_MAT_PER_QP = 0, FE_MAT_PER_ELEM = 1, FE_MAT_FULL_D = 2 } fe_material_kind;
 
