@@ -43,6 +43,9 @@
 #ifndef FEB200_SFP_GH
 #define FEB200_SFP_GH 1
 #endif
+#ifndef FEB200_SFP_YB
+#define FEB200_SFP_YB 3  // y pairs per X thread at p = 2 (1 or 3)
+#endif
 #ifndef FEB200_SF_MINB
 #define FEB200_SF_MINB 1
 #endif
@@ -425,8 +428,13 @@ template <int P, int NUPMAX, bool RES = false, int KB = 8>
 struct SFP {
   static constexpr int N1 = P + 1, Q1 = P + 1, NB = N1 * N1 * N1, NQ = Q1 * Q1 * Q1, Q2 = Q1 * Q1;
   static constexpr int YP = N1 * N1, YPS = N1 * (N1 + 1) / 2;
-  static constexpr int TOFF = YP * (N1 * (N1 - 1) / 2);
-  static constexpr int TPE = TOFF + N1 * YPS;             // X tasks per cell (one y pair each)
+  // YB: y pairs per X thread.  YB = 1: one task per (z pair, y pair), every T1 value a thread
+  // loads feeds one FMA.  YB = 3 (p = 2): one task per (z pair iz < jz, iy) over jy = 0..2,
+  // and two per diagonal z pair (y pairs (0,0),(0,1),(0,2) and (1,1),(1,2),(2,2)) -- each
+  // loaded T1 value feeds three FMAs, a third of the shared-memory load wavefronts per cell
+  static constexpr int YB = P == 2 ? FEB200_SFP_YB : 1;
+  static constexpr int TOFF = YB == 1 ? YP * (N1 * (N1 - 1) / 2) : N1 * (N1 * (N1 - 1) / 2);
+  static constexpr int TPE = YB == 1 ? TOFF + N1 * YPS : TOFF + 2 * N1;  // X tasks per cell
   static constexpr int E = P == 1 ? 16 : FEB200_SFP_E2;   // cells per batch (even: TMA size)
   static constexpr int GH = FEB200_SFP_GH;                // G thread groups per column
   static constexpr int NGW = (E * Q2 + 31) / 32;          // G warps per group
@@ -809,6 +817,172 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
       }
       sfp_arrive(&fullT[sl]);
     }
+  } else if constexpr (L::YB == 3) {
+    // ============ X, register-blocked: one z pair, three y pairs per thread ============
+    static_assert(P == 2, "YB = 3 is the p = 2 task map");
+    const int xtid = tid - 32 * (1 + L::NG);
+    constexpr int NXT = 32 * L::NX;
+    const bool xact = xtid < E * L::TPE;
+    int yx_el, iz, jz, yi[3], yj[3];
+    if (xtid < E * L::TOFF) {  // z pair iz < jz (zp 0, 1, 2 = (0,1), (0,2), (1,2)), row iy
+      yx_el = xtid / L::TOFF;
+      const int r = xtid - yx_el * L::TOFF, zp = r / N1, iy = r - zp * N1;
+      iz = zp >> 1;
+      jz = zp == 0 ? 1 : 2;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) { yi[k] = iy; yj[k] = k; }
+    } else {  // diagonal z pair iz == jz, upper-triangle y pairs in two groups of three
+      const int t = xtid - E * L::TOFF;
+      yx_el = t / (L::TPE - L::TOFF);
+      const int r = t - yx_el * (L::TPE - L::TOFF), hf = r & 1;
+      iz = jz = (r >> 1) < N1 ? (r >> 1) : N1 - 1;
+      yi[0] = hf; yj[0] = hf;        // (0,0) | (1,1)
+      yi[1] = hf; yj[1] = hf + 1;    // (0,1) | (1,2)
+      yi[2] = 2 * hf; yj[2] = 2;     // (0,2) | (2,2)
+    }
+    double Byp[3][4][Q1];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int q = 0; q < Q1; ++q)
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int bb = 0; bb < 2; ++bb) Byp[k][a * 2 + bb][q] = Bt(a, q, yi[k]) * Bt(bb, q, yj[k]);
+    for (int64_t it = 0;; ++it) {
+      const int64_t b = blockIdx.x + it * (int64_t)gridDim.x;
+      if (b >= nbatch) break;
+      const int64_t lb = b * E;
+      const int ne = (int)((nloc - lb) < E ? (nloc - lb) : E);
+      const int sl = (int)(it & 1);
+      SFP_T(5, sfp_named_bar(1, NXT));
+      SFP_T(4, sfp_wait(&fullT[sl], (uint32_t)((it >> 1) & 1)));
+      const double* T1e = reinterpret_cast<const double*>(smp + L::OFF_T1 + sl * L::T1SLOT) +
+                          yx_el * L::T1CELL;
+      double S[3][4][Q1];
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int q = 0; q < Q1; ++q) S[k][c][q] = 0.0;
+      if (xact && !FEB200_SFP_NOX) {
+        // ordered pairs (m, n): the unique pair first, its transpose (n, m) right after -- on a
+        // diagonal z pair that is the same T1 vector, kept in registers (no second load)
+        const bool zdiag = iz == jz;
+        double tv[Q2];
+#pragma unroll
+        for (int op = 0; op < NOP; ++op) {
+          int m, n;
+          // DIFF order: (0,0) (0,1) (1,0) (0,2) (2,0) (1,1) (1,2) (2,1) (2,2) [(3,3)]
+          if (DIFF && op < 9) {
+            m = (0x221120100 >> (4 * op)) & 0xF;
+            n = (0x212102010 >> (4 * op)) & 0xF;
+          } else { m = 3; n = 3; }
+          const int mm = m < n ? m : n, nn = m < n ? n : m;
+          const int ul = (mm == 3) ? NUP - 1 : (mm == 0 ? nn : (mm == 1 ? 2 + nn : 5));
+          const int zidx = (m > n) ? (jz * N1 + iz) : (iz * N1 + jz);
+          const double* src = T1e + (ul * N1 * N1 + zidx) * QQP;
+          if (m <= n || !zdiag) {
+#pragma unroll
+            for (int h = 0; h < Q2; ++h) tv[h] = src[h];
+          }
+          const int ay = m == 1, by = n == 1, cls = (m == 0) * 2 + (n == 0);
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int qx = 0; qx < Q1; ++qx)
+#pragma unroll
+              for (int qy = 0; qy < Q1; ++qy)
+                S[k][cls][qx] = fma(Byp[k][ay * 2 + by][qy], tv[qx * Q1 + qy], S[k][cls][qx]);
+        }
+      }
+      sfp_arrive(&emptyT[sl]);
+      KT* Kst = reinterpret_cast<KT*>(smp + L::OFF_K + sl * L::KSLOT);
+      const int su = (int)(it % L::SU);
+      if constexpr (RES) SFP_T(7, sfp_wait(&fullU[su], (uint32_t)((it / L::SU) & 1)));
+      if (xact && yx_el < ne) {
+        KT* Ke = Kst + yx_el * NB * NB;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          double acc[N1][N1];
+#pragma unroll
+          for (int a = 0; a < N1; ++a)
+#pragma unroll
+            for (int bb = 0; bb < N1; ++bb) acc[a][bb] = 0.0;
+#pragma unroll
+          for (int qx = 0; qx < Q1; ++qx)
+#pragma unroll
+            for (int ax = 0; ax < 2; ++ax) {
+              double u[N1];
+#pragma unroll
+              for (int bb = 0; bb < N1; ++bb)
+                u[bb] = Bt(0, qx, bb) * S[k][ax * 2 + 0][qx] + Bt(1, qx, bb) * S[k][ax * 2 + 1][qx];
+#pragma unroll
+              for (int a = 0; a < N1; ++a)
+#pragma unroll
+                for (int bb = 0; bb < N1; ++bb) acc[a][bb] = fma(Bt(ax, qx, a), u[bb], acc[a][bb]);
+            }
+          const bool mirror = (iz < jz) || (yi[k] < yj[k]);
+          const int ib = N1 * (yi[k] + N1 * iz), jb = N1 * (yj[k] + N1 * jz);
+#pragma unroll
+          for (int a = 0; a < N1; ++a)
+#pragma unroll
+            for (int bb = 0; bb < N1; ++bb) {
+              Ke[(ib + a) * NB + jb + bb] = (KT)acc[a][bb];
+              if (mirror) Ke[(jb + bb) * NB + ib + a] = (KT)acc[a][bb];
+            }
+          if constexpr (RES) {  // fixed (row, column-group) slots, as in the YB = 1 path
+            const double* ue = Ub + (su * E + yx_el) * NB;
+            double* re = Rb + yx_el * NB * N1 * N1;
+            const int gj = yj[k] + N1 * jz, gi = yi[k] + N1 * iz;
+#pragma unroll
+            for (int a = 0; a < N1; ++a) {
+              double t = 0.0;
+#pragma unroll
+              for (int bb = 0; bb < N1; ++bb) t = fma(acc[a][bb], ue[jb + bb], t);
+              re[(ib + a) * N1 * N1 + gj] = t;
+            }
+            if (mirror) {
+#pragma unroll
+              for (int bb = 0; bb < N1; ++bb) {
+                double t = 0.0;
+#pragma unroll
+                for (int a = 0; a < N1; ++a) t = fma(acc[a][bb], ue[ib + a], t);
+                re[(jb + bb) * N1 * N1 + gi] = t;
+              }
+            }
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      SFP_T(6, sfp_named_bar(2, NXT));
+      if constexpr (RES) {
+        for (int i = xtid; i < ne * NB; i += NXT) {
+          const double* rg = Rb + (size_t)i * N1 * N1;
+          double v = 0.0;
+#pragma unroll
+          for (int g = 0; g < N1 * N1; ++g) v += rg[g];
+          if (r_elem) r_elem[lb * NB + i] = v;
+          if (r_global) atomicAdd(r_global + DCb[su * E * NB + i], v);
+        }
+        sfp_arrive(&doneR[su]);
+      }
+      const uint32_t bytes = (uint32_t)ne * NB * NB * (uint32_t)sizeof(KT);
+      KT* gdst = K + lb * NB * NB;
+      if (FEB200_SFP_NOSTORE) {
+      } else if (((reinterpret_cast<uintptr_t>(gdst) | bytes) & 15u) == 0) {
+        if (xtid == 0) {
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                       :: "l"(gdst), "r"(smem_u32(Kst)), "r"(bytes) : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        }
+      } else {
+        for (int i = xtid; i < ne * NB * NB; i += NXT) gdst[i] = Kst[i];
+      }
+    }
+    if (xtid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else {
     // ======================= X: stages y and x, K store =======================
     const int xtid = tid - 32 * (1 + L::NG);
