@@ -46,12 +46,16 @@
 #ifndef FEB200_SFP_YB
 #define FEB200_SFP_YB 3  // y pairs per X thread at p = 2 (1 or 3)
 #endif
+#ifndef FEB200_SFP_MAP
+#define FEB200_SFP_MAP 1  // YB = 3: generated lane -> task permutation (sfp_tasks.h)
+#endif
 #ifndef FEB200_SF_MINB
 #define FEB200_SF_MINB 1
 #endif
 #include "fe_const.cuh"
 #include "fe_device.cuh"
 #include "fe_internal.h"
+#include "sfp_tasks.h"
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -822,17 +826,27 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
     static_assert(P == 2, "YB = 3 is the p = 2 task map");
     const int xtid = tid - 32 * (1 + L::NG);
     constexpr int NXT = 32 * L::NX;
-    const bool xact = xtid < E * L::TPE;
+    // lane -> task: the generated bank-conflict-optimised permutation (sfp_tasks.h) for the
+    // default batch of 8 cells, natural order otherwise
+    int task = xtid;
+#if FEB200_SFP_MAP
+    if constexpr (E == 8) {
+      static_assert(32 * L::NX == 128 && E * L::TPE == 120, "sfp_tasks.h is the E = 8 map");
+      task = sfp_tasks_yb3[xtid];
+    }
+#endif
+    const bool xact = task >= 0 && task < E * L::TPE;
+    if (!xact) task = 0;
     int yx_el, iz, jz, yi[3], yj[3];
-    if (xtid < E * L::TOFF) {  // z pair iz < jz (zp 0, 1, 2 = (0,1), (0,2), (1,2)), row iy
-      yx_el = xtid / L::TOFF;
-      const int r = xtid - yx_el * L::TOFF, zp = r / N1, iy = r - zp * N1;
+    if (task < E * L::TOFF) {  // z pair iz < jz (zp 0, 1, 2 = (0,1), (0,2), (1,2)), row iy
+      yx_el = task / L::TOFF;
+      const int r = task - yx_el * L::TOFF, zp = r / N1, iy = r - zp * N1;
       iz = zp >> 1;
       jz = zp == 0 ? 1 : 2;
 #pragma unroll
       for (int k = 0; k < 3; ++k) { yi[k] = iy; yj[k] = k; }
     } else {  // diagonal z pair iz == jz, upper-triangle y pairs in two groups of three
-      const int t = xtid - E * L::TOFF;
+      const int t = task - E * L::TOFF;
       yx_el = t / (L::TPE - L::TOFF);
       const int r = t - yx_el * (L::TPE - L::TOFF), hf = r & 1;
       iz = jz = (r >> 1) < N1 ? (r >> 1) : N1 - 1;
