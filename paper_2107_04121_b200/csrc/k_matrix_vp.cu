@@ -25,6 +25,7 @@
 #include "fe_device.cuh"
 #include "fe_internal.h"
 #include "vp_tasks.h"
+#include "vp_yb3_tasks.h"
 #ifndef FEB200_VP_L2PF
 #define FEB200_VP_L2PF 1
 #endif
@@ -48,6 +49,17 @@
 // 20-70 % slower in every X / G split tried -- the role becomes latency-bound.
 #ifndef FEB200_VP_XG_EL
 #define FEB200_VP_XG_EL 2
+#endif
+// YB3: the register-blocked X role of the scalar kernel (k_matrix_sf.cu) for the elasticity
+// items -- measured slower here (B200, C3 matrix: 2.29 ms natural lane map, 2.14 ms with the
+// annealed map of tools/gen_vp_yb3_tasks.c, vs 1.86 ms): the X shared-memory wavefronts halve
+// (data pipe 78 % -> 43 %) but with 6 X warps at 168 registers the role turns latency-bound and
+// waits on the single K staging buffer's store (kfree); off by default, kept for A/B
+#ifndef FEB200_VP_YB3
+#define FEB200_VP_YB3 0
+#endif
+#ifndef FEB200_VP_YB3MAP
+#define FEB200_VP_YB3MAP 1
 #endif
 #ifndef FEB200_VP_XG_CV
 #define FEB200_VP_XG_CV 2
@@ -126,6 +138,11 @@ __host__ __device__ constexpr int vp_voigt(int a, int j) {
 }
 __host__ __device__ constexpr int vp_um(int u) { return (0x3211000 >> (4 * u)) & 0xF; }
 __host__ __device__ constexpr int vp_un(int u) { return (0x3221210 >> (4 * u)) & 0xF; }
+// YB3 symmetric items: on a diagonal z pair the y pairs iy > jy are not stored (the (jy, iy)
+// task's mirror writes them)
+__device__ __forceinline__ bool zdiag_skip(bool sym, int iz, int jz, int iy, int jy) {
+  return sym && iz == jz && iy > jy;
+}
 template <int I, int N, class F>
 __device__ __forceinline__ void vp_static_for(F&& f) {
   if constexpr (I < N) {
@@ -213,12 +230,17 @@ struct VPL {
   static constexpr int NG2 = SPLIT ? NG - NG1 : NG;      // warps that run stage z
   static constexpr int NFULL = N1 * N1 * N1 * N1;        // (z pair, y pair) tasks, ordered
   static constexpr int NSYM = N1 * N1 * (N1 * (N1 - 1) / 2) + N1 * (N1 * (N1 + 1) / 2);
-  static constexpr int XG = EL ? FEB200_VP_XG_EL : FEB200_VP_XG_CV;  // X groups (alternate items)
-  static constexpr int NXW = (E * NFULL + 31) / 32;      // warps per X group
+  // YB3 (elasticity, E = 2): register-blocked X -- one thread per (z pair, iy) over jy = 0..2
+  // (a third of the T1 loads per output), every lane keeping one iy for all items so that its
+  // y-pair factors stay in registers; 3 X groups of 2 warps, each group one symmetric and one
+  // full item per batch
+  static constexpr bool YB3 = FEB200_VP_YB3 && EL && P == 2 && E == 2;
+  static constexpr int XG = YB3 ? 3 : (EL ? FEB200_VP_XG_EL : FEB200_VP_XG_CV);  // X groups (alternate items)
+  static constexpr int NXW = YB3 ? 2 : (E * NFULL + 31) / 32;  // warps per X group
   static constexpr int NX = XG * NXW;
   static constexpr int THREADS = 32 * (1 + NG + NX);
   static constexpr int S = EL ? FEB200_VP_S_EL : FEB200_VP_S_CV;  // T1 ring depth (items)
-  static constexpr bool TASKMAP = FEB200_VP_TASKMAP && P == 2 && E == 2 && NXW == 6;
+  static constexpr bool TASKMAP = FEB200_VP_TASKMAP && P == 2 && E == 2 && NXW == 6 && !YB3;
   static constexpr bool CONV = FORM == FE_FORM_CONVECTIVE;
   // L slot (doubles): coords [E][24], material a/b [E][NQ] | state [E][3][NB]
   static constexpr int LS_X = 0, LS_A = E * 24, LS_B = LS_A + E * NQ, LS_U = LS_B + E * NQ;
@@ -685,6 +707,160 @@ __global__ void __launch_bounds__(VPL<P, FORM, FD>::THREADS, 1)
         else g_item(std::false_type{}, i);
       }
       if constexpr (L::SPLIT) vp_arrive(&emptyW[wb]);
+    }
+  } else if constexpr (L::YB3) {
+    // ============ X, register-blocked (YB3): one (z pair, iy) per thread over jy = 0..2 ============
+    const int xall = tid - 32 * (1 + L::NG);
+    const int xg = xall / (32 * L::NXW), xtid = xall - xg * 32 * L::NXW;  // group, thread in group
+    // lane -> (iy; full task; symmetric task).  Full items: every ordered z pair (iz, jz);
+    // symmetric items: z pairs iz < jz and iz == jz -- the diagonal ones over all three iy
+    // (the y pairs iy > jy of those are computed and not stored: the (jy, iy) task's mirror
+    // writes them), so that every task has the form (z pair, iy; jy = 0..2)
+    int f_el = -1, f_iz = 0, f_jz = 0, s_el = -1, s_iz = 0, s_jz = 0, iy = 0;
+    if (FEB200_VP_YB3MAP) {  // generated bank-conflict-optimised map (tools/gen_vp_yb3_tasks.c)
+      const unsigned v = vp_yb3_tasks[xg][xtid];
+      iy = v & 3;
+      if (iy < 3) {
+        f_el = (v >> 2) & 3;
+        f_iz = (v >> 4) & 3;
+        f_jz = (v >> 6) & 3;
+        s_el = (v >> 8) & 3;
+        s_iz = (v >> 10) & 3;
+        s_jz = (v >> 12) & 3;
+        if (f_el == 3) f_el = -1;
+        if (s_el == 3) s_el = -1;
+      } else {
+        iy = 0;
+      }
+    } else {
+      const int cls = xtid / 21, j = xtid - cls * 21;
+      if (cls < 3) {
+        iy = cls;
+        if (j < E * 9) { f_el = j / 9; f_iz = (j % 9) / 3; f_jz = j % 3; }
+        if (j < E * 6) {
+          s_el = j / 6;
+          const int z6 = j % 6;
+          s_iz = z6 < 3 ? (z6 >> 1) : z6 - 3;
+          s_jz = z6 < 3 ? (z6 == 0 ? 1 : 2) : z6 - 3;
+        }
+      }
+    }
+    double Byp[3][4][Q1];  // Byp[jy][ay * 2 + by][qy] = B^ay[qy][iy] B^by[qy][jy]
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int q = 0; q < Q1; ++q)
+#pragma unroll
+        for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+          for (int b2 = 0; b2 < 2; ++b2) Byp[k][a2 * 2 + b2][q] = Bt(a2, q, iy) * Bt(b2, q, k);
+    for (int64_t it = 0;; ++it) {
+      int64_t lb;
+      int ne;
+      batch_of(it, lb, ne);
+      if (ne <= 0) break;
+      auto item = [&](auto SYMc, int I, int ia, int ib_) {
+        constexpr bool SYM = decltype(SYMc)::value;
+        const bool MIR = IT::mirror(I);
+        const int el = SYM ? s_el : f_el, iz = SYM ? s_iz : f_iz, jz = SYM ? s_jz : f_jz;
+        const bool xact = el >= 0;
+        const int64_t gi = it * NITEM + I;
+        const int s = (int)(gi % S);
+        VP_T(4, vp_wait(&fullT[s], (uint32_t)((gi / S) & 1)));
+        const double* T1e = reinterpret_cast<const double*>(smv + L::OFF_T1 + s * L::T1SLOT) +
+                            (xact ? el : 0) * IT::NPMAX * N1 * N1 * QQP;
+        double Sx[3][4][Q1];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int q = 0; q < Q1; ++q) Sx[k][c][q] = 0.0;
+        if (xact) {
+          const bool zdiag = SYM && iz == jz;
+          double tv[Q2];
+#pragma unroll
+          for (int op = 0; op < 9; ++op) {
+            int m, n, pidx, zidx;
+            if constexpr (SYM) {
+              // (0,0) (0,1) (1,0) (0,2) (2,0) (1,1) (1,2) (2,1) (2,2): a unique pair, then its
+              // transpose -- the same T1 vector on a diagonal z pair (kept, not reloaded)
+              m = (0x221120100 >> (4 * op)) & 0xF;
+              n = (0x212102010 >> (4 * op)) & 0xF;
+              const int mm = m < n ? m : n, nn = m < n ? n : m;
+              pidx = mm == 0 ? nn : (mm == 1 ? 2 + nn : 5);
+              zidx = (m > n) ? (jz * N1 + iz) : (iz * N1 + jz);
+            } else {
+              m = op / 3;
+              n = op % 3;
+              pidx = op;
+              zidx = iz * N1 + jz;
+            }
+            const double* src = T1e + (pidx * N1 * N1 + zidx) * QQP;
+            if (!SYM || m <= n || !zdiag) {
+#pragma unroll
+              for (int hh = 0; hh < Q2; ++hh) tv[hh] = src[hh];
+            }
+            const int ay = m == 1, by = n == 1, cls = (m == 0) * 2 + (n == 0);
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+              for (int qx = 0; qx < Q1; ++qx)
+#pragma unroll
+                for (int qy = 0; qy < Q1; ++qy)
+                  Sx[k][cls][qx] = fma(Byp[k][ay * 2 + by][qy], tv[qx * Q1 + qy], Sx[k][cls][qx]);
+          }
+        }
+        vp_arrive(&emptyT[s]);
+        if (I == xg && it > 0) {
+          // first K write of this thread in the batch: the store of batch it-1 has read the
+          // staging buffer
+          VP_T(5, vp_wait(kfree, (uint32_t)((it - 1) & 1)));
+        }
+        if (xact && el < ne) {
+          double* Kc = Kst + el * NDOF * NDOF;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            if (zdiag_skip(SYM, iz, jz, iy, k)) continue;
+            double acc[N1][N1];
+#pragma unroll
+            for (int a = 0; a < N1; ++a)
+#pragma unroll
+              for (int bb = 0; bb < N1; ++bb) acc[a][bb] = 0.0;
+#pragma unroll
+            for (int qx = 0; qx < Q1; ++qx)
+#pragma unroll
+              for (int ax = 0; ax < 2; ++ax) {
+                double u[N1];
+#pragma unroll
+                for (int bb = 0; bb < N1; ++bb)
+                  u[bb] = Bt(0, qx, bb) * Sx[k][ax * 2 + 0][qx] + Bt(1, qx, bb) * Sx[k][ax * 2 + 1][qx];
+#pragma unroll
+                for (int a = 0; a < N1; ++a)
+#pragma unroll
+                  for (int bb = 0; bb < N1; ++bb) acc[a][bb] = fma(Bt(ax, qx, a), u[bb], acc[a][bb]);
+              }
+            const int ib = N1 * (iy + N1 * iz), jb = N1 * (k + N1 * jz);
+            const bool mir_in = SYM && (iz < jz || iy < k);
+#pragma unroll
+            for (int a = 0; a < N1; ++a)
+#pragma unroll
+              for (int bb = 0; bb < N1; ++bb) {
+                const double v = acc[a][bb];
+                Kc[(ia * NB + ib + a) * NDOF + ib_ * NB + jb + bb] = v;
+                if (mir_in) Kc[(ia * NB + jb + bb) * NDOF + ib_ * NB + ib + a] = v;
+                if (MIR) Kc[(ib_ * NB + jb + bb) * NDOF + ia * NB + ib + a] = v;
+              }
+          }
+        }
+      };
+#pragma unroll 1
+      for (int i = xg; i < NITEM; i += L::XG) {
+        if (IT::sym(i)) item(std::true_type{}, i, IT::a(i), IT::b(i));
+        else item(std::false_type{}, i, IT::a(i), IT::b(i));
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      vp_arrive(kfull);
     }
   } else {
     // ======================= X: stages y and x per item, K staging, TMA store =======================
