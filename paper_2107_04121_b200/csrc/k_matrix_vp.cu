@@ -48,7 +48,7 @@
 // reuse (one thread per (cell, z pair, iy) over the three jy: a third of the T1 loads) was
 // 20-70 % slower in every X / G split tried -- the role becomes latency-bound.
 #ifndef FEB200_VP_XG_EL
-#define FEB200_VP_XG_EL 2
+#define FEB200_VP_XG_EL (FEB200_VP_E == 1 ? 1 : 2)
 #endif
 // YB3: the register-blocked X role of the scalar kernel (k_matrix_sf.cu) for the elasticity
 // items -- measured slower here (B200, C3 matrix: 2.29 ms natural lane map, 2.14 ms with the
@@ -62,7 +62,7 @@
 #define FEB200_VP_YB3MAP 1
 #endif
 #ifndef FEB200_VP_XG_CV
-#define FEB200_VP_XG_CV 2
+#define FEB200_VP_XG_CV (FEB200_VP_E == 1 ? 1 : 2)
 #endif
 #ifndef FEB200_VP_GH_EL
 #define FEB200_VP_GH_EL 4
@@ -255,10 +255,13 @@ struct VPL {
   static constexpr size_t OFF_IDX = OFF_L + 2 * size_t(LSLOT) * 8;       // [2][E][8 + NB] int32
   static constexpr size_t OFF_BAR = (OFF_IDX + 2 * size_t(E) * (8 + NB) * 4 + 15) / 16 * 16;
   static constexpr size_t BYTES = OFF_BAR + (10 + 2 * S) * 8;
+  // E = 1: two CTAs per SM (each ~100 KB), so that one CTA's K store drains while the other
+  // computes (the single K staging buffer of a CTA otherwise stalls X on kfree)
+  static constexpr int MINB = E == 1 ? 2 : 1;
 };
 
 template <int P, int FORM, bool FD>
-__global__ void __launch_bounds__(VPL<P, FORM, FD>::THREADS, 1)
+__global__ void __launch_bounds__(VPL<P, FORM, FD>::THREADS, VPL<P, FORM, FD>::MINB)
     k_matrix_vp(MeshView mv, int mat_kind, const double* __restrict__ ma, const double* __restrict__ mb,
                 const double* __restrict__ state_u, int64_t e0, int64_t e1, double* __restrict__ K,
                 int* __restrict__ nonsym) {
@@ -1086,7 +1089,7 @@ static cudaError_t launch_vp_t(const fe_mesh* mh, MatArgs mat, const double* sta
   auto kern = k_matrix_vp<P, FORM, FD>;
   const LaunchFacts lf = launch_facts((const void*)kern, L::THREADS, L::BYTES);
   if (lf.err != cudaSuccess) return lf.err;
-  const int nsm = lf.nsm;
+  const int64_t nsm = (int64_t)lf.nsm * (lf.per_sm < L::MINB ? lf.per_sm : L::MINB);
   const int64_t nbatch = (e1 - e0 + L::E - 1) / L::E;
   int grid = (int)(nbatch < nsm ? nbatch : nsm);
   grid = grid_cap(grid);

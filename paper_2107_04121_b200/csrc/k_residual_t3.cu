@@ -26,6 +26,12 @@
 #ifndef FEB200_T3C
 #define FEB200_T3C 1
 #endif
+// t3c flux: v = w C u (C the cofactors of J) is the same for the three components of a qp, so
+// component lane a forms it at the qps qx = a of its plane only and the others fetch it by
+// shuffle (a third of the per-qp geometry per lane, about as many shuffles as fetching u)
+#ifndef FEB200_T3C_VSHARE
+#define FEB200_T3C_VSHARE 1
+#endif
 #ifndef FEB200_T3C_MINB
 #define FEB200_T3C_MINB 4
 #endif
@@ -446,6 +452,14 @@ __global__ void __launch_bounds__(FEB200_T3_THREADS, FEB200_T3C_MINB)
   const int srcu0 = lane_ok ? 9 * cl + j : lane, srcu1 = lane_ok ? 9 * cl + 3 + j : lane,
             srcu2 = lane_ok ? 9 * cl + 6 + j : lane;  // component lanes of the same plane
   const double tZ = lane_ok ? c_x1d[P][j] : 0.5, wz = lane_ok ? c_w1d[P][j] : 0.0;
+  // VSHARE: this lane's qx = a (point, weight) and the lanes of component (a + s) % 3
+  const double tXa = lane_ok ? c_x1d[P][a] : 0.5, wXa = lane_ok ? c_w1d[P][a] : 0.0;
+  int srcc[3], srcv[3];
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    srcc[s] = lane_ok ? 9 * cl + 3 * ((a + s) % 3) + j : lane;
+    srcv[s] = lane_ok ? 9 * cl + 3 * s + j : lane;  // component lane s holds v at qx = s
+  }
   const int64_t nloc = e1 - e0;
   const int wpb = blockDim.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5), nw = (int64_t)gridDim.x * wpb;
@@ -603,6 +617,58 @@ __global__ void __launch_bounds__(FEB200_T3_THREADS, FEB200_T3C_MINB)
       }
     }
     double Fv[N][N];
+    if constexpr (FEB200_T3C_VSHARE) {
+      // u_b at the qps (qx = a, qy) of this plane: own component by select, the others from the
+      // component lanes b = (a + s) % 3, which send their value at qx = a = (b - s) % 3
+      double U3[N][3];
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const int xs = (a - s + 3) % 3;  // the qx the lane of component a - s asks this lane for
+#pragma unroll
+        for (int qy = 0; qy < N; ++qy) {
+          const double snd = xs == 0 ? Uq[qy][0] : (xs == 1 ? Uq[qy][1] : Uq[qy][2]);
+          U3[qy][s] = s == 0 ? snd : __shfl_sync(0xffffffffu, snd, srcc[s]);
+        }
+      }
+      // v = w C u at (qx = a, qy):  v_m = sum_r C_rm u_r
+      double V[N][3];
+#pragma unroll
+      for (int qy = 0; qy < N; ++qy) {
+        const double t1 = c_x1d[P][qy];
+        double J[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const double h0 = (1 - tXa) * (X[4][i] - X[0][i]) + tXa * (X[5][i] - X[1][i]);
+          const double h1 = (1 - tXa) * (X[6][i] - X[2][i]) + tXa * (X[7][i] - X[3][i]);
+          J[i][0] = fma(t1, gdE[i], gE0[i]);
+          J[i][1] = fma(tXa, gdF[i], gF0[i]);
+          J[i][2] = fma(t1, h1 - h0, h0);
+        }
+        const double C00 = J[1][1] * J[2][2] - J[1][2] * J[2][1], C01 = J[1][2] * J[2][0] - J[1][0] * J[2][2],
+                     C02 = J[1][0] * J[2][1] - J[1][1] * J[2][0], C10 = J[0][2] * J[2][1] - J[0][1] * J[2][2],
+                     C11 = J[0][0] * J[2][2] - J[0][2] * J[2][0], C12 = J[0][1] * J[2][0] - J[0][0] * J[2][1],
+                     C20 = J[0][1] * J[1][2] - J[0][2] * J[1][1], C21 = J[0][2] * J[1][0] - J[0][0] * J[1][2],
+                     C22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+        // U3[qy][s] = u_{(a + s) % 3}: back to component order
+        const double u0 = a == 0 ? U3[qy][0] : (a == 1 ? U3[qy][2] : U3[qy][1]);
+        const double u1 = a == 0 ? U3[qy][1] : (a == 1 ? U3[qy][0] : U3[qy][2]);
+        const double u2 = a == 0 ? U3[qy][2] : (a == 1 ? U3[qy][1] : U3[qy][0]);
+        const double wq = wXa * c_w1d[P][qy] * wz;
+        V[qy][0] = wq * (C00 * u0 + C10 * u1 + C20 * u2);
+        V[qy][1] = wq * (C01 * u0 + C11 * u1 + C21 * u2);
+        V[qy][2] = wq * (C02 * u0 + C12 * u1 + C22 * u2);
+      }
+      // detw f0_a = w sum_r t_r u_r = grad_ref u_a . v  (t = C^T grad_ref u_a)
+#pragma unroll
+      for (int qy = 0; qy < N; ++qy)
+#pragma unroll
+        for (int qx = 0; qx < N; ++qx) {
+          const double v0 = __shfl_sync(0xffffffffu, V[qy][0], srcv[qx]);
+          const double v1 = __shfl_sync(0xffffffffu, V[qy][1], srcv[qx]);
+          const double v2 = __shfl_sync(0xffffffffu, V[qy][2], srcv[qx]);
+          Fv[qy][qx] = valid ? (Gx[qy][qx] * v0 + Gy[qy][qx] * v1 + Gz[qy][qx] * v2) : 0.0;
+        }
+    } else {
 #pragma unroll
     for (int qy = 0; qy < N; ++qy)
 #pragma unroll
@@ -641,6 +707,7 @@ __global__ void __launch_bounds__(FEB200_T3_THREADS, FEB200_T3C_MINB)
         const double wq = c_w1d[P][qx] * c_w1d[P][qy] * wz;
         Fv[qy][qx] = valid ? wq * (tr0 * w0 + tr1 * w1 + tr2 * w2) : 0.0;
       }
+    }
     double Hv[N][N];
 #pragma unroll
     for (int qy = 0; qy < N; ++qy)
