@@ -32,6 +32,12 @@
 #ifndef FEB200_T3C_VSHARE
 #define FEB200_T3C_VSHARE 1
 #endif
+#ifndef FEB200_T3E
+#define FEB200_T3E 1  // register-resident elasticity residual (p = 2, isotropic)
+#endif
+#ifndef FEB200_T3E_MINB
+#define FEB200_T3E_MINB 4
+#endif
 #ifndef FEB200_T3C_MINB
 #define FEB200_T3C_MINB 4
 #endif
@@ -773,6 +779,347 @@ static cudaError_t launch_t3c(const fe_mesh* mh, const double* u, int64_t e0, in
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------
+// Isotropic linear elasticity residual r_(a,k) = int sum_r sigma_ar(u) d phi_k / dx_r (P:1033,
+// Voigt D = lambda m m^T + mu (2 I_3 (+) I_3), contracted analytically) at p = 2, fp64,
+// register-resident with the lane layout of k_residual_t3c: NINE lanes per cell, lane (a, j)
+// owning component a on z-plane j.  Forward pass per component (x, y in registers, z by
+// shuffles among the plane lanes) gives the reference gradient g of u_a at the lane's 9 qps;
+// t = C g = det grad u_a (C the cofactors of J).  The stress needs, from the other component
+// lanes b of the same plane, t_b[b] (the trace) and t_b[a] (the symmetric part): four shuffles
+// per qp.  With S_r = det sigma_ar = lambda delta_ar sum_b t_b[b] + mu (t_a[r] + t_r[a]),
+//   F_m = detw sum_r sigma_ar J^-1[m][r] = (w / det) sum_r C[r][m] S_r,
+// and the backward pass is that of the scalar diffusion kernel (z^T by shuffles, y^T, x^T in
+// registers, fused scatter).  PERQP: lambda, mu per quadrature point, else per cell.
+template <bool PERQP, bool EVAL, bool PEER = false>
+__global__ void __launch_bounds__(FEB200_T3_THREADS, FEB200_T3E_MINB)
+    k_residual_t3e(MeshView mv, const double* __restrict__ ma, const double* __restrict__ mb,
+                   const double* __restrict__ u, int64_t e0, int64_t e1, double* __restrict__ r_elem,
+                   double* __restrict__ r_global, double* __restrict__ eval_out, PeerWin pw) {
+  constexpr int P = 2, N = 3, NB = 27, NQ = 27;
+  constexpr int NM = PERQP ? 18 : 2;  // staged material values per lane (lambda, mu)
+#define B0(q, k) c_tab1d[P][0][q][k]
+#define B1(q, k) c_tab1d[P][1][q][k]
+  const int lane = threadIdx.x & 31;
+  const int cl = lane / 9, rem = lane - 9 * cl, a = rem / 3, j = rem - 3 * a;
+  const bool lane_ok = lane < 27;
+  const int base = 9 * cl + 3 * a;  // the three plane lanes of (cell, component)
+  double f0[3], f1[3];
+  int srcf[3], srcb[3], srcc[3];
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    const int k = (j + s) % 3;
+    f0[s] = lane_ok ? c_tab1d[P][0][j][k] : 0.0;
+    f1[s] = lane_ok ? c_tab1d[P][1][j][k] : 0.0;
+    srcf[s] = lane_ok ? base + k : lane;
+    srcb[s] = lane_ok ? base + (j - s + 3) % 3 : lane;
+    srcc[s] = lane_ok ? 9 * cl + 3 * ((a + s) % 3) + j : lane;  // component (a + s) % 3, same plane
+  }
+  const double tZ = lane_ok ? c_x1d[P][j] : 0.5, wz = lane_ok ? c_w1d[P][j] : 0.0;
+  const int64_t nloc = e1 - e0;
+  const int wpb = blockDim.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5), nw = (int64_t)gridDim.x * wpb;
+  constexpr int TH = FEB200_T3_THREADS;
+  extern __shared__ __align__(16) unsigned char t3s[];
+  double* s1m = reinterpret_cast<double*>(t3s);                 // [3][NM][TH]
+  double* s2u = s1m + 3 * NM * TH;                              // [2][9][TH]
+  double* s2x = s2u + 2 * 9 * TH;                               // [2][8][TH]
+  int32_t* s1d = reinterpret_cast<int32_t*>(s2x + 2 * 8 * TH);  // [3][9][TH]
+  int32_t* s1c = s1d + 3 * 9 * TH;                              // [3][8][TH]
+  const int tid = threadIdx.x;
+  auto group_cell = [&](int64_t g, int64_t& le, bool& ok) {
+    le = (gw + g * nw) * 3 + cl;
+    ok = lane_ok && le < nloc;
+  };
+  auto issue_s1 = [&](int64_t g) {
+    int64_t le;
+    bool ok;
+    group_cell(g, le, ok);
+    if (ok) {
+      const int sl = (int)(g % 3);
+      const int64_t e = e0 + le;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) t3_cp4(&s1d[(sl * 9 + k) * TH + tid], mv.dof_conn + e * NB + N * N * j + k);
+      if (a == 0) {
+#pragma unroll
+        for (int v = 0; v < 8; ++v) t3_cp4(&s1c[(sl * 8 + v) * TH + tid], mv.conn + 8 * e + v);
+      }
+      if constexpr (PERQP) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+          t3_cp8(&s1m[(sl * NM + k) * TH + tid], ma + e * NQ + N * N * j + k);
+          t3_cp8(&s1m[(sl * NM + 9 + k) * TH + tid], mb + e * NQ + N * N * j + k);
+        }
+      } else {
+        t3_cp8(&s1m[(sl * NM + 0) * TH + tid], ma + e);
+        t3_cp8(&s1m[(sl * NM + 1) * TH + tid], mb + e);
+      }
+    }
+    t3_commit();
+  };
+  auto issue_s2 = [&](int64_t g) {
+    int64_t le;
+    bool ok;
+    group_cell(g, le, ok);
+    if (ok) {
+      const int s1 = (int)(g % 3), s2 = (int)(g & 1);
+      int dd[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) dd[k] = s1d[(s1 * 9 + k) * TH + tid];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) t3_cp8(&s2u[(s2 * 9 + k) * TH + tid], u + 3 * (int64_t)dd[k] + a);
+      if (a == 0) {
+        int vv[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) vv[h] = s1c[(s1 * 8 + (8 * j + h) / 3) * TH + tid];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const int pidx = 8 * j + h, i = pidx % 3;
+          t3_cp8(&s2x[(s2 * 8 + h) * TH + tid], mv.coords + 3 * (int64_t)vv[h] + i);
+        }
+      }
+    }
+    t3_commit();
+  };
+  issue_s1(0);
+  issue_s1(1);
+  t3_wait<1>();
+  issue_s2(0);
+  for (int64_t g = 0;; ++g) {
+    int64_t le;
+    bool valid;
+    group_cell(g, le, valid);
+    if ((gw + g * nw) * 3 >= nloc) break;
+    t3_wait<0>();
+    __syncwarp();
+    issue_s2(g + 1);
+    issue_s1(g + 2);
+    const int s1 = (int)(g % 3), s2 = (int)(g & 1);
+    int dof[N][N];
+    double uv[N][N];
+#pragma unroll
+    for (int ky = 0; ky < N; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < N; ++kx) {
+        dof[ky][kx] = s1d[(s1 * 9 + kx + N * ky) * TH + tid];
+        uv[ky][kx] = valid ? s2u[(s2 * 9 + kx + N * ky) * TH + tid] : 0.0;
+      }
+    // ---- forward: reference gradient of u_a at the qps (qx, qy, qz = j)
+    double c01[N][N], c10[N][N], c00[N][N];
+    {
+      double a0[N][N], a1[N][N];
+#pragma unroll
+      for (int ky = 0; ky < N; ++ky)
+#pragma unroll
+        for (int qx = 0; qx < N; ++qx) {
+          double s0 = 0.0, sd = 0.0;
+#pragma unroll
+          for (int kx = 0; kx < N; ++kx) {
+            s0 = fma(B0(qx, kx), uv[ky][kx], s0);
+            sd = fma(B1(qx, kx), uv[ky][kx], sd);
+          }
+          a0[ky][qx] = s0;
+          a1[ky][qx] = sd;
+        }
+#pragma unroll
+      for (int qy = 0; qy < N; ++qy)
+#pragma unroll
+        for (int qx = 0; qx < N; ++qx) {
+          double s00 = 0.0, s01 = 0.0, s10 = 0.0;
+#pragma unroll
+          for (int ky = 0; ky < N; ++ky) {
+            s00 = fma(B0(qy, ky), a0[ky][qx], s00);
+            s01 = fma(B1(qy, ky), a0[ky][qx], s01);
+            s10 = fma(B0(qy, ky), a1[ky][qx], s10);
+          }
+          c00[qy][qx] = s00;
+          c01[qy][qx] = s01;
+          c10[qy][qx] = s10;
+        }
+    }
+    double Gx[N][N], Gy[N][N], Gz[N][N];
+#pragma unroll
+    for (int qy = 0; qy < N; ++qy)
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        const double v00 = c00[qy][qx], v01 = c01[qy][qx], v10 = c10[qy][qx];
+        double gz = f1[0] * v00, gy = f0[0] * v01, gx = f0[0] * v10;
+#pragma unroll
+        for (int s = 1; s < 3; ++s) {
+          const double w00 = __shfl_sync(0xffffffffu, v00, srcf[s]);
+          const double w01 = __shfl_sync(0xffffffffu, v01, srcf[s]);
+          const double w10 = __shfl_sync(0xffffffffu, v10, srcf[s]);
+          gz = fma(f1[s], w00, gz);
+          gy = fma(f0[s], w01, gy);
+          gx = fma(f0[s], w10, gx);
+        }
+        Gx[qy][qx] = gx;
+        Gy[qy][qx] = gy;
+        Gz[qy][qx] = gz;
+      }
+    double X[8][3];
+    const int wb = tid - lane;
+#pragma unroll
+    for (int pidx = 0; pidx < 24; ++pidx)
+      X[pidx / 3][pidx % 3] = valid ? s2x[(s2 * 8 + pidx % 8) * TH + wb + 9 * cl + pidx / 8] : 0.0;
+    double gE0[3], gdE[3], gF0[3], gdF[3], gH0[N][3], gdH[N][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double e0_ = (1 - tZ) * (X[1][i] - X[0][i]) + tZ * (X[5][i] - X[4][i]);
+      const double e1_ = (1 - tZ) * (X[3][i] - X[2][i]) + tZ * (X[7][i] - X[6][i]);
+      const double f0_ = (1 - tZ) * (X[2][i] - X[0][i]) + tZ * (X[6][i] - X[4][i]);
+      const double f1_ = (1 - tZ) * (X[3][i] - X[1][i]) + tZ * (X[7][i] - X[5][i]);
+      gE0[i] = e0_; gdE[i] = e1_ - e0_; gF0[i] = f0_; gdF[i] = f1_ - f0_;
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        const double t0 = c_x1d[P][qx];
+        const double h0 = (1 - t0) * (X[4][i] - X[0][i]) + t0 * (X[5][i] - X[1][i]);
+        const double h1 = (1 - t0) * (X[6][i] - X[2][i]) + t0 * (X[7][i] - X[3][i]);
+        gH0[qx][i] = h0;
+        gdH[qx][i] = h1 - h0;
+      }
+    }
+    double lamE = 0.0, muE = 0.0;
+    if constexpr (!PERQP) {
+      lamE = s1m[(s1 * NM + 0) * TH + tid];
+      muE = s1m[(s1 * NM + 1) * TH + tid];
+    }
+    // ---- flux F_m = (w / det) sum_r C[r][m] S_r at the 9 qps, the backward z^T pulled after
+    double Fx[N][N], Fy[N][N], Fz[N][N];
+#pragma unroll
+    for (int qy = 0; qy < N; ++qy)
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        const double t0 = c_x1d[P][qx], t1 = c_x1d[P][qy];
+        double J[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          J[i][0] = fma(t1, gdE[i], gE0[i]);
+          J[i][1] = fma(t0, gdF[i], gF0[i]);
+          J[i][2] = fma(t1, gdH[qx][i], gH0[qx][i]);
+        }
+        const double C00 = J[1][1] * J[2][2] - J[1][2] * J[2][1], C01 = J[1][2] * J[2][0] - J[1][0] * J[2][2],
+                     C02 = J[1][0] * J[2][1] - J[1][1] * J[2][0], C10 = J[0][2] * J[2][1] - J[0][1] * J[2][2],
+                     C11 = J[0][0] * J[2][2] - J[0][2] * J[2][0], C12 = J[0][1] * J[2][0] - J[0][0] * J[2][1],
+                     C20 = J[0][1] * J[1][2] - J[0][2] * J[1][1], C21 = J[0][2] * J[1][0] - J[0][0] * J[1][2],
+                     C22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+        const double det = J[0][0] * C00 + J[0][1] * C01 + J[0][2] * C02;
+        const double g0 = Gx[qy][qx], g1 = Gy[qy][qx], g2 = Gz[qy][qx];
+        // t_r = det (grad u_a)_r
+        const double ta0 = C00 * g0 + C01 * g1 + C02 * g2;
+        const double ta1 = C10 * g0 + C11 * g1 + C12 * g2;
+        const double ta2 = C20 * g0 + C21 * g1 + C22 * g2;
+        // own diagonal t_a[a]; for the lane of component a - s: t_a[(a - s) % 3]
+        const double dg = a == 0 ? ta0 : (a == 1 ? ta1 : ta2);
+        const double sn1 = a == 0 ? ta2 : (a == 1 ? ta0 : ta1);  // (a - 1) % 3
+        const double sn2 = a == 0 ? ta1 : (a == 1 ? ta2 : ta0);  // (a - 2) % 3
+        const double rd1 = __shfl_sync(0xffffffffu, dg, srcc[1]);   // t_b[b], b = (a + 1) % 3
+        const double ro1 = __shfl_sync(0xffffffffu, sn1, srcc[1]);  // t_b[a]
+        const double rd2 = __shfl_sync(0xffffffffu, dg, srcc[2]);   // b = (a + 2) % 3
+        const double ro2 = __shfl_sync(0xffffffffu, sn2, srcc[2]);
+        double lam = lamE, mu = muE;
+        if constexpr (PERQP) {
+          lam = s1m[(s1 * NM + qx + N * qy) * TH + tid];
+          mu = s1m[(s1 * NM + 9 + qx + N * qy) * TH + tid];
+        }
+        const double T = dg + rd1 + rd2;  // det tr(grad u)
+        // S_r in rotated order: r = a, (a + 1) % 3, (a + 2) % 3
+        const double S0r = fma(lam, T, 2.0 * mu * dg);
+        const double t_a1 = a == 0 ? ta1 : (a == 1 ? ta2 : ta0);  // t_a[(a + 1) % 3]
+        const double t_a2 = a == 0 ? ta2 : (a == 1 ? ta0 : ta1);  // t_a[(a + 2) % 3]
+        const double S1r = mu * (t_a1 + ro1);
+        const double S2r = mu * (t_a2 + ro2);
+        const double S0 = a == 0 ? S0r : (a == 1 ? S2r : S1r);
+        const double S1 = a == 0 ? S1r : (a == 1 ? S0r : S2r);
+        const double S2 = a == 0 ? S2r : (a == 1 ? S1r : S0r);
+        const double sc = valid ? c_w1d[P][qx] * c_w1d[P][qy] * wz * rcp_nr(det) : 0.0;
+        Fx[qy][qx] = sc * (C00 * S0 + C10 * S1 + C20 * S2);
+        Fy[qy][qx] = sc * (C01 * S0 + C11 * S1 + C21 * S2);
+        Fz[qy][qx] = sc * (C02 * S0 + C12 * S1 + C22 * S2);
+      }
+    // ---- z^T through the component's plane lanes
+    double Hv[N][N], Hx[N][N], Hy[N][N];
+#pragma unroll
+    for (int qy = 0; qy < N; ++qy)
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        const double fx = Fx[qy][qx], fy = Fy[qy][qx], fz = Fz[qy][qx];
+        double hv = f1[0] * fz, hx = f0[0] * fx, hy = f0[0] * fy;
+#pragma unroll
+        for (int s = 1; s < 3; ++s) {
+          hv += __shfl_sync(0xffffffffu, f1[s] * fz, srcb[s]);
+          hx += __shfl_sync(0xffffffffu, f0[s] * fx, srcb[s]);
+          hy += __shfl_sync(0xffffffffu, f0[s] * fy, srcb[s]);
+        }
+        Hv[qy][qx] = hv;
+        Hx[qy][qx] = hx;
+        Hy[qy][qx] = hy;
+      }
+    double ev = 0.0;
+#pragma unroll
+    for (int ky = 0; ky < N; ++ky) {
+      double Iv[N], Ix[N];
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        double sv = 0.0, sx = 0.0;
+#pragma unroll
+        for (int qy = 0; qy < N; ++qy) {
+          sv = fma(B0(qy, ky), Hv[qy][qx], sv);
+          sv = fma(B1(qy, ky), Hy[qy][qx], sv);
+          sx = fma(B0(qy, ky), Hx[qy][qx], sx);
+        }
+        Iv[qx] = sv;
+        Ix[qx] = sx;
+      }
+#pragma unroll
+      for (int kx = 0; kx < N; ++kx) {
+        double rr = 0.0;
+#pragma unroll
+        for (int qx = 0; qx < N; ++qx) {
+          rr = fma(B0(qx, kx), Iv[qx], rr);
+          rr = fma(B1(qx, kx), Ix[qx], rr);
+        }
+        if (valid) {
+          if (r_elem) r_elem[le * 3 * NB + a * NB + kx + N * ky + N * N * j] = rr;
+          if (r_global) atomicAdd(r_global + 3 * (int64_t)dof[ky][kx] + a, rr);
+          if constexpr (PEER) peer_scatter<3>(pw, dof[ky][kx], a, rr);
+          if (EVAL) ev = fma(rr, uv[ky][kx], ev);
+        }
+      }
+    }
+    if (EVAL) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
+      if (lane == 0 && ev != 0.0) atomicAdd(eval_out, ev);
+    }
+  }
+  t3_wait<0>();
+#undef B0
+#undef B1
+}
+
+template <bool PERQP>
+static cudaError_t launch_t3e_t(const fe_mesh* mh, MatArgs mat, const double* u, int64_t e0, int64_t e1,
+                                double* r_elem, double* r_global, double* eval_out, cudaStream_t st) {
+  const PeerWin pw = g_peer;
+  auto kern = eval_out ? k_residual_t3e<PERQP, true>
+                       : (pw.n > 0 ? k_residual_t3e<PERQP, false, true> : k_residual_t3e<PERQP, false>);
+  constexpr int NM = PERQP ? 18 : 2;
+  const size_t smem = (size_t)FEB200_T3_THREADS * (8 * (3 * NM + 2 * 9 + 2 * 8) + 4 * (3 * 9 + 3 * 8));
+  const LaunchFacts lf = launch_facts((const void*)kern, FEB200_T3_THREADS, smem);
+  if (lf.err != cudaSuccess) return lf.err;
+  const int nsm = lf.nsm, per_sm = lf.per_sm;
+  const int64_t ncg = (e1 - e0 + 2) / 3;  // 3 cells per warp
+  const int64_t nblk = (ncg + FEB200_T3_THREADS / 32 - 1) / (FEB200_T3_THREADS / 32);
+  int grid = (int)(nblk < (int64_t)nsm * per_sm ? nblk : (int64_t)nsm * per_sm);
+  grid = grid_cap(grid);
+  if (grid <= 0) return cudaSuccess;
+  kern<<<grid, FEB200_T3_THREADS, smem, st>>>(view_of(mh), (const double*)mat.a, (const double*)mat.b, u,
+                                              e0, e1, r_elem, r_global, eval_out, pw);
+  count_launch();
+  return cudaGetLastError();
+}
+
 // Scalar forms at p = 2 in fp64; cudaErrorNotSupported otherwise (the smem kernel runs).
 cudaError_t launch_residual_t3(const fe_mesh* mh, int form, MatArgs mat, const double* u, int64_t e0,
                                int64_t e1, double* r_elem, double* r_global, cudaStream_t st,
@@ -785,6 +1132,11 @@ cudaError_t launch_residual_t3(const fe_mesh* mh, int form, MatArgs mat, const d
       return launch_t3_t<FE_FORM_MASS_DIFFUSION>(mh, mat, u, e0, e1, r_elem, r_global, eval_out, st);
     case FE_FORM_CONVECTIVE:
       if (FEB200_T3C) return launch_t3c(mh, u, e0, e1, r_elem, r_global, eval_out, st);
+      return cudaErrorNotSupported;
+    case FE_FORM_ELASTICITY:  // isotropic lambda, mu per cell or per qp (general D: the smem kernel)
+      if (!FEB200_T3E) return cudaErrorNotSupported;
+      if (mat.kind == FE_MAT_PER_ELEM) return launch_t3e_t<false>(mh, mat, u, e0, e1, r_elem, r_global, eval_out, st);
+      if (mat.kind == FE_MAT_PER_QP) return launch_t3e_t<true>(mh, mat, u, e0, e1, r_elem, r_global, eval_out, st);
       return cudaErrorNotSupported;
     default: return cudaErrorNotSupported;
   }
