@@ -80,6 +80,15 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 #ifndef FEB200_RSF_PADP
 #define FEB200_RSF_PADP 4
 #endif
+// PENCIL (scalar forms, p >= 3): each stage runs on pencils along its own direction -- the
+// thread of a cell's (p0, p1) slot is the x-pencil (y, z) = (p0, p1) for stages x / x^T, the
+// y-pencil (x, z) for y / y^T and the z-column (x, y) for z / flux / z^T -- with the tensors
+// transposed through two shared-memory buffers in between: every exchanged value is stored
+// once and loaded once (5 + 5 per value and stage instead of 1 + p + 1 loads), one barrier
+// per stage
+#ifndef FEB200_RSF_PENCIL
+#define FEB200_RSF_PENCIL 1
+#endif
 #ifndef FEB200_RSF_COF
 #define FEB200_RSF_COF 1
 #endif
@@ -94,8 +103,11 @@ struct RSF {
   static constexpr int EB = (D == 3 && P >= 3) ? EB0 / 2
                            : ((D == 3 && P == 2) ? FEB200_RSF_EB3
                               : (P == 2 ? FEB200_RSF_EB2 : (P == 4 ? FEB200_RSF_EB4 : EB0)));
+  // PENCIL at p = 4: fp64 two CTAs per SM (204 registers, no spills; three: 168 with spills,
+  // 0.200 vs 0.181 ms on C4), fp32 three
   static constexpr int MINB = (D == 3 && P == 2) ? FEB200_RSF_MINB3
-                              : (D == 1 && P == 2 ? FEB200_RSF_MINB2 : (D == 1 && P == 4 ? FEB200_RSF_MINB4 : 2));
+                              : (D == 1 && P == 2 ? FEB200_RSF_MINB2
+                                 : (D == 1 && P == 4 ? ((FEB200_RSF_PENCIL && sizeof(T) == 8) ? 2 : FEB200_RSF_MINB4) : 2));
   static constexpr int THREADS = (EB * TPE + 31) / 32 * 32;
   static constexpr int THREADS_ = THREADS;
   // exchange buffer per cell (elements of T), padded so that consecutive cells start PADB
@@ -118,7 +130,8 @@ struct RSF {
   static constexpr size_t SL_MB = (SL_MA + size_t(EB) * NQ * sizeof(T) + 16 + 15) / 16 * 16;
   static constexpr size_t SL_SIZE = (SL_MB + size_t(EB) * NQ * sizeof(T) + 16 + 15) / 16 * 16;
   static constexpr size_t OFF_X = (2 * Q1 * N1 * 8 + 15) / 16 * 16;
-  static constexpr size_t OFF_XV = (OFF_X + size_t(EB) * XS * sizeof(T) + 15) / 16 * 16;
+  static constexpr bool PENCIL = FEB200_RSF_PENCIL && D == 1 && P >= 3;
+  static constexpr size_t OFF_XV = (OFF_X + size_t(EB) * XS * (PENCIL ? 2 : 1) * sizeof(T) + 15) / 16 * 16;
   static constexpr int XVS = 28;  // per-cell stride of the staged vertex coordinates (bank spread)
   static constexpr size_t OFF_SLOT = OFF_XV + size_t(EB) * XVS * 8;
   static constexpr int NSLOT = 3;  // index/material ring: TMA two batches ahead
@@ -154,6 +167,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
   // forms whose flux is linear in grad u (f0 of the convective form, f1 of elasticity): the
   // flux evaluated at det grad u in cofactor form (FEB200_RSF_COF)
   constexpr bool COFV = FEB200_RSF_COF && (FORM == FE_FORM_ELASTICITY || FORM == FE_FORM_CONVECTIVE);
+  constexpr bool PENCIL = L::PENCIL;
   using A = T;  // contraction arithmetic in the call's precision (geometry and flux stay fp64)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Bs = reinterpret_cast<T*>(smem_raw);  // [2][Q1][N1] in the arithmetic type
@@ -263,7 +277,9 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
     const bool v = active && el < ne;
 #pragma unroll
     for (int kz = 0; kz < N1; ++kz) {
-      const int dof = v ? ds[el * NB + tx + N1 * ty + N1 * N1 * kz] : 0;
+      // z-column (tx, ty, kz); PENCIL: x-pencil (kx = kz, y = tx, z = ty)
+      const int nidx = PENCIL ? kz + N1 * tx + N1 * N1 * ty : tx + N1 * ty + N1 * N1 * kz;
+      const int dof = v ? ds[el * NB + nidx] : 0;
 #pragma unroll
       for (int a = 0; a < D; ++a) u_next[a][kz] = v ? (A)u[(int64_t)dof * D + a] : A(0);
     }
@@ -299,13 +315,14 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
     A uc[D][N1];
 #pragma unroll
     for (int kz = 0; kz < N1; ++kz) {
-      dcol[kz] = valid ? ds[tx + N1 * ty + N1 * N1 * kz] : 0;
+      dcol[kz] = valid ? ds[PENCIL ? kz + N1 * tx + N1 * N1 * ty : tx + N1 * ty + N1 * N1 * kz] : 0;
 #pragma unroll
       for (int a = 0; a < D; ++a) uc[a][kz] = u_next[a][kz];
     }
     // gathers of the next batch now, so that their latency overlaps this whole batch
     gather_next(it + 1);
     MatQ<T> mq[Q1];
+    auto load_mq = [&]() {
 #pragma unroll
     for (int qz = 0; qz < Q1; ++qz) {
       const int q = tx + Q1 * ty + Q1 * Q1 * qz;
@@ -324,7 +341,64 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
       }
       mq[qz] = m;
     }
+    };
+    if constexpr (!PENCIL) load_mq();  // PENCIL: loaded after the transposes (register pressure)
     T* Xe = X + el * L::XS;
+    T* Xf = X + (size_t)EB * L::XS + el * L::XS;  // PENCIL: the second transpose buffer
+    A c00[D][N1], c01[D][N1], c10[D][N1];  // [kz] at (qx = tx, qy = ty)
+    if constexpr (PENCIL) {
+      // ---- stage x on the x-pencil (y, z) = (tx, ty): kx -> qx, into buffer Xe [z][y][qx]
+      if (active) {
+#pragma unroll
+        for (int qx = 0; qx < Q1; ++qx) {
+          A s0 = A(0), s1 = A(0);
+#pragma unroll
+          for (int kx = 0; kx < N1; ++kx) {
+            s0 = fma(B(0, qx, kx), uc[0][kx], s0);
+            if (GRAD) s1 = fma(B(1, qx, kx), uc[0][kx], s1);
+          }
+          Xe[ty * Q2 + tx * Q1 + qx] = (T)s0;
+          if (GRAD) Xe[NQ + ty * Q2 + tx * Q1 + qx] = (T)s1;
+        }
+      }
+      __syncthreads();
+      // ---- stage y on the y-pencil (x, z) = (tx, ty): ky -> qy, into buffer Xf [z][qy][x]
+      if (active) {
+        A v0[N1], v1[N1];
+#pragma unroll
+        for (int ky = 0; ky < N1; ++ky) {
+          v0[ky] = (A)Xe[ty * Q2 + ky * Q1 + tx];
+          v1[ky] = GRAD ? (A)Xe[NQ + ty * Q2 + ky * Q1 + tx] : A(0);
+        }
+#pragma unroll
+        for (int qy = 0; qy < Q1; ++qy) {
+          A s00 = A(0), s01 = A(0), s10 = A(0);
+#pragma unroll
+          for (int ky = 0; ky < N1; ++ky) {
+            s00 = fma(B(0, qy, ky), v0[ky], s00);
+            if (GRAD) {
+              s01 = fma(B(1, qy, ky), v0[ky], s01);
+              s10 = fma(B(0, qy, ky), v1[ky], s10);
+            }
+          }
+          const int o = ty * Q2 + qy * Q1 + tx;
+          Xf[o] = (T)s00;
+          if (GRAD) {
+            Xf[NQ + o] = (T)s01;
+            Xf[2 * NQ + o] = (T)s10;
+          }
+        }
+      }
+      __syncthreads();
+      // ---- the z-column (x, y) = (tx, ty) of the three tensors
+#pragma unroll
+      for (int kz = 0; kz < N1; ++kz) {
+        const int o = kz * Q2 + ty * Q1 + tx;
+        c00[0][kz] = active ? (A)Xf[o] : A(0);
+        c01[0][kz] = (active && GRAD) ? (A)Xf[NQ + o] : A(0);
+        c10[0][kz] = (active && GRAD) ? (A)Xf[2 * NQ + o] : A(0);
+      }
+    } else {
     // ---- stage x: contract kx -> qx
     if (active) {
 #pragma unroll
@@ -361,7 +435,6 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
         }
     }
     __syncthreads();
-    A c00[D][N1], c01[D][N1], c10[D][N1];  // [kz] at (qx = tx, qy = ty)
 #pragma unroll
     for (int a = 0; a < D; ++a)
 #pragma unroll
@@ -381,6 +454,8 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
         c01[a][kz] = s01;
         c10[a][kz] = s10;
       }
+    }
+    if constexpr (PENCIL) load_mq();
     // ---- geometry constants of this column from the cell's vertex coordinates (staged in
     // smem before the first sync; vertex v = a + 2b + 4c at X[3 v + i]):
     // J[:,0] = (1-tZ) e0y[0] + tZ e0y[1], J[:,1] = (1-tZ) e1x[0] + tZ e1x[1], J[:,2] = col2
@@ -560,6 +635,74 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
         }
       }
     }
+    double ev = 0.0;  // eval mode: sum_k u_k r_k(u) of this column
+    if constexpr (PENCIL) {
+      // ---- H (z-column) into Xe [kz][qy][qx]; Xe was last read by stage y (before a barrier)
+      if (active) {
+#pragma unroll
+        for (int kz = 0; kz < N1; ++kz) {
+          const int o = kz * Q2 + ty * Q1 + tx;
+          Xe[o] = (T)Hv[0][kz];
+          if (BGRAD) {
+            Xe[NQ + o] = (T)Hx[0][kz];
+            Xe[2 * NQ + o] = (T)Hy[0][kz];
+          }
+        }
+      }
+      __syncthreads();
+      // ---- y^T on the y-pencil (x, kz) = (tx, ty): qy -> ky, into Xf [kz][ky][qx]
+      if (active) {
+        A hv[Q1], hx[Q1], hy[Q1];
+#pragma unroll
+        for (int qy = 0; qy < Q1; ++qy) {
+          const int o = ty * Q2 + qy * Q1 + tx;
+          hv[qy] = (A)Xe[o];
+          hx[qy] = BGRAD ? (A)Xe[NQ + o] : A(0);
+          hy[qy] = BGRAD ? (A)Xe[2 * NQ + o] : A(0);
+        }
+#pragma unroll
+        for (int ky = 0; ky < N1; ++ky) {
+          A sv = A(0), sx = A(0);
+#pragma unroll
+          for (int qy = 0; qy < Q1; ++qy) {
+            sv = fma(B(0, qy, ky), hv[qy], sv);
+            if (BGRAD) {
+              sv = fma(B(1, qy, ky), hy[qy], sv);
+              sx = fma(B(0, qy, ky), hx[qy], sx);
+            }
+          }
+          const int o = ty * Q2 + ky * Q1 + tx;
+          Xf[o] = (T)sv;
+          if (BGRAD) Xf[NQ + o] = (T)sx;
+        }
+      }
+      __syncthreads();
+      // ---- x^T on the x-pencil (ky, kz) = (tx, ty): qx -> kx, scatter
+      if (valid) {
+        A iv[Q1], ix[Q1];
+#pragma unroll
+        for (int qx = 0; qx < Q1; ++qx) {
+          const int o = ty * Q2 + tx * Q1 + qx;
+          iv[qx] = (A)Xf[o];
+          ix[qx] = BGRAD ? (A)Xf[NQ + o] : A(0);
+        }
+#pragma unroll
+        for (int kx = 0; kx < N1; ++kx) {
+          A sr = A(0);
+#pragma unroll
+          for (int qx = 0; qx < Q1; ++qx) {
+            sr = fma(B(0, qx, kx), iv[qx], sr);
+            if (BGRAD) sr = fma(B(1, qx, kx), ix[qx], sr);
+          }
+          const T v = (T)sr;
+          const int k = kx + N1 * tx + N1 * N1 * ty;
+          if (r_elem) r_elem[(e - e0) * (int64_t)NB + k] = v;
+          if (r_global) atomicAdd(r_global + (int64_t)dcol[kx], v);
+          if constexpr (PEER) peer_scatter<D>(pw, dcol[kx], 0, (double)v);
+          if (eval_out) ev = fma((double)sr, (double)u[dcol[kx]], ev);  // u re-read: uc is dead after stage x
+        }
+      }
+    } else {
     __syncthreads();  // everyone is done reading Xe (stage y)
     // ---- y^T: contract qy -> ky
     if (active) {
@@ -606,7 +749,6 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
         }
     }
     __syncthreads();
-    double ev = 0.0;  // eval mode: sum_k u_k r_k(u) of this column
     if (valid) {
 #pragma unroll
       for (int a = 0; a < D; ++a)
@@ -626,6 +768,7 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
           if constexpr (PEER) peer_scatter<D>(pw, dcol[kz], a, (double)v);
           if (eval_out) ev = fma((double)s, (double)uc[a][kz], ev);
         }
+    }
     }
     if (eval_out) {
 #pragma unroll
