@@ -131,7 +131,16 @@ struct RSF {
   static constexpr size_t SL_SIZE = (SL_MB + size_t(EB) * NQ * sizeof(T) + 16 + 15) / 16 * 16;
   static constexpr size_t OFF_X = (2 * Q1 * N1 * 8 + 15) / 16 * 16;
   static constexpr bool PENCIL = FEB200_RSF_PENCIL && D == 1 && P >= 3;
-  static constexpr size_t OFF_XV = (OFF_X + size_t(EB) * XS * (PENCIL ? 2 : 1) * sizeof(T) + 15) / 16 * 16;
+  // PENCIL transpose layouts (element offset x sx + y sy + z sz + cell * CS), chosen with a
+  // bank model of the stage accesses at p = 4, 5 cells per CTA: XY for the tensors written and
+  // read along x and y (stage x -> y, y^T -> x^T), YZ for those along y and z (stage y -> z,
+  // z^T -> y^T); at p = 3 the same strides are injective too
+  static constexpr int PSX = sizeof(T) == 8 ? 5 : 1, PSY = sizeof(T) == 8 ? 11 : 5, PSZ = 25;
+  static constexpr int CSXY = sizeof(T) == 8 ? 509 : 381;
+  static constexpr int PZY = 37, CSYZ = 569, PTS = 185;  // YZ: x + 5 y + 37 z, tensor stride
+  static constexpr int PTSXY = sizeof(T) == 8 ? 165 : 125;
+  static constexpr int PXS = CSXY > CSYZ ? CSXY : CSYZ;  // per-cell footprint of a buffer
+  static constexpr size_t OFF_XV = (OFF_X + size_t(EB) * (PENCIL ? 2 * PXS : XS) * sizeof(T) + 15) / 16 * 16;
   static constexpr int XVS = 28;  // per-cell stride of the staged vertex coordinates (bank spread)
   static constexpr size_t OFF_SLOT = OFF_XV + size_t(EB) * XVS * 8;
   static constexpr int NSLOT = 3;  // index/material ring: TMA two batches ahead
@@ -344,10 +353,17 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
     };
     if constexpr (!PENCIL) load_mq();  // PENCIL: loaded after the transposes (register pressure)
     T* Xe = X + el * L::XS;
-    T* Xf = X + (size_t)EB * L::XS + el * L::XS;  // PENCIL: the second transpose buffer
+    // PENCIL: buffers A (X) and B (X + EB PXS), each in layout XY or YZ per use
+    T* XaXY = X + el * L::CSXY;
+    T* XaYZ = X + el * L::CSYZ;
+    T* XbXY = X + (size_t)EB * L::PXS + el * L::CSXY;
+    T* XbYZ = X + (size_t)EB * L::PXS + el * L::CSYZ;
+    auto oXY = [](int x, int y, int z) { return x * L::PSX + y * L::PSY + z * L::PSZ; };
+    auto oYZ = [](int x, int y, int z) { return x + 5 * y + L::PZY * z; };
+    (void)XaXY; (void)XaYZ; (void)XbXY; (void)XbYZ; (void)oXY; (void)oYZ;
     A c00[D][N1], c01[D][N1], c10[D][N1];  // [kz] at (qx = tx, qy = ty)
     if constexpr (PENCIL) {
-      // ---- stage x on the x-pencil (y, z) = (tx, ty): kx -> qx, into buffer Xe [z][y][qx]
+      // ---- stage x on the x-pencil (y, z) = (tx, ty): kx -> qx, into buffer A (layout XY)
       if (active) {
 #pragma unroll
         for (int qx = 0; qx < Q1; ++qx) {
@@ -357,18 +373,18 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
             s0 = fma(B(0, qx, kx), uc[0][kx], s0);
             if (GRAD) s1 = fma(B(1, qx, kx), uc[0][kx], s1);
           }
-          Xe[ty * Q2 + tx * Q1 + qx] = (T)s0;
-          if (GRAD) Xe[NQ + ty * Q2 + tx * Q1 + qx] = (T)s1;
+          XaXY[oXY(qx, tx, ty)] = (T)s0;
+          if (GRAD) XaXY[L::PTSXY + oXY(qx, tx, ty)] = (T)s1;
         }
       }
       __syncthreads();
-      // ---- stage y on the y-pencil (x, z) = (tx, ty): ky -> qy, into buffer Xf [z][qy][x]
+      // ---- stage y on the y-pencil (x, z) = (tx, ty): ky -> qy, into buffer B (layout YZ)
       if (active) {
         A v0[N1], v1[N1];
 #pragma unroll
         for (int ky = 0; ky < N1; ++ky) {
-          v0[ky] = (A)Xe[ty * Q2 + ky * Q1 + tx];
-          v1[ky] = GRAD ? (A)Xe[NQ + ty * Q2 + ky * Q1 + tx] : A(0);
+          v0[ky] = (A)XaXY[oXY(tx, ky, ty)];
+          v1[ky] = GRAD ? (A)XaXY[L::PTSXY + oXY(tx, ky, ty)] : A(0);
         }
 #pragma unroll
         for (int qy = 0; qy < Q1; ++qy) {
@@ -381,11 +397,11 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
               s10 = fma(B(0, qy, ky), v1[ky], s10);
             }
           }
-          const int o = ty * Q2 + qy * Q1 + tx;
-          Xf[o] = (T)s00;
+          const int o = oYZ(tx, qy, ty);
+          XbYZ[o] = (T)s00;
           if (GRAD) {
-            Xf[NQ + o] = (T)s01;
-            Xf[2 * NQ + o] = (T)s10;
+            XbYZ[L::PTS + o] = (T)s01;
+            XbYZ[2 * L::PTS + o] = (T)s10;
           }
         }
       }
@@ -393,10 +409,10 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
       // ---- the z-column (x, y) = (tx, ty) of the three tensors
 #pragma unroll
       for (int kz = 0; kz < N1; ++kz) {
-        const int o = kz * Q2 + ty * Q1 + tx;
-        c00[0][kz] = active ? (A)Xf[o] : A(0);
-        c01[0][kz] = (active && GRAD) ? (A)Xf[NQ + o] : A(0);
-        c10[0][kz] = (active && GRAD) ? (A)Xf[2 * NQ + o] : A(0);
+        const int o = oYZ(tx, ty, kz);
+        c00[0][kz] = active ? (A)XbYZ[o] : A(0);
+        c01[0][kz] = (active && GRAD) ? (A)XbYZ[L::PTS + o] : A(0);
+        c10[0][kz] = (active && GRAD) ? (A)XbYZ[2 * L::PTS + o] : A(0);
       }
     } else {
     // ---- stage x: contract kx -> qx
@@ -637,28 +653,28 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
     }
     double ev = 0.0;  // eval mode: sum_k u_k r_k(u) of this column
     if constexpr (PENCIL) {
-      // ---- H (z-column) into Xe [kz][qy][qx]; Xe was last read by stage y (before a barrier)
+      // ---- H (z-column) into buffer A (layout YZ); A was last read by stage y (before a barrier)
       if (active) {
 #pragma unroll
         for (int kz = 0; kz < N1; ++kz) {
-          const int o = kz * Q2 + ty * Q1 + tx;
-          Xe[o] = (T)Hv[0][kz];
+          const int o = oYZ(tx, ty, kz);
+          XaYZ[o] = (T)Hv[0][kz];
           if (BGRAD) {
-            Xe[NQ + o] = (T)Hx[0][kz];
-            Xe[2 * NQ + o] = (T)Hy[0][kz];
+            XaYZ[L::PTS + o] = (T)Hx[0][kz];
+            XaYZ[2 * L::PTS + o] = (T)Hy[0][kz];
           }
         }
       }
       __syncthreads();
-      // ---- y^T on the y-pencil (x, kz) = (tx, ty): qy -> ky, into Xf [kz][ky][qx]
+      // ---- y^T on the y-pencil (x, kz) = (tx, ty): qy -> ky, into buffer B (layout XY)
       if (active) {
         A hv[Q1], hx[Q1], hy[Q1];
 #pragma unroll
         for (int qy = 0; qy < Q1; ++qy) {
-          const int o = ty * Q2 + qy * Q1 + tx;
-          hv[qy] = (A)Xe[o];
-          hx[qy] = BGRAD ? (A)Xe[NQ + o] : A(0);
-          hy[qy] = BGRAD ? (A)Xe[2 * NQ + o] : A(0);
+          const int o = oYZ(tx, qy, ty);
+          hv[qy] = (A)XaYZ[o];
+          hx[qy] = BGRAD ? (A)XaYZ[L::PTS + o] : A(0);
+          hy[qy] = BGRAD ? (A)XaYZ[2 * L::PTS + o] : A(0);
         }
 #pragma unroll
         for (int ky = 0; ky < N1; ++ky) {
@@ -671,9 +687,9 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
               sx = fma(B(0, qy, ky), hx[qy], sx);
             }
           }
-          const int o = ty * Q2 + ky * Q1 + tx;
-          Xf[o] = (T)sv;
-          if (BGRAD) Xf[NQ + o] = (T)sx;
+          const int o = oXY(tx, ky, ty);
+          XbXY[o] = (T)sv;
+          if (BGRAD) XbXY[L::PTSXY + o] = (T)sx;
         }
       }
       __syncthreads();
@@ -682,9 +698,9 @@ __global__ void __launch_bounds__(RSF<P, FORM, T>::THREADS, RSF<P, FORM, T>::MIN
         A iv[Q1], ix[Q1];
 #pragma unroll
         for (int qx = 0; qx < Q1; ++qx) {
-          const int o = ty * Q2 + tx * Q1 + qx;
-          iv[qx] = (A)Xf[o];
-          ix[qx] = BGRAD ? (A)Xf[NQ + o] : A(0);
+          const int o = oXY(qx, tx, ty);
+          iv[qx] = (A)XbXY[o];
+          ix[qx] = BGRAD ? (A)XbXY[L::PTSXY + o] : A(0);
         }
 #pragma unroll
         for (int kx = 0; kx < N1; ++kx) {
