@@ -13,7 +13,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 cap "k_matrix_sfp" C2_matrix --config C2
 cap "k_residual_t3" C2_residual --config C2
 cap "k_matrix_vp" C3_matrix --config C3
-cap "k_residual_sf" C3_residual --config C3
+cap "k_residual_t3e" C3_residual --config C3
 cap "k_residual_sf" C4_residual_f64 --config C4
 cap "k_residual_sf" C4_residual_f32 --config C4 --dtype f32
 cap "k_residual_t3c" C5_residual --config C5
