@@ -58,6 +58,9 @@
 #ifndef FEB200_VP_YB3
 #define FEB200_VP_YB3 0
 #endif
+#ifndef FEB200_VP_NOSTORE
+#define FEB200_VP_NOSTORE 0
+#endif
 #ifndef FEB200_VP_YB3MAP
 #define FEB200_VP_YB3MAP 1
 #endif
@@ -354,7 +357,8 @@ __global__ void __launch_bounds__(VPL<P, FORM, FD>::THREADS, VPL<P, FORM, FD>::M
       VP_T(6, vp_wait(kfull, (uint32_t)(j & 1)));
       const uint32_t bytes = (uint32_t)((size_t)nej * NDOF * NDOF * 8);
       double* gdst = K + lbj * NDOF * NDOF;
-      if (((reinterpret_cast<uintptr_t>(gdst) | bytes) & 15u) == 0) {
+      if (FEB200_VP_NOSTORE) {  // experiment: K is not stored (the cost of the store path)
+      } else if (((reinterpret_cast<uintptr_t>(gdst) | bytes) & 15u) == 0) {
         if (lane == 0) {
           asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                        :: "l"(gdst), "r"(vp_u32(Kst)), "r"(bytes) : "memory");
