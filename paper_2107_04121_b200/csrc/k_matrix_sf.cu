@@ -46,6 +46,9 @@
 #ifndef FEB200_SFP_YB
 #define FEB200_SFP_YB 3  // y pairs per X thread at p = 2 (1 or 3)
 #endif
+#ifndef FEB200_SFP_ZTRI
+#define FEB200_SFP_ZTRI 1  // stage z: only z pairs iz <= jz for the pairs m == n
+#endif
 #ifndef FEB200_SFP_MAP
 #define FEB200_SFP_MAP 1  // YB = 3: generated lane -> task permutation (sfp_tasks.h)
 #endif
@@ -812,6 +815,9 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
           for (int a = 0; a < N1; ++a)
 #pragma unroll
             for (int bb = 0; bb < N1; ++bb) {
+              // pairs m == n: X reads T1 only at z pairs iz <= jz (the unique pair's vector
+              // serves both orders), so the lower entries are not formed
+              if (FEB200_SFP_ZTRI && m == n && a > bb) continue;
               double sacc = 0.0;
 #pragma unroll
               for (int qz = 0; qz < Q1; ++qz) sacc = fma(Wr[ul][qz], c_zz[P][az][bz][qz][a][bb], sacc);
