@@ -55,6 +55,9 @@
 #ifndef FEB200_SF_MINB
 #define FEB200_SF_MINB 1
 #endif
+#ifndef FEB200_SFP_EVF
+#define FEB200_SFP_EVF 0  // experiment: L2 evict_first hint on the K bulk stores (C2 +0.3 %: off)
+#endif
 #include "fe_const.cuh"
 #include "fe_device.cuh"
 #include "fe_internal.h"
@@ -404,7 +407,12 @@ __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_D
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
       if (tid == 0) {
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+        if (FEB200_SFP_EVF) {
+          uint64_t pol_;
+          asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_));
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                     :: "l"(gdst), "r"(smem_u32(Kst)), "r"(bytes), "l"(pol_) : "memory");
+        } else asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                      :: "l"(gdst), "r"(smem_u32(Kst)), "r"(bytes) : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
@@ -993,7 +1001,12 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
       if (FEB200_SFP_NOSTORE) {
       } else if (((reinterpret_cast<uintptr_t>(gdst) | bytes) & 15u) == 0) {
         if (xtid == 0) {
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+          if (FEB200_SFP_EVF) {
+          uint64_t pol_;
+          asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_));
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                       :: "l"(gdst), "r"(smem_u32(Kst)), "r"(bytes), "l"(pol_) : "memory");
+        } else asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                        :: "l"(gdst), "r"(smem_u32(Kst)), "r"(bytes) : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -1199,7 +1212,12 @@ __global__ void __launch_bounds__(SFP<P, (FORM != FE_FORM_MASS ? 6 : 0) + (FORM 
       if (FEB200_SFP_NOSTORE) {
       } else if (((reinterpret_cast<uintptr_t>(gdst) | bytes) & 15u) == 0) {
         if (xtid == 0) {
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+          if (FEB200_SFP_EVF) {
+          uint64_t pol_;
+          asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_));
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                       :: "l"(gdst), "r"(smem_u32(Kst)), "r"(bytes), "l"(pol_) : "memory");
+        } else asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                        :: "l"(gdst), "r"(smem_u32(Kst)), "r"(bytes) : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
