@@ -980,9 +980,27 @@ def main():
             tt = torch.tensor([h2d, d2h], device=dev, dtype=torch.float64)
             dist.all_reduce(tt)
             h2d, d2h = int(tt[0]), int(tt[1])
+        # the PCIe roofline of this leg: the same read-back as one plain D2H copy of this rank's
+        # biggest result buffer (best of 3), timed after the e2e region
+        link = None
+        hb, db = (h_K, Kbuf[0]) if h_K is not None else (h_r, r)
+        if hb.numel() * hb.element_size() >= (64 << 20):
+            la, lb_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            best = float("inf")
+            for _ in range(3):
+                la.record(st)
+                hb.copy_(db, non_blocking=True)
+                lb_.record(st)
+                torch.cuda.synchronize(dev)
+                best = min(best, la.elapsed_time(lb_))
+            peak = hb.numel() * hb.element_size() / (best * 1e-3) / 1e9
+            ach = d2h / world / (e_ms / n_e2e * 1e-3) / 1e9
+            link = {"bound": "pcie_d2h", "achieved_gbs": ach, "peak_gbs": peak, "frac": ach / peak,
+                    "note": "achieved = D2H bytes per step per rank / e2e step time; peak = one "
+                            "plain pinned D2H copy of the largest result buffer on this box"}
         e2e = {"value": prob.n_elems / (e_ms / n_e2e * 1e-3), "unit": "cells/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": e_ms / n_e2e, "steps": n_e2e,
+               "ms_per_step": e_ms / n_e2e, "steps": n_e2e, "link": link,
                "note": "every step: pinned host inputs (u, material) H2D, the step, D2H of r"
                        + (" and K" if K is not None else "") + "; the read-back of a step overlaps "
                        "the next step (copy stream, two device K buffers)"}
