@@ -464,6 +464,9 @@ class Runner:
         self.bev = torch.cuda.Event()   # boundary -> exchange dependency (preallocated)
         self.side = (torch.cuda.Stream(dev) if "matrix" in self.modes and "residual" in self.modes
                      and not self.fused and self.peer is None else None)
+        # C2 step (B200, graph replay): forking the residual branch before the matrix kernel
+        # 0.4876 -> 0.4804 ms (eager 0.5067 -> 0.4884); FEB200_BENCH_FORK=late forks after it
+        self.fork_early = os.environ.get("FEB200_BENCH_FORK", "early") == "early"
 
     def events(self, n):
         """Preallocated kernel events: rec[i][mode] = (start, end) for step i."""
@@ -493,6 +496,12 @@ class Runner:
             if rec:
                 rec["matrix+residual"][1].record(st)
             return
+        early = self.side is not None and self.fork_early
+        if early:
+            # the residual branch depends only on the step's inputs, not on K: fork it before
+            # the matrix kernel, so that its zeroing runs beside the matrix kernel and its CTAs
+            # take the SMs the matrix kernel's tail frees
+            self.side.wait_stream(st)
         if "matrix" in self.modes:
             if rec:
                 rec["matrix"][0].record(st)
@@ -521,11 +530,11 @@ class Runner:
             if rec:
                 rec["residual"][1].record(st)
         elif "residual" in self.modes:
-            # matrix + residual steps: the residual runs on a side stream forked after the
-            # matrix kernel was queued, so its CTAs fill the SMs the matrix kernel's tail frees
-            # (C2: 0.550 -> 0.542 ms); the current stream joins it at the end of the step
+            # matrix + residual steps: the residual runs on a side stream (forked before the
+            # matrix kernel by default, see fork_early; else after it was queued); the current
+            # stream joins it at the end of the step
             side = self.side
-            if side is not None:
+            if side is not None and not early:
                 side.wait_stream(st)
             with self.torch.cuda.stream(side if side is not None else st):
                 rst = self.torch.cuda.current_stream(self.dev)
@@ -654,9 +663,16 @@ def timed_run(run, steps, warmup, world, local_rank, window_s=1.2, graph=False):
         run.step()
         launches = (fe.fe_launch_count() - n0) * steps
         _barrier(torch, dist, world, local_rank, dev)
+    early = getattr(run, "fork_early", False)
+    if graph or early:
+        # per-kernel times from an eager pass after the timed region, each kernel on its own:
+        # with the early fork the residual's events would span the matrix kernel it waits
+        # behind, so this pass runs the step with the two kernels serialised
+        run.fork_early = False
         for i in range(steps):
             run.step(rec[i])
         _barrier(torch, dist, world, local_rank, dev)
+        run.fork_early = early
     if flush:
         per_step = [ev_beg[i].elapsed_time(ev_step[i + 1]) for i in range(steps)]
         total = float(sum(per_step))
@@ -1007,6 +1023,7 @@ def main():
         run.K = K
         del h_K, Kbuf
     launches = int(res["launches"])
+    fork_early, has_side = run.fork_early, run.side is not None
     run.close()
     del run, mesh, K, r, u
     torch.cuda.synchronize(dev)
@@ -1055,6 +1072,7 @@ def main():
         "untimed_repeats": res["untimed_repeats"],
         "graph": bool(res["graph"]),
         "graph_error": res["graph_error"],
+        "residual_fork": ("early" if fork_early else "late") if has_side else None,
         "l2_flush": res["l2_flush"],
         "host_us_per_step": res["host_us_per_step"],
         "configs": subs,
