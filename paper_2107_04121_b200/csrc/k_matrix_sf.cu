@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(SFM<P, FORM != FE_FORM_MASS, FORM != FE_FORM_D
     // E. write the batch: one TMA bulk store of ne * NB^2 doubles (contiguous in K)
     const uint32_t bytes = (uint32_t)ne * NB * NB * 8;
     double* gdst = K + lb * NB * NB;
-    if ((bytes & 15u) == 0) {
+    if (((reinterpret_cast<uintptr_t>(gdst) | bytes) & 15u) == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
       if (tid == 0) {

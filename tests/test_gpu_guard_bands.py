@@ -1,0 +1,239 @@
+"""Guard-band checks of every C-ABI call that writes device memory.
+
+compute-sanitizer is not available on the GPU pool, so the out-of-bounds checks are built into
+the tests: every output is a view into the middle of a larger buffer filled with a fixed NaN
+bit pattern, every input (u, material arrays) sits between NaN guard bands, and an element
+sub-range [lo, hi) with odd bounds is evaluated.  After each call
+
+* the guard bands of the outputs are bitwise intact (no write outside [lo, hi) / the view),
+* the view equals the oracle's rows lo..hi (tolerances of test_gpu_parity.py): a kernel that
+  used an input it fetched from outside the arrays (the kernels fetch 16-B-aligned enclosing
+  ranges) would carry the guard NaN into its result.
+
+The offsets of the views are chosen so that both the 16-B-aligned (bulk-store, vector) and the
+8-B-aligned (fallback) code paths run, with the grid capped to 2 CTAs (several batches per CTA
+and a ragged tail) and uncapped.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import fe_inputs as fi
+import oracle
+from test_gpu_parity import TOL32, TOL64, _dense_global, fe, gpu_mesh, rel
+
+pytestmark = pytest.mark.gpu
+
+SENT = 0x7FF8DEADBEEF1234          # a quiet NaN with a payload no kernel produces
+SENT32 = 0x7FC0BEEF
+GUARD = 257                        # guard-band length in values on each side
+
+
+class Banded:
+    """A view of `shape` starting `off` values into a sentinel-filled flat buffer."""
+
+    def __init__(self, shape, off, dtype=torch.float64, fill=None):
+        n = int(np.prod(shape))
+        it = torch.int64 if dtype == torch.float64 else torch.int32
+        self.bits = torch.full((off + n + GUARD,), SENT if dtype == torch.float64 else SENT32,
+                               dtype=it, device="cuda")
+        self.flat = self.bits.view(dtype)
+        self.off, self.n = off, n
+        self.view = self.flat[off:off + n].view(shape)
+        if fill is not None:
+            self.view.copy_(fill)
+        self.sent = SENT if dtype == torch.float64 else SENT32
+
+    def intact(self):
+        lo = self.bits[:self.off]
+        hi = self.bits[self.off + self.n:]
+        return bool((lo == self.sent).all()) and bool((hi == self.sent).all())
+
+    def rows_untouched(self, a, b):
+        """rows [a, b) of the view (first axis) still hold the sentinel"""
+        it = self.bits.dtype
+        return bool((self.view[a:b].contiguous().view(it) == self.sent).all())
+
+
+def banded_input(a, off, dtype=torch.float64):
+    if a is None:
+        return None
+    t = torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dtype)
+    return Banded(t.shape, off, dtype, fill=t).view
+
+
+CASES = [(f, p) for f in (0, 1, 2, 3, 4, 5) for p in (1, 2)] + [(0, 3), (3, 4), (2, 3), (5, 4)]
+
+
+@pytest.mark.parametrize("cap", [0, 2])
+@pytest.mark.parametrize("off", [GUARD - 1, GUARD])      # 16-B aligned / 8-B aligned views
+@pytest.mark.parametrize("form,p", CASES)
+def test_residual_guard_bands(form, p, off, cap, fe_opts):
+    fe_opts(max_ctas=cap)
+    pr = fi.make_problem(form, p, (5, 3, 4), 21000 + 7 * form + p)
+    mesh = gpu_mesh(pr)
+    E, nd = pr.n_elems, pr.ncomp * pr.nb
+    lo, hi = 3, E - 2
+    mat = (pr.mat_kind, banded_input(pr.mat_a, off), banded_input(pr.mat_b, off))
+    u = banded_input(pr.u, off)
+    re = Banded((hi - lo, nd), off)
+    rg = Banded((pr.n_nodes, pr.ncomp), off)
+    rg.view.zero_()
+    mesh.residual(form, u, *mat, elem_begin=lo, elem_end=hi, r_elem=re.view, r_global=rg.view)
+    torch.cuda.synchronize()
+    assert re.intact() and rg.intact()
+    r_ref = oracle.problem_residual(pr)
+    assert rel(re.view.cpu().numpy(), r_ref[lo:hi]) <= TOL64
+    R_ref = oracle.assemble(r_ref[lo:hi], pr.dof_conn[lo:hi], pr.n_nodes, pr.ncomp)
+    assert rel(rg.view.cpu().numpy().ravel(), R_ref) <= TOL64
+    # fe_assemble_vector on its own (r_elem holds the rows of the range [lo, hi))
+    ra = Banded((pr.n_nodes, pr.ncomp), off)
+    ra.view.zero_()
+    rin = banded_input(r_ref[lo:hi], off)
+    mesh.assemble(rin, pr.ncomp, r_global=ra.view, elem_begin=lo, elem_end=hi)
+    torch.cuda.synchronize()
+    assert ra.intact()
+    assert rel(ra.view.cpu().numpy().ravel(), R_ref) <= TOL64
+
+
+@pytest.mark.parametrize("off", [GUARD - 1, GUARD])
+@pytest.mark.parametrize("form,p", [(3, 4), (0, 2), (1, 2), (0, 1)])
+def test_residual_fp32_guard_bands(form, p, off):
+    pr = fi.make_problem(form, p, (5, 3, 4), 22000 + form)
+    mesh = gpu_mesh(pr)
+    E, nd = pr.n_elems, pr.ncomp * pr.nb
+    lo, hi = 3, E - 2
+    f32 = torch.float32
+    mat = (pr.mat_kind, banded_input(pr.mat_a, off, f32), banded_input(pr.mat_b, off, f32))
+    re = Banded((hi - lo, nd), off, f32)
+    rg = Banded((pr.n_nodes, pr.ncomp), off, f32)
+    rg.view.zero_()
+    mesh.residual(form, banded_input(pr.u, off, f32), *mat, elem_begin=lo, elem_end=hi,
+                  r_elem=re.view, r_global=rg.view)
+    torch.cuda.synchronize()
+    assert re.intact() and rg.intact()
+    r_ref = oracle.problem_residual(pr)
+    assert rel(re.view.cpu().numpy(), r_ref[lo:hi]) <= TOL32
+    R_ref = oracle.assemble(r_ref[lo:hi], pr.dof_conn[lo:hi], pr.n_nodes, pr.ncomp)
+    assert rel(rg.view.cpu().numpy().ravel(), R_ref) <= TOL32
+
+
+MATRIX_CASES = [(f, p) for f in (0, 1, 2, 3, 4, 5) for p in (1, 2)] + [(0, 3), (3, 3), (2, 3)]
+
+
+@pytest.mark.parametrize("cap", [0, 2])
+@pytest.mark.parametrize("off", [GUARD - 1, GUARD])
+@pytest.mark.parametrize("form,p", MATRIX_CASES)
+def test_matrix_guard_bands(form, p, off, cap, fe_opts):
+    fe_opts(max_ctas=cap)
+    pr = fi.make_problem(form, p, (5, 3, 4), 23000 + 7 * form + p)
+    mesh = gpu_mesh(pr)
+    E, nd = pr.n_elems, pr.ncomp * pr.nb
+    lo, hi = 3, E - 2
+    mat = (pr.mat_kind, banded_input(pr.mat_a, off), banded_input(pr.mat_b, off))
+    su = banded_input(pr.u, off) if form == fi.CONVECTIVE else None
+    # the whole-mesh K buffer: rows outside [lo, hi) must stay untouched as well
+    K = Banded((E, nd, nd), off)
+    mesh.element_matrices(form, *mat, su, elem_begin=lo, elem_end=hi, out=K.view[lo:hi])
+    torch.cuda.synchronize()
+    assert K.intact()
+    assert K.rows_untouched(0, lo) and K.rows_untouched(hi, E)
+    Kref = oracle.problem_matrix(pr)
+    assert rel(K.view[lo:hi].cpu().numpy(), Kref[lo:hi]) <= TOL64
+
+
+@pytest.mark.parametrize("off", [GUARD - 1, GUARD])
+@pytest.mark.parametrize("form,p", [(0, 1), (0, 2), (1, 2), (3, 2)])
+def test_matrix_fp32_guard_bands(form, p, off):
+    pr = fi.make_problem(form, p, (5, 3, 4), 24000 + form)
+    mesh = gpu_mesh(pr)
+    E, nd = pr.n_elems, pr.ncomp * pr.nb
+    lo, hi = 3, E - 2
+    f32 = torch.float32
+    mat = (pr.mat_kind, banded_input(pr.mat_a, off, f32), banded_input(pr.mat_b, off, f32))
+    K = Banded((E, nd, nd), off, f32)
+    mesh.element_matrices(form, *mat, None, elem_begin=lo, elem_end=hi, out=K.view[lo:hi])
+    torch.cuda.synchronize()
+    assert K.intact() and K.rows_untouched(0, lo) and K.rows_untouched(hi, E)
+    assert rel(K.view[lo:hi].cpu().numpy(), oracle.problem_matrix(pr)[lo:hi]) <= TOL32
+
+
+@pytest.mark.parametrize("cap", [0, 2])
+@pytest.mark.parametrize("off", [GUARD - 1, GUARD])
+@pytest.mark.parametrize("form,p", [(0, 1), (0, 2), (1, 2), (3, 2)])
+def test_fused_matrix_residual_guard_bands(form, p, off, cap, fe_opts):
+    fe_opts(max_ctas=cap)
+    pr = fi.make_problem(form, p, (5, 3, 4), 25000 + form)
+    mesh = gpu_mesh(pr)
+    E, nd = pr.n_elems, pr.nb
+    lo, hi = 3, E - 2
+    mat = (pr.mat_kind, banded_input(pr.mat_a, off), banded_input(pr.mat_b, off))
+    K = Banded((hi - lo, nd, nd), off)
+    re = Banded((hi - lo, nd), off)
+    rg = Banded((pr.n_nodes, 1), off)
+    rg.view.zero_()
+    mesh.matrix_residual(form, banded_input(pr.u, off), *mat, elem_begin=lo, elem_end=hi,
+                         K=K.view, r_elem=re.view, r_global=rg.view)
+    torch.cuda.synchronize()
+    assert K.intact() and re.intact() and rg.intact()
+    assert rel(K.view.cpu().numpy(), oracle.problem_matrix(pr)[lo:hi]) <= TOL64
+    r_ref = oracle.problem_residual(pr)
+    assert rel(re.view.cpu().numpy(), r_ref[lo:hi]) <= TOL64
+    R_ref = oracle.assemble(r_ref[lo:hi], pr.dof_conn[lo:hi], pr.n_nodes, 1)
+    assert rel(rg.view.cpu().numpy().ravel(), R_ref) <= TOL64
+
+
+@pytest.mark.parametrize("off", [GUARD - 1, GUARD])
+@pytest.mark.parametrize("p", [1, 2, 4])
+def test_geometry_stress_guard_bands(p, off):
+    m = fe()
+    pr = fi.make_problem(fi.ELASTICITY, p, (4, 3, 2), 26000 + p)
+    mesh = gpu_mesh(pr)
+    E, nq = pr.n_elems, (p + 1) ** 3
+    detw, jinv = Banded((E, nq), off), Banded((E, nq, 3, 3), off)
+    m.fe_geometry(mesh.handle, detw.view, jinv.view)
+    torch.cuda.synchronize()
+    assert detw.intact() and jinv.intact()
+    detw_ref, jinv_ref = oracle.geometry(p + 1, pr.coords, pr.conn)
+    assert rel(detw.view.cpu().numpy(), detw_ref) <= TOL64
+    assert rel(jinv.view.cpu().numpy(), jinv_ref) <= TOL64
+    if p > 2:
+        return
+    lo, hi = 3, E - 2
+    mat = (pr.mat_kind, banded_input(pr.mat_a, off), banded_input(pr.mat_b, off))
+    u = banded_input(pr.u, off)
+    sig, sint = Banded((hi - lo, nq, 6), off), Banded((hi - lo, 6), off)
+    m.fe_eval_stress(mesh.handle, *mat, u, lo, hi, sig.view)
+    m.fe_eval_stress_integral(mesh.handle, *mat, u, lo, hi, sint.view)
+    torch.cuda.synchronize()
+    assert sig.intact() and sint.intact()
+    assert rel(sig.view.cpu().numpy(), oracle.problem_stress(pr)[lo:hi]) <= TOL64
+    ref_i = oracle.eval_stress_integral(p, p + 1, pr.coords, pr.conn, pr.dof_conn, pr.u,
+                                        pr.mat_kind, pr.mat_a, pr.mat_b)
+    assert rel(sint.view.cpu().numpy(), ref_i[lo:hi]) <= TOL64
+
+
+@pytest.mark.parametrize("impl", ["atomic", "gather"])
+@pytest.mark.parametrize("off", [GUARD - 1, GUARD])
+@pytest.mark.parametrize("form,p", [(0, 1), (0, 2), (2, 1), (2, 2)])
+def test_csr_guard_bands(form, p, off, impl, fe_opts):
+    import scipy.sparse as sp
+    fe_opts(csr_impl=impl)
+    m = fe()
+    pr = fi.make_problem(form, p, (3, 2, 3), 27000 + form)
+    mesh = gpu_mesh(pr)
+    Kref = oracle.problem_matrix(pr)
+    K = banded_input(Kref, off)
+    csr = m.CSR(mesh, pr.ncomp)
+    vals = Banded((csr.nnz,), off)
+    vals.view.zero_()
+    csr.assemble(K, values=vals.view)
+    torch.cuda.synchronize()
+    assert vals.intact()
+    rp, ci = csr.arrays()
+    A = sp.csr_matrix((vals.view.cpu().numpy(), ci, rp), shape=(csr.n_rows, csr.n_rows)).toarray()
+    Aref = _dense_global(pr, Kref)
+    assert rel(A, Aref) <= TOL64
+    csr.close()
