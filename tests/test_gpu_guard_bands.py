@@ -237,3 +237,137 @@ def test_csr_guard_bands(form, p, off, impl, fe_opts):
     Aref = _dense_global(pr, Kref)
     assert rel(A, Aref) <= TOL64
     csr.close()
+
+
+# ---- the non-default implementations, the remaining forms and material kinds ----------------
+
+@pytest.mark.parametrize("off", [GUARD - 1, GUARD])
+@pytest.mark.parametrize("impl", ["sf1", "dense"])
+@pytest.mark.parametrize("form,p", [(0, 1), (0, 2), (3, 2), (4, 1), (4, 2), (5, 2), (2, 2), (4, 3)])
+def test_matrix_impl_guard_bands(form, p, impl, off, fe_opts):
+    fe_opts(matrix_impl=impl, max_ctas=2)
+    pr = fi.make_problem(form, p, (5, 3, 4), 28000 + 7 * form + p)
+    mesh = gpu_mesh(pr)
+    E, nd = pr.n_elems, pr.ncomp * pr.nb
+    lo, hi = 3, E - 2
+    mat = (pr.mat_kind, banded_input(pr.mat_a, off), banded_input(pr.mat_b, off))
+    su = banded_input(pr.u, off) if form == fi.CONVECTIVE else None
+    K = Banded((E, nd, nd), off)
+    mesh.element_matrices(form, *mat, su, elem_begin=lo, elem_end=hi, out=K.view[lo:hi])
+    torch.cuda.synchronize()
+    assert K.intact() and K.rows_untouched(0, lo) and K.rows_untouched(hi, E)
+    assert rel(K.view[lo:hi].cpu().numpy(), oracle.problem_matrix(pr)[lo:hi]) <= TOL64
+
+
+@pytest.mark.parametrize("off", [GUARD - 1, GUARD])
+@pytest.mark.parametrize("impl", ["sf", "dense"])
+@pytest.mark.parametrize("form,p", [(0, 1), (0, 2), (3, 2), (4, 2), (5, 2), (3, 4), (4, 3),
+                                    (fi.WEIGHTED_DOT, 2), (fi.DIVERGENCE, 2), (fi.WEIGHTED_DOT, 4)])
+def test_residual_impl_guard_bands(form, p, impl, off, fe_opts):
+    fe_opts(residual_impl=impl, max_ctas=2)
+    pr = fi.make_problem(form, p, (5, 3, 4), 29000 + 7 * form + p)
+    mesh = gpu_mesh(pr)
+    E, nd = pr.n_elems, pr.ncomp * pr.nb
+    lo, hi = 3, E - 2
+    mat = (pr.mat_kind, banded_input(pr.mat_a, off), banded_input(pr.mat_b, off))
+    re = Banded((hi - lo, nd), off)
+    rg = Banded((pr.n_nodes, pr.ncomp), off)
+    rg.view.zero_()
+    mesh.residual(form, banded_input(pr.u, off), *mat, elem_begin=lo, elem_end=hi,
+                  r_elem=re.view, r_global=rg.view)
+    torch.cuda.synchronize()
+    assert re.intact() and rg.intact()
+    r_ref = oracle.problem_residual(pr)
+    assert rel(re.view.cpu().numpy(), r_ref[lo:hi]) <= TOL64
+    R_ref = oracle.assemble(r_ref[lo:hi], pr.dof_conn[lo:hi], pr.n_nodes, pr.ncomp)
+    assert rel(rg.view.cpu().numpy().ravel(), R_ref) <= TOL64
+
+
+@pytest.mark.parametrize("cap", [0, 2])
+@pytest.mark.parametrize("off", [GUARD - 1, GUARD])
+@pytest.mark.parametrize("kind", [fi.MAT_PER_QP, fi.MAT_PER_ELEM, fi.MAT_FULL_D])
+@pytest.mark.parametrize("p", [1, 2])
+def test_elasticity_kinds_guard_bands(p, kind, off, cap, fe_opts):
+    """Every material layout of the elasticity form (lambda, mu per qp / per cell, D[6][6] per
+    qp), matrix and residual mode, plus the weighted dot 'ij,i,j' matrix."""
+    fe_opts(max_ctas=cap)
+    pr = fi.make_problem(fi.ELASTICITY, p, (5, 3, 4), 30000 + 10 * p + kind, mat_kind=kind)
+    mesh = gpu_mesh(pr)
+    E, nd = pr.n_elems, 3 * pr.nb
+    lo, hi = 3, E - 2
+    mat = (kind, banded_input(pr.mat_a, off), banded_input(pr.mat_b, off))
+    K = Banded((E, nd, nd), off)
+    mesh.element_matrices(fi.ELASTICITY, *mat, None, elem_begin=lo, elem_end=hi, out=K.view[lo:hi])
+    re = Banded((hi - lo, nd), off)
+    mesh.residual(fi.ELASTICITY, banded_input(pr.u, off), *mat, elem_begin=lo, elem_end=hi,
+                  r_elem=re.view, want_global=False)
+    torch.cuda.synchronize()
+    assert K.intact() and K.rows_untouched(0, lo) and K.rows_untouched(hi, E) and re.intact()
+    assert rel(K.view[lo:hi].cpu().numpy(), oracle.problem_matrix(pr)[lo:hi]) <= TOL64
+    assert rel(re.view.cpu().numpy(), oracle.problem_residual(pr)[lo:hi]) <= TOL64
+    wd = fi.make_problem(fi.WEIGHTED_DOT, p, (5, 3, 4), 31000 + p)
+    mesh2 = gpu_mesh(wd)
+    K2 = Banded((E, nd, nd), off)
+    mesh2.element_matrices(fi.WEIGHTED_DOT, wd.mat_kind, banded_input(wd.mat_a, off), None, None,
+                           elem_begin=lo, elem_end=hi, out=K2.view[lo:hi])
+    torch.cuda.synchronize()
+    assert K2.intact() and K2.rows_untouched(0, lo) and K2.rows_untouched(hi, E)
+    assert rel(K2.view[lo:hi].cpu().numpy(), oracle.problem_matrix(wd)[lo:hi]) <= TOL64
+
+
+@pytest.mark.parametrize("off", [GUARD - 1, GUARD])
+@pytest.mark.parametrize("pv,pp", [(2, 1), (1, 1), (3, 2)])
+def test_stokes_coupling_guard_bands(pv, pp, off):
+    m = fe()
+    shape = (5, 3, 4) if pv <= 2 else (3, 2, 3)
+    mp = fi.make_mixed_problem(pv, pp, shape, 32000 + 10 * pv + pp)
+    v = mp.vel
+    mesh = gpu_mesh(v)
+    pf = m.PressureField(mesh, pp, torch.from_numpy(mp.p_dof_conn), n_nodes=mp.n_p_nodes)
+    E = v.n_elems
+    lo, hi = 3, E - 2
+    args = (pv, pp, pv + 1, v.coords, v.conn)
+    for tr in (False, True):
+        shape_k = (pf.nb, 3 * mesh.nb) if tr else (3 * mesh.nb, pf.nb)
+        B = Banded((E,) + shape_k, off)
+        pf.coupling_matrices(transposed=tr, elem_begin=lo, elem_end=hi, out=B.view[lo:hi])
+        torch.cuda.synchronize()
+        assert B.intact() and B.rows_untouched(0, lo) and B.rows_untouched(hi, E)
+        ref = oracle.coupling_matrix(*args, transposed=tr)
+        assert rel(B.view[lo:hi].cpu().numpy(), ref[lo:hi]) <= TOL64
+    # r_v = B p (velocity-shaped) and r_q = C u (pressure-shaped), element rows + fused scatter
+    rv_ref = oracle.coupling_residual(*args, v.dof_conn, mp.p_dof_conn, p=mp.pres)
+    rq_ref = oracle.coupling_residual(*args, v.dof_conn, mp.p_dof_conn, u=v.u, transposed=True)
+    for tr, x, ref, conn, nn, D in ((False, mp.pres, rv_ref, v.dof_conn, v.n_nodes, 3),
+                                    (True, v.u, rq_ref, mp.p_dof_conn, mp.n_p_nodes, 1)):
+        re = Banded((hi - lo, ref.shape[1]), off)
+        rg = Banded((nn, 3) if not tr else (nn,), off)
+        rg.view.zero_()
+        pf.coupling_residual(banded_input(x, off), transposed=tr, elem_begin=lo, elem_end=hi,
+                             r_elem=re.view, r_global=rg.view)
+        torch.cuda.synchronize()
+        assert re.intact() and rg.intact()
+        assert rel(re.view.cpu().numpy(), ref[lo:hi]) <= TOL64
+        assert rel(rg.view.cpu().numpy().ravel(),
+                   oracle.assemble(ref[lo:hi], conn[lo:hi], nn, D)) <= TOL64
+    pf.close()
+
+
+@pytest.mark.parametrize("off", [GUARD - 1, GUARD])
+def test_eval_scalar_guard_bands(off):
+    """Eval mode adds into one fp64 value: its neighbours stay untouched."""
+    m = fe()
+    for form, p in ((fi.DIFFUSION, 2), (fi.ELASTICITY, 2), (fi.MASS_DIFFUSION, 4), (fi.CONVECTIVE, 2)):
+        pr = fi.make_problem(form, p, (4, 3, 3), 33000 + form)
+        mesh = gpu_mesh(pr)
+        val = Banded((1,), off)
+        val.view.zero_()
+        lo, hi = 3, pr.n_elems - 2
+        m.fe_eval_scalar(mesh.handle, form, m.F64, pr.mat_kind, banded_input(pr.mat_a, off),
+                         banded_input(pr.mat_b, off), banded_input(pr.u, off), lo, hi, val.view)
+        torch.cuda.synchronize()
+        assert val.intact()
+        ue = pr.u[pr.dof_conn]                       # [E][nb] or [E][nb][D]
+        ue = ue.reshape(pr.n_elems, pr.nb, -1).transpose(0, 2, 1).reshape(pr.n_elems, -1)
+        ref = float(np.sum(oracle.problem_residual(pr)[lo:hi] * ue[lo:hi]))
+        assert abs(val.view.item() - ref) <= 1e-11 * max(abs(ref), 1e-30)
