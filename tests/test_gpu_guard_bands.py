@@ -371,3 +371,35 @@ def test_eval_scalar_guard_bands(off):
         ue = ue.reshape(pr.n_elems, pr.nb, -1).transpose(0, 2, 1).reshape(pr.n_elems, -1)
         ref = float(np.sum(oracle.problem_residual(pr)[lo:hi] * ue[lo:hi]))
         assert abs(val.view.item() - ref) <= 1e-11 * max(abs(ref), 1e-30)
+
+
+@pytest.mark.parametrize("off", [GUARD - 1, GUARD])
+@pytest.mark.parametrize("form,p", [(0, 1), (0, 2), (4, 2), (5, 2), (3, 4), (4, 1)])
+def test_peer_window_guard_bands(form, p, off):
+    """fe_eval_residual_peer: the two windows receive exactly their nodes' contributions at the
+    requested node offsets of the destination buffers, nothing around them is written."""
+    m = fe()
+    pr = fi.make_problem(form, p, (4, 3, 5), 34000 + 7 * form + p)
+    mesh = gpu_mesh(pr)
+    D = pr.ncomp
+    plane = pr.n_nodes // 7
+    w0, w1 = (0, plane), (pr.n_nodes - plane - 3, pr.n_nodes)
+    o0, o1 = 5, 11
+    d0 = Banded((o0 + w0[1] - w0[0], D), off)
+    d1 = Banded((o1 + w1[1] - w1[0], D), off)
+    d0.view[o0:].zero_()
+    d1.view[o1:].zero_()
+    rg = Banded((pr.n_nodes, D), off)
+    rg.view.zero_()
+    m.fe_eval_residual_peer(mesh.handle, form, pr.mat_kind, banded_input(pr.mat_a, off),
+                            banded_input(pr.mat_b, off), banded_input(pr.u, off), 0, pr.n_elems,
+                            None, rg.view,
+                            [(w0[0], w0[1], d0.view.data_ptr(), o0),
+                             (w1[0], w1[1], d1.view.data_ptr(), o1)])
+    torch.cuda.synchronize()
+    assert rg.intact() and d0.intact() and d1.intact()
+    assert d0.rows_untouched(0, o0) and d1.rows_untouched(0, o1)
+    R = oracle.assemble(oracle.problem_residual(pr), pr.dof_conn, pr.n_nodes, D).reshape(-1, D)
+    assert rel(rg.view.cpu().numpy(), R) <= TOL64
+    assert rel(d0.view[o0:].cpu().numpy(), R[w0[0]:w0[1]]) <= TOL64
+    assert rel(d1.view[o1:].cpu().numpy(), R[w1[0]:w1[1]]) <= TOL64
