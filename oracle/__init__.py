@@ -25,8 +25,22 @@ ERR_ARG = -1
 ERR_DEGENERATE = -3
 
 
+# ORACLE_SANITIZE=1 in the environment: an AddressSanitizer + UndefinedBehaviorSanitizer build of
+# the same source (liboracle_san.so), used by tests/test_oracle_sanitized.py in a subprocess with
+# libasan preloaded (an ASan/UBSan host build of the oracle).
+_SANITIZE = os.environ.get("ORACLE_SANITIZE", "") not in ("", "0")
+_LIB_SAN = os.path.join(_HERE, "liboracle_san.so")
+
+
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (-O2, IEEE fp64, no fast-math, OpenMP over cells)."""
+    if _SANITIZE:
+        if force or not os.path.exists(_LIB_SAN) or os.path.getmtime(_LIB_SAN) < os.path.getmtime(_SRC):
+            cmd = ["gcc", "-O1", "-g", "-fno-omit-frame-pointer", "-fsanitize=address,undefined",
+                   "-fno-sanitize-recover=undefined", "-fopenmp", "-fPIC", "-shared", "-std=c11",
+                   "-Wall", "-o", _LIB_SAN, _SRC, "-lm"]
+            subprocess.run(cmd, check=True)
+        return _LIB_SAN
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         cmd = ["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11", "-Wall",
                "-o", _LIB, _SRC, "-lm"]

@@ -1,0 +1,27 @@
+"""Host logic of the product library, step a0 (csrc/tables.cpp): the Gauss rule and the Lagrange
+tables every kernel's __constant__ / global tables are filled from, checked on the CPU against
+what the mathematics fixes (exactness degree 2n-1, Kronecker property, partition of unity,
+tensor-product structure, x-fastest order, the fwd / bwd transposes) -- independently of the
+oracle's tables -- in an AddressSanitizer + UBSan build."""
+from __future__ import annotations
+
+import os
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CSRC = os.path.join(ROOT, "paper_2107_04121_b200", "csrc")
+
+
+def test_product_host_tables(tmp_path):
+    exe = tmp_path / "tables_check"
+    flags = ["-O1", "-g", "-std=c++17", "-Wall"]
+    san = ["-fsanitize=address,undefined", "-fno-sanitize-recover=undefined"]
+    cmd = ["g++", *flags, *san, "-I", CSRC, os.path.join(ROOT, "tests", "helpers", "tables_check.cpp"),
+           os.path.join(CSRC, "tables.cpp"), "-o", str(exe)]
+    if subprocess.run(cmd, capture_output=True).returncode != 0:     # no sanitizer runtimes
+        cmd = [c for c in cmd if c not in san]
+        subprocess.run(cmd, check=True)
+    env = dict(os.environ, ASAN_OPTIONS="detect_leaks=1")
+    pr = subprocess.run([str(exe)], capture_output=True, text=True, env=env, timeout=300)
+    assert pr.returncode == 0, (pr.stdout[-3000:], pr.stderr[-3000:])
+    assert pr.stdout.strip().endswith("tables ok")

@@ -1,0 +1,59 @@
+"""The oracle under AddressSanitizer + UndefinedBehaviorSanitizer.
+
+An out-of-bounds read in the C oracle could give right-looking numbers that the pins happen to
+accept; so the same source is built with -fsanitize=address,undefined and every entry point
+(every form, order 1-4, every material layout, element sub-ranges, the Stokes coupling pair,
+stress, geometry, assembly, the degenerate-cell error path) runs once in a subprocess with the
+sanitizer runtimes preloaded.  Any report fails the test."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _runtime(name):
+    p = subprocess.run(["gcc", f"-print-file-name={name}"], capture_output=True, text=True).stdout.strip()
+    return p if os.path.isabs(p) and os.path.exists(p) else None
+
+
+def test_oracle_under_asan_ubsan():
+    asan, ubsan = _runtime("libasan.so"), _runtime("libubsan.so")
+    if not asan or not ubsan:
+        pytest.skip("gcc sanitizer runtimes not installed")
+    env = dict(os.environ)
+    env.update(ORACLE_SANITIZE="1", LD_PRELOAD=f"{asan}:{ubsan}",
+               ASAN_OPTIONS="detect_leaks=0:abort_on_error=0:exitcode=87",
+               UBSAN_OPTIONS="print_stacktrace=1:halt_on_error=1:exitcode=88",
+               OMP_NUM_THREADS="4")
+    pr = subprocess.run([sys.executable, os.path.join(HERE, "helpers", "oracle_sanitized_driver.py")],
+                        capture_output=True, text=True, env=env, timeout=900)
+    log = pr.stdout[-2000:] + pr.stderr[-6000:]
+    assert pr.returncode == 0, log
+    assert "AddressSanitizer" not in pr.stderr and "runtime error:" not in pr.stderr, log
+    assert pr.stdout.strip().splitlines()[-1].startswith("done "), log
+
+
+def test_sanitizer_setup_detects_a_planted_overflow(tmp_path):
+    """Negative control of the set-up above: a heap overflow planted in a small library built
+    with the same flags and loaded the same way (ctypes, preloaded runtimes) is reported."""
+    asan, ubsan = _runtime("libasan.so"), _runtime("libubsan.so")
+    if not asan or not ubsan:
+        pytest.skip("gcc sanitizer runtimes not installed")
+    src = tmp_path / "bad.c"
+    src.write_text("#include <stdlib.h>\n"
+                   "double bad(int n) { double *a = malloc(n * sizeof(double)); double s = 0;\n"
+                   "  for (int i = 0; i <= n; ++i) s += a[i] = i; free(a); return s; }\n")
+    so = tmp_path / "libbad.so"
+    subprocess.run(["gcc", "-O1", "-g", "-fsanitize=address,undefined", "-fPIC", "-shared",
+                    "-o", str(so), str(src)], check=True)
+    env = dict(os.environ)
+    env.update(LD_PRELOAD=f"{asan}:{ubsan}", ASAN_OPTIONS="detect_leaks=0:exitcode=87")
+    code = f"import ctypes; l = ctypes.CDLL({str(so)!r}); l.bad.restype = ctypes.c_double; l.bad(8)"
+    pr = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                        timeout=120)
+    assert pr.returncode != 0 and "heap-buffer-overflow" in pr.stderr, pr.stderr[-2000:]
