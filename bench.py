@@ -608,6 +608,13 @@ def timed_run(run, steps, warmup, world, local_rank, window_s=1.2, graph=False):
             graph, graph_error = False, f"{type(ex).__name__}: {ex}"[:300]
             print(f"bench: CUDA-graph capture failed, eager steps: {graph_error}", file=sys.stderr)
             torch.cuda.synchronize(dev)
+        if world > 1:
+            # every rank replays, or none does: the NCCL P2P calls of an eager step and the
+            # captured ones of a replayed step must pair up across ranks
+            ok = torch.tensor([1 if graph else 0], device=dev, dtype=torch.int32)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if graph and int(ok[0]) == 0:
+                graph, graph_error = False, "capture failed on another rank: eager steps on all"
         _barrier(torch, dist, world, local_rank, dev)
     if graph:
         eager_step = run.step
